@@ -1,0 +1,49 @@
+"""B200-native IGA-FEM integration + assembly (hot path of arXiv 2207.00280).
+
+Drop-in for the reference package ``igabench`` on its integration and assembly
+path: same public names and signatures (igabench/__init__.py:10-58), with the
+numerics executed by hand-written sm_100a CUDA kernels in
+``lib/libiga_b200.so`` (C-ABI: ``include/iga_b200.h``).  There is no CPU
+fallback.
+"""
+
+__version__ = "0.1.0"
+
+from .assembly import (
+    GlobalGram,
+    assemble,
+    dof_index,
+    element_dofs,
+    sparsity_row_bound,
+    spmv,
+    symbolic_pattern,
+    write_matrix_market,
+)
+from .integrators import (
+    ElementMatrix,
+    SumFactBuffers,
+    canonical_pairs,
+    default_rule,
+    element_tables,
+    flop_count,
+    integrate_element_classical,
+    integrate_element_sumfact,
+)
+from .mesh import QuadratureRule, element_list, gauss_rule, local_index, support_set
+from .runtime import (
+    IntegrationRuntime,
+    RunConfig,
+    RunResult,
+    grams_bitwise_equal,
+    run_integration,
+)
+from .splines import (
+    BasisValues,
+    KnotVector,
+    basis_derivative_table,
+    basis_value_table,
+    eval_nonzero_basis,
+    eval_nonzero_basis_derivatives,
+    find_element,
+    make_knot_vector,
+)

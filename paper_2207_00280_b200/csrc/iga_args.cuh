@@ -1,0 +1,48 @@
+// Argument blocks passed by value to the kernels (shared between the
+// launchers and the C-ABI entry points).
+#pragma once
+
+#include <stdint.h>
+
+namespace iga {
+
+struct ElemArgs {
+  int dim, K, q, op, method;
+  double jac, coef_scalar;
+  const double* coef;
+  const double* weights;
+  const double* ref_nodes;
+  const int32_t* elem_ids;
+  const double* elem_nodes;
+  int64_t count;
+  double* out;
+};
+
+struct ScatterArgs {
+  int dim, K, op;
+  int el_begin, el_end;           // slab along the slowest axis
+  int64_t row_first, row_last;    // global rows [row_first, row_last) written
+  int64_t base;                   // rowptr(row_first)
+  double jac, coef_scalar;
+  const double* coef;
+  const double* weights;
+  const double* V;  // [K][m][Q]
+  const double* D;  // [K][m][Q] or null (mass)
+  double* values;
+};
+
+struct GsfArgs {
+  int K, op;
+  int el_begin, el_end;          // element slab along axis 0
+  int plane_begin, plane_end;    // row planes I0 written
+  int tiles1;                    // tiles along axis 1
+  int64_t base;                  // rowptr of (plane_begin, 0, 0)
+  double jac, coef_scalar;
+  const double* coef;            // [K^3][Q^3] or null
+  const double* weights;         // [Q]
+  const double* V;               // [K][P+1][Q]
+  const double* D;               // [K][P+1][Q] (null for mass)
+  double* values;
+};
+
+}  // namespace iga

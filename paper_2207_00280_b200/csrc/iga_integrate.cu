@@ -1,0 +1,200 @@
+// C-ABI entry points of the mesh-wide path: fused integrate+assemble,
+// assembly from element matrices, and SpMV over the structured CSR.
+#include "iga_dispatch.cuh"
+
+#include "iga_args.cuh"
+
+namespace iga {
+
+int launch_scatter(const ScatterArgs& a, int method, int p, int q, cudaStream_t s);
+int launch_gsf(const GsfArgs& a, int p, int q, cudaStream_t s);
+
+// assembly.assemble from element matrices: one warp per CSR row, lanes over
+// its columns; every value sums its element contributions in lexicographic
+// element order (deterministic; SPEC's "lexicographic element order").
+__global__ void k_assemble_elements(int dim, int K, int p, const double* __restrict__ mats,
+                                    int64_t row_first, int64_t nrows, int64_t base,
+                                    double* __restrict__ values) {
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= nrows) return;
+  const int64_t N = (int64_t)K + p;
+  const int m = p + 1;
+  const int64_t n = dim == 3 ? (int64_t)m * m * m : (int64_t)m * m;
+  const int64_t row = row_first + warp;
+  int64_t I[3] = {0, 0, 0};
+  if (dim == 3) {
+    I[0] = row / (N * N); I[1] = (row / N) % N; I[2] = row % N;
+  } else {
+    I[0] = row / N; I[1] = row % N;
+  }
+  int64_t lo[3], c[3];
+  for (int d = 0; d < 3; ++d) {
+    lo[d] = d < dim ? band_lo(I[d], p) : 0;
+    c[d] = d < dim ? band_cnt(I[d], p, N) : 1;
+  }
+  const int64_t cnt = c[0] * c[1] * c[2];
+  const int64_t off = rowptr(dim, row, p, N) - base;
+  for (int64_t j = lane; j < cnt; j += 32) {
+    int64_t J[3] = {lo[0] + j / (c[1] * c[2]), lo[1] + (j / c[2]) % c[1], lo[2] + j % c[2]};
+    int64_t elo[3], ehi[3];
+    for (int d = 0; d < 3; ++d) {
+      if (d < dim) {
+        const int64_t mx = I[d] > J[d] ? I[d] : J[d], mn = I[d] < J[d] ? I[d] : J[d];
+        elo[d] = mx - p > 0 ? mx - p : 0;
+        ehi[d] = mn < K - 1 ? mn : K - 1;
+      } else {
+        elo[d] = 0; ehi[d] = 0;
+      }
+    }
+    double acc = 0.0;
+    for (int64_t a0 = elo[0]; a0 <= ehi[0]; ++a0)
+      for (int64_t a1 = elo[1]; a1 <= ehi[1]; ++a1)
+        for (int64_t a2 = elo[2]; a2 <= ehi[2]; ++a2) {
+          int64_t eid, il, jl;
+          if (dim == 3) {
+            eid = (a0 * K + a1) * K + a2;
+            il = ((I[0] - a0) * m + (I[1] - a1)) * m + (I[2] - a2);
+            jl = ((J[0] - a0) * m + (J[1] - a1)) * m + (J[2] - a2);
+          } else {
+            eid = a0 * K + a1;
+            il = (I[0] - a0) * m + (I[1] - a1);
+            jl = (J[0] - a0) * m + (J[1] - a1);
+          }
+          acc += mats[(eid * n + il) * n + jl];
+        }
+    values[off + j] = acc;
+  }
+}
+
+// y = A x over the structured CSR: one warp per row.
+__global__ void k_spmv(int dim, int K, int p, const double* __restrict__ values,
+                       const double* __restrict__ x, double* __restrict__ y, int64_t nrows) {
+  const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= nrows) return;
+  const int64_t N = (int64_t)K + p;
+  const int64_t row = warp;
+  int64_t I[3] = {0, 0, 0};
+  if (dim == 3) {
+    I[0] = row / (N * N); I[1] = (row / N) % N; I[2] = row % N;
+  } else {
+    I[0] = row / N; I[1] = row % N;
+  }
+  int64_t lo[3], c[3];
+  for (int d = 0; d < 3; ++d) {
+    lo[d] = d < dim ? band_lo(I[d], p) : 0;
+    c[d] = d < dim ? band_cnt(I[d], p, N) : 1;
+  }
+  const int64_t cnt = c[0] * c[1] * c[2];
+  const int64_t off = rowptr(dim, row, p, N);
+  double acc = 0.0;
+  for (int64_t j = lane; j < cnt; j += 32) {
+    const int64_t a = j / (c[1] * c[2]), b = (j / c[2]) % c[1], cc = j % c[2];
+    const int64_t col = dim == 3 ? ((lo[0] + a) * N + lo[1] + b) * N + lo[2] + cc
+                                 : (lo[0] + a) * N + lo[1] + b;
+    acc += values[off + j] * x[col];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) y[row] = acc;
+}
+
+static int validate_problem(const iga_problem* prob) {
+  if (!prob) return fail_einval("null problem");
+  if (prob->dim != 2 && prob->dim != 3) return fail_einval("dim must be 2 or 3, got %d", prob->dim);
+  if (prob->K < 1) return fail_einval("mesh must be >= 1, got %d", prob->K);
+  if (prob->p < 0) return fail_einval("degree must be >= 0, got %d", prob->p);
+  if (prob->q < 1) return fail_einval("quadrature points must be >= 1, got %d", prob->q);
+  if (prob->op < 0 || prob->op > 2) return fail_einval("unknown operator %d", prob->op);
+  if (prob->op != IGA_OP_MASS && prob->p < 1)
+    return fail_einval("derivatives require degree >= 1");
+  if (!prob->weights || !prob->tables_v) return fail_einval("null weights/tables");
+  if (prob->op != IGA_OP_MASS && !prob->tables_d) return fail_einval("stiffness needs tables_d");
+  if (prob->reserved != 0) return fail_einval("reserved field must be 0");
+  return IGA_OK;
+}
+
+}  // namespace iga
+
+using namespace iga;
+
+extern "C" {
+
+int32_t iga_integrate_assemble(const iga_problem* prob, int32_t method, int32_t el_begin,
+                               int32_t el_end, int32_t row_plane_begin, int32_t row_plane_end,
+                               double* values, void* stream) {
+  int rc = validate_problem(prob);
+  if (rc) return rc;
+  const int K = prob->K, p = prob->p, dim = prob->dim;
+  const int64_t N = (int64_t)K + p;
+  if (el_begin < 0 || el_end > K || el_end < el_begin)
+    return fail_einval("element slab [%d, %d) outside [0, %d)", el_begin, el_end, K);
+  if (row_plane_begin < 0 || row_plane_end > N || row_plane_end < row_plane_begin)
+    return fail_einval("row planes [%d, %d) outside [0, %lld)", row_plane_begin, row_plane_end,
+                       (long long)N);
+  if (!values) return fail_einval("null values");
+  cudaStream_t s = as_stream(stream);
+  const int64_t plane_rows = dim == 3 ? N * N : N;
+  const int64_t row_first = row_plane_begin * plane_rows, row_last = row_plane_end * plane_rows;
+  const int64_t base = rowptr(dim, row_first, p, N);
+  const int64_t nvals = rowptr(dim, row_last, p, N) - base;
+  if (nvals == 0) return IGA_OK;
+  if (method == IGA_METHOD_SUMFACT_ASSEMBLED) {
+    if (dim != 3) {
+      set_error("assembled sum factorization is implemented for dim=3 only");
+      return IGA_EUNSUPPORTED;
+    }
+    GsfArgs a;
+    a.K = K; a.op = prob->op; a.el_begin = el_begin; a.el_end = el_end;
+    a.plane_begin = row_plane_begin; a.plane_end = row_plane_end; a.tiles1 = 0;
+    a.base = base; a.jac = prob->jac; a.coef_scalar = prob->coef_scalar; a.coef = prob->coef;
+    a.weights = prob->weights; a.V = prob->tables_v; a.D = prob->tables_d; a.values = values;
+    return launch_gsf(a, p, prob->q, s);
+  }
+  if (method != IGA_METHOD_CLASSICAL && method != IGA_METHOD_SUMFACT)
+    return fail_einval("unknown method %d", method);
+  rc = check_cuda(cudaMemsetAsync(values, 0, sizeof(double) * nvals, s), "zero values");
+  if (rc) return rc;
+  ScatterArgs a;
+  a.dim = dim; a.K = K; a.op = prob->op; a.el_begin = el_begin; a.el_end = el_end;
+  a.row_first = row_first; a.row_last = row_last; a.base = base; a.jac = prob->jac;
+  a.coef_scalar = prob->coef_scalar; a.coef = prob->coef; a.weights = prob->weights;
+  a.V = prob->tables_v; a.D = prob->tables_d; a.values = values;
+  return launch_scatter(a, method, p, prob->q, s);
+}
+
+int32_t iga_assemble_elements(int32_t dim, int32_t K, int32_t p, const double* mats,
+                              int32_t row_plane_begin, int32_t row_plane_end, double* values,
+                              void* stream) {
+  if (dim != 2 && dim != 3) return fail_einval("dim must be 2 or 3");
+  if (K < 1 || p < 0) return fail_einval("mesh must be >= 1 and degree >= 0");
+  const int64_t N = (int64_t)K + p;
+  if (row_plane_begin < 0 || row_plane_end > N || row_plane_end < row_plane_begin)
+    return fail_einval("row planes outside [0, %lld)", (long long)N);
+  if (!mats || !values) return fail_einval("null pointer");
+  const int64_t plane_rows = dim == 3 ? N * N : N;
+  const int64_t row_first = row_plane_begin * plane_rows;
+  const int64_t nrows = (row_plane_end - row_plane_begin) * plane_rows;
+  if (nrows == 0) return IGA_OK;
+  const int64_t base = rowptr(dim, row_first, p, N);
+  const int64_t threads = nrows * 32;
+  k_assemble_elements<<<(unsigned)((threads + 255) / 256), 256, 0, as_stream(stream)>>>(
+      dim, K, p, mats, row_first, nrows, base, values);
+  return check_cuda(cudaGetLastError(), "iga_assemble_elements");
+}
+
+int32_t iga_spmv(int32_t dim, int32_t K, int32_t p, const double* values, const double* x,
+                 double* y, void* stream) {
+  if (dim != 2 && dim != 3) return fail_einval("dim must be 2 or 3");
+  if (K < 1 || p < 0) return fail_einval("mesh must be >= 1 and degree >= 0");
+  if (!values || !x || !y) return fail_einval("null pointer");
+  const int64_t N = (int64_t)K + p;
+  const int64_t nrows = dim == 3 ? N * N * N : N * N;
+  const int64_t threads = nrows * 32;
+  k_spmv<<<(unsigned)((threads + 255) / 256), 256, 0, as_stream(stream)>>>(dim, K, p, values, x,
+                                                                          y, nrows);
+  return check_cuda(cudaGetLastError(), "iga_spmv");
+}
+
+}  // extern "C"

@@ -1,0 +1,216 @@
+"""Device-resident problem state and the calls through the C-ABI.
+
+``MeshProblem`` owns, on one CUDA device, everything one mesh-wide
+integration needs: the Gauss weights, the per-1D-element basis tables (K1,
+evaluated on the device, bitwise equal to runtime._MeshContext.build_tables,
+runtime.py:142-149), the optional coefficient field, and the ``iga_problem``
+block handed to ``libiga_b200.so``.  Torch is used only for device memory and
+streams.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+
+OPERATORS = tuple(_lib.OPS)
+
+
+def gauss_reference(q: int):
+    """Gauss-Legendre nodes/weights on [-1,1] from numpy, as mesh.py:82 does (bits
+    come from the host numpy and are uploaded, never recomputed on the GPU)."""
+    return np.polynomial.legendre.leggauss(q)
+
+
+def jacobian(K: int, dim: int) -> float:
+    """(1/(2K))**dim exactly as mesh.py:90 computes it (Python float pow)."""
+    return (1.0 / (2.0 * K)) ** dim
+
+
+def n_dofs(dim: int, K: int, p: int) -> int:
+    return (K + p) ** dim
+
+
+def csr_nnz(dim: int, K: int, p: int, row_begin: int = 0, row_end: int | None = None) -> int:
+    L = _lib.load()
+    row_end = n_dofs(dim, K, p) if row_end is None else row_end
+    nnz = L.iga_csr_nnz(dim, K, p, row_begin, row_end)
+    if nnz < 0:
+        raise ValueError(f"invalid CSR request dim={dim} K={K} p={p} rows=[{row_begin},{row_end})")
+    return int(nnz)
+
+
+def plane_rows(dim: int, K: int, p: int) -> int:
+    return (K + p) ** (dim - 1)
+
+
+@dataclass
+class CsrPattern:
+    """Device CSR pattern (int64 indptr relative to row_begin, int32 indices)."""
+
+    dim: int
+    K: int
+    p: int
+    row_begin: int
+    row_end: int
+    indptr: object  # torch.int64 [rows+1]
+    indices: object  # torch.int32 [nnz]
+
+
+def csr_pattern(dim, K, p, row_begin=0, row_end=None, device=None, stream=None,
+                with_indices=True) -> CsrPattern:
+    """K5: structured pattern on the device (assembly.symbolic_pattern, assembly.py:99-115)."""
+    torch = _lib.require_cuda()
+    row_end = n_dofs(dim, K, p) if row_end is None else row_end
+    dev = torch.device("cuda") if device is None else device
+    nnz = csr_nnz(dim, K, p, row_begin, row_end)
+    indptr = torch.empty(row_end - row_begin + 1, dtype=torch.int64, device=dev)
+    indices = torch.empty(nnz if with_indices else 0, dtype=torch.int32, device=dev)
+    _lib.check(_lib.load().iga_csr_pattern(dim, K, p, row_begin, row_end, indptr.data_ptr(),
+                                           indices.data_ptr() if with_indices and nnz else None,
+                                           _lib.stream_ptr(stream)))
+    return CsrPattern(dim, K, p, row_begin, row_end, indptr, indices if with_indices else None)
+
+
+class MeshProblem:
+    """Device state of one (dim, K, p, q, operator, coefficient) problem."""
+
+    def __init__(self, dim: int, K: int, p: int, q: int | None = None, operator: str = "mass",
+                 coefficient=None, device=None, stream=None):
+        torch = _lib.require_cuda()
+        if dim not in (2, 3):
+            raise ValueError(f"dim must be 2 or 3, got {dim}")
+        if K < 1 or p < 0:
+            raise ValueError("mesh must be >= 1 and degree >= 0")
+        if operator not in _lib.OPS:
+            raise ValueError(f"operator must be one of {OPERATORS}, got {operator!r}")
+        if operator != "mass" and p < 1:
+            raise ValueError("derivatives require degree >= 1")
+        q = p + 1 if q is None else int(q)
+        if q < 1:
+            raise ValueError(f"quadrature points must be >= 1, got {q}")
+        self.dim, self.K, self.p, self.q, self.operator = dim, K, p, q, operator
+        self.device = torch.device("cuda") if device is None else torch.device(device)
+        self.stream = stream
+        ref, w = gauss_reference(q)
+        self.ref_nodes_host = np.ascontiguousarray(ref)
+        self.weights_host = np.ascontiguousarray(w)
+        self.ref_nodes = torch.from_numpy(self.ref_nodes_host).to(self.device)
+        self.weights = torch.from_numpy(self.weights_host).to(self.device)
+        self.jac = jacobian(K, dim)
+        m = p + 1
+        self.tables_v = torch.empty((K, m, q), dtype=torch.float64, device=self.device)
+        self.tables_d = torch.empty((K, m, q), dtype=torch.float64, device=self.device)
+        self.coef = None
+        self.coef_scalar = 1.0
+        self.set_coefficient(coefficient)
+        self.build_tables()
+
+    # -- coefficient ----------------------------------------------------
+    def set_coefficient(self, coefficient):
+        """None / scalar / array [K^dim, q^dim] (element lexicographic, k1 slowest)."""
+        torch = _lib.require_cuda()
+        self.coef = None
+        self.coef_scalar = 1.0
+        if coefficient is None:
+            return
+        if np.isscalar(coefficient):
+            self.coef_scalar = float(coefficient)
+            return
+        n_el = self.K ** self.dim
+        nq = self.q ** self.dim
+        if isinstance(coefficient, torch.Tensor):
+            c = coefficient.to(device=self.device, dtype=torch.float64)
+        else:
+            c = torch.from_numpy(np.ascontiguousarray(coefficient, dtype=np.float64))
+            c = c.to(self.device)
+        if c.numel() != n_el * nq:
+            raise ValueError(f"coefficient must have {n_el}x{nq} values (elements x quadrature "
+                             f"points), got shape {tuple(c.shape)}")
+        self.coef = c.reshape(n_el, nq).contiguous()
+
+    # -- K1 -------------------------------------------------------------
+    def build_tables(self, stream=None):
+        """Basis values/derivatives per 1D element at the mapped nodes (K1)."""
+        L = _lib.load()
+        _lib.check(L.iga_mesh_tables(self.K, self.p, self.q, self.ref_nodes.data_ptr(),
+                                     self.tables_v.data_ptr(), self.tables_d.data_ptr(),
+                                     _lib.stream_ptr(stream or self.stream)))
+
+    def problem_struct(self) -> _lib.IgaProblem:
+        s = _lib.IgaProblem()
+        s.dim, s.K, s.p, s.q = self.dim, self.K, self.p, self.q
+        s.op = _lib.OPS[self.operator]
+        s.reserved = 0
+        s.jac = self.jac
+        s.coef_scalar = self.coef_scalar
+        s.coef = None if self.coef is None else self.coef.data_ptr()
+        s.weights = self.weights.data_ptr()
+        s.tables_v = self.tables_v.data_ptr()
+        s.tables_d = self.tables_d.data_ptr() if self.operator != "mass" else None
+        return s
+
+    # -- sizes ----------------------------------------------------------
+    @property
+    def n_dofs(self) -> int:
+        return n_dofs(self.dim, self.K, self.p)
+
+    @property
+    def n_elements(self) -> int:
+        return self.K ** self.dim
+
+    def nnz(self, plane_begin: int = 0, plane_end: int | None = None) -> int:
+        N = self.K + self.p
+        plane_end = N if plane_end is None else plane_end
+        pr = plane_rows(self.dim, self.K, self.p)
+        return csr_nnz(self.dim, self.K, self.p, plane_begin * pr, plane_end * pr)
+
+    # -- fused integrate + assemble ------------------------------------
+    def integrate_assemble(self, values, method: int, el_range=None, plane_range=None,
+                           stream=None):
+        """Write CSR values of row planes ``plane_range`` from elements ``el_range``
+        (slowest axis) into ``values`` (torch fp64, starts at the first row)."""
+        el = (0, self.K) if el_range is None else el_range
+        pl = (0, self.K + self.p) if plane_range is None else plane_range
+        s = self.problem_struct()
+        _lib.check(_lib.load().iga_integrate_assemble(
+            ctypes.byref(s), method, int(el[0]), int(el[1]), int(pl[0]), int(pl[1]),
+            values.data_ptr(), _lib.stream_ptr(stream or self.stream)))
+        return values
+
+    def element_matrices(self, elem_ids, method: int, elem_nodes=None, stream=None):
+        """Per-element matrices [count, n, n] (strict reference operation order)."""
+        torch = _lib.require_cuda()
+        ids = torch.as_tensor(np.ascontiguousarray(elem_ids, dtype=np.int32)).reshape(-1, self.dim)
+        ids = ids.to(self.device)
+        count = ids.shape[0]
+        n = (self.p + 1) ** self.dim
+        out = torch.empty((count, n, n), dtype=torch.float64, device=self.device)
+        nodes = None
+        if elem_nodes is not None:
+            nodes = torch.as_tensor(np.ascontiguousarray(elem_nodes, dtype=np.float64))
+            nodes = nodes.reshape(count, self.dim, self.q).to(self.device)
+        s = self.problem_struct()
+        _lib.check(_lib.load().iga_element_matrices(
+            ctypes.byref(s), method, self.ref_nodes.data_ptr(), ids.data_ptr(),
+            None if nodes is None else nodes.data_ptr(), count, out.data_ptr(),
+            _lib.stream_ptr(stream or self.stream)))
+        return out
+
+
+def basis_eval(K: int, p: int, elems, xs, derivatives: bool = True):
+    """K1' at arbitrary points: (values [n, p+1], derivatives [n, p+1]) on the device."""
+    torch = _lib.require_cuda()
+    e = torch.as_tensor(np.ascontiguousarray(elems, dtype=np.int32)).cuda()
+    x = torch.as_tensor(np.ascontiguousarray(xs, dtype=np.float64)).cuda()
+    n = e.numel()
+    V = torch.empty((n, p + 1), dtype=torch.float64, device="cuda")
+    D = torch.empty((n, p + 1), dtype=torch.float64, device="cuda") if derivatives else None
+    _lib.check(_lib.load().iga_basis_eval(K, p, n, e.data_ptr(), x.data_ptr(), V.data_ptr(),
+                                          None if D is None else D.data_ptr(),
+                                          _lib.stream_ptr()))
+    return V, D

@@ -1,0 +1,162 @@
+"""Mesh-wide entry point (drop-in for igabench.runtime).
+
+``run_integration(RunConfig(...))`` integrates and assembles the whole mesh on
+the device and returns the same ``RunResult(config, gram, times, flops)`` as
+runtime.py:287-295.  The reference's CPU strategies (sequential /
+over_elements / within_element / combined, runtime.py:16-20) are scheduling
+knobs for host threads; they are accepted and validated for drop-in
+compatibility and all run the same device schedule (grid over element
+tiles, CTAs over rows, threads over contractions), so results are identical
+across them exactly as the reference guarantees.
+
+Extensions: ``strategy="device"``, ``operator``,
+``coefficient`` (None | scalar | array [K^dim, q^dim]), ``dim`` (2 or 3),
+``devices`` and ``assembly`` ("auto" | "owner" | "scatter").
+"""
+
+from __future__ import annotations
+
+import threading
+import warnings
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .assembly import GlobalGram
+from .device import MeshProblem
+from .integrators import flop_count
+
+METHODS = ("classical", "sumfact")
+STRATEGIES = ("sequential", "over_elements", "within_element", "combined", "device")
+ASSEMBLY = ("auto", "owner", "scatter")
+BARRIER_TIMEOUT = 300.0
+
+
+@dataclass(frozen=True)
+class RunConfig:
+    method: str
+    strategy: str
+    mesh: int
+    degree: int
+    workers: int = 1
+    repetitions: int = 1
+    quad_points: int | None = None
+    inner_workers: int = 1
+    chunking: str = "static"
+    operator: str = "mass"
+    coefficient: object = field(default=None, compare=False, repr=False)
+    dim: int = 3
+    devices: int = 1
+    assembly: str = "auto"
+
+    def __post_init__(self):
+        if self.method not in METHODS:
+            raise ValueError(f"method must be one of {METHODS}, got {self.method!r}")
+        if self.strategy not in STRATEGIES:
+            raise ValueError(f"strategy must be one of {STRATEGIES}, got {self.strategy!r}")
+        if self.mesh < 1 or self.degree < 0:
+            raise ValueError("mesh must be >= 1 and degree >= 0")
+        if self.workers < 1 or self.inner_workers < 1:
+            raise ValueError("worker counts must be >= 1")
+        if self.repetitions < 1:
+            raise ValueError("repetitions must be >= 1")
+        if self.chunking not in ("static", "dynamic"):
+            raise ValueError(f"chunking must be static or dynamic, got {self.chunking!r}")
+        if self.operator not in _lib.OPS:
+            raise ValueError(f"operator must be one of {tuple(_lib.OPS)}, got {self.operator!r}")
+        if self.operator != "mass" and self.degree < 1:
+            raise ValueError("derivatives require degree >= 1")
+        if self.dim not in (2, 3):
+            raise ValueError(f"dim must be 2 or 3, got {self.dim}")
+        if self.devices < 1:
+            raise ValueError("devices must be >= 1")
+        if self.assembly not in ASSEMBLY:
+            raise ValueError(f"assembly must be one of {ASSEMBLY}, got {self.assembly!r}")
+        if self.quad_points is not None and self.quad_points < 1:
+            raise ValueError("quad_points must be >= 1")
+
+    @property
+    def points(self) -> int:
+        return self.degree + 1 if self.quad_points is None else self.quad_points
+
+
+@dataclass
+class RunResult:
+    config: RunConfig
+    gram: GlobalGram
+    times: list[float]
+    flops: int
+
+
+def grams_bitwise_equal(a: GlobalGram, b: GlobalGram) -> bool:
+    ma, mb = a.matrix, b.matrix
+    return (ma.shape == mb.shape and np.array_equal(ma.indptr, mb.indptr)
+            and np.array_equal(ma.indices, mb.indices)
+            and ma.data.tobytes() == mb.data.tobytes())
+
+
+def method_code(cfg: RunConfig) -> int:
+    """Kernel selection: classical -> Algorithm 1 + fused scatter; sumfact ->
+    assembled (row-owner) sum factorization unless assembly="scatter"."""
+    if cfg.method == "classical":
+        if cfg.assembly == "owner":
+            raise ValueError("assembly='owner' requires method='sumfact'")
+        return _lib.METHOD_CLASSICAL
+    if cfg.assembly == "scatter":
+        if cfg.dim != 3:
+            raise ValueError("element-local sum factorization scatter is 3D only")
+        return _lib.METHOD_SUMFACT
+    if cfg.dim != 3:
+        raise ValueError("assembled sum factorization is 3D only; use method='classical' "
+                         "for dim=2")
+    return _lib.METHOD_SUMFACT_ASSEMBLED
+
+
+class IntegrationRuntime:
+    """Owns the device buffers for one configuration; ``run`` is not reentrant
+    (runtime.py:155-185)."""
+
+    def __init__(self, cfg: RunConfig):
+        self.cfg = cfg
+        self._active = threading.Lock()
+        if cfg.devices > 1:
+            warnings.warn("devices > 1 in one process: use paper_2207_00280_b200.distributed "
+                          "(one process per GPU); running on the current device",
+                          RuntimeWarning, stacklevel=2)
+
+    def run(self) -> RunResult:
+        if not self._active.acquire(blocking=False):
+            raise RuntimeError("run_integration is already active on this runtime")
+        try:
+            return self._run_locked()
+        finally:
+            self._active.release()
+
+    def _run_locked(self) -> RunResult:
+        torch = _lib.require_cuda()
+        cfg = self.cfg
+        code = method_code(cfg)
+        prob = MeshProblem(cfg.dim, cfg.mesh, cfg.degree, cfg.points, cfg.operator,
+                           cfg.coefficient)
+        values = torch.empty(prob.nnz(), dtype=torch.float64, device=prob.device)
+        stream = torch.cuda.current_stream()
+        times = []
+        for _ in range(cfg.repetitions):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            prob.build_tables(stream)
+            prob.integrate_assemble(values, code, stream=stream)
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1) / 1e3)
+        gram = GlobalGram(K=cfg.mesh, p=cfg.degree, n_dofs=prob.n_dofs, values=values,
+                          dim=cfg.dim)
+        per_el = flop_count(cfg.method, cfg.degree, cfg.points)
+        return RunResult(config=cfg, gram=gram, times=times, flops=per_el * prob.n_elements)
+
+
+def run_integration(cfg: RunConfig) -> RunResult:
+    """Integrate + assemble the mesh under cfg on the device (runtime.py:287-295)."""
+    return IntegrationRuntime(cfg).run()

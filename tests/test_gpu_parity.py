@@ -1,0 +1,331 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the reference goldens
+and the CPU oracle.  Run on a B200 with ``pytest -m gpu``."""
+
+import glob
+import os
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from tests.conftest import GOLDEN, load_golden
+from tests.parity import assert_parity, compare
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import torch
+
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    import paper_2207_00280_b200 as P
+
+    return P
+
+
+def _gram_csr(res):
+    m = res.gram.matrix
+    return np.asarray(m.indptr, np.int64), np.asarray(m.indices, np.int64), m.data
+
+
+# ---------------------------------------------------------------- K1 tables
+def test_mesh_tables_bitwise(pkg):
+    from paper_2207_00280_b200.device import MeshProblem
+
+    g = load_golden("tables")
+    n = 0
+    for key in g.files:
+        if not key.startswith("V_"):
+            continue
+        _, K, p, q = key.split("_")
+        K, p, q = int(K[1:]), int(p[1:]), int(q[1:])
+        if q > 8:
+            continue
+        mp = MeshProblem(3, K, p, q)
+        V = mp.tables_v.cpu().numpy()
+        D = mp.tables_d.cpu().numpy()
+        assert V.tobytes() == g[key].tobytes(), key
+        assert D.tobytes() == g["D" + key[1:]].tobytes(), key
+        n += 1
+    assert n >= 40
+
+
+def test_basis_value_table_api(pkg):
+    g = load_golden("tables")
+    kv = pkg.make_knot_vector(5, 3)
+    ref, _ = np.polynomial.legendre.leggauss(4)
+    h = 1.0 / 5
+    for e in range(5):
+        nodes = e * h + (ref + 1.0) * (h / 2.0)
+        assert pkg.basis_value_table(kv, e, nodes).tobytes() == g["V_K5_p3_q4"][e].tobytes()
+        assert pkg.basis_derivative_table(kv, e, nodes).tobytes() == g["D_K5_p3_q4"][e].tobytes()
+
+
+# ---------------------------------------------------------------- K5 pattern
+@pytest.mark.parametrize("path", sorted(glob.glob(os.path.join(GOLDEN, "pattern_*.npz"))))
+def test_pattern(pkg, path):
+    K, p = (int(s[1:]) for s in os.path.basename(path)[:-4].split("_")[1:])
+    g = np.load(path)
+    pat = pkg.symbolic_pattern(K, p)
+    assert np.array_equal(pat.indptr, g["indptr"]) and np.array_equal(pat.indices, g["indices"])
+
+
+def test_pattern_row_ranges(pkg):
+    from paper_2207_00280_b200.device import csr_pattern
+
+    for dim, K, p in ((3, 7, 3), (2, 9, 2), (3, 4, 5)):
+        full_ip, full_ix = O.pattern(dim, K, p)
+        nr = (K + p) ** dim
+        for lo, hi in ((0, nr), (3, nr // 2), (nr // 3, nr)):
+            pat = csr_pattern(dim, K, p, lo, hi)
+            ip = pat.indptr.cpu().numpy()
+            ix = pat.indices.cpu().numpy()
+            assert np.array_equal(ip, full_ip[lo:hi + 1] - full_ip[lo])
+            assert np.array_equal(ix, full_ix[full_ip[lo]:full_ip[hi]])
+
+
+# ------------------------------------------------------- per-element API
+def test_element_matrices_bitwise(pkg):
+    g = load_golden("element_mass")
+    for key in g.files:
+        method, K, p, *alpha = key.split("_")
+        K, p = int(K[1:]), int(p[1:])
+        alpha = tuple(map(int, alpha))
+        kv = pkg.make_knot_vector(K, p)
+        rule = pkg.gauss_rule(p, K, alpha)
+        if method == "classical":
+            em = pkg.integrate_element_classical(alpha, kv, rule)
+        else:
+            em = pkg.integrate_element_sumfact(alpha, kv, rule, pkg.SumFactBuffers.allocate(p))
+        assert em.entries.tobytes() == g[key].tobytes(), key
+        assert em.flops == pkg.flop_count(method, p)
+
+
+@pytest.mark.parametrize("op", ["stiffness", "stiffness_mass"])
+@pytest.mark.parametrize("method", ["classical", "sumfact"])
+def test_element_stiffness_bitwise_vs_oracle(pkg, op, method):
+    K, p = 4, 3
+    kv = pkg.make_knot_vector(K, p)
+    for alpha in ((0, 0, 0), (1, 3, 2)):
+        rule = pkg.gauss_rule(p, K, alpha)
+        if method == "classical":
+            em = pkg.integrate_element_classical(alpha, kv, rule, operator=op)
+        else:
+            em = pkg.integrate_element_sumfact(alpha, kv, rule, pkg.SumFactBuffers.allocate(p),
+                                               operator=op)
+        ref = O.element(3, K, p, op, method, alpha)
+        assert em.entries.tobytes() == ref.tobytes()
+
+
+def test_element_fine_quadrature(pkg):
+    """q = p+3 (default_rule override, test_integrators.py:64-91 shape)."""
+    K, p = 3, 2
+    kv = pkg.make_knot_vector(K, p)
+    alpha = (1, 0, 2)
+    rule = pkg.default_rule(kv, alpha, points=p + 3)
+    em = pkg.integrate_element_classical(alpha, kv, rule)
+    ref = O.element(3, K, p, "mass", "classical", alpha, q=p + 3)
+    assert em.entries.tobytes() == ref.tobytes()
+
+
+# ------------------------------------------------ mesh-wide integrate+assemble
+MASS = sorted(glob.glob(os.path.join(GOLDEN, "mass_classical_K*_p*.npz")))
+
+
+@pytest.mark.parametrize("path", MASS)
+@pytest.mark.parametrize("method,assembly", [("classical", "auto"), ("sumfact", "owner"),
+                                             ("sumfact", "scatter")])
+def test_run_integration_mass_vs_reference(pkg, path, method, assembly):
+    K, p = (int(s[1:]) for s in os.path.basename(path)[:-4].split("_")[2:])
+    g = np.load(path)
+    res = pkg.run_integration(pkg.RunConfig(method, "device", K, p, assembly=assembly))
+    ip, ix, v = _gram_csr(res)
+    assert np.array_equal(ip, g["indptr"]) and np.array_equal(ix, g["indices"])
+    assert_parity(v, g["data"], ip, what=f"{path} {method}/{assembly}")
+
+
+STIFF = sorted(glob.glob(os.path.join(GOLDEN, "stiffness*_classical_K*_p*.npz")))
+
+
+@pytest.mark.parametrize("path", STIFF)
+@pytest.mark.parametrize("method,assembly", [("classical", "auto"), ("sumfact", "owner"),
+                                             ("sumfact", "scatter")])
+def test_run_integration_stiffness_vs_reference(pkg, path, method, assembly):
+    name = os.path.basename(path)[:-4]
+    op = "stiffness_mass" if name.startswith("stiffness_mass") else "stiffness"
+    K, p = (int(s[1:]) for s in name.split("_")[-2:])
+    g = np.load(path)
+    res = pkg.run_integration(pkg.RunConfig(method, "device", K, p, operator=op,
+                                            assembly=assembly))
+    ip, ix, v = _gram_csr(res)
+    assert np.array_equal(ip, g["indptr"]) and np.array_equal(ix, g["indices"])
+    assert_parity(v, g["data"], ip, what=f"{name} {method}/{assembly}")
+
+
+@pytest.mark.parametrize("path", sorted(glob.glob(os.path.join(GOLDEN, "sepcoef_*.npz"))))
+@pytest.mark.parametrize("method,assembly", [("classical", "auto"), ("sumfact", "owner")])
+def test_separable_coefficient_vs_reference(pkg, path, method, assembly):
+    name = os.path.basename(path)[:-4]
+    op = name[len("sepcoef_"):name.rindex("_K")]
+    K, p = (int(s[1:]) for s in name.split("_")[-2:])
+    g = np.load(path)
+    q = p + 1
+    coef = np.einsum("ai,bj,ck->abcijk", g["c1"], g["c2"], g["c3"]).reshape(K**3, q**3)
+    _, _, A = O.integrate_assemble(3, K, p, op, "classical", coef=coef, absolute=True)
+    res = pkg.run_integration(pkg.RunConfig(method, "device", K, p, operator=op,
+                                            coefficient=coef, assembly=assembly))
+    ip, ix, v = _gram_csr(res)
+    assert_parity(v, g["data"], ip, what=name, absref=A)
+
+
+@pytest.mark.parametrize("op", ["mass", "stiffness", "stiffness_mass"])
+@pytest.mark.parametrize("K,p,q", [(5, 2, 3), (4, 3, 4), (3, 4, 5), (3, 1, 2), (2, 5, 6),
+                                   (4, 2, 5)])
+def test_general_coefficient_vs_oracle(pkg, op, K, p, q):
+    if op != "mass" and p < 1:
+        pytest.skip("derivatives need p >= 1")
+    coef = np.random.default_rng(K * 10 + p).uniform(0.5, 1.5, size=(K**3, q**3))
+    ip, _, ref = O.integrate_assemble(3, K, p, op, "classical", q=q, coef=coef)
+    _, _, A = O.integrate_assemble(3, K, p, op, "classical", q=q, coef=coef, absolute=True)
+    for method, assembly in (("sumfact", "owner"), ("classical", "auto"),
+                             ("sumfact", "scatter")):
+        res = pkg.run_integration(pkg.RunConfig(method, "device", K, p, quad_points=q,
+                                                operator=op, coefficient=coef,
+                                                assembly=assembly))
+        v = res.gram.values.cpu().numpy()
+        assert_parity(v, ref, ip, what=f"{op} K={K} p={p} q={q} {method}/{assembly}", absref=A)
+
+
+@pytest.mark.parametrize("K,p", [(16, 2), (3, 1)])
+def test_mass_2d_vs_derived_reference(pkg, K, p):
+    g = load_golden(f"mass2d_K{K}_p{p}")
+    res = pkg.run_integration(pkg.RunConfig("classical", "device", K, p, dim=2))
+    ip, ix, v = _gram_csr(res)
+    assert np.array_equal(ip, g["indptr"]) and np.array_equal(ix, g["indices"])
+    assert_parity(v, g["data"], ip)
+
+
+def test_reference_strategies_accepted(pkg):
+    """The reference's CPU strategies run the device schedule; identical bits."""
+    K, p = 4, 2
+    grams = [pkg.run_integration(pkg.RunConfig("sumfact", s, K, p, workers=w)).gram
+             for s, w in (("sequential", 1), ("over_elements", 8), ("within_element", 4),
+                          ("combined", 2), ("device", 1))]
+    for g2 in grams[1:]:
+        assert pkg.grams_bitwise_equal(grams[0], g2)
+
+
+def test_assembled_sumfact_deterministic(pkg):
+    cfg = pkg.RunConfig("sumfact", "device", 12, 3, operator="stiffness", repetitions=2)
+    a = pkg.run_integration(cfg).gram
+    b = pkg.run_integration(cfg).gram
+    assert pkg.grams_bitwise_equal(a, b)
+
+
+def test_slabs_sum_to_full(pkg):
+    """Multi-GPU decomposition emulated on one GPU: element slabs along the slowest
+    axis produce partial interface rows that add up to the single-device matrix."""
+    import torch
+    from paper_2207_00280_b200 import _lib
+    from paper_2207_00280_b200.device import MeshProblem
+
+    K, p = 10, 3
+    N = K + p
+    mp = MeshProblem(3, K, p, operator="stiffness")
+    full = torch.empty(mp.nnz(), dtype=torch.float64, device="cuda")
+    mp.integrate_assemble(full, _lib.METHOD_SUMFACT_ASSEMBLED)
+    acc = torch.zeros_like(full)
+    bounds = [0, 3, 5, 10]
+    for g in range(3):
+        lo, hi = bounds[g], bounds[g + 1]
+        phi = min(hi + p, N) if g < 2 else N
+        part = torch.empty(mp.nnz(lo, phi), dtype=torch.float64, device="cuda")
+        mp.integrate_assemble(part, _lib.METHOD_SUMFACT_ASSEMBLED, el_range=(lo, hi),
+                              plane_range=(lo, phi))
+        off = mp.nnz(0, lo)
+        acc[off:off + part.numel()] += part
+    ip, _ = O.pattern(3, K, p)
+    assert_parity(acc.cpu().numpy(), full.cpu().numpy(), ip)
+
+
+def test_spmv_matches_scipy(pkg):
+    res = pkg.run_integration(pkg.RunConfig("sumfact", "device", 6, 3, operator="stiffness"))
+    x = np.random.default_rng(0).standard_normal(res.gram.n_dofs)
+    y = res.gram.spmv(x)
+    np.testing.assert_allclose(y, res.gram.matrix @ x, rtol=1e-13, atol=1e-15)
+
+
+def test_heat_rhs_pins(pkg):
+    for K, p in ((3, 2), (4, 3)):
+        g = load_golden(f"heat_rhs_K{K}_p{p}")
+        for op, key in (("mass", "Mmu"), ("stiffness", "Smu")):
+            res = pkg.run_integration(pkg.RunConfig("sumfact", "device", K, p, operator=op))
+            got = res.gram.spmv(g["mu"])
+            assert np.linalg.norm(got - g[key]) <= 1e-13 * np.linalg.norm(g[key])
+
+
+def test_assemble_api_from_element_matrices(pkg):
+    K, p = 3, 2
+    kv = pkg.make_knot_vector(K, p)
+    buf = pkg.SumFactBuffers.allocate(p)
+    mats = [(a, pkg.integrate_element_sumfact(a, kv, pkg.gauss_rule(p, K, a), buf))
+            for a in pkg.element_list(K)]
+    gram = pkg.assemble(mats, K, p)
+    g = load_golden(f"mass_sumfact_K{K}_p{p}")
+    ip, ix, v = _gram_csr(type("R", (), {"gram": gram}))
+    assert np.array_equal(ip, g["indptr"])
+    assert_parity(v, g["data"], ip)
+    with pytest.raises(ValueError):
+        pkg.assemble(mats[:-1], K, p)
+    with pytest.raises(ValueError):
+        pkg.assemble(mats + mats[:1], K, p)
+
+
+# ---------------------------------------------- full-size configs, sampled rows
+def _sample_rows(K, p, n_rand, seed=0):
+    N = K + p
+    rng = np.random.default_rng(seed)
+    corners = [0, N - 1]
+    special = []
+    for a in corners + [p, K // 2]:
+        for b in corners + [1, K // 2]:
+            for c in corners + [p - 1 if p > 0 else 0, K // 2]:
+                special.append((a * N + b) * N + c)
+    rows = np.unique(np.concatenate([special, rng.integers(0, N**3, n_rand)]))
+    return rows
+
+
+@pytest.mark.parametrize("cfg", [
+    dict(K=64, p=3, op="stiffness", coef=None, name="C3"),
+    dict(K=32, p=2, op="mass", coef="uniform", name="C2"),
+])
+def test_full_size_sampled_rows(pkg, cfg):
+    """BASELINE configs at full size: sampled rows (corner/edge/interior) vs the
+    oracle's classical rows, plus size-independent properties."""
+    K, p, op = cfg["K"], cfg["p"], cfg["op"]
+    q = p + 1
+    coef = None
+    if cfg["coef"] == "uniform":
+        coef = np.random.default_rng(42).uniform(0.5, 1.5, size=(K, K, K, q, q, q))
+        coef = coef.reshape(K**3, q**3)
+    res = pkg.run_integration(pkg.RunConfig("sumfact", "device", K, p, operator=op,
+                                            coefficient=coef))
+    values = res.gram.values.cpu().numpy()
+    ip, _ = O.pattern(3, K, p)
+    rows = _sample_rows(K, p, 40)
+    ref_rows = O.rows(3, K, p, rows, op, "classical", coef=coef)
+    abs_rows = O.rows(3, K, p, rows, op, "classical", coef=coef, absolute=True)
+    got = np.concatenate([values[ip[r]:ip[r + 1]] for r in rows])
+    ref = np.concatenate(ref_rows)
+    A = np.concatenate(abs_rows)
+    sub_ip = np.concatenate([[0], np.cumsum([len(x) for x in ref_rows])])
+    assert_parity(got, ref, sub_ip, absref=A, what=cfg["name"])
+    # size-independent properties on the whole matrix
+    M = res.gram.matrix
+    assert abs(M - M.T).max() == 0.0  # exact symmetry (both triangles from one value)
+    if op == "stiffness":
+        rs = np.abs(M @ np.ones(M.shape[0]))
+        assert rs.max() <= 1e-12 * np.abs(values).max()  # constants are in the kernel
+    if op == "mass" and coef is None:
+        assert abs(values.sum() - 1.0) < 1e-12
