@@ -1,0 +1,396 @@
+"""Benchmark: 3D p=3 stiffness elements/s integrated+assembled, fp64 (BASELINE.json).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c1..c5]
+
+N=1 runs config 3 (64^3, p=3, q=4, Laplace stiffness, c=1) on one B200;
+N>1 (torchrun, one rank per GPU) runs config 5 (256^3, p=3) split into
+element slabs along the slowest axis with the NCCL interface-row exchange.
+A step = K1 basis tables + the fused integrate+assemble kernel writing every
+CSR value of the rank's rows.  Prints one JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "3D p=3 stiffness elements/s integrated+assembled, fp64, 1-8 B200; % roofline"
+
+WORKLOADS = {
+    "c1": dict(dim=2, K=16, p=2, op="mass", coef=None, method="classical",
+               desc="C1: 2D mass 16^2 p=2 q=3 c=1, classical + fused CSR scatter"),
+    "c2": dict(dim=3, K=32, p=2, op="mass", coef="uniform", method="sumfact",
+               desc="C2: 3D mass 32^3 p=2 q=3, per-qp coefficient U[0.5,1.5] seed 42, "
+                    "assembled sum factorization"),
+    "c3": dict(dim=3, K=64, p=3, op="stiffness", coef=None, method="sumfact",
+               desc="C3: 3D Laplace stiffness 64^3 p=3 q=4 c=1, assembled sum factorization "
+                    "(general per-qp-coefficient kernel) fused with CSR assembly"),
+    "c4": dict(dim=3, K=96, p=4, op="stiffness_mass", coef="sines", method="sumfact",
+               desc="C4: 3D stiffness+mass 96^3 p=4 q=5, smooth 8-mode sine coefficient, "
+                    "assembled sum factorization"),
+    "c5": dict(dim=3, K=256, p=3, op="stiffness", coef=None, method="sumfact",
+               desc="C5: 3D Laplace stiffness 256^3 p=3 q=4 c=1, z-slabs + NCCL interface rows"),
+}
+
+
+def coefficient(kind, K, p, dim):
+    """Seeded synthetic coefficient fields."""
+    q = p + 1
+    if kind is None:
+        return None
+    rng = np.random.default_rng(42)
+    if kind == "uniform":
+        return rng.uniform(0.5, 1.5, size=(K,) * dim + (q,) * dim).reshape(K**dim, q**dim)
+    if kind == "sines":
+        # c(x) = 1 + sum_{j<8} (0.3/8) sin(2 pi k_j . x + phi_j), k_j in {1,2,3}^3 (c in [0.7, 1.3])
+        kvec = rng.integers(1, 4, size=(8, 3))
+        phase = rng.uniform(0.0, 2 * np.pi, size=8)
+        ref, _ = np.polynomial.legendre.leggauss(q)
+        h = 1.0 / K
+        x = (np.arange(K)[:, None] * h + (ref[None, :] + 1.0) * (h / 2.0)).reshape(-1)  # K*q
+        out = np.ones((K * q,) * 3)
+        for j in range(8):
+            ex = np.exp(1j * (2 * np.pi * kvec[j, 0] * x + phase[j]))
+            ey = np.exp(1j * 2 * np.pi * kvec[j, 1] * x)
+            ez = np.exp(1j * 2 * np.pi * kvec[j, 2] * x)
+            exy = ex[:, None] * ey[None, :]
+            for a in range(K * q):  # slab-wise to bound memory
+                out[a] += (0.3 / 8) * np.imag(exy[a][:, None] * ez[None, :])
+        out = out.reshape(K, q, K, q, K, q).transpose(0, 2, 4, 1, 3, 5)
+        return np.ascontiguousarray(out).reshape(K**3, q**3)
+    raise ValueError(kind)
+
+
+def load_peaks():
+    peaks = {"hbm_gbs": None, "fp64_tflops": None, "src": {}}
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        peaks["hbm_gbs"] = d.get("hbm_gbs")
+        peaks["src"]["hbm"] = "MEASURED_PEAKS.json (driver-measured copy)"
+    else:
+        peaks["hbm_gbs"] = 6650.0
+        peaks["src"]["hbm"] = "fallback 6.65 TB/s (B200_PROFILING.md)"
+    f = os.path.join(ROOT, "profiles", "MEASURED_FP64.json")
+    if os.path.exists(f):
+        d = json.load(open(f))
+        peaks["fp64_tflops"] = d["fp64_peak_tflops"]
+        peaks["src"]["fp64"] = "profiles/MEASURED_FP64.json (" + d.get("how", "") + ")"
+    else:
+        peaks["fp64_tflops"] = 37.2
+        peaks["src"]["fp64"] = "derived 148 SMs x 64 DFMA x 2 x 1.965 GHz"
+    return peaks
+
+
+class ClockSampler:
+    """Samples SM clock and throttle reasons through NVML during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index=0, period=0.002):
+        self.samples, self.reasons = [], 0
+        self.period = period
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:  # noqa: BLE001 - report clocks as unavailable
+            self.max_mhz = None
+
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                self.reasons |= nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.ok:
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        names = [n for bit, n in self.REASONS.items() if self.reasons & bit and n != "gpu_idle"]
+        return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max_mhz,
+                "reasons": names, "samples": len(self.samples)}
+
+
+def cpu_port_rate(wl, K, p, steps_planes, threads, coef, reps=1):
+    """The oracle port of the reference CPU path (element-local sum factorization +
+    scatter into the CSR, runtime.py:258-267 + assembly.py:46-83) on `threads` host
+    threads, over element slabs of `steps_planes` planes of the same mesh."""
+    from oracle import oracle as O
+
+    ip, _ = O.pattern(wl["dim"], K, p)
+    values = np.empty(ip[-1])
+    n_el_plane = K ** (wl["dim"] - 1)
+    O.cpu_baseline(wl["dim"], K, p, wl["op"], "sumfact", coef=coef, threads=threads, indptr=ip,
+                   el_range=(0, 1), values=values)  # warm-up (page-in)
+    times = []
+    for r in range(reps):
+        lo = (r * steps_planes) % max(1, K - steps_planes + 1)
+        t0 = time.perf_counter()
+        O.cpu_baseline(wl["dim"], K, p, wl["op"], "sumfact", coef=coef, threads=threads,
+                       indptr=ip, el_range=(lo, lo + steps_planes), values=values)
+        times.append(time.perf_counter() - t0)
+    return steps_planes * n_el_plane, times
+
+
+def run_reference(args, wl, K, p, rank):
+    """--impl reference: the reference's CPU path (oracle port) on all host cores."""
+    if rank != 0:
+        return
+    threads = os.cpu_count()
+    coef = coefficient(wl["coef"], K, p, wl["dim"])
+    planes = max(1, min(K, 8 if K <= 64 else 2))
+    n_el, _ = cpu_port_rate(wl, K, p, planes, threads, coef, reps=0)
+    _, times = cpu_port_rate(wl, K, p, planes, threads, coef, reps=args.warmup + args.steps)
+    t = times[args.warmup:]
+    step_s = float(np.mean(t))
+    v = n_el / step_s
+    sample = (f"{planes} element planes ({n_el} elements) of the {K}^{wl['dim']} mesh per step, "
+              f"element-local sum factorization + CSR scatter, OpenMP {threads} threads")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "elements/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": wl["desc"], "K": K, "p": p, "sample": sample},
+        "cpu_baseline": {"value": v, "unit": "elements/s", "cores": threads, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": v, "unit": "elements/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    wname = args.workload or ("c3" if world == 1 else "c5")
+    wl = WORKLOADS[wname]
+    K, p = wl["K"], wl["p"]
+    q = p + 1
+
+    if args.impl == "reference":
+        run_reference(args, wl, K, p, rank)
+        return
+
+    import torch
+
+    import paper_2207_00280_b200 as P
+    from paper_2207_00280_b200 import perfmodel
+    from paper_2207_00280_b200.runtime import DeviceSession
+
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    coef = coefficient(wl["coef"], K, p, wl["dim"])
+    cfg = P.RunConfig(wl["method"], "device", K, p, operator=wl["op"], coefficient=coef,
+                      dim=wl["dim"], devices=world)
+    stream = torch.cuda.current_stream()
+
+    if world > 1:
+        from paper_2207_00280_b200.distributed import SlabSession, slab_plan
+
+        plan = slab_plan(K, p, world, rank)
+        sess = SlabSession(cfg, plan)
+        step = sess.step
+        n_el = (plan.el_hi - plan.el_lo) * K * K
+        launches = sess.kernel_launches_per_step
+        kernel_values = sess.values
+    else:
+        sess = DeviceSession(cfg)
+        step = sess.step
+        n_el = K ** wl["dim"]
+        launches = 2
+        kernel_values = sess.values
+
+    # L2 flush buffer (2x the 126 MB L2), written between timed steps outside the step events
+    flush = torch.empty(256 * 2**20 // 4, dtype=torch.float32, device="cuda")
+
+    for _ in range(args.warmup):
+        step()
+        flush.fill_(1.0)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    region0 = torch.cuda.Event(enable_timing=True)
+    region1 = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        region0.record(stream)
+        for i in range(args.steps):
+            ev[i][0].record(stream)
+            step()
+            ev[i][1].record(stream)
+            flush.fill_(float(i))
+        region1.record(stream)
+        torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    ms = float(np.mean(step_ms))
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    total_el = K ** wl["dim"]  # whole job (all ranks) per step
+    value = total_el / (ms / 1e3)
+
+    # dominant kernel (fused integrate+assemble) alone, on the launching stream
+    kev = []
+    for i in range(max(5, min(args.steps, 20))):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        flush.fill_(float(i))
+        a.record(stream)
+        if world > 1:
+            sess.prob.integrate_assemble(sess.values, sess.code, el_range=(plan.el_lo, plan.el_hi),
+                                         plane_range=(plan.own_lo, plan.own_hi), stream=stream)
+        else:
+            sess.prob.integrate_assemble(sess.values, sess.code, stream=stream)
+        b.record(stream)
+        kev.append((a, b))
+    torch.cuda.synchronize()
+    kern_ms = float(np.mean([a.elapsed_time(b) for a, b in kev]))
+    peaks = load_peaks()
+    if world > 1:
+        k_el = (plan.el_hi - plan.el_lo) * K * K
+        k_planes = plan.own_hi - plan.own_lo
+    else:
+        k_el = n_el
+        k_planes = K + p
+    # algorithmic work of this kernel launch (rank-local rows / elements)
+    fl = perfmodel.assembled_flops(wl["op"], K, p, q) * k_el / K**3 if wl["method"] == "sumfact" \
+        else None
+    by = 8 * sess.prob.nnz(plan.own_lo, plan.own_hi) if world > 1 else \
+        perfmodel.algorithmic_bytes(wl["dim"], K, p, q, coef is not None)
+    t_f = fl / (peaks["fp64_tflops"] * 1e12) if fl else 0.0
+    t_b = by / (peaks["hbm_gbs"] * 1e9)
+    if t_f >= t_b:
+        achieved = fl / (kern_ms / 1e3) / 1e12
+        roof = {"bound": "fp64", "achieved": achieved, "peak": peaks["fp64_tflops"],
+                "unit": "TFLOP/s", "frac": achieved / peaks["fp64_tflops"]}
+    else:
+        achieved = by / (kern_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / peaks["hbm_gbs"]}
+    roof.update({
+        "kernel": "k_gsf3 (assembled sum factorization + CSR write)" if wl["method"] == "sumfact"
+        else "k_classical_scatter",
+        "kernel_ms": kern_ms, "alg_flops": fl, "alg_bytes": by,
+        "t_fp64_ms": t_f * 1e3, "t_hbm_ms": t_b * 1e3,
+        "hbm_frac": (by / (kern_ms / 1e3) / 1e9) / peaks["hbm_gbs"],
+        "fp64_frac": ((fl / (kern_ms / 1e3) / 1e12) / peaks["fp64_tflops"]) if fl else None,
+        "peak_src": peaks["src"], "traffic": None,
+    })
+    prof = os.path.join(ROOT, "profiles", f"ncu_{wname}_traffic.json")
+    if os.path.exists(prof):
+        roof["traffic"] = json.load(open(prof)).get("dram_bytes_per_launch")
+
+    # end to end through the public API with host buffers (pinned), N=1 only
+    e2e = None
+    if world == 1 and not args.no_e2e:
+        host_out = torch.empty(sess.values.numel(), dtype=torch.float64).pin_memory()
+        for _ in range(2):
+            sess.step_host(host_out)
+        torch.cuda.synchronize()
+        n_e2e = max(3, min(args.steps, 10))
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0 = time.perf_counter()
+        a.record(stream)
+        for _ in range(n_e2e):
+            sess.step_host(host_out)
+        b.record(stream)
+        torch.cuda.synchronize()
+        wall = (time.perf_counter() - t0) / n_e2e
+        e_ms = a.elapsed_time(b) / n_e2e
+        e2e = {"value": total_el / (e_ms / 1e3), "unit": "elements/s",
+               "h2d_bytes_per_step": sess.h2d_bytes, "d2h_bytes_per_step": sess.d2h_bytes,
+               "ms_per_step": e_ms, "wall_ms_per_step": wall * 1e3,
+               "api": "paper_2207_00280_b200.runtime.DeviceSession.step_host (pinned host out)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count()
+        planes = max(1, min(K, 16))
+        n_s, times = cpu_port_rate(wl, K, p, planes, threads, coef, reps=2)
+        tmin = min(times)
+        cpu = {"value": n_s / tmin, "unit": "elements/s", "cores": threads, "kind": "port",
+               "sample": f"{planes} element planes ({n_s} elements) of the same {K}^{wl['dim']} "
+                         f"mesh, oracle port of run_integration(over_elements)+assemble "
+                         f"(element-local sum factorization + CSR scatter), min of 2"}
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": "elements/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded; no dataset)",
+            "config": {"workload": wl["desc"], "K": K, "p": p, "q": q, "dim": wl["dim"],
+                       "operator": wl["op"], "method": wl["method"],
+                       "nnz": P.device.csr_nnz(wl["dim"], K, p),
+                       "parallelism": f"element slabs x{world}" if world > 1 else "1 GPU",
+                       "l2": "256 MB buffer written between timed steps (outside the per-step "
+                             "events); each step also writes the whole CSR (> 126 MB L2)"},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches * args.steps, "clocks": clk.summary(),
+            "region_ms": region0.elapsed_time(region1),
+        }
+        print(json.dumps(out), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

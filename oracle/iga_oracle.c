@@ -546,8 +546,8 @@ void orc_rows(int dim, int K, int p, int q, int op, int method, const double* re
  * scattered straight into the structured CSR.  Not bitwise-ordered like
  * orc_integrate_assemble; used only for the reported CPU baseline. */
 void orc_cpu_baseline(int dim, int K, int p, int q, int op, int method, const double* ref_nodes,
-                      const double* w, double jac, const double* coef, const int64_t* indptr,
-                      double* values, int nthreads) {
+                      const double* w, double jac, const double* coef, int el_begin, int el_end,
+                      const int64_t* indptr, double* values, int nthreads) {
   int m = p + 1;
   int n = dim == 3 ? m * m * m : m * m;
   int nq = dim == 3 ? q * q * q : q * q;
@@ -555,21 +555,34 @@ void orc_cpu_baseline(int dim, int K, int p, int q, int op, int method, const do
   double* V = (double*)malloc(sizeof(double) * K * m * q);
   double* D = (double*)malloc(sizeof(double) * K * m * q);
   orc_tables(K, p, q, ref_nodes, V, p >= 1 ? D : NULL);
-  int64_t n_rows = dim == 3 ? n1d * n1d * n1d : n1d * n1d;
-  memset(values, 0, sizeof(double) * indptr[n_rows]);
+  /* zero the rows the slab touches: planes [el_begin, el_end + p) */
+  int64_t plane = dim == 3 ? n1d * n1d : n1d;
+  int64_t r0 = (int64_t)el_begin * plane;
+  int64_t r1 = ((int64_t)el_end + p < n1d ? (int64_t)el_end + p : n1d) * plane;
+  memset(values + indptr[r0], 0, sizeof(double) * (indptr[r1] - indptr[r0]));
   int K2 = dim == 3 ? K : 1;
 #ifdef _OPENMP
   if (nthreads > 0) omp_set_num_threads(nthreads);
 #endif
-  for (int color = 0; color <= p; ++color) {
+  /* colour (e0 mod p+1, e1 mod p+1): concurrent (e0, e1) pencils of one colour
+   * touch disjoint rows, each pencil runs its e2 elements in order. */
+  int nc1 = dim == 3 ? p + 1 : 1;
+  for (int color = 0; color < (p + 1) * nc1; ++color) {
+    int c0 = color / nc1, c1 = color % nc1;
+    int n0 = (el_end - el_begin - c0 + p) / (p + 1);
+    int n1 = dim == 3 ? (K - c1 + p) / (p + 1) : 1;
+    if (n0 <= 0 || n1 <= 0) continue;
 #pragma omp parallel
     {
       double* E = (double*)malloc(sizeof(double) * n * n);
       double* scratch = (double*)malloc(sizeof(double) * (n * n + m * m * q * q + m * m * m * m * q));
       int64_t dofs[512];
 #pragma omp for schedule(dynamic, 1)
-      for (int e0 = color; e0 < K; e0 += p + 1) {
-        for (int e1 = 0; e1 < K; ++e1)
+      for (int task = 0; task < n0 * n1; ++task) {
+        int e0 = el_begin + c0 + (task / n1) * (p + 1);
+        int e1_lo = dim == 3 ? c1 + (task % n1) * (p + 1) : 0;
+        int e1_hi = dim == 3 ? e1_lo + 1 : K;
+        for (int e1 = e1_lo; e1 < e1_hi; ++e1)
           for (int e2 = 0; e2 < K2; ++e2) {
             int alpha[3] = {e0, e1, e2};
             int64_t eid = dim == 3 ? ((int64_t)e0 * K + e1) * K + e2 : (int64_t)e0 * K + e1;

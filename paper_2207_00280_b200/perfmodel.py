@@ -1,0 +1,54 @@
+"""Algorithmic work of the device kernels, for roofline reporting.
+
+Counts are exact for a K^3 mesh (boundary truncation of the 1D bands
+included), 1 FMA = 2 flops, and count only the work the algorithm needs --
+not the halo recomputation of a particular tiling.
+
+Assembled sum factorization (iga_gsf.cu), per operator:
+  stage A (axis 0): types x K^3 (p+1)^2 q^3            MACs   (types: mass 1, stiffness 2)
+  stage B (axis 1): prods_B x nnz1 K^2 (p+1)^2 q^2     MACs   (prods: mass 1, stiffness 3)
+  stage S (axis 2): prods_S x nnz1^2 K (p+1)^2 q       MACs   (prods: mass 1, stiffness 2)
+with nnz1 = (K+p)(2p+1) - p(p+1) the 1D band pairs.  Each 1D band pair
+(I, J) overlaps sum_e = K (p+1)^2 element-local pairs in total, which is
+where the K (p+1)^2 factors come from.
+
+Bytes: 8 nnz written (each CSR value exactly once) + 8 K^3 q^3 read when a
+per-quadrature-point coefficient field is given.
+"""
+
+from __future__ import annotations
+
+
+def nnz1(K: int, p: int) -> int:
+    return (K + p) * (2 * p + 1) - p * (p + 1)
+
+
+def assembled_macs(op: str, K: int, p: int, q: int) -> int:
+    m2 = (p + 1) ** 2
+    t = nnz1(K, p)
+    types, pb, ps = (1, 1, 1) if op == "mass" else (2, 3, 2)
+    a = types * K**3 * m2 * q**3
+    b = pb * t * K**2 * m2 * q**2
+    s = ps * t * t * K * m2 * q
+    return a + b + s
+
+
+def assembled_flops(op: str, K: int, p: int, q: int) -> int:
+    return 2 * assembled_macs(op, K, p, q)
+
+
+def element_sumfact_flops(op: str, p: int, q: int) -> int:
+    """SURVEY.md §8(d) general element-local sum factorization, per element."""
+    m = p + 1
+    S1, S2, S3 = m * m * q**3, m**4 * q * q, (m**3 * (m**3 + 1) // 2) * q
+    if op == "mass":
+        return 2 * (S1 + S2 + S3)
+    return 2 * (2 * S1 + 3 * S2 + 2 * S3)
+
+
+def algorithmic_bytes(dim: int, K: int, p: int, q: int, coefficient_field: bool) -> int:
+    nnz = nnz1(K, p) ** dim
+    b = 8 * nnz
+    if coefficient_field:
+        b += 8 * K**dim * q**dim
+    return b

@@ -113,6 +113,56 @@ def method_code(cfg: RunConfig) -> int:
     return _lib.METHOD_SUMFACT_ASSEMBLED
 
 
+class DeviceSession:
+    """Persistent device buffers for repeated integrate+assemble calls.
+
+    ``step()`` runs the device hot path (K1 tables + fused integrate/assemble)
+    on resident inputs; ``step_host(out)`` is the end-to-end call with host
+    buffers: the problem inputs (Gauss nodes/weights and the coefficient
+    field, if any) are copied host->device, the matrix is integrated and
+    assembled, and the CSR values are copied device->host into ``out``
+    (pinned host memory for full PCIe bandwidth)."""
+
+    def __init__(self, cfg: RunConfig, stream=None):
+        torch = _lib.require_cuda()
+        self.cfg = cfg
+        self.code = method_code(cfg)
+        self.prob = MeshProblem(cfg.dim, cfg.mesh, cfg.degree, cfg.points, cfg.operator,
+                                cfg.coefficient)
+        self.stream = stream if stream is not None else torch.cuda.current_stream()
+        self.values = torch.empty(self.prob.nnz(), dtype=torch.float64, device=self.prob.device)
+        self._host_in = [torch.from_numpy(self.prob.ref_nodes_host).pin_memory(),
+                         torch.from_numpy(self.prob.weights_host).pin_memory()]
+        self._host_coef = None
+        if self.prob.coef is not None:
+            self._host_coef = self.prob.coef.cpu().pin_memory()
+
+    @property
+    def h2d_bytes(self) -> int:
+        n = sum(t.numel() * 8 for t in self._host_in)
+        return n + (0 if self._host_coef is None else self._host_coef.numel() * 8)
+
+    @property
+    def d2h_bytes(self) -> int:
+        return self.values.numel() * 8
+
+    def step(self):
+        self.prob.build_tables(self.stream)
+        self.prob.integrate_assemble(self.values, self.code, stream=self.stream)
+        return self.values
+
+    def step_host(self, out):
+        torch = _lib.require_cuda()
+        with torch.cuda.stream(self.stream):
+            self.prob.ref_nodes.copy_(self._host_in[0], non_blocking=True)
+            self.prob.weights.copy_(self._host_in[1], non_blocking=True)
+            if self._host_coef is not None:
+                self.prob.coef.copy_(self._host_coef, non_blocking=True)
+            self.step()
+            out.copy_(self.values, non_blocking=True)
+        return out
+
+
 class IntegrationRuntime:
     """Owns the device buffers for one configuration; ``run`` is not reentrant
     (runtime.py:155-185)."""
@@ -136,22 +186,18 @@ class IntegrationRuntime:
     def _run_locked(self) -> RunResult:
         torch = _lib.require_cuda()
         cfg = self.cfg
-        code = method_code(cfg)
-        prob = MeshProblem(cfg.dim, cfg.mesh, cfg.degree, cfg.points, cfg.operator,
-                           cfg.coefficient)
-        values = torch.empty(prob.nnz(), dtype=torch.float64, device=prob.device)
-        stream = torch.cuda.current_stream()
+        sess = DeviceSession(cfg)
+        prob, stream = sess.prob, sess.stream
         times = []
         for _ in range(cfg.repetitions):
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            prob.build_tables(stream)
-            prob.integrate_assemble(values, code, stream=stream)
+            sess.step()
             e1.record(stream)
             e1.synchronize()
             times.append(e0.elapsed_time(e1) / 1e3)
-        gram = GlobalGram(K=cfg.mesh, p=cfg.degree, n_dofs=prob.n_dofs, values=values,
+        gram = GlobalGram(K=cfg.mesh, p=cfg.degree, n_dofs=prob.n_dofs, values=sess.values,
                           dim=cfg.dim)
         per_el = flop_count(cfg.method, cfg.degree, cfg.points)
         return RunResult(config=cfg, gram=gram, times=times, flops=per_el * prob.n_elements)
