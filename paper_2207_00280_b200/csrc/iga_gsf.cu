@@ -26,6 +26,8 @@
 //   stiffness       : X_V, X_D, Y_A = X_D VV + X_V DD, Y_B = X_V VV,
 //                     S += Y_A VV + Y_B DD
 //   stiffness+mass  : as stiffness with S += Y_A VV + Y_B (DD + VV)
+#include <cstdlib>
+
 #include "iga_args.cuh"
 #include "iga_dispatch.cuh"
 
@@ -242,9 +244,16 @@ struct GsfTile {
   static constexpr int TB = P <= 3 ? 4 : (P == 4 ? 2 : 1);
 };
 
+int launch_gsf_p3(const GsfArgs& a, cudaStream_t s);  // iga_gsf_p3.cu (DMMA, p=3 q=4)
+
 template <int P, int Q>
 struct GsfLaunch {
   static int run(const GsfArgs& a0, cudaStream_t s) {
+    if constexpr (P == 3 && Q == 4) {
+      // tensor-core specialisation; IGA_GSF_GENERIC=1 selects the generic kernel (A/B tests)
+      const char* env = getenv("IGA_GSF_GENERIC");
+      if (!(env && env[0] == '1')) return launch_gsf_p3(a0, s);
+    }
     constexpr int TA = GsfTile<P>::TA, TB = GsfTile<P>::TB;
     using Sh = GsfShape<P, Q, TA, TB>;
     if constexpr (Sh::bytes > 227 * 1024) {
