@@ -38,23 +38,24 @@ constexpr int WP = NCOL + 4;             // W row pitch (== 4 mod 16: conflict-f
 constexpr int NA0 = TA * NB;             // (ia, d0) rows (14)
 constexpr int NCOMBO = NA0 * TB * NB;    // (ia, d0, ib, d1) combos (392)
 constexpr int YP = NCOMBO + 4;           // Y pitch (== 12 mod 16: conflict-free A loads)
-constexpr int ROWV = NB * NB * NB;       // values of an interior CSR row (343)
-constexpr int NT = 256;                  // threads (8 warps)
+constexpr int NT = 512;                  // threads (16 warps)
 constexpr int NW = NT / 32;
-constexpr int MT_A = NCOL / 8;           // 14
-constexpr int MT_B = NA0 * Q / 8;        // 7
-constexpr int MT_S = NCOMBO / 8;         // 49
-constexpr int MT_S_PER_WARP = (MT_S + NW - 1) / NW;  // 7
+constexpr int MT_A = NCOL / 8;           // 14 m-tiles of (g1,k2) columns
+constexpr int MT_B = NA0 * Q / 8;        // 7 m-tiles of (a0,k2) rows
+constexpr int MT_S = NCOMBO / 8;         // 49 m-tiles of combos
+constexpr int MT_S_PER_WARP = (MT_S + NW - 1) / NW;  // 4
+constexpr int NPEN = TA * TB;            // row pencils (I0, I1) of the tile
 
 // shared memory layout (doubles)
-constexpr int OFF_W = 0;                                  // [LA*Q][WP]
-constexpr int OFF_X = OFF_W + LA * Q * WP;                // [2][NA0][NCOL]
-constexpr int OFF_Y = OFF_X + 2 * NA0 * NCOL;             // [2*Q][YP]
-constexpr int OFF_BA = OFF_Y + 2 * Q * YP;                // [2 types][LA][2 nt][32]
-constexpr int OFF_BB = OFF_BA + 2 * LA * 2 * 32;          // [2 prods][LB][2 nt][32]
-constexpr int OFF_ST = OFF_BB + 2 * LB * 2 * 32;          // staging [TA*TB][ROWV]
-constexpr int OFF_WQ = OFF_ST + TA * TB * ROWV;           // weights [Q]
-constexpr int SMEM_DOUBLES = OFF_WQ + 8;
+constexpr int OFF_W = 0;                          // [LA*Q][WP]
+constexpr int OFF_X = OFF_W + LA * Q * WP;        // [2 types][NA0][NCOL]
+constexpr int OFF_Y = OFF_X + 2 * NA0 * NCOL;     // [2 accs * Q][YP]
+constexpr int OFF_BA = OFF_Y + 2 * Q * YP;        // [2 types][LA][2 nt][32]
+constexpr int OFF_BB = OFF_BA + 2 * LA * 2 * 32;  // [2 prods][LB][2 nt][32]
+constexpr int OFF_WQ = OFF_BB + 2 * LB * 2 * 32;  // weights [Q]
+constexpr int OFF_PB = OFF_WQ + Q;                // pencil row-pointer bases (int64) [NPEN]
+constexpr int OFF_PC = OFF_PB + NPEN;             // pencil c0*c1 (as double-sized slots) [NPEN]
+constexpr int SMEM_DOUBLES = OFF_PC + NPEN;
 constexpr size_t SMEM_BYTES = SMEM_DOUBLES * sizeof(double);
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b, double c0,
@@ -64,10 +65,11 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b,
                : "d"(a), "d"(b), "d"(c0), "d"(c1));
 }
 
-// element offset of column k = 2*nt + j (r = k) for destination index i = l + r - P
-// to be inside [0, T): is any column of n-tile nt useful for window element l?
-__host__ __device__ constexpr bool nt_useful(int l, int nt, int T) {
-  return (l + 2 * nt - P >= 0 && l + 2 * nt - P < T) || (l + 2 * nt + 1 - P >= 0 && l + 2 * nt + 1 - P < T);
+// Is any column k in {2nt, 2nt+1} of window element l mapped to a destination
+// index l + k - P inside [lo, hi)?
+__host__ __device__ constexpr bool nt_useful(int l, int nt, int lo, int hi) {
+  return (l + 2 * nt - P >= lo && l + 2 * nt - P < hi) ||
+         (l + 2 * nt + 1 - P >= lo && l + 2 * nt + 1 - P < hi);
 }
 
 // B-fragment column mapping: lane (g, t) holds B[k=t][n=g]; column n of n-tile nt
@@ -75,40 +77,129 @@ __host__ __device__ constexpr bool nt_useful(int l, int nt, int T) {
 __device__ __forceinline__ int bcol_r(int nt, int g) { return 2 * nt + (g & 1); }
 __device__ __forceinline__ int bcol_s(int nt, int g) { return (bcol_r(nt, g) + (g >> 1)) & 3; }
 
+struct Ctx {
+  double* W;
+  double* X;
+  double* Y;
+  const double* BA;
+  const double* BB;
+  int lane, warp, g, t;
+  bool stiff, smass;
+};
+
+// ---- stage A unit: m-tile mt of (g1,k2) columns, type ty (0 = values, 1 = derivatives)
+__device__ __forceinline__ void stage_a_unit(const Ctx& c, int mt, int ty) {
+  double acc[TA][4];
+#pragma unroll
+  for (int ia = 0; ia < TA; ++ia)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) acc[ia][k] = 0.0;
+#pragma unroll
+  for (int la = 0; la < LA; ++la) {
+    const double av = c.W[(la * Q + c.t) * WP + mt * 8 + c.g];
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      if (!nt_useful(la, nt, 0, TA)) continue;
+      double c0, c1;
+      dmma(c0, c1, av, c.BA[((ty * LA + la) * 2 + nt) * 32 + c.lane], 0.0, 0.0);
+      const int ia0 = la + 2 * nt - P, ia1 = ia0 + 1;
+      if (ia0 >= 0 && ia0 < TA) acc[ia0][2 * nt] += c0;
+      if (ia1 >= 0 && ia1 < TA) acc[ia1][2 * nt + 1] += c1;
+    }
+  }
+  const int col = mt * 8 + c.g, t = c.t;
+#pragma unroll
+  for (int ia = 0; ia < TA; ++ia) {
+    double hi = 0.0, lo = 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (k < 4 - t) hi += acc[ia][k]; else lo += acc[ia][k];
+    }
+    c.X[(ty * NA0 + ia * NB + P + t) * NCOL + col] = hi;
+    if (t > 0) c.X[(ty * NA0 + ia * NB + t - 1) * NCOL + col] = lo;
+  }
+}
+
+// ---- stage B unit: m-tile mt of (a0,k2) rows, destination ib in {2H, 2H+1}
+template <int H>
+__device__ __forceinline__ void stage_b_unit(const Ctx& c, int mt) {
+  const int row = mt * 8 + c.g, a0 = row >> 2, k2 = row & 3, t = c.t;
+  double yA[2][2], yB[2][2];
+#pragma unroll
+  for (int i = 0; i < 2; ++i) yA[i][0] = yA[i][1] = yB[i][0] = yB[i][1] = 0.0;
+#pragma unroll
+  for (int lb = 2 * H; lb <= 2 * H + 4; ++lb) {
+    const int xo = (lb * Q + t) * Q + k2;
+    const double xv = c.X[(0 * NA0 + a0) * NCOL + xo];
+    const double xd = c.stiff ? c.X[(1 * NA0 + a0) * NCOL + xo] : 0.0;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) {
+      if (!nt_useful(lb, nt, 2 * H, 2 * H + 2)) continue;
+      const double vv = c.BB[((0 * LB + lb) * 2 + nt) * 32 + c.lane];
+      double cA0, cA1, cB0 = 0.0, cB1 = 0.0;
+      if (c.stiff) {
+        const double dd = c.BB[((1 * LB + lb) * 2 + nt) * 32 + c.lane];
+        dmma(cA0, cA1, xd, vv, 0.0, 0.0);
+        dmma(cB0, cB1, xv, vv, 0.0, 0.0);
+        dmma(cA0, cA1, xv, dd, cA0, cA1);
+      } else {
+        dmma(cA0, cA1, xv, vv, 0.0, 0.0);
+      }
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int k = 2 * nt + j, ib = lb + k - P - 2 * H;
+        if (ib >= 0 && ib < 2) {
+          const double ca = j ? cA1 : cA0, cb = j ? cB1 : cB0;
+          if (k < 4 - t) { yA[ib][0] += ca; yB[ib][0] += cb; }
+          else { yA[ib][1] += ca; yB[ib][1] += cb; }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int ib = 2 * H + i;
+    const int ch = (a0 * TB + ib) * NB + P + t;
+    c.Y[(0 * Q + k2) * YP + ch] = yA[i][0];
+    if (c.stiff) c.Y[(1 * Q + k2) * YP + ch] = yB[i][0];
+    if (t > 0) {
+      const int cl = (a0 * TB + ib) * NB + t - 1;
+      c.Y[(0 * Q + k2) * YP + cl] = yA[i][1];
+      if (c.stiff) c.Y[(1 * Q + k2) * YP + cl] = yB[i][1];
+    }
+  }
+}
+
+// ---- stage S: element e2 along axis 2 into the rolling row accumulators
 template <int PHI>
-__device__ __forceinline__ void stage_s_and_flush(double (&R)[MT_S_PER_WARP][4][2], const double* sm,
-                                                  double* stage, const GsfArgs& a, int e2,
-                                                  int warp, int g, int t, int lane, bool stiff,
-                                                  bool smass) {
-  // B fragments of element e2: Z0 = V V, Z1 = D D (+ V V for stiffness+mass)
+__device__ __forceinline__ void stage_s(const Ctx& c, double (&R)[MT_S_PER_WARP][4][2],
+                                        const GsfArgs& a, int e2) {
+  const int g = c.g, t = c.t;
   const double* V2 = a.V + (int64_t)e2 * M * Q;
   double b0[2], b1[2];
 #pragma unroll
   for (int nt = 0; nt < 2; ++nt) {
     const int r = bcol_r(nt, g), s = bcol_s(nt, g);
-    const double vr = __ldg(V2 + r * Q + t), vs = __ldg(V2 + s * Q + t);
-    b0[nt] = vr * vs;
-    if (stiff) {
+    b0[nt] = __ldg(V2 + r * Q + t) * __ldg(V2 + s * Q + t);
+    b1[nt] = 0.0;
+    if (c.stiff) {
       const double* D2 = a.D + (int64_t)e2 * M * Q;
       double z = __ldg(D2 + r * Q + t) * __ldg(D2 + s * Q + t);
-      if (smass) z += b0[nt];
+      if (c.smass) z += b0[nt];
       b1[nt] = z;
-    } else {
-      b1[nt] = 0.0;
     }
   }
-  const double* Ys = sm + OFF_Y;
 #pragma unroll
   for (int i = 0; i < MT_S_PER_WARP; ++i) {
-    const int mt = warp + i * NW;
+    const int mt = c.warp + i * NW;
     if (mt < MT_S) {
-      const double a0 = Ys[(0 * Q + t) * YP + mt * 8 + g];
-      const double a1 = stiff ? Ys[(1 * Q + t) * YP + mt * 8 + g] : 0.0;
+      const double a0 = c.Y[(0 * Q + t) * YP + mt * 8 + g];
+      const double a1 = c.stiff ? c.Y[(1 * Q + t) * YP + mt * 8 + g] : 0.0;
 #pragma unroll
       for (int nt = 0; nt < 2; ++nt) {
         double c0, c1;
         dmma(c0, c1, a0, b0[nt], 0.0, 0.0);
-        if (stiff) dmma(c0, c1, a1, b1[nt], c0, c1);
+        if (c.stiff) dmma(c0, c1, a1, b1[nt], c0, c1);
         // column k = 2nt + j has r = k: destination row e2 + k -> slot (PHI + k) & 3
         const int k0 = 2 * nt, k1 = 2 * nt + 1;
         if (k0 < 4 - t) R[i][(PHI + k0) & 3][0] += c0; else R[i][(PHI + k0) & 3][1] += c0;
@@ -118,87 +209,86 @@ __device__ __forceinline__ void stage_s_and_flush(double (&R)[MT_S_PER_WARP][4][
   }
 }
 
-// Row e2 (slot SL) is complete: lanes put their values into the staging rows.
+// Row I2 (slot SL) is complete: each lane stores its (up to) two values per m-tile
+// straight to the CSR row (neighbouring lanes cover contiguous row segments).
 template <int SL>
-__device__ __forceinline__ void flush_slot(double (&R)[MT_S_PER_WARP][4][2], double* stage,
-                                           int I2, int i00, int i10, int64_t N, int warp, int g,
-                                           int t) {
+__device__ __forceinline__ void flush(const Ctx& c, double (&R)[MT_S_PER_WARP][4][2],
+                                      const int (&meta)[MT_S_PER_WARP], const int64_t* pb,
+                                      const int* pc, const GsfArgs& a, int I2, int64_t N) {
+  const int t = c.t;
   const int lod2 = max(0, P - I2);
   const int c2 = (int)band_cnt(I2, P, N);
+  const int64_t pre2 = band_prefix(I2, P, N);
+  const int dh = P + t - lod2, dl = t - 1 - lod2;
 #pragma unroll
   for (int i = 0; i < MT_S_PER_WARP; ++i) {
-    const int mt = warp + i * NW;
-    if (mt < MT_S) {
-      const int c = mt * 8 + g;
-      const int d1 = c % NB, ib = (c / NB) % TB, a0 = c / (NB * TB);
-      const int d0 = a0 % NB, ia = a0 / NB;
-      const int I0 = i00 + ia, I1 = i10 + ib;
-      const int lod0 = max(0, P - I0), lod1 = max(0, P - I1);
-      const int c0 = (int)band_cnt(I0, P, N), c1 = (int)band_cnt(I1, P, N);
-      const bool ok01 = d0 >= lod0 && d0 < lod0 + c0 && d1 >= lod1 && d1 < lod1 + c1;
-      double* row = stage + (ia * TB + ib) * ROWV;
-      const int base = ((d0 - lod0) * c1 + (d1 - lod1)) * c2;
-      const int dh = P + t, dl = t - 1;
-      if (ok01 && dh >= lod2 && dh < lod2 + c2) row[base + dh - lod2] = R[i][SL][0];
-      if (ok01 && t > 0 && dl >= lod2 && dl < lod2 + c2) row[base + dl - lod2] = R[i][SL][1];
-      R[i][SL][0] = 0.0;
-      R[i][SL][1] = 0.0;
+    const int m = meta[i];
+    if (m >= 0) {
+      const int rc = m >> 16, b01 = m & 0xffff;
+      double* row = a.values + pb[rc] + (int64_t)pc[rc] * pre2 + b01 * c2;
+      if (dh >= 0 && dh < c2) row[dh] = R[i][SL][0];
+      if (t > 0 && dl >= 0 && dl < c2) row[dl] = R[i][SL][1];
     }
+    R[i][SL][0] = 0.0;
+    R[i][SL][1] = 0.0;
   }
 }
 
-__device__ __forceinline__ void flush_dispatch(int sl, double (&R)[MT_S_PER_WARP][4][2],
-                                               double* stage, int I2, int i00, int i10, int64_t N,
-                                               int warp, int g, int t) {
+__device__ __forceinline__ void flush_any(int sl, const Ctx& c, double (&R)[MT_S_PER_WARP][4][2],
+                                          const int (&meta)[MT_S_PER_WARP], const int64_t* pb,
+                                          const int* pc, const GsfArgs& a, int I2, int64_t N) {
   switch (sl) {
-    case 0: flush_slot<0>(R, stage, I2, i00, i10, N, warp, g, t); break;
-    case 1: flush_slot<1>(R, stage, I2, i00, i10, N, warp, g, t); break;
-    case 2: flush_slot<2>(R, stage, I2, i00, i10, N, warp, g, t); break;
-    default: flush_slot<3>(R, stage, I2, i00, i10, N, warp, g, t); break;
+    case 0: flush<0>(c, R, meta, pb, pc, a, I2, N); break;
+    case 1: flush<1>(c, R, meta, pb, pc, a, I2, N); break;
+    case 2: flush<2>(c, R, meta, pb, pc, a, I2, N); break;
+    default: flush<3>(c, R, meta, pb, pc, a, I2, N); break;
   }
 }
 
-// Coalesced copy of the finished rows (I0, I1, I2) of the tile to the CSR values.
-__device__ __forceinline__ void store_rows(const double* stage, const GsfArgs& a, int I2, int i00,
-                                           int i10, int64_t N, int tid) {
-  const int64_t c2 = band_cnt(I2, P, N);
-#pragma unroll
-  for (int rc = 0; rc < TA * TB; ++rc) {
-    const int ia = rc / TB, ib = rc % TB;
-    const int64_t I0 = i00 + ia, I1 = i10 + ib;
-    if (I0 >= a.plane_end || I1 >= N) continue;
-    const int cnt = (int)(band_cnt(I0, P, N) * band_cnt(I1, P, N) * c2);
-    double* dst = a.values + (rowptr3(I0, I1, I2, P, N) - a.base);
-    const double* src = stage + rc * ROWV;
-    for (int j = tid; j < cnt; j += NT) dst[j] = src[j];
+__device__ __forceinline__ void form_w(double* W, const double* wq, const GsfArgs& a, int e2,
+                                       int i00, int i10, int e0lo, int e0hi, int tid) {
+  const int K = a.K;
+  for (int u = tid; u < LA * Q * NCOL; u += NT) {
+    const int row = u / NCOL, col = u - row * NCOL;
+    const int la = row >> 2, k0 = row & 3;
+    const int g1 = col >> 2, k2 = col & 3, lb = g1 >> 2, k1 = g1 & 3;
+    const int e0 = i00 - P + la, e1 = i10 - P + lb;
+    double w = 0.0;
+    if (e0 >= e0lo && e0 < e0hi && e1 >= 0 && e1 < K) {
+      const double cf = a.coef ? __ldg(a.coef + (((int64_t)e0 * K + e1) * K + e2) * (Q * Q * Q) +
+                                       (k0 * Q + k1) * Q + k2)
+                               : a.coef_scalar;
+      w = wq[k0] * wq[k1] * wq[k2] * a.jac * cf;
+    }
+    W[row * WP + col] = w;
   }
 }
 
 __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
   extern __shared__ double sm[];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
+  const int tid = threadIdx.x;
+  Ctx c;
+  c.lane = tid & 31; c.warp = tid >> 5; c.g = c.lane >> 2; c.t = c.lane & 3;
+  c.stiff = a.op != IGA_OP_MASS;
+  c.smass = a.op == IGA_OP_STIFFNESS_MASS;
+  c.W = sm + OFF_W; c.X = sm + OFF_X; c.Y = sm + OFF_Y; c.BA = sm + OFF_BA; c.BB = sm + OFF_BB;
+  double* wq = sm + OFF_WQ;
+  int64_t* pb = reinterpret_cast<int64_t*>(sm + OFF_PB);
+  int* pc = reinterpret_cast<int*>(sm + OFF_PC);
   const int K = a.K;
   const int64_t N = (int64_t)K + P;
   const int tile0 = blockIdx.x / a.tiles1, tile1 = blockIdx.x % a.tiles1;
   const int i00 = a.plane_begin + tile0 * TA, i10 = tile1 * TB;
-  const bool stiff = a.op != IGA_OP_MASS;
-  const bool smass = a.op == IGA_OP_STIFFNESS_MASS;
   const int e0lo = max(a.el_begin, 0), e0hi = min(a.el_end, K);
-  double* W = sm + OFF_W;
-  double* X = sm + OFF_X;
-  double* Ys = sm + OFF_Y;
-  double* BA = sm + OFF_BA;
-  double* BB = sm + OFF_BB;
-  double* stage = sm + OFF_ST;
-  double* wq = sm + OFF_WQ;
 
   // ---- constant B fragments of axes 0 and 1 (pair products of the window elements)
+  double* BA = sm + OFF_BA;
+  double* BB = sm + OFF_BB;
   for (int u = tid; u < 2 * LA * 2 * 32; u += NT) {
     const int ln = u & 31, nt = (u >> 5) & 1, la = (u >> 6) % LA, type = u / (64 * LA);
-    const int gg = ln >> 2, tt = ln & 3;
-    const int e0 = i00 - P + la;
+    const int gg = ln >> 2, tt = ln & 3, e0 = i00 - P + la;
     double v = 0.0;
-    if (e0 >= 0 && e0 < K && (type == 0 || stiff)) {
+    if (e0 >= 0 && e0 < K && (type == 0 || c.stiff)) {
       const double* T = (type == 0 ? a.V : a.D) + (int64_t)e0 * M * Q;
       v = T[bcol_r(nt, gg) * Q + tt] * T[bcol_s(nt, gg) * Q + tt];
     }
@@ -206,16 +296,42 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
   }
   for (int u = tid; u < 2 * LB * 2 * 32; u += NT) {
     const int ln = u & 31, nt = (u >> 5) & 1, lb = (u >> 6) % LB, prod = u / (64 * LB);
-    const int gg = ln >> 2, tt = ln & 3;
-    const int e1 = i10 - P + lb;
+    const int gg = ln >> 2, tt = ln & 3, e1 = i10 - P + lb;
     double v = 0.0;
-    if (e1 >= 0 && e1 < K && (prod == 0 || stiff)) {
+    if (e1 >= 0 && e1 < K && (prod == 0 || c.stiff)) {
       const double* T = (prod == 0 ? a.V : a.D) + (int64_t)e1 * M * Q;
       v = T[bcol_r(nt, gg) * Q + tt] * T[bcol_s(nt, gg) * Q + tt];
     }
     BB[u] = v;
   }
   if (tid < Q) wq[tid] = a.weights[tid];
+  if (tid < NPEN) {
+    const int64_t I0 = i00 + tid / TB, I1 = i10 + tid % TB;
+    // rowptr of (I0, I1, 0) relative to the launch's first row; c0*c1 per I2-prefix unit
+    pb[tid] = (I0 < N && I1 < N) ? rowptr3(I0, I1, 0, P, N) - a.base : 0;
+    pc[tid] = (I0 < N && I1 < N) ? (int)(band_cnt(I0, P, N) * band_cnt(I1, P, N)) : 0;
+  }
+
+  // per-lane flush metadata of its stage-S m-tiles: staging pencil rc and the (d0,d1)
+  // block offset b01 = (d0-lo0)*c1 + (d1-lo1) in the CSR row; -1 if the combo is outside
+  int meta[MT_S_PER_WARP];
+#pragma unroll
+  for (int i = 0; i < MT_S_PER_WARP; ++i) {
+    const int mt = c.warp + i * NW;
+    meta[i] = -1;
+    if (mt < MT_S) {
+      const int cb = mt * 8 + c.g;
+      const int d1 = cb % NB, ib = (cb / NB) % TB, a0 = cb / (NB * TB);
+      const int d0 = a0 % NB, ia = a0 / NB;
+      const int I0 = i00 + ia, I1 = i10 + ib;
+      if (I0 < a.plane_end && I1 < N) {
+        const int lod0 = max(0, P - I0), lod1 = max(0, P - I1);
+        const int c0 = (int)band_cnt(I0, P, N), c1 = (int)band_cnt(I1, P, N);
+        if (d0 >= lod0 && d0 < lod0 + c0 && d1 >= lod1 && d1 < lod1 + c1)
+          meta[i] = ((ia * TB + ib) << 16) | ((d0 - lod0) * c1 + (d1 - lod1));
+      }
+    }
+  }
 
   double R[MT_S_PER_WARP][4][2];
 #pragma unroll
@@ -224,137 +340,34 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
     for (int s = 0; s < 4; ++s) R[i][s][0] = R[i][s][1] = 0.0;
 
   __syncthreads();
+  if (a.coef == nullptr) form_w(c.W, wq, a, 0, i00, i10, e0lo, e0hi, tid);  // step-invariant
 
+  const int nA = c.stiff ? 2 * MT_A : MT_A;
   for (int e2 = 0; e2 < K; ++e2) {
-    // ---- W[(la,k0)][(g1,k2)] = c * w0 w1 w2 * jac on the CTA's slab of element column e2
-    for (int u = tid; u < LA * Q * NCOL; u += NT) {
-      const int row = u / NCOL, col = u - row * NCOL;
-      const int la = row >> 2, k0 = row & 3;
-      const int g1 = col >> 2, k2 = col & 3, lb = g1 >> 2, k1 = g1 & 3;
-      const int e0 = i00 - P + la, e1 = i10 - P + lb;
-      double w = 0.0;
-      if (e0 >= e0lo && e0 < e0hi && e1 >= 0 && e1 < K) {
-        const double c = a.coef ? __ldg(a.coef + (((int64_t)e0 * K + e1) * K + e2) * (Q * Q * Q) +
-                                        (k0 * Q + k1) * Q + k2)
-                                : a.coef_scalar;
-        w = wq[k0] * wq[k1] * wq[k2] * a.jac * c;
-      }
-      W[row * WP + col] = w;
+    if (a.coef != nullptr) form_w(c.W, wq, a, e2, i00, i10, e0lo, e0hi, tid);
+    __syncthreads();
+    // stage A: units (m-tile, type)
+    for (int u = c.warp; u < nA; u += NW) {
+      if (c.stiff) stage_a_unit(c, u >> 1, u & 1);
+      else stage_a_unit(c, u, 0);
     }
     __syncthreads();
-
-    // ---- stage A: contract axis 0; lanes own columns (g1,k2), accumulate X[type][ia][d0]
-    for (int mt = warp; mt < MT_A; mt += NW) {
-      double acc[2][TA][2];
-#pragma unroll
-      for (int ty = 0; ty < 2; ++ty)
-#pragma unroll
-        for (int ia = 0; ia < TA; ++ia) acc[ty][ia][0] = acc[ty][ia][1] = 0.0;
-#pragma unroll
-      for (int la = 0; la < LA; ++la) {
-        const double av = W[(la * Q + t) * WP + mt * 8 + g];
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt) {
-          if (!nt_useful(la, nt, TA)) continue;
-#pragma unroll
-          for (int ty = 0; ty < 2; ++ty) {
-            if (ty == 1 && !stiff) continue;
-            double c0, c1;
-            dmma(c0, c1, av, BA[((ty * LA + la) * 2 + nt) * 32 + lane], 0.0, 0.0);
-#pragma unroll
-            for (int j = 0; j < 2; ++j) {
-              const int k = 2 * nt + j, ia = la + k - P;
-              if (ia >= 0 && ia < TA) {
-                const double c = j ? c1 : c0;
-                if (k < 4 - t) acc[ty][ia][0] += c; else acc[ty][ia][1] += c;
-              }
-            }
-          }
-        }
-      }
-      const int col = mt * 8 + g;
-#pragma unroll
-      for (int ty = 0; ty < 2; ++ty) {
-        if (ty == 1 && !stiff) continue;
-#pragma unroll
-        for (int ia = 0; ia < TA; ++ia) {
-          X[(ty * NA0 + ia * NB + P + t) * NCOL + col] = acc[ty][ia][0];
-          if (t > 0) X[(ty * NA0 + ia * NB + t - 1) * NCOL + col] = acc[ty][ia][1];
-        }
-      }
+    // stage B: units (m-tile, ib half)
+    if (c.warp < 2 * MT_B) {
+      if (c.warp & 1) stage_b_unit<1>(c, c.warp >> 1);
+      else stage_b_unit<0>(c, c.warp >> 1);
     }
     __syncthreads();
-
-    // ---- stage B: contract axis 1; rows (a0, k2), accumulate Y_A / Y_B[(a0, ib, d1)][k2]
-    if (warp < MT_B) {
-      const int mt = warp;
-      const int row = mt * 8 + g, a0 = row >> 2, k2 = row & 3;
-      double yA[TB][2], yB[TB][2];
-#pragma unroll
-      for (int ib = 0; ib < TB; ++ib) yA[ib][0] = yA[ib][1] = yB[ib][0] = yB[ib][1] = 0.0;
-#pragma unroll
-      for (int lb = 0; lb < LB; ++lb) {
-        const int xo = (lb * Q + t) * Q + k2;
-        const double xv = X[(0 * NA0 + a0) * NCOL + xo];
-        const double xd = stiff ? X[(1 * NA0 + a0) * NCOL + xo] : 0.0;
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt) {
-          if (!nt_useful(lb, nt, TB)) continue;
-          const double vv = BB[((0 * LB + lb) * 2 + nt) * 32 + lane];
-          double cA0, cA1, cB0 = 0.0, cB1 = 0.0;
-          if (stiff) {
-            const double dd = BB[((1 * LB + lb) * 2 + nt) * 32 + lane];
-            dmma(cA0, cA1, xd, vv, 0.0, 0.0);
-            dmma(cA0, cA1, xv, dd, cA0, cA1);
-            dmma(cB0, cB1, xv, vv, 0.0, 0.0);
-          } else {
-            dmma(cA0, cA1, xv, vv, 0.0, 0.0);
-          }
-#pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            const int k = 2 * nt + j, ib = lb + k - P;
-            if (ib >= 0 && ib < TB) {
-              const double ca = j ? cA1 : cA0, cb = j ? cB1 : cB0;
-              if (k < 4 - t) { yA[ib][0] += ca; yB[ib][0] += cb; }
-              else { yA[ib][1] += ca; yB[ib][1] += cb; }
-            }
-          }
-        }
-      }
-#pragma unroll
-      for (int ib = 0; ib < TB; ++ib) {
-        const int ch = (a0 * TB + ib) * NB + P + t;
-        Ys[(0 * Q + k2) * YP + ch] = yA[ib][0];
-        if (stiff) Ys[(1 * Q + k2) * YP + ch] = yB[ib][0];
-        if (t > 0) {
-          const int cl = (a0 * TB + ib) * NB + t - 1;
-          Ys[(0 * Q + k2) * YP + cl] = yA[ib][1];
-          if (stiff) Ys[(1 * Q + k2) * YP + cl] = yB[ib][1];
-        }
-      }
-    }
-    __syncthreads();
-
-    // ---- stage S: contract axis 2 within element e2 into the rolling rows; flush row e2
+    // stage S + flush of the finished row e2
     switch (e2 & 3) {
-      case 0: stage_s_and_flush<0>(R, sm, stage, a, e2, warp, g, t, lane, stiff, smass); break;
-      case 1: stage_s_and_flush<1>(R, sm, stage, a, e2, warp, g, t, lane, stiff, smass); break;
-      case 2: stage_s_and_flush<2>(R, sm, stage, a, e2, warp, g, t, lane, stiff, smass); break;
-      default: stage_s_and_flush<3>(R, sm, stage, a, e2, warp, g, t, lane, stiff, smass); break;
-    }
-    flush_dispatch(e2 & 3, R, stage, e2, i00, i10, N, warp, g, t);
-    __syncthreads();
-    store_rows(stage, a, e2, i00, i10, N, tid);
-    if (e2 == K - 1) {
-      // rows K .. K+P-1 received their last contribution from element K-1
-      for (int I2 = K; I2 < N; ++I2) {
-        __syncthreads();
-        flush_dispatch(I2 & 3, R, stage, I2, i00, i10, N, warp, g, t);
-        __syncthreads();
-        store_rows(stage, a, I2, i00, i10, N, tid);
-      }
+      case 0: stage_s<0>(c, R, a, e2); flush<0>(c, R, meta, pb, pc, a, e2, N); break;
+      case 1: stage_s<1>(c, R, a, e2); flush<1>(c, R, meta, pb, pc, a, e2, N); break;
+      case 2: stage_s<2>(c, R, a, e2); flush<2>(c, R, meta, pb, pc, a, e2, N); break;
+      default: stage_s<3>(c, R, a, e2); flush<3>(c, R, meta, pb, pc, a, e2, N); break;
     }
   }
+  // rows K .. K+P-1 received their last contribution from element K-1
+  for (int I2 = K; I2 < N; ++I2) flush_any(I2 & 3, c, R, meta, pb, pc, a, I2, N);
 }
 
 }  // namespace p3
