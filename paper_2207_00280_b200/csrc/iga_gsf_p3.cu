@@ -87,7 +87,11 @@ struct Ctx {
   bool stiff, smass;
 };
 
-// ---- stage A unit: m-tile mt of (g1,k2) columns, type ty (0 = values, 1 = derivatives)
+// Clamp helper for compile-time-resolved accumulator references.
+__host__ __device__ constexpr int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+
+// ---- stage A unit: m-tile mt of (g1,k2) columns, type ty (0 = values, 1 = derivatives).
+// Per-column accumulators acc[ia][k] are the DMMA C operands (in-place assembly over la).
 __device__ __forceinline__ void stage_a_unit(const Ctx& c, int mt, int ty) {
   double acc[TA][4];
 #pragma unroll
@@ -100,11 +104,11 @@ __device__ __forceinline__ void stage_a_unit(const Ctx& c, int mt, int ty) {
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) {
       if (!nt_useful(la, nt, 0, TA)) continue;
-      double c0, c1;
-      dmma(c0, c1, av, c.BA[((ty * LA + la) * 2 + nt) * 32 + c.lane], 0.0, 0.0);
       const int ia0 = la + 2 * nt - P, ia1 = ia0 + 1;
-      if (ia0 >= 0 && ia0 < TA) acc[ia0][2 * nt] += c0;
-      if (ia1 >= 0 && ia1 < TA) acc[ia1][2 * nt + 1] += c1;
+      double z0 = 0.0, z1 = 0.0;
+      double& r0 = (ia0 >= 0 && ia0 < TA) ? acc[clampi(ia0, 0, TA - 1)][2 * nt] : z0;
+      double& r1 = (ia1 >= 0 && ia1 < TA) ? acc[clampi(ia1, 0, TA - 1)][2 * nt + 1] : z1;
+      dmma(r0, r1, av, c.BA[((ty * LA + la) * 2 + nt) * 32 + c.lane], r0, r1);
     }
   }
   const int col = mt * 8 + c.g, t = c.t;
@@ -120,13 +124,16 @@ __device__ __forceinline__ void stage_a_unit(const Ctx& c, int mt, int ty) {
   }
 }
 
-// ---- stage B unit: m-tile mt of (a0,k2) rows, destination ib in {2H, 2H+1}
+// ---- stage B unit: m-tile mt of (a0,k2) rows, destination ib in {2H, 2H+1};
+// per-column accumulators are the DMMA C operands (in-place assembly over lb).
 template <int H>
 __device__ __forceinline__ void stage_b_unit(const Ctx& c, int mt) {
   const int row = mt * 8 + c.g, a0 = row >> 2, k2 = row & 3, t = c.t;
-  double yA[2][2], yB[2][2];
+  double yA[2][4], yB[2][4];
 #pragma unroll
-  for (int i = 0; i < 2; ++i) yA[i][0] = yA[i][1] = yB[i][0] = yB[i][1] = 0.0;
+  for (int i = 0; i < 2; ++i)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) yA[i][k] = yB[i][k] = 0.0;
 #pragma unroll
   for (int lb = 2 * H; lb <= 2 * H + 4; ++lb) {
     const int xo = (lb * Q + t) * Q + k2;
@@ -135,37 +142,40 @@ __device__ __forceinline__ void stage_b_unit(const Ctx& c, int mt) {
 #pragma unroll
     for (int nt = 0; nt < 2; ++nt) {
       if (!nt_useful(lb, nt, 2 * H, 2 * H + 2)) continue;
+      const int i0 = lb + 2 * nt - P - 2 * H, i1 = i0 + 1;
+      const bool v0 = i0 >= 0 && i0 < 2, v1 = i1 >= 0 && i1 < 2;
+      double z0 = 0.0, z1 = 0.0, z2 = 0.0, z3 = 0.0;
+      double& a0r = v0 ? yA[clampi(i0, 0, 1)][2 * nt] : z0;
+      double& a1r = v1 ? yA[clampi(i1, 0, 1)][2 * nt + 1] : z1;
+      double& b0r = v0 ? yB[clampi(i0, 0, 1)][2 * nt] : z2;
+      double& b1r = v1 ? yB[clampi(i1, 0, 1)][2 * nt + 1] : z3;
       const double vv = c.BB[((0 * LB + lb) * 2 + nt) * 32 + c.lane];
-      double cA0, cA1, cB0 = 0.0, cB1 = 0.0;
       if (c.stiff) {
         const double dd = c.BB[((1 * LB + lb) * 2 + nt) * 32 + c.lane];
-        dmma(cA0, cA1, xd, vv, 0.0, 0.0);
-        dmma(cB0, cB1, xv, vv, 0.0, 0.0);
-        dmma(cA0, cA1, xv, dd, cA0, cA1);
+        dmma(a0r, a1r, xd, vv, a0r, a1r);
+        dmma(b0r, b1r, xv, vv, b0r, b1r);
+        dmma(a0r, a1r, xv, dd, a0r, a1r);
       } else {
-        dmma(cA0, cA1, xv, vv, 0.0, 0.0);
-      }
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const int k = 2 * nt + j, ib = lb + k - P - 2 * H;
-        if (ib >= 0 && ib < 2) {
-          const double ca = j ? cA1 : cA0, cb = j ? cB1 : cB0;
-          if (k < 4 - t) { yA[ib][0] += ca; yB[ib][0] += cb; }
-          else { yA[ib][1] += ca; yB[ib][1] += cb; }
-        }
+        dmma(a0r, a1r, xv, vv, a0r, a1r);
       }
     }
   }
 #pragma unroll
   for (int i = 0; i < 2; ++i) {
+    double ah = 0.0, al = 0.0, bh = 0.0, bl = 0.0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      if (k < 4 - t) { ah += yA[i][k]; bh += yB[i][k]; }
+      else { al += yA[i][k]; bl += yB[i][k]; }
+    }
     const int ib = 2 * H + i;
     const int ch = (a0 * TB + ib) * NB + P + t;
-    c.Y[(0 * Q + k2) * YP + ch] = yA[i][0];
-    if (c.stiff) c.Y[(1 * Q + k2) * YP + ch] = yB[i][0];
+    c.Y[(0 * Q + k2) * YP + ch] = ah;
+    if (c.stiff) c.Y[(1 * Q + k2) * YP + ch] = bh;
     if (t > 0) {
       const int cl = (a0 * TB + ib) * NB + t - 1;
-      c.Y[(0 * Q + k2) * YP + cl] = yA[i][1];
-      if (c.stiff) c.Y[(1 * Q + k2) * YP + cl] = yB[i][1];
+      c.Y[(0 * Q + k2) * YP + cl] = al;
+      if (c.stiff) c.Y[(1 * Q + k2) * YP + cl] = bl;
     }
   }
 }
