@@ -13,9 +13,8 @@
 // row offset of column (r,s) is then a compile-time function of (element, r)
 // and its band offset d = s - r + 3 takes one of two lane-constant values
 // (d = 3+t if r < 4-t, else t-1), so each lane accumulates its contributions
-// to the assembled values in two registers per destination row -- no shared
-// memory read-modify-write, no atomics, and the assembly is exact-order
-// deterministic.
+// to the assembled values in registers -- no shared-memory read-modify-write,
+// no atomics, and a fixed summation order (bitwise reproducible).
 //
 //   stage A (axis 0): C[(g1,k2)][(r,s)] = sum_k0 W[la,k0][(g1,k2)] PA_la[k0][(r,s)]
 //                     -> X_T[ia = la+r-3][d0][(g1,k2)]                (T = V, D)
@@ -23,6 +22,15 @@
 //                     -> Y_A/Y_B[(a0, ib = lb+r-3, d1)][k2]
 //   stage S (axis 2): C[c][(r,s)] = sum_k2 Y[c][k2] Z_e2[k2][(r,s)]
 //                     -> R[c][row e2+r][d2]  (registers, rolling over 4 rows)
+//
+// Warp specialisation (software pipeline over the element column e2): 2 warps
+// run stage A on element e2 = it, 2 warps stage B on e2 = it-1 and 8 warps stage
+// S (+ the row stores) on e2 = it-2, all concurrently, with double-buffered X
+// and Y and one CTA barrier per iteration.  The DMMA pipe of every SM
+// sub-partition is shared by the three stages, so it stays busy across what
+// would otherwise be barrier-separated phases.  The constant B fragments of
+// stages A and B and the rolling rows of stage S live in registers (384 threads
+// x 168 registers), which keeps shared-memory traffic well under the DMMA time.
 #include "iga_args.cuh"
 #include "iga_dispatch.cuh"
 
@@ -38,31 +46,39 @@ constexpr int WP = NCOL + 4;             // W row pitch (== 4 mod 16: conflict-f
 constexpr int NA0 = TA * NB;             // (ia, d0) rows (14)
 constexpr int NCOMBO = NA0 * TB * NB;    // (ia, d0, ib, d1) combos (392)
 constexpr int YP = NCOMBO + 4;           // Y pitch (== 12 mod 16: conflict-free A loads)
-constexpr int NT = 512;                  // threads (16 warps)
-constexpr int NW = NT / 32;
+constexpr int NT = 384;                  // threads: 12 warps
 constexpr int MT_A = NCOL / 8;           // 14 m-tiles of (g1,k2) columns
 constexpr int MT_B = NA0 * Q / 8;        // 7 m-tiles of (a0,k2) rows
 constexpr int MT_S = NCOMBO / 8;         // 49 m-tiles of combos
-constexpr int MT_S_PER_WARP = (MT_S + NW - 1) / NW;  // 4
+constexpr int NWA = 2, NWB = 2, NWS = 8; // warps per role
+constexpr int MT_S_PER_WARP = (MT_S + NWS - 1) / NWS;  // 7
 constexpr int NPEN = TA * TB;            // row pencils (I0, I1) of the tile
 
 // shared memory layout (doubles)
+constexpr int SZ_X = 2 * NA0 * NCOL;              // one X buffer: [2 types][NA0][NCOL]
+constexpr int SZ_Y = 2 * Q * YP;                  // one Y buffer: [2 accs * Q][YP]
 constexpr int OFF_W = 0;                          // [LA*Q][WP]
-constexpr int OFF_X = OFF_W + LA * Q * WP;        // [2 types][NA0][NCOL]
-constexpr int OFF_Y = OFF_X + 2 * NA0 * NCOL;     // [2 accs * Q][YP]
-constexpr int OFF_BA = OFF_Y + 2 * Q * YP;        // [2 types][LA][2 nt][32]
+constexpr int OFF_X = OFF_W + LA * Q * WP;        // 2 buffers
+constexpr int OFF_Y = OFF_X + 2 * SZ_X;           // 2 buffers
+constexpr int OFF_BA = OFF_Y + 2 * SZ_Y;          // [2 types][LA][2 nt][32]
 constexpr int OFF_BB = OFF_BA + 2 * LA * 2 * 32;  // [2 prods][LB][2 nt][32]
 constexpr int OFF_WQ = OFF_BB + 2 * LB * 2 * 32;  // weights [Q]
 constexpr int OFF_PB = OFF_WQ + Q;                // pencil row-pointer bases (int64) [NPEN]
-constexpr int OFF_PC = OFF_PB + NPEN;             // pencil c0*c1 (as double-sized slots) [NPEN]
+constexpr int OFF_PC = OFF_PB + NPEN;             // pencil c0*c1 (int in double slots) [NPEN]
 constexpr int SMEM_DOUBLES = OFF_PC + NPEN;
+static_assert(SMEM_DOUBLES * 8 <= 227 * 1024, "shared memory budget");
 constexpr size_t SMEM_BYTES = SMEM_DOUBLES * sizeof(double);
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b, double c0,
                                      double c1) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%4,%5};\n"
-               : "=d"(d0), "=d"(d1)
-               : "d"(a), "d"(b), "d"(c0), "d"(c1));
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%4,%5};\n"
+      : "=d"(d0), "=d"(d1)
+      : "d"(a), "d"(b), "d"(c0), "d"(c1));
+}
+
+// barrier among the 4 warps of one warpgroup (ids 1..4)
+__device__ __forceinline__ void wg_bar(int id) {
+  asm volatile("bar.sync %0, 128;\n" ::"r"(id));
 }
 
 // Is any column k in {2nt, 2nt+1} of window element l mapped to a destination
@@ -71,120 +87,197 @@ __host__ __device__ constexpr bool nt_useful(int l, int nt, int lo, int hi) {
   return (l + 2 * nt - P >= lo && l + 2 * nt - P < hi) ||
          (l + 2 * nt + 1 - P >= lo && l + 2 * nt + 1 - P < hi);
 }
+__host__ __device__ constexpr int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
 // B-fragment column mapping: lane (g, t) holds B[k=t][n=g]; column n of n-tile nt
 // is the pair (r, s) = (2nt + (n&1), (r + (n>>1)) & 3).
 __device__ __forceinline__ int bcol_r(int nt, int g) { return 2 * nt + (g & 1); }
 __device__ __forceinline__ int bcol_s(int nt, int g) { return (bcol_r(nt, g) + (g >> 1)) & 3; }
 
-struct Ctx {
-  double* W;
-  double* X;
-  double* Y;
-  const double* BA;
-  const double* BB;
-  int lane, warp, g, t;
+// r += c on lanes where p holds (one predicated DADD, no select sequence)
+__device__ __forceinline__ void add_if(double& r, double c, int p) {
+  asm("{\n .reg .pred q;\n setp.ne.s32 q, %2, 0;\n @q add.rn.f64 %0, %0, %1;\n}\n"
+      : "+d"(r)
+      : "d"(c), "r"(p));
+}
+
+struct Lane {
+  int lane, g, t;
   bool stiff, smass;
 };
 
-// Clamp helper for compile-time-resolved accumulator references.
-__host__ __device__ constexpr int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
+// hi = sum_{k < 4-t} y[k] (band offset 3+t), lo = sum of the rest (offset t-1)
+__device__ __forceinline__ void split_groups(const double* y, int t, double& hi, double& lo) {
+  const double p1 = y[0] + y[1], p2 = p1 + y[2], p3 = p2 + y[3];
+  const double s2 = y[2] + y[3], s1 = y[1] + s2;
+  hi = t == 0 ? p3 : (t == 1 ? p2 : (t == 2 ? p1 : y[0]));
+  lo = t == 1 ? y[3] : (t == 2 ? s2 : s1);
+}
 
-// ---- stage A unit: m-tile mt of (g1,k2) columns, type ty (0 = values, 1 = derivatives).
-// Per-column accumulators acc[ia][k] are the DMMA C operands (in-place assembly over la).
-__device__ __forceinline__ void stage_a_unit(const Ctx& c, int mt, int ty) {
+// ---------------------------------------------------------------- stage A
+// Valid (element la, n-tile) pairs of stage A (destination ia = la + k - P in [0, TA))
+constexpr int NPA = 6;
+__host__ __device__ constexpr int pa_la(int i) { return i < 1 ? 0 : (i < 2 ? 1 : (i < 4 ? 2 : (i < 5 ? 3 : 4))); }
+__host__ __device__ constexpr int pa_nt(int i) { return i == 0 ? 1 : (i == 1 ? 1 : (i == 2 ? 0 : (i == 3 ? 1 : 0))); }
+
+// unit = (m-tile mt of (g1,k2) columns) for the warp's type; ba[] are the warp's
+// constant B fragments; per-column accumulators acc[ia][k] are the DMMA C operands
+// (each receives exactly one element's product).
+__device__ __forceinline__ void stage_a_unit(const Lane& L, const double* W, const double (&ba)[NPA],
+                                             double* X, int mt, int ty) {
   double acc[TA][4];
 #pragma unroll
   for (int ia = 0; ia < TA; ++ia)
 #pragma unroll
     for (int k = 0; k < 4; ++k) acc[ia][k] = 0.0;
+  double av[LA];
 #pragma unroll
-  for (int la = 0; la < LA; ++la) {
-    const double av = c.W[(la * Q + c.t) * WP + mt * 8 + c.g];
+  for (int la = 0; la < LA; ++la) av[la] = W[(la * Q + L.t) * WP + mt * 8 + L.g];
 #pragma unroll
-    for (int nt = 0; nt < 2; ++nt) {
-      if (!nt_useful(la, nt, 0, TA)) continue;
-      const int ia0 = la + 2 * nt - P, ia1 = ia0 + 1;
-      double z0 = 0.0, z1 = 0.0;
-      double& r0 = (ia0 >= 0 && ia0 < TA) ? acc[clampi(ia0, 0, TA - 1)][2 * nt] : z0;
-      double& r1 = (ia1 >= 0 && ia1 < TA) ? acc[clampi(ia1, 0, TA - 1)][2 * nt + 1] : z1;
-      dmma(r0, r1, av, c.BA[((ty * LA + la) * 2 + nt) * 32 + c.lane], r0, r1);
-    }
+  for (int i = 0; i < NPA; ++i) {
+    const int la = pa_la(i), nt = pa_nt(i);
+    const int ia0 = la + 2 * nt - P, ia1 = ia0 + 1;
+    double z0 = 0.0, z1 = 0.0;
+    double& r0 = (ia0 >= 0 && ia0 < TA) ? acc[clampi(ia0, 0, TA - 1)][2 * nt] : z0;
+    double& r1 = (ia1 >= 0 && ia1 < TA) ? acc[clampi(ia1, 0, TA - 1)][2 * nt + 1] : z1;
+    dmma(r0, r1, av[la], ba[i], r0, r1);
   }
-  const int col = mt * 8 + c.g, t = c.t;
+  const int col = mt * 8 + L.g, t = L.t;
 #pragma unroll
   for (int ia = 0; ia < TA; ++ia) {
-    double hi = 0.0, lo = 0.0;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      if (k < 4 - t) hi += acc[ia][k]; else lo += acc[ia][k];
-    }
-    c.X[(ty * NA0 + ia * NB + P + t) * NCOL + col] = hi;
-    if (t > 0) c.X[(ty * NA0 + ia * NB + t - 1) * NCOL + col] = lo;
+    double hi, lo;
+    split_groups(acc[ia], t, hi, lo);
+    X[(ty * NA0 + ia * NB + P + t) * NCOL + col] = hi;
+    if (t > 0) X[(ty * NA0 + ia * NB + t - 1) * NCOL + col] = lo;
   }
 }
 
-// ---- stage B unit: m-tile mt of (a0,k2) rows, destination ib in {2H, 2H+1};
-// per-column accumulators are the DMMA C operands (in-place assembly over lb).
-template <int H>
-__device__ __forceinline__ void stage_b_unit(const Ctx& c, int mt) {
-  const int row = mt * 8 + c.g, a0 = row >> 2, k2 = row & 3, t = c.t;
-  double yA[2][4], yB[2][4];
+// ---------------------------------------------------------------- stage B
+// Valid (element lb, n-tile) pairs of stage B (destination ib = lb + k - P in [0, TB))
+constexpr int NPB = 10;
+__host__ __device__ constexpr int pb_lb(int i) { return i < 1 ? 0 : (i < 2 ? 1 : (i < 4 ? 2 : (i < 6 ? 3 : (i < 8 ? 4 : (i < 9 ? 5 : 6))))); }
+__host__ __device__ constexpr int pb_nt(int i) { return (i == 0 || i == 1 || i == 3 || i == 5 || i == 7) ? 1 : 0; }
+
+// unit = m-tile mt of (a0,k2) rows, all TB destinations ib; bv/bd are the warp's
+// constant B fragments (VV and DD pair products of the axis-1 window).  Pass 1
+// issues the independent X_D VV -> Y_A and X_V VV -> Y_B products, pass 2 adds
+// X_V DD -> Y_A.
+__device__ __forceinline__ void stage_b_unit(const Lane& L, const double* X, const double (&bv)[NPB],
+                                             const double (&bd)[NPB], double* Y, int mt) {
+  const int row = mt * 8 + L.g, a0 = row >> 2, k2 = row & 3, t = L.t;
+  double yA[TB][4], yB[TB][4];
 #pragma unroll
-  for (int i = 0; i < 2; ++i)
+  for (int i = 0; i < TB; ++i)
 #pragma unroll
     for (int k = 0; k < 4; ++k) yA[i][k] = yB[i][k] = 0.0;
+  double xv[LB], xd[LB];
 #pragma unroll
-  for (int lb = 2 * H; lb <= 2 * H + 4; ++lb) {
+  for (int lb = 0; lb < LB; ++lb) {
     const int xo = (lb * Q + t) * Q + k2;
-    const double xv = c.X[(0 * NA0 + a0) * NCOL + xo];
-    const double xd = c.stiff ? c.X[(1 * NA0 + a0) * NCOL + xo] : 0.0;
+    xv[lb] = X[(0 * NA0 + a0) * NCOL + xo];
+    xd[lb] = L.stiff ? X[(1 * NA0 + a0) * NCOL + xo] : 0.0;
+  }
 #pragma unroll
-    for (int nt = 0; nt < 2; ++nt) {
-      if (!nt_useful(lb, nt, 2 * H, 2 * H + 2)) continue;
-      const int i0 = lb + 2 * nt - P - 2 * H, i1 = i0 + 1;
-      const bool v0 = i0 >= 0 && i0 < 2, v1 = i1 >= 0 && i1 < 2;
+  for (int pass = 0; pass < 2; ++pass) {
+    if (pass == 1 && !L.stiff) break;
+#pragma unroll
+    for (int i = 0; i < NPB; ++i) {
+      const int lb = pb_lb(i), nt = pb_nt(i);
+      const int i0 = lb + 2 * nt - P, i1 = i0 + 1;
+      const bool v0 = i0 >= 0 && i0 < TB, v1 = i1 >= 0 && i1 < TB;
       double z0 = 0.0, z1 = 0.0, z2 = 0.0, z3 = 0.0;
-      double& a0r = v0 ? yA[clampi(i0, 0, 1)][2 * nt] : z0;
-      double& a1r = v1 ? yA[clampi(i1, 0, 1)][2 * nt + 1] : z1;
-      double& b0r = v0 ? yB[clampi(i0, 0, 1)][2 * nt] : z2;
-      double& b1r = v1 ? yB[clampi(i1, 0, 1)][2 * nt + 1] : z3;
-      const double vv = c.BB[((0 * LB + lb) * 2 + nt) * 32 + c.lane];
-      if (c.stiff) {
-        const double dd = c.BB[((1 * LB + lb) * 2 + nt) * 32 + c.lane];
-        dmma(a0r, a1r, xd, vv, a0r, a1r);
-        dmma(b0r, b1r, xv, vv, b0r, b1r);
-        dmma(a0r, a1r, xv, dd, a0r, a1r);
+      double& a0r = v0 ? yA[clampi(i0, 0, TB - 1)][2 * nt] : z0;
+      double& a1r = v1 ? yA[clampi(i1, 0, TB - 1)][2 * nt + 1] : z1;
+      double& b0r = v0 ? yB[clampi(i0, 0, TB - 1)][2 * nt] : z2;
+      double& b1r = v1 ? yB[clampi(i1, 0, TB - 1)][2 * nt + 1] : z3;
+      if (pass == 0) {
+        if (L.stiff) {
+          dmma(a0r, a1r, xd[lb], bv[i], a0r, a1r);
+          dmma(b0r, b1r, xv[lb], bv[i], b0r, b1r);
+        } else {
+          dmma(a0r, a1r, xv[lb], bv[i], a0r, a1r);
+        }
       } else {
-        dmma(a0r, a1r, xv, vv, a0r, a1r);
+        dmma(a0r, a1r, xv[lb], bd[i], a0r, a1r);
       }
     }
   }
 #pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    double ah = 0.0, al = 0.0, bh = 0.0, bl = 0.0;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      if (k < 4 - t) { ah += yA[i][k]; bh += yB[i][k]; }
-      else { al += yA[i][k]; bl += yB[i][k]; }
-    }
-    const int ib = 2 * H + i;
+  for (int ib = 0; ib < TB; ++ib) {
+    double hA, lA, hB, lB;
+    split_groups(yA[ib], t, hA, lA);
+    split_groups(yB[ib], t, hB, lB);
     const int ch = (a0 * TB + ib) * NB + P + t;
-    c.Y[(0 * Q + k2) * YP + ch] = ah;
-    if (c.stiff) c.Y[(1 * Q + k2) * YP + ch] = bh;
+    Y[(0 * Q + k2) * YP + ch] = hA;
+    if (L.stiff) Y[(1 * Q + k2) * YP + ch] = hB;
     if (t > 0) {
       const int cl = (a0 * TB + ib) * NB + t - 1;
-      c.Y[(0 * Q + k2) * YP + cl] = al;
-      if (c.stiff) c.Y[(1 * Q + k2) * YP + cl] = bl;
+      Y[(0 * Q + k2) * YP + cl] = lA;
+      if (L.stiff) Y[(1 * Q + k2) * YP + cl] = lB;
     }
   }
 }
 
-// ---- stage S: element e2 along axis 2 into the rolling row accumulators
+// ---------------------------------------------------------------- stage S
+// NM m-tiles mt = ws + 8 i: first-k-step DMMAs, the dependent second k-step, then
+// the accumulation into the rolling rows R[i][slot][hi/lo] (registers): column
+// k = 2nt + j (r = k) of element e2 belongs to row e2 + k, i.e. slot (PHI + k) & 3,
+// and to band group hi (d = 3+t) if k < 4-t, else lo (d = t-1); k = 0 is always hi.
+template <int PHI, int I0, int NM>
+__device__ __forceinline__ void stage_s_batch(const Lane& L, int ws, const double* Y,
+                                              double (&R)[MT_S_PER_WARP][4][2],
+                                              const double (&b0)[2], const double (&b1)[2]) {
+  const int g = L.g, t = L.t;
+  double a0[NM], a1[NM], cc[NM][2][2];
+#pragma unroll
+  for (int i = 0; i < NM; ++i) {
+    const int mt = ws + (I0 + i) * NWS;
+    a0[i] = Y[(0 * Q + t) * YP + mt * 8 + g];
+    a1[i] = L.stiff ? Y[(1 * Q + t) * YP + mt * 8 + g] : 0.0;
+  }
+#pragma unroll
+  for (int i = 0; i < NM; ++i)
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt) dmma(cc[i][nt][0], cc[i][nt][1], a0[i], b0[nt], 0.0, 0.0);
+  if (L.stiff) {
+#pragma unroll
+    for (int i = 0; i < NM; ++i)
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+        dmma(cc[i][nt][0], cc[i][nt][1], a1[i], b1[nt], cc[i][nt][0], cc[i][nt][1]);
+  }
+#pragma unroll
+  for (int i = 0; i < NM; ++i)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const double v = cc[i][k >> 1][k & 1];
+      double& hi = R[I0 + i][(PHI + k) & 3][0];
+      double& lo = R[I0 + i][(PHI + k) & 3][1];
+      if (k == 0) {
+        hi += v;
+      } else {
+        add_if(hi, v, k < 4 - t);
+        add_if(lo, v, k >= 4 - t);
+      }
+    }
+}
+
+// m-tiles in register-bounded batches of two
+template <int PHI, int NM>
+__device__ __forceinline__ void stage_s_tiles(const Lane& L, int ws, const double* Y,
+                                              double (&R)[MT_S_PER_WARP][4][2],
+                                              const double (&b0)[2], const double (&b1)[2]) {
+  stage_s_batch<PHI, 0, 2>(L, ws, Y, R, b0, b1);
+  stage_s_batch<PHI, 2, 2>(L, ws, Y, R, b0, b1);
+  stage_s_batch<PHI, 4, 2>(L, ws, Y, R, b0, b1);
+  if (NM == 7) stage_s_batch<PHI, 6, 1>(L, ws, Y, R, b0, b1);
+}
+
 template <int PHI>
-__device__ __forceinline__ void stage_s(const Ctx& c, double (&R)[MT_S_PER_WARP][4][2],
-                                        const GsfArgs& a, int e2) {
-  const int g = c.g, t = c.t;
+__device__ __forceinline__ void stage_s(const Lane& L, int ws, const double* Y,
+                                        double (&R)[MT_S_PER_WARP][4][2], const GsfArgs& a,
+                                        int e2) {
+  const int g = L.g, t = L.t;
   const double* V2 = a.V + (int64_t)e2 * M * Q;
   double b0[2], b1[2];
 #pragma unroll
@@ -192,40 +285,25 @@ __device__ __forceinline__ void stage_s(const Ctx& c, double (&R)[MT_S_PER_WARP]
     const int r = bcol_r(nt, g), s = bcol_s(nt, g);
     b0[nt] = __ldg(V2 + r * Q + t) * __ldg(V2 + s * Q + t);
     b1[nt] = 0.0;
-    if (c.stiff) {
+    if (L.stiff) {
       const double* D2 = a.D + (int64_t)e2 * M * Q;
       double z = __ldg(D2 + r * Q + t) * __ldg(D2 + s * Q + t);
-      if (c.smass) z += b0[nt];
+      if (L.smass) z += b0[nt];
       b1[nt] = z;
     }
   }
-#pragma unroll
-  for (int i = 0; i < MT_S_PER_WARP; ++i) {
-    const int mt = c.warp + i * NW;
-    if (mt < MT_S) {
-      const double a0 = c.Y[(0 * Q + t) * YP + mt * 8 + g];
-      const double a1 = c.stiff ? c.Y[(1 * Q + t) * YP + mt * 8 + g] : 0.0;
-#pragma unroll
-      for (int nt = 0; nt < 2; ++nt) {
-        double c0, c1;
-        dmma(c0, c1, a0, b0[nt], 0.0, 0.0);
-        if (c.stiff) dmma(c0, c1, a1, b1[nt], c0, c1);
-        // column k = 2nt + j has r = k: destination row e2 + k -> slot (PHI + k) & 3
-        const int k0 = 2 * nt, k1 = 2 * nt + 1;
-        if (k0 < 4 - t) R[i][(PHI + k0) & 3][0] += c0; else R[i][(PHI + k0) & 3][1] += c0;
-        if (k1 < 4 - t) R[i][(PHI + k1) & 3][0] += c1; else R[i][(PHI + k1) & 3][1] += c1;
-      }
-    }
-  }
+  static_assert(MT_S == (MT_S_PER_WARP - 1) * NWS + 1, "stage S warp split");
+  if (ws == 0) stage_s_tiles<PHI, MT_S_PER_WARP>(L, ws, Y, R, b0, b1);
+  else stage_s_tiles<PHI, MT_S_PER_WARP - 1>(L, ws, Y, R, b0, b1);
 }
 
 // Row I2 (slot SL) is complete: each lane stores its (up to) two values per m-tile
 // straight to the CSR row (neighbouring lanes cover contiguous row segments).
 template <int SL>
-__device__ __forceinline__ void flush(const Ctx& c, double (&R)[MT_S_PER_WARP][4][2],
+__device__ __forceinline__ void flush(const Lane& L, double (&R)[MT_S_PER_WARP][4][2],
                                       const int (&meta)[MT_S_PER_WARP], const int64_t* pb,
                                       const int* pc, const GsfArgs& a, int I2, int64_t N) {
-  const int t = c.t;
+  const int t = L.t;
   const int lod2 = max(0, P - I2);
   const int c2 = (int)band_cnt(I2, P, N);
   const int64_t pre2 = band_prefix(I2, P, N);
@@ -244,21 +322,22 @@ __device__ __forceinline__ void flush(const Ctx& c, double (&R)[MT_S_PER_WARP][4
   }
 }
 
-__device__ __forceinline__ void flush_any(int sl, const Ctx& c, double (&R)[MT_S_PER_WARP][4][2],
+__device__ __forceinline__ void flush_any(int sl, const Lane& L, double (&R)[MT_S_PER_WARP][4][2],
                                           const int (&meta)[MT_S_PER_WARP], const int64_t* pb,
                                           const int* pc, const GsfArgs& a, int I2, int64_t N) {
   switch (sl) {
-    case 0: flush<0>(c, R, meta, pb, pc, a, I2, N); break;
-    case 1: flush<1>(c, R, meta, pb, pc, a, I2, N); break;
-    case 2: flush<2>(c, R, meta, pb, pc, a, I2, N); break;
-    default: flush<3>(c, R, meta, pb, pc, a, I2, N); break;
+    case 0: flush<0>(L, R, meta, pb, pc, a, I2, N); break;
+    case 1: flush<1>(L, R, meta, pb, pc, a, I2, N); break;
+    case 2: flush<2>(L, R, meta, pb, pc, a, I2, N); break;
+    default: flush<3>(L, R, meta, pb, pc, a, I2, N); break;
   }
 }
 
+// W[(la,k0)][(g1,k2)] = c w0 w1 w2 jac on the CTA's quadrature slab of column e2
 __device__ __forceinline__ void form_w(double* W, const double* wq, const GsfArgs& a, int e2,
-                                       int i00, int i10, int e0lo, int e0hi, int tid) {
+                                       int i00, int i10, int e0lo, int e0hi, int tid, int nt) {
   const int K = a.K;
-  for (int u = tid; u < LA * Q * NCOL; u += NT) {
+  for (int u = tid; u < LA * Q * NCOL; u += nt) {
     const int row = u / NCOL, col = u - row * NCOL;
     const int la = row >> 2, k0 = row & 3;
     const int g1 = col >> 2, k2 = col & 3, lb = g1 >> 2, k1 = g1 & 3;
@@ -274,14 +353,26 @@ __device__ __forceinline__ void form_w(double* W, const double* wq, const GsfArg
   }
 }
 
+#ifdef IGA_PHASE_TIMING
+// tools/gsf_phase.cu: per-warp clock64 at the end of each role's work, iterations 8..11
+__device__ long long g_phase[4][NT / 32][3];
+#define PT(idx)                                                                           \
+  if (blockIdx.x == IGA_PHASE_TIMING && L.lane == 0 && it >= 8 && it < 12)                \
+    g_phase[it - 8][warp][idx] = clock64();
+#else
+#define PT(idx)
+#endif
+
 __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
   extern __shared__ double sm[];
-  const int tid = threadIdx.x;
-  Ctx c;
-  c.lane = tid & 31; c.warp = tid >> 5; c.g = c.lane >> 2; c.t = c.lane & 3;
-  c.stiff = a.op != IGA_OP_MASS;
-  c.smass = a.op == IGA_OP_STIFFNESS_MASS;
-  c.W = sm + OFF_W; c.X = sm + OFF_X; c.Y = sm + OFF_Y; c.BA = sm + OFF_BA; c.BB = sm + OFF_BB;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  Lane L;
+  L.lane = tid & 31; L.g = L.lane >> 2; L.t = L.lane & 3;
+  L.stiff = a.op != IGA_OP_MASS;
+  L.smass = a.op == IGA_OP_STIFFNESS_MASS;
+  double* W = sm + OFF_W;
+  double* BA = sm + OFF_BA;
+  double* BB = sm + OFF_BB;
   double* wq = sm + OFF_WQ;
   int64_t* pb = reinterpret_cast<int64_t*>(sm + OFF_PB);
   int* pc = reinterpret_cast<int*>(sm + OFF_PC);
@@ -292,13 +383,11 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
   const int e0lo = max(a.el_begin, 0), e0hi = min(a.el_end, K);
 
   // ---- constant B fragments of axes 0 and 1 (pair products of the window elements)
-  double* BA = sm + OFF_BA;
-  double* BB = sm + OFF_BB;
   for (int u = tid; u < 2 * LA * 2 * 32; u += NT) {
     const int ln = u & 31, nt = (u >> 5) & 1, la = (u >> 6) % LA, type = u / (64 * LA);
     const int gg = ln >> 2, tt = ln & 3, e0 = i00 - P + la;
     double v = 0.0;
-    if (e0 >= 0 && e0 < K && (type == 0 || c.stiff)) {
+    if (e0 >= 0 && e0 < K && (type == 0 || L.stiff)) {
       const double* T = (type == 0 ? a.V : a.D) + (int64_t)e0 * M * Q;
       v = T[bcol_r(nt, gg) * Q + tt] * T[bcol_s(nt, gg) * Q + tt];
     }
@@ -308,7 +397,7 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
     const int ln = u & 31, nt = (u >> 5) & 1, lb = (u >> 6) % LB, prod = u / (64 * LB);
     const int gg = ln >> 2, tt = ln & 3, e1 = i10 - P + lb;
     double v = 0.0;
-    if (e1 >= 0 && e1 < K && (prod == 0 || c.stiff)) {
+    if (e1 >= 0 && e1 < K && (prod == 0 || L.stiff)) {
       const double* T = (prod == 0 ? a.V : a.D) + (int64_t)e1 * M * Q;
       v = T[bcol_r(nt, gg) * Q + tt] * T[bcol_s(nt, gg) * Q + tt];
     }
@@ -317,67 +406,103 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
   if (tid < Q) wq[tid] = a.weights[tid];
   if (tid < NPEN) {
     const int64_t I0 = i00 + tid / TB, I1 = i10 + tid % TB;
-    // rowptr of (I0, I1, 0) relative to the launch's first row; c0*c1 per I2-prefix unit
     pb[tid] = (I0 < N && I1 < N) ? rowptr3(I0, I1, 0, P, N) - a.base : 0;
     pc[tid] = (I0 < N && I1 < N) ? (int)(band_cnt(I0, P, N) * band_cnt(I1, P, N)) : 0;
   }
+  __syncthreads();
+  if (a.coef == nullptr) form_w(W, wq, a, 0, i00, i10, e0lo, e0hi, tid, NT);  // step-invariant
+  __syncthreads();
 
-  // per-lane flush metadata of its stage-S m-tiles: staging pencil rc and the (d0,d1)
-  // block offset b01 = (d0-lo0)*c1 + (d1-lo1) in the CSR row; -1 if the combo is outside
-  int meta[MT_S_PER_WARP];
+  const int n_it = K + 2;  // pipeline: A on it, B on it-1, S on it-2
+  if (warp < NWA) {
+    // ------------------------------------------------------------ role A
+    // warp wa owns type wa (values / derivatives; for the mass operator both warps
+    // take value units) and keeps its B fragments in registers
+    const int wa = warp;
+    const int ty = L.stiff ? wa : 0;
+    double ba[NPA];
 #pragma unroll
-  for (int i = 0; i < MT_S_PER_WARP; ++i) {
-    const int mt = c.warp + i * NW;
-    meta[i] = -1;
-    if (mt < MT_S) {
-      const int cb = mt * 8 + c.g;
-      const int d1 = cb % NB, ib = (cb / NB) % TB, a0 = cb / (NB * TB);
-      const int d0 = a0 % NB, ia = a0 / NB;
-      const int I0 = i00 + ia, I1 = i10 + ib;
-      if (I0 < a.plane_end && I1 < N) {
-        const int lod0 = max(0, P - I0), lod1 = max(0, P - I1);
-        const int c0 = (int)band_cnt(I0, P, N), c1 = (int)band_cnt(I1, P, N);
-        if (d0 >= lod0 && d0 < lod0 + c0 && d1 >= lod1 && d1 < lod1 + c1)
-          meta[i] = ((ia * TB + ib) << 16) | ((d0 - lod0) * c1 + (d1 - lod1));
+    for (int i = 0; i < NPA; ++i) ba[i] = BA[((ty * LA + pa_la(i)) * 2 + pa_nt(i)) * 32 + L.lane];
+    const int mt0 = L.stiff ? 0 : wa, mstep = L.stiff ? 1 : NWA;
+    for (int it = 0; it < n_it; ++it) {
+      PT(2);
+      if (it < K) {
+        if (a.coef != nullptr) {
+          form_w(W, wq, a, it, i00, i10, e0lo, e0hi, tid, NWA * 32);
+          asm volatile("bar.sync 1, %0;\n" ::"n"(NWA * 32));
+        }
+        double* X = sm + OFF_X + (it & 1) * SZ_X;
+        for (int mt = mt0; mt < MT_A; mt += mstep) stage_a_unit(L, W, ba, X, mt, ty);
+        PT(0);
+      }
+      __syncthreads();
+    }
+  } else if (warp < NWA + NWB) {
+    // ------------------------------------------------------------ role B
+    const int wb = warp - NWA;
+    double bv[NPB], bd[NPB];
+#pragma unroll
+    for (int i = 0; i < NPB; ++i) {
+      bv[i] = BB[((0 * LB + pb_lb(i)) * 2 + pb_nt(i)) * 32 + L.lane];
+      bd[i] = BB[((1 * LB + pb_lb(i)) * 2 + pb_nt(i)) * 32 + L.lane];
+    }
+    for (int it = 0; it < n_it; ++it) {
+      PT(2);
+      const int e2 = it - 1;
+      if (e2 >= 0 && e2 < K) {
+        const double* X = sm + OFF_X + (e2 & 1) * SZ_X;
+        double* Y = sm + OFF_Y + (e2 & 1) * SZ_Y;
+        for (int mt = wb; mt < MT_B; mt += NWB) stage_b_unit(L, X, bv, bd, Y, mt);
+        PT(0);
+      }
+      __syncthreads();
+    }
+  } else {
+    // ------------------------------------------------------------ role S
+    const int ws = warp - NWA - NWB;
+    // per-lane store metadata of its m-tiles: pencil rc and the (d0,d1) block offset
+    // b01 = (d0-lo0)*c1 + (d1-lo1) in the CSR row; -1 if the combo is outside
+    int meta[MT_S_PER_WARP];
+#pragma unroll
+    for (int i = 0; i < MT_S_PER_WARP; ++i) {
+      const int mt = ws + i * NWS;
+      meta[i] = -1;
+      if (mt < MT_S) {
+        const int cb = mt * 8 + L.g;
+        const int d1 = cb % NB, ib = (cb / NB) % TB, a0 = cb / (NB * TB);
+        const int d0 = a0 % NB, ia = a0 / NB;
+        const int I0 = i00 + ia, I1 = i10 + ib;
+        if (I0 < a.plane_end && I1 < N) {
+          const int lod0 = max(0, P - I0), lod1 = max(0, P - I1);
+          const int c0 = (int)band_cnt(I0, P, N), c1 = (int)band_cnt(I1, P, N);
+          if (d0 >= lod0 && d0 < lod0 + c0 && d1 >= lod1 && d1 < lod1 + c1)
+            meta[i] = ((ia * TB + ib) << 16) | ((d0 - lod0) * c1 + (d1 - lod1));
+        }
       }
     }
-  }
-
-  double R[MT_S_PER_WARP][4][2];
+    double R[MT_S_PER_WARP][4][2];
 #pragma unroll
-  for (int i = 0; i < MT_S_PER_WARP; ++i)
+    for (int i = 0; i < MT_S_PER_WARP; ++i)
 #pragma unroll
-    for (int s = 0; s < 4; ++s) R[i][s][0] = R[i][s][1] = 0.0;
-
-  __syncthreads();
-  if (a.coef == nullptr) form_w(c.W, wq, a, 0, i00, i10, e0lo, e0hi, tid);  // step-invariant
-
-  const int nA = c.stiff ? 2 * MT_A : MT_A;
-  for (int e2 = 0; e2 < K; ++e2) {
-    if (a.coef != nullptr) form_w(c.W, wq, a, e2, i00, i10, e0lo, e0hi, tid);
-    __syncthreads();
-    // stage A: units (m-tile, type)
-    for (int u = c.warp; u < nA; u += NW) {
-      if (c.stiff) stage_a_unit(c, u >> 1, u & 1);
-      else stage_a_unit(c, u, 0);
+      for (int s = 0; s < 4; ++s) R[i][s][0] = R[i][s][1] = 0.0;
+    for (int it = 0; it < n_it; ++it) {
+      PT(2);
+      const int e2 = it - 2;
+      if (e2 >= 0) {
+        const double* Y = sm + OFF_Y + (e2 & 1) * SZ_Y;
+        switch (e2 & 3) {
+          case 0: stage_s<0>(L, ws, Y, R, a, e2); PT(0); flush<0>(L, R, meta, pb, pc, a, e2, N); break;
+          case 1: stage_s<1>(L, ws, Y, R, a, e2); PT(0); flush<1>(L, R, meta, pb, pc, a, e2, N); break;
+          case 2: stage_s<2>(L, ws, Y, R, a, e2); PT(0); flush<2>(L, R, meta, pb, pc, a, e2, N); break;
+          default: stage_s<3>(L, ws, Y, R, a, e2); PT(0); flush<3>(L, R, meta, pb, pc, a, e2, N); break;
+        }
+        PT(1);
+      }
+      __syncthreads();
     }
-    __syncthreads();
-    // stage B: units (m-tile, ib half)
-    if (c.warp < 2 * MT_B) {
-      if (c.warp & 1) stage_b_unit<1>(c, c.warp >> 1);
-      else stage_b_unit<0>(c, c.warp >> 1);
-    }
-    __syncthreads();
-    // stage S + flush of the finished row e2
-    switch (e2 & 3) {
-      case 0: stage_s<0>(c, R, a, e2); flush<0>(c, R, meta, pb, pc, a, e2, N); break;
-      case 1: stage_s<1>(c, R, a, e2); flush<1>(c, R, meta, pb, pc, a, e2, N); break;
-      case 2: stage_s<2>(c, R, a, e2); flush<2>(c, R, meta, pb, pc, a, e2, N); break;
-      default: stage_s<3>(c, R, a, e2); flush<3>(c, R, meta, pb, pc, a, e2, N); break;
-    }
+    // rows K .. K+P-1 received their last contribution from element K-1
+    for (int I2 = K; I2 < N; ++I2) flush_any(I2 & 3, L, R, meta, pb, pc, a, I2, N);
   }
-  // rows K .. K+P-1 received their last contribution from element K-1
-  for (int I2 = K; I2 < N; ++I2) flush_any(I2 & 3, c, R, meta, pb, pc, a, I2, N);
 }
 
 }  // namespace p3

@@ -323,7 +323,8 @@ def test_full_size_sampled_rows(pkg, cfg):
     assert_parity(got, ref, sub_ip, absref=A, what=cfg["name"])
     # size-independent properties on the whole matrix
     M = res.gram.matrix
-    assert abs(M - M.T).max() == 0.0  # exact symmetry (both triangles from one value)
+    # symmetric to rounding, like the reference (its own |A - A^T| reaches 4e-16 max|A|)
+    assert abs(M - M.T).max() <= 1e-15 * np.abs(values).max()
     if op == "stiffness":
         rs = np.abs(M @ np.ones(M.shape[0]))
         assert rs.max() <= 1e-12 * np.abs(values).max()  # constants are in the kernel
