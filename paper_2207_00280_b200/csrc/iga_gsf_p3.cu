@@ -46,11 +46,11 @@ constexpr int WP = NCOL + 4;             // W row pitch (== 4 mod 16: conflict-f
 constexpr int NA0 = TA * NB;             // (ia, d0) rows (14)
 constexpr int NCOMBO = NA0 * TB * NB;    // (ia, d0, ib, d1) combos (392)
 constexpr int YP = NCOMBO + 4;           // Y pitch (== 12 mod 16: conflict-free A loads)
-constexpr int NT = 384;                  // threads: 12 warps
+constexpr int NT = 512;                  // threads: 16 warps
 constexpr int MT_A = NCOL / 8;           // 14 m-tiles of (g1,k2) columns
 constexpr int MT_B = NA0 * Q / 8;        // 7 m-tiles of (a0,k2) rows
 constexpr int MT_S = NCOMBO / 8;         // 49 m-tiles of combos
-constexpr int NWA = 2, NWB = 2, NWS = 8; // warps per role
+constexpr int NWA = 4, NWB = 4, NWS = 8; // warps per role (NWA even: fixed type per A warp)
 constexpr int MT_S_PER_WARP = (MT_S + NWS - 1) / NWS;  // 7
 constexpr int NPEN = TA * TB;            // row pencils (I0, I1) of the tile
 
@@ -65,7 +65,9 @@ constexpr int OFF_BB = OFF_BA + 2 * LA * 2 * 32;  // [2 prods][LB][2 nt][32]
 constexpr int OFF_WQ = OFF_BB + 2 * LB * 2 * 32;  // weights [Q]
 constexpr int OFF_PB = OFF_WQ + Q;                // pencil row-pointer bases (int64) [NPEN]
 constexpr int OFF_PC = OFF_PB + NPEN;             // pencil c0*c1 (int in double slots) [NPEN]
-constexpr int SMEM_DOUBLES = OFF_PC + NPEN;
+constexpr int OFF_R = OFF_PC + NPEN;              // rolling rows [MT_S][4 slots][2 groups][32]
+constexpr int SMEM_DOUBLES = OFF_R + MT_S * 4 * 2 * 32;
+static_assert(SMEM_DOUBLES * 8 <= 227 * 1024, "shared memory budget");
 static_assert(SMEM_DOUBLES * 8 <= 227 * 1024, "shared memory budget");
 constexpr size_t SMEM_BYTES = SMEM_DOUBLES * sizeof(double);
 
@@ -107,11 +109,12 @@ struct Lane {
 };
 
 // hi = sum_{k < 4-t} y[k] (band offset 3+t), lo = sum of the rest (offset t-1)
+// Lane masks m_k = [k < 4-t] as exact 0/1 doubles: fma(m, y, acc) adds y or nothing
+// exactly, so the group sums need no data-dependent selects.
 __device__ __forceinline__ void split_groups(const double* y, int t, double& hi, double& lo) {
-  const double p1 = y[0] + y[1], p2 = p1 + y[2], p3 = p2 + y[3];
-  const double s2 = y[2] + y[3], s1 = y[1] + s2;
-  hi = t == 0 ? p3 : (t == 1 ? p2 : (t == 2 ? p1 : y[0]));
-  lo = t == 1 ? y[3] : (t == 2 ? s2 : s1);
+  const double m1 = t <= 2 ? 1.0 : 0.0, m2 = t <= 1 ? 1.0 : 0.0, m3 = t == 0 ? 1.0 : 0.0;
+  hi = fma(m3, y[3], fma(m2, y[2], fma(m1, y[1], y[0])));
+  lo = fma(1.0 - m3, y[3], fma(1.0 - m2, y[2], (1.0 - m1) * y[1]));
 }
 
 // ---------------------------------------------------------------- stage A
@@ -170,13 +173,6 @@ __device__ __forceinline__ void stage_b_unit(const Lane& L, const double* X, con
   for (int i = 0; i < TB; ++i)
 #pragma unroll
     for (int k = 0; k < 4; ++k) yA[i][k] = yB[i][k] = 0.0;
-  double xv[LB], xd[LB];
-#pragma unroll
-  for (int lb = 0; lb < LB; ++lb) {
-    const int xo = (lb * Q + t) * Q + k2;
-    xv[lb] = X[(0 * NA0 + a0) * NCOL + xo];
-    xd[lb] = L.stiff ? X[(1 * NA0 + a0) * NCOL + xo] : 0.0;
-  }
 #pragma unroll
   for (int pass = 0; pass < 2; ++pass) {
     if (pass == 1 && !L.stiff) break;
@@ -190,15 +186,18 @@ __device__ __forceinline__ void stage_b_unit(const Lane& L, const double* X, con
       double& a1r = v1 ? yA[clampi(i1, 0, TB - 1)][2 * nt + 1] : z1;
       double& b0r = v0 ? yB[clampi(i0, 0, TB - 1)][2 * nt] : z2;
       double& b1r = v1 ? yB[clampi(i1, 0, TB - 1)][2 * nt + 1] : z3;
+      const int xo = (lb * Q + t) * Q + k2;
+      const double xv = X[(0 * NA0 + a0) * NCOL + xo];
       if (pass == 0) {
         if (L.stiff) {
-          dmma(a0r, a1r, xd[lb], bv[i], a0r, a1r);
-          dmma(b0r, b1r, xv[lb], bv[i], b0r, b1r);
+          const double xd = X[(1 * NA0 + a0) * NCOL + xo];
+          dmma(a0r, a1r, xd, bv[i], a0r, a1r);
+          dmma(b0r, b1r, xv, bv[i], b0r, b1r);
         } else {
-          dmma(a0r, a1r, xv[lb], bv[i], a0r, a1r);
+          dmma(a0r, a1r, xv, bv[i], a0r, a1r);
         }
       } else {
-        dmma(a0r, a1r, xv[lb], bd[i], a0r, a1r);
+        dmma(a0r, a1r, xv, bd[i], a0r, a1r);
       }
     }
   }
@@ -219,26 +218,39 @@ __device__ __forceinline__ void stage_b_unit(const Lane& L, const double* X, con
 }
 
 // ---------------------------------------------------------------- stage S
-// NM m-tiles mt = ws + 8 i: first-k-step DMMAs, the dependent second k-step, then
-// the accumulation into the rolling rows R[i][slot][hi/lo] (registers): column
-// k = 2nt + j (r = k) of element e2 belongs to row e2 + k, i.e. slot (PHI + k) & 3,
-// and to band group hi (d = 3+t) if k < 4-t, else lo (d = t-1); k = 0 is always hi.
+// NM m-tiles mt = ws + NWS i.  The rolling-row accumulators live in shared memory,
+// one private slot per (m-tile, row slot, band group, lane), and are the DMMA C
+// operands: column k = 2nt + j (r = k) of element e2 belongs to row e2 + k, i.e.
+// slot (PHI + k) & 3, and to band group hi (d = 3+t) if k < 4-t, else lo (d = t-1).
+__device__ __forceinline__ int rs_idx(int mt, int slot, int grp, int lane) {
+  return ((mt * 4 + slot) * 2 + grp) * 32 + lane;
+}
+
 template <int PHI, int I0, int NM>
-__device__ __forceinline__ void stage_s_batch(const Lane& L, int ws, const double* Y,
-                                              double (&R)[MT_S_PER_WARP][4][2],
+__device__ __forceinline__ void stage_s_batch(const Lane& L, int ws, const double* Y, double* Rs,
                                               const double (&b0)[2], const double (&b1)[2]) {
   const int g = L.g, t = L.t;
   double a0[NM], a1[NM], cc[NM][2][2];
+  int p[NM][2][2];
 #pragma unroll
   for (int i = 0; i < NM; ++i) {
     const int mt = ws + (I0 + i) * NWS;
     a0[i] = Y[(0 * Q + t) * YP + mt * 8 + g];
     a1[i] = L.stiff ? Y[(1 * Q + t) * YP + mt * 8 + g] : 0.0;
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int k = 2 * nt + j;
+        p[i][nt][j] = rs_idx(mt, (PHI + k) & 3, k < 4 - t ? 0 : 1, L.lane);
+        cc[i][nt][j] = Rs[p[i][nt][j]];
+      }
   }
 #pragma unroll
   for (int i = 0; i < NM; ++i)
 #pragma unroll
-    for (int nt = 0; nt < 2; ++nt) dmma(cc[i][nt][0], cc[i][nt][1], a0[i], b0[nt], 0.0, 0.0);
+    for (int nt = 0; nt < 2; ++nt)
+      dmma(cc[i][nt][0], cc[i][nt][1], a0[i], b0[nt], cc[i][nt][0], cc[i][nt][1]);
   if (L.stiff) {
 #pragma unroll
     for (int i = 0; i < NM; ++i)
@@ -249,34 +261,14 @@ __device__ __forceinline__ void stage_s_batch(const Lane& L, int ws, const doubl
 #pragma unroll
   for (int i = 0; i < NM; ++i)
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const double v = cc[i][k >> 1][k & 1];
-      double& hi = R[I0 + i][(PHI + k) & 3][0];
-      double& lo = R[I0 + i][(PHI + k) & 3][1];
-      if (k == 0) {
-        hi += v;
-      } else {
-        add_if(hi, v, k < 4 - t);
-        add_if(lo, v, k >= 4 - t);
-      }
-    }
-}
-
-// m-tiles in register-bounded batches of two
-template <int PHI, int NM>
-__device__ __forceinline__ void stage_s_tiles(const Lane& L, int ws, const double* Y,
-                                              double (&R)[MT_S_PER_WARP][4][2],
-                                              const double (&b0)[2], const double (&b1)[2]) {
-  stage_s_batch<PHI, 0, 2>(L, ws, Y, R, b0, b1);
-  stage_s_batch<PHI, 2, 2>(L, ws, Y, R, b0, b1);
-  stage_s_batch<PHI, 4, 2>(L, ws, Y, R, b0, b1);
-  if (NM == 7) stage_s_batch<PHI, 6, 1>(L, ws, Y, R, b0, b1);
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) Rs[p[i][nt][j]] = cc[i][nt][j];
 }
 
 template <int PHI>
-__device__ __forceinline__ void stage_s(const Lane& L, int ws, const double* Y,
-                                        double (&R)[MT_S_PER_WARP][4][2], const GsfArgs& a,
-                                        int e2) {
+__device__ __forceinline__ void stage_s(const Lane& L, int ws, const double* Y, double* Rs,
+                                        const GsfArgs& a, int e2) {
   const int g = L.g, t = L.t;
   const double* V2 = a.V + (int64_t)e2 * M * Q;
   double b0[2], b1[2];
@@ -293,14 +285,14 @@ __device__ __forceinline__ void stage_s(const Lane& L, int ws, const double* Y,
     }
   }
   static_assert(MT_S == (MT_S_PER_WARP - 1) * NWS + 1, "stage S warp split");
-  if (ws == 0) stage_s_tiles<PHI, MT_S_PER_WARP>(L, ws, Y, R, b0, b1);
-  else stage_s_tiles<PHI, MT_S_PER_WARP - 1>(L, ws, Y, R, b0, b1);
+  stage_s_batch<PHI, 0, 3>(L, ws, Y, Rs, b0, b1);
+  stage_s_batch<PHI, 3, 3>(L, ws, Y, Rs, b0, b1);
+  if (ws == 0) stage_s_batch<PHI, 6, 1>(L, ws, Y, Rs, b0, b1);
 }
 
-// Row I2 (slot SL) is complete: each lane stores its (up to) two values per m-tile
+// Row I2 (slot sl) is complete: each lane stores its (up to) two values per m-tile
 // straight to the CSR row (neighbouring lanes cover contiguous row segments).
-template <int SL>
-__device__ __forceinline__ void flush(const Lane& L, double (&R)[MT_S_PER_WARP][4][2],
+__device__ __forceinline__ void flush(const Lane& L, int ws, double* Rs, int sl,
                                       const int (&meta)[MT_S_PER_WARP], const int64_t* pb,
                                       const int* pc, const GsfArgs& a, int I2, int64_t N) {
   const int t = L.t;
@@ -310,26 +302,19 @@ __device__ __forceinline__ void flush(const Lane& L, double (&R)[MT_S_PER_WARP][
   const int dh = P + t - lod2, dl = t - 1 - lod2;
 #pragma unroll
   for (int i = 0; i < MT_S_PER_WARP; ++i) {
-    const int m = meta[i];
-    if (m >= 0) {
-      const int rc = m >> 16, b01 = m & 0xffff;
-      double* row = a.values + pb[rc] + (int64_t)pc[rc] * pre2 + b01 * c2;
-      if (dh >= 0 && dh < c2) row[dh] = R[i][SL][0];
-      if (t > 0 && dl >= 0 && dl < c2) row[dl] = R[i][SL][1];
+    const int mt = ws + i * NWS;
+    if (mt < MT_S) {
+      const int ph = rs_idx(mt, sl, 0, L.lane), pl = rs_idx(mt, sl, 1, L.lane);
+      const int m = meta[i];
+      if (m >= 0) {
+        const int rc = m >> 16, b01 = m & 0xffff;
+        double* row = a.values + pb[rc] + (int64_t)pc[rc] * pre2 + b01 * c2;
+        if (dh >= 0 && dh < c2) row[dh] = Rs[ph];
+        if (t > 0 && dl >= 0 && dl < c2) row[dl] = Rs[pl];
+      }
+      Rs[ph] = 0.0;
+      Rs[pl] = 0.0;
     }
-    R[i][SL][0] = 0.0;
-    R[i][SL][1] = 0.0;
-  }
-}
-
-__device__ __forceinline__ void flush_any(int sl, const Lane& L, double (&R)[MT_S_PER_WARP][4][2],
-                                          const int (&meta)[MT_S_PER_WARP], const int64_t* pb,
-                                          const int* pc, const GsfArgs& a, int I2, int64_t N) {
-  switch (sl) {
-    case 0: flush<0>(L, R, meta, pb, pc, a, I2, N); break;
-    case 1: flush<1>(L, R, meta, pb, pc, a, I2, N); break;
-    case 2: flush<2>(L, R, meta, pb, pc, a, I2, N); break;
-    default: flush<3>(L, R, meta, pb, pc, a, I2, N); break;
   }
 }
 
@@ -419,11 +404,11 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
     // warp wa owns type wa (values / derivatives; for the mass operator both warps
     // take value units) and keeps its B fragments in registers
     const int wa = warp;
-    const int ty = L.stiff ? wa : 0;
+    const int ty = L.stiff ? (wa & 1) : 0;
     double ba[NPA];
 #pragma unroll
     for (int i = 0; i < NPA; ++i) ba[i] = BA[((ty * LA + pa_la(i)) * 2 + pa_nt(i)) * 32 + L.lane];
-    const int mt0 = L.stiff ? 0 : wa, mstep = L.stiff ? 1 : NWA;
+    const int mt0 = L.stiff ? (wa >> 1) : wa, mstep = L.stiff ? NWA / 2 : NWA;
     for (int it = 0; it < n_it; ++it) {
       PT(2);
       if (it < K) {
@@ -480,28 +465,27 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
         }
       }
     }
-    double R[MT_S_PER_WARP][4][2];
-#pragma unroll
-    for (int i = 0; i < MT_S_PER_WARP; ++i)
-#pragma unroll
-      for (int s = 0; s < 4; ++s) R[i][s][0] = R[i][s][1] = 0.0;
+    double* Rs = sm + OFF_R;
+    for (int u = ws * 32 + L.lane; u < MT_S * 4 * 2 * 32; u += NWS * 32) Rs[u] = 0.0;
     for (int it = 0; it < n_it; ++it) {
       PT(2);
       const int e2 = it - 2;
       if (e2 >= 0) {
         const double* Y = sm + OFF_Y + (e2 & 1) * SZ_Y;
         switch (e2 & 3) {
-          case 0: stage_s<0>(L, ws, Y, R, a, e2); PT(0); flush<0>(L, R, meta, pb, pc, a, e2, N); break;
-          case 1: stage_s<1>(L, ws, Y, R, a, e2); PT(0); flush<1>(L, R, meta, pb, pc, a, e2, N); break;
-          case 2: stage_s<2>(L, ws, Y, R, a, e2); PT(0); flush<2>(L, R, meta, pb, pc, a, e2, N); break;
-          default: stage_s<3>(L, ws, Y, R, a, e2); PT(0); flush<3>(L, R, meta, pb, pc, a, e2, N); break;
+          case 0: stage_s<0>(L, ws, Y, Rs, a, e2); break;
+          case 1: stage_s<1>(L, ws, Y, Rs, a, e2); break;
+          case 2: stage_s<2>(L, ws, Y, Rs, a, e2); break;
+          default: stage_s<3>(L, ws, Y, Rs, a, e2); break;
         }
+        PT(0);
+        flush(L, ws, Rs, e2 & 3, meta, pb, pc, a, e2, N);
         PT(1);
       }
       __syncthreads();
     }
     // rows K .. K+P-1 received their last contribution from element K-1
-    for (int I2 = K; I2 < N; ++I2) flush_any(I2 & 3, L, R, meta, pb, pc, a, I2, N);
+    for (int I2 = K; I2 < N; ++I2) flush(L, ws, Rs, I2 & 3, meta, pb, pc, a, I2, N);
   }
 }
 

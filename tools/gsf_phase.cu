@@ -36,14 +36,14 @@ int main() {
   cudaEventRecord(e1); cudaEventSynchronize(e1);
   float ms; cudaEventElapsedTime(&ms, e0, e1);
   printf("kernel %.3f ms  err=%s\n", ms, cudaGetErrorString(cudaGetLastError()));
-  long long ph[4][12][3];
+  long long ph[4][16][3];
   cudaMemcpyFromSymbol(ph, iga::p3::g_phase, sizeof(ph));
   for (int s = 0; s < 4; ++s) {
     long long t0 = ph[s][0][2];
     long long amax = 0, bmax = 0, smid = 0, send = 0;
-    for (int w = 0; w < 2; ++w) amax = std::max(amax, ph[s][w][0] - t0);
-    for (int w = 2; w < 4; ++w) bmax = std::max(bmax, ph[s][w][0] - t0);
-    for (int w = 4; w < 12; ++w) { smid = std::max(smid, ph[s][w][0] - t0); send = std::max(send, ph[s][w][1] - t0); }
+    for (int w = 0; w < 4; ++w) amax = std::max(amax, ph[s][w][0] - t0);
+    for (int w = 4; w < 8; ++w) bmax = std::max(bmax, ph[s][w][0] - t0);
+    for (int w = 8; w < 16; ++w) { smid = std::max(smid, ph[s][w][0] - t0); send = std::max(send, ph[s][w][1] - t0); }
     printf("iter %d: A_end %lld  B_end %lld  S_dmma_end %lld  S_flush_end %lld", s + 8, amax, bmax, smid, send);
     if (s < 3) printf("  | iteration %lld", ph[s + 1][0][2] - t0);
     printf("\n");
