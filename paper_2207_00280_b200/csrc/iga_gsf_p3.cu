@@ -123,35 +123,47 @@ constexpr int NPA = 6;
 __host__ __device__ constexpr int pa_la(int i) { return i < 1 ? 0 : (i < 2 ? 1 : (i < 4 ? 2 : (i < 5 ? 3 : 4))); }
 __host__ __device__ constexpr int pa_nt(int i) { return i == 0 ? 1 : (i == 1 ? 1 : (i == 2 ? 0 : (i == 3 ? 1 : 0))); }
 
-// unit = (m-tile mt of (g1,k2) columns) for the warp's type; ba[] are the warp's
-// constant B fragments; per-column accumulators acc[ia][k] are the DMMA C operands
-// (each receives exactly one element's product).
-__device__ __forceinline__ void stage_a_unit(const Lane& L, const double* W, const double (&ba)[NPA],
-                                             double* X, int mt, int ty) {
-  double acc[TA][4];
+// NU units = m-tiles mt0 + i*mstep of (g1,k2) columns for the warp's type, interleaved
+// for ILP; ba[] are the warp's constant B fragments; per-column accumulators
+// acc[u][ia][k] are the DMMA C operands (each receives exactly one element's product).
+template <int NU>
+__device__ __forceinline__ void stage_a_units(const Lane& L, const double* W, const double (&ba)[NPA],
+                                              double* X, int mt0, int mstep, int ty) {
+  double acc[NU][TA][4];
 #pragma unroll
-  for (int ia = 0; ia < TA; ++ia)
+  for (int u = 0; u < NU; ++u)
 #pragma unroll
-    for (int k = 0; k < 4; ++k) acc[ia][k] = 0.0;
-  double av[LA];
+    for (int ia = 0; ia < TA; ++ia)
 #pragma unroll
-  for (int la = 0; la < LA; ++la) av[la] = W[(la * Q + L.t) * WP + mt * 8 + L.g];
+      for (int k = 0; k < 4; ++k) acc[u][ia][k] = 0.0;
+  double av[NU][LA];
+#pragma unroll
+  for (int u = 0; u < NU; ++u)
+#pragma unroll
+    for (int la = 0; la < LA; ++la) av[u][la] = W[(la * Q + L.t) * WP + (mt0 + u * mstep) * 8 + L.g];
 #pragma unroll
   for (int i = 0; i < NPA; ++i) {
     const int la = pa_la(i), nt = pa_nt(i);
     const int ia0 = la + 2 * nt - P, ia1 = ia0 + 1;
-    double z0 = 0.0, z1 = 0.0;
-    double& r0 = (ia0 >= 0 && ia0 < TA) ? acc[clampi(ia0, 0, TA - 1)][2 * nt] : z0;
-    double& r1 = (ia1 >= 0 && ia1 < TA) ? acc[clampi(ia1, 0, TA - 1)][2 * nt + 1] : z1;
-    dmma(r0, r1, av[la], ba[i], r0, r1);
-  }
-  const int col = mt * 8 + L.g, t = L.t;
 #pragma unroll
-  for (int ia = 0; ia < TA; ++ia) {
-    double hi, lo;
-    split_groups(acc[ia], t, hi, lo);
-    X[(ty * NA0 + ia * NB + P + t) * NCOL + col] = hi;
-    if (t > 0) X[(ty * NA0 + ia * NB + t - 1) * NCOL + col] = lo;
+    for (int u = 0; u < NU; ++u) {
+      double z0 = 0.0, z1 = 0.0;
+      double& r0 = (ia0 >= 0 && ia0 < TA) ? acc[u][clampi(ia0, 0, TA - 1)][2 * nt] : z0;
+      double& r1 = (ia1 >= 0 && ia1 < TA) ? acc[u][clampi(ia1, 0, TA - 1)][2 * nt + 1] : z1;
+      dmma(r0, r1, av[u][la], ba[i], r0, r1);
+    }
+  }
+  const int t = L.t;
+#pragma unroll
+  for (int u = 0; u < NU; ++u) {
+    const int col = (mt0 + u * mstep) * 8 + L.g;
+#pragma unroll
+    for (int ia = 0; ia < TA; ++ia) {
+      double hi, lo;
+      split_groups(acc[u][ia], t, hi, lo);
+      X[(ty * NA0 + ia * NB + P + t) * NCOL + col] = hi;
+      if (t > 0) X[(ty * NA0 + ia * NB + t - 1) * NCOL + col] = lo;
+    }
   }
 }
 
@@ -417,7 +429,9 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
           asm volatile("bar.sync 1, %0;\n" ::"n"(NWA * 32));
         }
         double* X = sm + OFF_X + (it & 1) * SZ_X;
-        for (int mt = mt0; mt < MT_A; mt += mstep) stage_a_unit(L, W, ba, X, mt, ty);
+        int mt = mt0;
+        for (; mt + mstep < MT_A; mt += 2 * mstep) stage_a_units<2>(L, W, ba, X, mt, mstep, ty);
+        if (mt < MT_A) stage_a_units<1>(L, W, ba, X, mt, mstep, ty);
         PT(0);
       }
       __syncthreads();
