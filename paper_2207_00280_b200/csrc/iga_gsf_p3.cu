@@ -74,7 +74,14 @@ constexpr int OFF_BA = OFF_Y + 2 * SZ_Y;          // [2 types][LA][2 nt][32]
 constexpr int OFF_BB = OFF_BA + 2 * LA * 2 * 32;  // [2 prods][LB][2 nt][32]
 constexpr int OFF_WQ = OFF_BB + 2 * LB * 2 * 32;  // weights [Q]
 constexpr int OFF_R = OFF_WQ + Q;                 // rolling rows [MT_S][4 slots][2 groups][32]
-constexpr int SMEM_DOUBLES = OFF_R + MT_S * 4 * 2 * 32;
+constexpr int ROWU = NUP * NB;                    // upper part of an interior CSR row (175)
+constexpr int MSLOT = 2 * P + 1;                  // mirror target rows in flight (J2 mod 7)
+constexpr int OFF_OS = OFF_R + MT_S * 4 * 2 * 32; // own-row staging [NPEN][ROWU]
+constexpr int OFF_MS = OFF_OS + NPEN * ROWU;      // mirror staging [NCOMBO][MSLOT][NB]
+constexpr int OFF_PI = OFF_MS + NCOMBO * MSLOT * NB;  // pencil info: base, c01, bP  [NPEN][3]
+constexpr int OFF_SEG = OFF_PI + NPEN * 3;        // mirror segment starts [NCOMBO], own
+                                                  // row starts [NPEN], lengths [NPEN] (int)
+constexpr int SMEM_DOUBLES = OFF_SEG + NCOMBO + NPEN + NPEN / 2;
 static_assert(SMEM_DOUBLES * 8 <= 227 * 1024, "shared memory budget");
 constexpr size_t SMEM_BYTES = SMEM_DOUBLES * sizeof(double);
 
@@ -314,6 +321,8 @@ struct Target {
   int own_c01, mir_c01;        // c(0) * c(1) of the pencil
   int own_b01, mir_b01;        // (d0', d1') block offset inside the row (per unit c2)
   int d0, d1;                  // band offsets of the combo (own row)
+  int own_s, own_rel;          // own staging row start (pen * ROWU) and block rel. to bP
+  int mir_s;                   // mirror staging start (c * MSLOT * NB)
   bool own_ok, mir_ok, self;   // own row written / mirror row written / (d0,d1) == (3,3)
 };
 
@@ -332,11 +341,16 @@ __device__ __forceinline__ void make_target(Target& tg, int c, int i00, int i10,
   tg.mir_ok = inside && !tg.self && J0 >= a.own_begin && J0 < a.mirror_end;
   tg.own_base = tg.mir_base = 0;
   tg.own_c01 = tg.mir_c01 = tg.own_b01 = tg.mir_b01 = 0;
+  tg.own_s = pen * ROWU;
+  tg.mir_s = c * MSLOT * NB;
+  tg.own_rel = 0;
   if (tg.own_ok) {
     const int c1 = (int)band_cnt(I1, P, N);
+    const int lod0 = (int)max((int64_t)0, P - I0), lod1 = (int)max((int64_t)0, P - I1);
     tg.own_base = rowptr3(I0, I1, 0, P, N) - a.base;
     tg.own_c01 = (int)(band_cnt(I0, P, N) * c1);
-    tg.own_b01 = (d0 - (int)max((int64_t)0, P - I0)) * c1 + (d1 - (int)max((int64_t)0, P - I1));
+    tg.own_b01 = (d0 - lod0) * c1 + (d1 - lod1);
+    tg.own_rel = tg.own_b01 - ((P - lod0) * c1 + (P - lod1));
   }
   if (tg.mir_ok) {
     const int c1 = (int)band_cnt(J1, P, N);
@@ -347,27 +361,29 @@ __device__ __forceinline__ void make_target(Target& tg, int c, int i00, int i10,
   }
 }
 
-// Row I2 (slot sl) is complete: each lane stores its two values (band offsets
-// d2 = 3+t and t-1) per m-tile in the own row and, mirrored, in row J.
-__device__ __forceinline__ void flush(const Lane& L, int ws, double* Rs, int sl,
-                                      const Target (&tg)[MT_S_PER_WARP], const GsfArgs& a, int I2,
-                                      int64_t N) {
+// Row I2 (slot sl) is complete: each lane stages its two values (band offsets
+// d2 = 3+t and t-1) per m-tile in the own-row staging (upper part of row I2) and
+// in the mirror staging of target row J2 = I2 + d2 - 3 (slot J2 mod 7, position
+// 2P - d2), then clears the rolling slot.
+__device__ __forceinline__ void stage_rows(const Lane& L, int ws, double* Rs, int sl,
+                                           const Target (&tg)[MT_S_PER_WARP], double* OS,
+                                           double* MS, int I2, int64_t N) {
   const int t = L.t;
-  // own row I2: prefix, count and first band offset along axis 2
-  const int64_t pre_i = band_prefix(I2, P, N);
   const int c_i = (int)band_cnt(I2, P, N), lod_i = max(0, P - I2);
-  // mirror rows J2 = I2 + d2 - 3 for the lane's two band offsets
-  int64_t pre_j[2];
-  int c_j[2], lod_j[2], ok_j[2];
   const int d2v[2] = {P + t, t - 1};
+  // per band offset: validity of column J2 = I2 + d2 - 3, own position, mirror slot
+  bool okh[2];
+  int op[2], mp[2];
+  const int i2m = I2 % MSLOT;
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
-    const int64_t J2 = I2 + d2v[h] - P;
-    ok_j[h] = (h == 0 || t > 0) && J2 >= 0 && J2 < N;
-    const int64_t J2c = ok_j[h] ? J2 : 0;
-    pre_j[h] = band_prefix(J2c, P, N);
-    c_j[h] = (int)band_cnt(J2c, P, N);
-    lod_j[h] = (int)max((int64_t)0, P - J2c);
+    const int d2 = d2v[h];
+    const int J2 = I2 + d2 - P;
+    okh[h] = !(h == 1 && t == 0) && J2 >= 0 && J2 < N;
+    op[h] = d2 - lod_i;
+    int slot = i2m + d2 - P;
+    slot = slot < 0 ? slot + MSLOT : (slot >= MSLOT ? slot - MSLOT : slot);
+    mp[h] = slot * NB + (2 * P - d2);
   }
 #pragma unroll
   for (int i = 0; i < MT_S_PER_WARP; ++i) {
@@ -376,20 +392,69 @@ __device__ __forceinline__ void flush(const Lane& L, int ws, double* Rs, int sl,
       const int ph = rs_idx(mt, sl, 0, L.lane), pl = rs_idx(mt, sl, 1, L.lane);
       const double v[2] = {Rs[ph], Rs[pl]};
       const Target& g = tg[i];
+      const int ob = g.own_s + g.own_rel * c_i;
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        if (!ok_j[h]) continue;  // the column J2 is outside the matrix (or no lo value)
-        const int d2 = d2v[h];
-        if (g.own_ok) {
-          a.values[g.own_base + (int64_t)g.own_c01 * pre_i + g.own_b01 * c_i + (d2 - lod_i)] = v[h];
-        }
-        if (g.mir_ok) {
-          a.values[g.mir_base + (int64_t)g.mir_c01 * pre_j[h] + g.mir_b01 * c_j[h] +
-                   (2 * P - d2 - lod_j[h])] = v[h];
-        }
+        if (!okh[h]) continue;
+        if (g.own_ok) OS[ob + op[h]] = v[h];
+        if (g.mir_ok) MS[g.mir_s + mp[h]] = v[h];
       }
       Rs[ph] = 0.0;
       Rs[pl] = 0.0;
+    }
+  }
+}
+
+// Write-out bases of the rows finished at this step: own row I2 of every pencil
+// (OB[pen] = first upper position or -1, OL[pen] = upper length) and the mirror
+// segment of every combo in target row J2 = I2 - 3 (SEGB[c] or -1).  Computed by
+// the S lanes right after staging, read by the flat write loop after the barrier.
+__device__ __forceinline__ void write_bases(const Target (&tg)[MT_S_PER_WARP], const int64_t* PI,
+                                            int64_t* OB, int* OL, int64_t* SEGB, const GsfArgs& a,
+                                            int I2, int64_t N, int ws, const Lane& L, int stid) {
+  if (stid < NPEN) {
+    const int64_t c01 = PI[stid * 3 + 1];
+    const int64_t bP = PI[stid * 3 + 2];
+    const int64_t c2 = band_cnt(I2, P, N);
+    OB[stid] = c01 > 0 ? PI[stid * 3] + c01 * band_prefix(I2, P, N) + bP * c2 : -1;
+    OL[stid] = c01 > 0 ? (int)((c01 - bP) * c2) : 0;
+  }
+  const int J2 = I2 - P;
+  if (J2 >= 0 && L.t == 0) {
+    const int64_t pre = band_prefix(J2, P, N);
+    const int64_t c2 = band_cnt(J2, P, N);
+#pragma unroll
+    for (int i = 0; i < MT_S_PER_WARP; ++i) {
+      const int mt = ws + i * NWS;
+      if (mt < MT_S) {
+        const Target& g = tg[i];
+        SEGB[mt * 8 + L.g] = g.mir_ok ? g.mir_base + (int64_t)g.mir_c01 * pre + (int64_t)g.mir_b01 * c2 : -1;
+      }
+    }
+  }
+}
+
+// Flat write loop: the staged upper parts of the tile's rows I2 (own) and the
+// mirrored segments of target row J2 = I2 - 3; fully unrolled so every thread keeps
+// its loads and stores in flight together.
+__device__ __forceinline__ void write_rows(const double* OS, const double* MS, const int64_t* OB,
+                                           const int* OL, const int64_t* SEGB, const GsfArgs& a,
+                                           int I2, int64_t N, int stid) {
+  constexpr int NOWN = NPEN * ROWU, NMIR = NCOMBO * NB, NTS = NWS * 32;
+  const int J2 = I2 - P;
+  const int slot = J2 >= 0 ? J2 % MSLOT : 0;
+  const int c2 = J2 >= 0 ? (int)band_cnt(J2, P, N) : 0, lod = J2 >= 0 ? max(0, P - J2) : 0;
+#pragma unroll
+  for (int k = 0; k < (NOWN + NMIR + NTS - 1) / NTS; ++k) {
+    const int u = stid + k * NTS;
+    if (u < NOWN) {
+      const int pen = u / ROWU, v = u - pen * ROWU;
+      const int64_t ob = OB[pen];
+      if (ob >= 0 && v < OL[pen]) a.values[ob + v] = OS[u];
+    } else if (u < NOWN + NMIR && J2 >= 0) {
+      const int w = u - NOWN, c = w / NB, d = w - c * NB;
+      const int64_t sb = SEGB[c];
+      if (sb >= 0 && d < c2) a.values[sb + d] = MS[(c * MSLOT + slot) * NB + lod + d];
     }
   }
 }
@@ -416,7 +481,7 @@ __device__ __forceinline__ void form_w(double* W, const double* wq, const GsfArg
 
 #ifdef IGA_PHASE_TIMING
 // tools/gsf_phase.cu: per-warp clock64 of one CTA, iterations 8..11
-__device__ long long g_phase[4][NT / 32][3];
+__device__ long long g_phase[4][NT / 32][6];
 #define PT(idx)                                                                           \
   if (blockIdx.x == IGA_PHASE_TIMING && L.lane == 0 && it >= 8 && it < 12)                \
     g_phase[it - 8][warp][idx] = clock64();
@@ -463,6 +528,17 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
     BB[u] = v;
   }
   if (tid < Q) wq[tid] = a.weights[tid];
+  if (tid < NPEN) {
+    // own-row write-out info of pencil (I0, I1): row pointer of (I0, I1, 0), c0*c1
+    // (0 if the pencil's rows are not written by this launch) and the first upper block
+    int64_t* PIw = reinterpret_cast<int64_t*>(sm + OFF_PI);
+    const int64_t I0 = i00 + tid / TB, I1 = i10 + tid % TB;
+    const bool ok = I0 < N && I1 < N && I0 >= a.own_begin && I0 < a.plane_end;
+    const int64_t c1 = ok ? band_cnt(I1, P, N) : 0;
+    PIw[tid * 3 + 0] = ok ? rowptr3(I0, I1, 0, P, N) - a.base : 0;
+    PIw[tid * 3 + 1] = ok ? band_cnt(I0, P, N) * c1 : 0;
+    PIw[tid * 3 + 2] = ok ? (P - max((int64_t)0, P - I0)) * c1 + (P - max((int64_t)0, P - I1)) : 0;
+  }
   __syncthreads();
   if (a.coef == nullptr) form_w(W, wq, a, 0, i00, i10, e0lo, e0hi, tid, NT);  // step-invariant
   __syncthreads();
@@ -524,7 +600,25 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
       if (mt >= MT_S) tg[i].own_ok = tg[i].mir_ok = false;
     }
     double* Rs = sm + OFF_R;
-    for (int u = ws * 32 + L.lane; u < MT_S * 4 * 2 * 32; u += NWS * 32) Rs[u] = 0.0;
+    double* OS = sm + OFF_OS;
+    double* MS = sm + OFF_MS;
+    const int64_t* PI = reinterpret_cast<const int64_t*>(sm + OFF_PI);
+    int64_t* SEGB = reinterpret_cast<int64_t*>(sm + OFF_SEG);
+    const int stid = tid - (NWA + NWB) * 32, snt = NWS * 32;
+    for (int u = stid; u < MT_S * 4 * 2 * 32; u += snt) Rs[u] = 0.0;
+    int64_t* OB = SEGB + NCOMBO;
+    int* OL = reinterpret_cast<int*>(OB + NPEN);
+    auto finish_row = [&](int I2, int it) {
+      // row I2 is complete: stage it, then write it and the mirror row I2-3
+      asm volatile("bar.sync 2, %0;\n" ::"n"(NWS * 32));
+      PT(3);
+      stage_rows(L, ws, Rs, I2 & 3, tg, OS, MS, I2, N);
+      write_bases(tg, PI, OB, OL, SEGB, a, I2, N, ws, L, stid);
+      PT(4);
+      asm volatile("bar.sync 2, %0;\n" ::"n"(NWS * 32));
+      write_rows(OS, MS, OB, OL, SEGB, a, I2, N, stid);
+      PT(5);
+    };
     for (int it = 0; it < n_it; ++it) {
       PT(2);
       const int e2 = it - 2;
@@ -537,13 +631,32 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
           default: stage_s<3>(L, ws, Y, Rs, a, e2); break;
         }
         PT(0);
-        flush(L, ws, Rs, e2 & 3, tg, a, e2, N);
+        finish_row(e2, it);
         PT(1);
       }
       __syncthreads();
     }
-    // rows K .. K+P-1 received their last contribution from element K-1
-    for (int I2 = K; I2 < N; ++I2) flush(L, ws, Rs, I2 & 3, tg, a, I2, N);
+    // rows K .. K+P-1 received their last contribution from element K-1; then the
+    // last P mirror rows
+    for (int I2 = K; I2 < N; ++I2) finish_row(I2, 0);
+    // mirror rows N-3 .. N-1: flushed as "rows" N .. N+2 whose own parts are empty
+    for (int I2 = (int)N; I2 < N + P; ++I2) {
+      asm volatile("bar.sync 2, %0;\n" ::"n"(NWS * 32));
+      if (stid < NPEN) { OB[stid] = -1; OL[stid] = 0; }
+      const int J2 = I2 - P;
+      if (J2 >= 0 && L.t == 0) {
+        const int64_t pre = band_prefix(J2, P, N), c2 = band_cnt(J2, P, N);
+#pragma unroll
+        for (int i = 0; i < MT_S_PER_WARP; ++i) {
+          const int mt = ws + i * NWS;
+          if (mt < MT_S)
+            SEGB[mt * 8 + L.g] = tg[i].mir_ok ? tg[i].mir_base + (int64_t)tg[i].mir_c01 * pre +
+                                                    (int64_t)tg[i].mir_b01 * c2 : -1;
+        }
+      }
+      asm volatile("bar.sync 2, %0;\n" ::"n"(NWS * 32));
+      write_rows(OS, MS, OB, OL, SEGB, a, I2, N, stid);
+    }
   }
 }
 
