@@ -36,7 +36,7 @@ int main() {
   cudaEventRecord(e1); cudaEventSynchronize(e1);
   float ms; cudaEventElapsedTime(&ms, e0, e1);
   printf("kernel %.3f ms  err=%s\n", ms, cudaGetErrorString(cudaGetLastError()));
-  long long ph[4][16][6];
+  long long ph[4][16][3];
   cudaMemcpyFromSymbol(ph, iga::p3::g_phase, sizeof(ph));
   for (int s = 0; s < 4; ++s) {
     long long t0 = ph[s][0][2];
@@ -44,9 +44,7 @@ int main() {
     for (int w = 0; w < 4; ++w) amax = std::max(amax, ph[s][w][0] - t0);
     for (int w = 4; w < 8; ++w) bmax = std::max(bmax, ph[s][w][0] - t0);
     for (int w = 8; w < 16; ++w) { smid = std::max(smid, ph[s][w][0] - t0); send = std::max(send, ph[s][w][1] - t0); }
-    long long b3 = 0, b4 = 0, b5 = 0;
-    for (int w = 8; w < 16; ++w) { b3 = std::max(b3, ph[s][w][3] - t0); b4 = std::max(b4, ph[s][w][4] - t0); b5 = std::max(b5, ph[s][w][5] - t0); }
-    printf("iter %d: A_end %lld  B_end %lld  S_dmma_end %lld  bar1 %lld staged %lld own_written %lld  S_flush_end %lld", s + 8, amax, bmax, smid, b3, b4, b5, send);
+    printf("iter %d: A_end %lld  B_end %lld  S_dmma_end %lld  S_flush_end %lld", s + 8, amax, bmax, smid, send);
     if (s < 3) printf("  | iteration %lld", ph[s + 1][0][2] - t0);
     printf("\n");
   }
