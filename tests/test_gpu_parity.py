@@ -330,3 +330,30 @@ def test_full_size_sampled_rows(pkg, cfg):
         assert rs.max() <= 1e-12 * np.abs(values).max()  # constants are in the kernel
     if op == "mass" and coef is None:
         assert abs(values.sum() - 1.0) < 1e-12
+
+
+@pytest.mark.parametrize("G", [2, 3, 4])
+def test_slab_sessions_emulated_ranks(pkg, G):
+    """The per-rank SlabSession launches (interface planes first, then owned planes)
+    for G emulated ranks on one GPU; the interface exchange is done here by copies
+    (the NCCL transfer itself is covered by tests/test_distributed.py over gloo)."""
+    import torch
+    from paper_2207_00280_b200.distributed import SlabSession, plane_nnz, slab_plan
+
+    K, p = 12, 3
+    N = K + p
+    cfg = pkg.RunConfig("sumfact", "device", K, p, operator="stiffness")
+    full = pkg.run_integration(cfg).gram.values
+    sessions = [SlabSession(cfg, slab_plan(K, p, G, g)) for g in range(G)]
+    outs = [s.step(exchange=False) for s in sessions]
+    for g in range(1, G):
+        prev, cur = sessions[g - 1], sessions[g]
+        send = prev.values[prev.n_own:]
+        n = plane_nnz(3, K, p, *cur.plan.recv_planes)
+        assert send.numel() == n
+        cur.values[:n] += send
+    torch.cuda.synchronize()
+    got = torch.cat([s.values[:s.n_own] for s in sessions]).cpu().numpy()
+    ip, _ = O.pattern(3, K, p)
+    assert got.size == ip[-1]
+    assert_parity(got, full.cpu().numpy(), ip)
