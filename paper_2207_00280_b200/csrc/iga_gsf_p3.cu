@@ -43,6 +43,7 @@ constexpr int LA = TA + P, LB = TB + P;  // element windows (5, 7)
 constexpr int GB = LB * Q;               // axis-1 quadrature points in the window (28)
 constexpr int NCOL = GB * Q;             // (g1, k2) columns (112)
 constexpr int WP = NCOL + 4;             // W row pitch (== 4 mod 16: conflict-free A loads)
+constexpr int XP = NCOL + 4;             // X row pitch (== 4 mod 16: conflict-free A stores)
 constexpr int NA0 = TA * NB;             // (ia, d0) rows (14)
 constexpr int NCOMBO = NA0 * TB * NB;    // (ia, d0, ib, d1) combos (392)
 constexpr int YP = NCOMBO + 4;           // Y pitch (== 12 mod 16: conflict-free A loads)
@@ -55,14 +56,17 @@ constexpr int MT_S_PER_WARP = (MT_S + NWS - 1) / NWS;  // 7
 constexpr int NPEN = TA * TB;            // row pencils (I0, I1) of the tile
 
 // shared memory layout (doubles)
-constexpr int SZ_X = 2 * NA0 * NCOL;              // one X buffer: [2 types][NA0][NCOL]
+constexpr int SZ_X = 2 * NA0 * XP;                // one X buffer: [2 types][NA0][XP]
 constexpr int SZ_Y = 2 * Q * YP;                  // one Y buffer: [2 accs * Q][YP]
 constexpr int OFF_W = 0;                          // [LA*Q][WP]
 constexpr int OFF_X = OFF_W + LA * Q * WP;        // 2 buffers
 constexpr int OFF_Y = OFF_X + 2 * SZ_X;           // 2 buffers
-constexpr int OFF_BA = OFF_Y + 2 * SZ_Y;          // [2 types][LA][2 nt][32]
+// the constant B fragments are read into registers before the pipeline starts, so
+// they alias Y buffer 1 (first written by stage B at iteration 2)
+constexpr int OFF_BA = OFF_Y + SZ_Y;              // [2 types][LA][2 nt][32]
 constexpr int OFF_BB = OFF_BA + 2 * LA * 2 * 32;  // [2 prods][LB][2 nt][32]
-constexpr int OFF_WQ = OFF_BB + 2 * LB * 2 * 32;  // weights [Q]
+static_assert(2 * LA * 2 * 32 + 2 * LB * 2 * 32 <= SZ_Y, "fragment tables fit Y buffer 1");
+constexpr int OFF_WQ = OFF_Y + 2 * SZ_Y;          // weights [Q]
 constexpr int OFF_PB = OFF_WQ + Q;                // pencil row-pointer bases (int64) [NPEN]
 constexpr int OFF_PC = OFF_PB + NPEN;             // pencil c0*c1 (int in double slots) [NPEN]
 constexpr int OFF_R = OFF_PC + NPEN;              // rolling rows [MT_S][4 slots][2 groups][32]
@@ -161,8 +165,8 @@ __device__ __forceinline__ void stage_a_units(const Lane& L, const double* W, co
     for (int ia = 0; ia < TA; ++ia) {
       double hi, lo;
       split_groups(acc[u][ia], t, hi, lo);
-      X[(ty * NA0 + ia * NB + P + t) * NCOL + col] = hi;
-      if (t > 0) X[(ty * NA0 + ia * NB + t - 1) * NCOL + col] = lo;
+      X[(ty * NA0 + ia * NB + P + t) * XP + col] = hi;
+      if (t > 0) X[(ty * NA0 + ia * NB + t - 1) * XP + col] = lo;
     }
   }
 }
@@ -199,10 +203,10 @@ __device__ __forceinline__ void stage_b_unit(const Lane& L, const double* X, con
       double& b0r = v0 ? yB[clampi(i0, 0, TB - 1)][2 * nt] : z2;
       double& b1r = v1 ? yB[clampi(i1, 0, TB - 1)][2 * nt + 1] : z3;
       const int xo = (lb * Q + t) * Q + k2;
-      const double xv = X[(0 * NA0 + a0) * NCOL + xo];
+      const double xv = X[(0 * NA0 + a0) * XP + xo];
       if (pass == 0) {
         if (L.stiff) {
-          const double xd = X[(1 * NA0 + a0) * NCOL + xo];
+          const double xd = X[(1 * NA0 + a0) * XP + xo];
           dmma(a0r, a1r, xd, bv[i], a0r, a1r);
           dmma(b0r, b1r, xv, bv[i], b0r, b1r);
         } else {
