@@ -118,6 +118,14 @@ int32_t iga_assemble_elements(int32_t dim, int32_t K, int32_t p, const double* m
                               int32_t row_plane_begin, int32_t row_plane_end, double* values,
                               void* stream);
 
+/* Matrix-free operator application y = alpha M x + beta S x over the whole mesh
+ * (x, y: [(K+p)^dim] dof vectors, lexicographic like dof_index), by sum
+ * factorization per element with the problem's coefficient; y is overwritten.
+ * Device version of heat.HeatProblem.assemble_rhs (heat.py:131-158), which is
+ * apply(alpha = 1, beta = -dt).  dim = 3. */
+int32_t iga_apply(const iga_problem* prob, double alpha, double beta, const double* x, double* y,
+                  void* stream);
+
 /* y[i] += x[i], i < n  (interface-row accumulation after the NCCL receive). */
 int32_t iga_axpy(int64_t n, const double* x, double* y, void* stream);
 

@@ -29,6 +29,7 @@ from .integrators import (
     integrate_element_classical,
     integrate_element_sumfact,
 )
+from .operator import MatrixFreeOperator, cg
 from .mesh import QuadratureRule, element_list, gauss_rule, local_index, support_set
 from .runtime import (
     IntegrationRuntime,

@@ -34,6 +34,7 @@ EXPORTS = (
     "iga_assemble_elements",
     "iga_axpy",
     "iga_spmv",
+    "iga_apply",
 )
 
 
@@ -90,8 +91,10 @@ def load():
     L.iga_assemble_elements.argtypes = [i32, i32, i32, vp, i32, i32, vp, vp]
     L.iga_axpy.argtypes = [i64, vp, vp, vp]
     L.iga_spmv.argtypes = [i32, i32, i32, vp, vp, vp, vp]
+    L.iga_apply.argtypes = [ctypes.POINTER(IgaProblem), dp, dp, vp, vp, vp]
     for name in ("iga_mesh_tables", "iga_basis_eval", "iga_csr_pattern", "iga_element_matrices",
-                 "iga_integrate_assemble", "iga_assemble_elements", "iga_axpy", "iga_spmv"):
+                 "iga_integrate_assemble", "iga_assemble_elements", "iga_axpy", "iga_spmv",
+                 "iga_apply"):
         getattr(L, name).restype = i32
     if L.iga_abi_version() != 1:
         raise ImportError("libiga_b200.so ABI version mismatch")

@@ -357,3 +357,43 @@ def test_slab_sessions_emulated_ranks(pkg, G):
     ip, _ = O.pattern(3, K, p)
     assert got.size == ip[-1]
     assert_parity(got, full.cpu().numpy(), ip)
+
+
+# ---------------------------------------------- §8(f): matrix-free apply, CG
+@pytest.mark.parametrize("K,p,coef", [(5, 3, False), (4, 2, True), (3, 4, True), (6, 1, False)])
+def test_matrix_free_apply_matches_assembled(pkg, K, p, coef):
+    from paper_2207_00280_b200.operator import MatrixFreeOperator
+
+    q = p + 1
+    c = np.random.default_rng(5).uniform(0.5, 1.5, size=(K**3, q**3)) if coef else None
+    op = MatrixFreeOperator(K, p, coefficient=c)
+    x = np.random.default_rng(6).standard_normal(op.n_dofs)
+    M = pkg.run_integration(pkg.RunConfig("sumfact", "device", K, p, coefficient=c)).gram.matrix
+    S = pkg.run_integration(pkg.RunConfig("sumfact", "device", K, p, operator="stiffness",
+                                          coefficient=c)).gram.matrix
+    for a, b in ((1.0, 0.0), (0.0, 1.0), (1.0, -0.37)):
+        got = op.apply(x, a, b)
+        ref = a * (M @ x) + b * (S @ x)
+        assert np.linalg.norm(got - ref) <= 1e-13 * np.linalg.norm(ref), (a, b)
+
+
+def test_matrix_free_heat_rhs_pins(pkg):
+    from paper_2207_00280_b200.operator import MatrixFreeOperator
+
+    for K, p in ((3, 2), (4, 3)):
+        g = load_golden(f"heat_rhs_K{K}_p{p}")
+        op = MatrixFreeOperator(K, p)
+        for dt, ref in ((0.0, g["Mmu"]), (1.0, g["Mmu"] - g["Smu"])):
+            got = op.rhs(g["mu"], dt)
+            assert np.linalg.norm(got - ref) <= 1e-13 * np.linalg.norm(ref)
+
+
+def test_cg_solves_gram_system(pkg):
+    from paper_2207_00280_b200.operator import cg
+
+    K, p = 6, 2
+    gram = pkg.run_integration(pkg.RunConfig("sumfact", "device", K, p)).gram
+    xs = np.random.default_rng(8).standard_normal(gram.n_dofs)
+    b = gram.matrix @ xs
+    x, it = cg(gram, b, rtol=1e-12)
+    assert np.linalg.norm(x - xs) <= 1e-8 * np.linalg.norm(xs)
