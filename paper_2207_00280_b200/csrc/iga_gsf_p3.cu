@@ -63,9 +63,9 @@ constexpr int OFF_X = OFF_W + LA * Q * WP;        // 2 buffers
 constexpr int OFF_Y = OFF_X + 2 * SZ_X;           // 2 buffers
 // the constant B fragments are read into registers before the pipeline starts, so
 // they alias Y buffer 1 (first written by stage B at iteration 2)
-constexpr int OFF_BA = OFF_Y + SZ_Y;              // [2 types][LA][2 nt][32]
-constexpr int OFF_BB = OFF_BA + 2 * LA * 2 * 32;  // [2 prods][LB][2 nt][32]
-static_assert(2 * LA * 2 * 32 + 2 * LB * 2 * 32 <= SZ_Y, "fragment tables fit Y buffer 1");
+constexpr int OFF_BA = OFF_Y + SZ_Y;              // [2 types][LA pairs][32]
+constexpr int OFF_BB = OFF_BA + 2 * LA * 32;      // [2 prods][LB][2 nt][32]
+static_assert(2 * LA * 32 + 2 * LB * 2 * 32 <= SZ_Y, "fragment tables fit Y buffer 1");
 constexpr int OFF_WQ = OFF_Y + 2 * SZ_Y;          // weights [Q]
 constexpr int OFF_PB = OFF_WQ + Q;                // pencil row-pointer bases (int64) [NPEN]
 constexpr int OFF_PC = OFF_PB + NPEN;             // pencil c0*c1 (int in double slots) [NPEN]
@@ -122,14 +122,16 @@ __device__ __forceinline__ void split_groups(const double* y, int t, double& hi,
 }
 
 // ---------------------------------------------------------------- stage A
-// Valid (element la, n-tile) pairs of stage A (destination ia = la + k - P in [0, TA))
-constexpr int NPA = 6;
-__host__ __device__ constexpr int pa_la(int i) { return i < 1 ? 0 : (i < 2 ? 1 : (i < 4 ? 2 : (i < 5 ? 3 : 4))); }
-__host__ __device__ constexpr int pa_nt(int i) { return i == 0 ? 1 : (i == 1 ? 1 : (i == 2 ? 0 : (i == 3 ? 1 : 0))); }
+// Stage-A B fragments pair two consecutive r = rb, rb+1 of one window element la;
+// rb is chosen per la so that the 8 useful (la, r) combos (destination ia = la + r - P
+// in [0, TA)) need 5 DMMAs per unit instead of 6 with fixed r-pairs.
+constexpr int NPA = 5;
+__host__ __device__ constexpr int pa_la(int i) { return i; }
+__host__ __device__ constexpr int pa_rb(int i) { return i == 0 ? 2 : (i == 1 ? 2 : (i == 2 ? 1 : 0)); }
 
 // NU units = m-tiles mt0 + i*mstep of (g1,k2) columns for the warp's type, interleaved
 // for ILP; ba[] are the warp's constant B fragments; per-column accumulators
-// acc[u][ia][k] are the DMMA C operands (each receives exactly one element's product).
+// acc[u][ia][r] are the DMMA C operands (each receives exactly one element's product).
 template <int NU>
 __device__ __forceinline__ void stage_a_units(const Lane& L, const double* W, const double (&ba)[NPA],
                                               double* X, int mt0, int mstep, int ty) {
@@ -147,13 +149,13 @@ __device__ __forceinline__ void stage_a_units(const Lane& L, const double* W, co
     for (int la = 0; la < LA; ++la) av[u][la] = W[(la * Q + L.t) * WP + (mt0 + u * mstep) * 8 + L.g];
 #pragma unroll
   for (int i = 0; i < NPA; ++i) {
-    const int la = pa_la(i), nt = pa_nt(i);
-    const int ia0 = la + 2 * nt - P, ia1 = ia0 + 1;
+    const int la = pa_la(i), rb = pa_rb(i);
+    const int ia0 = la + rb - P, ia1 = ia0 + 1;
 #pragma unroll
     for (int u = 0; u < NU; ++u) {
       double z0 = 0.0, z1 = 0.0;
-      double& r0 = (ia0 >= 0 && ia0 < TA) ? acc[u][clampi(ia0, 0, TA - 1)][2 * nt] : z0;
-      double& r1 = (ia1 >= 0 && ia1 < TA) ? acc[u][clampi(ia1, 0, TA - 1)][2 * nt + 1] : z1;
+      double& r0 = (ia0 >= 0 && ia0 < TA) ? acc[u][clampi(ia0, 0, TA - 1)][rb] : z0;
+      double& r1 = (ia1 >= 0 && ia1 < TA) ? acc[u][clampi(ia1, 0, TA - 1)][rb + 1] : z1;
       dmma(r0, r1, av[u][la], ba[i], r0, r1);
     }
   }
@@ -238,15 +240,51 @@ __device__ __forceinline__ void stage_b_unit(const Lane& L, const double* X, con
 // one private slot per (m-tile, row slot, band group, lane), and are the DMMA C
 // operands: column k = 2nt + j (r = k) of element e2 belongs to row e2 + k, i.e.
 // slot (PHI + k) & 3, and to band group hi (d = 3+t) if k < 4-t, else lo (d = t-1).
+//
+// A row's group receives its first contribution at k = 3 (lo) or k = 3-t (hi): that
+// DMMA takes C = 0 instead of the slot, so slots are never re-zeroed.  Row e2 (slot
+// PHI) is complete after its k = 0 product: the hi value goes from the register
+// straight to the CSR row and the lo value (complete since the previous element) is
+// read once from its slot -- the row flush is fused into the stage.
 __device__ __forceinline__ int rs_idx(int mt, int slot, int grp, int lane) {
   return ((mt * 4 + slot) * 2 + grp) * 32 + lane;
 }
 
+// destination of row I2's values for this lane: hi at band offset dh, lo at dl (or -1)
+struct RowDst {
+  int64_t pre2;
+  int c2, dh, dl;
+};
+
+__device__ __forceinline__ RowDst row_dst(int t, int I2, int64_t N) {
+  RowDst r;
+  const int lod2 = max(0, P - I2);
+  r.c2 = (int)band_cnt(I2, P, N);
+  r.pre2 = band_prefix(I2, P, N);
+  r.dh = P + t - lod2;
+  r.dl = t - 1 - lod2;
+  if (r.dh >= r.c2) r.dh = -1;
+  if (t == 0 || r.dl >= r.c2) r.dl = -1;
+  return r;
+}
+
+__device__ __forceinline__ void store_pair(const GsfArgs& a, int m, const int64_t* pb, const int* pc,
+                                           const RowDst& rd, double hi, double lo) {
+  if (m >= 0) {
+    const int rc = m >> 16, b01 = m & 0xffff;
+    double* row = a.values + pb[rc] + (int64_t)pc[rc] * rd.pre2 + b01 * rd.c2;
+    if (rd.dh >= 0) row[rd.dh] = hi;
+    if (rd.dl >= 0) row[rd.dl] = lo;
+  }
+}
+
 template <int PHI, int I0, int NM>
 __device__ __forceinline__ void stage_s_batch(const Lane& L, int ws, const double* Y, double* Rs,
-                                              const double (&b0)[2], const double (&b1)[2]) {
+                                              const double (&b0)[2], const double (&b1)[2],
+                                              const int (&meta)[MT_S_PER_WARP], const int64_t* pb,
+                                              const int* pc, const GsfArgs& a, const RowDst& rd) {
   const int g = L.g, t = L.t;
-  double a0[NM], a1[NM], cc[NM][2][2];
+  double a0[NM], a1[NM], cc[NM][2][2], lo[NM];
   int p[NM][2][2];
 #pragma unroll
   for (int i = 0; i < NM; ++i) {
@@ -259,8 +297,9 @@ __device__ __forceinline__ void stage_s_batch(const Lane& L, int ws, const doubl
       for (int j = 0; j < 2; ++j) {
         const int k = 2 * nt + j;
         p[i][nt][j] = rs_idx(mt, (PHI + k) & 3, k < 4 - t ? 0 : 1, L.lane);
-        cc[i][nt][j] = Rs[p[i][nt][j]];
+        cc[i][nt][j] = (k == 3 || k == 3 - t) ? 0.0 : Rs[p[i][nt][j]];
       }
+    lo[i] = Rs[rs_idx(mt, PHI, 1, L.lane)];
   }
 #pragma unroll
   for (int i = 0; i < NM; ++i)
@@ -275,16 +314,17 @@ __device__ __forceinline__ void stage_s_batch(const Lane& L, int ws, const doubl
         dmma(cc[i][nt][0], cc[i][nt][1], a1[i], b1[nt], cc[i][nt][0], cc[i][nt][1]);
   }
 #pragma unroll
-  for (int i = 0; i < NM; ++i)
+  for (int i = 0; i < NM; ++i) {
 #pragma unroll
-    for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-      for (int j = 0; j < 2; ++j) Rs[p[i][nt][j]] = cc[i][nt][j];
+    for (int k = 1; k < 4; ++k) Rs[p[i][k >> 1][k & 1]] = cc[i][k >> 1][k & 1];
+    store_pair(a, meta[I0 + i], pb, pc, rd, cc[i][0][0], lo[i]);
+  }
 }
 
 template <int PHI>
 __device__ __forceinline__ void stage_s(const Lane& L, int ws, const double* Y, double* Rs,
-                                        const GsfArgs& a, int e2) {
+                                        const GsfArgs& a, int e2, const int (&meta)[MT_S_PER_WARP],
+                                        const int64_t* pb, const int* pc, int64_t N) {
   const int g = L.g, t = L.t;
   const double* V2 = a.V + (int64_t)e2 * M * Q;
   double b0[2], b1[2];
@@ -300,37 +340,24 @@ __device__ __forceinline__ void stage_s(const Lane& L, int ws, const double* Y, 
       b1[nt] = z;
     }
   }
+  const RowDst rd = row_dst(t, e2, N);
   static_assert(MT_S == (MT_S_PER_WARP - 1) * NWS + 1, "stage S warp split");
-  stage_s_batch<PHI, 0, 3>(L, ws, Y, Rs, b0, b1);
-  stage_s_batch<PHI, 3, 3>(L, ws, Y, Rs, b0, b1);
-  if (ws == 0) stage_s_batch<PHI, 6, 1>(L, ws, Y, Rs, b0, b1);
+  stage_s_batch<PHI, 0, 3>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd);
+  stage_s_batch<PHI, 3, 3>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd);
+  if (ws == 0) stage_s_batch<PHI, 6, 1>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd);
 }
 
-// Row I2 (slot sl) is complete: each lane stores its (up to) two values per m-tile
-// straight to the CSR row (neighbouring lanes cover contiguous row segments).
-__device__ __forceinline__ void flush(const Lane& L, int ws, double* Rs, int sl,
-                                      const int (&meta)[MT_S_PER_WARP], const int64_t* pb,
-                                      const int* pc, const GsfArgs& a, int I2, int64_t N) {
-  const int t = L.t;
-  const int lod2 = max(0, P - I2);
-  const int c2 = (int)band_cnt(I2, P, N);
-  const int64_t pre2 = band_prefix(I2, P, N);
-  const int dh = P + t - lod2, dl = t - 1 - lod2;
+// Rows K .. K+P-1 (no element e2 = I2): both groups are complete in their slots.
+__device__ __forceinline__ void flush_tail(const Lane& L, int ws, const double* Rs, int I2,
+                                           const int (&meta)[MT_S_PER_WARP], const int64_t* pb,
+                                           const int* pc, const GsfArgs& a, int64_t N) {
+  const RowDst rd = row_dst(L.t, I2, N);
+  const int sl = I2 & 3;
 #pragma unroll
   for (int i = 0; i < MT_S_PER_WARP; ++i) {
     const int mt = ws + i * NWS;
-    if (mt < MT_S) {
-      const int ph = rs_idx(mt, sl, 0, L.lane), pl = rs_idx(mt, sl, 1, L.lane);
-      const int m = meta[i];
-      if (m >= 0) {
-        const int rc = m >> 16, b01 = m & 0xffff;
-        double* row = a.values + pb[rc] + (int64_t)pc[rc] * pre2 + b01 * c2;
-        if (dh >= 0 && dh < c2) row[dh] = Rs[ph];
-        if (t > 0 && dl >= 0 && dl < c2) row[dl] = Rs[pl];
-      }
-      Rs[ph] = 0.0;
-      Rs[pl] = 0.0;
-    }
+    if (mt < MT_S)
+      store_pair(a, meta[i], pb, pc, rd, Rs[rs_idx(mt, sl, 0, L.lane)], Rs[rs_idx(mt, sl, 1, L.lane)]);
   }
 }
 
@@ -384,13 +411,14 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
   const int e0lo = max(a.el_begin, 0), e0hi = min(a.el_end, K);
 
   // ---- constant B fragments of axes 0 and 1 (pair products of the window elements)
-  for (int u = tid; u < 2 * LA * 2 * 32; u += NT) {
-    const int ln = u & 31, nt = (u >> 5) & 1, la = (u >> 6) % LA, type = u / (64 * LA);
+  for (int u = tid; u < 2 * LA * 32; u += NT) {
+    const int ln = u & 31, la = (u >> 5) % LA, type = u / (32 * LA);
     const int gg = ln >> 2, tt = ln & 3, e0 = i00 - P + la;
+    const int r = pa_rb(la) + (gg & 1), sc = (r + (gg >> 1)) & 3;
     double v = 0.0;
     if (e0 >= 0 && e0 < K && (type == 0 || L.stiff)) {
       const double* T = (type == 0 ? a.V : a.D) + (int64_t)e0 * M * Q;
-      v = T[bcol_r(nt, gg) * Q + tt] * T[bcol_s(nt, gg) * Q + tt];
+      v = T[r * Q + tt] * T[sc * Q + tt];
     }
     BA[u] = v;
   }
@@ -423,7 +451,7 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
     const int ty = L.stiff ? (wa & 1) : 0;
     double ba[NPA];
 #pragma unroll
-    for (int i = 0; i < NPA; ++i) ba[i] = BA[((ty * LA + pa_la(i)) * 2 + pa_nt(i)) * 32 + L.lane];
+    for (int i = 0; i < NPA; ++i) ba[i] = BA[(ty * LA + pa_la(i)) * 32 + L.lane];
     const int mt0 = L.stiff ? (wa >> 1) : wa, mstep = L.stiff ? NWA / 2 : NWA;
     for (int it = 0; it < n_it; ++it) {
       PT(2);
@@ -491,19 +519,18 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
       if (e2 >= 0) {
         const double* Y = sm + OFF_Y + (e2 & 1) * SZ_Y;
         switch (e2 & 3) {
-          case 0: stage_s<0>(L, ws, Y, Rs, a, e2); break;
-          case 1: stage_s<1>(L, ws, Y, Rs, a, e2); break;
-          case 2: stage_s<2>(L, ws, Y, Rs, a, e2); break;
-          default: stage_s<3>(L, ws, Y, Rs, a, e2); break;
+          case 0: stage_s<0>(L, ws, Y, Rs, a, e2, meta, pb, pc, N); break;
+          case 1: stage_s<1>(L, ws, Y, Rs, a, e2, meta, pb, pc, N); break;
+          case 2: stage_s<2>(L, ws, Y, Rs, a, e2, meta, pb, pc, N); break;
+          default: stage_s<3>(L, ws, Y, Rs, a, e2, meta, pb, pc, N); break;
         }
         PT(0);
-        flush(L, ws, Rs, e2 & 3, meta, pb, pc, a, e2, N);
         PT(1);
       }
       __syncthreads();
     }
     // rows K .. K+P-1 received their last contribution from element K-1
-    for (int I2 = K; I2 < N; ++I2) flush(L, ws, Rs, I2 & 3, meta, pb, pc, a, I2, N);
+    for (int I2 = K; I2 < N; ++I2) flush_tail(L, ws, Rs, I2, meta, pb, pc, a, N);
   }
 }
 
