@@ -70,7 +70,8 @@ constexpr int OFF_WQ = OFF_Y + 2 * SZ_Y;          // weights [Q]
 constexpr int OFF_PB = OFF_WQ + Q;                // pencil row-pointer bases (int64) [NPEN]
 constexpr int OFF_PC = OFF_PB + NPEN;             // pencil c0*c1 (int in double slots) [NPEN]
 constexpr int OFF_R = OFF_PC + NPEN;              // rolling rows [MT_S][4 slots][2 groups][32]
-constexpr int SMEM_DOUBLES = OFF_R + MT_S * 4 * 2 * 32;
+constexpr int OFF_MB = OFF_R + MT_S * 4 * 2 * 32;  // mbarriers [xfull 2][xempty 2][yfull 2][yempty 2]
+constexpr int SMEM_DOUBLES = OFF_MB + 8;
 static_assert(SMEM_DOUBLES * 8 <= 227 * 1024, "shared memory budget");
 static_assert(SMEM_DOUBLES * 8 <= 227 * 1024, "shared memory budget");
 constexpr size_t SMEM_BYTES = SMEM_DOUBLES * sizeof(double);
@@ -82,9 +83,24 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b,
       : "d"(a), "d"(b), "d"(c0), "d"(c1));
 }
 
-// barrier among the 4 warps of one warpgroup (ids 1..4)
-__device__ __forceinline__ void wg_bar(int id) {
-  asm volatile("bar.sync %0, 128;\n" ::"r"(id));
+// shared-memory mbarriers: the roles hand buffers to each other (full / empty per
+// buffer) instead of a CTA-wide barrier per element column
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, int parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "MBW%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra MBW%=;\n}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
 }
 
 // Is any column k in {2nt, 2nt+1} of window element l mapped to a destination
@@ -432,6 +448,17 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
     }
     BB[u] = v;
   }
+  uint64_t* mb = reinterpret_cast<uint64_t*>(sm + OFF_MB);
+  uint64_t *xfull = mb, *xempty = mb + 2, *yfull = mb + 4, *yempty = mb + 6;
+  if (tid == 0) {
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(xfull + b, NWA * 32);
+      mbar_init(xempty + b, NWB * 32);
+      mbar_init(yfull + b, NWB * 32);
+      mbar_init(yempty + b, NWS * 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
   if (tid < Q) wq[tid] = a.weights[tid];
   if (tid < NPEN) {
     const int64_t I0 = i00 + tid / TB, I1 = i10 + tid % TB;
@@ -442,7 +469,7 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
   if (a.coef == nullptr) form_w(W, wq, a, 0, i00, i10, e0lo, e0hi, tid, NT);  // step-invariant
   __syncthreads();
 
-  const int n_it = K + 2;  // pipeline: A on it, B on it-1, S on it-2
+  // pipeline: A on element column it, B on it-1, S on it-2, handed over by mbarriers
   if (warp < NWA) {
     // ------------------------------------------------------------ role A
     // warp wa owns type wa (values / derivatives; for the mass operator both warps
@@ -453,20 +480,22 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
 #pragma unroll
     for (int i = 0; i < NPA; ++i) ba[i] = BA[(ty * LA + pa_la(i)) * 32 + L.lane];
     const int mt0 = L.stiff ? (wa >> 1) : wa, mstep = L.stiff ? NWA / 2 : NWA;
-    for (int it = 0; it < n_it; ++it) {
+    __syncthreads();  // every role holds its fragments before Y buffer 1 is written
+    for (int it = 0; it < K; ++it) {
       PT(2);
-      if (it < K) {
-        if (a.coef != nullptr) {
-          form_w(W, wq, a, it, i00, i10, e0lo, e0hi, tid, NWA * 32);
-          asm volatile("bar.sync 1, %0;\n" ::"n"(NWA * 32));
-        }
-        double* X = sm + OFF_X + (it & 1) * SZ_X;
-        int mt = mt0;
-        for (; mt + mstep < MT_A; mt += 2 * mstep) stage_a_units<2>(L, W, ba, X, mt, mstep, ty);
-        if (mt < MT_A) stage_a_units<1>(L, W, ba, X, mt, mstep, ty);
-        PT(0);
+      if (a.coef != nullptr) {
+        if (it > 0) asm volatile("bar.sync 1, %0;\n" ::"n"(NWA * 32));  // W of it-1 consumed
+        form_w(W, wq, a, it, i00, i10, e0lo, e0hi, tid, NWA * 32);
+        asm volatile("bar.sync 1, %0;\n" ::"n"(NWA * 32));
       }
-      __syncthreads();
+      const int b = it & 1;
+      if (it >= 2) mbar_wait(xempty + b, ((it >> 1) - 1) & 1);
+      double* X = sm + OFF_X + b * SZ_X;
+      int mt = mt0;
+      for (; mt + mstep < MT_A; mt += 2 * mstep) stage_a_units<2>(L, W, ba, X, mt, mstep, ty);
+      if (mt < MT_A) stage_a_units<1>(L, W, ba, X, mt, mstep, ty);
+      mbar_arrive(xfull + b);
+      PT(0);
     }
   } else if (warp < NWA + NWB) {
     // ------------------------------------------------------------ role B
@@ -477,16 +506,19 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
       bv[i] = BB[((0 * LB + pb_lb(i)) * 2 + pb_nt(i)) * 32 + L.lane];
       bd[i] = BB[((1 * LB + pb_lb(i)) * 2 + pb_nt(i)) * 32 + L.lane];
     }
-    for (int it = 0; it < n_it; ++it) {
+    __syncthreads();
+    for (int e2 = 0; e2 < K; ++e2) {
+      const int it = e2 + 1;
       PT(2);
-      const int e2 = it - 1;
-      if (e2 >= 0 && e2 < K) {
-        const double* X = sm + OFF_X + (e2 & 1) * SZ_X;
-        double* Y = sm + OFF_Y + (e2 & 1) * SZ_Y;
-        for (int mt = wb; mt < MT_B; mt += NWB) stage_b_unit(L, X, bv, bd, Y, mt);
-        PT(0);
-      }
-      __syncthreads();
+      const int b = e2 & 1, n = e2 >> 1;
+      mbar_wait(xfull + b, n & 1);
+      if (n >= 1) mbar_wait(yempty + b, (n - 1) & 1);
+      const double* X = sm + OFF_X + b * SZ_X;
+      double* Y = sm + OFF_Y + b * SZ_Y;
+      for (int mt = wb; mt < MT_B; mt += NWB) stage_b_unit(L, X, bv, bd, Y, mt);
+      mbar_arrive(xempty + b);
+      mbar_arrive(yfull + b);
+      PT(0);
     }
   } else {
     // ------------------------------------------------------------ role S
@@ -513,21 +545,22 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
     }
     double* Rs = sm + OFF_R;
     for (int u = ws * 32 + L.lane; u < MT_S * 4 * 2 * 32; u += NWS * 32) Rs[u] = 0.0;
-    for (int it = 0; it < n_it; ++it) {
+    __syncthreads();
+    for (int e2 = 0; e2 < K; ++e2) {
+      const int it = e2 + 2;
       PT(2);
-      const int e2 = it - 2;
-      if (e2 >= 0) {
-        const double* Y = sm + OFF_Y + (e2 & 1) * SZ_Y;
-        switch (e2 & 3) {
-          case 0: stage_s<0>(L, ws, Y, Rs, a, e2, meta, pb, pc, N); break;
-          case 1: stage_s<1>(L, ws, Y, Rs, a, e2, meta, pb, pc, N); break;
-          case 2: stage_s<2>(L, ws, Y, Rs, a, e2, meta, pb, pc, N); break;
-          default: stage_s<3>(L, ws, Y, Rs, a, e2, meta, pb, pc, N); break;
-        }
-        PT(0);
-        PT(1);
+      const int b = e2 & 1;
+      mbar_wait(yfull + b, (e2 >> 1) & 1);
+      const double* Y = sm + OFF_Y + b * SZ_Y;
+      switch (e2 & 3) {
+        case 0: stage_s<0>(L, ws, Y, Rs, a, e2, meta, pb, pc, N); break;
+        case 1: stage_s<1>(L, ws, Y, Rs, a, e2, meta, pb, pc, N); break;
+        case 2: stage_s<2>(L, ws, Y, Rs, a, e2, meta, pb, pc, N); break;
+        default: stage_s<3>(L, ws, Y, Rs, a, e2, meta, pb, pc, N); break;
       }
-      __syncthreads();
+      mbar_arrive(yempty + b);
+      PT(0);
+      PT(1);
     }
     // rows K .. K+P-1 received their last contribution from element K-1
     for (int I2 = K; I2 < N; ++I2) flush_tail(L, ws, Rs, I2, meta, pb, pc, a, N);
