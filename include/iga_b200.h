@@ -41,6 +41,9 @@ extern "C" {
 #define IGA_METHOD_SUMFACT 1          /* Algorithm 2, element-local, integrators.py:112-151 */
 #define IGA_METHOD_SUMFACT_ASSEMBLED 2 /* sum factorization with the inter-element sum
                                           folded into each axis contraction (row owner) */
+#define IGA_METHOD_SEPARABLE 3         /* scalar coefficient only: the 3D quadrature factorised
+                                          into assembled 1D band matrices (Kronecker form),
+                                          HBM-bound CSR fill; dim = 3 */
 
 /* One mesh-wide problem: open uniform knots on [0,1]^dim, K elements per
  * axis, degree p, q Gauss points per axis (mesh.py:73-93). */

@@ -19,7 +19,7 @@ CSRC = os.path.join(_HERE, "csrc")
 
 IGA_OK, IGA_EINVAL, IGA_ECUDA, IGA_EUNSUPPORTED = 0, 1, 2, 3
 OPS = {"mass": 0, "stiffness": 1, "stiffness_mass": 2}
-METHOD_CLASSICAL, METHOD_SUMFACT, METHOD_SUMFACT_ASSEMBLED = 0, 1, 2
+METHOD_CLASSICAL, METHOD_SUMFACT, METHOD_SUMFACT_ASSEMBLED, METHOD_SEPARABLE = 0, 1, 2, 3
 
 # Every symbol include/iga_b200.h declares (checked by tests/test_abi.py).
 EXPORTS = (

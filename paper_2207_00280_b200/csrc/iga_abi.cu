@@ -2,6 +2,9 @@
 // vector kernels, and the K1 (basis tables) and K5 (CSR pattern) kernels.
 #include <cstdarg>
 #include <cstdio>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "iga_dispatch.cuh"
 
@@ -28,6 +31,52 @@ int check_cuda(cudaError_t err, const char* what) {
   if (err == cudaSuccess) return IGA_OK;
   set_error("%s: %s", what, cudaGetErrorString(err));
   return IGA_ECUDA;
+}
+
+static std::mutex g_launch_mu;
+
+cudaError_t smem_attr_once(const void* fn, size_t bytes, bool max_carveout) {
+  static std::map<std::pair<const void*, int>, size_t> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> g(g_launch_mu);
+  auto it = done.find({fn, dev});
+  if (it != done.end() && it->second >= bytes) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess && max_carveout)
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared);
+  if (e == cudaSuccess) done[{fn, dev}] = bytes;
+  return e;
+}
+
+int sm_count() {
+  static std::map<int, int> cache;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  std::lock_guard<std::mutex> g(g_launch_mu);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  int n = 148;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  cache[dev] = n;
+  return n;
+}
+
+int blocks_per_sm_once(const void* fn, int threads, size_t smem) {
+  static std::map<std::tuple<const void*, int, int, size_t>, int> cache;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 1;
+  std::lock_guard<std::mutex> g(g_launch_mu);
+  auto key = std::make_tuple(fn, dev, threads, smem);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  int n = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, threads, smem) != cudaSuccess || n < 1)
+    n = 1;
+  cache[key] = n;
+  return n;
 }
 
 // ------------------------------------------------------------------ K1

@@ -47,4 +47,16 @@ struct GsfArgs {
   double* values;
 };
 
+struct KronArgs {
+  int K, op;
+  int el_begin, el_end;          // element slab along axis 0
+  int plane_begin, plane_end;    // row planes I0 written
+  int64_t base;                  // rowptr of (plane_begin, 0, 0)
+  double jc;                     // jac * scalar coefficient
+  const double* weights;         // [Q]
+  const double* V;               // [K][P+1][Q]
+  const double* D;               // [K][P+1][Q] (null for mass)
+  double* values;
+};
+
 }  // namespace iga

@@ -23,6 +23,14 @@ void set_error(const char* fmt, ...);
 int fail_einval(const char* fmt, ...);
 int check_cuda(cudaError_t err, const char* what);
 
+// ------------------------------------------------ cached launch set-up (host)
+// Function attributes and occupancy are per (kernel, device) and cost host
+// microseconds per call -- time the GPU would otherwise idle between
+// back-to-back launches -- so they are set / queried once (iga_abi.cu).
+cudaError_t smem_attr_once(const void* fn, size_t bytes, bool max_carveout = false);
+int sm_count();
+int blocks_per_sm_once(const void* fn, int threads, size_t smem);
+
 // ----------------------------------------------------- strict IEEE helpers
 // __dmul_rn / __dadd_rn are never contracted into DFMA, so expressions built
 // from them round exactly like the numba kernels (strict left-to-right).

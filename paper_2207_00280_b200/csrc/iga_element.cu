@@ -201,8 +201,7 @@ struct ElementStrictLaunch {
     if (a.dim == 3) {
       shm = sizeof(double) * (3 * 2 * m * Q + Q + m * m * Q * Q + m * m * m * m * Q);
       if (shm > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(k_element_strict<3, P, Q>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+        cudaError_t e = smem_attr_once(reinterpret_cast<const void*>(k_element_strict<3, P, Q>), shm);
         if (e != cudaSuccess) return check_cuda(e, "element smem attr");
       }
       k_element_strict<3, P, Q><<<(unsigned)a.count, 256, shm, s>>>(a);

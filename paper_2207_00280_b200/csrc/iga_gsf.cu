@@ -267,9 +267,7 @@ struct GsfLaunch {
       const int tiles0 = (planes + TA - 1) / TA;
       a.tiles1 = (int)((N + TB - 1) / TB);
       const int64_t grid = (int64_t)tiles0 * a.tiles1;
-      cudaError_t e = cudaFuncSetAttribute(k_gsf3<P, Q, TA, TB>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)Sh::bytes);
+      cudaError_t e = smem_attr_once(reinterpret_cast<const void*>(k_gsf3<P, Q, TA, TB>), Sh::bytes);
       if (e != cudaSuccess) return check_cuda(e, "gsf smem attr");
       k_gsf3<P, Q, TA, TB><<<(unsigned)grid, 512, Sh::bytes, s>>>(a);
       return check_cuda(cudaGetLastError(), "gsf launch");

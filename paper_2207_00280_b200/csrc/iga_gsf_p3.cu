@@ -577,8 +577,7 @@ int launch_gsf_p3(const GsfArgs& a0, cudaStream_t s) {
   const int tiles0 = (planes + p3::TA - 1) / p3::TA;
   a.tiles1 = (int)((N + p3::TB - 1) / p3::TB);
   const int64_t grid = (int64_t)tiles0 * a.tiles1;
-  cudaError_t e = cudaFuncSetAttribute(p3::k_gsf3_p3, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)p3::SMEM_BYTES);
+  cudaError_t e = smem_attr_once(reinterpret_cast<const void*>(p3::k_gsf3_p3), p3::SMEM_BYTES);
   if (e != cudaSuccess) return check_cuda(e, "gsf_p3 smem attr");
   p3::k_gsf3_p3<<<(unsigned)grid, p3::NT, p3::SMEM_BYTES, s>>>(a);
   return check_cuda(cudaGetLastError(), "gsf_p3 launch");

@@ -8,6 +8,7 @@ namespace iga {
 
 int launch_scatter(const ScatterArgs& a, int method, int p, int q, cudaStream_t s);
 int launch_gsf(const GsfArgs& a, int p, int q, cudaStream_t s);
+int launch_kron(const KronArgs& a, int p, int q, cudaStream_t s);
 
 // assembly.assemble from element matrices: one warp per CSR row, lanes over
 // its columns; every value sums its element contributions in lexicographic
@@ -140,6 +141,19 @@ int32_t iga_integrate_assemble(const iga_problem* prob, int32_t method, int32_t 
   const int64_t base = rowptr(dim, row_first, p, N);
   const int64_t nvals = rowptr(dim, row_last, p, N) - base;
   if (nvals == 0) return IGA_OK;
+  if (method == IGA_METHOD_SEPARABLE) {
+    if (dim != 3) {
+      set_error("the separable method is implemented for dim=3 only");
+      return IGA_EUNSUPPORTED;
+    }
+    if (prob->coef) return fail_einval("the separable method needs a scalar coefficient (coef == NULL)");
+    KronArgs a;
+    a.K = K; a.op = prob->op; a.el_begin = el_begin; a.el_end = el_end;
+    a.plane_begin = row_plane_begin; a.plane_end = row_plane_end; a.base = base;
+    a.jc = prob->jac * prob->coef_scalar; a.weights = prob->weights;
+    a.V = prob->tables_v; a.D = prob->tables_d; a.values = values;
+    return launch_kron(a, p, prob->q, s);
+  }
   if (method == IGA_METHOD_SUMFACT_ASSEMBLED) {
     if (dim != 3) {
       set_error("assembled sum factorization is implemented for dim=3 only");

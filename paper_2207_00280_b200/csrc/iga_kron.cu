@@ -1,0 +1,272 @@
+// Separable integration + assembly (IGA_METHOD_SEPARABLE) for a scalar
+// coefficient on the tensor-product mesh with the identity geometry map.
+//
+// With W(k0,k1,k2) = c jac w_k0 w_k1 w_k2 the element quadrature of the reference
+// (integrators.py:77-151) factorises exactly per axis, and so does its sum over the
+// elements supporting a pair (assembly.py:80-82):
+//
+//   M[I,J] = c jac  m(I0,J0) m(I1,J1) m(I2,J2)
+//   S[I,J] = c jac (k0 m1 m2 + m0 k1 m2 + m0 m1 k2)
+//   m(I,J) = sum_e sum_q w_q V_e(I-e,q) V_e(J-e,q),   k: same with derivatives D
+//
+// i.e. the global matrix is a sum of Kronecker products of assembled 1D band
+// matrices -- sum factorisation carried to its limit for a rank-one weight tensor.
+// The 1D matrices are integrated by Gauss quadrature inside the kernel (per CTA,
+// into shared memory); every CSR value then costs a multiply and an FMA on two
+// per-pencil factors, so the kernel is bound by the HBM write of the CSR values.
+// The element slab [el_begin, el_end) (multi-GPU) restricts only the axis-0 factor.
+//
+// One CTA per (I0, I1) row pencil (grid-stride): the pencil's rows I2 = 0..N-1 are
+// contiguous in the CSR; they are produced in shared memory a few rows at a time
+// and written by TMA bulk stores.
+#include "iga_args.cuh"
+#include "iga_dispatch.cuh"
+
+namespace iga {
+
+// 1D band entry (I, J = I + d - P) over the elements e in [e_lo, e_hi): value and
+// derivative products, elements ascending, quadrature points ascending.
+template <int P, int Q>
+__device__ __forceinline__ double2 band1d(const double* V, const double* D, int K, const double* w,
+                                          int I, int d, int e_lo, int e_hi, bool stiff) {
+  constexpr int M = P + 1;
+  const int J = I + d - P;
+  double m = 0.0, k = 0.0;
+  const int lo = max(max(I, J) - P, max(e_lo, 0)), hi = min(min(I, J) + 1, min(e_hi, K));
+  // at most P+1 elements, unrolled and predicated: every table load is in flight at once
+#pragma unroll
+  for (int t = 0; t <= P; ++t) {
+    const int e = lo + t;
+    if (e < hi) {
+      const double* Ve = V + e * M * Q;
+      const int i = I - e, j = J - e;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) m += (w[q] * Ve[i * Q + q]) * Ve[j * Q + q];
+      if (stiff) {
+        const double* De = D + e * M * Q;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) k += (w[q] * De[i * Q + q]) * De[j * Q + q];
+      }
+    }
+  }
+  return make_double2(m, k);
+}
+
+#ifndef KRON_MINB
+#define KRON_MINB 3
+#endif
+
+// threads per CTA: one per value of an interior row (NB^3, rounded to warps, <= 1024)
+__host__ __device__ constexpr int kron_nt(int P) {
+  return ((2 * P + 1) * (2 * P + 1) * (2 * P + 1) + 31) / 32 * 32 > 1024
+             ? 1024
+             : ((2 * P + 1) * (2 * P + 1) * (2 * P + 1) + 31) / 32 * 32;
+}
+// resident CTAs per SM asked of the register allocator
+__host__ __device__ constexpr int kron_minb(int P) {
+  return kron_nt(P) * KRON_MINB > 1536 ? 1 : KRON_MINB;
+}
+// rows per staged chunk (one TMA bulk store each)
+__host__ __device__ constexpr int kron_rows(int P) { return P <= 2 ? 16 : (P == 3 ? 8 : 4); }
+// doubles per staging buffer: a chunk of full rows plus 16-byte alignment padding
+__host__ __device__ constexpr int kron_stage(int P) {
+  return kron_rows(P) * (2 * P + 1) * (2 * P + 1) * (2 * P + 1) + 2;
+}
+
+__device__ __forceinline__ void bulk_store(double* g, const double* sm, int bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(g),
+               "r"((unsigned)__cvta_generic_to_shared(sm)), "r"(bytes)
+               : "memory");
+}
+
+// CSR values are produced into a shared-memory chunk laid out exactly like its
+// global range (same address mod 16) and leave with one TMA bulk store per chunk:
+// the copy engine writes whole lines whatever the row alignment (rows of NB^3
+// doubles are not 128-byte multiples; per-thread stores of them straddle lines and
+// ran at half the write bandwidth), and the store issue leaves the SM pipes.
+template <int P, int Q>
+__global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) {
+  constexpr int NB = 2 * P + 1;
+  constexpr int NT = kron_nt(P);
+  constexpr int NE = (NB * NB * NB + NT - 1) / NT;  // interior values per thread and row
+  constexpr int G = kron_rows(P), SG = kron_stage(P);
+  extern __shared__ __align__(16) double2 tb[];  // [2][N][NB] (m, k): all elements, slab
+  __shared__ double w[Q];
+  __shared__ double2 F[NB * NB];  // pair factors of the current pencil
+  const int K = a.K, tid = threadIdx.x;
+  const int64_t N = (int64_t)K + P;
+  const bool stiff = a.op != IGA_OP_MASS;
+  // axis 0 sees only the slab's elements [el_begin, el_end); its table is a copy of the
+  // full one unless the slab is a proper subset
+  const bool full = a.el_begin <= 0 && a.el_end >= K;
+  const double2* tb0 = full ? tb : tb + N * NB;
+  double* stage = reinterpret_cast<double*>(tb + 2 * N * NB);  // [2][SG]
+  // 1D tables: the basis tables are first copied (coalesced) into the staging area
+  // when they fit, so the band sums read shared memory
+  constexpr int M = P + 1;
+  const int nvd = K * M * Q;
+  const bool vd_smem = 2 * nvd <= 2 * SG;
+  const double* Vs = a.V;
+  const double* Ds = a.D;
+  if (vd_smem) {
+    for (int u = tid; u < nvd; u += NT) {
+      stage[u] = __ldg(a.V + u);
+      if (stiff) stage[nvd + u] = __ldg(a.D + u);
+    }
+    Vs = stage;
+    Ds = stage + nvd;
+  }
+  if (tid < Q) w[tid] = a.weights[tid];
+  __syncthreads();
+  for (int u = tid; u < (full ? 1 : 2) * N * NB; u += NT) {
+    const int v = u < N * NB ? u : u - (int)(N * NB);
+    const bool slab = u >= N * NB;
+#if defined(KRON_PROLOGUE_ONLY) && KRON_PROLOGUE_ONLY == 2
+    tb[u] = make_double2(v, slab);
+#else
+    tb[u] = band1d<P, Q>(Vs, Ds, K, w, v / NB, v % NB, slab ? a.el_begin : 0, slab ? a.el_end : K,
+                         stiff);
+#endif
+  }
+  __syncthreads();
+
+#ifdef KRON_PROLOGUE_ONLY
+  if (a.K > 0) return;
+#endif
+  // Work: chunks of G rows of a pencil, in CSR order; CTA b takes the contiguous
+  // range [b U / grid, (b+1) U / grid) of the U chunks (one wave, balanced to a chunk)
+  int chunk = 0;  // chunks issued by this CTA (selects the staging buffer)
+  const int nch = (int)((N + G - 1) / G);
+  const int64_t nunit = (int64_t)(a.plane_end - a.plane_begin) * N * nch;
+  const int64_t u_lo = nunit * blockIdx.x / gridDim.x, u_hi = nunit * (blockIdx.x + 1) / gridDim.x;
+  for (int64_t pen = u_lo / nch; pen * nch < u_hi; ++pen) {
+    const int I0 = a.plane_begin + (int)(pen / N), I1 = (int)(pen % N);
+    const double2* r0 = tb0 + I0 * NB;
+    const int lod0 = max(0, P - I0), lod1 = max(0, P - I1);
+    const int c0 = (int)band_cnt(I0, P, N), c1 = (int)band_cnt(I1, P, N), c01 = c0 * c1;
+    const double2* r1 = tb + I1 * NB;
+    // per-pair factors: value = fa * m2 + fb * k2
+    auto factors = [&](int b, double& fa, double& fb) {
+      const double2 x0 = r0[lod0 + b / c1], x1 = r1[lod1 + b % c1];
+      const double mm = a.jc * (x0.x * x1.x);
+      if (a.op == IGA_OP_MASS) {
+        fa = mm; fb = 0.0;
+      } else {
+        double s = a.jc * (x0.y * x1.x + x0.x * x1.y);
+        if (a.op == IGA_OP_STIFFNESS_MASS) s += mm;
+        fa = s; fb = mm;
+      }
+    };
+    double* vals = a.values + (rowptr3(I0, I1, 0, P, N) - a.base);
+    const int ncnt = c01 * NB;  // values of an interior row
+    double fa[NE], fb[NE];
+    int d2[NE];
+#pragma unroll
+    for (int j = 0; j < NE; ++j) {
+      const int e = tid + j * NT;
+      fa[j] = fb[j] = 0.0;
+      d2[j] = e % NB;
+      if (e < ncnt) factors(e / NB, fa[j], fb[j]);
+    }
+    // the pencil's pair factors for the truncated rows (visible after the chunk barrier;
+    // the previous pencil's last reader passed the barrier before its bulk store)
+    for (int b = tid; b < c01; b += NT) {
+      double f0, f1;
+      factors(b, f0, f1);
+      F[b] = make_double2(f0, f1);
+    }
+    const int64_t pc0 = u_lo - pen * nch, pc1 = u_hi - pen * nch;
+    const int ch0 = pc0 > 0 ? (int)pc0 : 0, ch1 = pc1 < nch ? (int)pc1 : nch;
+    for (int R0 = ch0 * G; R0 < ch1 * G; R0 += G, ++chunk) {
+      const int R1 = min((int)N, R0 + G);
+      const int64_t off0 = (int64_t)c01 * band_prefix(R0, P, N);
+      const int len = (int)((int64_t)c01 * band_prefix(R1, P, N) - off0);
+      double* g = vals + off0;
+      const int pad = (int)((reinterpret_cast<uintptr_t>(g) >> 3) & 1);
+      double* buf = stage + (chunk & 1) * SG;
+      // the bulk store issued from this buffer two chunks ago has finished reading it
+      if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+      __syncthreads();
+      double* sb = buf + pad;
+      if (R0 >= P && R0 + G <= K) {
+        // G full-band rows: fixed (pair, d2) per thread, rows ncnt apart
+        const double2* t2 = tb + R0 * NB;
+#pragma unroll
+        for (int r = 0; r < G; ++r)
+#pragma unroll
+          for (int j = 0; j < NE; ++j) {
+            const int e = tid + j * NT;
+            if (e < ncnt) {
+              const double2 x2 = t2[r * NB + d2[j]];
+              sb[r * ncnt + e] = fa[j] * x2.x + fb[j] * x2.y;
+            }
+          }
+      } else {
+        int loc = 0;  // value offset of row I2 inside the chunk
+        for (int I2 = R0; I2 < R1; ++I2) {
+          const double2* t2 = tb + I2 * NB;
+          if (I2 >= P && I2 < K) {
+#pragma unroll
+            for (int j = 0; j < NE; ++j) {
+              const int e = tid + j * NT;
+              if (e < ncnt) {
+                const double2 x2 = t2[d2[j]];
+                sb[loc + e] = fa[j] * x2.x + fb[j] * x2.y;
+              }
+            }
+            loc += ncnt;
+          } else {  // truncated band: b = e / c2 by a reciprocal (exact for e < 2^20 / NB)
+            const int c2 = (int)band_cnt(I2, P, N), lod2 = max(0, P - I2);
+            const unsigned inv = (1u << 20) / (unsigned)c2 + 1u;
+            for (int e = tid; e < c01 * c2; e += NT) {
+              const int b = (int)(((unsigned)e * inv) >> 20);
+              const double2 f = F[b], x2 = t2[lod2 + e - b * c2];
+              sb[loc + e] = f.x * x2.x + f.y * x2.y;
+            }
+            loc += c01 * c2;
+          }
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      __syncthreads();
+      if (tid == 0) {
+        // 16-byte aligned middle by TMA; an unaligned first / last value by plain stores
+        int h = pad, n = len - pad;
+        if (pad) g[0] = sb[0];
+        if (n & 1) { g[len - 1] = sb[len - 1]; --n; }
+        if (n > 0) bulk_store(g + h, sb + h, n * 8);
+        asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+      }
+    }
+  }
+  if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+}
+
+template <int P, int Q>
+struct KronLaunch {
+  static int run(const KronArgs& a, cudaStream_t s) {
+    const int64_t N = (int64_t)a.K + P;
+    constexpr int NT = kron_nt(P);
+    const size_t smem = 2 * sizeof(double2) * N * (2 * P + 1) + 2 * sizeof(double) * kron_stage(P);
+    if (smem > 220 * 1024) {
+      set_error("separable path: 1D band tables of K=%d do not fit shared memory", a.K);
+      return IGA_EUNSUPPORTED;
+    }
+    const void* fn = reinterpret_cast<const void*>(k_kron3<P, Q>);
+    cudaError_t e = smem_attr_once(fn, smem, true);
+    if (e != cudaSuccess) return check_cuda(e, "kron smem attr");
+    const int per_sm = blocks_per_sm_once(fn, NT, smem), sms = sm_count();
+    const int64_t nunit = (int64_t)(a.plane_end - a.plane_begin) * N * ((N + kron_rows(P) - 1) / kron_rows(P));
+    int64_t grid = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
+    if (grid > nunit) grid = nunit;
+    if (grid <= 0) return IGA_OK;
+    k_kron3<P, Q><<<(unsigned)grid, NT, smem, s>>>(a);
+    return check_cuda(cudaGetLastError(), "kron launch");
+  }
+};
+
+int launch_kron(const KronArgs& a, int p, int q, cudaStream_t s) {
+  return dispatch_pq<KronLaunch>(p, q, a, s);
+}
+
+}  // namespace iga

@@ -251,8 +251,7 @@ struct ScatterLaunch {
       const size_t shm = sizeof(double) * (6 * m * Q + Q * Q * Q + 2 * m * m * Q * Q +
                                            2 * m * m * m * m * Q);
       if (shm > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(k_sumfact_scatter<P, Q>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)shm);
+        cudaError_t e = smem_attr_once(reinterpret_cast<const void*>(k_sumfact_scatter<P, Q>), shm);
         if (e != cudaSuccess) return check_cuda(e, "sumfact smem attr");
       }
       k_sumfact_scatter<P, Q><<<(unsigned)grid, 256, shm, s>>>(a);

@@ -11,7 +11,10 @@ across them exactly as the reference guarantees.
 
 Extensions: ``strategy="device"``, ``operator``,
 ``coefficient`` (None | scalar | array [K^dim, q^dim]), ``dim`` (2 or 3),
-``devices`` and ``assembly`` ("auto" | "owner" | "scatter").
+``devices`` and ``assembly`` ("auto" | "owner" | "scatter" | "separable").
+``assembly="separable"`` (3D, scalar coefficient) integrates the 1D band
+matrices per axis and fills the CSR with their Kronecker combination
+(csrc/iga_kron.cu) -- exact for a constant coefficient, HBM-bound.
 """
 
 from __future__ import annotations
@@ -29,7 +32,7 @@ from .integrators import flop_count
 
 METHODS = ("classical", "sumfact")
 STRATEGIES = ("sequential", "over_elements", "within_element", "combined", "device")
-ASSEMBLY = ("auto", "owner", "scatter")
+ASSEMBLY = ("auto", "owner", "scatter", "separable")
 BARRIER_TIMEOUT = 300.0
 
 
@@ -103,6 +106,13 @@ def method_code(cfg: RunConfig) -> int:
         if cfg.assembly == "owner":
             raise ValueError("assembly='owner' requires method='sumfact'")
         return _lib.METHOD_CLASSICAL
+    if cfg.assembly == "separable":
+        if cfg.dim != 3:
+            raise ValueError("the separable method is 3D only")
+        c = cfg.coefficient
+        if c is not None and np.ndim(c) != 0:
+            raise ValueError("assembly='separable' needs a scalar coefficient")
+        return _lib.METHOD_SEPARABLE
     if cfg.assembly == "scatter":
         if cfg.dim != 3:
             raise ValueError("element-local sum factorization scatter is 3D only")

@@ -135,7 +135,7 @@ MASS = sorted(glob.glob(os.path.join(GOLDEN, "mass_classical_K*_p*.npz")))
 
 @pytest.mark.parametrize("path", MASS)
 @pytest.mark.parametrize("method,assembly", [("classical", "auto"), ("sumfact", "owner"),
-                                             ("sumfact", "scatter")])
+                                             ("sumfact", "scatter"), ("sumfact", "separable")])
 def test_run_integration_mass_vs_reference(pkg, path, method, assembly):
     K, p = (int(s[1:]) for s in os.path.basename(path)[:-4].split("_")[2:])
     g = np.load(path)
@@ -150,7 +150,7 @@ STIFF = sorted(glob.glob(os.path.join(GOLDEN, "stiffness*_classical_K*_p*.npz"))
 
 @pytest.mark.parametrize("path", STIFF)
 @pytest.mark.parametrize("method,assembly", [("classical", "auto"), ("sumfact", "owner"),
-                                             ("sumfact", "scatter")])
+                                             ("sumfact", "scatter"), ("sumfact", "separable")])
 def test_run_integration_stiffness_vs_reference(pkg, path, method, assembly):
     name = os.path.basename(path)[:-4]
     op = "stiffness_mass" if name.startswith("stiffness_mass") else "stiffness"
@@ -223,26 +223,27 @@ def test_assembled_sumfact_deterministic(pkg):
     assert pkg.grams_bitwise_equal(a, b)
 
 
-def test_slabs_sum_to_full(pkg):
+@pytest.mark.parametrize("method", ["assembled", "separable"])
+def test_slabs_sum_to_full(pkg, method):
     """Multi-GPU decomposition emulated on one GPU: element slabs along the slowest
     axis produce partial interface rows that add up to the single-device matrix."""
     import torch
     from paper_2207_00280_b200 import _lib
     from paper_2207_00280_b200.device import MeshProblem
 
+    code = _lib.METHOD_SUMFACT_ASSEMBLED if method == "assembled" else _lib.METHOD_SEPARABLE
     K, p = 10, 3
     N = K + p
     mp = MeshProblem(3, K, p, operator="stiffness")
     full = torch.empty(mp.nnz(), dtype=torch.float64, device="cuda")
-    mp.integrate_assemble(full, _lib.METHOD_SUMFACT_ASSEMBLED)
+    mp.integrate_assemble(full, code)
     acc = torch.zeros_like(full)
     bounds = [0, 3, 5, 10]
     for g in range(3):
         lo, hi = bounds[g], bounds[g + 1]
         phi = min(hi + p, N) if g < 2 else N
         part = torch.empty(mp.nnz(lo, phi), dtype=torch.float64, device="cuda")
-        mp.integrate_assemble(part, _lib.METHOD_SUMFACT_ASSEMBLED, el_range=(lo, hi),
-                              plane_range=(lo, phi))
+        mp.integrate_assemble(part, code, el_range=(lo, hi), plane_range=(lo, phi))
         off = mp.nnz(0, lo)
         acc[off:off + part.numel()] += part
     ip, _ = O.pattern(3, K, p)
@@ -298,6 +299,7 @@ def _sample_rows(K, p, n_rand, seed=0):
 
 @pytest.mark.parametrize("cfg", [
     dict(K=64, p=3, op="stiffness", coef=None, name="C3"),
+    dict(K=64, p=3, op="stiffness", coef=None, name="C3", assembly="separable"),
     dict(K=32, p=2, op="mass", coef="uniform", name="C2"),
 ])
 def test_full_size_sampled_rows(pkg, cfg):
@@ -310,7 +312,8 @@ def test_full_size_sampled_rows(pkg, cfg):
         coef = np.random.default_rng(42).uniform(0.5, 1.5, size=(K, K, K, q, q, q))
         coef = coef.reshape(K**3, q**3)
     res = pkg.run_integration(pkg.RunConfig("sumfact", "device", K, p, operator=op,
-                                            coefficient=coef))
+                                            coefficient=coef,
+                                            assembly=cfg.get("assembly", "auto")))
     values = res.gram.values.cpu().numpy()
     ip, _ = O.pattern(3, K, p)
     rows = _sample_rows(K, p, 40)
@@ -397,3 +400,27 @@ def test_cg_solves_gram_system(pkg):
     b = gram.matrix @ xs
     x, it = cg(gram, b, rtol=1e-12)
     assert np.linalg.norm(x - xs) <= 1e-8 * np.linalg.norm(xs)
+
+
+def test_separable_matches_assembled_all_ops(pkg):
+    """Separable (Kronecker) path vs the general assembled kernel and the oracle for
+    every operator, scalar coefficient != 1, p = 0..5, q != p+1."""
+    for op in ("mass", "stiffness", "stiffness_mass"):
+        for K, p, q in ((5, 2, 3), (4, 3, 4), (3, 4, 6), (6, 1, 2), (2, 5, 6), (4, 0, 1), (2, 3, 4)):
+            if op != "mass" and p < 1:
+                continue
+            cfg = dict(quad_points=q, operator=op, coefficient=1.7)
+            ip, _, ref = O.integrate_assemble(3, K, p, op, "classical", q=q, coef=np.full((K**3, q**3), 1.7))
+            _, _, A = O.integrate_assemble(3, K, p, op, "classical", q=q,
+                                           coef=np.full((K**3, q**3), 1.7), absolute=True)
+            v = pkg.run_integration(pkg.RunConfig("sumfact", "device", K, p, assembly="separable",
+                                                  **cfg)).gram.values.cpu().numpy()
+            assert_parity(v, ref, ip, what=f"separable {op} K={K} p={p} q={q}", absref=A)
+
+
+def test_separable_rejects_field_coefficient(pkg):
+    K, p = 3, 2
+    coef = np.ones((K**3, (p + 1)**3))
+    with pytest.raises(ValueError):
+        pkg.run_integration(pkg.RunConfig("sumfact", "device", K, p, coefficient=coef,
+                                          assembly="separable"))

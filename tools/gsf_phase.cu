@@ -8,12 +8,8 @@
 #define IGA_PHASE_TIMING 300
 #endif
 #include "../paper_2207_00280_b200/csrc/iga_gsf_p3.cu"
+#include "../paper_2207_00280_b200/csrc/iga_abi.cu"
 
-namespace iga {
-void set_error(const char*, ...) {}
-int fail_einval(const char*, ...) { return 1; }
-int check_cuda(cudaError_t e, const char* w) { if (e) { printf("%s: %s\n", w, cudaGetErrorString(e)); return 2; } return 0; }
-}
 
 int main() {
   const int K = 64, P = 3, Q = 4, M = 4;
