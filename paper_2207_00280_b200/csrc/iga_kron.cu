@@ -33,7 +33,7 @@ __device__ __forceinline__ double2 band1d(const double* V, const double* D, int 
   const int J = I + d - P;
   double m = 0.0, k = 0.0;
   const int lo = max(max(I, J) - P, max(e_lo, 0)), hi = min(min(I, J) + 1, min(e_hi, K));
-  // at most P+1 elements, unrolled and predicated: every table load is in flight at once
+  // at most P+1 elements
 #pragma unroll
   for (int t = 0; t <= P; ++t) {
     const int e = lo + t;
@@ -53,7 +53,7 @@ __device__ __forceinline__ double2 band1d(const double* V, const double* D, int 
 }
 
 #ifndef KRON_MINB
-#define KRON_MINB 3
+#define KRON_MINB 2
 #endif
 
 // threads per CTA: one per value of an interior row (NB^3, rounded to warps, <= 1024)
@@ -67,11 +67,13 @@ __host__ __device__ constexpr int kron_minb(int P) {
   return kron_nt(P) * KRON_MINB > 1536 ? 1 : KRON_MINB;
 }
 // rows per staged chunk (one TMA bulk store each)
-__host__ __device__ constexpr int kron_rows(int P) { return P <= 2 ? 16 : (P == 3 ? 8 : 4); }
-// doubles per staging buffer: a chunk of full rows plus 16-byte alignment padding
-__host__ __device__ constexpr int kron_stage(int P) {
-  return kron_rows(P) * (2 * P + 1) * (2 * P + 1) * (2 * P + 1) + 2;
+// (measured on B200: 16 rows with 2 CTAs/SM for the small meshes, where the chunk
+// count per pencil is low; 8 rows for K > 96)
+__host__ __device__ constexpr int kron_rows(int P, bool small_mesh) {
+  return P <= 2 ? 16 : (P == 3 ? (small_mesh ? 16 : 8) : 4);
 }
+// doubles per staging buffer: a chunk of full rows plus 16-byte alignment padding
+__host__ __device__ constexpr int kron_stage(int P, int G) { return G * (2 * P + 1) * (2 * P + 1) * (2 * P + 1) + 2; }
 
 __device__ __forceinline__ void bulk_store(double* g, const double* sm, int bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(g),
@@ -84,12 +86,12 @@ __device__ __forceinline__ void bulk_store(double* g, const double* sm, int byte
 // the copy engine writes whole lines whatever the row alignment (rows of NB^3
 // doubles are not 128-byte multiples; per-thread stores of them straddle lines and
 // ran at half the write bandwidth), and the store issue leaves the SM pipes.
-template <int P, int Q>
+template <int P, int Q, int G>
 __global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) {
   constexpr int NB = 2 * P + 1;
   constexpr int NT = kron_nt(P);
   constexpr int NE = (NB * NB * NB + NT - 1) / NT;  // interior values per thread and row
-  constexpr int G = kron_rows(P), SG = kron_stage(P);
+  constexpr int SG = kron_stage(P, G);
   extern __shared__ __align__(16) double2 tb[];  // [2][N][NB] (m, k): all elements, slab
   __shared__ double w[Q];
   __shared__ double2 F[NB * NB];  // pair factors of the current pencil
@@ -101,32 +103,62 @@ __global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) 
   const bool full = a.el_begin <= 0 && a.el_end >= K;
   const double2* tb0 = full ? tb : tb + N * NB;
   double* stage = reinterpret_cast<double*>(tb + 2 * N * NB);  // [2][SG]
-  // 1D tables: the basis tables are first copied (coalesced) into the staging area
-  // when they fit, so the band sums read shared memory
+  // 1D band tables.  When they fit in the staging area (small K, where this prologue
+  // is not amortised), the element integrals m_e(r,s), k_e(r,s) are formed first
+  // (one short dot product per thread) and summed per band entry over the <= P+1
+  // elements of the pair; otherwise each band entry is integrated directly from
+  // the global tables.
   constexpr int M = P + 1;
-  const int nvd = K * M * Q;
-  const bool vd_smem = 2 * nvd <= 2 * SG;
-  const double* Vs = a.V;
-  const double* Ds = a.D;
-  if (vd_smem) {
-    for (int u = tid; u < nvd; u += NT) {
-      stage[u] = __ldg(a.V + u);
-      if (stiff) stage[nvd + u] = __ldg(a.D + u);
-    }
-    Vs = stage;
-    Ds = stage + nvd;
-  }
+  const int nvd = K * M * Q, nem = K * M * M;
+  const bool small = 2 * nvd + 2 * nem <= 2 * SG;
   if (tid < Q) w[tid] = a.weights[tid];
-  __syncthreads();
-  for (int u = tid; u < (full ? 1 : 2) * N * NB; u += NT) {
-    const int v = u < N * NB ? u : u - (int)(N * NB);
-    const bool slab = u >= N * NB;
-#if defined(KRON_PROLOGUE_ONLY) && KRON_PROLOGUE_ONLY == 2
-    tb[u] = make_double2(v, slab);
-#else
-    tb[u] = band1d<P, Q>(Vs, Ds, K, w, v / NB, v % NB, slab ? a.el_begin : 0, slab ? a.el_end : K,
-                         stiff);
-#endif
+  if (small) {
+    double* Vs = stage;
+    double* Ds = stage + nvd;
+    double2* em = reinterpret_cast<double2*>(stage + 2 * nvd);  // [K][M][M] (m, k)
+    for (int u = tid; u < nvd; u += NT) {
+      Vs[u] = __ldg(a.V + u);
+      if (stiff) Ds[u] = __ldg(a.D + u);
+    }
+    __syncthreads();
+    for (int u = tid; u < nem; u += NT) {
+      const int e = u / (M * M), r = (u / M) % M, c = u % M;
+      const double* vr = Vs + (e * M + r) * Q;
+      const double* vc = Vs + (e * M + c) * Q;
+      double m = 0.0, k = 0.0;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) m += (w[q] * vr[q]) * vc[q];
+      if (stiff) {
+        const double* dr = Ds + (e * M + r) * Q;
+        const double* dc = Ds + (e * M + c) * Q;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) k += (w[q] * dr[q]) * dc[q];
+      }
+      em[u] = make_double2(m, k);
+    }
+    __syncthreads();
+    for (int u = tid; u < (full ? 1 : 2) * N * NB; u += NT) {
+      const int v = u < N * NB ? u : u - (int)(N * NB);
+      const bool slab = u >= N * NB;
+      const int I = v / NB, J = I + v % NB - P;
+      const int lo = max(max(I, J) - P, slab ? max(a.el_begin, 0) : 0);
+      const int hi = min(min(I, J) + 1, slab ? min(a.el_end, K) : K);
+      double m = 0.0, k = 0.0;
+      for (int e = lo; e < hi; ++e) {
+        const double2 x = em[(e * M + I - e) * M + J - e];
+        m += x.x;
+        k += x.y;
+      }
+      tb[u] = make_double2(m, k);
+    }
+  } else {
+    __syncthreads();
+    for (int u = tid; u < (full ? 1 : 2) * N * NB; u += NT) {
+      const int v = u < N * NB ? u : u - (int)(N * NB);
+      const bool slab = u >= N * NB;
+      tb[u] = band1d<P, Q>(a.V, a.D, K, w, v / NB, v % NB, slab ? a.el_begin : 0,
+                           slab ? a.el_end : K, stiff);
+    }
   }
   __syncthreads();
 
@@ -242,26 +274,33 @@ __global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) 
   if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
 }
 
+template <int P, int Q, int G>
+static int launch_kron_g(const KronArgs& a, cudaStream_t s) {
+  const int64_t N = (int64_t)a.K + P;
+  constexpr int NT = kron_nt(P);
+  const size_t smem = 2 * sizeof(double2) * N * (2 * P + 1) + 2 * sizeof(double) * kron_stage(P, G);
+  if (smem > 220 * 1024) {
+    set_error("separable path: 1D band tables of K=%d do not fit shared memory", a.K);
+    return IGA_EUNSUPPORTED;
+  }
+  const void* fn = reinterpret_cast<const void*>(k_kron3<P, Q, G>);
+  cudaError_t e = smem_attr_once(fn, smem, true);
+  if (e != cudaSuccess) return check_cuda(e, "kron smem attr");
+  const int per_sm = blocks_per_sm_once(fn, NT, smem), sms = sm_count();
+  const int64_t nunit = (int64_t)(a.plane_end - a.plane_begin) * N * ((N + G - 1) / G);
+  int64_t grid = (int64_t)sms * per_sm;
+  if (grid > nunit) grid = nunit;
+  if (grid <= 0) return IGA_OK;
+  k_kron3<P, Q, G><<<(unsigned)grid, NT, smem, s>>>(a);
+  return check_cuda(cudaGetLastError(), "kron launch");
+}
+
 template <int P, int Q>
 struct KronLaunch {
   static int run(const KronArgs& a, cudaStream_t s) {
-    const int64_t N = (int64_t)a.K + P;
-    constexpr int NT = kron_nt(P);
-    const size_t smem = 2 * sizeof(double2) * N * (2 * P + 1) + 2 * sizeof(double) * kron_stage(P);
-    if (smem > 220 * 1024) {
-      set_error("separable path: 1D band tables of K=%d do not fit shared memory", a.K);
-      return IGA_EUNSUPPORTED;
-    }
-    const void* fn = reinterpret_cast<const void*>(k_kron3<P, Q>);
-    cudaError_t e = smem_attr_once(fn, smem, true);
-    if (e != cudaSuccess) return check_cuda(e, "kron smem attr");
-    const int per_sm = blocks_per_sm_once(fn, NT, smem), sms = sm_count();
-    const int64_t nunit = (int64_t)(a.plane_end - a.plane_begin) * N * ((N + kron_rows(P) - 1) / kron_rows(P));
-    int64_t grid = (int64_t)sms * (per_sm > 0 ? per_sm : 1);
-    if (grid > nunit) grid = nunit;
-    if (grid <= 0) return IGA_OK;
-    k_kron3<P, Q><<<(unsigned)grid, NT, smem, s>>>(a);
-    return check_cuda(cudaGetLastError(), "kron launch");
+    constexpr int Gs = kron_rows(P, true), Gl = kron_rows(P, false);
+    if (Gs != Gl && a.K <= 96) return launch_kron_g<P, Q, Gs>(a, s);
+    return launch_kron_g<P, Q, Gl>(a, s);
   }
 };
 
