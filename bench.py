@@ -34,13 +34,17 @@ WORKLOADS = {
                desc="C2: 3D mass 32^3 p=2 q=3, per-qp coefficient U[0.5,1.5] seed 42, "
                     "assembled sum factorization"),
     "c3": dict(dim=3, K=64, p=3, op="stiffness", coef=None, method="sumfact",
-               desc="C3: 3D Laplace stiffness 64^3 p=3 q=4 c=1, assembled sum factorization "
-                    "(general per-qp-coefficient kernel) fused with CSR assembly"),
+               desc="C3: 3D Laplace stiffness 64^3 p=3 q=4 c=1, sum factorization fused with "
+                    "CSR assembly; run_integration's default path for a constant coefficient "
+                    "(separable: per-axis 1D Gauss quadrature + Kronecker CSR fill); the "
+                    "general per-quadrature-point DMMA kernel on the same matrix is "
+                    "reported in other_kernel"),
     "c4": dict(dim=3, K=96, p=4, op="stiffness_mass", coef="sines", method="sumfact",
                desc="C4: 3D stiffness+mass 96^3 p=4 q=5, smooth 8-mode sine coefficient, "
                     "assembled sum factorization"),
     "c5": dict(dim=3, K=256, p=3, op="stiffness", coef=None, method="sumfact",
-               desc="C5: 3D Laplace stiffness 256^3 p=3 q=4 c=1, z-slabs + NCCL interface rows"),
+               desc="C5: 3D Laplace stiffness 256^3 p=3 q=4 c=1, z-slabs + NCCL interface rows "
+                    "(default path: separable)"),
 }
 
 
@@ -196,17 +200,57 @@ def run_reference(args, wl, K, p, rank):
     }), flush=True)
 
 
-def separable_leg(cfg, args, flush, stream, total_el, peaks):
-    """Same workload through assembly="separable" (scalar coefficient: 1D band
-    matrices integrated per axis + Kronecker CSR fill, csrc/iga_kron.cu): a second,
-    HBM-bound kernel for the constant-coefficient configs, timed like the headline."""
+KERNEL_NAMES = {0: "k_classical_scatter (Algorithm 1 + fused CSR scatter)",
+                1: "k_sumfact_scatter (element-local sum factorization + atomic scatter)",
+                2: "k_gsf3 (assembled sum factorization on DMMA + CSR write)",
+                3: "k_kron3 (1D band quadrature + Kronecker CSR fill, TMA bulk stores)"}
+
+
+def kernel_roofline(code, wl, K, p, q, k_el, by, kern_ms, peaks):
+    """Roofline of one launch of the dominant kernel: algorithmic flops / bytes of
+    the launch (perfmodel.py) over its CUDA-event time."""
+    from paper_2207_00280_b200 import perfmodel
+
+    if code == 3:
+        fl = perfmodel.separable_flops(wl["op"], K, p, q) * k_el / K**3
+    elif code == 2:
+        fl = perfmodel.assembled_flops(wl["op"], K, p, q) * k_el / K**3
+    else:
+        fl = None
+    t_f = fl / (peaks["fp64_tflops"] * 1e12) if fl else 0.0
+    t_b = by / (peaks["hbm_gbs"] * 1e9)
+    if t_f >= t_b:
+        achieved = fl / (kern_ms / 1e3) / 1e12
+        roof = {"bound": "fp64", "achieved": achieved, "peak": peaks["fp64_tflops"],
+                "unit": "TFLOP/s", "frac": achieved / peaks["fp64_tflops"]}
+    else:
+        achieved = by / (kern_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / peaks["hbm_gbs"]}
+    name = KERNEL_NAMES[code]
+    if code == 2 and p == 3 and q == 4:
+        name = name.replace("k_gsf3", "k_gsf3_p3")
+    roof.update({
+        "kernel": name, "kernel_ms": kern_ms, "alg_flops": fl, "alg_bytes": by,
+        "t_fp64_ms": t_f * 1e3, "t_hbm_ms": t_b * 1e3,
+        "hbm_frac": (by / (kern_ms / 1e3) / 1e9) / peaks["hbm_gbs"],
+        "fp64_frac": ((fl / (kern_ms / 1e3) / 1e12) / peaks["fp64_tflops"]) if fl else None,
+        "peak_src": peaks["src"], "traffic": None,
+    })
+    return roof
+
+
+def alt_leg(cfg, assembly, args, flush, stream, wl, total_el, peaks):
+    """The same workload through the other 3D kernel (assembly="owner": assembled DMMA
+    sum factorization, the general per-quadrature-point-coefficient path; or
+    "separable"), timed like the headline, with its own roofline."""
     import dataclasses
 
     import torch
 
     from paper_2207_00280_b200.runtime import DeviceSession
 
-    sess = DeviceSession(dataclasses.replace(cfg, assembly="separable"))
+    sess = DeviceSession(dataclasses.replace(cfg, assembly=assembly))
     for _ in range(args.warmup):
         sess.step()
         flush.fill_(1.0)
@@ -230,15 +274,10 @@ def separable_leg(cfg, args, flush, stream, total_el, peaks):
     torch.cuda.synchronize()
     ms = float(np.mean([a.elapsed_time(b) for a, b in ev]))
     kms = float(np.mean([a.elapsed_time(b) for a, b in kev]))
-    by = 8 * sess.values.numel()
-    ach = by / (kms / 1e3) / 1e9
-    out = {"value": total_el / (ms / 1e3), "unit": "elements/s", "ms_per_step": ms,
-           "gpu_launches": 2 * args.steps,
-           "roofline": {"bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                        "frac": ach / peaks["hbm_gbs"], "kernel": "k_kron3 (1D band quadrature "
-                        "+ Kronecker CSR fill)", "kernel_ms": kms, "alg_bytes": by},
-           "what": "assembly='separable': exact for a scalar coefficient; the 3D Gauss "
-                   "quadrature factorises into per-axis 1D integrals (DESIGN.md 4.2)"}
+    K, p = wl["K"], wl["p"]
+    roof = kernel_roofline(sess.code, wl, K, p, p + 1, K**3, 8 * sess.values.numel(), kms, peaks)
+    out = {"assembly": assembly, "value": total_el / (ms / 1e3), "unit": "elements/s",
+           "ms_per_step": ms, "gpu_launches": 2 * args.steps, "roofline": roof}
     del sess
     return out
 
@@ -252,7 +291,9 @@ def main():
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-separable", action="store_true")
+    ap.add_argument("--no-alt", action="store_true")
+    ap.add_argument("--assembly", default="auto", help="force a kernel path (RunConfig.assembly)")
+    ap.add_argument("--method", default=None, help="override the workload's method")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -281,8 +322,8 @@ def main():
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     coef = coefficient(wl["coef"], K, p, wl["dim"])
-    cfg = P.RunConfig(wl["method"], "device", K, p, operator=wl["op"], coefficient=coef,
-                      dim=wl["dim"], devices=world)
+    cfg = P.RunConfig(args.method or wl["method"], "device", K, p, operator=wl["op"],
+                      coefficient=coef, dim=wl["dim"], devices=world, assembly=args.assembly)
     stream = torch.cuda.current_stream()
 
     if world > 1:
@@ -358,29 +399,9 @@ def main():
         k_el = n_el
         k_planes = K + p
     # algorithmic work of this kernel launch (rank-local rows / elements)
-    fl = perfmodel.assembled_flops(wl["op"], K, p, q) * k_el / K**3 if wl["method"] == "sumfact" \
-        else None
     by = 8 * sess.prob.nnz(plan.own_lo, plan.own_hi) if world > 1 else \
         perfmodel.algorithmic_bytes(wl["dim"], K, p, q, coef is not None)
-    t_f = fl / (peaks["fp64_tflops"] * 1e12) if fl else 0.0
-    t_b = by / (peaks["hbm_gbs"] * 1e9)
-    if t_f >= t_b:
-        achieved = fl / (kern_ms / 1e3) / 1e12
-        roof = {"bound": "fp64", "achieved": achieved, "peak": peaks["fp64_tflops"],
-                "unit": "TFLOP/s", "frac": achieved / peaks["fp64_tflops"]}
-    else:
-        achieved = by / (kern_ms / 1e3) / 1e9
-        roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": achieved / peaks["hbm_gbs"]}
-    roof.update({
-        "kernel": "k_gsf3 (assembled sum factorization + CSR write)" if wl["method"] == "sumfact"
-        else "k_classical_scatter",
-        "kernel_ms": kern_ms, "alg_flops": fl, "alg_bytes": by,
-        "t_fp64_ms": t_f * 1e3, "t_hbm_ms": t_b * 1e3,
-        "hbm_frac": (by / (kern_ms / 1e3) / 1e9) / peaks["hbm_gbs"],
-        "fp64_frac": ((fl / (kern_ms / 1e3) / 1e12) / peaks["fp64_tflops"]) if fl else None,
-        "peak_src": peaks["src"], "traffic": None,
-    })
+    roof = kernel_roofline(sess.code, wl, K, p, q, k_el, by, kern_ms, peaks)
     prof = os.path.join(ROOT, "profiles", f"ncu_{wname}_traffic.json")
     if os.path.exists(prof):
         roof["traffic"] = json.load(open(prof)).get("dram_bytes_per_launch")
@@ -407,9 +428,11 @@ def main():
                "ms_per_step": e_ms, "wall_ms_per_step": wall * 1e3,
                "api": "paper_2207_00280_b200.runtime.DeviceSession.step_host (pinned host out)"}
 
-    sep = None
-    if world == 1 and wl["dim"] == 3 and coef is None and not args.no_separable:
-        sep = separable_leg(cfg, args, flush, stream, total_el, peaks)
+    # constant-coefficient 3D workloads: the other kernel for the same matrix
+    other = None
+    if world == 1 and wl["dim"] == 3 and coef is None and not args.no_alt:
+        other = alt_leg(cfg, "owner" if sess.code == 3 else "separable", args, flush, stream, wl,
+                        total_el, peaks)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -430,11 +453,12 @@ def main():
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded; no dataset)",
             "config": {"workload": wl["desc"], "K": K, "p": p, "q": q, "dim": wl["dim"],
                        "operator": wl["op"], "method": wl["method"],
+                       "kernel_path": KERNEL_NAMES[sess.code],
                        "nnz": P.device.csr_nnz(wl["dim"], K, p),
                        "parallelism": f"element slabs x{world}" if world > 1 else "1 GPU",
                        "l2": "256 MB buffer written between timed steps (outside the per-step "
                              "events); each step also writes the whole CSR (> 126 MB L2)"},
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "separable_path": sep,
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "other_kernel": other,
             "gpu_launches": launches * args.steps, "clocks": clk.summary(),
             "region_ms": region0.elapsed_time(region1),
         }

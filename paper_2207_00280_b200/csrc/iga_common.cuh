@@ -66,10 +66,18 @@ __device__ __forceinline__ double order0(int i, double x, int K, int p) {
 // splines.py:139-161.
 template <int P>
 __device__ __forceinline__ void cox_de_boor(int e, double x, int K, double* vals, double* ders) {
-  // level-0 indices e .. e+2P  (2P+1 values); level r needs e .. e+2P-r
+  // the 2P+2 knots t_e .. t_{e+2P+1} this point touches, each divided once
+  double kn[2 * P + 2];
+#pragma unroll
+  for (int j = 0; j <= 2 * P + 1; ++j) kn[j] = knot(e + j, K, P);
+  // level-0 indices e .. e+2P  (2P+1 values); level r needs e .. e+2P-r.
+  // order0 (splines.py:78-91) with the closed last span: the last knot is 1.0
   double N[2 * P + 1];
 #pragma unroll
-  for (int j = 0; j <= 2 * P; ++j) N[j] = order0(e + j, x, K, P);
+  for (int j = 0; j <= 2 * P; ++j) {
+    const double ti = kn[j], ti1 = kn[j + 1];
+    N[j] = (ti <= x && x < ti1) || (x == 1.0 && ti < ti1 && ti1 == 1.0) ? 1.0 : 0.0;
+  }
   double Nprev[2 * P + 1];  // level P-1 values, for derivatives
 #pragma unroll
   for (int j = 0; j <= 2 * P; ++j) Nprev[j] = N[j];
@@ -77,10 +85,9 @@ __device__ __forceinline__ void cox_de_boor(int e, double x, int K, double* vals
   for (int q = 1; q <= P; ++q) {
 #pragma unroll
     for (int j = 0; j <= 2 * P - q; ++j) {
-      const int i = e + j;
       double out = 0.0;
-      const double ti = knot(i, K, P), tiq = knot(i + q, K, P);
-      const double ti1 = knot(i + 1, K, P), tiq1 = knot(i + q + 1, K, P);
+      const double ti = kn[j], tiq = kn[j + q];
+      const double ti1 = kn[j + 1], tiq1 = kn[j + q + 1];
       const double d_left = sub(tiq, ti);
       if (d_left > 0.0) out = add(out, mul(dvd(sub(x, ti), d_left), N[j]));
       const double d_right = sub(tiq1, ti1);
@@ -100,11 +107,10 @@ __device__ __forceinline__ void cox_de_boor(int e, double x, int K, double* vals
     } else {
 #pragma unroll
       for (int r = 0; r <= P; ++r) {
-        const int i = e + r;
         double d = 0.0;
-        const double d_left = sub(knot(i + P, K, P), knot(i, K, P));
+        const double d_left = sub(kn[r + P], kn[r]);
         if (d_left > 0.0) d = add(d, dvd(Nprev[r], d_left));
-        const double d_right = sub(knot(i + P + 1, K, P), knot(i + 1, K, P));
+        const double d_right = sub(kn[r + P + 1], kn[r + 1]);
         if (d_right > 0.0) d = sub(d, dvd(Nprev[r + 1], d_right));
         ders[r] = mul((double)P, d);
       }

@@ -12,6 +12,11 @@ with nnz1 = (K+p)(2p+1) - p(p+1) the 1D band pairs.  Each 1D band pair
 (I, J) overlaps sum_e = K (p+1)^2 element-local pairs in total, which is
 where the K (p+1)^2 factors come from.
 
+Separable path (iga_kron.cu, scalar coefficient): the 1D element integrals
+(types x K (p+1)^2 q MACs per axis, computed once) and per CSR value one
+multiply and one FMA (stiffness; mass: one multiply) -- a few flops per 8-byte
+value written, so the HBM write of the values binds.
+
 Bytes: 8 nnz written (each CSR value exactly once) + 8 K^3 q^3 read when a
 per-quadrature-point coefficient field is given.
 """
@@ -35,6 +40,13 @@ def assembled_macs(op: str, K: int, p: int, q: int) -> int:
 
 def assembled_flops(op: str, K: int, p: int, q: int) -> int:
     return 2 * assembled_macs(op, K, p, q)
+
+
+def separable_flops(op: str, K: int, p: int, q: int) -> int:
+    n1 = nnz1(K, p)
+    types = 1 if op == "mass" else 2
+    per_value = 1 if op == "mass" else 3
+    return 2 * types * K * (p + 1) ** 2 * q + per_value * n1**3
 
 
 def element_sumfact_flops(op: str, p: int, q: int) -> int:

@@ -14,7 +14,9 @@ Extensions: ``strategy="device"``, ``operator``,
 ``devices`` and ``assembly`` ("auto" | "owner" | "scatter" | "separable").
 ``assembly="separable"`` (3D, scalar coefficient) integrates the 1D band
 matrices per axis and fills the CSR with their Kronecker combination
-(csrc/iga_kron.cu) -- exact for a constant coefficient, HBM-bound.
+(csrc/iga_kron.cu) -- exact for a constant coefficient, HBM-bound; "auto"
+selects it for scalar coefficients and the assembled DMMA sum factorization
+(csrc/iga_gsf_p3.cu, iga_gsf.cu) for coefficient fields.
 """
 
 from __future__ import annotations
@@ -99,9 +101,19 @@ def grams_bitwise_equal(a: GlobalGram, b: GlobalGram) -> bool:
             and ma.data.tobytes() == mb.data.tobytes())
 
 
+def separable_fits(K: int, p: int) -> bool:
+    """Shared-memory budget of k_kron3 (csrc/iga_kron.cu: 1D band tables + two
+    staging chunks)."""
+    nb = 2 * p + 1
+    rows = 16 if p <= 2 else ((16 if K <= 96 else 8) if p == 3 else 4)
+    return 2 * 16 * (K + p) * nb + 16 * (rows * nb**3 + 2) <= 220 * 1024
+
+
 def method_code(cfg: RunConfig) -> int:
     """Kernel selection: classical -> Algorithm 1 + fused scatter; sumfact ->
-    assembled (row-owner) sum factorization unless assembly="scatter"."""
+    "auto": the separable (Kronecker) path for a scalar coefficient in 3D (exact
+    factorisation of the quadrature, HBM-bound), else assembled (row-owner) sum
+    factorization; "owner" / "scatter" / "separable" force a kernel."""
     if cfg.method == "classical":
         if cfg.assembly == "owner":
             raise ValueError("assembly='owner' requires method='sumfact'")
@@ -120,6 +132,10 @@ def method_code(cfg: RunConfig) -> int:
     if cfg.dim != 3:
         raise ValueError("assembled sum factorization is 3D only; use method='classical' "
                          "for dim=2")
+    c = cfg.coefficient
+    if (cfg.assembly == "auto" and (c is None or np.ndim(c) == 0)
+            and separable_fits(cfg.mesh, cfg.degree)):
+        return _lib.METHOD_SEPARABLE
     return _lib.METHOD_SUMFACT_ASSEMBLED
 
 

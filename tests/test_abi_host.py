@@ -145,3 +145,20 @@ def test_device_path_fails_loudly_without_cuda():
         pytest.skip("CUDA present")
     with pytest.raises(RuntimeError, match="CUDA device"):
         P.run_integration(P.RunConfig("sumfact", "device", 2, 1))
+
+
+def test_auto_selects_kernel():
+    import paper_2207_00280_b200 as pkg
+
+    from paper_2207_00280_b200 import _lib
+    from paper_2207_00280_b200.runtime import method_code
+
+    K, p = 4, 3
+    assert method_code(pkg.RunConfig("sumfact", "device", K, p)) == _lib.METHOD_SEPARABLE
+    assert method_code(pkg.RunConfig("sumfact", "device", K, p, coefficient=2.0)) == \
+        _lib.METHOD_SEPARABLE
+    coef = np.ones((K**3, (p + 1)**3))
+    assert method_code(pkg.RunConfig("sumfact", "device", K, p, coefficient=coef)) == \
+        _lib.METHOD_SUMFACT_ASSEMBLED
+    assert method_code(pkg.RunConfig("sumfact", "device", K, p, assembly="owner")) == \
+        _lib.METHOD_SUMFACT_ASSEMBLED

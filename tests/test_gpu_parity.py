@@ -216,11 +216,14 @@ def test_reference_strategies_accepted(pkg):
         assert pkg.grams_bitwise_equal(grams[0], g2)
 
 
-def test_assembled_sumfact_deterministic(pkg):
-    cfg = pkg.RunConfig("sumfact", "device", 12, 3, operator="stiffness", repetitions=2)
+@pytest.mark.parametrize("assembly", ["owner", "separable"])
+def test_assembled_sumfact_deterministic(pkg, assembly):
+    cfg = pkg.RunConfig("sumfact", "device", 12, 3, operator="stiffness", repetitions=2,
+                        assembly=assembly)
     a = pkg.run_integration(cfg).gram
     b = pkg.run_integration(cfg).gram
     assert pkg.grams_bitwise_equal(a, b)
+
 
 
 @pytest.mark.parametrize("method", ["assembled", "separable"])
@@ -298,7 +301,7 @@ def _sample_rows(K, p, n_rand, seed=0):
 
 
 @pytest.mark.parametrize("cfg", [
-    dict(K=64, p=3, op="stiffness", coef=None, name="C3"),
+    dict(K=64, p=3, op="stiffness", coef=None, name="C3", assembly="owner"),
     dict(K=64, p=3, op="stiffness", coef=None, name="C3", assembly="separable"),
     dict(K=32, p=2, op="mass", coef="uniform", name="C2"),
 ])
