@@ -81,17 +81,24 @@ __device__ __forceinline__ void cox_de_boor(int e, double x, int K, double* vals
   double Nprev[2 * P + 1];  // level P-1 values, for derivatives
 #pragma unroll
   for (int j = 0; j <= 2 * P; ++j) Nprev[j] = N[j];
+  // the triangle's divisions depend only on x and the knots: all of them are issued
+  // before the level recursion (independent, so their latencies overlap)
+  double cl[P + 1][2 * P + 1], cr[P + 1][2 * P + 1];
+#pragma unroll
+  for (int q = 1; q <= P; ++q)
+#pragma unroll
+    for (int j = 0; j <= 2 * P - q; ++j) {
+      const double d_left = sub(kn[j + q], kn[j]), d_right = sub(kn[j + q + 1], kn[j + 1]);
+      cl[q][j] = d_left > 0.0 ? dvd(sub(x, kn[j]), d_left) : 0.0;
+      cr[q][j] = d_right > 0.0 ? dvd(sub(kn[j + q + 1], x), d_right) : 0.0;
+    }
 #pragma unroll
   for (int q = 1; q <= P; ++q) {
 #pragma unroll
     for (int j = 0; j <= 2 * P - q; ++j) {
       double out = 0.0;
-      const double ti = kn[j], tiq = kn[j + q];
-      const double ti1 = kn[j + 1], tiq1 = kn[j + q + 1];
-      const double d_left = sub(tiq, ti);
-      if (d_left > 0.0) out = add(out, mul(dvd(sub(x, ti), d_left), N[j]));
-      const double d_right = sub(tiq1, ti1);
-      if (d_right > 0.0) out = add(out, mul(dvd(sub(tiq1, x), d_right), N[j + 1]));
+      if (sub(kn[j + q], kn[j]) > 0.0) out = add(out, mul(cl[q][j], N[j]));
+      if (sub(kn[j + q + 1], kn[j + 1]) > 0.0) out = add(out, mul(cr[q][j], N[j + 1]));
       N[j] = out;
     }
     if (q == P - 1) {
