@@ -209,18 +209,22 @@ __global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) 
     }
     const int64_t pc0 = u_lo - pen * nch, pc1 = u_hi - pen * nch;
     const int ch0 = pc0 > 0 ? (int)pc0 : 0, ch1 = pc1 < nch ? (int)pc1 : nch;
+    // value offset of row R0 inside the pencil (int: a pencil holds < 2^31 values);
+    // full-band chunks advance it without the band_prefix arithmetic
+    int off0 = c01 * (int)band_prefix(ch0 * G, P, N);
     for (int R0 = ch0 * G; R0 < ch1 * G; R0 += G, ++chunk) {
       const int R1 = min((int)N, R0 + G);
-      const int64_t off0 = (int64_t)c01 * band_prefix(R0, P, N);
-      const int len = (int)((int64_t)c01 * band_prefix(R1, P, N) - off0);
+      const bool fast = R0 >= P && R0 + G <= K;
+      const int len = fast ? G * ncnt : c01 * (int)(band_prefix(R1, P, N) - band_prefix(R0, P, N));
       double* g = vals + off0;
+      off0 += len;
       const int pad = (int)((reinterpret_cast<uintptr_t>(g) >> 3) & 1);
       double* buf = stage + (chunk & 1) * SG;
       // the bulk store issued from this buffer two chunks ago has finished reading it
       if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
       __syncthreads();
       double* sb = buf + pad;
-      if (R0 >= P && R0 + G <= K) {
+      if (fast) {
         // G full-band rows: fixed (pair, d2) per thread, rows ncnt apart
         const double2* t2 = tb + R0 * NB;
 #pragma unroll
@@ -249,7 +253,7 @@ __global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) 
             loc += ncnt;
           } else {  // truncated band: b = e / c2 by a reciprocal (exact for e < 2^20 / NB)
             const int c2 = (int)band_cnt(I2, P, N), lod2 = max(0, P - I2);
-            const unsigned inv = (1u << 20) / (unsigned)c2 + 1u;
+            const unsigned inv = (1u << 20) / (unsigned)c2 + 1u;  // c2 <= NB: a few rows/pencil
             for (int e = tid; e < c01 * c2; e += NT) {
               const int b = (int)(((unsigned)e * inv) >> 20);
               const double2 f = F[b], x2 = t2[lod2 + e - b * c2];

@@ -61,6 +61,8 @@ keys = [
     "launch__registers_per_thread", "launch__block_size", "launch__grid_size",
     "launch__shared_mem_per_block_dynamic", "sm__warps_active.avg.pct_of_peak_sustained_active",
     "gpu__compute_memory_throughput.avg.pct_of_peak_sustained_elapsed",
+    "dram__throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_sectors_op_write.sum",
+    "l1tex__t_sectors_pipe_lsu_mem_global_op_st.sum",
 ]
 lines = [f"# ncu --set full --clock-control none capture ({os.path.basename(rep)})"]
 for k in keys:
