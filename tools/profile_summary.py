@@ -75,7 +75,8 @@ tot_s = sum(v for _, v in stalls) or 1.0
 lines.append("# warp stall sampling (share of samples)")
 for h, v in sorted(stalls, key=lambda x: -x[1])[:10]:
     lines.append(f"  {h.replace('smsp__pcsamp_warps_issue_stalled_', ''):35s} {v / tot_s * 100:5.1f}%")
-kname = get.get("Kernel Name", ("kernel", ""))[0].split("(")[0].split("::")[-1].replace("<", "_").replace(">", "")
+kname = get.get("Kernel Name", ("kernel", ""))[0].split("(")[0].split("::")[-1].replace("void ", "")
+kname = kname.replace("<", "_").replace(">", "").replace(", ", "_").replace(" ", "")
 path = os.path.join(out_dir, f"{tag}_{kname}_ncu.txt")
 open(path, "w").write("\n".join(lines) + "\n")
 print("\n".join(lines))
