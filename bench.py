@@ -228,7 +228,9 @@ def kernel_roofline(code, wl, K, p, q, k_el, by, kern_ms, peaks):
         roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / peaks["hbm_gbs"]}
     name = KERNEL_NAMES[code]
-    if code == 2 and p == 3 and q == 4:
+    if code == 2 and not (p == 3 and q == 4):
+        name = f"k_gsf3<{p},{q}> (assembled sum factorization, scalar FP64 + CSR write)"
+    elif code == 2:
         name = name.replace("k_gsf3", "k_gsf3_p3")
     roof.update({
         "kernel": name, "kernel_ms": kern_ms, "alg_flops": fl, "alg_bytes": by,
@@ -237,6 +239,15 @@ def kernel_roofline(code, wl, K, p, q, k_el, by, kern_ms, peaks):
         "fp64_frac": ((fl / (kern_ms / 1e3) / 1e12) / peaks["fp64_tflops"]) if fl else None,
         "peak_src": peaks["src"], "traffic": None,
     })
+    if code in (1, 2) and wl["dim"] == 3:
+        # SURVEY.md 8(d) yardstick: elements/s against the roofline of general element-local
+        # sum factorization (its minimal flop count per element)
+        f_el = perfmodel.element_sumfact_flops(wl["op"], p, q)
+        el_roof = 1.0 / max(f_el / (peaks["fp64_tflops"] * 1e12),
+                            (by / k_el) / (peaks["hbm_gbs"] * 1e9))
+        roof["survey_sumfact_flops_per_el"] = f_el
+        roof["survey_roofline_el_s"] = el_roof
+        roof["frac_of_survey_roofline"] = (k_el / (kern_ms / 1e3)) / el_roof
     return roof
 
 

@@ -132,6 +132,18 @@ int32_t iga_apply(const iga_problem* prob, double alpha, double beta, const doub
 /* y[i] += x[i], i < n  (interface-row accumulation after the NCCL receive). */
 int32_t iga_axpy(int64_t n, const double* x, double* y, void* stream);
 
+/* Matrix Market export (assembly.write_matrix_market, assembly.py:118-120 =
+ * scipy.io.mmwrite(path, coo, symmetry="symmetric")): the lower triangle of the
+ * structured CSR whose values are given, byte-identical to scipy 1.18's output.
+ * The device version streams row blocks to the host (two pinned staging buffers
+ * it allocates and frees, one cudaMemcpyAsync per block on `stream`) and formats
+ * them with `threads` host threads while the next block is in flight; it returns
+ * after the file is closed.  The _host version takes host values and needs no GPU. */
+int32_t iga_write_matrix_market(int32_t dim, int32_t K, int32_t p, const double* values,
+                                const char* path, int32_t threads, void* stream);
+int32_t iga_write_matrix_market_host(int32_t dim, int32_t K, int32_t p, const double* values,
+                                     const char* path, int32_t threads);
+
 /* CSR SpMV y = A x over the structured pattern (assembly.spmv, assembly.py:86-91). */
 int32_t iga_spmv(int32_t dim, int32_t K, int32_t p, const double* values, const double* x,
                  double* y, void* stream);

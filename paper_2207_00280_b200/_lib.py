@@ -35,6 +35,8 @@ EXPORTS = (
     "iga_axpy",
     "iga_spmv",
     "iga_apply",
+    "iga_write_matrix_market",
+    "iga_write_matrix_market_host",
 )
 
 
@@ -92,9 +94,11 @@ def load():
     L.iga_axpy.argtypes = [i64, vp, vp, vp]
     L.iga_spmv.argtypes = [i32, i32, i32, vp, vp, vp, vp]
     L.iga_apply.argtypes = [ctypes.POINTER(IgaProblem), dp, dp, vp, vp, vp]
+    L.iga_write_matrix_market.argtypes = [i32, i32, i32, vp, ctypes.c_char_p, i32, vp]
+    L.iga_write_matrix_market_host.argtypes = [i32, i32, i32, vp, ctypes.c_char_p, i32]
     for name in ("iga_mesh_tables", "iga_basis_eval", "iga_csr_pattern", "iga_element_matrices",
                  "iga_integrate_assemble", "iga_assemble_elements", "iga_axpy", "iga_spmv",
-                 "iga_apply"):
+                 "iga_apply", "iga_write_matrix_market", "iga_write_matrix_market_host"):
         getattr(L, name).restype = i32
     if L.iga_abi_version() != 1:
         raise ImportError("libiga_b200.so ABI version mismatch")

@@ -138,7 +138,29 @@ def symbolic_pattern(K: int, p: int):
     return pat
 
 
-def write_matrix_market(gram: GlobalGram, path) -> None:
-    import scipy.io
+def write_matrix_market(gram: GlobalGram, path, threads: int | None = None) -> None:
+    """Symmetric Matrix Market coordinate file (assembly.py:118-120), byte-identical to
+    ``scipy.io.mmwrite(path, gram.matrix.tocoo(), symmetry="symmetric")``.
 
-    scipy.io.mmwrite(path, gram.matrix.tocoo(), symmetry="symmetric")
+    Device-resident values stream to the host in row blocks through the native writer
+    (csrc/iga_mmio.cu: double-buffered copies, multi-threaded formatting); a gram that
+    only has a host CSR is written by the same formatter from host memory."""
+    import os
+
+    L = _lib.load()
+    path = os.fspath(path)
+    nthr = int(threads or os.cpu_count() or 1)
+    if gram.values is not None:
+        torch = _lib.require_cuda()
+        vals = gram.values.contiguous()
+        _lib.check(L.iga_write_matrix_market(gram.dim, gram.K, gram.p, _lib.ptr(vals),
+                                             path.encode(), nthr, _lib.stream_ptr()))
+        del torch
+        return
+    m = gram.matrix
+    indptr, indices = host_pattern(gram.dim, gram.K, gram.p)
+    if not (np.array_equal(m.indptr, indptr) and np.array_equal(m.indices, indices)):
+        raise ValueError("matrix does not have the structured IGA pattern")
+    data = np.ascontiguousarray(m.data, dtype=np.float64)
+    _lib.check(L.iga_write_matrix_market_host(gram.dim, gram.K, gram.p, data.ctypes.data,
+                                              path.encode(), nthr))

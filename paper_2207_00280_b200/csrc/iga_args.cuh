@@ -35,8 +35,8 @@ struct GsfArgs {
   int K, op;
   int el_begin, el_end;          // element slab along axis 0
   int plane_begin, plane_end;    // row planes I0 computed
-  int own_begin;                 // first plane whose own rows are written (symmetric kernel)
-  int mirror_end;                // mirrored (lower-triangle) writes go to planes < mirror_end
+  int segs;                      // segments of the element column e2 per tile (>= 1)
+  int seg_len;                   // elements per segment
   int tiles1;                    // tiles along axis 1
   int64_t base;                  // rowptr of (plane_begin, 0, 0)
   double jac, coef_scalar;

@@ -53,7 +53,7 @@ struct GsfShape {
 };
 
 template <int P, int Q, int TA, int TB>
-__global__ void __launch_bounds__(512) k_gsf3(GsfArgs a) {
+__global__ void __launch_bounds__(512, 2) k_gsf3(GsfArgs a) {
   using S = GsfShape<P, Q, TA, TB>;
   constexpr int m = S::m, NB = S::NB, GB = S::GB;
   extern __shared__ double smem[];
@@ -69,11 +69,17 @@ __global__ void __launch_bounds__(512) k_gsf3(GsfArgs a) {
   double* R = Y1 + S::nY;
   double* Z0 = R + S::nR;
   double* Z1 = Z0 + S::nZ;
+  __shared__ int64_t rowoff[TA * TB];
 
   const int K = a.K;
   const int64_t N = (int64_t)K + P;
-  const int tile0 = blockIdx.x / a.tiles1, tile1 = blockIdx.x % a.tiles1;
+  const int tile = blockIdx.x / a.segs, seg = blockIdx.x % a.segs;
+  const int tile0 = tile / a.tiles1, tile1 = tile % a.tiles1;
   const int i00 = a.plane_begin + tile0 * TA;  // first row plane of the tile (axis 0)
+  // element-column segment: rows I2 in [s0, s1) are written by this CTA, which streams
+  // the elements [s0 - P, s1) that contribute to them (the first P recomputed as halo)
+  const int s0 = seg * a.seg_len, s1 = min(K, s0 + a.seg_len);
+  const int e_first = max(0, s0 - P);
   const int i10 = tile1 * TB;                  // first row index along axis 1
   const int tid = threadIdx.x, nt = blockDim.x;
   const bool stiff = a.op != IGA_OP_MASS;
@@ -94,24 +100,42 @@ __global__ void __launch_bounds__(512) k_gsf3(GsfArgs a) {
   }
   for (int t = tid; t < S::nR; t += nt) R[t] = 0.0;
 
-  for (int e2 = 0; e2 < K; ++e2) {
+  // coefficient of element column e2 for this thread's W entries (loaded one column
+  // ahead, so the global-memory latency overlaps the previous column's stages)
+  constexpr int WPT = (S::nW + 511) / 512;
+  auto load_coef = [&](int e2, double (&cv)[WPT]) {
+#pragma unroll
+    for (int i = 0; i < WPT; ++i) {
+      const int t = tid + i * nt;
+      cv[i] = a.coef_scalar;
+      if (a.coef && t < S::nW && e2 < K) {
+        const int k2 = t % Q, g1 = (t / Q) % GB, g0 = t / (Q * GB);
+        const int la = g0 / Q, k0 = g0 % Q, lb = g1 / Q, k1 = g1 % Q;
+        const int e0 = i00 - P + la, e1 = i10 - P + lb;
+        if (e0 >= e0lo && e0 < e0hi && e1 >= 0 && e1 < K)
+          cv[i] = __ldg(a.coef + (((int64_t)e0 * K + e1) * K + e2) * (Q * Q * Q) + (k0 * Q + k1) * Q + k2);
+      }
+    }
+  };
+  double cv[WPT];
+  load_coef(e_first, cv);
+  for (int e2 = e_first; e2 < s1; ++e2) {
     __syncthreads();
     // ---- stage W: weights x coefficient on the (axis0, axis1) slab of element column e2
-    for (int t = tid; t < S::nW; t += nt) {
-      const int k2 = t % Q;
-      const int g1 = (t / Q) % GB;
-      const int g0 = t / (Q * GB);
-      const int la = g0 / Q, k0 = g0 % Q, lb = g1 / Q, k1 = g1 % Q;
-      const int e0 = i00 - P + la, e1 = i10 - P + lb;
-      double W = 0.0;
-      if (e0 >= e0lo && e0 < e0hi && e1 >= 0 && e1 < K) {
-        const double c = a.coef ? a.coef[(((int64_t)e0 * K + e1) * K + e2) * (Q * Q * Q) +
-                                         (k0 * Q + k1) * Q + k2]
-                                : a.coef_scalar;
-        W = a.weights[k0] * a.weights[k1] * a.weights[k2] * a.jac * c;
+#pragma unroll
+    for (int i = 0; i < WPT; ++i) {
+      const int t = tid + i * nt;
+      if (t < S::nW) {
+        const int k2 = t % Q, g1 = (t / Q) % GB, g0 = t / (Q * GB);
+        const int la = g0 / Q, k0 = g0 % Q, lb = g1 / Q, k1 = g1 % Q;
+        const int e0 = i00 - P + la, e1 = i10 - P + lb;
+        double W = 0.0;
+        if (e0 >= e0lo && e0 < e0hi && e1 >= 0 && e1 < K)
+          W = a.weights[k0] * a.weights[k1] * a.weights[k2] * a.jac * cv[i];
+        sW[t] = W;
       }
-      sW[t] = W;
     }
+    load_coef(e2 + 1, cv);
     // pair tables of axis 2 for element e2: Z0 = VV, Z1 = DD (+VV)
     for (int t = tid; t < S::nZ; t += nt) {
       const int k = t % Q, s = (t / Q) % m, r = t / (Q * m);
@@ -203,36 +227,36 @@ __global__ void __launch_bounds__(512) k_gsf3(GsfArgs a) {
       R[(((ia * TB + ib) * m + slot) * NB + d0) * NB * NB + d1 * NB + d2] += acc;
     }
     __syncthreads();
-    // ---- write the finished rows I2 = e2 (and the tail rows after the last element)
+    // ---- write the finished rows I2 = e2 (and the tail rows after the last element) of
+    // this segment; every slot is cleared after use (halo rows I2 < s0 are dropped)
     const int last = (e2 == K - 1) ? (int)N - 1 : e2;
     for (int I2 = e2; I2 <= last; ++I2) {
       const int slot = I2 % m;
-      const int64_t c2 = band_cnt(I2, P, N), lo2 = band_lo(I2, P);
-      for (int rc = 0; rc < TA * TB; ++rc) {
-        const int ia = rc / TB, ib = rc % TB;
+      const bool write = I2 >= s0;
+      if (write && tid < TA * TB) {  // per-pencil row offsets (64-bit) for this row
+        const int ia = tid / TB, ib = tid % TB;
         const int64_t I0 = i00 + ia, I1 = i10 + ib;
-        if (I0 >= a.plane_end || I1 >= N) continue;
-        const int64_t c0 = band_cnt(I0, P, N), c1 = band_cnt(I1, P, N);
-        const int64_t lo0 = band_lo(I0, P), lo1 = band_lo(I1, P);
-        const int64_t off = rowptr3(I0, I1, I2, P, N) - a.base;
-        const int cnt = (int)(c0 * c1 * c2);
-        const double* Rr = R + ((ia * TB + ib) * m + slot) * S::rowVals;
-        for (int j = tid; j < cnt; j += nt) {
-          const int64_t jc = j % c2, jb = (j / c2) % c1, ja = j / (c2 * c1);
-          const int d0 = (int)(lo0 + ja - (I0 - P));
-          const int d1 = (int)(lo1 + jb - (I1 - P));
-          const int d2 = (int)(lo2 + jc - (I2 - P));
-          a.values[off + j] = Rr[(d0 * NB + d1) * NB + d2];
-        }
+        rowoff[tid] = (I0 < a.plane_end && I1 < N) ? rowptr3(I0, I1, I2, P, N) - a.base : -1;
       }
-    }
-    __syncthreads();
-    for (int I2 = e2; I2 <= last; ++I2) {
-      const int slot = I2 % m;
+      __syncthreads();
+      const int lod2 = max(0, P - I2), c2 = (int)band_cnt(I2, P, N);
       for (int t = tid; t < TA * TB * S::rowVals; t += nt) {
         const int rc = t / S::rowVals, v = t % S::rowVals;
-        R[(rc * m + slot) * S::rowVals + v] = 0.0;
+        const int d2 = v % NB, d1 = (v / NB) % NB, d0 = v / (NB * NB);
+        double* Rv = R + (rc * m + slot) * S::rowVals + v;
+        if (write) {
+          const int64_t off = rowoff[rc];
+          const int ia = rc / TB, ib = rc % TB;
+          const int I0 = i00 + ia, I1 = i10 + ib;
+          const int lod0 = max(0, P - I0), lod1 = max(0, P - I1);
+          const int c0 = (int)band_cnt(I0, P, N), c1 = (int)band_cnt(I1, P, N);
+          if (off >= 0 && d0 >= lod0 && d0 < lod0 + c0 && d1 >= lod1 && d1 < lod1 + c1 &&
+              d2 >= lod2 && d2 < lod2 + c2)
+            a.values[off + ((d0 - lod0) * c1 + (d1 - lod1)) * c2 + (d2 - lod2)] = *Rv;
+        }
+        *Rv = 0.0;
       }
+      __syncthreads();
     }
   }
 }
@@ -266,10 +290,26 @@ struct GsfLaunch {
       if (planes <= 0) return IGA_OK;
       const int tiles0 = (planes + TA - 1) / TA;
       a.tiles1 = (int)((N + TB - 1) / TB);
-      const int64_t grid = (int64_t)tiles0 * a.tiles1;
-      cudaError_t e = smem_attr_once(reinterpret_cast<const void*>(k_gsf3<P, Q, TA, TB>), Sh::bytes);
+      const int64_t tiles = (int64_t)tiles0 * a.tiles1;
+      const void* fn = reinterpret_cast<const void*>(k_gsf3<P, Q, TA, TB>);
+      cudaError_t e = smem_attr_once(fn, Sh::bytes);
       if (e != cudaSuccess) return check_cuda(e, "gsf smem attr");
-      k_gsf3<P, Q, TA, TB><<<(unsigned)grid, 512, Sh::bytes, s>>>(a);
+      // split the element column into segments when the tiles alone do not fill the GPU:
+      // minimise waves x (segment + halo) element iterations
+      const int64_t slots = (int64_t)sm_count() * blocks_per_sm_once(fn, 512, Sh::bytes);
+      int best = 1;
+      double best_cost = 1e300;
+      for (int sg = 1; sg <= a.K; ++sg) {
+        const int L = (a.K + sg - 1) / sg;
+        if (L < P && sg > 1) break;
+        const int64_t ctas = tiles * sg;
+        const double waves = (double)((ctas + slots - 1) / slots);
+        const double cost = waves * (L + (sg > 1 ? P : 0));
+        if (cost < best_cost - 1e-9) { best_cost = cost; best = sg; }
+      }
+      a.segs = best;
+      a.seg_len = (a.K + best - 1) / best;
+      k_gsf3<P, Q, TA, TB><<<(unsigned)(tiles * best), 512, Sh::bytes, s>>>(a);
       return check_cuda(cudaGetLastError(), "gsf launch");
     }
   }

@@ -162,7 +162,7 @@ int32_t iga_integrate_assemble(const iga_problem* prob, int32_t method, int32_t 
     GsfArgs a;
     a.K = K; a.op = prob->op; a.el_begin = el_begin; a.el_end = el_end;
     a.plane_begin = row_plane_begin; a.plane_end = row_plane_end; a.tiles1 = 0;
-    a.own_begin = row_plane_begin; a.mirror_end = row_plane_end;
+    a.segs = 1; a.seg_len = K;
     a.base = base; a.jac = prob->jac; a.coef_scalar = prob->coef_scalar; a.coef = prob->coef;
     a.weights = prob->weights; a.V = prob->tables_v; a.D = prob->tables_d; a.values = values;
     return launch_gsf(a, p, prob->q, s);

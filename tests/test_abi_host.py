@@ -162,3 +162,26 @@ def test_auto_selects_kernel():
         _lib.METHOD_SUMFACT_ASSEMBLED
     assert method_code(pkg.RunConfig("sumfact", "device", K, p, assembly="owner")) == \
         _lib.METHOD_SUMFACT_ASSEMBLED
+
+
+@pytest.mark.parametrize("dim,K,p,op", [(3, 3, 2, "stiffness"), (3, 4, 1, "mass"), (2, 5, 2, "mass"),
+                                        (3, 2, 3, "stiffness_mass"), (3, 1, 0, "mass")])
+def test_matrix_market_host_writer_matches_scipy(lib, tmp_path, dim, K, p, op):
+    """Native Matrix Market writer (csrc/iga_mmio.cu) vs the reference's
+    scipy.io.mmwrite(..., symmetry="symmetric") (assembly.py:118-120): identical bytes."""
+    import io
+
+    import scipy.io
+    import scipy.sparse
+
+    ip, ix, v = O.integrate_assemble(dim, K, p, op, "classical")
+    if K == 3:  # exercise the value formatter: signed zero, subnormal, huge, integers
+        v = v.copy()
+        v[:6] = [-0.0, 5e-324, 1.7976931348623157e308, 2.0, -123.5, 1e-5]
+    n = len(ip) - 1
+    m = scipy.sparse.csr_matrix((v, ix, ip), shape=(n, n))
+    ref = io.BytesIO()
+    scipy.io.mmwrite(ref, m.tocoo(), symmetry="symmetric")
+    f = tmp_path / "a.mtx"
+    assert lib.iga_write_matrix_market_host(dim, K, p, v.ctypes.data, str(f).encode(), 3) == 0
+    assert f.read_bytes() == ref.getvalue()

@@ -427,3 +427,23 @@ def test_separable_rejects_field_coefficient(pkg):
     with pytest.raises(ValueError):
         pkg.run_integration(pkg.RunConfig("sumfact", "device", K, p, coefficient=coef,
                                           assembly="separable"))
+
+
+@pytest.mark.parametrize("K,p,op", [(5, 3, "stiffness"), (7, 2, "mass")])
+def test_matrix_market_export_streams_from_device(pkg, tmp_path, K, p, op):
+    """write_matrix_market from device values (row-block streaming) is byte-identical
+    to scipy.io.mmwrite of the same matrix (assembly.py:118-120)."""
+    import io
+
+    import scipy.io
+
+    gram = pkg.run_integration(pkg.RunConfig("sumfact", "device", K, p, operator=op)).gram
+    f = tmp_path / "g.mtx"
+    pkg.write_matrix_market(gram, f)
+    ref = io.BytesIO()
+    scipy.io.mmwrite(ref, gram.matrix.tocoo(), symmetry="symmetric")
+    assert f.read_bytes() == ref.getvalue()
+    import scipy.sparse
+
+    back = scipy.io.mmread(str(f)).tocsr()  # symmetric file: the lower triangle, mirrored
+    assert abs(scipy.sparse.tril(back) - scipy.sparse.tril(gram.matrix)).max() == 0.0

@@ -24,7 +24,7 @@ int main() {
   cudaMemcpy(dD, D.data(), D.size() * 8, cudaMemcpyHostToDevice);
   cudaMemcpy(dw, w.data(), 32, cudaMemcpyHostToDevice);
   iga::GsfArgs a{};
-  a.K = K; a.op = 1; a.el_begin = 0; a.el_end = K; a.plane_begin = 0; a.plane_end = K + P; a.own_begin = 0; a.mirror_end = K + P;
+  a.K = K; a.op = 1; a.el_begin = 0; a.el_end = K; a.plane_begin = 0; a.plane_end = K + P; a.segs = 1; a.seg_len = K;
   a.base = 0; a.jac = 1.0 / (8.0 * K * K * K); a.coef_scalar = 1.0; a.coef = nullptr;
   a.weights = dw; a.V = dV; a.D = dD; a.values = dval;
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
