@@ -68,7 +68,82 @@ __global__ void k_assemble_elements(int dim, int K, int p, const double* __restr
   }
 }
 
-// y = A x over the structured CSR: one warp per row.
+// y = A x over the structured CSR: one warp per row, lanes over the row's values
+// (contiguous, so each warp load is one coalesced 256-byte segment); the column of
+// value j is (lo0 + a, lo1 + b, lo2 + c) with j = (a c1 + b) c2 + c, decomposed with
+// compile-time divisors for the full-band rows.  HBM-bound on the values.
+template <int P>
+__global__ void __launch_bounds__(256, 5) k_spmv3(int K, const double* __restrict__ values,
+                                               const double* __restrict__ x,
+                                               double* __restrict__ y, int nseg) {
+  constexpr int NB = 2 * P + 1;
+  const int lane = threadIdx.x & 31;
+  const int64_t N = (int64_t)K + P;
+  // work unit: a run of rows I2 in [h0, h1) of one (I0, I1) pencil; the row offset and
+  // the x window advance incrementally along the run (no per-row 64-bit arithmetic)
+  const int64_t nunits = N * N * nseg;
+  for (int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < nunits;
+       u += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t pen = u / nseg;
+    const int sg = (int)(u - pen * nseg);
+    const int I0 = (int)(pen / N), I1 = (int)(pen - (int64_t)I0 * N);
+    const int h0 = (int)(N * sg / nseg), h1 = (int)(N * (sg + 1) / nseg);
+    const int c0 = (int)band_cnt(I0, P, N), c1 = (int)band_cnt(I1, P, N), c01 = c0 * c1;
+    const double* v = values + rowptr3(I0, I1, h0, P, N);
+    const double* xp = x + ((int64_t)band_lo(I0, P) * N + band_lo(I1, P)) * N;
+    double* yp = y + ((int64_t)I0 * N + I1) * N;
+    // x offsets of this lane's values in a full-band row (the same for every such row)
+    constexpr int NE = (NB * NB * NB + 31) / 32;
+    int xo[NE];
+#pragma unroll
+    for (int k = 0; k < NE; ++k) {
+      const int j = lane + 32 * k, a = j / (NB * NB), b = (j / NB) % NB, c = j % NB;
+      xo[k] = (int)(((int64_t)a * N + b) * N + c);
+    }
+    for (int I2 = h0; I2 < h1; ++I2) {
+      const int lo2 = I2 - P < 0 ? 0 : I2 - P;
+      const int c2 = (int)band_cnt(I2, P, N);
+      const double* xb = xp + lo2;
+      const int cnt = c01 * c2;
+      double acc = 0.0;
+      if (cnt == NB * NB * NB) {
+#pragma unroll
+        for (int k = 0; k < NE; ++k) {
+          const int j = lane + 32 * k;
+          if (j < NB * NB * NB) acc += v[j] * xb[xo[k]];
+        }
+      } else {
+        for (int j = lane; j < cnt; j += 32) {
+          const int a = j / (c1 * c2), b = (j / c2) % c1, c = j % c2;
+          acc += v[j] * xb[((int64_t)a * N + b) * N + c];
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) yp[I2] = acc;
+      v += cnt;
+    }
+  }
+}
+
+template <int P>
+struct Spmv3Launch {
+  static int run(int K, const double* values, const double* x, double* y, cudaStream_t s) {
+    const int64_t N = (int64_t)K + P;
+    // ~4 row runs per resident warp (balance), runs of >= 8 rows
+    const int64_t want_units = (int64_t)sm_count() * 64 * 4;
+    int nseg = (int)((want_units + N * N - 1) / (N * N));
+    if (nseg > (int)(N / 8)) nseg = (int)(N / 8);
+    if (nseg < 1) nseg = 1;
+    const int64_t units = N * N * nseg;
+    const int64_t want = (units * 32 + 255) / 256;
+    const int64_t grid = want < (int64_t)sm_count() * 5 ? want : (int64_t)sm_count() * 5;
+    k_spmv3<P><<<(unsigned)grid, 256, 0, s>>>(K, values, x, y, nseg);
+    return check_cuda(cudaGetLastError(), "iga_spmv");
+  }
+};
+
+// 2D: one warp per row (general path).
 __global__ void k_spmv(int dim, int K, int p, const double* __restrict__ values,
                        const double* __restrict__ x, double* __restrict__ y, int64_t nrows) {
   const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -205,7 +280,8 @@ int32_t iga_spmv(int32_t dim, int32_t K, int32_t p, const double* values, const 
   if (K < 1 || p < 0) return fail_einval("mesh must be >= 1 and degree >= 0");
   if (!values || !x || !y) return fail_einval("null pointer");
   const int64_t N = (int64_t)K + p;
-  const int64_t nrows = dim == 3 ? N * N * N : N * N;
+  if (dim == 3) return dispatch_p<Spmv3Launch>(p, K, values, x, y, as_stream(stream));
+  const int64_t nrows = N * N;
   const int64_t threads = nrows * 32;
   k_spmv<<<(unsigned)((threads + 255) / 256), 256, 0, as_stream(stream)>>>(dim, K, p, values, x,
                                                                           y, nrows);
