@@ -5,10 +5,10 @@
 // the Gauss points by per-axis contractions, weighted, then the transposed
 // contractions, scattered into the result).
 //
-// One CTA per element (grid-stride).  Forward: x_e (m^3) -> u, du/dx0, du/dx1,
-// du/dx2 at the q^3 points (three axis contractions, value and derivative tables).
-// Pointwise: f = W (alpha u, beta grad u), W = w w w jac c.  Backward: the
-// transposed contractions, then an atomicAdd of the m^3 element result into y.
+// Per element: forward x_e (m^3) -> u, du/dx0, du/dx1, du/dx2 at the q^3 points
+// (three axis contractions, value and derivative tables); pointwise f = W (alpha u,
+// beta grad u), W = w w w jac c; backward: the transposed contractions, then
+// atomicAdd of the element result into y.  A CTA runs a batch of E elements.
 #include "iga_args.cuh"
 #include "iga_dispatch.cuh"
 
@@ -25,129 +25,166 @@ struct ApplyArgs {
   double* y;
 };
 
-template <int P, int Q>
-__global__ void __launch_bounds__(128) k_apply3(ApplyArgs a) {
-  constexpr int m = P + 1;
-  __shared__ double sx[m * m * m];
-  __shared__ double t0[m][m][Q], t1[m][m][Q];                  // axis-2 contractions
-  __shared__ double u0[m][Q][Q], u1[m][Q][Q], u2[m][Q][Q];     // axis-1
-  __shared__ double f[4][Q][Q][Q];                             // point values
-  __shared__ double h0[m][Q][Q], h1[m][Q][Q], h2[m][Q][Q];     // backward axis 0
-  __shared__ double j0[m][m][Q], j1[m][m][Q];                  // backward axis 1
-  __shared__ double tv[3][m][Q], td[3][m][Q], w[Q];
+// E consecutive elements along the fastest axis per CTA (they share the axis-0/1
+// tables and overlap in their dof windows): every stage runs over the E elements at
+// once (fewer barriers per element), and the backward axis-2 contraction sums the
+// batch's contributions per dof in shared memory, so only (E+P) m^2 atomics leave
+// the CTA instead of E m^3.
+template <int P, int Q, int E>
+__global__ void __launch_bounds__(256, 4) k_apply3(ApplyArgs a) {
+  constexpr int m = P + 1, W2 = E + P;  // dof window of the batch along axis 2
+  __shared__ double sx[m][m][W2];
+  __shared__ double t0[E][m][m][Q], t1[E][m][m][Q];               // axis-2 contractions
+  __shared__ double u0[E][m][Q][Q], u1[E][m][Q][Q], u2[E][m][Q][Q];  // axis-1
+  __shared__ double f[4][E][Q][Q][Q];                              // point values
+  __shared__ double h0[E][m][Q][Q], h1[E][m][Q][Q], h2[E][m][Q][Q];  // backward axis 0
+  __shared__ double j0[E][m][m][Q], j1[E][m][m][Q];               // backward axis 1
+  __shared__ double tv01[2][m][Q], td01[2][m][Q], tv2[E][m][Q], td2[E][m][Q], w[Q];
   const int K = a.K;
   const int64_t N = (int64_t)K + P;
-  const int64_t n_el = (int64_t)K * K * K;
+  const int nb = (K + E - 1) / E;  // batches along axis 2
+  const int64_t n_batch = (int64_t)K * K * nb;
   const bool stiff = a.beta != 0.0;
   const int tid = threadIdx.x, nt = blockDim.x;
-  for (int64_t el = blockIdx.x; el < n_el; el += gridDim.x) {
-    const int e2 = (int)(el % K), e1 = (int)((el / K) % K), e0 = (int)(el / ((int64_t)K * K));
-    const int ev[3] = {e0, e1, e2};
+  for (int64_t bt = blockIdx.x; bt < n_batch; bt += gridDim.x) {
+    const int eb = (int)(bt % nb) * E, e1 = (int)((bt / nb) % K), e0 = (int)(bt / ((int64_t)nb * K));
+    const int ne = min(E, K - eb);  // elements in this batch
     __syncthreads();
-    for (int u = tid; u < 3 * m * Q; u += nt) {
+    for (int u = tid; u < 2 * m * Q; u += nt) {
       const int d = u / (m * Q), rk = u % (m * Q);
-      tv[d][rk / Q][rk % Q] = a.V[(int64_t)ev[d] * m * Q + rk];
-      td[d][rk / Q][rk % Q] = stiff ? a.D[(int64_t)ev[d] * m * Q + rk] : 0.0;
+      const int64_t e = d == 0 ? e0 : e1;
+      tv01[d][rk / Q][rk % Q] = a.V[e * m * Q + rk];
+      td01[d][rk / Q][rk % Q] = stiff ? a.D[e * m * Q + rk] : 0.0;
+    }
+    for (int u = tid; u < E * m * Q; u += nt) {
+      const int b = u / (m * Q), rk = u % (m * Q);
+      const bool ok = b < ne;
+      tv2[b][rk / Q][rk % Q] = ok ? a.V[(int64_t)(eb + b) * m * Q + rk] : 0.0;
+      td2[b][rk / Q][rk % Q] = ok && stiff ? a.D[(int64_t)(eb + b) * m * Q + rk] : 0.0;
     }
     if (tid < Q) w[tid] = a.weights[tid];
-    for (int u = tid; u < m * m * m; u += nt) {
-      const int i0 = u / (m * m), i1 = (u / m) % m, i2 = u % m;
-      sx[u] = a.x[((int64_t)(e0 + i0) * N + e1 + i1) * N + e2 + i2];
+    for (int u = tid; u < m * m * W2; u += nt) {
+      const int i0 = u / (m * W2), i1 = (u / W2) % m, z = u % W2;
+      sx[i0][i1][z] = eb + z < N ? a.x[((int64_t)(e0 + i0) * N + e1 + i1) * N + eb + z] : 0.0;
     }
     __syncthreads();
     // forward axis 2: t0 = sum x V2, t1 = sum x D2
-    for (int u = tid; u < m * m * Q; u += nt) {
-      const int i0 = u / (m * Q), i1 = (u / Q) % m, k2 = u % Q;
+    for (int u = tid; u < E * m * m * Q; u += nt) {
+      const int b = u / (m * m * Q), i0 = (u / (m * Q)) % m, i1 = (u / Q) % m, k2 = u % Q;
       double s0 = 0.0, s1 = 0.0;
 #pragma unroll
       for (int i2 = 0; i2 < m; ++i2) {
-        const double xv = sx[(i0 * m + i1) * m + i2];
-        s0 += xv * tv[2][i2][k2];
-        s1 += xv * td[2][i2][k2];
+        const double xv = sx[i0][i1][b + i2];
+        s0 += xv * tv2[b][i2][k2];
+        s1 += xv * td2[b][i2][k2];
       }
-      t0[i0][i1][k2] = s0;
-      t1[i0][i1][k2] = s1;
+      t0[b][i0][i1][k2] = s0;
+      t1[b][i0][i1][k2] = s1;
     }
     __syncthreads();
     // forward axis 1: u0 = t0 V1, u1 = t0 D1, u2 = t1 V1
-    for (int u = tid; u < m * Q * Q; u += nt) {
-      const int i0 = u / (Q * Q), k1 = (u / Q) % Q, k2 = u % Q;
+    for (int u = tid; u < E * m * Q * Q; u += nt) {
+      const int b = u / (m * Q * Q), i0 = (u / (Q * Q)) % m, k1 = (u / Q) % Q, k2 = u % Q;
       double s0 = 0.0, s1 = 0.0, s2 = 0.0;
 #pragma unroll
       for (int i1 = 0; i1 < m; ++i1) {
-        s0 += t0[i0][i1][k2] * tv[1][i1][k1];
-        s1 += t0[i0][i1][k2] * td[1][i1][k1];
-        s2 += t1[i0][i1][k2] * tv[1][i1][k1];
+        s0 += t0[b][i0][i1][k2] * tv01[1][i1][k1];
+        s1 += t0[b][i0][i1][k2] * td01[1][i1][k1];
+        s2 += t1[b][i0][i1][k2] * tv01[1][i1][k1];
       }
-      u0[i0][k1][k2] = s0;
-      u1[i0][k1][k2] = s1;
-      u2[i0][k1][k2] = s2;
+      u0[b][i0][k1][k2] = s0;
+      u1[b][i0][k1][k2] = s1;
+      u2[b][i0][k1][k2] = s2;
     }
     __syncthreads();
     // forward axis 0 + pointwise weights: f0 = W a u, f1..3 = W b du/dx_d
-    for (int u = tid; u < Q * Q * Q; u += nt) {
-      const int k0 = u / (Q * Q), k1 = (u / Q) % Q, k2 = u % Q;
+    for (int u = tid; u < E * Q * Q * Q; u += nt) {
+      const int b = u / (Q * Q * Q), k = u % (Q * Q * Q);
+      const int k0 = k / (Q * Q), k1 = (k / Q) % Q, k2 = k % Q;
       double val = 0.0, g0 = 0.0, g1 = 0.0, g2 = 0.0;
 #pragma unroll
       for (int i0 = 0; i0 < m; ++i0) {
-        val += u0[i0][k1][k2] * tv[0][i0][k0];
-        g0 += u0[i0][k1][k2] * td[0][i0][k0];
-        g1 += u1[i0][k1][k2] * tv[0][i0][k0];
-        g2 += u2[i0][k1][k2] * tv[0][i0][k0];
+        val += u0[b][i0][k1][k2] * tv01[0][i0][k0];
+        g0 += u0[b][i0][k1][k2] * td01[0][i0][k0];
+        g1 += u1[b][i0][k1][k2] * tv01[0][i0][k0];
+        g2 += u2[b][i0][k1][k2] * tv01[0][i0][k0];
       }
-      double W = w[k0] * w[k1] * w[k2] * a.jac;
-      W *= a.coef ? a.coef[el * (Q * Q * Q) + u] : a.coef_scalar;
-      f[0][k0][k1][k2] = W * a.alpha * val;
-      f[1][k0][k1][k2] = W * a.beta * g0;
-      f[2][k0][k1][k2] = W * a.beta * g1;
-      f[3][k0][k1][k2] = W * a.beta * g2;
+      double Wt = w[k0] * w[k1] * w[k2] * a.jac;
+      if (b < ne) {
+        const int64_t el = ((int64_t)e0 * K + e1) * K + eb + b;
+        Wt *= a.coef ? a.coef[el * (Q * Q * Q) + k] : a.coef_scalar;
+      } else {
+        Wt = 0.0;
+      }
+      f[0][b][k0][k1][k2] = Wt * a.alpha * val;
+      f[1][b][k0][k1][k2] = Wt * a.beta * g0;
+      f[2][b][k0][k1][k2] = Wt * a.beta * g1;
+      f[3][b][k0][k1][k2] = Wt * a.beta * g2;
     }
     __syncthreads();
     // backward axis 0: h0 = V0 f0 + D0 f1 (pairs with V1 V2), h1 = V0 f2 (D1 V2), h2 = V0 f3 (V1 D2)
-    for (int u = tid; u < m * Q * Q; u += nt) {
-      const int i0 = u / (Q * Q), k1 = (u / Q) % Q, k2 = u % Q;
+    for (int u = tid; u < E * m * Q * Q; u += nt) {
+      const int b = u / (m * Q * Q), i0 = (u / (Q * Q)) % m, k1 = (u / Q) % Q, k2 = u % Q;
       double s0 = 0.0, s1 = 0.0, s2 = 0.0;
 #pragma unroll
       for (int k0 = 0; k0 < Q; ++k0) {
-        s0 += tv[0][i0][k0] * f[0][k0][k1][k2] + td[0][i0][k0] * f[1][k0][k1][k2];
-        s1 += tv[0][i0][k0] * f[2][k0][k1][k2];
-        s2 += tv[0][i0][k0] * f[3][k0][k1][k2];
+        s0 += tv01[0][i0][k0] * f[0][b][k0][k1][k2] + td01[0][i0][k0] * f[1][b][k0][k1][k2];
+        s1 += tv01[0][i0][k0] * f[2][b][k0][k1][k2];
+        s2 += tv01[0][i0][k0] * f[3][b][k0][k1][k2];
       }
-      h0[i0][k1][k2] = s0;
-      h1[i0][k1][k2] = s1;
-      h2[i0][k1][k2] = s2;
+      h0[b][i0][k1][k2] = s0;
+      h1[b][i0][k1][k2] = s1;
+      h2[b][i0][k1][k2] = s2;
     }
     __syncthreads();
     // backward axis 1: j0 = V1 h0 + D1 h1 (pairs with V2), j1 = V1 h2 (D2)
-    for (int u = tid; u < m * m * Q; u += nt) {
-      const int i0 = u / (m * Q), i1 = (u / Q) % m, k2 = u % Q;
+    for (int u = tid; u < E * m * m * Q; u += nt) {
+      const int b = u / (m * m * Q), i0 = (u / (m * Q)) % m, i1 = (u / Q) % m, k2 = u % Q;
       double s0 = 0.0, s1 = 0.0;
 #pragma unroll
       for (int k1 = 0; k1 < Q; ++k1) {
-        s0 += tv[1][i1][k1] * h0[i0][k1][k2] + td[1][i1][k1] * h1[i0][k1][k2];
-        s1 += tv[1][i1][k1] * h2[i0][k1][k2];
+        s0 += tv01[1][i1][k1] * h0[b][i0][k1][k2] + td01[1][i1][k1] * h1[b][i0][k1][k2];
+        s1 += tv01[1][i1][k1] * h2[b][i0][k1][k2];
       }
-      j0[i0][i1][k2] = s0;
-      j1[i0][i1][k2] = s1;
+      j0[b][i0][i1][k2] = s0;
+      j1[b][i0][i1][k2] = s1;
     }
     __syncthreads();
-    // backward axis 2 and scatter
-    for (int u = tid; u < m * m * m; u += nt) {
-      const int i0 = u / (m * m), i1 = (u / m) % m, i2 = u % m;
+    // backward axis 2, summed over the batch's elements per dof, then one atomic per dof
+    for (int u = tid; u < m * m * W2; u += nt) {
+      const int i0 = u / (m * W2), i1 = (u / W2) % m, z = u % W2;
+      if (eb + z >= N) continue;
       double s = 0.0;
 #pragma unroll
-      for (int k2 = 0; k2 < Q; ++k2) s += tv[2][i2][k2] * j0[i0][i1][k2] + td[2][i2][k2] * j1[i0][i1][k2];
-      atomicAdd(a.y + ((int64_t)(e0 + i0) * N + e1 + i1) * N + e2 + i2, s);
+      for (int b = 0; b < E; ++b) {
+        const int i2 = z - b;
+        if (b < ne && i2 >= 0 && i2 < m) {
+#pragma unroll
+          for (int k2 = 0; k2 < Q; ++k2) s += tv2[b][i2][k2] * j0[b][i0][i1][k2] + td2[b][i2][k2] * j1[b][i0][i1][k2];
+        }
+      }
+      atomicAdd(a.y + ((int64_t)(e0 + i0) * N + e1 + i1) * N + eb + z, s);
     }
   }
+}
+
+// static shared memory of k_apply3<P,Q,E> in doubles (must stay under 48 KB)
+constexpr int apply_smem(int P, int Q, int E) {
+  return (P + 1) * (P + 1) * (E + P) + 4 * E * (P + 1) * (P + 1) * Q + 6 * E * (P + 1) * Q * Q +
+         4 * E * Q * Q * Q + 4 * (P + 1) * Q + 2 * E * (P + 1) * Q + Q;
+}
+constexpr int apply_batch(int P, int Q) {
+  return apply_smem(P, Q, 4) * 8 <= 48 * 1024 ? 4 : (apply_smem(P, Q, 2) * 8 <= 48 * 1024 ? 2 : 1);
 }
 
 template <int P, int Q>
 struct ApplyLaunch {
   static int run(const ApplyArgs& a, cudaStream_t s) {
-    const int64_t n_el = (int64_t)a.K * a.K * a.K;
-    const int64_t grid = n_el < 148 * 16 ? n_el : 148 * 16;
-    k_apply3<P, Q><<<(unsigned)grid, 128, 0, s>>>(a);
+    constexpr int E = apply_batch(P, Q);
+    const int64_t n_batch = (int64_t)a.K * a.K * ((a.K + E - 1) / E);
+    const int64_t cap = (int64_t)sm_count() * 8;
+    const int64_t grid = n_batch < cap ? n_batch : cap;
+    k_apply3<P, Q, E><<<(unsigned)grid, 256, 0, s>>>(a);
     return check_cuda(cudaGetLastError(), "iga_apply launch");
   }
 };
