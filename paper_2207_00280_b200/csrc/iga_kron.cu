@@ -171,15 +171,21 @@ __global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) 
   const int nch = (int)((N + G - 1) / G);
   const int64_t nunit = (int64_t)(a.plane_end - a.plane_begin) * N * nch;
   const int64_t u_lo = nunit * blockIdx.x / gridDim.x, u_hi = nunit * (blockIdx.x + 1) / gridDim.x;
+  const int64_t T = band_prefix(N, P, N);  // values of a full-length band row set
+  double* vals = nullptr;                   // first value of the current pencil
   for (int64_t pen = u_lo / nch; pen * nch < u_hi; ++pen) {
     const int I0 = a.plane_begin + (int)(pen / N), I1 = (int)(pen % N);
+    // consecutive pencils are contiguous in the CSR: one 64-bit rowptr per CTA
+    if (vals == nullptr) vals = a.values + (rowptr3(I0, I1, 0, P, N) - a.base);
     const double2* r0 = tb0 + I0 * NB;
     const int lod0 = max(0, P - I0), lod1 = max(0, P - I1);
     const int c0 = (int)band_cnt(I0, P, N), c1 = (int)band_cnt(I1, P, N), c01 = c0 * c1;
     const double2* r1 = tb + I1 * NB;
     // per-pair factors: value = fa * m2 + fb * k2
+    const unsigned inv1 = (1u << 20) / (unsigned)c1 + 1u;  // b / c1 for b < 2^20 / NB
     auto factors = [&](int b, double& fa, double& fb) {
-      const double2 x0 = r0[lod0 + b / c1], x1 = r1[lod1 + b % c1];
+      const int bq = (int)(((unsigned)b * inv1) >> 20);
+      const double2 x0 = r0[lod0 + bq], x1 = r1[lod1 + b - bq * c1];
       const double mm = a.jc * (x0.x * x1.x);
       if (a.op == IGA_OP_MASS) {
         fa = mm; fb = 0.0;
@@ -189,7 +195,6 @@ __global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) 
         fa = s; fb = mm;
       }
     };
-    double* vals = a.values + (rowptr3(I0, I1, 0, P, N) - a.base);
     const int ncnt = c01 * NB;  // values of an interior row
     double fa[NE], fb[NE];
     int d2[NE];
@@ -224,45 +229,41 @@ __global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) 
       if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
       __syncthreads();
       double* sb = buf + pad;
-      if (fast) {
-        // G full-band rows: fixed (pair, d2) per thread, rows ncnt apart
-        const double2* t2 = tb + R0 * NB;
+      // truncated-band rows (I2 < P or I2 >= K): b = e / c2 by a reciprocal (exact for
+      // e < 2^20 / NB), factors from the pencil table F
+      auto boundary_row = [&](int I2, int loc) {
+        const double2* t2 = tb + I2 * NB;
+        const int c2 = (int)band_cnt(I2, P, N), lod2 = max(0, P - I2);
+        const unsigned inv = (1u << 20) / (unsigned)c2 + 1u;
+        for (int e = tid; e < c01 * c2; e += NT) {
+          const int b = (int)(((unsigned)e * inv) >> 20);
+          const double2 f = F[b], x2 = t2[lod2 + e - b * c2];
+          sb[loc + e] = f.x * x2.x + f.y * x2.y;
+        }
+        return loc + c01 * c2;
+      };
+      int loc = 0;  // value offset of the next row inside the chunk
+      for (int I2 = R0; I2 < min(R1, P); ++I2) loc = boundary_row(I2, loc);
+      // full-band rows [max(R0,P), min(R1,K)): a fixed (pair, d2) per thread, rows ncnt apart
+      const int ib = max(R0, P), nr = min(R1, K) - ib;
+      if (nr > 0) {
+        const double2* t2 = tb + ib * NB;
+        double* sbi = sb + loc;
 #pragma unroll
         for (int r = 0; r < G; ++r)
-#pragma unroll
-          for (int j = 0; j < NE; ++j) {
-            const int e = tid + j * NT;
-            if (e < ncnt) {
-              const double2 x2 = t2[r * NB + d2[j]];
-              sb[r * ncnt + e] = fa[j] * x2.x + fb[j] * x2.y;
-            }
-          }
-      } else {
-        int loc = 0;  // value offset of row I2 inside the chunk
-        for (int I2 = R0; I2 < R1; ++I2) {
-          const double2* t2 = tb + I2 * NB;
-          if (I2 >= P && I2 < K) {
+          if (r < nr) {
 #pragma unroll
             for (int j = 0; j < NE; ++j) {
               const int e = tid + j * NT;
               if (e < ncnt) {
-                const double2 x2 = t2[d2[j]];
-                sb[loc + e] = fa[j] * x2.x + fb[j] * x2.y;
+                const double2 x2 = t2[r * NB + d2[j]];
+                sbi[r * ncnt + e] = fa[j] * x2.x + fb[j] * x2.y;
               }
             }
-            loc += ncnt;
-          } else {  // truncated band: b = e / c2 by a reciprocal (exact for e < 2^20 / NB)
-            const int c2 = (int)band_cnt(I2, P, N), lod2 = max(0, P - I2);
-            const unsigned inv = (1u << 20) / (unsigned)c2 + 1u;  // c2 <= NB: a few rows/pencil
-            for (int e = tid; e < c01 * c2; e += NT) {
-              const int b = (int)(((unsigned)e * inv) >> 20);
-              const double2 f = F[b], x2 = t2[lod2 + e - b * c2];
-              sb[loc + e] = f.x * x2.x + f.y * x2.y;
-            }
-            loc += c01 * c2;
           }
-        }
+        loc += nr * ncnt;
       }
+      for (int I2 = max(R0, max(K, P)); I2 < R1; ++I2) loc = boundary_row(I2, loc);
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
       __syncthreads();
       if (tid == 0) {
@@ -274,6 +275,7 @@ __global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) 
         asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
       }
     }
+    vals += (int64_t)c01 * T;
   }
   if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
 }
