@@ -1,5 +1,5 @@
-// Assembled sum factorization (row-owner): the headline integrate+assemble
-// kernel.
+// Assembled sum factorization (row-owner), generic in (p, q): the general-coefficient
+// integrate+assemble kernel for every degree (k_gsf3_p3 specialises p=3, q=4 on DMMA).
 //
 // The global CSR value of rows I = (I0, I1, I2), J (I0 slowest, assembly.py:25)
 //   S[I,J] = sum_e sum_k W_e(k) prod_d T_d[e_d](I_d - e_d, k_d) T_d[e_d](J_d - e_d, k_d)
@@ -21,6 +21,14 @@
 // and the row e2 finishes after element e2: it is written, coalesced, in CSR
 // order, and its rolling slot recycled for row e2+p+1.
 //
+// Each contraction is a small dense GEMM whose one operand is constant for the CTA
+// (the pair products of the tile's element windows, PA / PB / Z) and is read as a
+// warp-uniform shared-memory broadcast, while the other operand (one W column, one
+// X row, one Y combo) sits in registers: an item = (column or row, group of outputs),
+// items enumerated column-fastest so that every lane of a warp works on the same
+// output (the broadcast) of a different column.  Invalid element/row combinations
+// carry zero pair products, so the loops have no data-dependent bounds.
+//
 // Operators (T = value table V or derivative table D of each axis):
 //   mass            : X_V, Y_M = X_V VV,             S += Y_M VV
 //   stiffness       : X_V, X_D, Y_A = X_D VV + X_V DD, Y_B = X_V VV,
@@ -33,42 +41,62 @@
 
 namespace iga {
 
-template <int P, int Q, int TA, int TB>
+constexpr int kGsfThreads = 512;
+
+__host__ __device__ constexpr int cdiv(int a, int b) { return (a + b - 1) / b; }
+__host__ __device__ constexpr int rup32(int a) { return cdiv(a, 32) * 32; }
+__host__ __device__ constexpr int cmin(int a, int b) { return a < b ? a : b; }
+__host__ __device__ constexpr int cmax(int a, int b) { return a > b ? a : b; }
+
+template <int P, int Q, int TA, int TB, bool STIFF>
 struct GsfShape {
   static constexpr int m = P + 1;
-  static constexpr int NB = 2 * P + 1;                 // band width
-  static constexpr int GA = (TA + P) * Q;              // quadrature points on axis 0 slab
-  static constexpr int GB = (TB + P) * Q;              // ... axis 1
-  static constexpr int nW = GA * GB * Q;
-  static constexpr int nTabA = (TA + P) * m * Q;
-  static constexpr int nTabB = (TB + P) * m * Q;
-  static constexpr int nX = TA * NB * GB * Q;          // per type
-  static constexpr int nCombo = TA * NB * TB * NB;
-  static constexpr int nY = nCombo * Q;                // per accumulator
+  static constexpr int NB = 2 * P + 1;  // band width
+  static constexpr int LA = TA + P, LB = TB + P;  // element windows of the tile
+  static constexpr int KA = LA * Q, KB = LB * Q;  // contraction lengths (elements x points)
+  static constexpr int GC = KB * Q;               // stage-A columns (lb, k1, k2)
+  static constexpr int NA0 = TA * NB, NB1 = TB * NB;
+  static constexpr int NC = NA0 * NB1;            // (a0, b1) combos
+  static constexpr int NR = NA0 * Q;              // stage-B rows (a0, k2)
   static constexpr int rowVals = NB * NB * NB;
+  // stage A items: (column, group of AG outputs a0)
+  static constexpr int GCp = rup32(GC);
+  static constexpr int AG = cmax(1, cmin(NA0, cdiv(NA0 * GCp, kGsfThreads)));
+  static constexpr int NGA = cdiv(NA0, AG);
+  // stage B items: (row, group of BG outputs b1)
+  static constexpr int NRp = rup32(NR);
+  static constexpr int BG = cmax(1, cmin(NB1, cdiv(NB1 * NRp, kGsfThreads)));
+  static constexpr int NGB = cdiv(NB1, BG);
+  // stage S items: (combo, group of SG rows r)
+  static constexpr int NCp = rup32(NC);
+  static constexpr int SG = cmax(1, cmin(m, cdiv(m * NCp, kGsfThreads)));
+  static constexpr int NGS = cdiv(m, SG);
+  // shared memory (doubles); Y aliases W (W is dead after stage A)
+  static constexpr int nW = KA * GC;
+  static constexpr int nY = 2 * NC * Q;
+  static constexpr int nWY = nW > nY ? nW : nY;
+  static constexpr int nPA = 2 * NA0 * KA;
+  static constexpr int nPB = 2 * NB1 * KB;
+  static constexpr int nX = 2 * NA0 * GC;
+  static constexpr int nZ = 2 * m * m * Q;
   static constexpr int nR = TA * TB * m * rowVals;
-  static constexpr int nZ = m * m * Q;
-  static constexpr size_t doubles = (size_t)nW + 2 * nTabA + 2 * nTabB + 2 * nX + 2 * nY + nR + 2 * nZ;
+  static constexpr size_t doubles = (size_t)nWY + nPA + nPB + nX + nZ + nR;
   static constexpr size_t bytes = doubles * sizeof(double);
 };
 
-template <int P, int Q, int TA, int TB>
-__global__ void __launch_bounds__(512, 2) k_gsf3(GsfArgs a) {
-  using S = GsfShape<P, Q, TA, TB>;
-  constexpr int m = S::m, NB = S::NB, GB = S::GB;
+template <int P, int Q, int TA, int TB, bool STIFF>
+__global__ void __launch_bounds__(kGsfThreads, 1) k_gsf3(GsfArgs a) {
+  using S = GsfShape<P, Q, TA, TB, STIFF>;
+  constexpr int m = S::m, NB = S::NB, LA = S::LA, LB = S::LB, KA = S::KA, KB = S::KB;
+  constexpr int GC = S::GC, NA0 = S::NA0, NB1 = S::NB1, NC = S::NC, NR = S::NR;
   extern __shared__ double smem[];
-  double* sW = smem;
-  double* tAV = sW + S::nW;
-  double* tAD = tAV + S::nTabA;
-  double* tBV = tAD + S::nTabA;
-  double* tBD = tBV + S::nTabB;
-  double* XV = tBD + S::nTabB;
-  double* XD = XV + S::nX;
-  double* Y0 = XD + S::nX;
-  double* Y1 = Y0 + S::nY;
-  double* R = Y1 + S::nY;
-  double* Z0 = R + S::nR;
-  double* Z1 = Z0 + S::nZ;
+  double* sW = smem;                                               // [KA][GC]
+  double2* Y2 = reinterpret_cast<double2*>(smem);                  // [NC][Q] (aliases W)
+  double2* PA2 = reinterpret_cast<double2*>(smem + S::nWY);        // [NA0][KA] (VV, DD)
+  double2* PB2 = PA2 + NA0 * KA;                                   // [NB1][KB] (VV, DD)
+  double2* X2 = PB2 + NB1 * KB;                                    // [NA0][KB][Q] (XV, XD)
+  double2* Z2 = X2 + NA0 * GC;                                     // [m][m][Q] (VV, DD(+VV))
+  double* R = reinterpret_cast<double*>(Z2 + m * m * Q);           // [TA*TB][m][rowVals]
   __shared__ int64_t rowoff[TA * TB];
 
   const int K = a.K;
@@ -76,43 +104,61 @@ __global__ void __launch_bounds__(512, 2) k_gsf3(GsfArgs a) {
   const int tile = blockIdx.x / a.segs, seg = blockIdx.x % a.segs;
   const int tile0 = tile / a.tiles1, tile1 = tile % a.tiles1;
   const int i00 = a.plane_begin + tile0 * TA;  // first row plane of the tile (axis 0)
+  const int i10 = tile1 * TB;                  // first row index along axis 1
   // element-column segment: rows I2 in [s0, s1) are written by this CTA, which streams
   // the elements [s0 - P, s1) that contribute to them (the first P recomputed as halo)
   const int s0 = seg * a.seg_len, s1 = min(K, s0 + a.seg_len);
   const int e_first = max(0, s0 - P);
-  const int i10 = tile1 * TB;                  // first row index along axis 1
   const int tid = threadIdx.x, nt = blockDim.x;
-  const bool stiff = a.op != IGA_OP_MASS;
   const int e0lo = max(a.el_begin, 0), e0hi = min(a.el_end, K);  // slab, clipped to the mesh
+  const double* V = a.V;
+  const double* D = a.D;
 
-  // per-axis tables of the CTA's element windows (zero outside the mesh)
-  for (int t = tid; t < S::nTabA; t += nt) {
-    const int e = i00 - P + t / (m * Q);
-    const bool ok = e >= 0 && e < K;
-    tAV[t] = ok ? a.V[(int64_t)e * m * Q + t % (m * Q)] : 0.0;
-    tAD[t] = ok && stiff ? a.D[(int64_t)e * m * Q + t % (m * Q)] : 0.0;
+  // ---- constant pair tables of the tile: PA (axis 0, slab-restricted), PB (axis 1)
+  for (int t = tid; t < NA0 * KA; t += nt) {
+    const int a0 = t / KA, kk = t % KA, la = kk / Q, k0 = kk % Q;
+    const int I0 = i00 + a0 / NB, J0 = I0 - P + a0 % NB, e0 = i00 - P + la;
+    const int r = I0 - e0, sidx = J0 - e0;
+    double2 v = make_double2(0.0, 0.0);
+    if (e0 >= e0lo && e0 < e0hi && r >= 0 && r <= P && sidx >= 0 && sidx <= P && J0 >= 0 && J0 < N) {
+      const double* Te = V + (int64_t)e0 * m * Q;
+      v.x = Te[r * Q + k0] * Te[sidx * Q + k0];
+      if (STIFF) {
+        const double* De = D + (int64_t)e0 * m * Q;
+        v.y = De[r * Q + k0] * De[sidx * Q + k0];
+      }
+    }
+    PA2[t] = v;
   }
-  for (int t = tid; t < S::nTabB; t += nt) {
-    const int e = i10 - P + t / (m * Q);
-    const bool ok = e >= 0 && e < K;
-    tBV[t] = ok ? a.V[(int64_t)e * m * Q + t % (m * Q)] : 0.0;
-    tBD[t] = ok && stiff ? a.D[(int64_t)e * m * Q + t % (m * Q)] : 0.0;
+  for (int t = tid; t < NB1 * KB; t += nt) {
+    const int b1 = t / KB, kk = t % KB, lb = kk / Q, k1 = kk % Q;
+    const int I1 = i10 + b1 / NB, J1 = I1 - P + b1 % NB, e1 = i10 - P + lb;
+    const int r = I1 - e1, sidx = J1 - e1;
+    double2 v = make_double2(0.0, 0.0);
+    if (e1 >= 0 && e1 < K && r >= 0 && r <= P && sidx >= 0 && sidx <= P && J1 >= 0 && J1 < N) {
+      const double* Te = V + (int64_t)e1 * m * Q;
+      v.x = Te[r * Q + k1] * Te[sidx * Q + k1];
+      if (STIFF) {
+        const double* De = D + (int64_t)e1 * m * Q;
+        v.y = De[r * Q + k1] * De[sidx * Q + k1];
+      }
+    }
+    PB2[t] = v;
   }
   for (int t = tid; t < S::nR; t += nt) R[t] = 0.0;
 
-  // coefficient of element column e2 for this thread's W entries (loaded one column
-  // ahead, so the global-memory latency overlaps the previous column's stages)
-  constexpr int WPT = (S::nW + 511) / 512;
+  // coefficient of element column e2 for this thread's W entries, loaded one column ahead
+  constexpr int WPT = cdiv(S::nW, kGsfThreads);
   auto load_coef = [&](int e2, double (&cv)[WPT]) {
 #pragma unroll
     for (int i = 0; i < WPT; ++i) {
       const int t = tid + i * nt;
       cv[i] = a.coef_scalar;
       if (a.coef && t < S::nW && e2 < K) {
-        const int k2 = t % Q, g1 = (t / Q) % GB, g0 = t / (Q * GB);
-        const int la = g0 / Q, k0 = g0 % Q, lb = g1 / Q, k1 = g1 % Q;
+        const int kk = t / GC, col = t % GC;
+        const int la = kk / Q, k0 = kk % Q, lb = col / (Q * Q), k1 = (col / Q) % Q, k2 = col % Q;
         const int e0 = i00 - P + la, e1 = i10 - P + lb;
-        if (e0 >= e0lo && e0 < e0hi && e1 >= 0 && e1 < K)
+        if (e0 >= 0 && e0 < K && e1 >= 0 && e1 < K)
           cv[i] = __ldg(a.coef + (((int64_t)e0 * K + e1) * K + e2) * (Q * Q * Q) + (k0 * Q + k1) * Q + k2);
       }
     }
@@ -120,111 +166,137 @@ __global__ void __launch_bounds__(512, 2) k_gsf3(GsfArgs a) {
   double cv[WPT];
   load_coef(e_first, cv);
   for (int e2 = e_first; e2 < s1; ++e2) {
-    __syncthreads();
-    // ---- stage W: weights x coefficient on the (axis0, axis1) slab of element column e2
+    __syncthreads();  // previous column's stage S (reads Y, aliasing W) is done
+    // ---- stage W: weights x coefficient, [(la,k0)][(lb,k1,k2)]; Z: axis-2 pair products
 #pragma unroll
     for (int i = 0; i < WPT; ++i) {
       const int t = tid + i * nt;
       if (t < S::nW) {
-        const int k2 = t % Q, g1 = (t / Q) % GB, g0 = t / (Q * GB);
-        const int la = g0 / Q, k0 = g0 % Q, lb = g1 / Q, k1 = g1 % Q;
-        const int e0 = i00 - P + la, e1 = i10 - P + lb;
-        double W = 0.0;
-        if (e0 >= e0lo && e0 < e0hi && e1 >= 0 && e1 < K)
-          W = a.weights[k0] * a.weights[k1] * a.weights[k2] * a.jac * cv[i];
-        sW[t] = W;
+        const int kk = t / GC, col = t % GC;
+        const int k0 = kk % Q, k1 = (col / Q) % Q, k2 = col % Q;
+        sW[t] = a.weights[k0] * a.weights[k1] * a.weights[k2] * a.jac * cv[i];
       }
     }
     load_coef(e2 + 1, cv);
-    // pair tables of axis 2 for element e2: Z0 = VV, Z1 = DD (+VV)
-    for (int t = tid; t < S::nZ; t += nt) {
-      const int k = t % Q, s = (t / Q) % m, r = t / (Q * m);
-      const double* V2 = a.V + (int64_t)e2 * m * Q;
-      const double vv = V2[r * Q + k] * V2[s * Q + k];
-      Z0[t] = vv;
-      if (stiff) {
-        const double* D2 = a.D + (int64_t)e2 * m * Q;
-        double dd = D2[r * Q + k] * D2[s * Q + k];
+    for (int t = tid; t < m * m * Q; t += nt) {
+      const int k = t % Q, sidx = (t / Q) % m, r = t / (Q * m);
+      const double* V2 = V + (int64_t)e2 * m * Q;
+      const double vv = V2[r * Q + k] * V2[sidx * Q + k];
+      double dd = 0.0;
+      if (STIFF) {
+        const double* D2 = D + (int64_t)e2 * m * Q;
+        dd = D2[r * Q + k] * D2[sidx * Q + k];
         if (a.op == IGA_OP_STIFFNESS_MASS) dd += vv;
-        Z1[t] = dd;
       }
+      Z2[t] = make_double2(vv, dd);
     }
     __syncthreads();
-    // ---- stage A: contract axis 0 (elements e0 and points k0)
-    for (int t = tid; t < S::nX; t += nt) {
-      const int k2 = t % Q;
-      const int g1 = (t / Q) % GB;
-      const int d0 = (t / (Q * GB)) % NB;
-      const int ia = t / (Q * GB * NB);
-      const int I0 = i00 + ia, J0 = I0 - P + d0;
-      const int lo = max(max(I0, J0) - P, 0), hi = min(min(I0, J0), K - 1);
-      double xv = 0.0, xd = 0.0;
-      for (int e0 = lo; e0 <= hi; ++e0) {
-        const int la = e0 - (i00 - P);
-        const double* av = tAV + la * m * Q;
-        const double* ad = tAD + la * m * Q;
-        const int r = I0 - e0, s = J0 - e0;
+    // ---- stage A (axis 0): X_T[a0][col] = sum_{(la,k0)} PA_T[a0][(la,k0)] W[(la,k0)][col]
+    for (int it = tid; it < S::GCp * S::NGA; it += nt) {
+      const int col = it % S::GCp, g = it / S::GCp;
+      if (col < GC) {
+        double w[KA];
 #pragma unroll
-        for (int k0 = 0; k0 < Q; ++k0) {
-          const double W = sW[((la * Q + k0) * GB + g1) * Q + k2];
-          xv += av[r * Q + k0] * av[s * Q + k0] * W;
-          if (stiff) xd += ad[r * Q + k0] * ad[s * Q + k0] * W;
-        }
-      }
-      XV[t] = xv;
-      XD[t] = xd;
-    }
-    __syncthreads();
-    // ---- stage B: contract axis 1 (elements e1 and points k1)
-    for (int t = tid; t < S::nY; t += nt) {
-      const int k2 = t % Q;
-      const int d1 = (t / Q) % NB;
-      const int ib = (t / (Q * NB)) % TB;
-      const int a0 = t / (Q * NB * TB);  // = ia * NB + d0
-      const int I1 = i10 + ib, J1 = I1 - P + d1;
-      const int lo = max(max(I1, J1) - P, 0), hi = min(min(I1, J1), K - 1);
-      double y0 = 0.0, y1 = 0.0;
-      for (int e1 = lo; e1 <= hi; ++e1) {
-        const int lb = e1 - (i10 - P);
-        const double* bv = tBV + lb * m * Q;
-        const double* bd = tBD + lb * m * Q;
-        const int r = I1 - e1, s = J1 - e1;
+        for (int kk = 0; kk < KA; ++kk) w[kk] = sW[kk * GC + col];
 #pragma unroll
-        for (int k1 = 0; k1 < Q; ++k1) {
-          const int xi = (a0 * GB + lb * Q + k1) * Q + k2;
-          const double vv = bv[r * Q + k1] * bv[s * Q + k1];
-          if (stiff) {
-            const double dd = bd[r * Q + k1] * bd[s * Q + k1];
-            y0 += XD[xi] * vv + XV[xi] * dd;
-            y1 += XV[xi] * vv;
-          } else {
-            y0 += XV[xi] * vv;
+        for (int j = 0; j < S::AG; ++j) {
+          const int a0 = g * S::AG + j;
+          if (a0 < NA0) {
+            const double2* pa = PA2 + a0 * KA;
+            double xv = 0.0, xd = 0.0;
+#pragma unroll
+            for (int kk = 0; kk < KA; ++kk) {
+              const double2 pp = pa[kk];
+              xv += pp.x * w[kk];
+              if (STIFF) xd += pp.y * w[kk];
+            }
+            X2[a0 * GC + col] = make_double2(xv, xd);
           }
         }
       }
-      Y0[t] = y0;
-      Y1[t] = y1;
     }
     __syncthreads();
-    // ---- stage S: contract axis 2 within element e2 into the rolling rows
-    for (int t = tid; t < S::nCombo * m * m; t += nt) {
-      const int s = t % m;
-      const int r = (t / m) % m;
-      const int c = t / (m * m);  // ((ia*NB + d0)*TB + ib)*NB + d1
-      const int d1 = c % NB, ib = (c / NB) % TB, d0 = (c / (NB * TB)) % NB, ia = c / (NB * TB * NB);
-      const double* y0 = Y0 + c * Q;
-      const double* y1 = Y1 + c * Q;
-      const double* z0 = Z0 + (r * m + s) * Q;
-      const double* z1 = Z1 + (r * m + s) * Q;
-      double acc = 0.0;
+    // ---- stage B (axis 1): per row (a0, k2), Y over b1:
+    //   mass: Y = sum XV VV;  stiffness: YA = sum XV DD + XD VV, YB = sum XV VV
+    for (int it = tid; it < S::NRp * S::NGB; it += nt) {
+      const int row = it % S::NRp, g = it / S::NRp;
+      if (row < NR) {
+        const int a0 = row / Q, k2 = row % Q;
+        // pass 1: XV against (VV, DD); pass 2 (stiffness): XD against VV into YA
+        double xr[KB];
 #pragma unroll
-      for (int k = 0; k < Q; ++k) {
-        acc += y0[k] * z0[k];
-        if (stiff) acc += y1[k] * z1[k];
+        for (int kk = 0; kk < KB; ++kk) xr[kk] = X2[a0 * GC + kk * Q + k2].x;
+#pragma unroll
+        for (int j = 0; j < S::BG; ++j) {
+          const int b1 = g * S::BG + j;
+          if (b1 < NB1) {
+            const double2* pb = PB2 + b1 * KB;
+            double ya = 0.0, yb = 0.0;
+#pragma unroll
+            for (int kk = 0; kk < KB; ++kk) {
+              const double2 pp = pb[kk];
+              if (STIFF) {
+                ya += xr[kk] * pp.y;
+                yb += xr[kk] * pp.x;
+              } else {
+                ya += xr[kk] * pp.x;
+              }
+            }
+            Y2[(a0 * NB1 + b1) * Q + k2] = make_double2(ya, yb);
+          }
+        }
+        if (STIFF) {
+#pragma unroll
+          for (int kk = 0; kk < KB; ++kk) xr[kk] = X2[a0 * GC + kk * Q + k2].y;
+#pragma unroll
+          for (int j = 0; j < S::BG; ++j) {
+            const int b1 = g * S::BG + j;
+            if (b1 < NB1) {
+              const double2* pb = PB2 + b1 * KB;
+              double ya = 0.0;
+#pragma unroll
+              for (int kk = 0; kk < KB; ++kk) ya += xr[kk] * pb[kk].x;
+              Y2[(a0 * NB1 + b1) * Q + k2].x += ya;
+            }
+          }
+        }
       }
-      const int slot = (e2 + r) % m;
-      const int d2 = s - r + P;
-      R[(((ia * TB + ib) * m + slot) * NB + d0) * NB * NB + d1 * NB + d2] += acc;
+    }
+    __syncthreads();
+    // ---- stage S (axis 2): rolling rows R[row e2 + r] += sum_k2 Y Z(r, s)
+    for (int it = tid; it < S::NCp * S::NGS; it += nt) {
+      const int c = it % S::NCp, g = it / S::NCp;
+      if (c < NC) {
+        const int a0 = c / NB1, b1 = c % NB1;
+        const int ia = a0 / NB, d0 = a0 % NB, ib = b1 / NB, d1 = b1 % NB;
+        double ya[Q], yb[Q];
+#pragma unroll
+        for (int k = 0; k < Q; ++k) {
+          const double2 y = Y2[c * Q + k];
+          ya[k] = y.x;
+          yb[k] = y.y;
+        }
+        double* Rc = R + (ia * TB + ib) * m * S::rowVals + (d0 * NB + d1) * NB;
+#pragma unroll
+        for (int j = 0; j < S::SG; ++j) {
+          const int r = g * S::SG + j;
+          if (r < m) {
+            double* Rr = Rc + ((e2 + r) % m) * S::rowVals + P - r;
+#pragma unroll
+            for (int sidx = 0; sidx < m; ++sidx) {
+              const double2* z = Z2 + (r * m + sidx) * Q;
+              double acc = 0.0;
+#pragma unroll
+              for (int k = 0; k < Q; ++k) {
+                const double2 zz = z[k];
+                acc += ya[k] * zz.x;
+                if (STIFF) acc += yb[k] * zz.y;
+              }
+              Rr[sidx] += acc;
+            }
+          }
+        }
+      }
     }
     __syncthreads();
     // ---- write the finished rows I2 = e2 (and the tail rows after the last element) of
@@ -261,14 +333,56 @@ __global__ void __launch_bounds__(512, 2) k_gsf3(GsfArgs a) {
   }
 }
 
-template <int P>
+// tile sizes: the largest of (2,4), (2,2), (2,1), (1,1) whose shared memory fits
+template <int P, int Q, bool ST>
 struct GsfTile {
-  // tile sizes keep the shared-memory footprint under 227 KB
-  static constexpr int TA = P <= 3 ? 2 : (P == 4 ? 2 : 1);
-  static constexpr int TB = P <= 3 ? 4 : (P == 4 ? 2 : 1);
+  static constexpr size_t cap = 227 * 1024;
+  static constexpr int TA = GsfShape<P, Q, 2, 4, ST>::bytes <= cap ? 2
+                            : GsfShape<P, Q, 2, 2, ST>::bytes <= cap ? 2
+                            : GsfShape<P, Q, 2, 1, ST>::bytes <= cap ? 2 : 1;
+  static constexpr int TB = GsfShape<P, Q, 2, 4, ST>::bytes <= cap ? 4
+                            : GsfShape<P, Q, 2, 2, ST>::bytes <= cap ? 2 : 1;
 };
 
 int launch_gsf_p3(const GsfArgs& a, cudaStream_t s);  // iga_gsf_p3.cu (DMMA, p=3 q=4)
+
+template <int P, int Q, bool ST>
+static int launch_gsf_generic(const GsfArgs& a0, cudaStream_t s) {
+  constexpr int TA = GsfTile<P, Q, ST>::TA, TB = GsfTile<P, Q, ST>::TB;
+  using Sh = GsfShape<P, Q, TA, TB, ST>;
+  if constexpr (Sh::bytes > 227 * 1024) {
+    set_error("assembled sum factorization: p=%d q=%d needs %zu B shared memory", P, Q, Sh::bytes);
+    return IGA_EUNSUPPORTED;
+  } else {
+    GsfArgs a = a0;
+    const int64_t N = (int64_t)a.K + P;
+    const int planes = a.plane_end - a.plane_begin;
+    if (planes <= 0) return IGA_OK;
+    const int tiles0 = (planes + TA - 1) / TA;
+    a.tiles1 = (int)((N + TB - 1) / TB);
+    const int64_t tiles = (int64_t)tiles0 * a.tiles1;
+    const void* fn = reinterpret_cast<const void*>(k_gsf3<P, Q, TA, TB, ST>);
+    cudaError_t e = smem_attr_once(fn, Sh::bytes);
+    if (e != cudaSuccess) return check_cuda(e, "gsf smem attr");
+    // split the element column into segments when the tiles alone do not fill the GPU:
+    // minimise waves x (segment + halo) element iterations
+    const int64_t slots = (int64_t)sm_count() * blocks_per_sm_once(fn, kGsfThreads, Sh::bytes);
+    int best = 1;
+    double best_cost = 1e300;
+    for (int sg = 1; sg <= a.K; ++sg) {
+      const int L = (a.K + sg - 1) / sg;
+      if (L < P && sg > 1) break;
+      const int64_t ctas = tiles * sg;
+      const double waves = (double)((ctas + slots - 1) / slots);
+      const double cost = waves * (L + (sg > 1 ? P : 0));
+      if (cost < best_cost - 1e-9) { best_cost = cost; best = sg; }
+    }
+    a.segs = best;
+    a.seg_len = (a.K + best - 1) / best;
+    k_gsf3<P, Q, TA, TB, ST><<<(unsigned)(tiles * best), kGsfThreads, Sh::bytes, s>>>(a);
+    return check_cuda(cudaGetLastError(), "gsf launch");
+  }
+}
 
 template <int P, int Q>
 struct GsfLaunch {
@@ -278,40 +392,10 @@ struct GsfLaunch {
       const char* env = getenv("IGA_GSF_GENERIC");
       if (!(env && env[0] == '1')) return launch_gsf_p3(a0, s);
     }
-    constexpr int TA = GsfTile<P>::TA, TB = GsfTile<P>::TB;
-    using Sh = GsfShape<P, Q, TA, TB>;
-    if constexpr (Sh::bytes > 227 * 1024) {
-      set_error("assembled sum factorization: p=%d q=%d needs %zu B shared memory", P, Q, Sh::bytes);
-      return IGA_EUNSUPPORTED;
-    } else {
-      GsfArgs a = a0;
-      const int64_t N = (int64_t)a.K + P;
-      const int planes = a.plane_end - a.plane_begin;
-      if (planes <= 0) return IGA_OK;
-      const int tiles0 = (planes + TA - 1) / TA;
-      a.tiles1 = (int)((N + TB - 1) / TB);
-      const int64_t tiles = (int64_t)tiles0 * a.tiles1;
-      const void* fn = reinterpret_cast<const void*>(k_gsf3<P, Q, TA, TB>);
-      cudaError_t e = smem_attr_once(fn, Sh::bytes);
-      if (e != cudaSuccess) return check_cuda(e, "gsf smem attr");
-      // split the element column into segments when the tiles alone do not fill the GPU:
-      // minimise waves x (segment + halo) element iterations
-      const int64_t slots = (int64_t)sm_count() * blocks_per_sm_once(fn, 512, Sh::bytes);
-      int best = 1;
-      double best_cost = 1e300;
-      for (int sg = 1; sg <= a.K; ++sg) {
-        const int L = (a.K + sg - 1) / sg;
-        if (L < P && sg > 1) break;
-        const int64_t ctas = tiles * sg;
-        const double waves = (double)((ctas + slots - 1) / slots);
-        const double cost = waves * (L + (sg > 1 ? P : 0));
-        if (cost < best_cost - 1e-9) { best_cost = cost; best = sg; }
-      }
-      a.segs = best;
-      a.seg_len = (a.K + best - 1) / best;
-      k_gsf3<P, Q, TA, TB><<<(unsigned)(tiles * best), 512, Sh::bytes, s>>>(a);
-      return check_cuda(cudaGetLastError(), "gsf launch");
-    }
+    if (a0.op == IGA_OP_MASS) return launch_gsf_generic<P, Q, false>(a0, s);
+    if constexpr (P >= 1) return launch_gsf_generic<P, Q, true>(a0, s);
+    set_error("derivatives require degree >= 1");
+    return IGA_EINVAL;
   }
 };
 
