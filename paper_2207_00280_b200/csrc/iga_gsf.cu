@@ -313,18 +313,24 @@ __global__ void __launch_bounds__(kGsfThreads, 1) k_gsf3(GsfArgs a) {
       __syncthreads();
       const int lod2 = max(0, P - I2), c2 = (int)band_cnt(I2, P, N);
       for (int t = tid; t < TA * TB * S::rowVals; t += nt) {
-        const int rc = t / S::rowVals, v = t % S::rowVals;
-        const int d2 = v % NB, d1 = (v / NB) % NB, d0 = v / (NB * NB);
+        const int rc = t / S::rowVals, v = t - rc * S::rowVals;
         double* Rv = R + (rc * m + slot) * S::rowVals + v;
         if (write) {
           const int64_t off = rowoff[rc];
-          const int ia = rc / TB, ib = rc % TB;
+          const int ia = rc / TB, ib = rc - ia * TB;
           const int I0 = i00 + ia, I1 = i10 + ib;
-          const int lod0 = max(0, P - I0), lod1 = max(0, P - I1);
-          const int c0 = (int)band_cnt(I0, P, N), c1 = (int)band_cnt(I1, P, N);
-          if (off >= 0 && d0 >= lod0 && d0 < lod0 + c0 && d1 >= lod1 && d1 < lod1 + c1 &&
-              d2 >= lod2 && d2 < lod2 + c2)
-            a.values[off + ((d0 - lod0) * c1 + (d1 - lod1)) * c2 + (d2 - lod2)] = *Rv;
+          if (off >= 0) {
+            if (I0 >= P && I0 < K && I1 >= P && I1 < K && lod2 == 0 && c2 == NB) {
+              a.values[off + v] = *Rv;  // full band: CSR order is the R order
+            } else {
+              const int d2 = v % NB, d1 = (v / NB) % NB, d0 = v / (NB * NB);
+              const int lod0 = max(0, P - I0), lod1 = max(0, P - I1);
+              const int c0 = (int)band_cnt(I0, P, N), c1 = (int)band_cnt(I1, P, N);
+              if (d0 >= lod0 && d0 < lod0 + c0 && d1 >= lod1 && d1 < lod1 + c1 && d2 >= lod2 &&
+                  d2 < lod2 + c2)
+                a.values[off + ((d0 - lod0) * c1 + (d1 - lod1)) * c2 + (d2 - lod2)] = *Rv;
+            }
+          }
         }
         *Rv = 0.0;
       }
