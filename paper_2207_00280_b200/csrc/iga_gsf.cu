@@ -165,6 +165,28 @@ __global__ void __launch_bounds__(kGsfThreads, 1) k_gsf3(GsfArgs a) {
   };
   double cv[WPT];
   load_coef(e_first, cv);
+  // axis-2 pair products of element e2: the table entries are loaded one column ahead
+  constexpr int ZPT = cdiv(m * m * Q, kGsfThreads);
+  auto load_z = [&](int e2, double (&zv)[ZPT][4]) {
+#pragma unroll
+    for (int i = 0; i < ZPT; ++i) {
+      const int t = tid + i * nt;
+      zv[i][0] = zv[i][1] = zv[i][2] = zv[i][3] = 0.0;
+      if (t < m * m * Q && e2 < K) {
+        const int k = t % Q, sidx = (t / Q) % m, r = t / (Q * m);
+        const double* V2 = V + (int64_t)e2 * m * Q;
+        zv[i][0] = __ldg(V2 + r * Q + k);
+        zv[i][1] = __ldg(V2 + sidx * Q + k);
+        if (STIFF) {
+          const double* D2 = D + (int64_t)e2 * m * Q;
+          zv[i][2] = __ldg(D2 + r * Q + k);
+          zv[i][3] = __ldg(D2 + sidx * Q + k);
+        }
+      }
+    }
+  };
+  double zv[ZPT][4];
+  load_z(e_first, zv);
   for (int e2 = e_first; e2 < s1; ++e2) {
     __syncthreads();  // previous column's stage S (reads Y, aliasing W) is done
     // ---- stage W: weights x coefficient, [(la,k0)][(lb,k1,k2)]; Z: axis-2 pair products
@@ -178,18 +200,20 @@ __global__ void __launch_bounds__(kGsfThreads, 1) k_gsf3(GsfArgs a) {
       }
     }
     load_coef(e2 + 1, cv);
-    for (int t = tid; t < m * m * Q; t += nt) {
-      const int k = t % Q, sidx = (t / Q) % m, r = t / (Q * m);
-      const double* V2 = V + (int64_t)e2 * m * Q;
-      const double vv = V2[r * Q + k] * V2[sidx * Q + k];
-      double dd = 0.0;
-      if (STIFF) {
-        const double* D2 = D + (int64_t)e2 * m * Q;
-        dd = D2[r * Q + k] * D2[sidx * Q + k];
-        if (a.op == IGA_OP_STIFFNESS_MASS) dd += vv;
+#pragma unroll
+    for (int i = 0; i < ZPT; ++i) {
+      const int t = tid + i * nt;
+      if (t < m * m * Q) {
+        const double vv = zv[i][0] * zv[i][1];
+        double dd = 0.0;
+        if (STIFF) {
+          dd = zv[i][2] * zv[i][3];
+          if (a.op == IGA_OP_STIFFNESS_MASS) dd += vv;
+        }
+        Z2[t] = make_double2(vv, dd);
       }
-      Z2[t] = make_double2(vv, dd);
     }
+    load_z(e2 + 1, zv);
     __syncthreads();
     // ---- stage A (axis 0): X_T[a0][col] = sum_{(la,k0)} PA_T[a0][(la,k0)] W[(la,k0)][col]
     for (int it = tid; it < S::GCp * S::NGA; it += nt) {
