@@ -85,7 +85,7 @@ struct GsfShape {
 };
 
 template <int P, int Q, int TA, int TB, bool STIFF>
-__global__ void __launch_bounds__(kGsfThreads, 1) k_gsf3(GsfArgs a) {
+__global__ void __launch_bounds__(kGsfThreads, P <= 2 ? 2 : 1) k_gsf3(GsfArgs a) {
   using S = GsfShape<P, Q, TA, TB, STIFF>;
   constexpr int m = S::m, NB = S::NB, LA = S::LA, LB = S::LB, KA = S::KA, KB = S::KB;
   constexpr int GC = S::GC, NA0 = S::NA0, NB1 = S::NB1, NC = S::NC, NR = S::NR;
