@@ -287,6 +287,9 @@ def alt_leg(cfg, assembly, args, flush, stream, wl, total_el, peaks):
     kms = float(np.mean([a.elapsed_time(b) for a, b in kev]))
     K, p = wl["K"], wl["p"]
     roof = kernel_roofline(sess.code, wl, K, p, p + 1, K**3, 8 * sess.values.numel(), kms, peaks)
+    prof = os.path.join(ROOT, "profiles", f"ncu_{wl['name']}_{assembly}_traffic.json")
+    if os.path.exists(prof):
+        roof["traffic"] = json.load(open(prof)).get("dram_bytes_per_launch")
     out = {"assembly": assembly, "value": total_el / (ms / 1e3), "unit": "elements/s",
            "ms_per_step": ms, "gpu_launches": 2 * args.steps, "roofline": roof}
     del sess
@@ -312,7 +315,7 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     wname = args.workload or ("c3" if world == 1 else "c5")
-    wl = WORKLOADS[wname]
+    wl = dict(WORKLOADS[wname], name=wname)
     K, p = wl["K"], wl["p"]
     q = p + 1
 
