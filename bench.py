@@ -35,16 +35,12 @@ WORKLOADS = {
                     "assembled sum factorization"),
     "c3": dict(dim=3, K=64, p=3, op="stiffness", coef=None, method="sumfact",
                desc="C3: 3D Laplace stiffness 64^3 p=3 q=4 c=1, sum factorization fused with "
-                    "CSR assembly; run_integration's default path for a constant coefficient "
-                    "(separable: per-axis 1D Gauss quadrature + Kronecker CSR fill); the "
-                    "general per-quadrature-point DMMA kernel on the same matrix is "
-                    "reported in other_kernel"),
+                    "CSR assembly"),
     "c4": dict(dim=3, K=96, p=4, op="stiffness_mass", coef="sines", method="sumfact",
                desc="C4: 3D stiffness+mass 96^3 p=4 q=5, smooth 8-mode sine coefficient, "
                     "assembled sum factorization"),
     "c5": dict(dim=3, K=256, p=3, op="stiffness", coef=None, method="sumfact",
-               desc="C5: 3D Laplace stiffness 256^3 p=3 q=4 c=1, z-slabs + NCCL interface rows "
-                    "(default path: separable)"),
+               desc="C5: 3D Laplace stiffness 256^3 p=3 q=4 c=1, z-slabs + NCCL interface rows"),
 }
 
 
@@ -467,7 +463,10 @@ def main():
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded; no dataset)",
             "config": {"workload": wl["desc"], "K": K, "p": p, "q": q, "dim": wl["dim"],
                        "operator": wl["op"], "method": wl["method"],
-                       "kernel_path": KERNEL_NAMES[sess.code],
+                       "kernel_path": KERNEL_NAMES[sess.code] + (
+                           "; run_integration's default for a scalar coefficient (the general "
+                           "per-quadrature-point kernel on the same matrix: other_kernel)"
+                           if sess.code == 3 else ""),
                        "nnz": P.device.csr_nnz(wl["dim"], K, p),
                        "parallelism": f"element slabs x{world}" if world > 1 else "1 GPU",
                        "l2": "256 MB buffer written between timed steps (outside the per-step "
