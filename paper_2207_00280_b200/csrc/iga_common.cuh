@@ -48,16 +48,6 @@ __device__ __forceinline__ double knot(int i, int K, int p) {
   return dvd((double)(i - p), (double)K);
 }
 
-// Order-0 basis with the closed last span (splines.py:78-91).
-__device__ __forceinline__ double order0(int i, double x, int K, int p) {
-  const int nt = K + 2 * p + 1;
-  double ti = knot(i, K, p), ti1 = knot(i + 1, K, p);
-  if (ti <= x && x < ti1) return 1.0;
-  double tl = knot(nt - 1, K, p);
-  if (x == tl && ti < ti1 && ti1 == tl) return 1.0;
-  return 0.0;
-}
-
 // Bottom-up Cox-de Boor: N[j] holds B_{lo+j, level}(x).  The value of
 // B_{i,r}(x) does not depend on the recursion path, so evaluating the
 // triangle level by level with the same two-term expression as _cox

@@ -21,16 +21,18 @@
 //   stage B (axis 1): C[(a0,k2)][(r,s)] = sum_k1 X_T[a0][(lb,k1,k2)] PB_lb[k1][(r,s)]
 //                     -> Y_A/Y_B[(a0, ib = lb+r-3, d1)][k2]
 //   stage S (axis 2): C[c][(r,s)] = sum_k2 Y[c][k2] Z_e2[k2][(r,s)]
-//                     -> R[c][row e2+r][d2]  (registers, rolling over 4 rows)
+//                     -> R[c][row e2+r][d2]  (rolling over 4 rows)
 //
-// Warp specialisation (software pipeline over the element column e2): 2 warps
-// run stage A on element e2 = it, 2 warps stage B on e2 = it-1 and 8 warps stage
-// S (+ the row stores) on e2 = it-2, all concurrently, with double-buffered X
-// and Y and one CTA barrier per iteration.  The DMMA pipe of every SM
-// sub-partition is shared by the three stages, so it stays busy across what
-// would otherwise be barrier-separated phases.  The constant B fragments of
-// stages A and B and the rolling rows of stage S live in registers (384 threads
-// x 168 registers), which keeps shared-memory traffic well under the DMMA time.
+// Warp specialisation (software pipeline over the element column e2): 4 warps
+// run stage A on element e2 = it, 4 warps stage B on e2 = it-1 and 8 warps stage
+// S (+ the row stores) on e2 = it-2, all concurrently (512 threads x 128
+// registers).  X and Y are double-buffered and handed from role to role by
+// shared-memory mbarriers (full / empty per buffer), so no role waits for the
+// whole CTA.  The DMMA pipe of every SM sub-partition is shared by the three
+// stages and stays busy across what would otherwise be barrier-separated phases.
+// The constant B fragments of stages A and B live in registers; the rolling rows
+// of stage S live in per-lane shared-memory slots that are the DMMA C operands,
+// and a row leaves for the CSR straight from the register of its last product.
 #include "iga_args.cuh"
 #include "iga_dispatch.cuh"
 
@@ -103,12 +105,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, int parity) {
       : "memory");
 }
 
-// Is any column k in {2nt, 2nt+1} of window element l mapped to a destination
-// index l + k - P inside [lo, hi)?
-__host__ __device__ constexpr bool nt_useful(int l, int nt, int lo, int hi) {
-  return (l + 2 * nt - P >= lo && l + 2 * nt - P < hi) ||
-         (l + 2 * nt + 1 - P >= lo && l + 2 * nt + 1 - P < hi);
-}
 __host__ __device__ constexpr int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
 // B-fragment column mapping: lane (g, t) holds B[k=t][n=g]; column n of n-tile nt
