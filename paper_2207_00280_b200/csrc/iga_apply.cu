@@ -10,6 +10,7 @@
 // beta grad u), W = w w w jac c; backward: the transposed contractions, then
 // atomicAdd of the element result into y.  A CTA runs a batch of E elements.
 #include "iga_args.cuh"
+#include "iga_band.cuh"
 #include "iga_dispatch.cuh"
 
 namespace iga {
@@ -189,6 +190,118 @@ struct ApplyLaunch {
   }
 };
 
+// Scalar coefficient: the operator is a sum of Kronecker products of 1D band matrices
+// (iga_kron.cu header),  y = cj [ (alpha m0 + beta k0) c + beta m0 (k1 a + m1 b) ]
+// with a = m2 x, b = k2 x, c = m1 a (each a 2P+1-point stencil along one axis), so
+// y costs ~7 (2P+1) flops per dof instead of an element-by-element quadrature.
+// One CTA per T0 x T1 block of (I0, I1) dof lines, the lines swept in z-chunks of
+// ZC dofs; the x window (with a P halo on every side) and the intermediates live in
+// shared memory, and every y value is written once by its owner (no atomics).
+constexpr int AK_T = 4, AK_ZC = 32;
+
+template <int P>
+__host__ __device__ constexpr int apply_kron_work(int) {
+  return (AK_T + 2 * P) * (AK_T + 2 * P) * (AK_ZC + 2 * P) +      // X
+         2 * (AK_T + 2 * P) * (AK_T + 2 * P) * AK_ZC +           // (a, b)
+         2 * (AK_T + 2 * P) * AK_T * AK_ZC;                      // (c, de)
+}
+
+template <int P, int Q>
+__global__ void __launch_bounds__(256) k_apply_kron(ApplyArgs a) {
+  constexpr int NB = 2 * P + 1, T = AK_T, W = T + 2 * P, ZC = AK_ZC, ZH = ZC + 2 * P;
+  extern __shared__ __align__(16) double2 tb[];  // [N][NB] (m, k), then the work area
+  __shared__ double w_s[Q];
+  const int K = a.K, tid = threadIdx.x, nt = blockDim.x;
+  const int N = K + P;
+  const bool stiff = a.beta != 0.0;
+  double* work = reinterpret_cast<double*>(tb + N * NB);
+  double* X = work;                                        // [W][W][ZH]
+  double2* AB = reinterpret_cast<double2*>(X + W * W * ZH);  // [W][W][ZC]
+  double2* CD = AB + W * W * ZC;                           // [W][T][ZC]
+  build_band_tables<P, Q>(a.V, a.D, a.weights, K, stiff, 0, K, false, tb, work,
+                          apply_kron_work<P>(0), w_s, tid, nt);
+  const double cj = a.jac * a.coef_scalar;
+  const int nblk = (N + T - 1) / T;
+  for (int blk = blockIdx.x; blk < nblk * nblk; blk += gridDim.x) {
+    const int i0 = (blk / nblk) * T, j0 = (blk % nblk) * T;
+    for (int z0 = 0; z0 < N; z0 += ZC) {
+      __syncthreads();  // previous chunk's CD / X consumed
+      for (int u = tid; u < W * W * ZH; u += nt) {
+        const int w0 = u / (W * ZH), w1 = (u / ZH) % W, zz = u % ZH;
+        const int I0 = i0 - P + w0, I1 = j0 - P + w1, I2 = z0 - P + zz;
+        X[u] = (I0 >= 0 && I0 < N && I1 >= 0 && I1 < N && I2 >= 0 && I2 < N)
+                   ? a.x[((int64_t)I0 * N + I1) * N + I2]
+                   : 0.0;
+      }
+      __syncthreads();
+      // axis 2: a = m2 x, b = k2 x
+      for (int u = tid; u < W * W * ZC; u += nt) {
+        const int wl = u / ZC, z = u % ZC;
+        const double2* t = tb + min(z0 + z, N - 1) * NB;
+        const double* xl = X + wl * ZH + z;
+        double sa = 0.0, sb = 0.0;
+#pragma unroll
+        for (int d = 0; d < NB; ++d) {
+          sa += t[d].x * xl[d];
+          sb += t[d].y * xl[d];
+        }
+        AB[u] = make_double2(sa, sb);
+      }
+      __syncthreads();
+      // axis 1: c = m1 a, de = k1 a + m1 b
+      for (int u = tid; u < W * T * ZC; u += nt) {
+        const int w0 = u / (T * ZC), o1 = (u / ZC) % T, z = u % ZC;
+        const double2* t = tb + min(j0 + o1, N - 1) * NB;
+        const double2* ab = AB + (w0 * W + o1) * ZC + z;
+        double sc = 0.0, sd = 0.0;
+#pragma unroll
+        for (int d = 0; d < NB; ++d) {
+          const double2 v = ab[d * ZC];
+          sc += t[d].x * v.x;
+          sd += t[d].y * v.x + t[d].x * v.y;
+        }
+        CD[u] = make_double2(sc, sd);
+      }
+      __syncthreads();
+      // axis 0 and the output
+      for (int u = tid; u < T * T * ZC; u += nt) {
+        const int o0 = u / (T * ZC), o1 = (u / ZC) % T, z = u % ZC;
+        const int I0 = i0 + o0, I1 = j0 + o1, I2 = z0 + z;
+        if (I0 >= N || I1 >= N || I2 >= N) continue;
+        const double2* t = tb + I0 * NB;
+        const double2* cd = CD + (o0 * T + o1) * ZC + z;
+        double sy = 0.0;
+#pragma unroll
+        for (int d = 0; d < NB; ++d) {
+          const double2 v = cd[d * T * ZC];
+          sy += (a.alpha * t[d].x + a.beta * t[d].y) * v.x + a.beta * t[d].x * v.y;
+        }
+        a.y[((int64_t)I0 * N + I1) * N + I2] = cj * sy;
+      }
+    }
+  }
+}
+
+template <int P, int Q>
+struct ApplyKronLaunch {
+  static int run(const ApplyArgs& a, cudaStream_t s) {
+    const int N = a.K + P;
+    const size_t smem = sizeof(double2) * (size_t)N * (2 * P + 1) + sizeof(double) * apply_kron_work<P>(0);
+    if (smem > 220 * 1024) {
+      set_error("separable apply: 1D band tables of K=%d do not fit shared memory", a.K);
+      return IGA_EUNSUPPORTED;
+    }
+    const void* fn = reinterpret_cast<const void*>(k_apply_kron<P, Q>);
+    cudaError_t e = smem_attr_once(fn, smem, true);
+    if (e != cudaSuccess) return check_cuda(e, "apply smem attr");
+    const int nblk = (N + AK_T - 1) / AK_T;
+    const int64_t slots = (int64_t)sm_count() * blocks_per_sm_once(fn, 256, smem);
+    const int64_t grid = (int64_t)nblk * nblk < slots ? (int64_t)nblk * nblk : slots;
+    k_apply_kron<P, Q><<<(unsigned)grid, 256, smem, s>>>(a);
+    return check_cuda(cudaGetLastError(), "iga_apply (separable) launch");
+  }
+};
+
 }  // namespace iga
 
 using namespace iga;
@@ -202,11 +315,15 @@ extern "C" int32_t iga_apply(const iga_problem* prob, double alpha, double beta,
   if (!prob->weights || !prob->tables_v || !x || !y) return fail_einval("null pointer");
   const int64_t N = (int64_t)prob->K + prob->p;
   cudaStream_t s = as_stream(stream);
-  int rc = check_cuda(cudaMemsetAsync(y, 0, sizeof(double) * N * N * N, s), "zero y");
-  if (rc) return rc;
   ApplyArgs a;
   a.K = prob->K; a.alpha = alpha; a.beta = beta; a.jac = prob->jac;
   a.coef_scalar = prob->coef_scalar; a.coef = prob->coef; a.weights = prob->weights;
   a.V = prob->tables_v; a.D = prob->tables_d; a.x = x; a.y = y;
+  if (!prob->coef) {  // scalar coefficient: separable operator, y written once per dof
+    const int rc = dispatch_pq<ApplyKronLaunch>(prob->p, prob->q, a, s);
+    if (rc != IGA_EUNSUPPORTED) return rc;  // (too large for the shared-memory tables)
+  }
+  int rc = check_cuda(cudaMemsetAsync(y, 0, sizeof(double) * N * N * N, s), "zero y");
+  if (rc) return rc;
   return dispatch_pq<ApplyLaunch>(prob->p, prob->q, a, s);
 }

@@ -20,37 +20,10 @@
 // contiguous in the CSR; they are produced in shared memory a few rows at a time
 // and written by TMA bulk stores.
 #include "iga_args.cuh"
+#include "iga_band.cuh"
 #include "iga_dispatch.cuh"
 
 namespace iga {
-
-// 1D band entry (I, J = I + d - P) over the elements e in [e_lo, e_hi): value and
-// derivative products, elements ascending, quadrature points ascending.
-template <int P, int Q>
-__device__ __forceinline__ double2 band1d(const double* V, const double* D, int K, const double* w,
-                                          int I, int d, int e_lo, int e_hi, bool stiff) {
-  constexpr int M = P + 1;
-  const int J = I + d - P;
-  double m = 0.0, k = 0.0;
-  const int lo = max(max(I, J) - P, max(e_lo, 0)), hi = min(min(I, J) + 1, min(e_hi, K));
-  // at most P+1 elements
-#pragma unroll
-  for (int t = 0; t <= P; ++t) {
-    const int e = lo + t;
-    if (e < hi) {
-      const double* Ve = V + e * M * Q;
-      const int i = I - e, j = J - e;
-#pragma unroll
-      for (int q = 0; q < Q; ++q) m += (w[q] * Ve[i * Q + q]) * Ve[j * Q + q];
-      if (stiff) {
-        const double* De = D + e * M * Q;
-#pragma unroll
-        for (int q = 0; q < Q; ++q) k += (w[q] * De[i * Q + q]) * De[j * Q + q];
-      }
-    }
-  }
-  return make_double2(m, k);
-}
 
 #ifndef KRON_MINB
 #define KRON_MINB 2
@@ -103,64 +76,8 @@ __global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) 
   const bool full = a.el_begin <= 0 && a.el_end >= K;
   const double2* tb0 = full ? tb : tb + N * NB;
   double* stage = reinterpret_cast<double*>(tb + 2 * N * NB);  // [2][SG]
-  // 1D band tables.  When they fit in the staging area (small K, where this prologue
-  // is not amortised), the element integrals m_e(r,s), k_e(r,s) are formed first
-  // (one short dot product per thread) and summed per band entry over the <= P+1
-  // elements of the pair; otherwise each band entry is integrated directly from
-  // the global tables.
-  constexpr int M = P + 1;
-  const int nvd = K * M * Q, nem = K * M * M;
-  const bool small = 2 * nvd + 2 * nem <= 2 * SG;
-  if (tid < Q) w[tid] = a.weights[tid];
-  if (small) {
-    double* Vs = stage;
-    double* Ds = stage + nvd;
-    double2* em = reinterpret_cast<double2*>(stage + 2 * nvd);  // [K][M][M] (m, k)
-    for (int u = tid; u < nvd; u += NT) {
-      Vs[u] = __ldg(a.V + u);
-      if (stiff) Ds[u] = __ldg(a.D + u);
-    }
-    __syncthreads();
-    for (int u = tid; u < nem; u += NT) {
-      const int e = u / (M * M), r = (u / M) % M, c = u % M;
-      const double* vr = Vs + (e * M + r) * Q;
-      const double* vc = Vs + (e * M + c) * Q;
-      double m = 0.0, k = 0.0;
-#pragma unroll
-      for (int q = 0; q < Q; ++q) m += (w[q] * vr[q]) * vc[q];
-      if (stiff) {
-        const double* dr = Ds + (e * M + r) * Q;
-        const double* dc = Ds + (e * M + c) * Q;
-#pragma unroll
-        for (int q = 0; q < Q; ++q) k += (w[q] * dr[q]) * dc[q];
-      }
-      em[u] = make_double2(m, k);
-    }
-    __syncthreads();
-    for (int u = tid; u < (full ? 1 : 2) * N * NB; u += NT) {
-      const int v = u < N * NB ? u : u - (int)(N * NB);
-      const bool slab = u >= N * NB;
-      const int I = v / NB, J = I + v % NB - P;
-      const int lo = max(max(I, J) - P, slab ? max(a.el_begin, 0) : 0);
-      const int hi = min(min(I, J) + 1, slab ? min(a.el_end, K) : K);
-      double m = 0.0, k = 0.0;
-      for (int e = lo; e < hi; ++e) {
-        const double2 x = em[(e * M + I - e) * M + J - e];
-        m += x.x;
-        k += x.y;
-      }
-      tb[u] = make_double2(m, k);
-    }
-  } else {
-    __syncthreads();
-    for (int u = tid; u < (full ? 1 : 2) * N * NB; u += NT) {
-      const int v = u < N * NB ? u : u - (int)(N * NB);
-      const bool slab = u >= N * NB;
-      tb[u] = band1d<P, Q>(a.V, a.D, K, w, v / NB, v % NB, slab ? a.el_begin : 0,
-                           slab ? a.el_end : K, stiff);
-    }
-  }
-  __syncthreads();
+  build_band_tables<P, Q>(a.V, a.D, a.weights, K, stiff, a.el_begin, a.el_end, !full, tb, stage,
+                          2 * SG, w, tid, NT);
 
 #ifdef KRON_PROLOGUE_ONLY
   if (a.K > 0) return;
