@@ -44,20 +44,27 @@ class MatrixFreeOperator:
         return self.apply(mu, 1.0, -float(dt))
 
 
-def cg(gram, b, x0=None, rtol: float = 1e-10, maxiter: int | None = None):
-    """Conjugate gradients on the device for the assembled GlobalGram (SPD)."""
+def cg(A, b, x0=None, rtol: float = 1e-10, maxiter: int | None = None, alpha: float = 1.0,
+       beta: float = 0.0):
+    """Conjugate gradients on the device (HeatProblem._solve, heat.py:168-175: rtol 1e-10,
+    maxiter 10 n).  ``A`` is an assembled GlobalGram (SpMV on the structured CSR) or a
+    MatrixFreeOperator applied as ``alpha M + beta S`` (SPD for alpha > 0, beta >= 0)."""
     torch = _lib.require_cuda()
     L = _lib.load()
-    n = gram.n_dofs
+    n = A.n_dofs
     bd = torch.as_tensor(np.ascontiguousarray(b, dtype=np.float64)).cuda()
     x = torch.zeros_like(bd) if x0 is None else torch.as_tensor(
         np.ascontiguousarray(x0, dtype=np.float64)).cuda()
     Ap = torch.empty_like(bd)
 
-    def spmv(v, out):
-        _lib.check(L.iga_spmv(gram.dim, gram.K, gram.p, gram.values.data_ptr(), v.data_ptr(),
-                              out.data_ptr(), _lib.stream_ptr()))
-        return out
+    if isinstance(A, MatrixFreeOperator):
+        def spmv(v, out):
+            return A.apply(v, alpha, beta, out=out)
+    else:
+        def spmv(v, out):
+            _lib.check(L.iga_spmv(A.dim, A.K, A.p, A.values.data_ptr(), v.data_ptr(),
+                                  out.data_ptr(), _lib.stream_ptr()))
+            return out
 
     r = bd - spmv(x, Ap)
     p = r.clone()
@@ -69,9 +76,9 @@ def cg(gram, b, x0=None, rtol: float = 1e-10, maxiter: int | None = None):
         if torch.sqrt(rr) <= tol:
             return x.cpu().numpy(), it
         spmv(p, Ap)
-        alpha = rr / torch.dot(p, Ap)
-        x += alpha * p
-        r -= alpha * Ap
+        step = rr / torch.dot(p, Ap)
+        x += step * p
+        r -= step * Ap
         rr_new = torch.dot(r, r)
         p = r + (rr_new / rr) * p
         rr = rr_new

@@ -447,3 +447,22 @@ def test_matrix_market_export_streams_from_device(pkg, tmp_path, K, p, op):
 
     back = scipy.io.mmread(str(f)).tocsr()  # symmetric file: the lower triangle, mirrored
     assert abs(scipy.sparse.tril(back) - scipy.sparse.tril(gram.matrix)).max() == 0.0
+
+
+def test_cg_matrix_free_implicit_heat_step(pkg):
+    """(M + dt S) u = M mu solved matrix-free (separable apply) matches the assembled
+    operators' solution."""
+    import scipy.sparse.linalg as spla
+
+    from paper_2207_00280_b200.operator import MatrixFreeOperator, cg
+
+    K, p, dt = 6, 3, 0.01
+    op = MatrixFreeOperator(K, p)
+    mu = np.random.default_rng(9).standard_normal(op.n_dofs)
+    b = op.apply(mu, 1.0, 0.0)
+    x, it = cg(op, b, rtol=1e-12, alpha=1.0, beta=dt)
+    M = pkg.run_integration(pkg.RunConfig("sumfact", "device", K, p, assembly="owner")).gram.matrix
+    S = pkg.run_integration(pkg.RunConfig("sumfact", "device", K, p, operator="stiffness",
+                                          assembly="owner")).gram.matrix
+    ref = spla.spsolve((M + dt * S).tocsc(), M @ mu)
+    assert np.linalg.norm(x - ref) <= 1e-9 * np.linalg.norm(ref)
