@@ -83,3 +83,14 @@ def cg(A, b, x0=None, rtol: float = 1e-10, maxiter: int | None = None, alpha: fl
         p = r + (rr_new / rr) * p
         rr = rr_new
     raise RuntimeError("conjugate gradient did not converge")
+
+
+def heat_step(op: MatrixFreeOperator, mu, dt: float, rtol: float = 1e-10):
+    """One forward-Euler step of the heat demo on the device (HeatProblem.step,
+    heat.py:101-107): L = M mu - dt S mu (assemble_rhs), then G mu' = L by CG from
+    x0 = mu with the Gram (mass) operator applied matrix-free."""
+    if dt < 0:
+        raise ValueError("timestep must be >= 0")
+    L = op.rhs(mu, dt)
+    x, _ = cg(op, L, x0=mu, rtol=rtol, alpha=1.0, beta=0.0)
+    return x

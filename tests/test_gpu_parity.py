@@ -466,3 +466,24 @@ def test_cg_matrix_free_implicit_heat_step(pkg):
                                           assembly="owner")).gram.matrix
     ref = spla.spsolve((M + dt * S).tocsc(), M @ mu)
     assert np.linalg.norm(x - ref) <= 1e-9 * np.linalg.norm(ref)
+
+
+def test_heat_step_matches_assembled_reference(pkg):
+    """HeatProblem.step semantics (heat.py:101-107) on the device: M mu' = M mu - dt S mu."""
+    import scipy.sparse.linalg as spla
+
+    from paper_2207_00280_b200.operator import MatrixFreeOperator, heat_step
+
+    K, p = 5, 2
+    dt = (1.0 / K) ** 2 / 6.0  # heat.stable_timestep
+    op = MatrixFreeOperator(K, p)
+    mu = 1.0 + np.random.default_rng(4).standard_normal(op.n_dofs) * 0.1
+    got = heat_step(op, mu, dt)
+    M = pkg.run_integration(pkg.RunConfig("sumfact", "device", K, p, assembly="owner")).gram.matrix
+    S = pkg.run_integration(pkg.RunConfig("sumfact", "device", K, p, operator="stiffness",
+                                          assembly="owner")).gram.matrix
+    ref = spla.spsolve(M.tocsc(), M @ mu - dt * (S @ mu))
+    assert np.linalg.norm(got - ref) <= 1e-8 * np.linalg.norm(ref)
+    # mass conservation with Neumann boundaries: the total integral is unchanged
+    ones = np.ones(op.n_dofs)
+    assert abs(ones @ (M @ got) - ones @ (M @ mu)) <= 1e-10 * abs(ones @ (M @ mu))
