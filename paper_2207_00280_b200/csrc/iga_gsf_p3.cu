@@ -333,13 +333,12 @@ __device__ __forceinline__ void stage_s_batch(const Lane& L, int ws, const doubl
   }
 }
 
-template <int PHI>
-__device__ __forceinline__ void stage_s(const Lane& L, int ws, const double* Y, double* Rs,
-                                        const GsfArgs& a, int e2, const int (&meta)[MT_S_PER_WARP],
-                                        const int64_t* pb, const int* pc, int64_t N) {
+// axis-2 B fragments of element e2 (value and derivative pair products); the S warps
+// compute them one element ahead so the table loads are off the critical path
+__device__ __forceinline__ void s_fragments(const Lane& L, const GsfArgs& a, int e2, double (&b0)[2],
+                                            double (&b1)[2]) {
   const int g = L.g, t = L.t;
   const double* V2 = a.V + (int64_t)e2 * M * Q;
-  double b0[2], b1[2];
 #pragma unroll
   for (int nt = 0; nt < 2; ++nt) {
     const int r = bcol_r(nt, g), s = bcol_s(nt, g);
@@ -352,6 +351,14 @@ __device__ __forceinline__ void stage_s(const Lane& L, int ws, const double* Y, 
       b1[nt] = z;
     }
   }
+}
+
+template <int PHI>
+__device__ __forceinline__ void stage_s(const Lane& L, int ws, const double* Y, double* Rs,
+                                        const GsfArgs& a, int e2, const int (&meta)[MT_S_PER_WARP],
+                                        const int64_t* pb, const int* pc, int64_t N,
+                                        const double (&b0)[2], const double (&b1)[2]) {
+  const int t = L.t;
   const RowDst rd = row_dst(t, e2, N);
   static_assert(MT_S == (MT_S_PER_WARP - 1) * NWS + 1, "stage S warp split");
   stage_s_batch<PHI, 0, 3>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd);
@@ -541,6 +548,8 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
     }
     double* Rs = sm + OFF_R;
     for (int u = ws * 32 + L.lane; u < MT_S * 4 * 2 * 32; u += NWS * 32) Rs[u] = 0.0;
+    double sb0[2], sb1[2];
+    s_fragments(L, a, 0, sb0, sb1);
     __syncthreads();
     for (int e2 = 0; e2 < K; ++e2) {
       const int it = e2 + 2;
@@ -549,11 +558,12 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
       mbar_wait(yfull + b, (e2 >> 1) & 1);
       const double* Y = sm + OFF_Y + b * SZ_Y;
       switch (e2 & 3) {
-        case 0: stage_s<0>(L, ws, Y, Rs, a, e2, meta, pb, pc, N); break;
-        case 1: stage_s<1>(L, ws, Y, Rs, a, e2, meta, pb, pc, N); break;
-        case 2: stage_s<2>(L, ws, Y, Rs, a, e2, meta, pb, pc, N); break;
-        default: stage_s<3>(L, ws, Y, Rs, a, e2, meta, pb, pc, N); break;
+        case 0: stage_s<0>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1); break;
+        case 1: stage_s<1>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1); break;
+        case 2: stage_s<2>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1); break;
+        default: stage_s<3>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1); break;
       }
+      if (e2 + 1 < K) s_fragments(L, a, e2 + 1, sb0, sb1);
       mbar_arrive(yempty + b);
       PT(0);
       PT(1);
