@@ -487,3 +487,19 @@ def test_heat_step_matches_assembled_reference(pkg):
     # mass conservation with Neumann boundaries: the total integral is unchanged
     ones = np.ones(op.n_dofs)
     assert abs(ones @ (M @ got) - ones @ (M @ mu)) <= 1e-10 * abs(ones @ (M @ mu))
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("K", [1, 2])
+def test_tiny_meshes_all_paths(pkg, K, p):
+    """Degenerate meshes (K <= p: every row truncated on both sides) through every
+    device path, every operator, against the oracle."""
+    for op in ("mass", "stiffness", "stiffness_mass"):
+        ip, _, ref = O.integrate_assemble(3, K, p, op, "classical")
+        _, _, A = O.integrate_assemble(3, K, p, op, "classical", absolute=True)
+        for method, assembly in (("sumfact", "owner"), ("sumfact", "separable"),
+                                 ("sumfact", "scatter"), ("classical", "auto")):
+            res = pkg.run_integration(pkg.RunConfig(method, "device", K, p, operator=op,
+                                                    assembly=assembly))
+            v = res.gram.values.cpu().numpy()
+            assert_parity(v, ref, ip, absref=A, what=f"{op} K={K} p={p} {method}/{assembly}")
