@@ -375,6 +375,7 @@ struct GsfTile {
 };
 
 int launch_gsf_p3(const GsfArgs& a, cudaStream_t s);  // iga_gsf_p3.cu (DMMA, p=3 q=4)
+int launch_gsf_mma(const GsfArgs& a, int p, int q, cudaStream_t s);  // iga_gsf_mma.cu (DMMA)
 
 template <int P, int Q, bool ST>
 static int launch_gsf_generic(const GsfArgs& a0, cudaStream_t s) {
@@ -422,6 +423,9 @@ struct GsfLaunch {
       const char* env = getenv("IGA_GSF_GENERIC");
       if (!(env && env[0] == '1')) return launch_gsf_p3(a0, s);
     }
+    // DMMA GEMM formulation; IGA_GSF_SCALAR=1 selects this file's scalar kernel (A/B tests)
+    const char* sc = getenv("IGA_GSF_SCALAR");
+    if (!(sc && sc[0] == '1')) return launch_gsf_mma(a0, P, Q, s);
     if (a0.op == IGA_OP_MASS) return launch_gsf_generic<P, Q, false>(a0, s);
     if constexpr (P >= 1) return launch_gsf_generic<P, Q, true>(a0, s);
     set_error("derivatives require degree >= 1");

@@ -1,0 +1,340 @@
+// Assembled sum factorization for every (p, q) on FP64 tensor cores (DMMA.8x8x4).
+//
+// Same mathematics, tiling and element-column streaming as the scalar generic
+// kernel (iga_gsf.cu header): per element column e2 a CTA forms the weights W of
+// its quadrature slab and runs the three contractions, each a small dense GEMM
+// against the CTA's constant pair-product tables (invalid element/row pairs carry
+// zeros, so the GEMMs need no data-dependent structure):
+//
+//   stage A: X_T[a0][col]        = sum_kk PA_T[a0][kk] W[kk][col]     (M = TA(2P+1),
+//                                                                      N = cols, K = (TA+P) q)
+//   stage B: Y[(a0,k2)][b1]      = sum_kk X[a0][kk][k2] PB[b1][kk]    (three products)
+//   stage S: R[combo][(r,s)]    += sum_k2 Y[combo][k2] Z_e2[k2][(r,s)] (scattered into the
+//                                                                      rolling rows)
+//
+// Warps take (m-tile, n-tile) items of each GEMM; operands are read from shared
+// memory per k-step as DMMA fragments (lane (g,t): A[g][t], B[t][g]; out-of-range
+// rows/columns/k predicated to zero, nothing is padded in memory), and the
+// accumulators leave as the C fragments (C[g][2t], C[g][2t+1]).  k_gsf3_p3 keeps
+// its hand-scheduled p = 3, q = 4 pipeline; this kernel serves the other degrees.
+#include <cstdlib>
+
+#include "iga_args.cuh"
+#include "iga_dispatch.cuh"
+
+namespace iga {
+namespace mma {
+
+constexpr int NT = 512;
+__host__ __device__ constexpr int cdiv(int a, int b) { return (a + b - 1) / b; }
+
+template <int P, int Q, int TA, int TB>
+struct Shape {
+  static constexpr int m = P + 1, NB = 2 * P + 1;
+  static constexpr int LA = TA + P, LB = TB + P;
+  static constexpr int KA = LA * Q, KB = LB * Q;  // contraction lengths of stages A, B
+  static constexpr int GC = KB * Q;               // stage-A columns (lb, k1, k2)
+  static constexpr int NA0 = TA * NB, NB1 = TB * NB, NC = NA0 * NB1, NR = NA0 * Q;
+  static constexpr int rowVals = NB * NB * NB;
+  static constexpr int nW = KA * GC, nY = 2 * NC * Q;
+  static constexpr int nWY = nW > nY ? nW : nY;   // Y aliases W (W is dead after stage A)
+  static constexpr int nX = 2 * NA0 * GC;
+  static constexpr int nPA = 2 * NA0 * KA, nPB = 2 * NB1 * KB;
+  static constexpr int nZ = 2 * m * m * Q;
+  static constexpr int nR = TA * TB * m * rowVals;
+  static constexpr size_t bytes = sizeof(double) * ((size_t)nWY + nX + nPA + nPB + nZ + nR);
+};
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+
+template <int P, int Q, int TA, int TB, bool STIFF>
+__global__ void __launch_bounds__(NT, 1) k_gsf3_mma(GsfArgs a) {
+  using S = Shape<P, Q, TA, TB>;
+  constexpr int m = S::m, NB = S::NB, KA = S::KA, KB = S::KB, GC = S::GC;
+  constexpr int NA0 = S::NA0, NB1 = S::NB1, NC = S::NC, NR = S::NR;
+  extern __shared__ double smem[];
+  double* sW = smem;                                         // [KA][GC]
+  double2* Y2 = reinterpret_cast<double2*>(smem);            // [NC][Q] (aliases W)
+  double2* X2 = reinterpret_cast<double2*>(smem + S::nWY);   // [NA0][GC] (XV, XD)
+  double2* PA2 = X2 + NA0 * GC;                              // [NA0][KA] (VV, DD)
+  double2* PB2 = PA2 + NA0 * KA;                             // [NB1][KB] (VV, DD)
+  double2* Z2 = PB2 + NB1 * KB;                              // [Q][m*m] (VV, DD(+VV))
+  double* R = reinterpret_cast<double*>(Z2 + m * m * Q);     // [TA*TB][m][rowVals]
+  __shared__ int64_t rowoff[TA * TB];
+
+  const int K = a.K;
+  const int64_t N = (int64_t)K + P;
+  const int tile = blockIdx.x / a.segs, seg = blockIdx.x % a.segs;
+  const int tile0 = tile / a.tiles1, tile1 = tile % a.tiles1;
+  const int i00 = a.plane_begin + tile0 * TA, i10 = tile1 * TB;
+  const int s0 = seg * a.seg_len, s1 = min(K, s0 + a.seg_len);
+  const int e_first = max(0, s0 - P);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
+  constexpr int NWARP = NT / 32;
+  const int e0lo = max(a.el_begin, 0), e0hi = min(a.el_end, K);
+  const double* V = a.V;
+  const double* D = a.D;
+
+  // ---- constant pair tables (axis 0 slab-restricted, axis 1)
+  for (int u = tid; u < NA0 * KA; u += NT) {
+    const int a0 = u / KA, kk = u % KA, la = kk / Q, k0 = kk % Q;
+    const int I0 = i00 + a0 / NB, J0 = I0 - P + a0 % NB, e0 = i00 - P + la;
+    const int r = I0 - e0, sc = J0 - e0;
+    double2 v = make_double2(0.0, 0.0);
+    if (e0 >= e0lo && e0 < e0hi && r >= 0 && r <= P && sc >= 0 && sc <= P && J0 >= 0 && J0 < N) {
+      v.x = V[((int64_t)e0 * m + r) * Q + k0] * V[((int64_t)e0 * m + sc) * Q + k0];
+      if (STIFF) v.y = D[((int64_t)e0 * m + r) * Q + k0] * D[((int64_t)e0 * m + sc) * Q + k0];
+    }
+    PA2[u] = v;
+  }
+  for (int u = tid; u < NB1 * KB; u += NT) {
+    const int b1 = u / KB, kk = u % KB, lb = kk / Q, k1 = kk % Q;
+    const int I1 = i10 + b1 / NB, J1 = I1 - P + b1 % NB, e1 = i10 - P + lb;
+    const int r = I1 - e1, sc = J1 - e1;
+    double2 v = make_double2(0.0, 0.0);
+    if (e1 >= 0 && e1 < K && r >= 0 && r <= P && sc >= 0 && sc <= P && J1 >= 0 && J1 < N) {
+      v.x = V[((int64_t)e1 * m + r) * Q + k1] * V[((int64_t)e1 * m + sc) * Q + k1];
+      if (STIFF) v.y = D[((int64_t)e1 * m + r) * Q + k1] * D[((int64_t)e1 * m + sc) * Q + k1];
+    }
+    PB2[u] = v;
+  }
+  for (int u = tid; u < S::nR; u += NT) R[u] = 0.0;
+
+  // coefficient of the next element column for this thread's W entries
+  constexpr int WPT = cdiv(S::nW, NT);
+  auto load_coef = [&](int e2, double (&cv)[WPT]) {
+#pragma unroll
+    for (int i = 0; i < WPT; ++i) {
+      const int u = tid + i * NT;
+      cv[i] = a.coef_scalar;
+      if (a.coef && u < S::nW && e2 < K) {
+        const int kk = u / GC, col = u % GC;
+        const int la = kk / Q, k0 = kk % Q, lb = col / (Q * Q), k1 = (col / Q) % Q, k2 = col % Q;
+        const int e0 = i00 - P + la, e1 = i10 - P + lb;
+        if (e0 >= 0 && e0 < K && e1 >= 0 && e1 < K)
+          cv[i] = __ldg(a.coef + (((int64_t)e0 * K + e1) * K + e2) * (Q * Q * Q) + (k0 * Q + k1) * Q + k2);
+      }
+    }
+  };
+  double cv[WPT];
+  load_coef(e_first, cv);
+
+  for (int e2 = e_first; e2 < s1; ++e2) {
+    __syncthreads();  // previous column's stage S (reads Y, aliasing W) and flush are done
+#pragma unroll
+    for (int i = 0; i < WPT; ++i) {
+      const int u = tid + i * NT;
+      if (u < S::nW) {
+        const int kk = u / GC, col = u % GC;
+        const int k0 = kk % Q, k1 = (col / Q) % Q, k2 = col % Q;
+        sW[u] = a.weights[k0] * a.weights[k1] * a.weights[k2] * a.jac * cv[i];
+      }
+    }
+    load_coef(e2 + 1, cv);
+    for (int u = tid; u < m * m * Q; u += NT) {  // Z[k2][(r,s)]
+      const int k = u / (m * m), n = u % (m * m), r = n / m, sc = n % m;
+      const double* V2 = V + (int64_t)e2 * m * Q;
+      const double vv = V2[r * Q + k] * V2[sc * Q + k];
+      double dd = 0.0;
+      if (STIFF) {
+        const double* D2 = D + (int64_t)e2 * m * Q;
+        dd = D2[r * Q + k] * D2[sc * Q + k];
+        if (a.op == IGA_OP_STIFFNESS_MASS) dd += vv;
+      }
+      Z2[u] = make_double2(vv, dd);
+    }
+    __syncthreads();
+
+    // ---- stage A: X_T[a0][col] = sum_kk PA_T[a0][kk] W[kk][col]
+    {
+      constexpr int MT = cdiv(NA0, 8), NTL = cdiv(GC, 8), KS = cdiv(KA, 4);
+      for (int item = warp; item < MT * NTL; item += NWARP) {
+        const int mt = item % MT, ntl = item / MT;
+        const int row = mt * 8 + g, col = ntl * 8 + g;
+        double cv0 = 0.0, cv1 = 0.0, cd0 = 0.0, cd1 = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+          const int kk = ks * 4 + t;
+          const double2 pa = (row < NA0 && kk < KA) ? PA2[row * KA + kk] : make_double2(0.0, 0.0);
+          const double w = (kk < KA && col < GC) ? sW[kk * GC + col] : 0.0;
+          dmma(cv0, cv1, pa.x, w);
+          if (STIFF) dmma(cd0, cd1, pa.y, w);
+        }
+        const int c0 = ntl * 8 + 2 * t;
+        if (row < NA0) {
+          if (c0 < GC) X2[row * GC + c0] = make_double2(cv0, cd0);
+          if (c0 + 1 < GC) X2[row * GC + c0 + 1] = make_double2(cv1, cd1);
+        }
+      }
+    }
+    __syncthreads();
+
+    // ---- stage B: rows (a0, k2), columns b1:
+    //   mass YA = XV VV;  stiffness YA = XV DD + XD VV, YB = XV VV
+    {
+      constexpr int MT = cdiv(NR, 8), NTL = cdiv(NB1, 8), KS = cdiv(KB, 4);
+      for (int item = warp; item < MT * NTL; item += NWARP) {
+        const int mt = item % MT, ntl = item / MT;
+        const int row = mt * 8 + g, b1 = ntl * 8 + g;
+        const int a0 = row / Q, k2 = row % Q;
+        double ya0 = 0.0, ya1 = 0.0, yb0 = 0.0, yb1 = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+          const int kk = ks * 4 + t;
+          const double2 x = (row < NR && kk < KB) ? X2[a0 * GC + kk * Q + k2] : make_double2(0.0, 0.0);
+          const double2 pb = (b1 < NB1 && kk < KB) ? PB2[b1 * KB + kk] : make_double2(0.0, 0.0);
+          if (STIFF) {
+            dmma(ya0, ya1, x.x, pb.y);
+            dmma(ya0, ya1, x.y, pb.x);
+            dmma(yb0, yb1, x.x, pb.x);
+          } else {
+            dmma(ya0, ya1, x.x, pb.x);
+          }
+        }
+        // C[g][2t..2t+1]: row (a0,k2) = mt*8+g, columns b1 = ntl*8 + 2t, +1
+        const int rr = mt * 8 + g, ra0 = rr / Q, rk2 = rr % Q, c0 = ntl * 8 + 2 * t;
+        if (rr < NR) {
+          if (c0 < NB1) Y2[(ra0 * NB1 + c0) * Q + rk2] = make_double2(ya0, yb0);
+          if (c0 + 1 < NB1) Y2[(ra0 * NB1 + c0 + 1) * Q + rk2] = make_double2(ya1, yb1);
+        }
+      }
+    }
+    __syncthreads();
+
+    // ---- stage S: C[combo][(r,s)] = sum_k2 Y[combo][k2] Z[k2][(r,s)] into the rolling rows
+    {
+      constexpr int MM = m * m, MT = cdiv(NC, 8), NTL = cdiv(MM, 8), KS = cdiv(Q, 4);
+      for (int item = warp; item < MT * NTL; item += NWARP) {
+        const int mt = item % MT, ntl = item / MT;
+        const int combo = mt * 8 + g, n = ntl * 8 + g;
+        double c0v = 0.0, c1v = 0.0;
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+          const int k = ks * 4 + t;
+          const double2 y = (combo < NC && k < Q) ? Y2[combo * Q + k] : make_double2(0.0, 0.0);
+          const double2 z = (n < MM && k < Q) ? Z2[k * MM + n] : make_double2(0.0, 0.0);
+          dmma(c0v, c1v, y.x, z.x);
+          if (STIFF) dmma(c0v, c1v, y.y, z.y);
+        }
+        if (combo < NC) {
+          const int a0 = combo / NB1, b1 = combo % NB1;
+          const int ia = a0 / NB, d0 = a0 % NB, ib = b1 / NB, d1 = b1 % NB;
+          double* Rc = R + (ia * TB + ib) * m * S::rowVals + (d0 * NB + d1) * NB;
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int nn = ntl * 8 + 2 * t + j;
+            if (nn < MM) {
+              const int r = nn / m, sc = nn % m;
+              Rc[((e2 + r) % m) * S::rowVals + sc - r + P] += j ? c1v : c0v;
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+
+    // ---- write the finished rows of this segment; clear every used slot
+    const int last = (e2 == K - 1) ? (int)N - 1 : e2;
+    for (int I2 = e2; I2 <= last; ++I2) {
+      const int slot = I2 % m;
+      const bool write = I2 >= s0;
+      if (write && tid < TA * TB) {
+        const int ia = tid / TB, ib = tid % TB;
+        const int64_t I0 = i00 + ia, I1 = i10 + ib;
+        rowoff[tid] = (I0 < a.plane_end && I1 < N) ? rowptr3(I0, I1, I2, P, N) - a.base : -1;
+      }
+      __syncthreads();
+      const int lod2 = max(0, P - I2), c2 = (int)band_cnt(I2, P, N);
+      for (int u = tid; u < TA * TB * S::rowVals; u += NT) {
+        const int rc = u / S::rowVals, v = u - rc * S::rowVals;
+        double* Rv = R + (rc * m + slot) * S::rowVals + v;
+        if (write) {
+          const int64_t off = rowoff[rc];
+          const int ia = rc / TB, ib = rc - ia * TB;
+          const int I0 = i00 + ia, I1 = i10 + ib;
+          if (off >= 0) {
+            if (I0 >= P && I0 < K && I1 >= P && I1 < K && lod2 == 0 && c2 == NB) {
+              a.values[off + v] = *Rv;
+            } else {
+              const int d2 = v % NB, d1 = (v / NB) % NB, d0 = v / (NB * NB);
+              const int lod0 = max(0, P - I0), lod1 = max(0, P - I1);
+              const int c0 = (int)band_cnt(I0, P, N), c1 = (int)band_cnt(I1, P, N);
+              if (d0 >= lod0 && d0 < lod0 + c0 && d1 >= lod1 && d1 < lod1 + c1 && d2 >= lod2 &&
+                  d2 < lod2 + c2)
+                a.values[off + ((d0 - lod0) * c1 + (d1 - lod1)) * c2 + (d2 - lod2)] = *Rv;
+            }
+          }
+        }
+        *Rv = 0.0;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+template <int P, int Q, bool ST>
+struct Tile {
+  static constexpr size_t cap = 227 * 1024;
+  static constexpr int TA = Shape<P, Q, 2, 4>::bytes <= cap ? 2
+                            : Shape<P, Q, 2, 2>::bytes <= cap ? 2
+                            : Shape<P, Q, 2, 1>::bytes <= cap ? 2 : 1;
+  static constexpr int TB = Shape<P, Q, 2, 4>::bytes <= cap ? 4
+                            : Shape<P, Q, 2, 2>::bytes <= cap ? 2 : 1;
+};
+
+template <int P, int Q, bool ST>
+static int launch_t(const GsfArgs& a0, cudaStream_t s) {
+  constexpr int TA = Tile<P, Q, ST>::TA, TB = Tile<P, Q, ST>::TB;
+  using Sh = Shape<P, Q, TA, TB>;
+  if constexpr (Sh::bytes > 227 * 1024) {
+    set_error("assembled sum factorization: p=%d q=%d needs %zu B shared memory", P, Q, Sh::bytes);
+    return IGA_EUNSUPPORTED;
+  } else {
+    GsfArgs a = a0;
+    const int64_t N = (int64_t)a.K + P;
+    const int planes = a.plane_end - a.plane_begin;
+    if (planes <= 0) return IGA_OK;
+    const int tiles0 = (planes + TA - 1) / TA;
+    a.tiles1 = (int)((N + TB - 1) / TB);
+    const int64_t tiles = (int64_t)tiles0 * a.tiles1;
+    const void* fn = reinterpret_cast<const void*>(k_gsf3_mma<P, Q, TA, TB, ST>);
+    cudaError_t e = smem_attr_once(fn, Sh::bytes);
+    if (e != cudaSuccess) return check_cuda(e, "gsf mma smem attr");
+    const int64_t slots = (int64_t)sm_count() * blocks_per_sm_once(fn, NT, Sh::bytes);
+    int best = 1;
+    double best_cost = 1e300;
+    for (int sg = 1; sg <= a.K; ++sg) {
+      const int L = (a.K + sg - 1) / sg;
+      if (L < P && sg > 1) break;
+      const double waves = (double)((tiles * sg + slots - 1) / slots);
+      const double cost = waves * (L + (sg > 1 ? P : 0));
+      if (cost < best_cost - 1e-9) { best_cost = cost; best = sg; }
+    }
+    a.segs = best;
+    a.seg_len = (a.K + best - 1) / best;
+    k_gsf3_mma<P, Q, TA, TB, ST><<<(unsigned)(tiles * best), NT, Sh::bytes, s>>>(a);
+    return check_cuda(cudaGetLastError(), "gsf mma launch");
+  }
+}
+
+template <int P, int Q>
+struct Launch {
+  static int run(const GsfArgs& a, cudaStream_t s) {
+    if (a.op == IGA_OP_MASS) return launch_t<P, Q, false>(a, s);
+    if constexpr (P >= 1) return launch_t<P, Q, true>(a, s);
+    set_error("derivatives require degree >= 1");
+    return IGA_EINVAL;
+  }
+};
+
+}  // namespace mma
+
+int launch_gsf_mma(const GsfArgs& a, int p, int q, cudaStream_t s) {
+  return dispatch_pq<mma::Launch>(p, q, a, s);
+}
+
+}  // namespace iga
