@@ -65,6 +65,7 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_mma(GsfArgs a) {
   double2* Z2 = PB2 + NB1 * KB;                              // [Q][m*m] (VV, DD(+VV))
   double* R = reinterpret_cast<double*>(Z2 + m * m * Q);     // [TA*TB][m][rowVals]
   __shared__ int64_t rowoff[TA * TB];
+  __shared__ int comboR[NC];  // R offset of combo (a0, b1): pencil block + (d0, d1) row
 
   const int K = a.K;
   const int64_t N = (int64_t)K + P;
@@ -103,6 +104,11 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_mma(GsfArgs a) {
     PB2[u] = v;
   }
   for (int u = tid; u < S::nR; u += NT) R[u] = 0.0;
+  for (int c = tid; c < NC; c += NT) {
+    const int a0 = c / NB1, b1 = c % NB1;
+    const int ia = a0 / NB, d0 = a0 % NB, ib = b1 / NB, d1 = b1 % NB;
+    comboR[c] = (ia * TB + ib) * m * S::rowVals + (d0 * NB + d1) * NB;
+  }
 
   // coefficient of the next element column for this thread's W entries
   constexpr int WPT = cdiv(S::nW, NT);
@@ -149,88 +155,112 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_mma(GsfArgs a) {
     }
     __syncthreads();
 
-    // ---- stage A: X_T[a0][col] = sum_kk PA_T[a0][kk] W[kk][col]
+    // ---- stage A: X_T[a0][col] = sum_kk PA_T[a0][kk] W[kk][col]; warp w keeps the PA
+    // fragments of m-tile w % MT in registers and sweeps its n-tiles
     {
-      constexpr int MT = cdiv(NA0, 8), NTL = cdiv(GC, 8), KS = cdiv(KA, 4);
-      for (int item = warp; item < MT * NTL; item += NWARP) {
-        const int mt = item % MT, ntl = item / MT;
-        const int row = mt * 8 + g, col = ntl * 8 + g;
-        double cv0 = 0.0, cv1 = 0.0, cd0 = 0.0, cd1 = 0.0;
+      constexpr int MT = cdiv(NA0, 8), NTL = cdiv(GC, 8), KS = cdiv(KA, 4), GRP = NWARP / MT;
+      if (warp < MT * GRP) {
+        const int mt = warp % MT, grp = warp / MT, row = mt * 8 + g;
+        double2 pa[KS];
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks) {
           const int kk = ks * 4 + t;
-          const double2 pa = (row < NA0 && kk < KA) ? PA2[row * KA + kk] : make_double2(0.0, 0.0);
-          const double w = (kk < KA && col < GC) ? sW[kk * GC + col] : 0.0;
-          dmma(cv0, cv1, pa.x, w);
-          if (STIFF) dmma(cd0, cd1, pa.y, w);
+          pa[ks] = (row < NA0 && kk < KA) ? PA2[row * KA + kk] : make_double2(0.0, 0.0);
         }
-        const int c0 = ntl * 8 + 2 * t;
-        if (row < NA0) {
-          if (c0 < GC) X2[row * GC + c0] = make_double2(cv0, cd0);
-          if (c0 + 1 < GC) X2[row * GC + c0 + 1] = make_double2(cv1, cd1);
-        }
-      }
-    }
-    __syncthreads();
-
-    // ---- stage B: rows (a0, k2), columns b1:
-    //   mass YA = XV VV;  stiffness YA = XV DD + XD VV, YB = XV VV
-    {
-      constexpr int MT = cdiv(NR, 8), NTL = cdiv(NB1, 8), KS = cdiv(KB, 4);
-      for (int item = warp; item < MT * NTL; item += NWARP) {
-        const int mt = item % MT, ntl = item / MT;
-        const int row = mt * 8 + g, b1 = ntl * 8 + g;
-        const int a0 = row / Q, k2 = row % Q;
-        double ya0 = 0.0, ya1 = 0.0, yb0 = 0.0, yb1 = 0.0;
+        for (int ntl = grp; ntl < NTL; ntl += GRP) {
+          const int col = ntl * 8 + g;
+          double cv0 = 0.0, cv1 = 0.0, cd0 = 0.0, cd1 = 0.0;
 #pragma unroll
-        for (int ks = 0; ks < KS; ++ks) {
-          const int kk = ks * 4 + t;
-          const double2 x = (row < NR && kk < KB) ? X2[a0 * GC + kk * Q + k2] : make_double2(0.0, 0.0);
-          const double2 pb = (b1 < NB1 && kk < KB) ? PB2[b1 * KB + kk] : make_double2(0.0, 0.0);
-          if (STIFF) {
-            dmma(ya0, ya1, x.x, pb.y);
-            dmma(ya0, ya1, x.y, pb.x);
-            dmma(yb0, yb1, x.x, pb.x);
-          } else {
-            dmma(ya0, ya1, x.x, pb.x);
+          for (int ks = 0; ks < KS; ++ks) {
+            const int kk = ks * 4 + t;
+            const double w = (kk < KA && col < GC) ? sW[kk * GC + col] : 0.0;
+            dmma(cv0, cv1, pa[ks].x, w);
+            if (STIFF) dmma(cd0, cd1, pa[ks].y, w);
+          }
+          const int c0 = ntl * 8 + 2 * t;
+          if (row < NA0) {
+            if (c0 < GC) X2[row * GC + c0] = make_double2(cv0, cd0);
+            if (c0 + 1 < GC) X2[row * GC + c0 + 1] = make_double2(cv1, cd1);
           }
         }
-        // C[g][2t..2t+1]: row (a0,k2) = mt*8+g, columns b1 = ntl*8 + 2t, +1
-        const int rr = mt * 8 + g, ra0 = rr / Q, rk2 = rr % Q, c0 = ntl * 8 + 2 * t;
-        if (rr < NR) {
-          if (c0 < NB1) Y2[(ra0 * NB1 + c0) * Q + rk2] = make_double2(ya0, yb0);
-          if (c0 + 1 < NB1) Y2[(ra0 * NB1 + c0 + 1) * Q + rk2] = make_double2(ya1, yb1);
+      }
+    }
+    __syncthreads();
+
+    // ---- stage B: rows (a0, k2), columns b1; warp w keeps the PB fragments of n-tile
+    // w % NTL in registers:  mass YA = XV VV;  stiffness YA = XV DD + XD VV, YB = XV VV
+    {
+      constexpr int MT = cdiv(NR, 8), NTL = cdiv(NB1, 8), KS = cdiv(KB, 4), GRP = NWARP / NTL;
+      if (warp < NTL * GRP) {
+        const int ntl = warp % NTL, grp = warp / NTL, b1 = ntl * 8 + g;
+        double2 pb[KS];
+#pragma unroll
+        for (int ks = 0; ks < KS; ++ks) {
+          const int kk = ks * 4 + t;
+          pb[ks] = (b1 < NB1 && kk < KB) ? PB2[b1 * KB + kk] : make_double2(0.0, 0.0);
+        }
+        for (int mt = grp; mt < MT; mt += GRP) {
+          const int row = mt * 8 + g, a0 = row / Q, k2 = row % Q;
+          double ya0 = 0.0, ya1 = 0.0, yb0 = 0.0, yb1 = 0.0;
+#pragma unroll
+          for (int ks = 0; ks < KS; ++ks) {
+            const int kk = ks * 4 + t;
+            const double2 x = (row < NR && kk < KB) ? X2[a0 * GC + kk * Q + k2] : make_double2(0.0, 0.0);
+            if (STIFF) {
+              dmma(ya0, ya1, x.x, pb[ks].y);
+              dmma(ya0, ya1, x.y, pb[ks].x);
+              dmma(yb0, yb1, x.x, pb[ks].x);
+            } else {
+              dmma(ya0, ya1, x.x, pb[ks].x);
+            }
+          }
+          const int c0 = ntl * 8 + 2 * t;
+          if (row < NR) {
+            if (c0 < NB1) Y2[(a0 * NB1 + c0) * Q + k2] = make_double2(ya0, yb0);
+            if (c0 + 1 < NB1) Y2[(a0 * NB1 + c0 + 1) * Q + k2] = make_double2(ya1, yb1);
+          }
         }
       }
     }
     __syncthreads();
 
-    // ---- stage S: C[combo][(r,s)] = sum_k2 Y[combo][k2] Z[k2][(r,s)] into the rolling rows
+    // ---- stage S: C[combo][(r,s)] = sum_k2 Y[combo][k2] Z[k2][(r,s)] into the rolling
+    // rows; warp w keeps the Z fragments of n-tile w % NTL and its lanes' two (r,s)
+    // destinations, and sweeps the combo m-tiles
     {
       constexpr int MM = m * m, MT = cdiv(NC, 8), NTL = cdiv(MM, 8), KS = cdiv(Q, 4);
-      for (int item = warp; item < MT * NTL; item += NWARP) {
-        const int mt = item % MT, ntl = item / MT;
-        const int combo = mt * 8 + g, n = ntl * 8 + g;
-        double c0v = 0.0, c1v = 0.0;
+      constexpr int GRP = NWARP / NTL;
+      if (warp < NTL * GRP) {
+        const int ntl = warp % NTL, grp = warp / NTL, n = ntl * 8 + g;
+        double2 z[KS];
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks) {
           const int k = ks * 4 + t;
-          const double2 y = (combo < NC && k < Q) ? Y2[combo * Q + k] : make_double2(0.0, 0.0);
-          const double2 z = (n < MM && k < Q) ? Z2[k * MM + n] : make_double2(0.0, 0.0);
-          dmma(c0v, c1v, y.x, z.x);
-          if (STIFF) dmma(c0v, c1v, y.y, z.y);
+          z[ks] = (n < MM && k < Q) ? Z2[k * MM + n] : make_double2(0.0, 0.0);
         }
-        if (combo < NC) {
-          const int a0 = combo / NB1, b1 = combo % NB1;
-          const int ia = a0 / NB, d0 = a0 % NB, ib = b1 / NB, d1 = b1 % NB;
-          double* Rc = R + (ia * TB + ib) * m * S::rowVals + (d0 * NB + d1) * NB;
+        int dst[2];  // offset of column (r, s) in a combo's R block, -1 if padding
+        const int slot0 = e2 % m;
 #pragma unroll
-          for (int j = 0; j < 2; ++j) {
-            const int nn = ntl * 8 + 2 * t + j;
-            if (nn < MM) {
-              const int r = nn / m, sc = nn % m;
-              Rc[((e2 + r) % m) * S::rowVals + sc - r + P] += j ? c1v : c0v;
-            }
+        for (int j = 0; j < 2; ++j) {
+          const int nn = ntl * 8 + 2 * t + j, r = nn / m, sc = nn % m;
+          const int slot = slot0 + r >= m ? slot0 + r - m : slot0 + r;
+          dst[j] = nn < MM ? slot * S::rowVals + sc - r + P : -1;
+        }
+        for (int mt = grp; mt < MT; mt += GRP) {
+          const int combo = mt * 8 + g;
+          double c0v = 0.0, c1v = 0.0;
+#pragma unroll
+          for (int ks = 0; ks < KS; ++ks) {
+            const int k = ks * 4 + t;
+            const double2 y = (combo < NC && k < Q) ? Y2[combo * Q + k] : make_double2(0.0, 0.0);
+            dmma(c0v, c1v, y.x, z[ks].x);
+            if (STIFF) dmma(c0v, c1v, y.y, z[ks].y);
+          }
+          const int cc = mt * 8 + g;
+          if (cc < NC) {
+            double* Rc = R + comboR[cc];
+            if (dst[0] >= 0) Rc[dst[0]] += c0v;
+            if (dst[1] >= 0) Rc[dst[1]] += c1v;
           }
         }
       }
