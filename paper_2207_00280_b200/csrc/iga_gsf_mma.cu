@@ -128,6 +128,24 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_mma(GsfArgs a) {
   };
   double cv[WPT];
   load_coef(e_first, cv);
+  // axis-2 table entries of the next element (one (r, s, k) per thread)
+  static_assert(m * m * Q <= NT, "one Z entry per thread");
+  auto load_z = [&](int e2, double (&zv)[4]) {
+    zv[0] = zv[1] = zv[2] = zv[3] = 0.0;
+    if (tid < m * m * Q && e2 < K) {
+      const int k = tid / (m * m), n = tid % (m * m), r = n / m, sc = n % m;
+      const double* V2 = V + (int64_t)e2 * m * Q;
+      zv[0] = __ldg(V2 + r * Q + k);
+      zv[1] = __ldg(V2 + sc * Q + k);
+      if (STIFF) {
+        const double* D2 = D + (int64_t)e2 * m * Q;
+        zv[2] = __ldg(D2 + r * Q + k);
+        zv[3] = __ldg(D2 + sc * Q + k);
+      }
+    }
+  };
+  double zv[4];
+  load_z(e_first, zv);
 
   for (int e2 = e_first; e2 < s1; ++e2) {
     __syncthreads();  // previous column's stage S (reads Y, aliasing W) and flush are done
@@ -141,18 +159,16 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_mma(GsfArgs a) {
       }
     }
     load_coef(e2 + 1, cv);
-    for (int u = tid; u < m * m * Q; u += NT) {  // Z[k2][(r,s)]
-      const int k = u / (m * m), n = u % (m * m), r = n / m, sc = n % m;
-      const double* V2 = V + (int64_t)e2 * m * Q;
-      const double vv = V2[r * Q + k] * V2[sc * Q + k];
+    if (tid < m * m * Q) {  // Z[k2][(r,s)]
+      const double vv = zv[0] * zv[1];
       double dd = 0.0;
       if (STIFF) {
-        const double* D2 = D + (int64_t)e2 * m * Q;
-        dd = D2[r * Q + k] * D2[sc * Q + k];
+        dd = zv[2] * zv[3];
         if (a.op == IGA_OP_STIFFNESS_MASS) dd += vv;
       }
-      Z2[u] = make_double2(vv, dd);
+      Z2[tid] = make_double2(vv, dd);
     }
+    load_z(e2 + 1, zv);
     __syncthreads();
 
     // ---- stage A: X_T[a0][col] = sum_kk PA_T[a0][kk] W[kk][col]; warp w keeps the PA
