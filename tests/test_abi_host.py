@@ -185,3 +185,13 @@ def test_matrix_market_host_writer_matches_scipy(lib, tmp_path, dim, K, p, op):
     f = tmp_path / "a.mtx"
     assert lib.iga_write_matrix_market_host(dim, K, p, v.ctypes.data, str(f).encode(), 3) == 0
     assert f.read_bytes() == ref.getvalue()
+
+
+def test_bench_csv_columns_match_reference_cli():
+    from paper_2207_00280_b200.benchcsv import BENCH_COLUMNS
+
+    src = open("/root/reference/pkg/src/igabench/cli.py").read() if os.path.exists(
+        "/root/reference/pkg/src/igabench/cli.py") else None
+    if src is None:
+        pytest.skip("reference not mounted")
+    assert f"BENCH_COLUMNS = {BENCH_COLUMNS!r}".replace("'", '"') in src

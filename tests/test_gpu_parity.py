@@ -503,3 +503,21 @@ def test_tiny_meshes_all_paths(pkg, K, p):
                                                     assembly=assembly))
             v = res.gram.values.cpu().numpy()
             assert_parity(v, ref, ip, absref=A, what=f"{op} K={K} p={p} {method}/{assembly}")
+
+
+def test_bench_csv_schema(pkg):
+    """Bench CSV: the reference's columns (cli.py:31) first, one row per repetition."""
+    import csv
+    import io
+
+    from paper_2207_00280_b200 import benchcsv
+
+    buf = io.StringIO()
+    n = benchcsv.write_bench_csv(buf, method="both", p=2, K=6, threads=(1, 4), repeat=2)
+    lines = buf.getvalue().splitlines()
+    assert lines[0].startswith("#")
+    rows = list(csv.reader(lines[1:]))
+    assert rows[0][:8] == ["method", "strategy", "p", "K", "threads", "rep", "seconds", "flops"]
+    assert len(rows) - 1 == n == 2 * 2 * 2
+    assert {r[0] for r in rows[1:]} == {"classical", "sumfact"}
+    assert all(float(r[6]) > 0 for r in rows[1:])
