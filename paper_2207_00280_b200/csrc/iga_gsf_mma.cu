@@ -52,7 +52,7 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 }
 
 template <int P, int Q, int TA, int TB, bool STIFF>
-__global__ void __launch_bounds__(NT, 1) k_gsf3_mma(GsfArgs a) {
+__global__ void __launch_bounds__(NT, P <= 2 ? 2 : 1) k_gsf3_mma(GsfArgs a) {
   using S = Shape<P, Q, TA, TB>;
   constexpr int m = S::m, NB = S::NB, KA = S::KA, KB = S::KB, GC = S::GC;
   constexpr int NA0 = S::NA0, NB1 = S::NB1, NC = S::NC, NR = S::NR;
@@ -348,7 +348,7 @@ static int launch_t(const GsfArgs& a0, cudaStream_t s) {
     a.tiles1 = (int)((N + TB - 1) / TB);
     const int64_t tiles = (int64_t)tiles0 * a.tiles1;
     const void* fn = reinterpret_cast<const void*>(k_gsf3_mma<P, Q, TA, TB, ST>);
-    cudaError_t e = smem_attr_once(fn, Sh::bytes);
+    cudaError_t e = smem_attr_once(fn, Sh::bytes, true);
     if (e != cudaSuccess) return check_cuda(e, "gsf mma smem attr");
     const int64_t slots = (int64_t)sm_count() * blocks_per_sm_once(fn, NT, Sh::bytes);
     int best = 1;
