@@ -33,6 +33,8 @@
 // The constant B fragments of stages A and B live in registers; the rolling rows
 // of stage S live in per-lane shared-memory slots that are the DMMA C operands,
 // and a row leaves for the CSR straight from the register of its last product.
+#include <type_traits>
+
 #include "iga_args.cuh"
 #include "iga_dispatch.cuh"
 
@@ -53,8 +55,10 @@ constexpr int NT = 512;                  // threads: 16 warps
 constexpr int MT_A = NCOL / 8;           // 14 m-tiles of (g1,k2) columns
 constexpr int MT_B = NA0 * Q / 8;        // 7 m-tiles of (a0,k2) rows
 constexpr int MT_S = NCOMBO / 8;         // 49 m-tiles of combos
-constexpr int NWA = 4, NWB = 4, NWS = 8; // warps per role (NWA even: fixed type per A warp)
+constexpr int NWA = 4, NWB = 5, NWS = 7; // warps per role (NWA even: fixed type per A warp)
 constexpr int MT_S_PER_WARP = (MT_S + NWS - 1) / NWS;  // 7
+static_assert(MT_S == MT_S_PER_WARP * NWS, "stage S m-tiles split evenly");
+constexpr int NHB = 2 * MT_B;            // stage-B half units (m-tile, ib pair)
 constexpr int NPEN = TA * TB;            // row pencils (I0, I1) of the tile
 
 // shared memory layout (doubles)
@@ -66,8 +70,8 @@ constexpr int OFF_Y = OFF_X + 2 * SZ_X;           // 2 buffers
 // the constant B fragments are read into registers before the pipeline starts, so
 // they alias Y buffer 1 (first written by stage B at iteration 2)
 constexpr int OFF_BA = OFF_Y + SZ_Y;              // [2 types][LA pairs][32]
-constexpr int OFF_BB = OFF_BA + 2 * LA * 32;      // [2 prods][LB][2 nt][32]
-static_assert(2 * LA * 32 + 2 * LB * 2 * 32 <= SZ_Y, "fragment tables fit Y buffer 1");
+constexpr int OFF_BB = OFF_BA + 2 * LA * 32;      // [2 prods][10 pairs][32]
+static_assert(2 * LA * 32 + 2 * 10 * 32 <= SZ_Y, "fragment tables fit Y buffer 1");
 constexpr int OFF_WQ = OFF_Y + 2 * SZ_Y;          // weights [Q]
 constexpr int OFF_PB = OFF_WQ + Q;                // pencil row-pointer bases (int64) [NPEN]
 constexpr int OFF_PC = OFF_PB + NPEN;             // pencil c0*c1 (int in double slots) [NPEN]
@@ -186,56 +190,65 @@ __device__ __forceinline__ void stage_a_units(const Lane& L, const double* W, co
 }
 
 // ---------------------------------------------------------------- stage B
-// Valid (element lb, n-tile) pairs of stage B (destination ib = lb + k - P in [0, TB))
+// A half unit (m-tile mt, destinations ib in {2h, 2h+1}) sees the window elements
+// lb = 2h .. 2h+4 with the same pairing as stage A: fragment i of half h pairs
+// r = rb, rb+1 of element lb (5 DMMAs per product instead of 10 for a full unit, so
+// the 14 half units balance over the B warps).
 constexpr int NPB = 10;
-__host__ __device__ constexpr int pb_lb(int i) { return i < 1 ? 0 : (i < 2 ? 1 : (i < 4 ? 2 : (i < 6 ? 3 : (i < 8 ? 4 : (i < 9 ? 5 : 6))))); }
-__host__ __device__ constexpr int pb_nt(int i) { return (i == 0 || i == 1 || i == 3 || i == 5 || i == 7) ? 1 : 0; }
+__host__ __device__ constexpr int pb_lb(int i) { return i < 5 ? i : i - 5 + 2; }
+__host__ __device__ constexpr int pb_rb(int i) { return pa_rb(i % 5); }
 
-// unit = m-tile mt of (a0,k2) rows, all TB destinations ib; bv/bd are the warp's
-// constant B fragments (VV and DD pair products of the axis-1 window).  Pass 1
-// issues the independent X_D VV -> Y_A and X_V VV -> Y_B products, pass 2 adds
-// X_V DD -> Y_A.
-__device__ __forceinline__ void stage_b_unit(const Lane& L, const double* X, const double (&bv)[NPB],
-                                             const double (&bd)[NPB], double* Y, int mt) {
+// bv/bd are the warp's constant B fragments (VV and DD pair products of the axis-1
+// window).  Pass 1 issues the independent X_D VV -> Y_A and X_V VV -> Y_B products,
+// pass 2 adds X_V DD -> Y_A.
+__device__ __forceinline__ void stage_b_half(const Lane& L, const double* X, const double (&bv)[NPB],
+                                             const double (&bd)[NPB], double* Y, int mt, int h) {
   const int row = mt * 8 + L.g, a0 = row >> 2, k2 = row & 3, t = L.t;
-  double yA[TB][4], yB[TB][4];
+  double yA[2][4], yB[2][4];
 #pragma unroll
-  for (int i = 0; i < TB; ++i)
+  for (int i = 0; i < 2; ++i)
 #pragma unroll
     for (int k = 0; k < 4; ++k) yA[i][k] = yB[i][k] = 0.0;
+  auto body = [&](auto hc) {
+    constexpr int H = decltype(hc)::value;
 #pragma unroll
-  for (int pass = 0; pass < 2; ++pass) {
-    if (pass == 1 && !L.stiff) break;
+    for (int pass = 0; pass < 2; ++pass) {
+      if (pass == 1 && !L.stiff) break;
 #pragma unroll
-    for (int i = 0; i < NPB; ++i) {
-      const int lb = pb_lb(i), nt = pb_nt(i);
-      const int i0 = lb + 2 * nt - P, i1 = i0 + 1;
-      const bool v0 = i0 >= 0 && i0 < TB, v1 = i1 >= 0 && i1 < TB;
-      double z0 = 0.0, z1 = 0.0, z2 = 0.0, z3 = 0.0;
-      double& a0r = v0 ? yA[clampi(i0, 0, TB - 1)][2 * nt] : z0;
-      double& a1r = v1 ? yA[clampi(i1, 0, TB - 1)][2 * nt + 1] : z1;
-      double& b0r = v0 ? yB[clampi(i0, 0, TB - 1)][2 * nt] : z2;
-      double& b1r = v1 ? yB[clampi(i1, 0, TB - 1)][2 * nt + 1] : z3;
-      const int xo = (lb * Q + t) * Q + k2;
-      const double xv = X[(0 * NA0 + a0) * XP + xo];
-      if (pass == 0) {
-        if (L.stiff) {
-          const double xd = X[(1 * NA0 + a0) * XP + xo];
-          dmma(a0r, a1r, xd, bv[i], a0r, a1r);
-          dmma(b0r, b1r, xv, bv[i], b0r, b1r);
+      for (int j = 0; j < 5; ++j) {
+        const int i = 5 * H + j;
+        const int lb = pb_lb(i), rb = pb_rb(i);
+        const int i0 = lb + rb - P - 2 * H, i1 = i0 + 1;  // local destinations (0 or 1)
+        const bool v0 = i0 >= 0 && i0 < 2, v1 = i1 >= 0 && i1 < 2;
+        double z0 = 0.0, z1 = 0.0, z2 = 0.0, z3 = 0.0;
+        double& a0r = v0 ? yA[clampi(i0, 0, 1)][rb] : z0;
+        double& a1r = v1 ? yA[clampi(i1, 0, 1)][rb + 1] : z1;
+        double& b0r = v0 ? yB[clampi(i0, 0, 1)][rb] : z2;
+        double& b1r = v1 ? yB[clampi(i1, 0, 1)][rb + 1] : z3;
+        const int xo = (lb * Q + t) * Q + k2;
+        const double xv = X[(0 * NA0 + a0) * XP + xo];
+        if (pass == 0) {
+          if (L.stiff) {
+            const double xd = X[(1 * NA0 + a0) * XP + xo];
+            dmma(a0r, a1r, xd, bv[i], a0r, a1r);
+            dmma(b0r, b1r, xv, bv[i], b0r, b1r);
+          } else {
+            dmma(a0r, a1r, xv, bv[i], a0r, a1r);
+          }
         } else {
-          dmma(a0r, a1r, xv, bv[i], a0r, a1r);
+          dmma(a0r, a1r, xv, bd[i], a0r, a1r);
         }
-      } else {
-        dmma(a0r, a1r, xv, bd[i], a0r, a1r);
       }
     }
-  }
+  };
+  if (h == 0) body(std::integral_constant<int, 0>());
+  else body(std::integral_constant<int, 1>());
 #pragma unroll
-  for (int ib = 0; ib < TB; ++ib) {
+  for (int il = 0; il < 2; ++il) {
+    const int ib = 2 * h + il;
     double hA, lA, hB, lB;
-    split_groups(yA[ib], t, hA, lA);
-    split_groups(yB[ib], t, hB, lB);
+    split_groups(yA[il], t, hA, lA);
+    split_groups(yB[il], t, hB, lB);
     const int ch = (a0 * TB + ib) * NB + P + t;
     Y[(0 * Q + k2) * YP + ch] = hA;
     if (L.stiff) Y[(1 * Q + k2) * YP + ch] = hB;
@@ -360,10 +373,9 @@ __device__ __forceinline__ void stage_s(const Lane& L, int ws, const double* Y, 
                                         const double (&b0)[2], const double (&b1)[2]) {
   const int t = L.t;
   const RowDst rd = row_dst(t, e2, N);
-  static_assert(MT_S == (MT_S_PER_WARP - 1) * NWS + 1, "stage S warp split");
   stage_s_batch<PHI, 0, 3>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd);
   stage_s_batch<PHI, 3, 3>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd);
-  if (ws == 0) stage_s_batch<PHI, 6, 1>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd);
+  stage_s_batch<PHI, 6, 1>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd);
 }
 
 // Rows K .. K+P-1 (no element e2 = I2): both groups are complete in their slots.
@@ -441,13 +453,14 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
     }
     BA[u] = v;
   }
-  for (int u = tid; u < 2 * LB * 2 * 32; u += NT) {
-    const int ln = u & 31, nt = (u >> 5) & 1, lb = (u >> 6) % LB, prod = u / (64 * LB);
-    const int gg = ln >> 2, tt = ln & 3, e1 = i10 - P + lb;
+  for (int u = tid; u < 2 * NPB * 32; u += NT) {
+    const int ln = u & 31, i = (u >> 5) % NPB, prod = u / (32 * NPB);
+    const int gg = ln >> 2, tt = ln & 3, e1 = i10 - P + pb_lb(i);
+    const int r = pb_rb(i) + (gg & 1), sc = (r + (gg >> 1)) & 3;
     double v = 0.0;
     if (e1 >= 0 && e1 < K && (prod == 0 || L.stiff)) {
       const double* T = (prod == 0 ? a.V : a.D) + (int64_t)e1 * M * Q;
-      v = T[bcol_r(nt, gg) * Q + tt] * T[bcol_s(nt, gg) * Q + tt];
+      v = T[r * Q + tt] * T[sc * Q + tt];
     }
     BB[u] = v;
   }
@@ -506,8 +519,8 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
     double bv[NPB], bd[NPB];
 #pragma unroll
     for (int i = 0; i < NPB; ++i) {
-      bv[i] = BB[((0 * LB + pb_lb(i)) * 2 + pb_nt(i)) * 32 + L.lane];
-      bd[i] = BB[((1 * LB + pb_lb(i)) * 2 + pb_nt(i)) * 32 + L.lane];
+      bv[i] = BB[(0 * NPB + i) * 32 + L.lane];
+      bd[i] = BB[(1 * NPB + i) * 32 + L.lane];
     }
     __syncthreads();
     for (int e2 = 0; e2 < K; ++e2) {
@@ -518,7 +531,7 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
       if (n >= 1) mbar_wait(yempty + b, (n - 1) & 1);
       const double* X = sm + OFF_X + b * SZ_X;
       double* Y = sm + OFF_Y + b * SZ_Y;
-      for (int mt = wb; mt < MT_B; mt += NWB) stage_b_unit(L, X, bv, bd, Y, mt);
+      for (int u = wb; u < NHB; u += NWB) stage_b_half(L, X, bv, bd, Y, u >> 1, u & 1);
       mbar_arrive(xempty + b);
       mbar_arrive(yfull + b);
       PT(0);
