@@ -373,9 +373,8 @@ __device__ __forceinline__ void stage_s(const Lane& L, int ws, const double* Y, 
                                         const double (&b0)[2], const double (&b1)[2]) {
   const int t = L.t;
   const RowDst rd = row_dst(t, e2, N);
-  stage_s_batch<PHI, 0, 3>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd);
-  stage_s_batch<PHI, 3, 3>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd);
-  stage_s_batch<PHI, 6, 1>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd);
+  stage_s_batch<PHI, 0, 4>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd);
+  stage_s_batch<PHI, 4, 3>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd);
 }
 
 // Rows K .. K+P-1 (no element e2 = I2): both groups are complete in their slots.
