@@ -151,11 +151,10 @@ def write_matrix_market(gram: GlobalGram, path, threads: int | None = None) -> N
     path = os.fspath(path)
     nthr = int(threads or os.cpu_count() or 1)
     if gram.values is not None:
-        torch = _lib.require_cuda()
+        _lib.require_cuda()
         vals = gram.values.contiguous()
         _lib.check(L.iga_write_matrix_market(gram.dim, gram.K, gram.p, _lib.ptr(vals),
                                              path.encode(), nthr, _lib.stream_ptr()))
-        del torch
         return
     m = gram.matrix
     indptr, indices = host_pattern(gram.dim, gram.K, gram.p)
