@@ -521,3 +521,58 @@ def test_bench_csv_schema(pkg):
     assert len(rows) - 1 == n == 2 * 2 * 2
     assert {r[0] for r in rows[1:]} == {"classical", "sumfact"}
     assert all(float(r[6]) > 0 for r in rows[1:])
+
+
+def _device_rows(values, dim, K, p, rows):
+    """Values of the listed rows, sliced on the device (no host CSR for huge meshes)."""
+    from paper_2207_00280_b200.device import csr_nnz
+
+    return [values[csr_nnz(dim, K, p, 0, int(r)):csr_nnz(dim, K, p, 0, int(r) + 1)].cpu().numpy()
+            for r in rows]
+
+
+def _check_rows(got_rows, K, p, rows, op, coef, name):
+    ref_rows = O.rows(3, K, p, rows, op, "classical", coef=coef)
+    abs_rows = O.rows(3, K, p, rows, op, "classical", coef=coef, absolute=True)
+    got = np.concatenate(got_rows)
+    ref = np.concatenate(ref_rows)
+    A = np.concatenate(abs_rows)
+    sub_ip = np.concatenate([[0], np.cumsum([len(x) for x in ref_rows])])
+    assert_parity(got, ref, sub_ip, absref=A, what=name)
+
+
+def test_full_size_c4_sampled_rows(pkg):
+    """C4 at full size (96^3, p=4, q=5, stiffness+mass, 8-mode sine field from bench.py's
+    seeded generator): sampled corner/edge/interior rows vs the oracle's classical rows."""
+    import bench
+
+    K, p = 96, 4
+    coef = bench.coefficient("sines", K, p, 3)
+    res = pkg.run_integration(pkg.RunConfig("sumfact", "device", K, p, operator="stiffness_mass",
+                                            coefficient=coef))
+    rows = _sample_rows(K, p, 24, seed=1)
+    _check_rows(_device_rows(res.gram.values, 3, K, p, rows), K, p, rows, "stiffness_mass", coef,
+                "C4")
+
+
+@pytest.mark.parametrize("assembly", ["separable", "owner"])
+def test_full_size_c5_sampled_rows(pkg, assembly):
+    """C5 at full size on one GPU (256^3, p=3: 5.84e9 values, 46.7 GB resident): sampled
+    rows, including the planes at the 2/4/8-way slab boundaries, vs the oracle; the
+    stiffness row sums vanish."""
+    import torch
+
+    K, p = 256, 3
+    res = pkg.run_integration(pkg.RunConfig("sumfact", "device", K, p, operator="stiffness",
+                                            assembly=assembly))
+    N = K + p
+    rng = np.random.default_rng(5)
+    planes = [0, 1, 2, 3, 31, 32, 33, 64, 127, 128, 129, 130, 192, 255, 256, 258]
+    rows = sorted({(a * N + int(rng.integers(0, N))) * N + int(rng.integers(0, N)) for a in planes}
+                  | {0, N**3 - 1, (N // 2 * N + N // 2) * N + N // 2})
+    got = _device_rows(res.gram.values, 3, K, p, rows)
+    _check_rows(got, K, p, rows, "stiffness", None, f"C5 {assembly}")
+    for r in got:
+        assert abs(r.sum()) <= 1e-12 * np.abs(r).max()
+    del res
+    torch.cuda.empty_cache()
