@@ -257,7 +257,7 @@ def alt_leg(cfg, assembly, args, flush, stream, wl, total_el, peaks):
 
     from paper_2207_00280_b200.runtime import DeviceSession
 
-    sess = DeviceSession(dataclasses.replace(cfg, assembly=assembly))
+    sess = DeviceSession(dataclasses.replace(cfg, assembly=assembly), use_graph=not args.no_graph)
     for _ in range(args.warmup):
         sess.step()
         flush.fill_(1.0)
@@ -302,6 +302,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-alt", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="launch the step eagerly")
     ap.add_argument("--assembly", default="auto", help="force a kernel path (RunConfig.assembly)")
     ap.add_argument("--method", default=None, help="override the workload's method")
     args = ap.parse_args()
@@ -346,7 +347,7 @@ def main():
         launches = sess.kernel_launches_per_step
         kernel_values = sess.values
     else:
-        sess = DeviceSession(cfg)
+        sess = DeviceSession(cfg, use_graph=not args.no_graph)
         step = sess.step
         n_el = K ** wl["dim"]
         launches = 2

@@ -149,9 +149,11 @@ class DeviceSession:
     assembled, and the CSR values are copied device->host into ``out``
     (pinned host memory for full PCIe bandwidth)."""
 
-    def __init__(self, cfg: RunConfig, stream=None):
+    def __init__(self, cfg: RunConfig, stream=None, use_graph: bool = False):
         torch = _lib.require_cuda()
         self.cfg = cfg
+        self.use_graph = use_graph  # replay the step's launches as one CUDA graph
+        self._graph = None
         self.code = method_code(cfg)
         self.prob = MeshProblem(cfg.dim, cfg.mesh, cfg.degree, cfg.points, cfg.operator,
                                 cfg.coefficient)
@@ -172,9 +174,28 @@ class DeviceSession:
     def d2h_bytes(self) -> int:
         return self.values.numel() * 8
 
+    def _launch(self, stream):
+        self.prob.build_tables(stream)
+        self.prob.integrate_assemble(self.values, self.code, stream=stream)
+
     def step(self):
-        self.prob.build_tables(self.stream)
-        self.prob.integrate_assemble(self.values, self.code, stream=self.stream)
+        if not self.use_graph:
+            self._launch(self.stream)
+            return self.values
+        torch = _lib.require_cuda()
+        if self._graph is None:
+            # one eager step first (kernel attributes and launch set-up are cached outside
+            # the capture), then capture K1 + the integrate+assemble kernel once
+            self._launch(self.stream)
+            self.stream.synchronize()
+            side = torch.cuda.Stream()
+            side.wait_stream(self.stream)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=side):
+                self._launch(side)
+            self._graph = g
+        with torch.cuda.stream(self.stream):
+            self._graph.replay()
         return self.values
 
     def step_host(self, out):

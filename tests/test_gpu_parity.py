@@ -576,3 +576,15 @@ def test_full_size_c5_sampled_rows(pkg, assembly):
         assert abs(r.sum()) <= 1e-12 * np.abs(r).max()
     del res
     torch.cuda.empty_cache()
+
+
+def test_device_session_graph_replay_matches_eager(pkg):
+    """DeviceSession(use_graph=True): the captured step (K1 + kernel) gives the same bits."""
+    from paper_2207_00280_b200.runtime import DeviceSession
+
+    cfg = pkg.RunConfig("sumfact", "device", 6, 3, operator="stiffness")
+    a = DeviceSession(cfg).step().clone()
+    s = DeviceSession(cfg, use_graph=True)
+    for _ in range(3):
+        b = s.step()
+    assert (a == b).all().item()
