@@ -26,7 +26,7 @@
 namespace iga {
 
 #ifndef KRON_MINB
-#define KRON_MINB 2
+#define KRON_MINB 1
 #endif
 
 // threads per CTA: one per value of an interior row (NB^3, rounded to warps, <= 1024)
@@ -42,8 +42,11 @@ __host__ __device__ constexpr int kron_minb(int P) {
 // rows per staged chunk (one TMA bulk store each)
 // (measured on B200: 16 rows with 2 CTAs/SM for the small meshes, where the chunk
 // count per pencil is low; 8 rows for K > 96)
+#ifndef KRON_GS
+#define KRON_GS 16
+#endif
 __host__ __device__ constexpr int kron_rows(int P, bool small_mesh) {
-  return P <= 2 ? 16 : (P == 3 ? (small_mesh ? 16 : 8) : 4);
+  return P <= 2 ? 16 : (P == 3 ? (small_mesh ? KRON_GS : 8) : 4);
 }
 // doubles per staging buffer: a chunk of full rows plus 16-byte alignment padding
 __host__ __device__ constexpr int kron_stage(int P, int G) { return G * (2 * P + 1) * (2 * P + 1) * (2 * P + 1) + 2; }
