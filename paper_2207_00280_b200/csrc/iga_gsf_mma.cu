@@ -147,8 +147,44 @@ __global__ void __launch_bounds__(NT, P <= 2 ? 2 : 1) k_gsf3_mma(GsfArgs a) {
   double zv[4];
   load_z(e_first, zv);
 
+  // a finished row leaves (and its slot is cleared) in the next column's stage-A phase, so
+  // the row store costs no barrier of its own
+  auto set_rowoff = [&](int I2) {
+    if (tid < TA * TB) {
+      const int ia = tid / TB, ib = tid % TB;
+      const int64_t I0 = i00 + ia, I1 = i10 + ib;
+      rowoff[tid] = (I2 >= s0 && I0 < a.plane_end && I1 < N) ? rowptr3(I0, I1, I2, P, N) - a.base
+                                                            : -1;
+    }
+  };
+  auto flush_row = [&](int I2) {
+    const int slot = I2 % m;
+    const int lod2 = max(0, P - I2), c2 = (int)band_cnt(I2, P, N);
+    for (int u = tid; u < TA * TB * S::rowVals; u += NT) {
+      const int rc = u / S::rowVals, v = u - rc * S::rowVals;
+      double* Rv = R + (rc * m + slot) * S::rowVals + v;
+      const int64_t off = rowoff[rc];
+      if (off >= 0) {
+        const int ia = rc / TB, ib = rc - ia * TB;
+        const int I0 = i00 + ia, I1 = i10 + ib;
+        if (I0 >= P && I0 < K && I1 >= P && I1 < K && lod2 == 0 && c2 == NB) {
+          a.values[off + v] = *Rv;  // full band: CSR order is the R order
+        } else {
+          const int d2 = v % NB, d1 = (v / NB) % NB, d0 = v / (NB * NB);
+          const int lod0 = max(0, P - I0), lod1 = max(0, P - I1);
+          const int c0 = (int)band_cnt(I0, P, N), c1 = (int)band_cnt(I1, P, N);
+          if (d0 >= lod0 && d0 < lod0 + c0 && d1 >= lod1 && d1 < lod1 + c1 && d2 >= lod2 &&
+              d2 < lod2 + c2)
+            a.values[off + ((d0 - lod0) * c1 + (d1 - lod1)) * c2 + (d2 - lod2)] = *Rv;
+        }
+      }
+      *Rv = 0.0;
+    }
+  };
+  int pending = -1;
   for (int e2 = e_first; e2 < s1; ++e2) {
-    __syncthreads();  // previous column's stage S (reads Y, aliasing W) and flush are done
+    __syncthreads();  // previous column's stage S (reads Y, aliasing W) is done
+    if (pending >= 0) set_rowoff(pending);
 #pragma unroll
     for (int i = 0; i < WPT; ++i) {
       const int u = tid + i * NT;
@@ -171,6 +207,7 @@ __global__ void __launch_bounds__(NT, P <= 2 ? 2 : 1) k_gsf3_mma(GsfArgs a) {
     load_z(e2 + 1, zv);
     __syncthreads();
 
+    if (pending >= 0) flush_row(pending);
     // ---- stage A: X_T[a0][col] = sum_kk PA_T[a0][kk] W[kk][col]; warp w keeps the PA
     // fragments of m-tile w % MT in registers and sweeps its n-tiles
     {
@@ -281,43 +318,17 @@ __global__ void __launch_bounds__(NT, P <= 2 ? 2 : 1) k_gsf3_mma(GsfArgs a) {
         }
       }
     }
-    __syncthreads();
 
-    // ---- write the finished rows of this segment; clear every used slot
-    const int last = (e2 == K - 1) ? (int)N - 1 : e2;
-    for (int I2 = e2; I2 <= last; ++I2) {
-      const int slot = I2 % m;
-      const bool write = I2 >= s0;
-      if (write && tid < TA * TB) {
-        const int ia = tid / TB, ib = tid % TB;
-        const int64_t I0 = i00 + ia, I1 = i10 + ib;
-        rowoff[tid] = (I0 < a.plane_end && I1 < N) ? rowptr3(I0, I1, I2, P, N) - a.base : -1;
-      }
+    pending = e2;  // row e2 has its last contribution; written during the next column
+  }
+  // rows still in flight: the last column's row and, after element K-1, rows K .. N-1
+  if (pending >= 0) {
+    const int last = (pending == K - 1) ? (int)N - 1 : pending;
+    for (int I2 = pending; I2 <= last; ++I2) {
       __syncthreads();
-      const int lod2 = max(0, P - I2), c2 = (int)band_cnt(I2, P, N);
-      for (int u = tid; u < TA * TB * S::rowVals; u += NT) {
-        const int rc = u / S::rowVals, v = u - rc * S::rowVals;
-        double* Rv = R + (rc * m + slot) * S::rowVals + v;
-        if (write) {
-          const int64_t off = rowoff[rc];
-          const int ia = rc / TB, ib = rc - ia * TB;
-          const int I0 = i00 + ia, I1 = i10 + ib;
-          if (off >= 0) {
-            if (I0 >= P && I0 < K && I1 >= P && I1 < K && lod2 == 0 && c2 == NB) {
-              a.values[off + v] = *Rv;
-            } else {
-              const int d2 = v % NB, d1 = (v / NB) % NB, d0 = v / (NB * NB);
-              const int lod0 = max(0, P - I0), lod1 = max(0, P - I1);
-              const int c0 = (int)band_cnt(I0, P, N), c1 = (int)band_cnt(I1, P, N);
-              if (d0 >= lod0 && d0 < lod0 + c0 && d1 >= lod1 && d1 < lod1 + c1 && d2 >= lod2 &&
-                  d2 < lod2 + c2)
-                a.values[off + ((d0 - lod0) * c1 + (d1 - lod1)) * c2 + (d2 - lod2)] = *Rv;
-            }
-          }
-        }
-        *Rv = 0.0;
-      }
+      set_rowoff(I2);
       __syncthreads();
+      flush_row(I2);
     }
   }
 }
