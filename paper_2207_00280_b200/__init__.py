@@ -48,3 +48,42 @@ from .splines import (
     find_element,
     make_knot_vector,
 )
+
+__all__ = [
+    "BasisValues",
+    "ElementMatrix",
+    "GlobalGram",
+    "IntegrationRuntime",
+    "KnotVector",
+    "MatrixFreeOperator",
+    "QuadratureRule",
+    "RunConfig",
+    "RunResult",
+    "SumFactBuffers",
+    "assemble",
+    "basis_derivative_table",
+    "basis_value_table",
+    "canonical_pairs",
+    "cg",
+    "default_rule",
+    "dof_index",
+    "element_dofs",
+    "element_list",
+    "element_tables",
+    "eval_nonzero_basis",
+    "eval_nonzero_basis_derivatives",
+    "find_element",
+    "flop_count",
+    "gauss_rule",
+    "grams_bitwise_equal",
+    "integrate_element_classical",
+    "integrate_element_sumfact",
+    "local_index",
+    "make_knot_vector",
+    "run_integration",
+    "sparsity_row_bound",
+    "spmv",
+    "support_set",
+    "symbolic_pattern",
+    "write_matrix_market",
+]

@@ -9,7 +9,7 @@ import pytest
 
 from oracle import oracle as O
 from tests.conftest import GOLDEN, load_golden
-from tests.parity import assert_parity, compare
+from tests.parity import assert_parity
 
 pytestmark = pytest.mark.gpu
 

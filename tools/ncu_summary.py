@@ -1,6 +1,5 @@
 """Summarise an ncu report: key metrics + stall/instruction mix by opcode (run here, no GPU)."""
 import csv, io, subprocess, sys
-from collections import Counter
 
 rep = sys.argv[1]
 out = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True).stdout
