@@ -196,7 +196,7 @@ def run_reference(args, wl, K, p, rank):
     }), flush=True)
 
 
-KERNEL_NAMES = {0: "k_classical_scatter (Algorithm 1 + fused CSR scatter)",
+KERNEL_NAMES = {0: "k_classical_mma (Algorithm 1 on DMMA + fused CSR scatter; 2D: k_classical_scatter)",
                 1: "k_sumfact_scatter (element-local sum factorization + atomic scatter)",
                 2: "k_gsf3 (assembled sum factorization on DMMA + CSR write)",
                 3: "k_kron3 (1D band quadrature + Kronecker CSR fill, TMA bulk stores)"}
@@ -211,6 +211,8 @@ def kernel_roofline(code, wl, K, p, q, k_el, by, kern_ms, peaks):
         fl = perfmodel.separable_flops(wl["op"], K, p, q) * k_el / K**3
     elif code == 2:
         fl = perfmodel.assembled_flops(wl["op"], K, p, q) * k_el / K**3
+    elif code == 0:
+        fl = perfmodel.classical_flops(wl["op"], p, q, wl["dim"]) * k_el
     else:
         fl = None
     t_f = fl / (peaks["fp64_tflops"] * 1e12) if fl else 0.0
@@ -224,6 +226,8 @@ def kernel_roofline(code, wl, K, p, q, k_el, by, kern_ms, peaks):
         roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / peaks["hbm_gbs"]}
     name = KERNEL_NAMES[code]
+    if code == 0 and wl["dim"] == 2:
+        name = f"k_classical_scatter<2,{p},{q}> (Algorithm 1, scalar FP64 + fused CSR scatter)"
     if code == 2 and not (p == 3 and q == 4):
         name = f"k_gsf3<{p},{q}> (assembled sum factorization, scalar FP64 + CSR write)"
     elif code == 2:
@@ -285,7 +289,10 @@ def alt_leg(cfg, assembly, args, flush, stream, wl, total_el, peaks):
     roof = kernel_roofline(sess.code, wl, K, p, p + 1, K**3, 8 * sess.values.numel(), kms, peaks)
     prof = os.path.join(ROOT, "profiles", f"ncu_{wl['name']}_{assembly}_traffic.json")
     if os.path.exists(prof):
-        roof["traffic"] = json.load(open(prof)).get("dram_bytes_per_launch")
+        tr = json.load(open(prof))
+        # only the kernel that capture measured
+        if tr.get("kernel", "").startswith(roof["kernel"].split(" ")[0].split("<")[0]):
+            roof["traffic"] = tr.get("dram_bytes_per_launch")
     out = {"assembly": assembly, "value": total_el / (ms / 1e3), "unit": "elements/s",
            "ms_per_step": ms, "gpu_launches": 2 * args.steps, "roofline": roof}
     del sess
@@ -415,7 +422,10 @@ def main():
     roof = kernel_roofline(sess.code, wl, K, p, q, k_el, by, kern_ms, peaks)
     prof = os.path.join(ROOT, "profiles", f"ncu_{wname}_traffic.json")
     if os.path.exists(prof):
-        roof["traffic"] = json.load(open(prof)).get("dram_bytes_per_launch")
+        tr = json.load(open(prof))
+        # only the kernel that capture measured
+        if tr.get("kernel", "").startswith(roof["kernel"].split(" ")[0].split("<")[0]):
+            roof["traffic"] = tr.get("dram_bytes_per_launch")
 
     # end to end through the public API with host buffers (pinned), N=1 only
     e2e = None

@@ -12,6 +12,8 @@
 //  * k_sumfact_scatter -- Algorithm 2 element-local, stages in shared memory
 //    (Foata classes p+1..p+6 of taskgraph.py:204-223 -> barrier phases),
 //    fused atomic scatter.
+#include <cstdlib>
+
 #include "iga_args.cuh"
 #include "iga_dispatch.cuh"
 
@@ -122,6 +124,171 @@ __global__ void __launch_bounds__(256) k_classical_scatter(ScatterArgs a) {
         }
         scatter_add(a, P, N, I, J, acc);
         if (row != col) scatter_add(a, P, N, J, I, acc);
+      }
+    }
+  }
+}
+
+// Algorithm 1 in 3D on the FP64 tensor cores (mma.sync m8n8k4 f64, "DMMA").
+// Per element the local matrix is a sum of Gram products over the quadrature
+// points,  M_e = sum_t  A_t^T diag(W) B_t,  A_t(q, i) = prod_d T_{t,d}(i_d, q_d),
+// with t over the terms of the operator (mass: V V V; stiffness: D V V, V D V,
+// V V D), so each 8x8 output tile of the n x n matrix is KS = ceil(q^3 / 4)
+// DMMA steps per term with operands formed on the fly from the per-axis tables.
+// Only the upper triangle of tiles is computed; each warp owns one row tile and
+// a chunk of CH column tiles, so an A fragment is built once per k-step and
+// reused over the chunk.  The scatter mirrors every strictly-upper value to the
+// lower triangle, which keeps the assembled matrix bitwise symmetric like the
+// reference's (integrators.py:5 fills the mirror of each canonical pair, and
+// assembly.py:71-79 adds all n^2 entries of the symmetric element matrix).
+// Column slots come from per-element tables (row offset into the CSR window,
+// per-axis band shifts and counts) instead of per-entry int64 index math.
+__device__ __forceinline__ void dmma_acc(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(d0), "+d"(d1)
+      : "d"(a), "d"(b));
+}
+
+template <int P, int Q>
+struct ClassicalMma {
+  static constexpr int m = P + 1, n = m * m * m, nq = Q * Q * Q;
+  static constexpr int MT = (n + 7) / 8, KS = (nq + 3) / 4, CH = 4;
+  // work items: (row tile mt, column tiles nt0 .. nt0+CH-1), nt >= mt
+  static constexpr int items() {
+    int c = 0;
+    for (int mt = 0; mt < MT; ++mt) c += (MT - mt + CH - 1) / CH;
+    return c;
+  }
+};
+
+template <int P, int Q>
+__global__ void __launch_bounds__(256) k_classical_mma(ScatterArgs a) {
+  using C = ClassicalMma<P, Q>;
+  constexpr int m = C::m, n = C::n, nq = C::nq, MT = C::MT, KS = C::KS, CH = C::CH;
+  constexpr int NITEMS = C::items();
+  __shared__ double sV[3][m][Q], sD[3][m][Q], sW[nq];
+  __shared__ int64_t s_rowoff[n];  // CSR offset of local row i (relative to a.base), -1: not owned
+  __shared__ int s_shift[3][m], s_cnt[3][m];
+  const int64_t N = (int64_t)a.K + P;
+  const int64_t n_el = (int64_t)(a.el_end - a.el_begin) * a.K * a.K;
+  const bool stiff = a.op != IGA_OP_MASS;
+  const bool with_mass = a.op != IGA_OP_STIFFNESS;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, tq = lane & 3;
+  for (int64_t el = blockIdx.x; el < n_el; el += gridDim.x) {
+    int alpha[3];
+    alpha[2] = (int)(el % a.K);
+    alpha[1] = (int)((el / a.K) % a.K);
+    alpha[0] = a.el_begin + (int)(el / ((int64_t)a.K * a.K));
+    __syncthreads();
+    for (int t = threadIdx.x; t < 3 * m * Q; t += blockDim.x) {
+      const int d = t / (m * Q), rk = t % (m * Q);
+      sV[d][rk / Q][rk % Q] = a.V[(int64_t)alpha[d] * m * Q + rk];
+      sD[d][rk / Q][rk % Q] = stiff ? a.D[(int64_t)alpha[d] * m * Q + rk] : 0.0;
+    }
+    const int64_t eid = ((int64_t)alpha[0] * a.K + alpha[1]) * a.K + alpha[2];
+    for (int t = threadIdx.x; t < nq; t += blockDim.x) {
+      const int k1 = t / (Q * Q), k2 = (t / Q) % Q, k3 = t % Q;
+      double W = a.weights[k1] * a.weights[k2] * a.jac * a.weights[k3];
+      W *= a.coef ? a.coef[eid * nq + t] : a.coef_scalar;
+      sW[t] = W;
+    }
+    for (int t = threadIdx.x; t < n; t += blockDim.x) {
+      const int64_t I0 = alpha[0] + t / (m * m), I1 = alpha[1] + (t / m) % m, I2 = alpha[2] + t % m;
+      const int64_t row = (I0 * N + I1) * N + I2;
+      s_rowoff[t] = row >= a.row_first && row < a.row_last ? rowptr3(I0, I1, I2, P, N) - a.base : -1;
+    }
+    for (int t = threadIdx.x; t < 3 * m; t += blockDim.x) {
+      const int d = t / m, k = t % m;
+      const int64_t I = alpha[d] + k;
+      s_shift[d][k] = (int)(alpha[d] - band_lo(I, P));  // slot of column alpha_d + c: c + shift
+      s_cnt[d][k] = (int)band_cnt(I, P, N);
+    }
+    __syncthreads();
+    for (int item = warp; item < NITEMS; item += blockDim.x >> 5) {
+      int it = item, mt = 0;
+      for (; mt < MT; ++mt) {
+        const int c = (MT - mt + CH - 1) / CH;
+        if (it < c) break;
+        it -= c;
+      }
+      const int nt0 = mt + it * CH;
+      // A row of this lane, B columns of this lane per chunk tile (clamped; zeroed below)
+      const int ia = min(8 * mt + g, n - 1);
+      const int a0 = ia / (m * m), a1 = (ia / m) % m, a2 = ia % m;
+      const bool a_ok = 8 * mt + g < n;
+      int b0[CH], b1[CH], b2[CH];
+      bool b_ok[CH];
+#pragma unroll
+      for (int c = 0; c < CH; ++c) {
+        const int jb = 8 * (nt0 + c) + g;
+        b_ok[c] = jb < n;
+        const int j = min(jb, n - 1);
+        b0[c] = j / (m * m); b1[c] = (j / m) % m; b2[c] = j % m;
+      }
+      double acc[CH][2];
+#pragma unroll
+      for (int c = 0; c < CH; ++c) acc[c][0] = acc[c][1] = 0.0;
+#pragma unroll 2
+      for (int ks = 0; ks < KS; ++ks) {
+        const int qr = 4 * ks + tq;
+        const int q = min(qr, nq - 1);
+        const int q0 = q / (Q * Q), q1 = (q / Q) % Q, q2 = q % Q;
+        const double w = a_ok && qr < nq ? sW[q] : 0.0;
+        const double va0 = sV[0][a0][q0], va1 = sV[1][a1][q1], va2 = sV[2][a2][q2];
+        const double wv12 = w * va1 * va2;
+        const double am = wv12 * va0;
+        double ad0 = 0.0, ad1 = 0.0, ad2 = 0.0;
+        if (stiff) {
+          const double wv0 = w * va0;
+          ad0 = wv12 * sD[0][a0][q0];
+          ad1 = wv0 * sD[1][a1][q1] * va2;
+          ad2 = wv0 * va1 * sD[2][a2][q2];
+        }
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+          if (nt0 + c >= MT) break;  // warp-uniform
+          const double z = b_ok[c] ? 1.0 : 0.0;
+          const double vb0 = sV[0][b0[c]][q0] * z, vb1 = sV[1][b1[c]][q1], vb2 = sV[2][b2[c]][q2];
+          if (stiff) {
+            const double v12 = vb1 * vb2;
+            dmma_acc(acc[c][0], acc[c][1], ad0, sD[0][b0[c]][q0] * z * v12);
+            dmma_acc(acc[c][0], acc[c][1], ad1, vb0 * sD[1][b1[c]][q1] * vb2);
+            dmma_acc(acc[c][0], acc[c][1], ad2, vb0 * vb1 * sD[2][b2[c]][q2]);
+            if (with_mass) dmma_acc(acc[c][0], acc[c][1], am, vb0 * v12);
+          } else {
+            dmma_acc(acc[c][0], acc[c][1], am, vb0 * vb1 * vb2);
+          }
+        }
+      }
+      // C fragment: lane holds (i = 8 mt + g, j = 8 nt + 2 tq + e), e = 0, 1
+      const int i = 8 * mt + g;
+      if (i < n) {
+        const int i0 = i / (m * m), i1 = (i / m) % m, i2 = i % m;
+        const int64_t off_i = s_rowoff[i];
+#pragma unroll
+        for (int c = 0; c < CH; ++c) {
+          const int nt = nt0 + c;
+          if (nt >= MT) break;
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int j = 8 * nt + 2 * tq + e;
+            if (j >= n || (nt == mt && j < i)) continue;
+            const int j0 = j / (m * m), j1 = (j / m) % m, j2 = j % m;
+            const double v = acc[c][e];
+            if (off_i >= 0) {
+              const int slot = ((j0 + s_shift[0][i0]) * s_cnt[1][i1] + j1 + s_shift[1][i1]) * s_cnt[2][i2] +
+                               j2 + s_shift[2][i2];
+              atomicAdd(a.values + off_i + slot, v);
+            }
+            const int64_t off_j = s_rowoff[j];
+            if (j != i && off_j >= 0) {
+              const int slot = ((i0 + s_shift[0][j0]) * s_cnt[1][j1] + i1 + s_shift[1][j1]) * s_cnt[2][j2] +
+                               i2 + s_shift[2][j2];
+              atomicAdd(a.values + off_j + slot, v);
+            }
+          }
+        }
       }
     }
   }
@@ -241,7 +408,13 @@ struct ScatterLaunch {
     if (n_el <= 0) return IGA_OK;
     int64_t grid = n_el < 148 * 64 ? n_el : 148 * 64;
     if (method == IGA_METHOD_CLASSICAL) {
-      if (a.dim == 3)
+      static const bool scalar = [] {
+        const char* e = getenv("IGA_CLASSICAL_SCALAR");
+        return e && e[0] == '1';
+      }();
+      if (a.dim == 3 && !scalar)
+        k_classical_mma<P, Q><<<(unsigned)grid, 256, 0, s>>>(a);
+      else if (a.dim == 3)
         k_classical_scatter<3, P, Q><<<(unsigned)grid, 256, 0, s>>>(a);
       else
         k_classical_scatter<2, P, Q><<<(unsigned)grid, 256, 0, s>>>(a);

@@ -17,6 +17,9 @@ Separable path (iga_kron.cu, scalar coefficient): the 1D element integrals
 multiply and one FMA (stiffness; mass: one multiply) -- a few flops per 8-byte
 value written, so the HBM write of the values binds.
 
+Classical (Algorithm 1, iga_scatter.cu k_classical_mma): 2 x terms x pairs x q^3
+per element, see classical_flops.
+
 Bytes: 8 nnz written (each CSR value exactly once) + 8 K^3 q^3 read when a
 per-quadrature-point coefficient field is given.
 """
@@ -56,6 +59,16 @@ def element_sumfact_flops(op: str, p: int, q: int) -> int:
     if op == "mass":
         return 2 * (S1 + S2 + S3)
     return 2 * (2 * S1 + 3 * S2 + 2 * S3)
+
+
+def classical_flops(op: str, p: int, q: int, dim: int = 3) -> int:
+    """Algorithm 1 per element: one FMA per (canonical pair, quadrature point,
+    operator term) -- terms: mass 1, stiffness dim, stiffness+mass dim + 1 (the
+    Gram-product form k_classical_mma evaluates; operand formation not counted).
+    The reference's own count (integrators.py:154-170) is 10 per pair and point."""
+    n = (p + 1) ** dim
+    terms = {"mass": 1, "stiffness": dim, "stiffness_mass": dim + 1}[op]
+    return 2 * terms * (n * (n + 1) // 2) * q**dim
 
 
 def algorithmic_bytes(dim: int, K: int, p: int, q: int, coefficient_field: bool) -> int:
