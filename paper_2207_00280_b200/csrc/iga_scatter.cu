@@ -135,12 +135,14 @@ __global__ void __launch_bounds__(256) k_classical_scatter(ScatterArgs a) {
 // with t over the terms of the operator (mass: V V V; stiffness: D V V, V D V,
 // V V D), so each 8x8 output tile of the n x n matrix is KS = ceil(q^3 / 4)
 // DMMA steps per term with operands formed on the fly from the per-axis tables.
-// Only the upper triangle of tiles is computed; each warp owns one row tile and
-// a chunk of CH column tiles, so an A fragment is built once per k-step and
-// reused over the chunk.  The scatter mirrors every strictly-upper value to the
-// lower triangle, which keeps the assembled matrix bitwise symmetric like the
+// Only the upper triangle of tiles is computed; each warp owns a balanced
+// contiguous range of the row-major tile list, walked in segments of <= CH
+// tiles of one row tile, so an A fragment is built once per k-step and reused
+// over the segment.  The scatter mirrors every strictly-upper value to the
+// lower triangle, so each element matrix is exactly symmetric like the
 // reference's (integrators.py:5 fills the mirror of each canonical pair, and
-// assembly.py:71-79 adds all n^2 entries of the symmetric element matrix).
+// assembly.py:71-79 adds all n^2 entries of the symmetric element matrix); the
+// atomic inter-element order makes the assembled matrix symmetric to rounding.
 // Column slots come from per-element tables (row offset into the CSR window,
 // per-axis band shifts and counts) instead of per-entry int64 index math.
 __device__ __forceinline__ void dmma_acc(double& d0, double& d1, double a, double b) {
@@ -153,19 +155,14 @@ template <int P, int Q>
 struct ClassicalMma {
   static constexpr int m = P + 1, n = m * m * m, nq = Q * Q * Q;
   static constexpr int MT = (n + 7) / 8, KS = (nq + 3) / 4, CH = 4;
-  // work items: (row tile mt, column tiles nt0 .. nt0+CH-1), nt >= mt
-  static constexpr int items() {
-    int c = 0;
-    for (int mt = 0; mt < MT; ++mt) c += (MT - mt + CH - 1) / CH;
-    return c;
-  }
+  static constexpr int NTILES = MT * (MT + 1) / 2;  // upper 8x8 tiles (nt >= mt)
 };
 
 template <int P, int Q>
 __global__ void __launch_bounds__(256) k_classical_mma(ScatterArgs a) {
   using C = ClassicalMma<P, Q>;
   constexpr int m = C::m, n = C::n, nq = C::nq, MT = C::MT, KS = C::KS, CH = C::CH;
-  constexpr int NITEMS = C::items();
+  constexpr int NTILES = C::NTILES;
   __shared__ double sV[3][m][Q], sD[3][m][Q], sW[nq];
   __shared__ int64_t s_rowoff[n];  // CSR offset of local row i (relative to a.base), -1: not owned
   __shared__ int s_shift[3][m], s_cnt[3][m];
@@ -205,15 +202,17 @@ __global__ void __launch_bounds__(256) k_classical_mma(ScatterArgs a) {
       s_cnt[d][k] = (int)band_cnt(I, P, N);
     }
     __syncthreads();
-    for (int item = warp; item < NITEMS; item += blockDim.x >> 5) {
-      int it = item, mt = 0;
-      for (; mt < MT; ++mt) {
-        const int c = (MT - mt + CH - 1) / CH;
-        if (it < c) break;
-        it -= c;
-      }
-      const int nt0 = mt + it * CH;
-      // A row of this lane, B columns of this lane per chunk tile (clamped; zeroed below)
+    // contiguous, balanced ranges of the row-major upper-tile list per warp, cut into
+    // segments of <= CH tiles sharing the row tile mt
+    const int nwarps = blockDim.x >> 5;
+    const int t_hi = (warp + 1) * NTILES / nwarps;
+    for (int t = warp * NTILES / nwarps; t < t_hi;) {
+      int mt = 0, nt0 = t;
+      while (nt0 >= MT - mt) nt0 -= MT - mt++;
+      nt0 += mt;
+      const int len = min(min(CH, t_hi - t), MT - nt0);
+      t += len;
+      // A row of this lane, B columns of this lane per segment tile (clamped; zeroed below)
       const int ia = min(8 * mt + g, n - 1);
       const int a0 = ia / (m * m), a1 = (ia / m) % m, a2 = ia % m;
       const bool a_ok = 8 * mt + g < n;
@@ -247,7 +246,7 @@ __global__ void __launch_bounds__(256) k_classical_mma(ScatterArgs a) {
         }
 #pragma unroll
         for (int c = 0; c < CH; ++c) {
-          if (nt0 + c >= MT) break;  // warp-uniform
+          if (c >= len) break;  // warp-uniform
           const double z = b_ok[c] ? 1.0 : 0.0;
           const double vb0 = sV[0][b0[c]][q0] * z, vb1 = sV[1][b1[c]][q1], vb2 = sV[2][b2[c]][q2];
           if (stiff) {
@@ -269,7 +268,7 @@ __global__ void __launch_bounds__(256) k_classical_mma(ScatterArgs a) {
 #pragma unroll
         for (int c = 0; c < CH; ++c) {
           const int nt = nt0 + c;
-          if (nt >= MT) break;
+          if (c >= len) break;
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int j = 8 * nt + 2 * tq + e;

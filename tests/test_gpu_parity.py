@@ -226,7 +226,7 @@ def test_assembled_sumfact_deterministic(pkg, assembly):
 
 
 
-@pytest.mark.parametrize("method", ["assembled", "separable"])
+@pytest.mark.parametrize("method", ["assembled", "separable", "classical"])
 def test_slabs_sum_to_full(pkg, method):
     """Multi-GPU decomposition emulated on one GPU: element slabs along the slowest
     axis produce partial interface rows that add up to the single-device matrix."""
@@ -234,7 +234,8 @@ def test_slabs_sum_to_full(pkg, method):
     from paper_2207_00280_b200 import _lib
     from paper_2207_00280_b200.device import MeshProblem
 
-    code = _lib.METHOD_SUMFACT_ASSEMBLED if method == "assembled" else _lib.METHOD_SEPARABLE
+    code = {"assembled": _lib.METHOD_SUMFACT_ASSEMBLED, "separable": _lib.METHOD_SEPARABLE,
+            "classical": _lib.METHOD_CLASSICAL}[method]
     K, p = 10, 3
     N = K + p
     mp = MeshProblem(3, K, p, operator="stiffness")
@@ -304,6 +305,8 @@ def _sample_rows(K, p, n_rand, seed=0):
     dict(K=64, p=3, op="stiffness", coef=None, name="C3", assembly="owner"),
     dict(K=64, p=3, op="stiffness", coef=None, name="C3", assembly="separable"),
     dict(K=32, p=2, op="mass", coef="uniform", name="C2"),
+    dict(K=32, p=2, op="mass", coef="uniform", name="C2 classical", method="classical"),
+    dict(K=48, p=3, op="stiffness", coef="uniform", name="C3-48 classical", method="classical"),
 ])
 def test_full_size_sampled_rows(pkg, cfg):
     """BASELINE configs at full size: sampled rows (corner/edge/interior) vs the
@@ -314,8 +317,8 @@ def test_full_size_sampled_rows(pkg, cfg):
     if cfg["coef"] == "uniform":
         coef = np.random.default_rng(42).uniform(0.5, 1.5, size=(K, K, K, q, q, q))
         coef = coef.reshape(K**3, q**3)
-    res = pkg.run_integration(pkg.RunConfig("sumfact", "device", K, p, operator=op,
-                                            coefficient=coef,
+    res = pkg.run_integration(pkg.RunConfig(cfg.get("method", "sumfact"), "device", K, p,
+                                            operator=op, coefficient=coef,
                                             assembly=cfg.get("assembly", "auto")))
     values = res.gram.values.cpu().numpy()
     ip, _ = O.pattern(3, K, p)
