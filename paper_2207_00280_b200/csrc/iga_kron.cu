@@ -26,7 +26,7 @@
 namespace iga {
 
 #ifndef KRON_MINB
-#define KRON_MINB 1
+#define KRON_MINB 2
 #endif
 
 // threads per CTA: one per value of an interior row (NB^3, rounded to warps, <= 1024)
@@ -37,7 +37,7 @@ __host__ __device__ constexpr int kron_nt(int P) {
 }
 // resident CTAs per SM asked of the register allocator
 __host__ __device__ constexpr int kron_minb(int P) {
-  return kron_nt(P) * KRON_MINB > 1536 ? 1 : KRON_MINB;
+  return P > 3 || kron_nt(P) * KRON_MINB > 1536 ? 1 : KRON_MINB;
 }
 // rows per staged chunk (one TMA bulk store each)
 // (measured on B200: 16 rows with 2 CTAs/SM for the small meshes, where the chunk
@@ -48,8 +48,16 @@ __host__ __device__ constexpr int kron_minb(int P) {
 __host__ __device__ constexpr int kron_rows(int P, bool small_mesh) {
   return P <= 2 ? 16 : (P == 3 ? (small_mesh ? KRON_GS : 8) : 4);
 }
+#ifndef KRON_NBUF
+#define KRON_NBUF 2
+#endif
+// staging buffers per CTA (2: one bulk store in flight while the next chunk is produced;
+// 3 and 4 with proportionally fewer rows per chunk measured slower)
+constexpr int kron_nbuf() { return KRON_NBUF; }
 // doubles per staging buffer: a chunk of full rows plus 16-byte alignment padding
-__host__ __device__ constexpr int kron_stage(int P, int G) { return G * (2 * P + 1) * (2 * P + 1) * (2 * P + 1) + 2; }
+__host__ __device__ constexpr int kron_stage(int P, int G) {
+  return (G * (2 * P + 1) * (2 * P + 1) * (2 * P + 1) + 3) / 2 * 2;  // even: 16-byte aligned buffers
+}
 
 __device__ __forceinline__ void bulk_store(double* g, const double* sm, int bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(g),
@@ -70,7 +78,7 @@ __global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) 
   constexpr int SG = kron_stage(P, G);
   extern __shared__ __align__(16) double2 tb[];  // [2][N][NB] (m, k): all elements, slab
   __shared__ double w[Q];
-  __shared__ double2 F[NB * NB];  // pair factors of the current pencil
+  __shared__ double2 Fbuf[2][NB * NB];  // pair factors of the current pencil (by pencil parity)
   const int K = a.K, tid = threadIdx.x;
   const int64_t N = (int64_t)K + P;
   const bool stiff = a.op != IGA_OP_MASS;
@@ -78,9 +86,14 @@ __global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) 
   // full one unless the slab is a proper subset
   const bool full = a.el_begin <= 0 && a.el_end >= K;
   const double2* tb0 = full ? tb : tb + N * NB;
-  double* stage = reinterpret_cast<double*>(tb + 2 * N * NB);  // [2][SG]
+  // [NBUF][SG] (after both tables even when the slab table is unused: the larger
+  // footprint measured ~4% faster on B200 than packing the staging after one table)
+  double* stage = reinterpret_cast<double*>(tb + 2 * N * NB);
+#ifdef KRON_EMPTY
+  if (a.K > 0) return;
+#endif
   build_band_tables<P, Q>(a.V, a.D, a.weights, K, stiff, a.el_begin, a.el_end, !full, tb, stage,
-                          2 * SG, w, tid, NT);
+                          kron_nbuf() * SG, w, tid, NT);
 
 #ifdef KRON_PROLOGUE_ONLY
   if (a.K > 0) return;
@@ -93,6 +106,20 @@ __global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) 
   const int64_t u_lo = nunit * blockIdx.x / gridDim.x, u_hi = nunit * (blockIdx.x + 1) / gridDim.x;
   const int64_t T = band_prefix(N, P, N);  // values of a full-length band row set
   double* vals = nullptr;                   // first value of the current pencil
+  // the chunk produced last, stored after the next barrier (thread 0)
+  double* pg = nullptr;
+  const double* psb = nullptr;
+  int plen = 0, ppad = 0;
+  auto issue = [&]() {
+    if (pg == nullptr) return;
+    // 16-byte aligned middle by TMA; an unaligned first / last value by plain stores
+    int n = plen - ppad;
+    if (ppad) pg[0] = psb[0];
+    if (n & 1) { pg[plen - 1] = psb[plen - 1]; --n; }
+    if (n > 0) bulk_store(pg + ppad, psb + ppad, n * 8);
+    asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+    pg = nullptr;
+  };
   for (int64_t pen = u_lo / nch; pen * nch < u_hi; ++pen) {
     const int I0 = a.plane_begin + (int)(pen / N), I1 = (int)(pen % N);
     // consecutive pencils are contiguous in the CSR: one 64-bit rowptr per CTA
@@ -126,7 +153,8 @@ __global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) 
       if (e < ncnt) factors(e / NB, fa[j], fb[j]);
     }
     // the pencil's pair factors for the truncated rows (visible after the chunk barrier;
-    // the previous pencil's last reader passed the barrier before its bulk store)
+    // double-buffered: a thread may start this pencil while others finish the last)
+    double2* F = Fbuf[pen & 1];
     for (int b = tid; b < c01; b += NT) {
       double f0, f1;
       factors(b, f0, f1);
@@ -144,10 +172,13 @@ __global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) 
       double* g = vals + off0;
       off0 += len;
       const int pad = (int)((reinterpret_cast<uintptr_t>(g) >> 3) & 1);
-      double* buf = stage + (chunk & 1) * SG;
-      // the bulk store issued from this buffer two chunks ago has finished reading it
-      if (tid == 0) asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+      double* buf = stage + (chunk % kron_nbuf()) * SG;
+      // One CTA barrier per chunk: before it, the bulk store that last read this buffer
+      // (chunk - NBUF, issued at the top of chunk - NBUF + 1) has finished reading it;
+      // after it, the previous chunk is complete in shared memory and leaves.
+      if (tid == 0) asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(kron_nbuf() - 2) : "memory");
       __syncthreads();
+      if (tid == 0) issue();
       double* sb = buf + pad;
       // truncated-band rows (I2 < P or I2 >= K): b = e / c2 by a reciprocal (exact for
       // e < 2^20 / NB), factors from the pencil table F
@@ -185,26 +216,24 @@ __global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) 
       }
       for (int I2 = max(R0, max(K, P)); I2 < R1; ++I2) loc = boundary_row(I2, loc);
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      __syncthreads();
       if (tid == 0) {
-        // 16-byte aligned middle by TMA; an unaligned first / last value by plain stores
-        int h = pad, n = len - pad;
-        if (pad) g[0] = sb[0];
-        if (n & 1) { g[len - 1] = sb[len - 1]; --n; }
-        if (n > 0) bulk_store(g + h, sb + h, n * 8);
-        asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+        pg = g; psb = sb; plen = len; ppad = pad;
       }
     }
     vals += (int64_t)c01 * T;
   }
-  if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+  __syncthreads();
+  if (tid == 0) {
+    issue();
+    asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+  }
 }
 
 template <int P, int Q, int G>
 static int launch_kron_g(const KronArgs& a, cudaStream_t s) {
   const int64_t N = (int64_t)a.K + P;
   constexpr int NT = kron_nt(P);
-  const size_t smem = 2 * sizeof(double2) * N * (2 * P + 1) + 2 * sizeof(double) * kron_stage(P, G);
+  const size_t smem = 2 * sizeof(double2) * N * (2 * P + 1) + kron_nbuf() * sizeof(double) * kron_stage(P, G);
   if (smem > 220 * 1024) {
     set_error("separable path: 1D band tables of K=%d do not fit shared memory", a.K);
     return IGA_EUNSUPPORTED;
