@@ -17,8 +17,8 @@ Separable path (iga_kron.cu, scalar coefficient): the 1D element integrals
 multiply and one FMA (stiffness; mass: one multiply) -- a few flops per 8-byte
 value written, so the HBM write of the values binds.
 
-Classical (Algorithm 1, iga_scatter.cu k_classical_mma): 2 x terms x pairs x q^3
-per element, see classical_flops.
+Classical (Algorithm 1, iga_scatter.cu k_classical_mma): SURVEY.md §8(d)'s
+per-(pair, point) counts, see classical_flops.
 
 Bytes: 8 nnz written (each CSR value exactly once) + 8 K^3 q^3 read when a
 per-quadrature-point coefficient field is given.
@@ -62,13 +62,14 @@ def element_sumfact_flops(op: str, p: int, q: int) -> int:
 
 
 def classical_flops(op: str, p: int, q: int, dim: int = 3) -> int:
-    """Algorithm 1 per element: one FMA per (canonical pair, quadrature point,
-    operator term) -- terms: mass 1, stiffness dim, stiffness+mass dim + 1 (the
-    Gram-product form k_classical_mma evaluates; operand formation not counted).
-    The reference's own count (integrators.py:154-170) is 10 per pair and point."""
+    """Algorithm 1 per element, SURVEY.md §8(d)'s minimal count with the per-axis pair
+    products precomputed: per (canonical pair, quadrature point) mass 4 flops,
+    stiffness 10, stiffness+mass 12 (3D; 2D: mass 3, stiffness 6, stiffness+mass 8).
+    The reference's own model (integrators.py:154-170) is 10 per pair and point."""
     n = (p + 1) ** dim
-    terms = {"mass": 1, "stiffness": dim, "stiffness_mass": dim + 1}[op]
-    return 2 * terms * (n * (n + 1) // 2) * q**dim
+    per = {3: {"mass": 4, "stiffness": 10, "stiffness_mass": 12},
+           2: {"mass": 3, "stiffness": 6, "stiffness_mass": 8}}[dim][op]
+    return per * (n * (n + 1) // 2) * q**dim
 
 
 def algorithmic_bytes(dim: int, K: int, p: int, q: int, coefficient_field: bool) -> int:

@@ -195,3 +195,20 @@ def test_bench_csv_columns_match_reference_cli():
     if src is None:
         pytest.skip("reference not mounted")
     assert f"BENCH_COLUMNS = {BENCH_COLUMNS!r}".replace("'", '"') in src
+
+
+def test_perfmodel_matches_survey_counts():
+    """Roofline numerators (bench.py): the algorithmic counts of SURVEY.md §8(d)'s table
+    and §8 derived sizes."""
+    from paper_2207_00280_b200 import perfmodel as m
+
+    # classical, per element (§8(d) "flops/el (classical)")
+    assert m.classical_flops("mass", 2, 3) == 40_824                 # C2
+    assert m.classical_flops("stiffness", 3, 4) == 1_331_200         # C3, C5
+    assert m.classical_flops("stiffness_mass", 4, 5) == 11_812_500   # C4
+    # general element-local sum factorization, per element (§8(d) "flops/el (sumfact general)")
+    assert m.element_sumfact_flops("mass", 2, 3) == 4_212
+    assert m.element_sumfact_flops("stiffness", 3, 4) == 61_952
+    # bytes: 8 nnz (+ 8 q^3 per element for a field); nnz from §8's size table
+    assert m.algorithmic_bytes(3, 64, 3, 4, False) == 8 * 95_443_993
+    assert m.algorithmic_bytes(3, 32, 2, 3, True) == 8 * 4_410_944 + 8 * 32**3 * 27
