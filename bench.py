@@ -312,6 +312,8 @@ def main():
     ap.add_argument("--no-graph", action="store_true", help="launch the step eagerly")
     ap.add_argument("--assembly", default="auto", help="force a kernel path (RunConfig.assembly)")
     ap.add_argument("--method", default=None, help="override the workload's method")
+    ap.add_argument("--halo", choices=["exchange", "recompute"], default="exchange",
+                    help="N>1: NCCL interface exchange (default) or the NCCL-free recompute ablation")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -348,7 +350,7 @@ def main():
         from paper_2207_00280_b200.distributed import SlabSession, slab_plan
 
         plan = slab_plan(K, p, world, rank)
-        sess = SlabSession(cfg, plan)
+        sess = SlabSession(cfg, plan, halo=args.halo)
         step = sess.step
         n_el = (plan.el_hi - plan.el_lo) * K * K
         launches = sess.kernel_launches_per_step
@@ -401,7 +403,8 @@ def main():
         flush.fill_(float(i))
         a.record(stream)
         if world > 1:
-            sess.prob.integrate_assemble(sess.values, sess.code, el_range=(plan.el_lo, plan.el_hi),
+            el = plan.recompute_elements if args.halo == "recompute" else (plan.el_lo, plan.el_hi)
+            sess.prob.integrate_assemble(sess.values, sess.code, el_range=el,
                                          plane_range=(plan.own_lo, plan.own_hi), stream=stream)
         else:
             sess.prob.integrate_assemble(sess.values, sess.code, stream=stream)
@@ -411,7 +414,8 @@ def main():
     kern_ms = float(np.mean([a.elapsed_time(b) for a, b in kev]))
     peaks = load_peaks()
     if world > 1:
-        k_el = (plan.el_hi - plan.el_lo) * K * K
+        el = plan.recompute_elements if args.halo == "recompute" else (plan.el_lo, plan.el_hi)
+        k_el = (el[1] - el[0]) * K * K
         k_planes = plan.own_hi - plan.own_lo
     else:
         k_el = n_el
@@ -479,7 +483,8 @@ def main():
                            "per-quadrature-point kernel on the same matrix: other_kernel)"
                            if sess.code == 3 else ""),
                        "nnz": P.device.csr_nnz(wl["dim"], K, p),
-                       "parallelism": f"element slabs x{world}" if world > 1 else "1 GPU",
+                       "parallelism": (f"element slabs x{world}, halo {args.halo}" if world > 1
+                                       else "1 GPU"),
                        "l2": "256 MB buffer written between timed steps (outside the per-step "
                              "events); each step also writes the whole CSR (> 126 MB L2)"},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "other_kernel": other,

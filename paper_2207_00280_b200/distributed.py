@@ -12,6 +12,11 @@ point-to-point transfer (overlapped with the interior compute), and added by
 g+1 into its own first p planes with ``iga_axpy``.  No other data crosses
 ranks.  The exchange is the only collective: the path is otherwise
 embarrassingly parallel.
+
+``SlabSession(..., halo="recompute")`` is the NCCL-free ablation of SURVEY.md
+§8(e): rank g also integrates the p element layers below its slab, restricted
+to its own planes, so its first p planes are complete without any transfer
+(p / (K/G) extra element work: 9.4% at C5 with G=8, 2.3% with G=2).
 """
 
 from __future__ import annotations
@@ -36,6 +41,12 @@ class SlabPlan:
     @property
     def send_planes(self) -> tuple[int, int]:
         return (self.own_hi, self.comp_hi)
+
+    @property
+    def recompute_elements(self) -> tuple[int, int]:
+        """Element slab of the NCCL-free ablation: the own slab plus the p layers below
+        it, whose contributions complete the first p owned planes."""
+        return (max(0, self.el_lo - self.p), self.el_hi)
 
     @property
     def recv_planes(self) -> tuple[int, int]:
@@ -117,25 +128,33 @@ def exchange_interface(plan: SlabPlan, values, dim: int = 3, group=None, add=Non
     return recv
 
 
+HALO_MODES = ("exchange", "recompute")
+
+
 class SlabSession:
     """Per-rank device state for the distributed integrate+assemble step.
 
-    step(): interface planes first (so the NCCL send can start), then the
-    owned planes, then the exchange and the interface accumulation."""
+    halo="exchange" (default, the deliverable): step() computes the interface
+    planes first (so the NCCL send can start), then the owned planes, then the
+    exchange and the interface accumulation.  halo="recompute": one launch over
+    the elements [el_lo - p, el_hi) restricted to the owned planes, no exchange."""
 
-    def __init__(self, cfg, plan: SlabPlan):
+    def __init__(self, cfg, plan: SlabPlan, halo: str = "exchange"):
         torch = _lib.require_cuda()
         from .device import MeshProblem
         from .runtime import method_code
 
         if cfg.dim != 3:
             raise ValueError("distributed slabs are implemented for dim=3")
-        self.cfg, self.plan = cfg, plan
+        if halo not in HALO_MODES:
+            raise ValueError(f"halo must be one of {HALO_MODES}, got {halo!r}")
+        self.cfg, self.plan, self.halo = cfg, plan, halo
         self.code = method_code(cfg)
         self.prob = MeshProblem(3, cfg.mesh, cfg.degree, cfg.points, cfg.operator,
                                 cfg.coefficient)
         self.n_own = plane_nnz(3, plan.K, plan.p, plan.own_lo, plan.own_hi)
-        self.n_comp = plane_nnz(3, plan.K, plan.p, plan.own_lo, plan.comp_hi)
+        hi = plan.own_hi if halo == "recompute" else plan.comp_hi
+        self.n_comp = plane_nnz(3, plan.K, plan.p, plan.own_lo, hi)
         self.values = torch.empty(self.n_comp, dtype=torch.float64, device=self.prob.device)
         self.stream = torch.cuda.current_stream()
 
@@ -146,6 +165,10 @@ class SlabSession:
     def step(self, exchange: bool = True):
         pl = self.plan
         self.prob.build_tables(self.stream)
+        if self.halo == "recompute":
+            self.prob.integrate_assemble(self.values, self.code, el_range=pl.recompute_elements,
+                                         plane_range=(pl.own_lo, pl.own_hi), stream=self.stream)
+            return self.values
         el = (pl.el_lo, pl.el_hi)
         if pl.comp_hi > pl.own_hi:
             iface = self.values[self.n_own:]
@@ -163,4 +186,6 @@ class SlabSession:
     @property
     def kernel_launches_per_step(self) -> int:
         pl = self.plan
+        if self.halo == "recompute":
+            return 2
         return 1 + 1 + (1 if pl.comp_hi > pl.own_hi else 0) + (1 if pl.rank > 0 else 0)

@@ -368,6 +368,40 @@ def test_slab_sessions_emulated_ranks(pkg, G):
     assert_parity(got, full.cpu().numpy(), ip)
 
 
+@pytest.mark.parametrize("G,K,p,assembly,coef", [
+    (2, 12, 3, "auto", False), (3, 12, 3, "auto", False), (4, 12, 3, "owner", False),
+    (3, 9, 2, "auto", True), (2, 8, 4, "auto", True), (3, 12, 3, "classical", False)])
+def test_slab_sessions_recompute_halo(pkg, G, K, p, assembly, coef):
+    """NCCL-free ablation: each rank also integrates the p element
+    layers below its slab, restricted to its owned planes; the owned rows concatenated
+    over ranks equal the single-device matrix with no exchange at all."""
+    import torch
+    from paper_2207_00280_b200.distributed import SlabSession, slab_plan
+
+    q = p + 1
+    c = np.random.default_rng(3).uniform(0.5, 1.5, size=(K**3, q**3)) if coef else None
+    method = "classical" if assembly == "classical" else "sumfact"
+    asm = "auto" if assembly == "classical" else assembly
+    cfg = pkg.RunConfig(method, "device", K, p, operator="stiffness_mass" if coef else "stiffness",
+                        coefficient=c, assembly=asm)
+    full = pkg.run_integration(cfg).gram.values
+    sessions = [SlabSession(cfg, slab_plan(K, p, G, g), halo="recompute") for g in range(G)]
+    outs = [s.step() for s in sessions]
+    assert all(s.kernel_launches_per_step == 2 for s in sessions)
+    torch.cuda.synchronize()
+    got = torch.cat(outs).cpu().numpy()
+    ip, _ = O.pattern(3, K, p)
+    assert got.size == ip[-1]
+    assert_parity(got, full.cpu().numpy(), ip)
+
+
+def test_slab_session_rejects_unknown_halo(pkg):
+    from paper_2207_00280_b200.distributed import SlabSession, slab_plan
+
+    with pytest.raises(ValueError):
+        SlabSession(pkg.RunConfig("sumfact", "device", 8, 2), slab_plan(8, 2, 2, 0), halo="x")
+
+
 # ---------------------------------------------- §8(f): matrix-free apply, CG
 @pytest.mark.parametrize("K,p,coef", [(5, 3, False), (4, 2, True), (3, 4, True), (6, 1, False)])
 def test_matrix_free_apply_matches_assembled(pkg, K, p, coef):
