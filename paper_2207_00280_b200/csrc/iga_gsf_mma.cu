@@ -110,23 +110,31 @@ __global__ void __launch_bounds__(NT, P <= 2 ? 2 : 1) k_gsf3_mma(GsfArgs a) {
     comboR[c] = (ia * TB + ib) * m * S::rowVals + (d0 * NB + d1) * NB;
   }
 
-  // coefficient of the next element column for this thread's W entries
-  constexpr int WPT = cdiv(S::nW, NT);
-  auto load_coef = [&](int e2, double (&cv)[WPT]) {
+  // W units: one (kk, (lb, k1)) row segment of Q contiguous k2 columns per unit (the Q
+  // coefficients of a unit are contiguous in memory); the thread's units are fixed, and
+  // their coefficients for the next element column are prefetched into registers
+  constexpr int NUW = KA * KB, UPT = cdiv(NUW, NT), Q3 = Q * Q * Q;
+  __shared__ double wqs[Q];
+  if (tid < Q) wqs[tid] = a.weights[tid];
+  auto load_coef = [&](int e2, double (&cv)[UPT][Q]) {
 #pragma unroll
-    for (int i = 0; i < WPT; ++i) {
+    for (int i = 0; i < UPT; ++i) {
+#pragma unroll
+      for (int k2 = 0; k2 < Q; ++k2) cv[i][k2] = a.coef_scalar;
       const int u = tid + i * NT;
-      cv[i] = a.coef_scalar;
-      if (a.coef && u < S::nW && e2 < K) {
-        const int kk = u / GC, col = u % GC;
-        const int la = kk / Q, k0 = kk % Q, lb = col / (Q * Q), k1 = (col / Q) % Q, k2 = col % Q;
+      if (a.coef && u < NUW && e2 < K) {
+        const int kk = u / KB, c1 = u - kk * KB, la = kk / Q, k0 = kk - la * Q;
+        const int lb = c1 / Q, k1 = c1 - lb * Q;
         const int e0 = i00 - P + la, e1 = i10 - P + lb;
-        if (e0 >= 0 && e0 < K && e1 >= 0 && e1 < K)
-          cv[i] = __ldg(a.coef + (((int64_t)e0 * K + e1) * K + e2) * (Q * Q * Q) + (k0 * Q + k1) * Q + k2);
+        if (e0 >= 0 && e0 < K && e1 >= 0 && e1 < K) {
+          const double* src = a.coef + (((int64_t)e0 * K + e1) * K + e2) * Q3 + (k0 * Q + k1) * Q;
+#pragma unroll
+          for (int k2 = 0; k2 < Q; ++k2) cv[i][k2] = __ldg(src + k2);
+        }
       }
     }
   };
-  double cv[WPT];
+  double cv[UPT][Q];
   load_coef(e_first, cv);
   // axis-2 table entries of the next element (one (r, s, k) per thread)
   static_assert(m * m * Q <= NT, "one Z entry per thread");
@@ -149,12 +157,19 @@ __global__ void __launch_bounds__(NT, P <= 2 ? 2 : 1) k_gsf3_mma(GsfArgs a) {
 
   // a finished row leaves (and its slot is cleared) in the next column's stage-A phase, so
   // the row store costs no barrier of its own
+  // per pencil rc of the row being flushed: CSR offset (-1: not written here) and, for
+  // rows with a truncated band, the packed (lod0, lod1, c0, c1); 0 marks a full band
+  __shared__ int rowmeta[TA * TB];
   auto set_rowoff = [&](int I2) {
     if (tid < TA * TB) {
       const int ia = tid / TB, ib = tid % TB;
-      const int64_t I0 = i00 + ia, I1 = i10 + ib;
-      rowoff[tid] = (I2 >= s0 && I0 < a.plane_end && I1 < N) ? rowptr3(I0, I1, I2, P, N) - a.base
-                                                            : -1;
+      const int I0 = i00 + ia, I1 = i10 + ib;
+      const bool ok = I2 >= s0 && I0 < a.plane_end && I1 < N;
+      rowoff[tid] = ok ? rowptr3(I0, I1, I2, P, N) - a.base : -1;
+      const bool full = I0 >= P && I0 < K && I1 >= P && I1 < K && I2 >= P && I2 < K;
+      rowmeta[tid] = full ? 0
+                          : 1 | max(0, P - I0) << 1 | max(0, P - I1) << 6 |
+                                (int)band_cnt(I0, P, N) << 11 | (int)band_cnt(I1, P, N) << 16;
     }
   };
   auto flush_row = [&](int I2) {
@@ -165,14 +180,13 @@ __global__ void __launch_bounds__(NT, P <= 2 ? 2 : 1) k_gsf3_mma(GsfArgs a) {
       double* Rv = R + (rc * m + slot) * S::rowVals + v;
       const int64_t off = rowoff[rc];
       if (off >= 0) {
-        const int ia = rc / TB, ib = rc - ia * TB;
-        const int I0 = i00 + ia, I1 = i10 + ib;
-        if (I0 >= P && I0 < K && I1 >= P && I1 < K && lod2 == 0 && c2 == NB) {
+        const int mt = rowmeta[rc];
+        if (mt == 0) {
           a.values[off + v] = *Rv;  // full band: CSR order is the R order
         } else {
+          const int lod0 = (mt >> 1) & 31, lod1 = (mt >> 6) & 31, c0 = (mt >> 11) & 31,
+                    c1 = (mt >> 16) & 31;
           const int d2 = v % NB, d1 = (v / NB) % NB, d0 = v / (NB * NB);
-          const int lod0 = max(0, P - I0), lod1 = max(0, P - I1);
-          const int c0 = (int)band_cnt(I0, P, N), c1 = (int)band_cnt(I1, P, N);
           if (d0 >= lod0 && d0 < lod0 + c0 && d1 >= lod1 && d1 < lod1 + c1 && d2 >= lod2 &&
               d2 < lod2 + c2)
             a.values[off + ((d0 - lod0) * c1 + (d1 - lod1)) * c2 + (d2 - lod2)] = *Rv;
@@ -186,12 +200,14 @@ __global__ void __launch_bounds__(NT, P <= 2 ? 2 : 1) k_gsf3_mma(GsfArgs a) {
     __syncthreads();  // previous column's stage S (reads Y, aliasing W) is done
     if (pending >= 0) set_rowoff(pending);
 #pragma unroll
-    for (int i = 0; i < WPT; ++i) {
+    for (int i = 0; i < UPT; ++i) {  // W = ((w0 w1) w2) jac c, the reference's factor order
       const int u = tid + i * NT;
-      if (u < S::nW) {
-        const int kk = u / GC, col = u % GC;
-        const int k0 = kk % Q, k1 = (col / Q) % Q, k2 = col % Q;
-        sW[u] = a.weights[k0] * a.weights[k1] * a.weights[k2] * a.jac * cv[i];
+      if (u < NUW) {
+        const int kk = u / KB, c1 = u - kk * KB;
+        const double w01 = wqs[kk % Q] * wqs[c1 % Q];
+        double* dst = sW + kk * GC + c1 * Q;
+#pragma unroll
+        for (int k2 = 0; k2 < Q; ++k2) dst[k2] = w01 * wqs[k2] * a.jac * cv[i][k2];
       }
     }
     load_coef(e2 + 1, cv);
