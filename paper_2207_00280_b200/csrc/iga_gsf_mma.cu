@@ -37,7 +37,8 @@ struct Shape {
   static constexpr int NA0 = TA * NB, NB1 = TB * NB, NC = NA0 * NB1, NR = NA0 * Q;
   static constexpr int rowVals = NB * NB * NB;
   static constexpr int nW = KA * GC, nY = 2 * NC * Q;
-  static constexpr int nWY = nW > nY ? nW : nY;   // Y aliases W (W is dead after stage A)
+  // Y aliases W (W is dead after stage A); even, so the double2 arrays after it are aligned
+  static constexpr int nWY = ((nW > nY ? nW : nY) + 1) / 2 * 2;
   static constexpr int nX = 2 * NA0 * GC;
   static constexpr int nPA = 2 * NA0 * KA, nPB = 2 * NB1 * KB;
   static constexpr int nZ = 2 * m * m * Q;
@@ -349,19 +350,24 @@ __global__ void __launch_bounds__(NT, P <= 2 ? 2 : 1) k_gsf3_mma(GsfArgs a) {
   }
 }
 
+// Tile of row pencils per CTA: 3 x 3 for p = 2 (stage-A rows 15 of 16 and stage-B columns
+// 15 of 16 in their DMMA tiles; C2 32^3: 144 tiles, 0.087 vs 0.099 ms with 2 x 4), else the
+// largest of 2 x 4 / 2 x 2 / 2 x 1 / 1 x 1 that fits shared memory
 template <int P, int Q, bool ST>
 struct Tile {
   static constexpr size_t cap = 227 * 1024;
-  static constexpr int TA = Shape<P, Q, 2, 4>::bytes <= cap ? 2
+  static constexpr bool t33 = P == 2 && Shape<P, Q, 3, 3>::bytes <= cap;
+  static constexpr int TA = t33 ? 3
+                            : Shape<P, Q, 2, 4>::bytes <= cap ? 2
                             : Shape<P, Q, 2, 2>::bytes <= cap ? 2
                             : Shape<P, Q, 2, 1>::bytes <= cap ? 2 : 1;
-  static constexpr int TB = Shape<P, Q, 2, 4>::bytes <= cap ? 4
+  static constexpr int TB = t33 ? 3
+                            : Shape<P, Q, 2, 4>::bytes <= cap ? 4
                             : Shape<P, Q, 2, 2>::bytes <= cap ? 2 : 1;
 };
 
-template <int P, int Q, bool ST>
+template <int P, int Q, bool ST, int TA = Tile<P, Q, ST>::TA, int TB = Tile<P, Q, ST>::TB>
 static int launch_t(const GsfArgs& a0, cudaStream_t s) {
-  constexpr int TA = Tile<P, Q, ST>::TA, TB = Tile<P, Q, ST>::TB;
   using Sh = Shape<P, Q, TA, TB>;
   if constexpr (Sh::bytes > 227 * 1024) {
     set_error("assembled sum factorization: p=%d q=%d needs %zu B shared memory", P, Q, Sh::bytes);
@@ -380,7 +386,9 @@ static int launch_t(const GsfArgs& a0, cudaStream_t s) {
     const int64_t slots = (int64_t)sm_count() * blocks_per_sm_once(fn, NT, Sh::bytes);
     int best = 1;
     double best_cost = 1e300;
+    const char* es = getenv("IGA_GSF_SEGS");  // tuning knob: force the segment count
     for (int sg = 1; sg <= a.K; ++sg) {
+      if (es && *es && sg != atoi(es)) continue;
       const int L = (a.K + sg - 1) / sg;
       if (L < P && sg > 1) break;
       const double waves = (double)((tiles * sg + slots - 1) / slots);
