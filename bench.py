@@ -229,7 +229,9 @@ def kernel_roofline(code, wl, K, p, q, k_el, by, kern_ms, peaks):
     if code == 0 and wl["dim"] == 2:
         name = f"k_classical_scatter<2,{p},{q}> (Algorithm 1, scalar FP64 + fused CSR scatter)"
     if code == 2 and not (p == 3 and q == 4):
-        name = f"k_gsf3<{p},{q}> (assembled sum factorization, scalar FP64 + CSR write)"
+        name = (f"k_gsf3<{p},{q}> (assembled sum factorization, scalar FP64 + CSR write)"
+                if os.environ.get("IGA_GSF_SCALAR") == "1" else
+                f"k_gsf3_mma<{p},{q}> (assembled sum factorization, DMMA GEMMs + CSR write)")
     elif code == 2:
         name = name.replace("k_gsf3", "k_gsf3_p3")
     roof.update({
