@@ -27,20 +27,34 @@ namespace mma {
 
 constexpr int NT = 512;
 __host__ __device__ constexpr int cdiv(int a, int b) { return (a + b - 1) / b; }
+// smallest pitch >= n with pitch == r (mod mod)
+__host__ __device__ constexpr int pitch_mod(int n, int mod, int r) { return n + ((r - n % mod) % mod + mod) % mod; }
+// Row order inside an 8-row DMMA m-tile so that the two rows (g = 2i, 2i+1) of each
+// 16-byte quarter-warp phase sit `d` rows apart: for a row stride s (double2 units),
+// d = 4 (s odd), 2 (s = 2, 6 mod 8), 1 (s = 4 mod 8) puts their 4 consecutive k-step
+// columns in disjoint halves of the 8 bank groups (no shared-memory bank conflicts).
+__host__ __device__ constexpr int qw_dist(int s) { return s % 2 ? 4 : (s % 4 == 2 ? 2 : 1); }
+__device__ __forceinline__ int qw_row(int g, int d) {
+  return d == 4 ? (g >> 1) + 4 * (g & 1) : (d == 2 ? (g & 4) + ((g >> 1) & 1) + 2 * (g & 1) : g);
+}
 
 template <int P, int Q, int TA, int TB>
 struct Shape {
   static constexpr int m = P + 1, NB = 2 * P + 1;
   static constexpr int LA = TA + P, LB = TB + P;
   static constexpr int KA = LA * Q, KB = LB * Q;  // contraction lengths of stages A, B
-  static constexpr int GC = KB * Q;               // stage-A columns (lb, k1, k2)
+  static constexpr int GC = KB * Q;               // stage-A columns (k2, lb, k1), k2 slowest
+  // conflict-free pitches: W rows (8-byte B fragments, 16-lane phases) == 4 mod 16
+  // doubles; PA / PB rows (16-byte A / B fragments, 8-lane phases) == 4 mod 8 double2
+  static constexpr int GCW = pitch_mod(GC, 16, 4);
+  static constexpr int KAP = pitch_mod(KA, 8, 4), KBP = pitch_mod(KB, 8, 4);
   static constexpr int NA0 = TA * NB, NB1 = TB * NB, NC = NA0 * NB1, NR = NA0 * Q;
   static constexpr int rowVals = NB * NB * NB;
-  static constexpr int nW = KA * GC, nY = 2 * NC * Q;
+  static constexpr int nW = KA * GCW, nY = 2 * NC * Q;
   // Y aliases W (W is dead after stage A); even, so the double2 arrays after it are aligned
   static constexpr int nWY = ((nW > nY ? nW : nY) + 1) / 2 * 2;
   static constexpr int nX = 2 * NA0 * GC;
-  static constexpr int nPA = 2 * NA0 * KA, nPB = 2 * NB1 * KB;
+  static constexpr int nPA = 2 * NA0 * KAP, nPB = 2 * NB1 * KBP;
   static constexpr int nZ = 2 * m * m * Q;
   static constexpr int nR = TA * TB * m * rowVals;
   static constexpr size_t bytes = sizeof(double) * ((size_t)nWY + nX + nPA + nPB + nZ + nR);
@@ -56,14 +70,15 @@ template <int P, int Q, int TA, int TB, bool STIFF>
 __global__ void __launch_bounds__(NT, P <= 2 ? 2 : 1) k_gsf3_mma(GsfArgs a) {
   using S = Shape<P, Q, TA, TB>;
   constexpr int m = S::m, NB = S::NB, KA = S::KA, KB = S::KB, GC = S::GC;
+  constexpr int GCW = S::GCW, KAP = S::KAP, KBP = S::KBP;
   constexpr int NA0 = S::NA0, NB1 = S::NB1, NC = S::NC, NR = S::NR;
   extern __shared__ double smem[];
-  double* sW = smem;                                         // [KA][GC]
+  double* sW = smem;                                         // [KA][GCW]
   double2* Y2 = reinterpret_cast<double2*>(smem);            // [NC][Q] (aliases W)
-  double2* X2 = reinterpret_cast<double2*>(smem + S::nWY);   // [NA0][GC] (XV, XD)
-  double2* PA2 = X2 + NA0 * GC;                              // [NA0][KA] (VV, DD)
-  double2* PB2 = PA2 + NA0 * KA;                             // [NB1][KB] (VV, DD)
-  double2* Z2 = PB2 + NB1 * KB;                              // [Q][m*m] (VV, DD(+VV))
+  double2* X2 = reinterpret_cast<double2*>(smem + S::nWY);   // [NA0][Q][KB] (XV, XD)
+  double2* PA2 = X2 + NA0 * GC;                              // [NA0][KAP] (VV, DD)
+  double2* PB2 = PA2 + NA0 * KAP;                            // [NB1][KBP] (VV, DD)
+  double2* Z2 = PB2 + NB1 * KBP;                             // [Q][m*m] (VV, DD(+VV))
   double* R = reinterpret_cast<double*>(Z2 + m * m * Q);     // [TA*TB][m][rowVals]
   __shared__ int64_t rowoff[TA * TB];
   __shared__ int comboR[NC];  // R offset of combo (a0, b1): pencil block + (d0, d1) row
@@ -91,7 +106,7 @@ __global__ void __launch_bounds__(NT, P <= 2 ? 2 : 1) k_gsf3_mma(GsfArgs a) {
       v.x = V[((int64_t)e0 * m + r) * Q + k0] * V[((int64_t)e0 * m + sc) * Q + k0];
       if (STIFF) v.y = D[((int64_t)e0 * m + r) * Q + k0] * D[((int64_t)e0 * m + sc) * Q + k0];
     }
-    PA2[u] = v;
+    PA2[a0 * KAP + kk] = v;
   }
   for (int u = tid; u < NB1 * KB; u += NT) {
     const int b1 = u / KB, kk = u % KB, lb = kk / Q, k1 = kk % Q;
@@ -102,7 +117,7 @@ __global__ void __launch_bounds__(NT, P <= 2 ? 2 : 1) k_gsf3_mma(GsfArgs a) {
       v.x = V[((int64_t)e1 * m + r) * Q + k1] * V[((int64_t)e1 * m + sc) * Q + k1];
       if (STIFF) v.y = D[((int64_t)e1 * m + r) * Q + k1] * D[((int64_t)e1 * m + sc) * Q + k1];
     }
-    PB2[u] = v;
+    PB2[b1 * KBP + kk] = v;
   }
   for (int u = tid; u < S::nR; u += NT) R[u] = 0.0;
   for (int c = tid; c < NC; c += NT) {
@@ -206,9 +221,9 @@ __global__ void __launch_bounds__(NT, P <= 2 ? 2 : 1) k_gsf3_mma(GsfArgs a) {
       if (u < NUW) {
         const int kk = u / KB, c1 = u - kk * KB;
         const double w01 = wqs[kk % Q] * wqs[c1 % Q];
-        double* dst = sW + kk * GC + c1 * Q;
+        double* dst = sW + kk * GCW + c1;  // column (k2, c1): k2 slowest
 #pragma unroll
-        for (int k2 = 0; k2 < Q; ++k2) dst[k2] = w01 * wqs[k2] * a.jac * cv[i][k2];
+        for (int k2 = 0; k2 < Q; ++k2) dst[k2 * KB] = w01 * wqs[k2] * a.jac * cv[i][k2];
       }
     }
     load_coef(e2 + 1, cv);
@@ -235,7 +250,7 @@ __global__ void __launch_bounds__(NT, P <= 2 ? 2 : 1) k_gsf3_mma(GsfArgs a) {
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks) {
           const int kk = ks * 4 + t;
-          pa[ks] = (row < NA0 && kk < KA) ? PA2[row * KA + kk] : make_double2(0.0, 0.0);
+          pa[ks] = (row < NA0 && kk < KA) ? PA2[row * KAP + kk] : make_double2(0.0, 0.0);
         }
         for (int ntl = grp; ntl < NTL; ntl += GRP) {
           const int col = ntl * 8 + g;
@@ -243,7 +258,7 @@ __global__ void __launch_bounds__(NT, P <= 2 ? 2 : 1) k_gsf3_mma(GsfArgs a) {
 #pragma unroll
           for (int ks = 0; ks < KS; ++ks) {
             const int kk = ks * 4 + t;
-            const double w = (kk < KA && col < GC) ? sW[kk * GC + col] : 0.0;
+            const double w = (kk < KA && col < GC) ? sW[kk * GCW + col] : 0.0;
             dmma(cv0, cv1, pa[ks].x, w);
             if (STIFF) dmma(cd0, cd1, pa[ks].y, w);
           }
@@ -263,19 +278,20 @@ __global__ void __launch_bounds__(NT, P <= 2 ? 2 : 1) k_gsf3_mma(GsfArgs a) {
       constexpr int MT = cdiv(NR, 8), NTL = cdiv(NB1, 8), KS = cdiv(KB, 4), GRP = NWARP / NTL;
       if (warp < NTL * GRP) {
         const int ntl = warp % NTL, grp = warp / NTL, b1 = ntl * 8 + g;
+        constexpr int DQ = qw_dist(KB);  // X rows (a0, k2) are KB double2 apart
         double2 pb[KS];
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks) {
           const int kk = ks * 4 + t;
-          pb[ks] = (b1 < NB1 && kk < KB) ? PB2[b1 * KB + kk] : make_double2(0.0, 0.0);
+          pb[ks] = (b1 < NB1 && kk < KB) ? PB2[b1 * KBP + kk] : make_double2(0.0, 0.0);
         }
         for (int mt = grp; mt < MT; mt += GRP) {
-          const int row = mt * 8 + g, a0 = row / Q, k2 = row % Q;
+          const int row = mt * 8 + qw_row(g, DQ), a0 = row / Q, k2 = row % Q;
           double ya0 = 0.0, ya1 = 0.0, yb0 = 0.0, yb1 = 0.0;
 #pragma unroll
           for (int ks = 0; ks < KS; ++ks) {
             const int kk = ks * 4 + t;
-            const double2 x = (row < NR && kk < KB) ? X2[a0 * GC + kk * Q + k2] : make_double2(0.0, 0.0);
+            const double2 x = (row < NR && kk < KB) ? X2[row * KB + kk] : make_double2(0.0, 0.0);
             if (STIFF) {
               dmma(ya0, ya1, x.x, pb[ks].y);
               dmma(ya0, ya1, x.y, pb[ks].x);
@@ -317,7 +333,7 @@ __global__ void __launch_bounds__(NT, P <= 2 ? 2 : 1) k_gsf3_mma(GsfArgs a) {
           dst[j] = nn < MM ? slot * S::rowVals + sc - r + P : -1;
         }
         for (int mt = grp; mt < MT; mt += GRP) {
-          const int combo = mt * 8 + g;
+          const int combo = mt * 8 + qw_row(g, qw_dist(Q));  // Y rows are Q double2 apart
           double c0v = 0.0, c1v = 0.0;
 #pragma unroll
           for (int ks = 0; ks < KS; ++ks) {
@@ -326,7 +342,7 @@ __global__ void __launch_bounds__(NT, P <= 2 ? 2 : 1) k_gsf3_mma(GsfArgs a) {
             dmma(c0v, c1v, y.x, z[ks].x);
             if (STIFF) dmma(c0v, c1v, y.y, z[ks].y);
           }
-          const int cc = mt * 8 + g;
+          const int cc = combo;  // C row = A row of this lane
           if (cc < NC) {
             double* Rc = R + comboR[cc];
             if (dst[0] >= 0) Rc[dst[0]] += c0v;
