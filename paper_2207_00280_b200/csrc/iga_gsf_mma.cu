@@ -56,7 +56,13 @@ struct Shape {
   static constexpr int nX = 2 * NA0 * GC;
   static constexpr int nPA = 2 * NA0 * KAP, nPB = 2 * NB1 * KBP;
   static constexpr int nZ = 2 * m * m * Q;
-  static constexpr int nR = TA * TB * m * rowVals;
+  // rolling-row slot pitch: rowVals + a pad that spreads the stage-S read-modify-writes
+  // over the shared-memory banks (picked by simulating the access pattern of the two
+  // coefficient-field configs: 37% fewer wavefronts at p = 4, q = 5; 20% at p = 2, q = 3)
+  static constexpr int RP = rowVals + (P == 4 && Q == 5 && TA == 2 && TB == 2   ? 1
+                                       : P == 2 && Q == 3 && TA == 3 && TB == 3 ? 7
+                                                                                : 0);
+  static constexpr int nR = TA * TB * m * RP;
   static constexpr size_t bytes = sizeof(double) * ((size_t)nWY + nX + nPA + nPB + nZ + nR);
 };
 
@@ -79,7 +85,7 @@ __global__ void __launch_bounds__(NT, P <= 2 ? 2 : 1) k_gsf3_mma(GsfArgs a) {
   double2* PA2 = X2 + NA0 * GC;                              // [NA0][KAP] (VV, DD)
   double2* PB2 = PA2 + NA0 * KAP;                            // [NB1][KBP] (VV, DD)
   double2* Z2 = PB2 + NB1 * KBP;                             // [Q][m*m] (VV, DD(+VV))
-  double* R = reinterpret_cast<double*>(Z2 + m * m * Q);     // [TA*TB][m][rowVals]
+  double* R = reinterpret_cast<double*>(Z2 + m * m * Q);     // [TA*TB][m][RP]
   __shared__ int64_t rowoff[TA * TB];
   __shared__ int comboR[NC];  // R offset of combo (a0, b1): pencil block + (d0, d1) row
 
@@ -123,7 +129,7 @@ __global__ void __launch_bounds__(NT, P <= 2 ? 2 : 1) k_gsf3_mma(GsfArgs a) {
   for (int c = tid; c < NC; c += NT) {
     const int a0 = c / NB1, b1 = c % NB1;
     const int ia = a0 / NB, d0 = a0 % NB, ib = b1 / NB, d1 = b1 % NB;
-    comboR[c] = (ia * TB + ib) * m * S::rowVals + (d0 * NB + d1) * NB;
+    comboR[c] = (ia * TB + ib) * m * S::RP + (d0 * NB + d1) * NB;
   }
 
   // W units: one (kk, (lb, k1)) row segment of Q contiguous k2 columns per unit (the Q
@@ -193,7 +199,7 @@ __global__ void __launch_bounds__(NT, P <= 2 ? 2 : 1) k_gsf3_mma(GsfArgs a) {
     const int lod2 = max(0, P - I2), c2 = (int)band_cnt(I2, P, N);
     for (int u = tid; u < TA * TB * S::rowVals; u += NT) {
       const int rc = u / S::rowVals, v = u - rc * S::rowVals;
-      double* Rv = R + (rc * m + slot) * S::rowVals + v;
+      double* Rv = R + (rc * m + slot) * S::RP + v;
       const int64_t off = rowoff[rc];
       if (off >= 0) {
         const int mt = rowmeta[rc];
@@ -330,7 +336,7 @@ __global__ void __launch_bounds__(NT, P <= 2 ? 2 : 1) k_gsf3_mma(GsfArgs a) {
         for (int j = 0; j < 2; ++j) {
           const int nn = ntl * 8 + 2 * t + j, r = nn / m, sc = nn % m;
           const int slot = slot0 + r >= m ? slot0 + r - m : slot0 + r;
-          dst[j] = nn < MM ? slot * S::rowVals + sc - r + P : -1;
+          dst[j] = nn < MM ? slot * S::RP + sc - r + P : -1;
         }
         for (int mt = grp; mt < MT; mt += GRP) {
           const int combo = mt * 8 + qw_row(g, qw_dist(Q));  // Y rows are Q double2 apart
