@@ -93,12 +93,12 @@ def _weights_uniform(rule: QuadratureRule) -> np.ndarray:
 
 
 def _device_element(alpha, kv, rule, method_code, operator, coefficient):
+    q = _check_inputs(alpha, kv, rule)  # ValueError before any device work, as the reference
+    w = _weights_uniform(rule)
     torch = _lib.require_cuda()
     from .device import MeshProblem
 
-    q = _check_inputs(alpha, kv, rule)
     prob = MeshProblem(3, kv.elements, kv.degree, q, operator=operator)
-    w = _weights_uniform(rule)
     prob.weights = torch.from_numpy(w).to(prob.device)
     prob.jac = float(rule.jacobian)
     if coefficient is not None:

@@ -1,0 +1,187 @@
+"""The reference's own per-element test cases (igabench tests/test_integrators.py),
+restated against the drop-in API: the same inputs and assertions, with the element
+matrices computed by the CUDA path (``iga_element_matrices``) instead of numba.
+
+Kernel-free cases (the operation-count model, argument validation) run on CPU;
+the rest are ``gpu``-marked.  Cited lines are in
+/root/reference/pkg/tests/test_integrators.py."""
+
+import numpy as np
+import pytest
+
+import paper_2207_00280_b200 as P
+
+
+def _two_methods(K, p, alpha):
+    """Classical and sum-factorization element matrices of one element
+    (the reference's helper, test_integrators.py:16-21)."""
+    kv = P.make_knot_vector(K, p)
+    rule = P.gauss_rule(p, K, alpha)
+    a = P.integrate_element_classical(alpha, kv, rule)
+    b = P.integrate_element_sumfact(alpha, kv, rule, P.SumFactBuffers.allocate(p))
+    return a, b
+
+
+# ----------------------------------------------------------------- CPU: counts, validation
+def test_classical_count_example_p0():
+    """test_integrators.py:234-235: one pair, one point."""
+    assert P.flop_count("classical", 0) == 10
+
+
+def test_classical_count_ratio_tends_to_ninth_power():
+    """test_integrators.py:238-241: the classical count grows like (p+1)^9."""
+    for p in (6, 8, 10):
+        ratio = P.flop_count("classical", p) / P.flop_count("classical", p - 1)
+        assert ratio == pytest.approx(((p + 1) / p) ** 9, rel=2e-3)
+
+
+def test_sumfact_cheaper_and_ratio_at_p9():
+    """test_integrators.py:244-247."""
+    for p in range(1, 10):
+        assert P.flop_count("sumfact", p) < P.flop_count("classical", p)
+    assert P.flop_count("classical", 9) / P.flop_count("sumfact", 9) >= 10
+
+
+def test_unknown_method_rejected():
+    """test_integrators.py:255-257."""
+    with pytest.raises(ValueError):
+        P.flop_count("magic", 2)
+
+
+def test_buffer_shape_mismatch_rejected():
+    """test_integrators.py:135-139: buffers for another degree -> ValueError, before
+    any device work."""
+    kv = P.make_knot_vector(2, 2)
+    rule = P.gauss_rule(2, 2, (0, 0, 0))
+    with pytest.raises(ValueError):
+        P.integrate_element_sumfact((0, 0, 0), kv, rule, P.SumFactBuffers.allocate(1))
+
+
+def test_inconsistent_inputs_rejected():
+    """test_integrators.py:142-146: nodes of another element -> ValueError."""
+    kv = P.make_knot_vector(2, 2)
+    rule = P.gauss_rule(2, 2, (1, 1, 1))
+    with pytest.raises(ValueError):
+        P.integrate_element_classical((0, 0, 0), kv, rule)
+
+
+# ----------------------------------------------------------------- GPU: element matrices
+@pytest.mark.gpu
+def test_p0_unit_cube_volume():
+    """test_integrators.py:24-28."""
+    a, b = _two_methods(1, 0, (0, 0, 0))
+    assert a.entries.shape == (1, 1)
+    assert a.entries[0, 0] == pytest.approx(1.0, abs=1e-14)
+    assert b.entries[0, 0] == pytest.approx(1.0, abs=1e-14)
+
+
+@pytest.mark.gpu
+def test_k1_p1_analytic_mass_matrix():
+    """test_integrators.py:31-38: the element matrix is the Kronecker cube of the 1D
+    hat-function mass matrix [[1/3, 1/6], [1/6, 1/3]]."""
+    a, _ = _two_methods(1, 1, (0, 0, 0))
+    m1 = np.array([[1 / 3, 1 / 6], [1 / 6, 1 / 3]])
+    assert np.abs(a.entries - np.kron(np.kron(m1, m1), m1)).max() < 1e-12
+    assert a.entries[0, 0] == pytest.approx(1 / 27, abs=1e-12)
+    assert a.entries[0, 7] == pytest.approx((1 / 6) ** 3, abs=1e-12)
+
+
+@pytest.mark.gpu
+def test_k2_p1_corner_diagonal():
+    """test_integrators.py:41-44: each supported 1D hat has mass h/3 = 1/6 at h = 1/2."""
+    a, _ = _two_methods(2, 1, (0, 0, 0))
+    assert a.entries[0, 0] == pytest.approx((1 / 6) ** 3, abs=1e-12)
+
+
+@pytest.mark.gpu
+def test_sumfact_equals_classical_entrywise():
+    """test_integrators.py:47-50."""
+    a, b = _two_methods(1, 1, (0, 0, 0))
+    assert np.abs(a.entries - b.entries).max() < 1e-12
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("p", [0, 1, 2, 3])
+@pytest.mark.parametrize("K", [1, 2])
+def test_oracle_equivalence_small_grid(p, K):
+    """test_integrators.py:53-61: both methods on every element of small meshes."""
+    kv = P.make_knot_vector(K, p)
+    buffers = P.SumFactBuffers.allocate(p)
+    for alpha in P.element_list(K):
+        rule = P.gauss_rule(p, K, alpha)
+        a = P.integrate_element_classical(alpha, kv, rule).entries
+        b = P.integrate_element_sumfact(alpha, kv, rule, buffers).entries
+        assert np.linalg.norm(a - b) / np.linalg.norm(a) <= 1e-10
+
+
+@pytest.mark.gpu
+def test_fine_quadrature_oracle():
+    """test_integrators.py:64-91: the integrand checked by a richer Gauss rule (q = p+3)
+    evaluated here with numpy and the spline API, independent of the kernels."""
+    K, p, alpha = 2, 2, (1, 0, 1)
+    kv = P.make_knot_vector(K, p)
+    q = p + 3
+    xr, wr = np.polynomial.legendre.leggauss(q)
+    h = 1.0 / K
+    tabs = []
+    for d in range(3):
+        xs = alpha[d] * h + (xr + 1.0) * h / 2.0
+        tabs.append(np.array([P.eval_nonzero_basis(kv, alpha[d], x).values for x in xs]).T)
+    m = p + 1
+    per_axis = [np.einsum("k,ik,jk->ij", wr, t, t) for t in tabs]  # 1D element matrices
+    expected = np.einsum("ad,be,cf->abcdef", *per_axis).reshape(m**3, m**3) * (h / 2.0) ** 3
+    a = P.integrate_element_classical(alpha, kv, P.gauss_rule(p, K, alpha)).entries
+    assert np.abs(a - expected).max() < 1e-13
+
+
+@pytest.mark.gpu
+def test_exact_symmetry():
+    """test_integrators.py:94-98: both triangles written from one value (bitwise)."""
+    for K, p in [(2, 1), (2, 2), (3, 3)]:
+        a, b = _two_methods(K, p, (K - 1, 0, 1 % K))
+        assert np.array_equal(a.entries, a.entries.T)
+        assert np.array_equal(b.entries, b.entries.T)
+
+
+@pytest.mark.gpu
+def test_positive_diagonal():
+    """test_integrators.py:101-104."""
+    a, b = _two_methods(3, 2, (1, 2, 0))
+    assert np.all(np.diag(a.entries) > 0)
+    assert np.all(np.diag(b.entries) > 0)
+
+
+@pytest.mark.gpu
+def test_element_matrices_translated_in_the_interior():
+    """test_integrators.py:107-121: interior elements share one matrix, the corner
+    element (boundary knots, p >= 2) differs."""
+    K, p = 6, 2
+    kv = P.make_knot_vector(K, p)
+    buffers = P.SumFactBuffers.allocate(p)
+    mats = [P.integrate_element_sumfact((e, e, e), kv, P.gauss_rule(p, K, (e, e, e)), buffers).entries
+            for e in range(p, K - p)]
+    for mt in mats[1:]:
+        assert np.abs(mt - mats[0]).max() < 1e-15
+    corner = P.integrate_element_sumfact((0, 0, 0), kv, P.gauss_rule(p, K, (0, 0, 0)),
+                                         buffers).entries
+    assert np.abs(corner - mats[0]).max() > 1e-6
+
+
+@pytest.mark.gpu
+def test_all_elements_equal_for_p1():
+    """test_integrators.py:124-132: p = 1 has no boundary effect."""
+    K, p = 3, 1
+    kv = P.make_knot_vector(K, p)
+    ref = None
+    for alpha in P.element_list(K):
+        mt = P.integrate_element_classical(alpha, kv, P.gauss_rule(p, K, alpha)).entries
+        ref = mt if ref is None else ref
+        assert np.abs(mt - ref).max() < 1e-15
+
+
+@pytest.mark.gpu
+def test_sumfact_flops_beat_classical_on_real_element():
+    """test_integrators.py:250-252: the ElementMatrix carries the reference's op model."""
+    a, b = _two_methods(2, 3, (1, 0, 1))
+    assert b.flops < a.flops
+    assert a.flops == P.flop_count("classical", 3) and b.flops == P.flop_count("sumfact", 3)
