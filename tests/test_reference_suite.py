@@ -185,3 +185,141 @@ def test_sumfact_flops_beat_classical_on_real_element():
     a, b = _two_methods(2, 3, (1, 0, 1))
     assert b.flops < a.flops
     assert a.flops == P.flop_count("classical", 3) and b.flops == P.flop_count("sumfact", 3)
+
+
+# ----------------------------------------------------------------- mesh (tests/test_mesh.py)
+def test_element_list_and_support():
+    """test_mesh.py:7-40: lexicographic element ids, support sets."""
+    assert P.element_list(1) == [(0, 0, 0)]
+    ids = P.element_list(2)
+    assert len(ids) == 8 and ids[0] == (0, 0, 0) and ids[-1] == (1, 1, 1) and ids == sorted(ids)
+    assert len(P.element_list(20)) == 8000
+    with pytest.raises(ValueError):
+        P.element_list(0)
+    assert set(P.support_set((0, 0, 0), 1)) == {(a, b, c) for a in (0, 1) for b in (0, 1)
+                                                for c in (0, 1)}
+    assert P.support_set((0, 0, 0), 0) == [(0, 0, 0)]
+    s = P.support_set((1, 1, 1), 2)
+    assert len(s) == 27 and set(s) == {(a, b, c) for a in (1, 2, 3) for b in (1, 2, 3)
+                                       for c in (1, 2, 3)}
+
+
+def test_local_index():
+    """test_mesh.py:43-58."""
+    assert P.local_index((0, 0, 0), (0, 0, 0), 1) == 0
+    assert P.local_index((0, 0, 0), (1, 1, 1), 1) == 7
+    assert P.local_index((2, 3, 4), (3, 4, 5), 2) == 13
+    for p in (0, 1, 2, 3):
+        hits = [P.local_index((1, 0, 2), b, p) for b in P.support_set((1, 0, 2), p)]
+        assert sorted(hits) == list(range((p + 1) ** 3))
+    with pytest.raises(ValueError):
+        P.local_index((0, 0, 0), (2, 0, 0), 1)
+
+
+def test_gauss_rules():
+    """test_mesh.py:61-109: midpoint rule, the 2-point nodes against a Newton solve of
+    P2, unit integral, polynomial exactness, constant Jacobian."""
+    r = P.gauss_rule(0, 2, (1, 0, 1))
+    assert r.points_per_direction == (1, 1, 1)
+    assert r.nodes[0][0] == pytest.approx(0.75) and r.nodes[1][0] == pytest.approx(0.25)
+    for d in range(3):
+        assert r.weights[d].sum() * (1 / (2 * 2)) == pytest.approx(0.5)
+    x = 0.5
+    for _ in range(60):
+        x -= (1.5 * x * x - 0.5) / (3.0 * x)
+    r = P.gauss_rule(1, 1, (0, 0, 0))
+    assert np.allclose(np.sort((r.nodes[0] - 0.5) * 2.0), [-x, x], atol=1e-14)
+    assert np.allclose(r.weights[0], [1.0, 1.0])
+    for p, K in [(0, 1), (1, 2), (2, 3), (4, 2)]:
+        for alpha in [(0, 0, 0), (K - 1, K - 1, K - 1)]:
+            r = P.gauss_rule(p, K, alpha)
+            tot = r.weights[0].sum() * r.weights[1].sum() * r.weights[2].sum() * r.jacobian
+            assert tot == pytest.approx((1 / K) ** 3, rel=1e-13)
+    for p, K in [(0, 2), (1, 2), (3, 4), (5, 3)]:
+        alpha = (1, 0, K - 1)
+        r = P.gauss_rule(p, K, alpha)
+        for deg in range(2 * p + 2):
+            for ax in range(3):
+                lo, hi = alpha[ax] / K, (alpha[ax] + 1) / K
+                exact = (hi ** (deg + 1) - lo ** (deg + 1)) / (deg + 1)
+                assert (r.weights[ax] * r.nodes[ax] ** deg).sum() / (2 * K) == pytest.approx(
+                    exact, abs=1e-12)
+    assert {P.gauss_rule(2, 4, a).jacobian for a in P.element_list(4)} == {(1 / 8) ** 3}
+
+
+# ----------------------------------------------------------------- splines (tests/test_splines.py)
+def test_knot_vectors():
+    """test_splines.py:14-43."""
+    assert np.array_equal(P.make_knot_vector(1, 0).knots, [0.0, 1.0])
+    assert np.allclose(P.make_knot_vector(2, 1).knots, [0, 0, 0.5, 1, 1])
+    assert np.allclose(P.make_knot_vector(2, 2).knots, [0, 0, 0, 0.5, 1, 1, 1])
+    for K, p in [(1, 0), (2, 1), (4, 3), (8, 5)]:
+        kv = P.make_knot_vector(K, p)
+        t = kv.knots
+        assert len(t) == K + 2 * p + 1 and kv.n_basis == K + p and np.all(np.diff(t) >= 0)
+        assert np.all(t[: p + 1] == 0.0) and np.all(t[-(p + 1):] == 1.0)
+    with pytest.raises(ValueError):
+        P.make_knot_vector(0, 1)
+    with pytest.raises(ValueError):
+        P.make_knot_vector(2, -1)
+
+
+def test_find_element_and_point_checks():
+    """test_splines.py:97-100, :119-122, :187-193 (host-side checks, no launch)."""
+    kv = P.make_knot_vector(4, 2)
+    assert P.find_element(kv, 0.0) == 0 and P.find_element(kv, 0.26) == 1
+    assert P.find_element(kv, 1.0) == 3
+    with pytest.raises(ValueError):
+        P.find_element(kv, 1.5)
+    with pytest.raises(ValueError):
+        P.eval_nonzero_basis(kv, 0, 0.9)
+    with pytest.raises(ValueError):
+        P.eval_nonzero_basis_derivatives(P.make_knot_vector(2, 0), 0, 0.25)
+
+
+@pytest.mark.gpu
+def test_nonzero_basis_values_on_device():
+    """test_splines.py:77-94, :138-167 through the device evaluator (K1'): linear hats,
+    interpolation at both ends, partition of unity and nonnegativity on a grid."""
+    kv = P.make_knot_vector(2, 1)
+    assert np.allclose(P.eval_nonzero_basis(kv, 0, 0.25).values, [0.5, 0.5])
+    assert np.allclose(P.eval_nonzero_basis(kv, 0, 0.0).values, [1.0, 0.0])
+    for K, p in [(1, 0), (2, 1), (4, 3)]:
+        kv = P.make_knot_vector(K, p)
+        at0 = P.eval_nonzero_basis(kv, 0, 0.0).values
+        at1 = P.eval_nonzero_basis(kv, K - 1, 1.0).values
+        assert at0[0] == pytest.approx(1.0) and (p == 0 or at0[1:].max() == 0.0)
+        assert at1[-1] == pytest.approx(1.0) and (p == 0 or at1[:-1].max() == 0.0)
+    grid = np.linspace(0.0, 1.0, 21)
+    for p in range(6):
+        for K in (1, 3, 8):
+            kv = P.make_knot_vector(K, p)
+            for x in grid:
+                v = P.eval_nonzero_basis(kv, P.find_element(kv, x), x).values
+                assert v.min() >= 0.0 and abs(v.sum() - 1.0) < 1e-12
+
+
+@pytest.mark.gpu
+def test_nonzero_basis_derivatives_on_device():
+    """test_splines.py:103-135, :170-184: hat slopes, zero sum, central differences."""
+    kv = P.make_knot_vector(2, 1)
+    for x in (0.1, 0.25, 0.4):
+        assert np.allclose(P.eval_nonzero_basis_derivatives(kv, 0, x), [-2.0, 2.0])
+    rng = np.random.default_rng(7)
+    for K, p in [(2, 1), (3, 2), (5, 4)]:
+        kv = P.make_knot_vector(K, p)
+        for _ in range(5):
+            e = int(rng.integers(K))
+            x = (e + rng.random()) / K
+            assert abs(P.eval_nonzero_basis_derivatives(kv, e, x).sum()) < 1e-10
+    h = 1e-6
+    rng = np.random.default_rng(11)
+    for K, p in [(2, 1), (4, 2), (5, 3)]:
+        kv = P.make_knot_vector(K, p)
+        for _ in range(10):
+            e = int(rng.integers(K))
+            x = (e + 0.2 + 0.6 * rng.random()) / K
+            ana = P.eval_nonzero_basis_derivatives(kv, e, x)
+            fd = (P.eval_nonzero_basis(kv, e, x + h).values
+                  - P.eval_nonzero_basis(kv, e, x - h).values) / (2 * h)
+            assert np.abs(ana - fd).max() / max(1.0, np.abs(ana).max()) < 1e-5
