@@ -281,7 +281,7 @@ def alt_leg(cfg, assembly, args, flush, stream, wl, total_el, peaks):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         flush.fill_(float(i))
         a.record(stream)
-        sess.prob.integrate_assemble(sess.values, sess.code, stream=stream)
+        sess.prob.integrate_assemble(sess.values, sess.code, stream=stream, band=sess.use_band)
         b.record(stream)
         kev.append((a, b))
     torch.cuda.synchronize()
@@ -361,7 +361,7 @@ def main():
         sess = DeviceSession(cfg, use_graph=not args.no_graph)
         step = sess.step
         n_el = K ** wl["dim"]
-        launches = 2
+        launches = sess.launches_per_step
         kernel_values = sess.values
 
     # L2 flush buffer (2x the 126 MB L2), written between timed steps outside the step events
@@ -407,9 +407,11 @@ def main():
         if world > 1:
             el = plan.recompute_elements if args.halo == "recompute" else (plan.el_lo, plan.el_hi)
             sess.prob.integrate_assemble(sess.values, sess.code, el_range=el,
-                                         plane_range=(plan.own_lo, plan.own_hi), stream=stream)
+                                         plane_range=(plan.own_lo, plan.own_hi), stream=stream,
+                                         band=sess.use_band)
         else:
-            sess.prob.integrate_assemble(sess.values, sess.code, stream=stream)
+            sess.prob.integrate_assemble(sess.values, sess.code, stream=stream,
+                                         band=sess.use_band)
         b.record(stream)
         kev.append((a, b))
     torch.cuda.synchronize()

@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define IGA_ABI_VERSION 1
+#define IGA_ABI_VERSION 2
 
 #define IGA_OK 0
 #define IGA_EINVAL 1       /* invalid argument -> ValueError            */
@@ -61,6 +61,10 @@ typedef struct iga_problem {
   const double* weights; /* device [q] reference Gauss weights (leggauss, mesh.py:82) */
   const double* tables_v; /* device [K][p+1][q] basis values from iga_mesh_tables */
   const double* tables_d; /* device [K][p+1][q] basis derivatives (NULL for IGA_OP_MASS) */
+  const double* band;     /* device [K+p][2p+1][2] assembled 1D band matrices from
+                             iga_band_tables, or NULL.  Used by the separable method only:
+                             with it the integration kernel reads the 1D integrals instead of
+                             forming them in every CTA (a shorter prologue). */
 } iga_problem;
 
 const char* iga_last_error(void);
@@ -78,6 +82,16 @@ int32_t iga_mesh_tables(int32_t K, int32_t p, int32_t q, const double* ref_nodes
  * (splines.eval_nonzero_basis / eval_nonzero_basis_derivatives, splines.py:127-161). */
 int32_t iga_basis_eval(int32_t K, int32_t p, int64_t n, const int32_t* elem, const double* x,
                        double* vals, double* ders, void* stream);
+
+/* K1 + the assembled 1D band matrices of the separable method in one launch:
+ * vals/ders [K][p+1][q] as iga_mesh_tables (either may be NULL: not stored), and
+ * band[I][d] = (m, k), I < K+p, d = J-I+p in [0, 2p]:
+ *   m(I,J) = sum_e sum_k w_k V_e(I-e,k) V_e(J-e,k)   (k(I,J): the same with derivatives)
+ * over all elements, elements ascending -- the 1D factors of the Kronecker form of the
+ * reference's element quadrature summed by assemble (integrators.py:77-151,
+ * assembly.py:80-82).  Uses prob->K, p, q, op, weights. */
+int32_t iga_band_tables(const iga_problem* prob, const double* ref_nodes, double* vals,
+                        double* ders, double* band, void* stream);
 
 /* Host arithmetic: number of CSR entries in global rows [row_begin, row_end). */
 int64_t iga_csr_nnz(int32_t dim, int32_t K, int32_t p, int64_t row_begin, int64_t row_end);

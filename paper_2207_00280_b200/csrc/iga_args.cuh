@@ -56,6 +56,7 @@ struct KronArgs {
   const double* weights;         // [Q]
   const double* V;               // [K][P+1][Q]
   const double* D;               // [K][P+1][Q] (null for mass)
+  const double2* band;           // [N][2P+1] (m, k) from iga_band_tables, or null
   double* values;
 };
 

@@ -37,6 +37,32 @@ __device__ __forceinline__ double2 band1d(const double* V, const double* D, int 
 }
 
 
+// band1d summed as build_band_tables' shared-memory path does (each element's integral
+// over its points first, then the elements ascending), so it reproduces those bits
+template <int P, int Q>
+__device__ __forceinline__ double2 band1d_el(const double* V, const double* D, int K, const double* w,
+                                             int I, int d, int e_lo, int e_hi, bool stiff) {
+  constexpr int M = P + 1;
+  const int J = I + d - P;
+  double m = 0.0, k = 0.0;
+  const int lo = max(max(I, J) - P, max(e_lo, 0)), hi = min(min(I, J) + 1, min(e_hi, K));
+  for (int e = lo; e < hi; ++e) {
+    const double* Ve = V + e * M * Q;
+    const int i = I - e, j = J - e;
+    double me = 0.0, ke = 0.0;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) me += (w[q] * Ve[i * Q + q]) * Ve[j * Q + q];
+    if (stiff) {
+      const double* De = D + e * M * Q;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) ke += (w[q] * De[i * Q + q]) * De[j * Q + q];
+    }
+    m += me;
+    k += ke;
+  }
+  return make_double2(m, k);
+}
+
 // Fill tb[0][N][NB] (all elements) and, if with_slab, tb[1][N][NB] (elements in
 // [slab_lo, slab_hi)) in shared memory, (m, k) per entry.  When the basis tables and
 // the element integrals fit in `scratch` (small K, where this prologue is not

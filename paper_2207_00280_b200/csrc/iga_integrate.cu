@@ -1,5 +1,7 @@
 // C-ABI entry points of the mesh-wide path: fused integrate+assemble,
 // assembly from element matrices, and SpMV over the structured CSR.
+#include <cstdlib>
+
 #include "iga_dispatch.cuh"
 
 #include "iga_args.cuh"
@@ -9,6 +11,8 @@ namespace iga {
 int launch_scatter(const ScatterArgs& a, int method, int p, int q, cudaStream_t s);
 int launch_gsf(const GsfArgs& a, int p, int q, cudaStream_t s);
 int launch_kron(const KronArgs& a, int p, int q, cudaStream_t s);
+int launch_band_tables(int K, int p, int q, const double* ref, const double* weights, int stiff,
+                       double* V, double* D, double* band, cudaStream_t s);
 
 // assembly.assemble from element matrices: one warp per CSR row, lanes over
 // its columns; every value sums its element contributions in lexicographic
@@ -197,6 +201,15 @@ using namespace iga;
 
 extern "C" {
 
+int32_t iga_band_tables(const iga_problem* prob, const double* ref_nodes, double* vals,
+                        double* ders, double* band, void* stream) {
+  int rc = validate_problem(prob);
+  if (rc) return rc;
+  if (!ref_nodes || !band) return fail_einval("null ref_nodes/band");
+  return launch_band_tables(prob->K, prob->p, prob->q, ref_nodes, prob->weights,
+                            prob->op != IGA_OP_MASS, vals, ders, band, as_stream(stream));
+}
+
 int32_t iga_integrate_assemble(const iga_problem* prob, int32_t method, int32_t el_begin,
                                int32_t el_end, int32_t row_plane_begin, int32_t row_plane_end,
                                double* values, void* stream) {
@@ -227,6 +240,7 @@ int32_t iga_integrate_assemble(const iga_problem* prob, int32_t method, int32_t 
     a.plane_begin = row_plane_begin; a.plane_end = row_plane_end; a.base = base;
     a.jc = prob->jac * prob->coef_scalar; a.weights = prob->weights;
     a.V = prob->tables_v; a.D = prob->tables_d; a.values = values;
+    a.band = reinterpret_cast<const double2*>(prob->band);
     return launch_kron(a, p, prob->q, s);
   }
   if (method == IGA_METHOD_SUMFACT_ASSEMBLED) {

@@ -92,18 +92,36 @@ __global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) 
 #ifdef KRON_EMPTY
   if (a.K > 0) return;
 #endif
-  build_band_tables<P, Q>(a.V, a.D, a.weights, K, stiff, a.el_begin, a.el_end, !full, tb, stage,
-                          kron_nbuf() * SG, w, tid, NT);
+  // Work: chunks of G rows of a pencil, in CSR order; CTA b takes the contiguous
+  // range [b U / grid, (b+1) U / grid) of the U chunks (balanced to a chunk)
+  const int nch = (int)((N + G - 1) / G);
+  const int64_t nunit = (int64_t)(a.plane_end - a.plane_begin) * N * nch;
+  const int64_t u_lo = nunit * blockIdx.x / gridDim.x, u_hi = nunit * (blockIdx.x + 1) / gridDim.x;
+  if (a.band) {
+    // 1D band matrices precomputed once per step (iga_band_tables): a short copy instead
+    // of the quadrature in every CTA; the axis-0 rows of an element slab are integrated
+    // here for the CTA's planes only
+    for (int u = tid; u < N * NB; u += NT) tb[u] = __ldg(a.band + u);
+    if (!full) {
+      if (tid < Q) w[tid] = a.weights[tid];
+      __syncthreads();
+      const int i0lo = a.plane_begin + (int)(u_lo / nch / N);
+      const int i0hi = a.plane_begin + (int)((u_hi - 1) / nch / N);
+      for (int u = tid; u < (i0hi - i0lo + 1) * NB; u += NT) {
+        const int I0 = i0lo + u / NB, d = u % NB;
+        tb[N * NB + I0 * NB + d] = band1d_el<P, Q>(a.V, a.D, K, w, I0, d, a.el_begin, a.el_end, stiff);
+      }
+    }
+    __syncthreads();
+  } else {
+    build_band_tables<P, Q>(a.V, a.D, a.weights, K, stiff, a.el_begin, a.el_end, !full, tb, stage,
+                            kron_nbuf() * SG, w, tid, NT);
+  }
 
 #ifdef KRON_PROLOGUE_ONLY
   if (a.K > 0) return;
 #endif
-  // Work: chunks of G rows of a pencil, in CSR order; CTA b takes the contiguous
-  // range [b U / grid, (b+1) U / grid) of the U chunks (one wave, balanced to a chunk)
   int chunk = 0;  // chunks issued by this CTA (selects the staging buffer)
-  const int nch = (int)((N + G - 1) / G);
-  const int64_t nunit = (int64_t)(a.plane_end - a.plane_begin) * N * nch;
-  const int64_t u_lo = nunit * blockIdx.x / gridDim.x, u_hi = nunit * (blockIdx.x + 1) / gridDim.x;
   const int64_t T = band_prefix(N, P, N);  // values of a full-length band row set
   double* vals = nullptr;                   // first value of the current pencil
   // the chunk produced last, stored after the next barrier (thread 0)
@@ -227,6 +245,88 @@ __global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) 
     issue();
     asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
   }
+}
+
+// K1 + the band matrices, one CTA per RB band rows: each CTA evaluates the Cox-de Boor
+// tables of the elements its rows touch (its own and P halo elements, k_mesh_tables'
+// arithmetic; halo elements are evaluated twice with identical bits), their element
+// integrals, and the sums per band entry in build_band_tables' order -- so k_kron3
+// produces the same bits either way, and the launch is a few latency rounds on several
+// SMs instead of the quadrature prologue of every k_kron3 CTA.
+constexpr int kBandRows = 8;
+template <int P, int Q>
+__global__ void __launch_bounds__(128) k_mesh_band(int K, const double* __restrict__ ref,
+                                                   const double* __restrict__ weights, int stiff,
+                                                   double* __restrict__ V, double* __restrict__ D,
+                                                   double2* __restrict__ band) {
+  constexpr int M = P + 1, NB = 2 * P + 1, NEL = kBandRows + P;
+  __shared__ double Vs[NEL * M * Q], Ds[NEL * M * Q];
+  __shared__ double2 em[NEL * M * M];
+  __shared__ double w[Q];
+  const int N = K + P, tid = threadIdx.x, nt = blockDim.x;
+  const int i_lo = blockIdx.x * kBandRows, i_hi = min(N, i_lo + kBandRows);
+  const int e0 = max(0, i_lo - P), e1 = min(K, i_hi), ne = e1 - e0;
+  if (tid < Q) w[tid] = weights[tid];
+  for (int u = tid; u < ne * Q; u += nt) {
+    const int le = u / Q, k = u - le * Q, e = e0 + le;
+    double vals[M], ders[M];
+    cox_de_boor<P>(e, map_node(e, ref[k], K), K, vals, stiff ? ders : nullptr);
+#pragma unroll
+    for (int r = 0; r < M; ++r) {
+      const int o = (le * M + r) * Q + k, og = (e * M + r) * Q + k;
+      Vs[o] = vals[r];
+      if (V) V[og] = vals[r];
+      if (stiff) {
+        Ds[o] = ders[r];
+        if (D) D[og] = ders[r];
+      }
+    }
+  }
+  __syncthreads();
+  for (int u = tid; u < ne * M * M; u += nt) {
+    const int le = u / (M * M), r = (u / M) % M, c = u % M;
+    const double* vr = Vs + (le * M + r) * Q;
+    const double* vc = Vs + (le * M + c) * Q;
+    double m = 0.0, k = 0.0;
+#pragma unroll
+    for (int q = 0; q < Q; ++q) m += (w[q] * vr[q]) * vc[q];
+    if (stiff) {
+      const double* dr = Ds + (le * M + r) * Q;
+      const double* dc = Ds + (le * M + c) * Q;
+#pragma unroll
+      for (int q = 0; q < Q; ++q) k += (w[q] * dr[q]) * dc[q];
+    }
+    em[u] = make_double2(m, k);
+  }
+  __syncthreads();
+  for (int u = tid; u < (i_hi - i_lo) * NB; u += nt) {
+    const int I = i_lo + u / NB, J = I + u % NB - P;
+    const int lo = max(max(I, J) - P, 0), hi = min(min(I, J) + 1, K);
+    double m = 0.0, k = 0.0;
+    for (int e = lo; e < hi; ++e) {
+      const double2 x = em[((e - e0) * M + I - e) * M + J - e];
+      m += x.x;
+      k += x.y;
+    }
+    band[I * NB + u % NB] = make_double2(m, k);
+  }
+}
+
+template <int P, int Q>
+struct BandLaunch {
+  static int run(int K, const double* ref, const double* weights, int stiff, double* V, double* D,
+                 double2* band, cudaStream_t s) {
+    const int N = K + P;
+    k_mesh_band<P, Q><<<(N + kBandRows - 1) / kBandRows, 128, 0, s>>>(K, ref, weights, stiff, V,
+                                                                       D, band);
+    return check_cuda(cudaGetLastError(), "band launch");
+  }
+};
+
+int launch_band_tables(int K, int p, int q, const double* ref, const double* weights, int stiff,
+                       double* V, double* D, double* band, cudaStream_t s) {
+  return dispatch_pq<BandLaunch>(p, q, K, ref, weights, stiff, V, D,
+                                 reinterpret_cast<double2*>(band), s);
 }
 
 template <int P, int Q, int G>

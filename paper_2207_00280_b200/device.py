@@ -107,6 +107,7 @@ class MeshProblem:
         self.tables_d = torch.empty((K, m, q), dtype=torch.float64, device=self.device)
         self.coef = None
         self.coef_scalar = 1.0
+        self.band = None
         self.set_coefficient(coefficient)
         self.build_tables()
 
@@ -141,7 +142,9 @@ class MeshProblem:
                                      self.tables_v.data_ptr(), self.tables_d.data_ptr(),
                                      _lib.stream_ptr(stream or self.stream)))
 
-    def problem_struct(self) -> _lib.IgaProblem:
+    def problem_struct(self, band: bool = False) -> _lib.IgaProblem:
+        """iga_problem of this mesh; ``band`` passes the band tables of the last
+        ``build_band_tables`` (separable method)."""
         s = _lib.IgaProblem()
         s.dim, s.K, s.p, s.q = self.dim, self.K, self.p, self.q
         s.op = _lib.OPS[self.operator]
@@ -152,7 +155,26 @@ class MeshProblem:
         s.weights = self.weights.data_ptr()
         s.tables_v = self.tables_v.data_ptr()
         s.tables_d = self.tables_d.data_ptr() if self.operator != "mass" else None
+        s.band = self.band.data_ptr() if band else None
         return s
+
+    # -- K1 + 1D band matrices (separable method) ------------------------
+    def build_band_tables(self, stream=None) -> bool:
+        """K1 tables and the assembled 1D band matrices in one launch
+        (``iga_band_tables``); False if the library cannot (the separable kernel then
+        integrates the band matrices itself)."""
+        torch = _lib.require_cuda()
+        if getattr(self, "band", None) is None:
+            N, nb = self.K + self.p, 2 * self.p + 1
+            self.band = torch.empty(N * nb * 2, dtype=torch.float64, device=self.device)
+        s = self.problem_struct()
+        rc = _lib.load().iga_band_tables(ctypes.byref(s), self.ref_nodes.data_ptr(),
+                                         self.tables_v.data_ptr(), self.tables_d.data_ptr(),
+                                         self.band.data_ptr(), _lib.stream_ptr(stream or self.stream))
+        if rc == _lib.IGA_EUNSUPPORTED:
+            return False
+        _lib.check(rc)
+        return True
 
     # -- sizes ----------------------------------------------------------
     @property
@@ -171,12 +193,13 @@ class MeshProblem:
 
     # -- fused integrate + assemble ------------------------------------
     def integrate_assemble(self, values, method: int, el_range=None, plane_range=None,
-                           stream=None):
+                           stream=None, band: bool = False):
         """Write CSR values of row planes ``plane_range`` from elements ``el_range``
-        (slowest axis) into ``values`` (torch fp64, starts at the first row)."""
+        (slowest axis) into ``values`` (torch fp64, starts at the first row); ``band``:
+        use the band tables of the last ``build_band_tables`` (separable method)."""
         el = (0, self.K) if el_range is None else el_range
         pl = (0, self.K + self.p) if plane_range is None else plane_range
-        s = self.problem_struct()
+        s = self.problem_struct(band)
         _lib.check(_lib.load().iga_integrate_assemble(
             ctypes.byref(s), method, int(el[0]), int(el[1]), int(pl[0]), int(pl[1]),
             values.data_ptr(), _lib.stream_ptr(stream or self.stream)))

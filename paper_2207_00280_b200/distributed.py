@@ -157,6 +157,12 @@ class SlabSession:
         self.n_comp = plane_nnz(3, plan.K, plan.p, plan.own_lo, hi)
         self.values = torch.empty(self.n_comp, dtype=torch.float64, device=self.prob.device)
         self.stream = torch.cuda.current_stream()
+        # separable kernel: 1D band matrices precomputed by the K1 launch
+        self.use_band = self.code == 3 and self.prob.build_band_tables(self.stream)
+
+    def _ia(self, values, el, planes):
+        self.prob.integrate_assemble(values, self.code, el_range=el, plane_range=planes,
+                                     stream=self.stream, band=self.use_band)
 
     def _axpy(self, x, y):
         _lib.check(_lib.load().iga_axpy(x.numel(), x.data_ptr(), y.data_ptr(),
@@ -164,21 +170,20 @@ class SlabSession:
 
     def step(self, exchange: bool = True):
         pl = self.plan
-        self.prob.build_tables(self.stream)
+        if self.use_band:
+            self.prob.build_band_tables(self.stream)
+        else:
+            self.prob.build_tables(self.stream)
         if self.halo == "recompute":
-            self.prob.integrate_assemble(self.values, self.code, el_range=pl.recompute_elements,
-                                         plane_range=(pl.own_lo, pl.own_hi), stream=self.stream)
+            self._ia(self.values, pl.recompute_elements, (pl.own_lo, pl.own_hi))
             return self.values
         el = (pl.el_lo, pl.el_hi)
         if pl.comp_hi > pl.own_hi:
-            iface = self.values[self.n_own:]
-            self.prob.integrate_assemble(iface, self.code, el_range=el,
-                                         plane_range=(pl.own_hi, pl.comp_hi), stream=self.stream)
+            self._ia(self.values[self.n_own:], el, (pl.own_hi, pl.comp_hi))
         pending = None
         if exchange and pl.world > 1:
             pending = start_interface_exchange(pl, self.values)
-        self.prob.integrate_assemble(self.values, self.code, el_range=el,
-                                     plane_range=(pl.own_lo, pl.own_hi), stream=self.stream)
+        self._ia(self.values, el, (pl.own_lo, pl.own_hi))
         if pending is not None:
             finish_interface_exchange(*pending, self.values, add=self._axpy)
         return self.values[:self.n_own]

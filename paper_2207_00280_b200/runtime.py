@@ -158,6 +158,8 @@ class DeviceSession:
         self.prob = MeshProblem(cfg.dim, cfg.mesh, cfg.degree, cfg.points, cfg.operator,
                                 cfg.coefficient)
         self.stream = stream if stream is not None else torch.cuda.current_stream()
+        # separable kernel: 1D band matrices precomputed by the K1 launch
+        self.use_band = self.code == 3 and self.prob.build_band_tables(self.stream)
         self.values = torch.empty(self.prob.nnz(), dtype=torch.float64, device=self.prob.device)
         self._host_in = [torch.from_numpy(self.prob.ref_nodes_host).pin_memory(),
                          torch.from_numpy(self.prob.weights_host).pin_memory()]
@@ -174,7 +176,15 @@ class DeviceSession:
     def d2h_bytes(self) -> int:
         return self.values.numel() * 8
 
+    @property
+    def launches_per_step(self) -> int:
+        return 2
+
     def _launch(self, stream):
+        if self.use_band:  # K1 + band matrices in one launch, then the separable kernel
+            self.prob.build_band_tables(stream)
+            self.prob.integrate_assemble(self.values, self.code, stream=stream, band=True)
+            return
         self.prob.build_tables(stream)
         self.prob.integrate_assemble(self.values, self.code, stream=stream)
 

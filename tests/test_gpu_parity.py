@@ -625,3 +625,43 @@ def test_device_session_graph_replay_matches_eager(pkg):
     for _ in range(3):
         b = s.step()
     assert (a == b).all().item()
+
+
+@pytest.mark.parametrize("K,p,op,slab", [(6, 3, "stiffness", None), (64, 3, "stiffness", None),
+                                         (64, 3, "stiffness", (21, 40)), (9, 1, "stiffness_mass", (2, 6)),
+                                         (7, 2, "mass", None), (5, 4, "stiffness_mass", None),
+                                         (4, 5, "stiffness", None), (3, 0, "mass", None),
+                                         (120, 3, "stiffness", None), (120, 2, "mass", (30, 61))])
+def test_separable_band_tables(pkg, K, p, op, slab):
+    """iga_band_tables (K1 + the assembled 1D band matrices in one launch) and the separable
+    kernel reading them (many short CTAs) against the kernel that integrates the band
+    matrices in every CTA: K1 tables bitwise, CSR values bitwise where the old kernel sums
+    element by element (meshes whose tables fit its shared memory), else to rounding."""
+    import torch
+
+    from paper_2207_00280_b200.device import MeshProblem
+
+    mp = MeshProblem(3, K, p, p + 1, op, 1.3)
+    mp.build_tables()
+    V0, D0 = mp.tables_v.clone(), mp.tables_d.clone()
+    el = (0, K) if slab is None else slab
+    pl = (0, K + p) if slab is None else (slab[0], min(K + p, slab[1] + p))
+    n = mp.nnz(*pl)
+    a = torch.full((n,), float("nan"), dtype=torch.float64, device="cuda")
+    b = torch.full((n,), float("nan"), dtype=torch.float64, device="cuda")
+    mp.integrate_assemble(a, 3, el_range=el, plane_range=pl)
+    mp.tables_v.zero_()
+    mp.tables_d.zero_()
+    assert mp.build_band_tables()
+    assert torch.equal(mp.tables_v, V0)
+    if op != "mass":
+        assert torch.equal(mp.tables_d, D0)
+    mp.integrate_assemble(b, 3, el_range=el, plane_range=pl, band=True)
+    torch.cuda.synchronize()
+    assert not torch.isnan(b).any().item()
+    if K <= 64:
+        assert torch.equal(a, b)
+    else:
+        assert torch.allclose(a, b, rtol=1e-13, atol=1e-13 * a.abs().max().item())
+    del a, b
+    torch.cuda.empty_cache()
