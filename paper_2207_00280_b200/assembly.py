@@ -83,7 +83,6 @@ def assemble(elements, K: int, p: int) -> GlobalGram:
 
     Element matrices are uploaded once and summed on the device into the
     structured CSR in lexicographic element order."""
-    torch = _lib.require_cuda()
     by_id: dict[ElementId, ElementMatrix] = {}
     for alpha, mat in elements:
         if alpha in by_id:
@@ -99,6 +98,7 @@ def assemble(elements, K: int, p: int) -> GlobalGram:
         if ent.shape != (n, n):
             raise ValueError(f"element matrix for {alpha} has wrong shape")
         host[e] = ent
+    torch = _lib.require_cuda()  # after the reference's ValueError checks
     mats = torch.from_numpy(host).cuda()
     nd = _n_dofs(3, K, p)
     values = torch.empty(csr_nnz(3, K, p), dtype=torch.float64, device=mats.device)

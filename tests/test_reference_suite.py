@@ -323,3 +323,60 @@ def test_nonzero_basis_derivatives_on_device():
             fd = (P.eval_nonzero_basis(kv, e, x + h).values
                   - P.eval_nonzero_basis(kv, e, x - h).values) / (2 * h)
             assert np.abs(ana - fd).max() / max(1.0, np.abs(ana).max()) < 1e-5
+
+
+# ----------------------------------------------------------------- assembly (assembly.py:46-83)
+def test_assemble_rejects_bad_element_sets():
+    """assemble's input checks (assembly.py:56-63, :73-74), before any device work:
+    empty, incomplete and duplicated element sets, wrong element-matrix shapes."""
+    K, p = 2, 1
+    n = (p + 1) ** 3
+    mat = P.ElementMatrix(element=(0, 0, 0), n=n, entries=np.eye(n), flops=0)
+    full = [(a, mat) for a in P.element_list(K)]
+    with pytest.raises(ValueError, match="cover"):
+        P.assemble([], K, p)
+    with pytest.raises(ValueError, match="cover"):
+        P.assemble(full[:-1], K, p)
+    with pytest.raises(ValueError, match="duplicate"):
+        P.assemble(full + full[:1], K, p)
+    bad = P.ElementMatrix(element=(0, 0, 0), n=n + 1, entries=np.eye(n + 1), flops=0)
+    with pytest.raises(ValueError, match="shape"):
+        P.assemble([(full[0][0], bad)] + full[1:], K, p)
+
+
+@pytest.mark.gpu
+def test_empty_ranges_through_the_abi():
+    """Degenerate calls of the C-ABI: an empty row-plane range writes nothing, an empty
+    element slab zeroes the rows it owns (every method), zero element matrices and an
+    empty pattern range are no-ops."""
+    import ctypes
+
+    import torch
+
+    from paper_2207_00280_b200 import _lib
+    from paper_2207_00280_b200.device import MeshProblem
+
+    L = _lib.load()
+    K, p = 4, 2
+    mp = MeshProblem(3, K, p, p + 1, "stiffness", None)
+    v = torch.full((mp.nnz(),), 7.0, dtype=torch.float64, device="cuda")
+    s = mp.problem_struct()
+    for method in (0, 1, 2, 3):
+        assert L.iga_integrate_assemble(ctypes.byref(s), method, 0, K, 3, 3, v.data_ptr(), None) == 0
+        torch.cuda.synchronize()
+        assert (v == 7.0).all().item()
+    for method in (0, 1, 2, 3):
+        v.fill_(7.0)
+        assert L.iga_integrate_assemble(ctypes.byref(s), method, 2, 2, 0, K + p, v.data_ptr(), None) == 0
+        torch.cuda.synchronize()
+        assert (v == 0.0).all().item(), method
+    out = torch.full((1,), 3.0, dtype=torch.float64, device="cuda")
+    ids = torch.zeros((1, 3), dtype=torch.int32, device="cuda")
+    assert L.iga_element_matrices(ctypes.byref(s), 0, mp.ref_nodes.data_ptr(), ids.data_ptr(), None,
+                                  0, out.data_ptr(), None) == 0
+    torch.cuda.synchronize()
+    assert out.item() == 3.0
+    ip = torch.full((1,), -1, dtype=torch.int64, device="cuda")
+    assert L.iga_csr_pattern(3, K, p, 5, 5, ip.data_ptr(), None, None) == 0
+    torch.cuda.synchronize()
+    assert ip.item() in (-1, 0)
