@@ -665,3 +665,36 @@ def test_separable_band_tables(pkg, K, p, op, slab):
         assert torch.allclose(a, b, rtol=1e-13, atol=1e-13 * a.abs().max().item())
     del a, b
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("K,p,op", [(5, 3, "stiffness"), (4, 2, "mass"), (3, 4, "stiffness_mass"),
+                                    (6, 1, "stiffness"), (2, 5, "mass")])
+def test_writes_stay_in_bounds(pkg, K, p, op):
+    """Bounds check by canaries (compute-sanitizer is unavailable on this pool): every
+    method writes exactly its row range -- the NaN-prefilled range fully, the sentinel
+    guard zones around it (4096 values each side) not at all -- for full meshes and
+    element slabs with partial plane ranges, with and without precomputed band tables."""
+    import torch
+
+    from paper_2207_00280_b200.device import MeshProblem
+
+    q = p + 1
+    coef = np.random.default_rng(3).uniform(0.5, 1.5, size=(K**3, q**3))
+    G = 4096
+    for c in (None, coef):
+        mp = MeshProblem(3, K, p, q, op, c)
+        mp.build_tables()
+        band = mp.build_band_tables()
+        N = K + p
+        for el, pl in (((0, K), (0, N)), ((1, K - 1), (1, min(N, K - 1 + p))), ((0, 1), (0, p + 1))):
+            n = mp.nnz(*pl)
+            buf = torch.full((n + 2 * G,), 12345.0, dtype=torch.float64, device="cuda")
+            methods = (0, 1, 2) if c is not None else (0, 1, 2, 3)
+            for method in methods:
+                for use_band in ((False, True) if method == 3 and band else (False,)):
+                    buf[G:G + n] = float("nan")
+                    mp.integrate_assemble(buf[G:], method, el_range=el, plane_range=pl, band=use_band)
+                    torch.cuda.synchronize()
+                    assert (buf[:G] == 12345.0).all().item() and (buf[G + n:] == 12345.0).all().item(), \
+                        (method, el, pl, use_band)
+                    assert not torch.isnan(buf[G:G + n]).any().item(), (method, el, pl, use_band)

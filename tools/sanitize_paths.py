@@ -21,6 +21,17 @@ def main():
                                     ("classical", "auto", coef)):
             P.run_integration(P.RunConfig(method, "device", K, p, operator=op, coefficient=c,
                                           assembly=assembly)).gram.values.sum().item()
+    # element slabs (multi-GPU launches) through the band-table and per-CTA paths
+    import torch
+
+    from paper_2207_00280_b200.device import MeshProblem
+
+    mp = MeshProblem(3, 7, 3, 4, "stiffness", None)
+    v = torch.empty(mp.nnz(2, 8), dtype=torch.float64, device="cuda")
+    mp.build_band_tables()
+    for method in (3, 2):
+        mp.integrate_assemble(v, method, el_range=(2, 5), plane_range=(2, 8), band=method == 3)
+    mp.integrate_assemble(v, 3, el_range=(2, 5), plane_range=(2, 8))
     g = P.run_integration(P.RunConfig("sumfact", "device", 6, 3, operator="stiffness")).gram
     g.spmv(np.ones(g.n_dofs))
     P.write_matrix_market(g, "/tmp/sanitize.mtx")
