@@ -25,7 +25,10 @@
 namespace iga {
 namespace mma {
 
-constexpr int NT = 512;
+// threads per CTA: 512 (one CTA per SM, shared-memory bound) for p >= 3; 256 for p <= 2, whose
+// small tiles run four CTAs per SM (more element-column segments in flight for small meshes)
+template <int P>
+__host__ __device__ constexpr int nt_of() { return P <= 2 ? 256 : 512; }
 __host__ __device__ constexpr int cdiv(int a, int b) { return (a + b - 1) / b; }
 // smallest pitch >= n with pitch == r (mod mod)
 __host__ __device__ constexpr int pitch_mod(int n, int mod, int r) { return n + ((r - n % mod) % mod + mod) % mod; }
@@ -73,7 +76,8 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 }
 
 template <int P, int Q, int TA, int TB, bool STIFF>
-__global__ void __launch_bounds__(NT, P <= 2 ? 2 : 1) k_gsf3_mma(GsfArgs a) {
+__global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs a) {
+  constexpr int NT = nt_of<P>();
   using S = Shape<P, Q, TA, TB>;
   constexpr int m = S::m, NB = S::NB, KA = S::KA, KB = S::KB, GC = S::GC;
   constexpr int GCW = S::GCW, KAP = S::KAP, KBP = S::KBP;
@@ -405,6 +409,7 @@ static int launch_t(const GsfArgs& a0, cudaStream_t s) {
     const void* fn = reinterpret_cast<const void*>(k_gsf3_mma<P, Q, TA, TB, ST>);
     cudaError_t e = smem_attr_once(fn, Sh::bytes, true);
     if (e != cudaSuccess) return check_cuda(e, "gsf mma smem attr");
+    constexpr int NT = nt_of<P>();
     const int64_t slots = (int64_t)sm_count() * blocks_per_sm_once(fn, NT, Sh::bytes);
     int best = 1;
     double best_cost = 1e300;
