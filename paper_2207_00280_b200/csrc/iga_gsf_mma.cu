@@ -62,7 +62,7 @@ struct Shape {
   // rolling-row slot pitch: rowVals + a pad that spreads the stage-S read-modify-writes
   // over the shared-memory banks (picked by simulating the access pattern of the two
   // coefficient-field configs: 37% fewer wavefronts at p = 4, q = 5; 20% at p = 2, q = 3)
-  static constexpr int RP = rowVals + (P == 4 && Q == 5 && TA == 2 && TB == 2   ? 1
+  static constexpr int RP = rowVals + (P == 4 && Q == 5 && TA * TB == 4          ? 1
                                        : P == 2 && Q == 3 && TA == 3 && TB == 3 ? 7
                                                                                 : 0);
   static constexpr int nR = TA * TB * m * RP;
@@ -377,17 +377,21 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
 }
 
 // Tile of row pencils per CTA: 3 x 3 for p = 2 (stage-A rows 15 of 16 and stage-B columns
-// 15 of 16 in their DMMA tiles; C2 32^3: 144 tiles, 0.087 vs 0.099 ms with 2 x 4), else the
-// largest of 2 x 4 / 2 x 2 / 2 x 1 / 1 x 1 that fits shared memory
+// 15 of 16 in their DMMA tiles; C2 32^3: 144 tiles, 0.087 vs 0.099 ms with 2 x 4), 1 x 4 for
+// p = 4 (7% fewer DMMAs per pencil than 2 x 2; C4 16.0 vs 16.3 ms), else the largest of
+// 2 x 4 / 2 x 2 / 2 x 1 / 1 x 1 that fits shared memory
 template <int P, int Q, bool ST>
 struct Tile {
   static constexpr size_t cap = 227 * 1024;
   static constexpr bool t33 = P == 2 && Shape<P, Q, 3, 3>::bytes <= cap;
+  static constexpr bool t14 = P == 4 && Shape<P, Q, 1, 4>::bytes <= cap;
   static constexpr int TA = t33 ? 3
+                            : t14 ? 1
                             : Shape<P, Q, 2, 4>::bytes <= cap ? 2
                             : Shape<P, Q, 2, 2>::bytes <= cap ? 2
                             : Shape<P, Q, 2, 1>::bytes <= cap ? 2 : 1;
   static constexpr int TB = t33 ? 3
+                            : t14 ? 4
                             : Shape<P, Q, 2, 4>::bytes <= cap ? 4
                             : Shape<P, Q, 2, 2>::bytes <= cap ? 2 : 1;
 };
