@@ -199,7 +199,8 @@ def run_reference(args, wl, K, p, rank):
 KERNEL_NAMES = {0: "k_classical_mma (Algorithm 1 on DMMA + fused CSR scatter; 2D: k_classical_scatter)",
                 1: "k_sumfact_scatter (element-local sum factorization + atomic scatter)",
                 2: "k_gsf3 (assembled sum factorization on DMMA + CSR write)",
-                3: "k_kron3 (1D band quadrature + Kronecker CSR fill, TMA bulk stores)"}
+                3: "k_kron3 (Kronecker CSR fill from the 1D band matrices that K1 (k_mesh_band) "
+                   "integrates, TMA bulk stores)"}
 
 
 def kernel_roofline(code, wl, K, p, q, k_el, by, kern_ms, peaks):
