@@ -130,6 +130,70 @@ __global__ void __launch_bounds__(256, 5) k_spmv3(int K, const double* __restric
   }
 }
 
+// Same product with the x window in shared memory: a CTA takes one dof plane I0, a block
+// of SB1 pencils I1 (one warp each) and a segment of SEG rows I2; the x values its rows
+// touch (<= 2P+1 planes x SB1+2P pencils x SEG+2P rows) are staged once, so the per-value
+// gathers hit shared memory instead of L1/L2 (the values stream from HBM as before).
+constexpr int kSpmvSB1 = 8, kSpmvSeg = 64;
+template <int P>
+__global__ void __launch_bounds__(32 * kSpmvSB1) k_spmv3s(int K, const double* __restrict__ values,
+                                                        const double* __restrict__ x,
+                                                        double* __restrict__ y) {
+  constexpr int NB = 2 * P + 1, WB = kSpmvSB1 + 2 * P, WC = kSpmvSeg + 2 * P;
+  extern __shared__ double xs[];  // [NB][WB][WC]
+  const int N = K + P;
+  const int nb1 = (N + kSpmvSB1 - 1) / kSpmvSB1, nsg = (N + kSpmvSeg - 1) / kSpmvSeg;
+  const int seg = (N + nsg - 1) / nsg;  // balanced segments of <= kSpmvSeg rows
+  const int blk = blockIdx.x;
+  const int I0 = blk / (nb1 * nsg), r = blk - I0 * nb1 * nsg, i1b = (r / nsg) * kSpmvSB1,
+            h0 = (r % nsg) * seg, h1 = min(N, h0 + seg);
+  const int lo0 = max(0, I0 - P), c0 = (int)band_cnt(I0, P, N);
+  const int b_lo = max(0, i1b - P), b_hi = min(N, i1b + kSpmvSB1 + P);
+  const int c_lo = max(0, h0 - P), c_hi = min(N, h1 + P);
+  const int nbw = b_hi - b_lo, ncw = c_hi - c_lo;
+  for (int u = threadIdx.x; u < c0 * nbw * ncw; u += blockDim.x) {
+    const int a = u / (nbw * ncw), rr = u - a * nbw * ncw, b = rr / ncw, c = rr - b * ncw;
+    xs[(a * WB + b) * WC + c] = __ldg(x + ((int64_t)(lo0 + a) * N + b_lo + b) * N + c_lo + c);
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31, I1 = i1b + (threadIdx.x >> 5);
+  if (I1 >= N) return;
+  const int c1 = (int)band_cnt(I1, P, N), c01 = c0 * c1;
+  const double* v = values + rowptr3(I0, I1, h0, P, N);
+  const double* xw = xs + (band_lo(I1, P) - b_lo) * WC - c_lo;  // + (a WB + b) WC + column
+  constexpr int NE = (NB * NB * NB + 31) / 32;
+  int xo[NE];
+#pragma unroll
+  for (int k = 0; k < NE; ++k) {
+    const int j = lane + 32 * k, a = j / (NB * NB), b = (j / NB) % NB, c = j % NB;
+    xo[k] = (a * WB + b) * WC + c;
+  }
+  double* yp = y + ((int64_t)I0 * N + I1) * N;
+  for (int I2 = h0; I2 < h1; ++I2) {
+    const int lo2 = I2 - P < 0 ? 0 : I2 - P;
+    const int c2 = (int)band_cnt(I2, P, N);
+    const double* xb = xw + lo2;
+    const int cnt = c01 * c2;
+    double acc = 0.0;
+    if (cnt == NB * NB * NB) {
+#pragma unroll
+      for (int k = 0; k < NE; ++k) {
+        const int j = lane + 32 * k;
+        if (j < NB * NB * NB) acc += v[j] * xb[xo[k]];
+      }
+    } else {
+      for (int j = lane; j < cnt; j += 32) {
+        const int a = j / (c1 * c2), b = (j / c2) % c1, c = j % c2;
+        acc += v[j] * xb[(a * WB + b) * WC + c];
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) yp[I2] = acc;
+    v += cnt;
+  }
+}
+
 template <int P>
 struct Spmv3Launch {
   static int run(int K, const double* values, const double* x, double* y, cudaStream_t s) {
@@ -142,6 +206,17 @@ struct Spmv3Launch {
     const int64_t units = N * N * nseg;
     const int64_t want = (units * 32 + 255) / 256;
     const int64_t grid = want < (int64_t)sm_count() * 5 ? want : (int64_t)sm_count() * 5;
+    // the staged-window kernel wins on large meshes only (measured: K = 256 9.8 vs 11.5 ms,
+    // K = 192 4.3 vs 4.8; K <= 128 the L1 version is faster); IGA_SPMV_L1=1 forces L1
+    if (N >= 160 && !getenv("IGA_SPMV_L1")) {
+      const int64_t nb1 = (N + kSpmvSB1 - 1) / kSpmvSB1, nsg = (N + kSpmvSeg - 1) / kSpmvSeg;
+      const size_t sm = sizeof(double) * (2 * P + 1) * (kSpmvSB1 + 2 * P) * (kSpmvSeg + 2 * P);
+      const void* fn = reinterpret_cast<const void*>(k_spmv3s<P>);
+      cudaError_t e = smem_attr_once(fn, sm, false);
+      if (e != cudaSuccess) return check_cuda(e, "spmv smem attr");
+      k_spmv3s<P><<<(unsigned)(N * nb1 * nsg), 32 * kSpmvSB1, sm, s>>>(K, values, x, y);
+      return check_cuda(cudaGetLastError(), "iga_spmv");
+    }
     k_spmv3<P><<<(unsigned)grid, 256, 0, s>>>(K, values, x, y, nseg);
     return check_cuda(cudaGetLastError(), "iga_spmv");
   }

@@ -698,3 +698,31 @@ def test_writes_stay_in_bounds(pkg, K, p, op):
                     assert (buf[:G] == 12345.0).all().item() and (buf[G + n:] == 12345.0).all().item(), \
                         (method, el, pl, use_band)
                     assert not torch.isnan(buf[G:G + n]).any().item(), (method, el, pl, use_band)
+
+
+def test_spmv_staged_window_matches(pkg, monkeypatch):
+    """Large meshes (N >= 160) take the SpMV with the x window staged in shared memory;
+    it sums in the same order as the L1-gather kernel (IGA_SPMV_L1=1): bitwise equal."""
+    import torch
+
+    from paper_2207_00280_b200 import _lib
+
+    K, p = 170, 3
+    g = pkg.run_integration(pkg.RunConfig("sumfact", "device", K, p, operator="stiffness")).gram
+    n = (K + p) ** 3
+    x = torch.randn(n, dtype=torch.float64, device="cuda", generator=torch.Generator("cuda").manual_seed(5))
+    y1, y2 = torch.empty_like(x), torch.empty_like(x)
+    L = _lib.load()
+    _lib.check(L.iga_spmv(3, K, p, _lib.ptr(g.values), _lib.ptr(x), _lib.ptr(y1), _lib.stream_ptr()))
+    monkeypatch.setenv("IGA_SPMV_L1", "1")
+    _lib.check(L.iga_spmv(3, K, p, _lib.ptr(g.values), _lib.ptr(x), _lib.ptr(y2), _lib.stream_ptr()))
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y2)
+    # and against the matrix: row sums of the stiffness matrix vanish, so A 1 = 0
+    ones = torch.ones(n, dtype=torch.float64, device="cuda")
+    monkeypatch.delenv("IGA_SPMV_L1")
+    _lib.check(L.iga_spmv(3, K, p, _lib.ptr(g.values), _lib.ptr(ones), _lib.ptr(y1), _lib.stream_ptr()))
+    torch.cuda.synchronize()
+    assert y1.abs().max().item() <= 1e-12 * g.values.abs().max().item() * 343
+    del g, x, y1, y2, ones
+    torch.cuda.empty_cache()
