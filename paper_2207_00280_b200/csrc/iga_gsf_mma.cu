@@ -41,8 +41,11 @@ __device__ __forceinline__ int qw_row(int g, int d) {
   return d == 4 ? (g >> 1) + 4 * (g & 1) : (d == 2 ? (g & 4) + ((g >> 1) & 1) + 2 * (g & 1) : g);
 }
 
-template <int P, int Q, int TA, int TB>
+// ST: stiffness (two operand types, double2 elements) or mass (one type: double elements,
+// half the footprint of X, Y, PA, PB and Z, so p = 2 mass runs four CTAs per SM)
+template <int P, int Q, int TA, int TB, bool ST = true>
 struct Shape {
+  static constexpr int EW = ST ? 2 : 1;
   static constexpr int m = P + 1, NB = 2 * P + 1;
   static constexpr int LA = TA + P, LB = TB + P;
   static constexpr int KA = LA * Q, KB = LB * Q;  // contraction lengths of stages A, B
@@ -53,12 +56,12 @@ struct Shape {
   static constexpr int KAP = pitch_mod(KA, 8, 4), KBP = pitch_mod(KB, 8, 4);
   static constexpr int NA0 = TA * NB, NB1 = TB * NB, NC = NA0 * NB1, NR = NA0 * Q;
   static constexpr int rowVals = NB * NB * NB;
-  static constexpr int nW = KA * GCW, nY = 2 * NC * Q;
+  static constexpr int nW = KA * GCW, nY = EW * NC * Q;
   // Y aliases W (W is dead after stage A); even, so the double2 arrays after it are aligned
   static constexpr int nWY = ((nW > nY ? nW : nY) + 1) / 2 * 2;
-  static constexpr int nX = 2 * NA0 * GC;
-  static constexpr int nPA = 2 * NA0 * KAP, nPB = 2 * NB1 * KBP;
-  static constexpr int nZ = 2 * m * m * Q;
+  static constexpr int nX = EW * NA0 * GC;
+  static constexpr int nPA = EW * NA0 * KAP, nPB = EW * NB1 * KBP;
+  static constexpr int nZ = EW * m * m * Q;
   // rolling-row slot pitch: rowVals + a pad that spreads the stage-S read-modify-writes
   // over the shared-memory banks (picked by simulating the access pattern of the two
   // coefficient-field configs: 37% fewer wavefronts at p = 4, q = 5; 20% at p = 2, q = 3)
@@ -69,6 +72,20 @@ struct Shape {
   static constexpr size_t bytes = sizeof(double) * ((size_t)nWY + nX + nPA + nPB + nZ + nR);
 };
 
+// shared-memory element of the operand tables: (V, D) pairs for stiffness, V only for mass
+template <bool ST>
+struct Elem {
+  using T = double2;
+  static __device__ __forceinline__ double2 mk(double x, double y) { return make_double2(x, y); }
+};
+template <>
+struct Elem<false> {
+  using T = double;
+  static __device__ __forceinline__ double mk(double x, double) { return x; }
+};
+__device__ __forceinline__ double2 as2(double2 v) { return v; }
+__device__ __forceinline__ double2 as2(double v) { return make_double2(v, 0.0); }
+
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
       : "+d"(d0), "+d"(d1)
@@ -78,17 +95,18 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 template <int P, int Q, int TA, int TB, bool STIFF>
 __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs a) {
   constexpr int NT = nt_of<P>();
-  using S = Shape<P, Q, TA, TB>;
+  using S = Shape<P, Q, TA, TB, STIFF>;
+  using E = typename Elem<STIFF>::T;
   constexpr int m = S::m, NB = S::NB, KA = S::KA, KB = S::KB, GC = S::GC;
   constexpr int GCW = S::GCW, KAP = S::KAP, KBP = S::KBP;
   constexpr int NA0 = S::NA0, NB1 = S::NB1, NC = S::NC, NR = S::NR;
   extern __shared__ double smem[];
   double* sW = smem;                                         // [KA][GCW]
-  double2* Y2 = reinterpret_cast<double2*>(smem);            // [NC][Q] (aliases W)
-  double2* X2 = reinterpret_cast<double2*>(smem + S::nWY);   // [NA0][Q][KB] (XV, XD)
-  double2* PA2 = X2 + NA0 * GC;                              // [NA0][KAP] (VV, DD)
-  double2* PB2 = PA2 + NA0 * KAP;                            // [NB1][KBP] (VV, DD)
-  double2* Z2 = PB2 + NB1 * KBP;                             // [Q][m*m] (VV, DD(+VV))
+  E* Y2 = reinterpret_cast<E*>(smem);                        // [NC][Q] (aliases W)
+  E* X2 = reinterpret_cast<E*>(smem + S::nWY);               // [NA0][Q][KB] (XV, XD)
+  E* PA2 = X2 + NA0 * GC;                                    // [NA0][KAP] (VV, DD)
+  E* PB2 = PA2 + NA0 * KAP;                                  // [NB1][KBP] (VV, DD)
+  E* Z2 = PB2 + NB1 * KBP;                                   // [Q][m*m] (VV, DD(+VV))
   double* R = reinterpret_cast<double*>(Z2 + m * m * Q);     // [TA*TB][m][RP]
   __shared__ int64_t rowoff[TA * TB];
   __shared__ int comboR[NC];  // R offset of combo (a0, b1): pencil block + (d0, d1) row
@@ -116,7 +134,7 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
       v.x = V[((int64_t)e0 * m + r) * Q + k0] * V[((int64_t)e0 * m + sc) * Q + k0];
       if (STIFF) v.y = D[((int64_t)e0 * m + r) * Q + k0] * D[((int64_t)e0 * m + sc) * Q + k0];
     }
-    PA2[a0 * KAP + kk] = v;
+    PA2[a0 * KAP + kk] = Elem<STIFF>::mk(v.x, v.y);
   }
   for (int u = tid; u < NB1 * KB; u += NT) {
     const int b1 = u / KB, kk = u % KB, lb = kk / Q, k1 = kk % Q;
@@ -127,7 +145,7 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
       v.x = V[((int64_t)e1 * m + r) * Q + k1] * V[((int64_t)e1 * m + sc) * Q + k1];
       if (STIFF) v.y = D[((int64_t)e1 * m + r) * Q + k1] * D[((int64_t)e1 * m + sc) * Q + k1];
     }
-    PB2[b1 * KBP + kk] = v;
+    PB2[b1 * KBP + kk] = Elem<STIFF>::mk(v.x, v.y);
   }
   for (int u = tid; u < S::nR; u += NT) R[u] = 0.0;
   for (int c = tid; c < NC; c += NT) {
@@ -198,9 +216,43 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
                                 (int)band_cnt(I0, P, N) << 11 | (int)band_cnt(I1, P, N) << 16;
     }
   };
+  // Row flush by (band position v, pencil rc).  When a row's band padded to whole warps
+  // divides the CTA (p <= 2: 125 -> 128 lanes, two pencils per pass), every thread keeps one
+  // v and its (d0, d1, d2) for the whole flush and walks the pencils; otherwise the flat
+  // (rc, v) loop below.  Both write the same values to the same addresses.
+  constexpr int VT = cdiv(S::rowVals, 32) * 32, RCS = NT / VT;
+  constexpr bool by_v = RCS >= 1 && RCS * VT == NT;
   auto flush_row = [&](int I2) {
     const int slot = I2 % m;
     const int lod2 = max(0, P - I2), c2 = (int)band_cnt(I2, P, N);
+    if constexpr (by_v) {
+      const int v = tid % VT;
+      if (v >= S::rowVals) return;
+      double* Rv = R + slot * S::RP + v;
+      if (I2 < s0) {  // recomputed halo row of this segment: nothing is written here
+        for (int rc = tid / VT; rc < TA * TB; rc += RCS) Rv[rc * m * S::RP] = 0.0;
+        return;
+      }
+      const int d2 = v % NB, d1 = (v / NB) % NB, d0 = v / (NB * NB);
+      const bool in2 = d2 >= lod2 && d2 < lod2 + c2;
+      for (int rc = tid / VT; rc < TA * TB; rc += RCS) {
+        double* Rr = Rv + rc * m * S::RP;
+        const int64_t off = rowoff[rc];
+        if (off >= 0) {
+          const int mt = rowmeta[rc];
+          if (mt == 0) {
+            a.values[off + v] = *Rr;
+          } else {
+            const int lod0 = (mt >> 1) & 31, lod1 = (mt >> 6) & 31, c0 = (mt >> 11) & 31,
+                      c1 = (mt >> 16) & 31;
+            if (in2 && d0 >= lod0 && d0 < lod0 + c0 && d1 >= lod1 && d1 < lod1 + c1)
+              a.values[off + ((d0 - lod0) * c1 + (d1 - lod1)) * c2 + (d2 - lod2)] = *Rr;
+          }
+        }
+        *Rr = 0.0;
+      }
+      return;
+    }
     for (int u = tid; u < TA * TB * S::rowVals; u += NT) {
       const int rc = u / S::rowVals, v = u - rc * S::rowVals;
       double* Rv = R + (rc * m + slot) * S::RP + v;
@@ -244,7 +296,7 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
         dd = zv[2] * zv[3];
         if (a.op == IGA_OP_STIFFNESS_MASS) dd += vv;
       }
-      Z2[tid] = make_double2(vv, dd);
+      Z2[tid] = Elem<STIFF>::mk(vv, dd);
     }
     load_z(e2 + 1, zv);
     __syncthreads();
@@ -260,7 +312,7 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks) {
           const int kk = ks * 4 + t;
-          pa[ks] = (row < NA0 && kk < KA) ? PA2[row * KAP + kk] : make_double2(0.0, 0.0);
+          pa[ks] = (row < NA0 && kk < KA) ? as2(PA2[row * KAP + kk]) : make_double2(0.0, 0.0);
         }
         for (int ntl = grp; ntl < NTL; ntl += GRP) {
           const int col = ntl * 8 + g;
@@ -274,8 +326,8 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
           }
           const int c0 = ntl * 8 + 2 * t;
           if (row < NA0) {
-            if (c0 < GC) X2[row * GC + c0] = make_double2(cv0, cd0);
-            if (c0 + 1 < GC) X2[row * GC + c0 + 1] = make_double2(cv1, cd1);
+            if (c0 < GC) X2[row * GC + c0] = Elem<STIFF>::mk(cv0, cd0);
+            if (c0 + 1 < GC) X2[row * GC + c0 + 1] = Elem<STIFF>::mk(cv1, cd1);
           }
         }
       }
@@ -293,7 +345,7 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks) {
           const int kk = ks * 4 + t;
-          pb[ks] = (b1 < NB1 && kk < KB) ? PB2[b1 * KBP + kk] : make_double2(0.0, 0.0);
+          pb[ks] = (b1 < NB1 && kk < KB) ? as2(PB2[b1 * KBP + kk]) : make_double2(0.0, 0.0);
         }
         for (int mt = grp; mt < MT; mt += GRP) {
           const int row = mt * 8 + qw_row(g, DQ), a0 = row / Q, k2 = row % Q;
@@ -301,7 +353,7 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
 #pragma unroll
           for (int ks = 0; ks < KS; ++ks) {
             const int kk = ks * 4 + t;
-            const double2 x = (row < NR && kk < KB) ? X2[row * KB + kk] : make_double2(0.0, 0.0);
+            const double2 x = (row < NR && kk < KB) ? as2(X2[row * KB + kk]) : make_double2(0.0, 0.0);
             if (STIFF) {
               dmma(ya0, ya1, x.x, pb[ks].y);
               dmma(ya0, ya1, x.y, pb[ks].x);
@@ -312,8 +364,8 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
           }
           const int c0 = ntl * 8 + 2 * t;
           if (row < NR) {
-            if (c0 < NB1) Y2[(a0 * NB1 + c0) * Q + k2] = make_double2(ya0, yb0);
-            if (c0 + 1 < NB1) Y2[(a0 * NB1 + c0 + 1) * Q + k2] = make_double2(ya1, yb1);
+            if (c0 < NB1) Y2[(a0 * NB1 + c0) * Q + k2] = Elem<STIFF>::mk(ya0, yb0);
+            if (c0 + 1 < NB1) Y2[(a0 * NB1 + c0 + 1) * Q + k2] = Elem<STIFF>::mk(ya1, yb1);
           }
         }
       }
@@ -332,7 +384,7 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks) {
           const int k = ks * 4 + t;
-          z[ks] = (n < MM && k < Q) ? Z2[k * MM + n] : make_double2(0.0, 0.0);
+          z[ks] = (n < MM && k < Q) ? as2(Z2[k * MM + n]) : make_double2(0.0, 0.0);
         }
         int dst[2];  // offset of column (r, s) in a combo's R block, -1 if padding
         const int slot0 = e2 % m;
@@ -348,7 +400,7 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
 #pragma unroll
           for (int ks = 0; ks < KS; ++ks) {
             const int k = ks * 4 + t;
-            const double2 y = (combo < NC && k < Q) ? Y2[combo * Q + k] : make_double2(0.0, 0.0);
+            const double2 y = (combo < NC && k < Q) ? as2(Y2[combo * Q + k]) : make_double2(0.0, 0.0);
             dmma(c0v, c1v, y.x, z[ks].x);
             if (STIFF) dmma(c0v, c1v, y.y, z[ks].y);
           }
@@ -383,22 +435,22 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
 template <int P, int Q, bool ST>
 struct Tile {
   static constexpr size_t cap = 227 * 1024;
-  static constexpr bool t33 = P == 2 && Shape<P, Q, 3, 3>::bytes <= cap;
-  static constexpr bool t14 = P == 4 && Shape<P, Q, 1, 4>::bytes <= cap;
+  static constexpr bool t33 = P == 2 && Shape<P, Q, 3, 3, ST>::bytes <= cap;
+  static constexpr bool t14 = P == 4 && Shape<P, Q, 1, 4, ST>::bytes <= cap;
   static constexpr int TA = t33 ? 3
                             : t14 ? 1
-                            : Shape<P, Q, 2, 4>::bytes <= cap ? 2
-                            : Shape<P, Q, 2, 2>::bytes <= cap ? 2
-                            : Shape<P, Q, 2, 1>::bytes <= cap ? 2 : 1;
+                            : Shape<P, Q, 2, 4, ST>::bytes <= cap ? 2
+                            : Shape<P, Q, 2, 2, ST>::bytes <= cap ? 2
+                            : Shape<P, Q, 2, 1, ST>::bytes <= cap ? 2 : 1;
   static constexpr int TB = t33 ? 3
                             : t14 ? 4
-                            : Shape<P, Q, 2, 4>::bytes <= cap ? 4
-                            : Shape<P, Q, 2, 2>::bytes <= cap ? 2 : 1;
+                            : Shape<P, Q, 2, 4, ST>::bytes <= cap ? 4
+                            : Shape<P, Q, 2, 2, ST>::bytes <= cap ? 2 : 1;
 };
 
 template <int P, int Q, bool ST, int TA = Tile<P, Q, ST>::TA, int TB = Tile<P, Q, ST>::TB>
 static int launch_t(const GsfArgs& a0, cudaStream_t s) {
-  using Sh = Shape<P, Q, TA, TB>;
+  using Sh = Shape<P, Q, TA, TB, ST>;
   if constexpr (Sh::bytes > 227 * 1024) {
     set_error("assembled sum factorization: p=%d q=%d needs %zu B shared memory", P, Q, Sh::bytes);
     return IGA_EUNSUPPORTED;
