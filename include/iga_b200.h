@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define IGA_ABI_VERSION 2
+#define IGA_ABI_VERSION 3
 
 #define IGA_OK 0
 #define IGA_EINVAL 1       /* invalid argument -> ValueError            */
@@ -61,10 +61,12 @@ typedef struct iga_problem {
   const double* weights; /* device [q] reference Gauss weights (leggauss, mesh.py:82) */
   const double* tables_v; /* device [K][p+1][q] basis values from iga_mesh_tables */
   const double* tables_d; /* device [K][p+1][q] basis derivatives (NULL for IGA_OP_MASS) */
-  const double* band;     /* device [K+p][2p+1][2] assembled 1D band matrices from
+  const double* band;     /* device [K+p][2p+1][2] + 2 assembled 1D band matrices from
                              iga_band_tables, or NULL.  Used by the separable method only:
                              with it the integration kernel reads the 1D integrals instead of
-                             forming them in every CTA (a shorter prologue). */
+                             forming them in every CTA (a shorter prologue).  ABI v3: the 2
+                             trailing doubles are the kernel's chunk counter (zeroed by
+                             iga_band_tables; one stream at a time per buffer). */
 } iga_problem;
 
 const char* iga_last_error(void);
@@ -85,7 +87,8 @@ int32_t iga_basis_eval(int32_t K, int32_t p, int64_t n, const int32_t* elem, con
 
 /* K1 + the assembled 1D band matrices of the separable method in one launch:
  * vals/ders [K][p+1][q] as iga_mesh_tables (either may be NULL: not stored), and
- * band[I][d] = (m, k), I < K+p, d = J-I+p in [0, 2p]:
+ * band[I][d] = (m, k), I < K+p, d = J-I+p in [0, 2p], followed by 2 doubles of counter
+ * state for iga_integrate_assemble (zeroed here; band holds (K+p)(2p+1)*2 + 2 doubles):
  *   m(I,J) = sum_e sum_k w_k V_e(I-e,k) V_e(J-e,k)   (k(I,J): the same with derivatives)
  * over all elements, elements ascending -- the 1D factors of the Kronecker form of the
  * reference's element quadrature summed by assemble (integrators.py:77-151,

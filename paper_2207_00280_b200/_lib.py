@@ -103,7 +103,7 @@ def load():
                  "iga_integrate_assemble", "iga_assemble_elements", "iga_axpy", "iga_spmv",
                  "iga_apply", "iga_write_matrix_market", "iga_write_matrix_market_host"):
         getattr(L, name).restype = i32
-    if L.iga_abi_version() != 2:
+    if L.iga_abi_version() != 3:
         raise ImportError("libiga_b200.so ABI version mismatch")
     _lib = L
     return L

@@ -57,6 +57,8 @@ struct KronArgs {
   const double* V;               // [K][P+1][Q]
   const double* D;               // [K][P+1][Q] (null for mass)
   const double2* band;           // [N][2P+1] (m, k) from iga_band_tables, or null
+  unsigned long long* claim;     // [2] chunk counter + finished CTAs after the band tables
+                                 // (zeroed by iga_band_tables, re-armed by the last CTA), or null
   double* values;
 };
 

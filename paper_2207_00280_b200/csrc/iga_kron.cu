@@ -96,7 +96,15 @@ __global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) 
   // range [b U / grid, (b+1) U / grid) of the U chunks (balanced to a chunk)
   const int nch = (int)((N + G - 1) / G);
   const int64_t nunit = (int64_t)(a.plane_end - a.plane_begin) * N * nch;
-  const int64_t u_lo = nunit * blockIdx.x / gridDim.x, u_hi = nunit * (blockIdx.x + 1) / gridDim.x;
+  const int64_t u_lo0 = nunit * blockIdx.x / gridDim.x, u_hi0 = nunit * (blockIdx.x + 1) / gridDim.x;
+  // Dynamic order (a.claim, whole-mesh launches, opt-in): CTAs claim whole pencils in CSR
+  // order from a global counter, so the grid's writes move through the array together.  A
+  // persistent TMA fill of the C3 array claiming 16-40 KB chunks that way reaches 6.9-7.0
+  // TB/s (cudaMemset's rate) against 5.9 TB/s for contiguous per-CTA ranges
+  // (tools/order_probe.cu), but this kernel measured slower with it (C3 0.149 vs 0.133 ms;
+  // claiming single chunks 0.223 ms), so the static ranges are the default.  Element slabs
+  // always use the static ranges (their axis-0 table covers only the CTA's planes).
+  const bool dyn = a.claim != nullptr && full;
   if (a.band) {
     // 1D band matrices precomputed once per step (iga_band_tables): a short copy instead
     // of the quadrature in every CTA; the axis-0 rows of an element slab are integrated
@@ -105,8 +113,8 @@ __global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) 
     if (!full) {
       if (tid < Q) w[tid] = a.weights[tid];
       __syncthreads();
-      const int i0lo = a.plane_begin + (int)(u_lo / nch / N);
-      const int i0hi = a.plane_begin + (int)((u_hi - 1) / nch / N);
+      const int i0lo = a.plane_begin + (int)(u_lo0 / nch / N);
+      const int i0hi = a.plane_begin + (int)((u_hi0 - 1) / nch / N);
       for (int u = tid; u < (i0hi - i0lo + 1) * NB; u += NT) {
         const int I0 = i0lo + u / NB, d = u % NB;
         tb[N * NB + I0 * NB + d] = band1d_el<P, Q>(a.V, a.D, K, w, I0, d, a.el_begin, a.el_end, stiff);
@@ -122,8 +130,12 @@ __global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) 
   if (a.K > 0) return;
 #endif
   int chunk = 0;  // chunks issued by this CTA (selects the staging buffer)
+  int npen = 0;   // pencil set-ups of this CTA (selects the pair-factor buffer)
   const int64_t T = band_prefix(N, P, N);  // values of a full-length band row set
-  double* vals = nullptr;                   // first value of the current pencil
+  // claims, three chunks ahead: slot (c+3)%4 is written (thread 0) after the barrier of chunk
+  // c+1 from the atomic issued during chunk c, and read before the barrier of chunk c+3
+  __shared__ long long s_claim[4];
+  unsigned long long nxt = 0;
   // the chunk produced last, stored after the next barrier (thread 0)
   double* pg = nullptr;
   const double* psb = nullptr;
@@ -138,6 +150,9 @@ __global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) 
     asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
     pg = nullptr;
   };
+  auto run_units = [&](int64_t u_lo, int64_t u_hi, int c) {
+  double* vals = nullptr;  // first value of the current pencil
+  bool claimed = false;    // thread 0: the claim three ahead was taken for this unit range
   for (int64_t pen = u_lo / nch; pen * nch < u_hi; ++pen) {
     const int I0 = a.plane_begin + (int)(pen / N), I1 = (int)(pen % N);
     // consecutive pencils are contiguous in the CSR: one 64-bit rowptr per CTA
@@ -172,7 +187,7 @@ __global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) 
     }
     // the pencil's pair factors for the truncated rows (visible after the chunk barrier;
     // double-buffered: a thread may start this pencil while others finish the last)
-    double2* F = Fbuf[pen & 1];
+    double2* F = Fbuf[npen++ & 1];
     for (int b = tid; b < c01; b += NT) {
       double f0, f1;
       factors(b, f0, f1);
@@ -196,7 +211,14 @@ __global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) 
       // after it, the previous chunk is complete in shared memory and leaves.
       if (tid == 0) asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(kron_nbuf() - 2) : "memory");
       __syncthreads();
-      if (tid == 0) issue();
+      if (tid == 0) {
+        issue();
+        if (dyn && !claimed) {
+          claimed = true;
+          s_claim[(c + 3) & 3] = (long long)nxt;
+          nxt = atomicAdd(a.claim, 1ull);
+        }
+      }
       double* sb = buf + pad;
       // truncated-band rows (I2 < P or I2 >= K): b = e / c2 by a reciprocal (exact for
       // e < 2^20 / NB), factors from the pencil table F
@@ -240,10 +262,33 @@ __global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) 
     }
     vals += (int64_t)c01 * T;
   }
+  };
+  if (dyn) {
+    if (tid == 0) {
+      for (int i = 0; i < 3; ++i) s_claim[i] = (long long)atomicAdd(a.claim, 1ull);
+      nxt = atomicAdd(a.claim, 1ull);
+    }
+    __syncthreads();
+    for (int c = 0;; ++c) {
+      const long long u = s_claim[c & 3];  // a whole pencil (its chunks share the set-up)
+      if (u * nch >= nunit) break;
+      run_units(u * nch, (u + 1) * nch, c);
+    }
+  } else {
+    run_units(u_lo0, u_hi0, 0);
+  }
   __syncthreads();
   if (tid == 0) {
     issue();
     asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
+    if (dyn) {  // the last CTA to finish re-arms the counter for the next launch
+      __threadfence();
+      if (atomicAdd(a.claim + 1, 1ull) == gridDim.x - 1) {
+        a.claim[0] = 0;
+        a.claim[1] = 0;
+        __threadfence();
+      }
+    }
   }
 }
 
@@ -258,7 +303,8 @@ template <int P, int Q>
 __global__ void __launch_bounds__(128) k_mesh_band(int K, const double* __restrict__ ref,
                                                    const double* __restrict__ weights, int stiff,
                                                    double* __restrict__ V, double* __restrict__ D,
-                                                   double2* __restrict__ band) {
+                                                   double2* __restrict__ band,
+                                                   unsigned long long* __restrict__ claim) {
   constexpr int M = P + 1, NB = 2 * P + 1, NEL = kBandRows + P;
   __shared__ double Vs[NEL * M * Q], Ds[NEL * M * Q];
   __shared__ double2 em[NEL * M * M];
@@ -267,6 +313,7 @@ __global__ void __launch_bounds__(128) k_mesh_band(int K, const double* __restri
   const int i_lo = blockIdx.x * kBandRows, i_hi = min(N, i_lo + kBandRows);
   const int e0 = max(0, i_lo - P), e1 = min(K, i_hi), ne = e1 - e0;
   if (tid < Q) w[tid] = weights[tid];
+  if (blockIdx.x == 0 && tid == 0) claim[0] = claim[1] = 0;  // k_kron3's chunk counter
   for (int u = tid; u < ne * Q; u += nt) {
     const int le = u / Q, k = u - le * Q, e = e0 + le;
     double vals[M], ders[M];
@@ -317,8 +364,9 @@ struct BandLaunch {
   static int run(int K, const double* ref, const double* weights, int stiff, double* V, double* D,
                  double2* band, cudaStream_t s) {
     const int N = K + P;
-    k_mesh_band<P, Q><<<(N + kBandRows - 1) / kBandRows, 128, 0, s>>>(K, ref, weights, stiff, V,
-                                                                       D, band);
+    k_mesh_band<P, Q><<<(N + kBandRows - 1) / kBandRows, 128, 0, s>>>(
+        K, ref, weights, stiff, V, D, band,
+        reinterpret_cast<unsigned long long*>(band + (size_t)N * (2 * P + 1)));
     return check_cuda(cudaGetLastError(), "band launch");
   }
 };

@@ -166,7 +166,8 @@ class MeshProblem:
         torch = _lib.require_cuda()
         if getattr(self, "band", None) is None:
             N, nb = self.K + self.p, 2 * self.p + 1
-            self.band = torch.empty(N * nb * 2, dtype=torch.float64, device=self.device)
+            # the tables + 2 doubles of chunk-counter state for the separable kernel (ABI v3)
+            self.band = torch.empty(N * nb * 2 + 2, dtype=torch.float64, device=self.device)
         s = self.problem_struct()
         rc = _lib.load().iga_band_tables(ctypes.byref(s), self.ref_nodes.data_ptr(),
                                          self.tables_v.data_ptr(), self.tables_d.data_ptr(),
