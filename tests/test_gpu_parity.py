@@ -726,3 +726,28 @@ def test_spmv_staged_window_matches(pkg, monkeypatch):
     assert y1.abs().max().item() <= 1e-12 * g.values.abs().max().item() * 343
     del g, x, y1, y2, ones
     torch.cuda.empty_cache()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("K,p,op", [(64, 3, "stiffness"), (17, 2, "mass"), (9, 4, "stiffness_mass")])
+def test_separable_claim_order_bitwise(K, p, op, monkeypatch):
+    """The opt-in claim-ordered schedule of k_kron3 (IGA_KRON_DYNAMIC, pencils claimed from
+    the counter after the band tables) writes the same bits as the static ranges, and the
+    counter re-arms itself: three launches after one K1 all write every value."""
+    import torch
+
+    from paper_2207_00280_b200.device import MeshProblem
+
+    mp = MeshProblem(3, K, p, p + 1, op, 1.3)
+    assert mp.build_band_tables()
+    n = mp.nnz(0, K + p)
+    ref = torch.full((n,), float("nan"), dtype=torch.float64, device="cuda")
+    mp.integrate_assemble(ref, 3, band=True)
+    monkeypatch.setenv("IGA_KRON_DYNAMIC", "1")
+    for _ in range(3):
+        out = torch.full((n,), float("nan"), dtype=torch.float64, device="cuda")
+        mp.integrate_assemble(out, 3, band=True)
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref)
+    monkeypatch.delenv("IGA_KRON_DYNAMIC")
+    assert not torch.isnan(ref).any().item()
