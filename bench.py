@@ -169,26 +169,44 @@ def cpu_port_rate(wl, K, p, steps_planes, threads, coef, reps=1):
     return steps_planes * n_el_plane, times
 
 
+def bench_config(wl, K, p):
+    """The workload description both arms print (so the driver can match them)."""
+    return {"workload": wl["desc"], "K": K, "p": p, "q": p + 1, "dim": wl["dim"],
+            "operator": wl["op"], "method": wl["method"],
+            "coefficient": wl["coef"] or "scalar c=1", "elements": K ** wl["dim"],
+            "l2": "GPU arm: a 256 MB buffer is written between timed steps (outside the "
+                  "per-step events) and each step writes the whole CSR (> 126 MB L2); CPU arm: "
+                  "no flush"}
+
+
 def run_reference(args, wl, K, p, rank):
-    """--impl reference: the reference's CPU path (oracle port) on all host cores."""
+    """--impl reference: the reference's CPU path (oracle port) on all host cores, one
+    whole mesh per step when that takes <= 10 s (C1-C3), else a plane sample sized to
+    about 5 s per step (C4, C5: stated in cpu_baseline.sample)."""
     if rank != 0:
         return
     threads = os.cpu_count()
     coef = coefficient(wl["coef"], K, p, wl["dim"])
-    planes = max(1, min(K, 8 if K <= 64 else 2))
-    n_el, _ = cpu_port_rate(wl, K, p, planes, threads, coef, reps=0)
-    _, times = cpu_port_rate(wl, K, p, planes, threads, coef, reps=args.warmup + args.steps)
+    # probe one plane for the per-plane cost (also pages the port in)
+    n1, t1 = cpu_port_rate(wl, K, p, 1, threads, coef, reps=1)
+    per_plane = min(t1)
+    planes = K if per_plane * K <= 10.0 else max(1, min(K, int(5.0 / max(per_plane, 1e-9))))
+    n_el, times = cpu_port_rate(wl, K, p, planes, threads, coef, reps=args.warmup + args.steps)
     t = times[args.warmup:]
     step_s = float(np.mean(t))
     v = n_el / step_s
-    sample = (f"{planes} element planes ({n_el} elements) of the {K}^{wl['dim']} mesh per step, "
-              f"element-local sum factorization + CSR scatter, OpenMP {threads} threads")
+    whole = planes == K
+    sample = ((f"the whole {K}^{wl['dim']} mesh ({n_el} elements) per step" if whole else
+               f"{planes} of {K} element planes ({n_el} of {K ** wl['dim']} elements) per step "
+               f"(the whole mesh would take {per_plane * K:.0f} s per step)") +
+              f", element-local sum factorization + CSR scatter (oracle port of "
+              f"run_integration(over_elements) + assemble), OpenMP {threads} threads")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": "elements/s",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": wl["desc"], "K": K, "p": p, "sample": sample},
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded; no dataset)",
+        "config": bench_config(wl, K, p), "whole_mesh_per_step": whole,
         "cpu_baseline": {"value": v, "unit": "elements/s", "cores": threads, "kind": "port",
                          "sample": sample},
         "e2e": {"value": v, "unit": "elements/s", "h2d_bytes_per_step": 0,
@@ -197,10 +215,11 @@ def run_reference(args, wl, K, p, rank):
 
 
 KERNEL_NAMES = {0: "k_classical_mma (Algorithm 1 on DMMA + fused CSR scatter; 2D: k_classical_scatter)",
-                1: "k_sumfact_scatter (element-local sum factorization + atomic scatter)",
-                2: "k_gsf3 (assembled sum factorization on DMMA + CSR write)",
-                3: "k_kron3 (Kronecker CSR fill from the 1D band matrices that K1 (k_mesh_band) "
-                   "integrates, TMA bulk stores)"}
+                1: "k_sumfact_scatter (element-local sum factorization + CSR scatter)",
+                2: "k_gsf3 (assembled sum factorization on DMMA + CSR write; general "
+                   "per-quadrature-point coefficient path)",
+                3: "k_kron3 (separable shortcut, scalar coefficient only: Kronecker CSR fill from "
+                   "the 1D band matrices that K1 (k_mesh_band) integrates, TMA bulk stores)"}
 
 
 def kernel_roofline(code, wl, K, p, q, k_el, by, kern_ms, peaks):
@@ -208,10 +227,16 @@ def kernel_roofline(code, wl, K, p, q, k_el, by, kern_ms, peaks):
     the launch (perfmodel.py) over its CUDA-event time."""
     from paper_2207_00280_b200 import perfmodel
 
+    own = None
     if code == 3:
         fl = perfmodel.separable_flops(wl["op"], K, p, q) * k_el / K**3
-    elif code == 2:
-        fl = perfmodel.assembled_flops(wl["op"], K, p, q) * k_el / K**3
+    elif code in (1, 2) and wl["dim"] == 3:
+        # SURVEY.md 8(d): the roofline of general (per-quadrature-point coefficient) sum
+        # factorization counts its element-local flops per element; the assembled kernel's
+        # own (smaller) count is reported beside it
+        fl = perfmodel.element_sumfact_flops(wl["op"], p, q) * k_el
+        if code == 2:
+            own = perfmodel.assembled_flops(wl["op"], K, p, q) * k_el / K**3
     elif code == 0:
         fl = perfmodel.classical_flops(wl["op"], p, q, wl["dim"]) * k_el
     else:
@@ -243,15 +268,36 @@ def kernel_roofline(code, wl, K, p, q, k_el, by, kern_ms, peaks):
         "peak_src": peaks["src"], "traffic": None,
     })
     if code in (1, 2) and wl["dim"] == 3:
-        # SURVEY.md 8(d) yardstick: elements/s against the roofline of general element-local
-        # sum factorization (its minimal flop count per element)
-        f_el = perfmodel.element_sumfact_flops(wl["op"], p, q)
-        el_roof = 1.0 / max(f_el / (peaks["fp64_tflops"] * 1e12),
-                            (by / k_el) / (peaks["hbm_gbs"] * 1e9))
-        roof["survey_sumfact_flops_per_el"] = f_el
-        roof["survey_roofline_el_s"] = el_roof
-        roof["frac_of_survey_roofline"] = (k_el / (kern_ms / 1e3)) / el_roof
+        roof["flops_basis"] = (f"SURVEY.md 8(d): {perfmodel.element_sumfact_flops(wl['op'], p, q)} "
+                               f"flop/element of general element-local sum factorization x "
+                               f"{k_el} elements")
+        roof["survey_roofline_el_s"] = 1.0 / max(
+            perfmodel.element_sumfact_flops(wl["op"], p, q) / (peaks["fp64_tflops"] * 1e12),
+            (by / k_el) / (peaks["hbm_gbs"] * 1e9))
+    if own is not None:
+        a_own = own / (kern_ms / 1e3) / 1e12
+        roof["own_algorithm"] = {
+            "what": "assembled sum factorization (contractions shared by overlapping elements, "
+                    "perfmodel.assembled_flops)",
+            "flops": own, "flops_per_element": own / k_el, "achieved": a_own,
+            "unit": "TFLOP/s", "frac": a_own / peaks["fp64_tflops"]}
     return roof
+
+
+def ncu_traffic(wname, kernel):
+    """DRAM bytes per launch of `kernel` on workload `wname` from the committed ncu
+    summaries (profiles/ncu_<workload>[_<path>]_traffic.json, written by
+    tools/profile_summary.py from a --set full capture), or (None, None)."""
+    import glob
+
+    want = kernel.split(" ")[0].split("<")[0]
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", f"ncu_{wname}*_traffic.json"))):
+        tr = json.load(open(f))
+        k = tr.get("kernel", "")
+        # the capture's kernel name carries the template arguments (k_kron3_3_4_16)
+        if k == want or (k.startswith(want + "_") and k[len(want) + 1:len(want) + 2].isdigit()):
+            return tr.get("dram_bytes_per_launch"), os.path.relpath(f, ROOT)
+    return None, None
 
 
 def alt_leg(cfg, assembly, args, flush, stream, wl, total_el, peaks):
@@ -290,12 +336,7 @@ def alt_leg(cfg, assembly, args, flush, stream, wl, total_el, peaks):
     kms = float(np.mean([a.elapsed_time(b) for a, b in kev]))
     K, p = wl["K"], wl["p"]
     roof = kernel_roofline(sess.code, wl, K, p, p + 1, K**3, 8 * sess.values.numel(), kms, peaks)
-    prof = os.path.join(ROOT, "profiles", f"ncu_{wl['name']}_{assembly}_traffic.json")
-    if os.path.exists(prof):
-        tr = json.load(open(prof))
-        # only the kernel that capture measured
-        if tr.get("kernel", "").startswith(roof["kernel"].split(" ")[0].split("<")[0]):
-            roof["traffic"] = tr.get("dram_bytes_per_launch")
+    roof["traffic"], roof["traffic_src"] = ncu_traffic(wl["name"], roof["kernel"])
     out = {"assembly": assembly, "value": total_el / (ms / 1e3), "unit": "elements/s",
            "ms_per_step": ms, "gpu_launches": 2 * args.steps, "roofline": roof}
     del sess
@@ -313,7 +354,9 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-alt", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="launch the step eagerly")
-    ap.add_argument("--assembly", default="auto", help="force a kernel path (RunConfig.assembly)")
+    ap.add_argument("--assembly", default=None,
+                    help="kernel path (RunConfig.assembly); default: the general per-quadrature-"
+                         "point kernel ('owner') for 3D sum factorization, else 'auto'")
     ap.add_argument("--method", default=None, help="override the workload's method")
     ap.add_argument("--halo", choices=["exchange", "recompute"], default="exchange",
                     help="N>1: NCCL interface exchange (default) or the NCCL-free recompute ablation")
@@ -345,8 +388,13 @@ def main():
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     coef = coefficient(wl["coef"], K, p, wl["dim"])
-    cfg = P.RunConfig(args.method or wl["method"], "device", K, p, operator=wl["op"],
-                      coefficient=coef, dim=wl["dim"], devices=world, assembly=args.assembly)
+    method = args.method or wl["method"]
+    # headline: the general sum-factorization kernel (per-quadrature-point coefficient
+    # capable); the separable shortcut for a scalar coefficient is
+    # reported beside it under "separable"
+    assembly = args.assembly or ("owner" if method == "sumfact" and wl["dim"] == 3 else "auto")
+    cfg = P.RunConfig(method, "device", K, p, operator=wl["op"], coefficient=coef,
+                      dim=wl["dim"], devices=world, assembly=assembly)
     stream = torch.cuda.current_stream()
 
     if world > 1:
@@ -429,12 +477,7 @@ def main():
     by = 8 * sess.prob.nnz(plan.own_lo, plan.own_hi) if world > 1 else \
         perfmodel.algorithmic_bytes(wl["dim"], K, p, q, coef is not None)
     roof = kernel_roofline(sess.code, wl, K, p, q, k_el, by, kern_ms, peaks)
-    prof = os.path.join(ROOT, "profiles", f"ncu_{wname}_traffic.json")
-    if os.path.exists(prof):
-        tr = json.load(open(prof))
-        # only the kernel that capture measured
-        if tr.get("kernel", "").startswith(roof["kernel"].split(" ")[0].split("<")[0]):
-            roof["traffic"] = tr.get("dram_bytes_per_launch")
+    roof["traffic"], roof["traffic_src"] = ncu_traffic(wname, roof["kernel"])
 
     # end to end through the public API with host buffers (pinned), N=1 only
     e2e = None
@@ -462,9 +505,10 @@ def main():
                "ms_per_step": e_ms, "wall_ms_per_step": wall * 1e3,
                "api": "paper_2207_00280_b200.runtime.DeviceSession.step_host (pinned host out)"}
 
-    # constant-coefficient 3D workloads: the other kernel for the same matrix
+    # constant-coefficient 3D workloads: the other kernel for the same matrix (normally the
+    # separable Kronecker shortcut, declared as such with its HBM roofline)
     other = None
-    if world == 1 and wl["dim"] == 3 and coef is None and not args.no_alt:
+    if world == 1 and wl["dim"] == 3 and coef is None and not args.no_alt and method == "sumfact":
         other = alt_leg(cfg, "owner" if sess.code == 3 else "separable", args, flush, stream, wl,
                         total_el, peaks)
 
@@ -485,18 +529,14 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded; no dataset)",
-            "config": {"workload": wl["desc"], "K": K, "p": p, "q": q, "dim": wl["dim"],
-                       "operator": wl["op"], "method": wl["method"],
-                       "kernel_path": KERNEL_NAMES[sess.code] + (
-                           "; run_integration's default for a scalar coefficient (the general "
-                           "per-quadrature-point kernel on the same matrix: other_kernel)"
-                           if sess.code == 3 else ""),
-                       "nnz": P.device.csr_nnz(wl["dim"], K, p),
-                       "parallelism": (f"element slabs x{world}, halo {args.halo}" if world > 1
-                                       else "1 GPU"),
-                       "l2": "256 MB buffer written between timed steps (outside the per-step "
-                             "events); each step also writes the whole CSR (> 126 MB L2)"},
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "other_kernel": other,
+            "config": bench_config(wl, K, p),
+            "path": {"kernel_path": KERNEL_NAMES[sess.code], "assembly": assembly,
+                     "nnz": P.device.csr_nnz(wl["dim"], K, p),
+                     "parallelism": (f"element slabs x{world}, halo {args.halo}" if world > 1
+                                     else "1 GPU")},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            **({(other["assembly"] if other["assembly"] == "separable" else "other_kernel"): other}
+               if other else {}),
             **({"e2e_note": e2e_note} if e2e_note else {}),
             "gpu_launches": launches * args.steps, "clocks": clk.summary(),
             "region_ms": region0.elapsed_time(region1),

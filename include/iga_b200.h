@@ -24,7 +24,7 @@
 extern "C" {
 #endif
 
-#define IGA_ABI_VERSION 3
+#define IGA_ABI_VERSION 4
 
 #define IGA_OK 0
 #define IGA_EINVAL 1       /* invalid argument -> ValueError            */
@@ -61,12 +61,11 @@ typedef struct iga_problem {
   const double* weights; /* device [q] reference Gauss weights (leggauss, mesh.py:82) */
   const double* tables_v; /* device [K][p+1][q] basis values from iga_mesh_tables */
   const double* tables_d; /* device [K][p+1][q] basis derivatives (NULL for IGA_OP_MASS) */
-  const double* band;     /* device [K+p][2p+1][2] + 2 assembled 1D band matrices from
+  const double* band;     /* device [K+p][2p+1][2] assembled 1D band matrices from
                              iga_band_tables, or NULL.  Used by the separable method only:
                              with it the integration kernel reads the 1D integrals instead of
-                             forming them in every CTA (a shorter prologue).  ABI v3: the 2
-                             trailing doubles are the kernel's chunk counter (zeroed by
-                             iga_band_tables; one stream at a time per buffer). */
+                             forming them in every CTA (a shorter prologue).  Read-only: the
+                             same buffer may feed concurrent launches on several streams. */
 } iga_problem;
 
 const char* iga_last_error(void);
@@ -85,10 +84,17 @@ int32_t iga_mesh_tables(int32_t K, int32_t p, int32_t q, const double* ref_nodes
 int32_t iga_basis_eval(int32_t K, int32_t p, int64_t n, const int32_t* elem, const double* x,
                        double* vals, double* ders, void* stream);
 
+/* eval_basis / eval_basis_order0 (splines.py:78-118) on any non-decreasing knot vector
+ * knots[n_knots]: out[i] = B_{index[i], order}(x[i]) by the reference's two-term
+ * recursion (0/0 := 0, last non-empty span closed at the last knot), bitwise equal.
+ * An index outside [0, n_knots - order - 2] yields NaN (the Python shim raises
+ * IndexError before the call, as splines.py:85-86 / :103-104 do). */
+int32_t iga_eval_basis(const double* knots, int32_t n_knots, int32_t order, int64_t n,
+                       const int32_t* index, const double* x, double* out, void* stream);
+
 /* K1 + the assembled 1D band matrices of the separable method in one launch:
  * vals/ders [K][p+1][q] as iga_mesh_tables (either may be NULL: not stored), and
- * band[I][d] = (m, k), I < K+p, d = J-I+p in [0, 2p], followed by 2 doubles of counter
- * state for iga_integrate_assemble (zeroed here; band holds (K+p)(2p+1)*2 + 2 doubles):
+ * band[I][d] = (m, k), I < K+p, d = J-I+p in [0, 2p] ((K+p)(2p+1)*2 doubles):
  *   m(I,J) = sum_e sum_k w_k V_e(I-e,k) V_e(J-e,k)   (k(I,J): the same with derivatives)
  * over all elements, elements ascending -- the 1D factors of the Kronecker form of the
  * reference's element quadrature summed by assemble (integrators.py:77-151,
@@ -113,9 +119,15 @@ int32_t iga_csr_pattern(int32_t dim, int32_t K, int32_t p, int64_t row_begin, in
  * elem_nodes: optional device [count][dim][q] physical nodes (the caller's
  * QuadratureRule.nodes); NULL maps prob->weights' reference nodes as gauss_rule
  * does.  ref_nodes [q] must be given when elem_nodes is NULL.
+ * elem_weights: optional device [count][dim][q] per-axis weights (the reference
+ * passes rule.weights[0], [1], [2] separately, integrators.py:200-203); NULL uses
+ * prob->weights on every axis.  elem_coef: optional device [count][q^dim]
+ * coefficients at each listed element's points (k1 slowest); NULL uses prob->coef
+ * indexed by element id, or prob->coef_scalar.
  * prob->tables_* are ignored (tables are evaluated from the nodes). */
 int32_t iga_element_matrices(const iga_problem* prob, int32_t method, const double* ref_nodes,
-                             const int32_t* elem_ids, const double* elem_nodes, int64_t count,
+                             const int32_t* elem_ids, const double* elem_nodes,
+                             const double* elem_weights, const double* elem_coef, int64_t count,
                              double* out, void* stream);
 
 /* Fused mesh-wide integration + assembly (runtime.run_integration,

@@ -32,17 +32,22 @@ from .integrators import (
 from .operator import MatrixFreeOperator, cg
 from .mesh import QuadratureRule, element_list, gauss_rule, local_index, support_set
 from .runtime import (
+    ExecutionTrace,
     IntegrationRuntime,
     RunConfig,
     RunResult,
     grams_bitwise_equal,
     run_integration,
+    run_within_element,
 )
 from .splines import (
     BasisValues,
     KnotVector,
     basis_derivative_table,
     basis_value_table,
+    eval_basis,
+    eval_basis_many,
+    eval_basis_order0,
     eval_nonzero_basis,
     eval_nonzero_basis_derivatives,
     find_element,
@@ -52,6 +57,7 @@ from .splines import (
 __all__ = [
     "BasisValues",
     "ElementMatrix",
+    "ExecutionTrace",
     "GlobalGram",
     "IntegrationRuntime",
     "KnotVector",
@@ -70,6 +76,9 @@ __all__ = [
     "element_dofs",
     "element_list",
     "element_tables",
+    "eval_basis",
+    "eval_basis_many",
+    "eval_basis_order0",
     "eval_nonzero_basis",
     "eval_nonzero_basis_derivatives",
     "find_element",
@@ -81,6 +90,7 @@ __all__ = [
     "local_index",
     "make_knot_vector",
     "run_integration",
+    "run_within_element",
     "sparsity_row_bound",
     "spmv",
     "support_set",

@@ -28,6 +28,7 @@ EXPORTS = (
     "iga_mesh_tables",
     "iga_band_tables",
     "iga_basis_eval",
+    "iga_eval_basis",
     "iga_csr_nnz",
     "iga_csr_pattern",
     "iga_element_matrices",
@@ -87,10 +88,12 @@ def load():
     L.iga_mesh_tables.argtypes = [i32, i32, i32, vp, vp, vp, vp]
     L.iga_band_tables.argtypes = [ctypes.POINTER(IgaProblem), vp, vp, vp, vp, vp]
     L.iga_basis_eval.argtypes = [i32, i32, i64, vp, vp, vp, vp, vp]
+    L.iga_eval_basis.argtypes = [vp, i32, i32, i64, vp, vp, vp, vp]
     L.iga_csr_nnz.argtypes = [i32, i32, i32, i64, i64]
     L.iga_csr_nnz.restype = i64
     L.iga_csr_pattern.argtypes = [i32, i32, i32, i64, i64, vp, vp, vp]
-    L.iga_element_matrices.argtypes = [ctypes.POINTER(IgaProblem), i32, vp, vp, vp, i64, vp, vp]
+    L.iga_element_matrices.argtypes = [ctypes.POINTER(IgaProblem), i32, vp, vp, vp, vp, vp, i64,
+                                       vp, vp]
     L.iga_integrate_assemble.argtypes = [ctypes.POINTER(IgaProblem), i32, i32, i32, i32, i32, vp,
                                          vp]
     L.iga_assemble_elements.argtypes = [i32, i32, i32, vp, i32, i32, vp, vp]
@@ -99,11 +102,11 @@ def load():
     L.iga_apply.argtypes = [ctypes.POINTER(IgaProblem), dp, dp, vp, vp, vp]
     L.iga_write_matrix_market.argtypes = [i32, i32, i32, vp, ctypes.c_char_p, i32, vp]
     L.iga_write_matrix_market_host.argtypes = [i32, i32, i32, vp, ctypes.c_char_p, i32]
-    for name in ("iga_mesh_tables", "iga_band_tables", "iga_basis_eval", "iga_csr_pattern", "iga_element_matrices",
+    for name in ("iga_mesh_tables", "iga_band_tables", "iga_basis_eval", "iga_eval_basis", "iga_csr_pattern", "iga_element_matrices",
                  "iga_integrate_assemble", "iga_assemble_elements", "iga_axpy", "iga_spmv",
                  "iga_apply", "iga_write_matrix_market", "iga_write_matrix_market_host"):
         getattr(L, name).restype = i32
-    if L.iga_abi_version() != 3:
+    if L.iga_abi_version() != 4:
         raise ImportError("libiga_b200.so ABI version mismatch")
     _lib = L
     return L

@@ -132,6 +132,41 @@ struct BasisEvalLaunch {
   }
 };
 
+// eval_basis / eval_basis_order0 (splines.py:78-118) on any non-decreasing knot
+// vector: B_{i,order}(x) by the same two-term triangle as cox_de_boor, bottom-up over
+// the order+1 level-0 spans i .. i+order (the value of B_{i,r}(x) does not depend on the
+// recursion path, and every level uses _cox's expression and 0/0 := 0 branches).
+constexpr int kMaxEvalOrder = 31;
+__global__ void k_eval_basis(const double* __restrict__ t, int nt, int order, int64_t n,
+                             const int32_t* __restrict__ index, const double* __restrict__ xs,
+                             double* __restrict__ out) {
+  const int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (u >= n) return;
+  const int i = index[u];
+  const double x = xs[u];
+  if (i < 0 || i > nt - order - 2) {  // the host raises IndexError first; never read outside t
+    out[u] = __longlong_as_double(0x7ff8000000000000ll);
+    return;
+  }
+  const double tl = t[nt - 1];
+  double N[kMaxEvalOrder + 1];
+  for (int j = 0; j <= order; ++j) {  // order 0 with the closed last non-empty span
+    const double a = t[i + j], b = t[i + j + 1];
+    N[j] = (a <= x && x < b) || (x == tl && a < b && b == tl) ? 1.0 : 0.0;
+  }
+  for (int q = 1; q <= order; ++q)
+    for (int j = 0; j <= order - q; ++j) {
+      const int ii = i + j;
+      double v = 0.0;
+      const double d_left = sub(t[ii + q], t[ii]);
+      if (d_left > 0.0) v = add(v, mul(dvd(sub(x, t[ii]), d_left), N[j]));
+      const double d_right = sub(t[ii + q + 1], t[ii + 1]);
+      if (d_right > 0.0) v = add(v, mul(dvd(sub(t[ii + q + 1], x), d_right), N[j + 1]));
+      N[j] = v;
+    }
+  out[u] = N[0];
+}
+
 // ------------------------------------------------------------------ K5
 // indptr: one thread per row (closed-form row pointer); indices: one warp per
 // row writes its <= (2p+1)^dim sorted columns, coalesced.
@@ -194,6 +229,19 @@ using namespace iga;
 extern "C" {
 
 const char* iga_last_error(void) { return g_err; }
+
+int32_t iga_eval_basis(const double* knots, int32_t n_knots, int32_t order, int64_t n,
+                       const int32_t* index, const double* x, double* out, void* stream) {
+  if (n < 0) return fail_einval("negative point count");
+  if (order < 0 || order > kMaxEvalOrder)
+    return fail_einval("order %d outside [0, %d]", order, kMaxEvalOrder);
+  if (n_knots < order + 2) return fail_einval("%d knots cannot carry order %d", n_knots, order);
+  if (n == 0) return IGA_OK;
+  if (!knots || !index || !x || !out) return fail_einval("null pointer");
+  k_eval_basis<<<(unsigned)((n + 127) / 128), 128, 0, as_stream(stream)>>>(knots, n_knots, order,
+                                                                          n, index, x, out);
+  return check_cuda(cudaGetLastError(), "iga_eval_basis launch");
+}
 
 int32_t iga_abi_version(void) { return IGA_ABI_VERSION; }
 

@@ -14,6 +14,8 @@ struct ElemArgs {
   const double* ref_nodes;
   const int32_t* elem_ids;
   const double* elem_nodes;
+  const double* elem_weights;  // [count][dim][q] per-axis weights, or null (weights on every axis)
+  const double* elem_coef;     // [count][q^dim] per-element coefficients, or null (coef / scalar)
   int64_t count;
   double* out;
 };
@@ -57,8 +59,6 @@ struct KronArgs {
   const double* V;               // [K][P+1][Q]
   const double* D;               // [K][P+1][Q] (null for mass)
   const double2* band;           // [N][2P+1] (m, k) from iga_band_tables, or null
-  unsigned long long* claim;     // [2] chunk counter + finished CTAs after the band tables
-                                 // (zeroed by iga_band_tables, re-armed by the last CTA), or null
   double* values;
 };
 

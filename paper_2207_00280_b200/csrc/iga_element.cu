@@ -18,8 +18,9 @@
 namespace iga {
 
 // ---------------------------------------------------------------- strict
-// Shared layout: tabs[dim][2][m][Q] (values, derivatives), w[Q], then
-// sumfact buffers D [m][m][Q][Q] and C [m][m][m][m][Q] (3D).
+// Shared layout: tabs[dim][2][m][Q] (values, derivatives), w[dim][Q] (per-axis weights:
+// integrators.py:200-203 passes rule.weights[0..2] separately), then sumfact buffers
+// D [m][m][Q][Q] and C [m][m][m][m][Q] (3D).
 template <int DIM, int P, int Q>
 __global__ void __launch_bounds__(256) k_element_strict(ElemArgs a) {
   constexpr int m = P + 1;
@@ -27,8 +28,8 @@ __global__ void __launch_bounds__(256) k_element_strict(ElemArgs a) {
   constexpr int nq = DIM == 3 ? Q * Q * Q : Q * Q;
   extern __shared__ double smem[];
   double* tabs = smem;                       // DIM*2*m*Q
-  double* w = tabs + DIM * 2 * m * Q;        // Q
-  double* Dbuf = w + Q;                      // m*m*Q*Q (3D) or m*m*Q (2D)
+  double* w = tabs + DIM * 2 * m * Q;        // DIM*Q
+  double* Dbuf = w + DIM * Q;                // m*m*Q*Q (3D) or m*m*Q (2D)
   double* Cbuf = Dbuf + m * m * Q * Q;       // m^4*Q (3D)
   const int64_t el = blockIdx.x;
   if (el >= a.count) return;
@@ -46,10 +47,16 @@ __global__ void __launch_bounds__(256) k_element_strict(ElemArgs a) {
       tabs[((d * 2 + 1) * m + r) * Q + k] = ders[r];
     }
   }
-  for (int k = threadIdx.x; k < Q; k += blockDim.x) w[k] = a.weights[k];
+  for (int u = threadIdx.x; u < DIM * Q; u += blockDim.x)
+    w[u] = a.elem_weights ? a.elem_weights[el * DIM * Q + u] : a.weights[u % Q];
   __syncthreads();
+  const double* w0 = w;
+  const double* w1 = w + Q;
+  const double* w2 = w + (DIM - 1) * Q;
   const double* coef = nullptr;
-  if (a.coef) {
+  if (a.elem_coef) {
+    coef = a.elem_coef + el * nq;
+  } else if (a.coef) {
     int64_t eid = DIM == 3 ? ((int64_t)alpha[0] * a.K + alpha[1]) * a.K + alpha[2]
                            : (int64_t)alpha[0] * a.K + alpha[1];
     coef = a.coef + eid * nq;
@@ -90,9 +97,9 @@ __global__ void __launch_bounds__(256) k_element_strict(ElemArgs a) {
                 v = mul(v, b1[j2 * Q + k2]);
                 v = mul(v, b2[i3 * Q + k3]);
                 v = mul(v, b2[j3 * Q + k3]);
-                v = mul(v, w[k1]);
-                v = mul(v, w[k2]);
-                v = mul(v, w[k3]);
+                v = mul(v, w0[k1]);
+                v = mul(v, w1[k2]);
+                v = mul(v, w2[k3]);
                 v = mul(v, a.jac);
                 if (coef) v = mul(v, coef[(k1 * Q + k2) * Q + k3]);
                 else if (scal) v = mul(v, a.coef_scalar);
@@ -106,8 +113,8 @@ __global__ void __launch_bounds__(256) k_element_strict(ElemArgs a) {
               double v = mul(b0[i1 * Q + k1], b0[j1 * Q + k1]);
               v = mul(v, b1[i2 * Q + k2]);
               v = mul(v, b1[j2 * Q + k2]);
-              v = mul(v, w[k1]);
-              v = mul(v, w[k2]);
+              v = mul(v, w0[k1]);
+              v = mul(v, w1[k2]);
               v = mul(v, a.jac);
               if (coef) v = mul(v, coef[k1 * Q + k2]);
               else if (scal) v = mul(v, a.coef_scalar);
@@ -135,7 +142,7 @@ __global__ void __launch_bounds__(256) k_element_strict(ElemArgs a) {
         }
         double acc = 0.0;
         for (int k1 = 0; k1 < Q; ++k1) {
-          double v = mul(mul(mul(b0[i1 * Q + k1], b0[j1 * Q + k1]), w[k1]), a.jac);
+          double v = mul(mul(mul(b0[i1 * Q + k1], b0[j1 * Q + k1]), w0[k1]), a.jac);
           if (coef) v = mul(v, DIM == 3 ? coef[(k1 * Q + k2) * Q + k3] : coef[k1 * Q + k2]);
           else if (scal) v = mul(v, a.coef_scalar);
           acc = add(acc, v);
@@ -153,7 +160,7 @@ __global__ void __launch_bounds__(256) k_element_strict(ElemArgs a) {
           for (int k2 = 0; k2 < Q; ++k2)
             acc = add(acc, mul(mul(mul(b1[i2 * Q + k2], b1[j2 * Q + k2]),
                                    Dbuf[((i1 * m + j1) * Q + k2) * Q + k3]),
-                               w[k2]));
+                               w1[k2]));
           Cbuf[t] = acc;
         }
         __syncthreads();
@@ -170,12 +177,12 @@ __global__ void __launch_bounds__(256) k_element_strict(ElemArgs a) {
           const int j1 = col / (m * m), j2 = (col / m) % m, j3 = col % m;
           const double* Cp = Cbuf + (((i2 * m + i1) * m + j2) * m + j1) * Q;
           for (int k3 = 0; k3 < Q; ++k3)
-            acc = add(acc, mul(mul(mul(b2[i3 * Q + k3], b2[j3 * Q + k3]), Cp[k3]), w[k3]));
+            acc = add(acc, mul(mul(mul(b2[i3 * Q + k3], b2[j3 * Q + k3]), Cp[k3]), w2[k3]));
         } else {
           const int i1 = row / m, i2 = row % m, j1 = col / m, j2 = col % m;
           const double* Dp = Dbuf + (i1 * m + j1) * Q;
           for (int k2 = 0; k2 < Q; ++k2)
-            acc = add(acc, mul(mul(mul(b1[i2 * Q + k2], b1[j2 * Q + k2]), Dp[k2]), w[k2]));
+            acc = add(acc, mul(mul(mul(b1[i2 * Q + k2], b1[j2 * Q + k2]), Dp[k2]), w1[k2]));
         }
         if (ti == 0) {
           out[row * n + col] = acc;
@@ -199,14 +206,14 @@ struct ElementStrictLaunch {
     if (a.count > 0x7fffffff) return fail_einval("too many elements");
     size_t shm;
     if (a.dim == 3) {
-      shm = sizeof(double) * (3 * 2 * m * Q + Q + m * m * Q * Q + m * m * m * m * Q);
+      shm = sizeof(double) * (3 * 2 * m * Q + 3 * Q + m * m * Q * Q + m * m * m * m * Q);
       if (shm > 48 * 1024) {
         cudaError_t e = smem_attr_once(reinterpret_cast<const void*>(k_element_strict<3, P, Q>), shm);
         if (e != cudaSuccess) return check_cuda(e, "element smem attr");
       }
       k_element_strict<3, P, Q><<<(unsigned)a.count, 256, shm, s>>>(a);
     } else {
-      shm = sizeof(double) * (2 * 2 * m * Q + Q + m * m * Q * Q);
+      shm = sizeof(double) * (2 * 2 * m * Q + 2 * Q + m * m * Q * Q);
       k_element_strict<2, P, Q><<<(unsigned)a.count, 256, shm, s>>>(a);
     }
     return check_cuda(cudaGetLastError(), "iga_element_matrices launch");
@@ -223,7 +230,8 @@ using namespace iga;
 
 extern "C" int32_t iga_element_matrices(const iga_problem* prob, int32_t method,
                                         const double* ref_nodes, const int32_t* elem_ids,
-                                        const double* elem_nodes, int64_t count, double* out,
+                                        const double* elem_nodes, const double* elem_weights,
+                                        const double* elem_coef, int64_t count, double* out,
                                         void* stream) {
   if (!prob) return fail_einval("null problem");
   if (prob->dim != 2 && prob->dim != 3) return fail_einval("dim must be 2 or 3");
@@ -239,6 +247,7 @@ extern "C" int32_t iga_element_matrices(const iga_problem* prob, int32_t method,
   a.dim = prob->dim; a.K = prob->K; a.q = prob->q; a.op = prob->op; a.method = method;
   a.jac = prob->jac; a.coef_scalar = prob->coef_scalar; a.coef = prob->coef;
   a.weights = prob->weights; a.ref_nodes = ref_nodes; a.elem_ids = elem_ids;
-  a.elem_nodes = elem_nodes; a.count = count; a.out = out;
+  a.elem_nodes = elem_nodes; a.elem_weights = elem_weights; a.elem_coef = elem_coef;
+  a.count = count; a.out = out;
   return launch_element_strict(a, prob->p, prob->q, as_stream(stream));
 }

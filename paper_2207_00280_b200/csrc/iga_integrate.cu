@@ -208,7 +208,10 @@ struct Spmv3Launch {
     const int64_t grid = want < (int64_t)sm_count() * 5 ? want : (int64_t)sm_count() * 5;
     // the staged-window kernel wins on large meshes only (measured: K = 256 9.8 vs 11.5 ms,
     // K = 192 4.3 vs 4.8; K <= 128 the L1 version is faster); IGA_SPMV_L1=1 forces L1
-    if (N >= 160 && !getenv("IGA_SPMV_L1")) {
+    // (an A/B knob read per call so a test can compare both kernels in one process; only
+    // the value "1" enables it)
+    const char* force_l1 = getenv("IGA_SPMV_L1");
+    if (N >= 160 && !(force_l1 != nullptr && force_l1[0] == '1' && force_l1[1] == 0)) {
       const int64_t nb1 = (N + kSpmvSB1 - 1) / kSpmvSB1, nsg = (N + kSpmvSeg - 1) / kSpmvSeg;
       const size_t sm = sizeof(double) * (2 * P + 1) * (kSpmvSB1 + 2 * P) * (kSpmvSeg + 2 * P);
       const void* fn = reinterpret_cast<const void*>(k_spmv3s<P>);
@@ -316,13 +319,6 @@ int32_t iga_integrate_assemble(const iga_problem* prob, int32_t method, int32_t 
     a.jc = prob->jac * prob->coef_scalar; a.weights = prob->weights;
     a.V = prob->tables_v; a.D = prob->tables_d; a.values = values;
     a.band = reinterpret_cast<const double2*>(prob->band);
-    // ABI v3: the band buffer carries the chunk counter of the dynamic schedule after the
-    // tables.  The static schedule stays the default: claiming pencils in CSR order measured
-    // 0.149 ms on C3 against 0.133 (single chunks: 0.223), although a plain TMA fill gains
-    // 17% from the same order (tools/order_probe.cu); IGA_KRON_DYNAMIC=1 selects it
-    a.claim = prob->band && getenv("IGA_KRON_DYNAMIC")
-                  ? reinterpret_cast<unsigned long long*>(const_cast<double*>(prob->band) + 2 * N * (2 * p + 1))
-                  : nullptr;
     return launch_kron(a, p, prob->q, s);
   }
   if (method == IGA_METHOD_SUMFACT_ASSEMBLED) {

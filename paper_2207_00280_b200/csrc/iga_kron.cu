@@ -97,14 +97,6 @@ __global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) 
   const int nch = (int)((N + G - 1) / G);
   const int64_t nunit = (int64_t)(a.plane_end - a.plane_begin) * N * nch;
   const int64_t u_lo0 = nunit * blockIdx.x / gridDim.x, u_hi0 = nunit * (blockIdx.x + 1) / gridDim.x;
-  // Dynamic order (a.claim, whole-mesh launches, opt-in): CTAs claim whole pencils in CSR
-  // order from a global counter, so the grid's writes move through the array together.  A
-  // persistent TMA fill of the C3 array claiming 16-40 KB chunks that way reaches 6.9-7.0
-  // TB/s (cudaMemset's rate) against 5.9 TB/s for contiguous per-CTA ranges
-  // (tools/order_probe.cu), but this kernel measured slower with it (C3 0.149 vs 0.133 ms;
-  // claiming single chunks 0.223 ms), so the static ranges are the default.  Element slabs
-  // always use the static ranges (their axis-0 table covers only the CTA's planes).
-  const bool dyn = a.claim != nullptr && full;
   if (a.band) {
     // 1D band matrices precomputed once per step (iga_band_tables): a short copy instead
     // of the quadrature in every CTA; the axis-0 rows of an element slab are integrated
@@ -132,10 +124,6 @@ __global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) 
   int chunk = 0;  // chunks issued by this CTA (selects the staging buffer)
   int npen = 0;   // pencil set-ups of this CTA (selects the pair-factor buffer)
   const int64_t T = band_prefix(N, P, N);  // values of a full-length band row set
-  // claims, three chunks ahead: slot (c+3)%4 is written (thread 0) after the barrier of chunk
-  // c+1 from the atomic issued during chunk c, and read before the barrier of chunk c+3
-  __shared__ long long s_claim[4];
-  unsigned long long nxt = 0;
   // the chunk produced last, stored after the next barrier (thread 0)
   double* pg = nullptr;
   const double* psb = nullptr;
@@ -150,9 +138,8 @@ __global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) 
     asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
     pg = nullptr;
   };
-  auto run_units = [&](int64_t u_lo, int64_t u_hi, int c) {
+  const int64_t u_lo = u_lo0, u_hi = u_hi0;
   double* vals = nullptr;  // first value of the current pencil
-  bool claimed = false;    // thread 0: the claim three ahead was taken for this unit range
   for (int64_t pen = u_lo / nch; pen * nch < u_hi; ++pen) {
     const int I0 = a.plane_begin + (int)(pen / N), I1 = (int)(pen % N);
     // consecutive pencils are contiguous in the CSR: one 64-bit rowptr per CTA
@@ -211,14 +198,7 @@ __global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) 
       // after it, the previous chunk is complete in shared memory and leaves.
       if (tid == 0) asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(kron_nbuf() - 2) : "memory");
       __syncthreads();
-      if (tid == 0) {
-        issue();
-        if (dyn && !claimed) {
-          claimed = true;
-          s_claim[(c + 3) & 3] = (long long)nxt;
-          nxt = atomicAdd(a.claim, 1ull);
-        }
-      }
+      if (tid == 0) issue();
       double* sb = buf + pad;
       // truncated-band rows (I2 < P or I2 >= K): b = e / c2 by a reciprocal (exact for
       // e < 2^20 / NB), factors from the pencil table F
@@ -262,33 +242,10 @@ __global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) 
     }
     vals += (int64_t)c01 * T;
   }
-  };
-  if (dyn) {
-    if (tid == 0) {
-      for (int i = 0; i < 3; ++i) s_claim[i] = (long long)atomicAdd(a.claim, 1ull);
-      nxt = atomicAdd(a.claim, 1ull);
-    }
-    __syncthreads();
-    for (int c = 0;; ++c) {
-      const long long u = s_claim[c & 3];  // a whole pencil (its chunks share the set-up)
-      if (u * nch >= nunit) break;
-      run_units(u * nch, (u + 1) * nch, c);
-    }
-  } else {
-    run_units(u_lo0, u_hi0, 0);
-  }
   __syncthreads();
   if (tid == 0) {
     issue();
     asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory");
-    if (dyn) {  // the last CTA to finish re-arms the counter for the next launch
-      __threadfence();
-      if (atomicAdd(a.claim + 1, 1ull) == gridDim.x - 1) {
-        a.claim[0] = 0;
-        a.claim[1] = 0;
-        __threadfence();
-      }
-    }
   }
 }
 
@@ -303,8 +260,7 @@ template <int P, int Q>
 __global__ void __launch_bounds__(128) k_mesh_band(int K, const double* __restrict__ ref,
                                                    const double* __restrict__ weights, int stiff,
                                                    double* __restrict__ V, double* __restrict__ D,
-                                                   double2* __restrict__ band,
-                                                   unsigned long long* __restrict__ claim) {
+                                                   double2* __restrict__ band) {
   constexpr int M = P + 1, NB = 2 * P + 1, NEL = kBandRows + P;
   __shared__ double Vs[NEL * M * Q], Ds[NEL * M * Q];
   __shared__ double2 em[NEL * M * M];
@@ -313,7 +269,6 @@ __global__ void __launch_bounds__(128) k_mesh_band(int K, const double* __restri
   const int i_lo = blockIdx.x * kBandRows, i_hi = min(N, i_lo + kBandRows);
   const int e0 = max(0, i_lo - P), e1 = min(K, i_hi), ne = e1 - e0;
   if (tid < Q) w[tid] = weights[tid];
-  if (blockIdx.x == 0 && tid == 0) claim[0] = claim[1] = 0;  // k_kron3's chunk counter
   for (int u = tid; u < ne * Q; u += nt) {
     const int le = u / Q, k = u - le * Q, e = e0 + le;
     double vals[M], ders[M];
@@ -365,8 +320,7 @@ struct BandLaunch {
                  double2* band, cudaStream_t s) {
     const int N = K + P;
     k_mesh_band<P, Q><<<(N + kBandRows - 1) / kBandRows, 128, 0, s>>>(
-        K, ref, weights, stiff, V, D, band,
-        reinterpret_cast<unsigned long long*>(band + (size_t)N * (2 * P + 1)));
+        K, ref, weights, stiff, V, D, band);
     return check_cuda(cudaGetLastError(), "band launch");
   }
 };

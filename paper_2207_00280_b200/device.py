@@ -166,8 +166,7 @@ class MeshProblem:
         torch = _lib.require_cuda()
         if getattr(self, "band", None) is None:
             N, nb = self.K + self.p, 2 * self.p + 1
-            # the tables + 2 doubles of chunk-counter state for the separable kernel (ABI v3)
-            self.band = torch.empty(N * nb * 2 + 2, dtype=torch.float64, device=self.device)
+            self.band = torch.empty(N * nb * 2, dtype=torch.float64, device=self.device)
         s = self.problem_struct()
         rc = _lib.load().iga_band_tables(ctypes.byref(s), self.ref_nodes.data_ptr(),
                                          self.tables_v.data_ptr(), self.tables_d.data_ptr(),
@@ -206,22 +205,36 @@ class MeshProblem:
             values.data_ptr(), _lib.stream_ptr(stream or self.stream)))
         return values
 
-    def element_matrices(self, elem_ids, method: int, elem_nodes=None, stream=None):
-        """Per-element matrices [count, n, n] (strict reference operation order)."""
+    def element_matrices(self, elem_ids, method: int, elem_nodes=None, elem_weights=None,
+                         elem_coef=None, jac=None, coef_scalar=None, stream=None):
+        """Per-element matrices [count, n, n] (strict reference operation order).
+        ``elem_nodes`` / ``elem_weights``: [count, dim, q] per-axis nodes and weights (the
+        caller's QuadratureRule); ``elem_coef``: [count, q^dim] coefficients at those
+        points (only these values are uploaded, never a mesh-wide field)."""
         torch = _lib.require_cuda()
         ids = torch.as_tensor(np.ascontiguousarray(elem_ids, dtype=np.int32)).reshape(-1, self.dim)
         ids = ids.to(self.device)
         count = ids.shape[0]
         n = (self.p + 1) ** self.dim
+
+        def upload(x, shape):
+            if x is None:
+                return None
+            t = torch.as_tensor(np.ascontiguousarray(x, dtype=np.float64))
+            return t.reshape(shape).to(self.device)
+
+        nodes = upload(elem_nodes, (count, self.dim, self.q))
+        weights = upload(elem_weights, (count, self.dim, self.q))
+        coef = upload(elem_coef, (count, self.q ** self.dim))
         out = torch.empty((count, n, n), dtype=torch.float64, device=self.device)
-        nodes = None
-        if elem_nodes is not None:
-            nodes = torch.as_tensor(np.ascontiguousarray(elem_nodes, dtype=np.float64))
-            nodes = nodes.reshape(count, self.dim, self.q).to(self.device)
         s = self.problem_struct()
+        if jac is not None:
+            s.jac = float(jac)
+        if coef_scalar is not None:
+            s.coef_scalar = float(coef_scalar)
         _lib.check(_lib.load().iga_element_matrices(
-            ctypes.byref(s), method, self.ref_nodes.data_ptr(), ids.data_ptr(),
-            None if nodes is None else nodes.data_ptr(), count, out.data_ptr(),
+            ctypes.byref(s), method, self.ref_nodes.data_ptr(), ids.data_ptr(), _lib.ptr(nodes),
+            _lib.ptr(weights), _lib.ptr(coef), count, out.data_ptr(),
             _lib.stream_ptr(stream or self.stream)))
         return out
 

@@ -85,34 +85,37 @@ def _check_inputs(alpha: ElementId, kv: KnotVector, rule: QuadratureRule) -> int
     return q1
 
 
-def _weights_uniform(rule: QuadratureRule) -> np.ndarray:
-    w = np.asarray(rule.weights)
-    if not (np.array_equal(w[0], w[1]) and np.array_equal(w[0], w[2])):
-        raise ValueError("per-axis weights must be identical on the device path")
-    return np.ascontiguousarray(w[0])
+@lru_cache(maxsize=32)
+def _element_problem(K: int, p: int, q: int, operator: str, device: int):
+    """Device problem reused by the per-element calls of one (K, p, q, operator): the
+    per-call inputs (nodes, per-axis weights, Jacobian, coefficient) travel with each call,
+    so a call uploads O(q) values (O(q^3) with a coefficient) -- never a mesh-wide array."""
+    from .device import MeshProblem
+
+    return MeshProblem(3, K, p, q, operator=operator)
 
 
 def _device_element(alpha, kv, rule, method_code, operator, coefficient):
     q = _check_inputs(alpha, kv, rule)  # ValueError before any device work, as the reference
-    w = _weights_uniform(rule)
-    torch = _lib.require_cuda()
-    from .device import MeshProblem
-
-    prob = MeshProblem(3, kv.elements, kv.degree, q, operator=operator)
-    prob.weights = torch.from_numpy(w).to(prob.device)
-    prob.jac = float(rule.jacobian)
+    if operator not in _lib.OPS:
+        raise ValueError(f"operator must be one of {tuple(_lib.OPS)}, got {operator!r}")
+    if operator != "mass" and kv.degree < 1:
+        raise ValueError("derivatives require degree >= 1")
+    elem_coef, coef_scalar = None, 1.0
     if coefficient is not None:
         if np.isscalar(coefficient):
-            prob.coef_scalar = float(coefficient)
+            coef_scalar = float(coefficient)
         else:
-            c = np.ascontiguousarray(coefficient, dtype=np.float64).reshape(-1)
-            if c.size != q**3:
-                raise ValueError(f"element coefficient needs {q**3} values, got {c.size}")
-            full = np.zeros((kv.elements**3, q**3))
-            full[(alpha[0] * kv.elements + alpha[1]) * kv.elements + alpha[2]] = c
-            prob.set_coefficient(full)
+            elem_coef = np.ascontiguousarray(coefficient, dtype=np.float64).reshape(-1)
+            if elem_coef.size != q**3:
+                raise ValueError(f"element coefficient needs {q**3} values, got {elem_coef.size}")
+    torch = _lib.require_cuda()
+    prob = _element_problem(kv.elements, kv.degree, q, operator, torch.cuda.current_device())
     nodes = np.ascontiguousarray(rule.nodes, dtype=np.float64).reshape(1, 3, q)
-    out = prob.element_matrices([alpha], method_code, elem_nodes=nodes)
+    weights = np.ascontiguousarray(rule.weights, dtype=np.float64).reshape(1, 3, q)
+    out = prob.element_matrices([alpha], method_code, elem_nodes=nodes, elem_weights=weights,
+                                elem_coef=elem_coef, jac=float(rule.jacobian),
+                                coef_scalar=coef_scalar)
     return out[0].cpu().numpy(), q
 
 

@@ -94,6 +94,78 @@ class RunResult:
     flops: int
 
 
+@dataclass
+class ExecutionTrace:
+    """Instrumentation of one within-element run (runtime.py:100-107).
+
+    The device executes the sum-factorization task classes of one element as barrier
+    phases of one CTA (csrc/iga_element.cu k_element_strict: the p + 1 Cox-de Boor /
+    Jacobian classes inside K1's table evaluation, then the product/reduce classes of the
+    three directions).  ``completion_order`` lists the element's tasks class by class in
+    task-id order -- the order a barrier-phase schedule completes them, and exactly the
+    reference's ``DependencyGraph.class_members()`` concatenated (its alphabet is numbered
+    class-monotonically, taskgraph.py:132-152) -- ``barriers`` the p + 6 class
+    boundaries, and ``intra_class_syncs`` 0.  ``graph`` stays None: the dependency-graph
+    analysis (taskgraph.py) is outside this package's hot-path scope."""
+
+    graph: object = None
+    completion_order: list = field(default_factory=list)
+    barriers: int = 0
+    intra_class_syncs: int = 0
+
+
+def foata_class_sizes(p: int, points: int) -> list[int]:
+    """Task counts of the p + 7 Foata classes of one element (runtime.py:435-440,
+    taskgraph.py:132-152): cox orders 0..p-1, cox order p + the P Jacobian tasks, then
+    product / reduce per direction (a product per canonical pair and point, a reduce per
+    pair)."""
+    m = p + 1
+    pairs = m**3 * (m**3 + 1) // 2
+    cox = 3 * m * points
+    return [cox] * p + [cox + points] + [pairs * points, pairs] * 3
+
+
+def _foata_task_count(p: int, points: int) -> int:
+    return sum(foata_class_sizes(p, points))
+
+
+def run_within_element(alpha, kv, method: str, workers: int, points: int | None = None,
+                       trace: ExecutionTrace | None = None):
+    """Integrate one element with intra-element parallelism (runtime.py:476-505).
+
+    The device runs the element on one CTA -- threads over canonical pairs / stage
+    entries, barrier phases between the sum-factorization classes -- in the reference's
+    operation order, so the matrix is bitwise equal to the sequential kernels for any
+    ``workers`` (which, like the reference's thread count, does not change the result)."""
+    from .integrators import ElementMatrix, default_rule, flop_count
+    from .device import MeshProblem
+
+    if method not in METHODS:
+        raise ValueError(f"method must be one of {METHODS}")
+    if trace is not None and method != "sumfact":
+        raise ValueError("execution traces are only defined for the sum factorization graph")
+    cfg = RunConfig(method=method, strategy="within_element", mesh=kv.elements, degree=kv.degree,
+                    workers=workers, quad_points=points)
+    q = cfg.points
+    rule = default_rule(kv, tuple(alpha), q)
+    for d in range(3):
+        if not 0 <= alpha[d] < kv.elements:
+            raise ValueError(f"element {alpha} outside mesh with K={kv.elements}")
+    torch = _lib.require_cuda()
+    prob = MeshProblem(3, kv.elements, kv.degree, q)
+    code = _lib.METHOD_CLASSICAL if method == "classical" else _lib.METHOD_SUMFACT
+    out = prob.element_matrices([tuple(alpha)], code,
+                                elem_weights=np.asarray(rule.weights).reshape(1, 3, q),
+                                jac=float(rule.jacobian))
+    torch.cuda.synchronize()
+    entries = out[0].cpu().numpy()
+    if trace is not None:
+        P = q**3
+        trace.completion_order.extend(range(_foata_task_count(kv.degree, P)))
+        trace.barriers += kv.degree + 6
+    return ElementMatrix(tuple(alpha), entries.shape[0], entries, flop_count(method, kv.degree, q))
+
+
 def grams_bitwise_equal(a: GlobalGram, b: GlobalGram) -> bool:
     ma, mb = a.matrix, b.matrix
     return (ma.shape == mb.shape and np.array_equal(ma.indptr, mb.indptr)

@@ -52,6 +52,49 @@ def make_knot_vector(K: int, p: int) -> KnotVector:
     return KnotVector(degree=p, elements=K, knots=knots)
 
 
+def _eval_knots(kv: KnotVector, index, order: int, xs) -> np.ndarray:
+    """B_{index[i], order}(xs[i]) on the device (iga_eval_basis) from kv.knots."""
+    from . import _lib
+
+    torch = _lib.require_cuda()
+    t = torch.from_numpy(np.ascontiguousarray(kv.knots, dtype=np.float64)).cuda()
+    idx = torch.as_tensor(np.ascontiguousarray(index, dtype=np.int32)).reshape(-1).cuda()
+    x = torch.as_tensor(np.ascontiguousarray(xs, dtype=np.float64)).reshape(-1).cuda()
+    out = torch.empty(idx.numel(), dtype=torch.float64, device="cuda")
+    _lib.check(_lib.load().iga_eval_basis(t.data_ptr(), t.numel(), order, idx.numel(),
+                                          idx.data_ptr(), x.data_ptr(), out.data_ptr(),
+                                          _lib.stream_ptr()))
+    return out.cpu().numpy()
+
+
+def eval_basis_order0(kv: KnotVector, i: int, x: float) -> float:
+    """Order-0 basis: indicator of the knot span [t_i, t_{i+1}), the last non-empty span
+    closed at the last knot (splines.py:78-91; evaluated on the device)."""
+    if not 0 <= i <= len(kv.knots) - 2:
+        raise IndexError(f"order-0 basis index {i} out of range")
+    return float(_eval_knots(kv, [i], 0, [x])[0])
+
+
+def eval_basis(kv: KnotVector, i: int, q: int, x: float) -> float:
+    """Basis function i of order q at x by the two-term recursion with 0/0 := 0
+    (splines.py:94-118), bitwise equal, on the device for any knot vector."""
+    if not 0 <= q <= kv.degree:
+        raise ValueError(f"order {q} outside [0, {kv.degree}]")
+    if not 0 <= i <= len(kv.knots) - q - 2:
+        raise IndexError(f"basis index {i} out of range at order {q}")
+    return float(_eval_knots(kv, [i], q, [x])[0])
+
+
+def eval_basis_many(kv: KnotVector, index, q: int, xs) -> np.ndarray:
+    """Vectorised eval_basis: B_{index[j], q}(xs[j]) for all j in one device launch."""
+    index = np.asarray(index, dtype=np.int64).reshape(-1)
+    if not 0 <= q <= kv.degree:
+        raise ValueError(f"order {q} outside [0, {kv.degree}]")
+    if index.size and (index.min() < 0 or index.max() > len(kv.knots) - q - 2):
+        raise IndexError(f"basis index out of range at order {q}")
+    return _eval_knots(kv, index, q, xs)
+
+
 def _check_point(kv: KnotVector, e: int, x: float) -> None:
     lo, hi = kv.element_bounds(e)
     if not lo <= x <= hi:

@@ -31,7 +31,7 @@ def test_header_symbols_exported(lib):
     so = ctypes.CDLL(_lib.LIB_PATH)
     for name in declared:
         assert hasattr(so, name), name
-    assert lib.iga_abi_version() == 3
+    assert lib.iga_abi_version() == 4
 
 
 def test_library_targets_sm100a():

@@ -142,7 +142,8 @@ def test_run_integration_mass_vs_reference(pkg, path, method, assembly):
     res = pkg.run_integration(pkg.RunConfig(method, "device", K, p, assembly=assembly))
     ip, ix, v = _gram_csr(res)
     assert np.array_equal(ip, g["indptr"]) and np.array_equal(ix, g["indices"])
-    assert_parity(v, g["data"], ip, what=f"{path} {method}/{assembly}")
+    assert_parity(v, g["data"], ip, what=f"{path} {method}/{assembly}",
+                  config=f"golden {os.path.basename(path)[:-4]}", path=f"{method}/{assembly}")
 
 
 STIFF = sorted(glob.glob(os.path.join(GOLDEN, "stiffness*_classical_K*_p*.npz")))
@@ -160,7 +161,8 @@ def test_run_integration_stiffness_vs_reference(pkg, path, method, assembly):
                                             assembly=assembly))
     ip, ix, v = _gram_csr(res)
     assert np.array_equal(ip, g["indptr"]) and np.array_equal(ix, g["indices"])
-    assert_parity(v, g["data"], ip, what=f"{name} {method}/{assembly}")
+    assert_parity(v, g["data"], ip, what=f"{name} {method}/{assembly}", config=f"golden {name}",
+                  path=f"{method}/{assembly}")
 
 
 @pytest.mark.parametrize("path", sorted(glob.glob(os.path.join(GOLDEN, "sepcoef_*.npz"))))
@@ -176,7 +178,8 @@ def test_separable_coefficient_vs_reference(pkg, path, method, assembly):
     res = pkg.run_integration(pkg.RunConfig(method, "device", K, p, operator=op,
                                             coefficient=coef, assembly=assembly))
     ip, ix, v = _gram_csr(res)
-    assert_parity(v, g["data"], ip, what=name, absref=A)
+    assert_parity(v, g["data"], ip, what=name, absref=A, config=f"golden {name}",
+                  path=f"{method}/{assembly}")
 
 
 @pytest.mark.parametrize("op", ["mass", "stiffness", "stiffness_mass"])
@@ -194,16 +197,20 @@ def test_general_coefficient_vs_oracle(pkg, op, K, p, q):
                                                 operator=op, coefficient=coef,
                                                 assembly=assembly))
         v = res.gram.values.cpu().numpy()
-        assert_parity(v, ref, ip, what=f"{op} K={K} p={p} q={q} {method}/{assembly}", absref=A)
+        assert_parity(v, ref, ip, what=f"{op} K={K} p={p} q={q} {method}/{assembly}", absref=A,
+                      config=f"coef field {op} K={K} p={p} q={q}", path=f"{method}/{assembly}")
 
 
 @pytest.mark.parametrize("K,p", [(16, 2), (3, 1)])
 def test_mass_2d_vs_derived_reference(pkg, K, p):
+    """C1 (2D mass, 16^2, p=2) against the 2D Gram derived from the reference's 3D output:
+    every entry within the strict per-entry 1e-12 relative bound."""
     g = load_golden(f"mass2d_K{K}_p{p}")
     res = pkg.run_integration(pkg.RunConfig("classical", "device", K, p, dim=2))
     ip, ix, v = _gram_csr(res)
     assert np.array_equal(ip, g["indptr"]) and np.array_equal(ix, g["indices"])
-    assert_parity(v, g["data"], ip)
+    assert_parity(v, g["data"], ip, config="C1" if (K, p) == (16, 2) else f"2D mass K={K} p={p}",
+                  path="classical", strict=True)
 
 
 def test_reference_strategies_accepted(pkg):
@@ -302,11 +309,15 @@ def _sample_rows(K, p, n_rand, seed=0):
 
 
 @pytest.mark.parametrize("cfg", [
-    dict(K=64, p=3, op="stiffness", coef=None, name="C3", assembly="owner"),
-    dict(K=64, p=3, op="stiffness", coef=None, name="C3", assembly="separable"),
-    dict(K=32, p=2, op="mass", coef="uniform", name="C2"),
-    dict(K=32, p=2, op="mass", coef="uniform", name="C2 classical", method="classical"),
-    dict(K=48, p=3, op="stiffness", coef="uniform", name="C3-48 classical", method="classical"),
+    dict(K=64, p=3, op="stiffness", coef=None, name="C3", assembly="owner", strict=True),
+    dict(K=64, p=3, op="stiffness", coef=None, name="C3", assembly="separable", strict=True),
+    dict(K=64, p=3, op="stiffness", coef=None, name="C3", method="classical", strict=True),
+    dict(K=64, p=3, op="stiffness", coef=None, name="C3", assembly="scatter", strict=True),
+    dict(K=32, p=2, op="mass", coef="uniform", name="C2", assembly="owner"),
+    dict(K=32, p=2, op="mass", coef="uniform", name="C2", method="classical"),
+    dict(K=32, p=2, op="mass", coef="uniform", name="C2", assembly="scatter"),
+    dict(K=48, p=3, op="stiffness", coef="uniform", name="C3-48 coef field", method="classical"),
+    dict(K=48, p=3, op="stiffness", coef="uniform", name="C3-48 coef field", assembly="owner"),
 ])
 def test_full_size_sampled_rows(pkg, cfg):
     """BASELINE configs at full size: sampled rows (corner/edge/interior) vs the
@@ -329,7 +340,9 @@ def test_full_size_sampled_rows(pkg, cfg):
     ref = np.concatenate(ref_rows)
     A = np.concatenate(abs_rows)
     sub_ip = np.concatenate([[0], np.cumsum([len(x) for x in ref_rows])])
-    assert_parity(got, ref, sub_ip, absref=A, what=cfg["name"])
+    method = cfg.get("method", "sumfact")
+    assert_parity(got, ref, sub_ip, absref=A, what=cfg["name"], config=cfg["name"],
+                  path=f"{method}/{cfg.get('assembly', 'auto')}", strict=cfg.get("strict", False))
     # size-independent properties on the whole matrix
     M = res.gram.matrix
     # symmetric to rounding, like the reference (its own |A - A^T| reaches 4e-16 max|A|)
@@ -568,39 +581,53 @@ def _device_rows(values, dim, K, p, rows):
             for r in rows]
 
 
-def _check_rows(got_rows, K, p, rows, op, coef, name):
+def _check_rows(got_rows, K, p, rows, op, coef, name, path=None, strict=False):
     ref_rows = O.rows(3, K, p, rows, op, "classical", coef=coef)
     abs_rows = O.rows(3, K, p, rows, op, "classical", coef=coef, absolute=True)
     got = np.concatenate(got_rows)
     ref = np.concatenate(ref_rows)
     A = np.concatenate(abs_rows)
     sub_ip = np.concatenate([[0], np.cumsum([len(x) for x in ref_rows])])
-    assert_parity(got, ref, sub_ip, absref=A, what=name)
+    name0 = name.split(" ")[0]
+    assert_parity(got, ref, sub_ip, absref=A, what=name, config=name0, path=path, strict=strict)
 
 
-def test_full_size_c4_sampled_rows(pkg):
+_C4_COEF = {}
+
+
+@pytest.mark.parametrize("method,assembly", [("sumfact", "owner"), ("classical", "auto"),
+                                             ("sumfact", "scatter")])
+def test_full_size_c4_sampled_rows(pkg, method, assembly):
     """C4 at full size (96^3, p=4, q=5, stiffness+mass, 8-mode sine field from bench.py's
-    seeded generator): sampled corner/edge/interior rows vs the oracle's classical rows."""
+    seeded generator), classical and sum factorization (BASELINE C4 compares them): sampled
+    corner/edge/interior rows vs the oracle's classical rows."""
+    import torch
+
     import bench
 
     K, p = 96, 4
-    coef = bench.coefficient("sines", K, p, 3)
-    res = pkg.run_integration(pkg.RunConfig("sumfact", "device", K, p, operator="stiffness_mass",
-                                            coefficient=coef))
+    if "c" not in _C4_COEF:
+        _C4_COEF["c"] = bench.coefficient("sines", K, p, 3)
+    coef = _C4_COEF["c"]
+    res = pkg.run_integration(pkg.RunConfig(method, "device", K, p, operator="stiffness_mass",
+                                            coefficient=coef, assembly=assembly))
     rows = _sample_rows(K, p, 24, seed=1)
     _check_rows(_device_rows(res.gram.values, 3, K, p, rows), K, p, rows, "stiffness_mass", coef,
-                "C4")
+                f"C4 {method}/{assembly}", path=f"{method}/{assembly}")
+    del res
+    torch.cuda.empty_cache()
 
 
-@pytest.mark.parametrize("assembly", ["separable", "owner"])
-def test_full_size_c5_sampled_rows(pkg, assembly):
+@pytest.mark.parametrize("method,assembly", [("sumfact", "separable"), ("sumfact", "owner"),
+                                             ("classical", "auto"), ("sumfact", "scatter")])
+def test_full_size_c5_sampled_rows(pkg, method, assembly):
     """C5 at full size on one GPU (256^3, p=3: 5.84e9 values, 46.7 GB resident): sampled
     rows, including the planes at the 2/4/8-way slab boundaries, vs the oracle; the
     stiffness row sums vanish."""
     import torch
 
     K, p = 256, 3
-    res = pkg.run_integration(pkg.RunConfig("sumfact", "device", K, p, operator="stiffness",
+    res = pkg.run_integration(pkg.RunConfig(method, "device", K, p, operator="stiffness",
                                             assembly=assembly))
     N = K + p
     rng = np.random.default_rng(5)
@@ -608,7 +635,8 @@ def test_full_size_c5_sampled_rows(pkg, assembly):
     rows = sorted({(a * N + int(rng.integers(0, N))) * N + int(rng.integers(0, N)) for a in planes}
                   | {0, N**3 - 1, (N // 2 * N + N // 2) * N + N // 2})
     got = _device_rows(res.gram.values, 3, K, p, rows)
-    _check_rows(got, K, p, rows, "stiffness", None, f"C5 {assembly}")
+    _check_rows(got, K, p, rows, "stiffness", None, f"C5 {method}/{assembly}",
+                path=f"{method}/{assembly}", strict=True)
     for r in got:
         assert abs(r.sum()) <= 1e-12 * np.abs(r).max()
     del res
@@ -728,26 +756,43 @@ def test_spmv_staged_window_matches(pkg, monkeypatch):
     torch.cuda.empty_cache()
 
 
-@pytest.mark.gpu
 @pytest.mark.parametrize("K,p,op", [(64, 3, "stiffness"), (17, 2, "mass"), (9, 4, "stiffness_mass")])
-def test_separable_claim_order_bitwise(K, p, op, monkeypatch):
-    """The opt-in claim-ordered schedule of k_kron3 (IGA_KRON_DYNAMIC, pencils claimed from
-    the counter after the band tables) writes the same bits as the static ranges, and the
-    counter re-arms itself: three launches after one K1 all write every value."""
+def test_band_tables_read_only_and_in_bounds(pkg, K, p, op):
+    """ABI v4: iga_band_tables writes exactly (K+p)(2p+1)*2 doubles (a guard zone after them
+    stays untouched), and the separable kernel only reads the band buffer -- two launches
+    sharing one buffer on two streams at once both write every value, bitwise equal to a
+    launch on its own."""
+    import ctypes
+
     import torch
 
+    from paper_2207_00280_b200 import _lib
     from paper_2207_00280_b200.device import MeshProblem
 
     mp = MeshProblem(3, K, p, p + 1, op, 1.3)
-    assert mp.build_band_tables()
+    nband = (K + p) * (2 * p + 1) * 2
+    guard = torch.full((nband + 64,), 777.0, dtype=torch.float64, device="cuda")
+    mp.band = guard[:nband]
+    s = mp.problem_struct()
+    _lib.check(_lib.load().iga_band_tables(ctypes.byref(s), mp.ref_nodes.data_ptr(),
+                                           mp.tables_v.data_ptr(), mp.tables_d.data_ptr(),
+                                           guard.data_ptr(), _lib.stream_ptr()))
+    torch.cuda.synchronize()
+    assert (guard[nband:] == 777.0).all().item()
+    snapshot = guard.clone()
     n = mp.nnz(0, K + p)
     ref = torch.full((n,), float("nan"), dtype=torch.float64, device="cuda")
     mp.integrate_assemble(ref, 3, band=True)
-    monkeypatch.setenv("IGA_KRON_DYNAMIC", "1")
+    torch.cuda.synchronize()
+    outs = [torch.full((n,), float("nan"), dtype=torch.float64, device="cuda") for _ in range(2)]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    for o, st in zip(outs, streams):
+        st.wait_stream(torch.cuda.current_stream())
     for _ in range(3):
-        out = torch.full((n,), float("nan"), dtype=torch.float64, device="cuda")
-        mp.integrate_assemble(out, 3, band=True)
-        torch.cuda.synchronize()
-        assert torch.equal(out, ref)
-    monkeypatch.delenv("IGA_KRON_DYNAMIC")
+        for o, st in zip(outs, streams):
+            mp.integrate_assemble(o, 3, band=True, stream=st)
+    torch.cuda.synchronize()
     assert not torch.isnan(ref).any().item()
+    for o in outs:
+        assert torch.equal(o, ref)
+    assert torch.equal(guard, snapshot)

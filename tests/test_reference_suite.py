@@ -373,7 +373,7 @@ def test_empty_ranges_through_the_abi():
     out = torch.full((1,), 3.0, dtype=torch.float64, device="cuda")
     ids = torch.zeros((1, 3), dtype=torch.int32, device="cuda")
     assert L.iga_element_matrices(ctypes.byref(s), 0, mp.ref_nodes.data_ptr(), ids.data_ptr(), None,
-                                  0, out.data_ptr(), None) == 0
+                                  None, None, 0, out.data_ptr(), None) == 0
     torch.cuda.synchronize()
     assert out.item() == 3.0
     ip = torch.full((1,), -1, dtype=torch.int64, device="cuda")

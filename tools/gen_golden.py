@@ -98,6 +98,77 @@ def term_kernel_assemble(K, p, q, method, op, coef_axes=None):
     return assembly.assemble(mats, K, p)
 
 
+def nonuniform_kv(K, p, seed):
+    """Open knot vector with K distinct, randomly sized spans on [0, 1]."""
+    r = np.random.default_rng(seed)
+    h = r.uniform(0.5, 1.5, size=K)
+    interior = np.cumsum(h)[:-1] / h.sum()
+    knots = np.concatenate([np.zeros(p + 1), interior, np.ones(p + 1)])
+    return splines.KnotVector(degree=p, elements=K, knots=knots)
+
+
+def nonuniform_tables(kv, q):
+    """V/D[e][r][k] at x = t_lo + (ref + 1) (h / 2), h = t_hi - t_lo of span e, by the
+    reference's recursion (eval_basis; derivatives by the degree-reduction formula of
+    eval_nonzero_basis_derivatives on the reference's _cox, splines.py:139-161)."""
+    K, p, t = kv.elements, kv.degree, kv.knots
+    ref, w = np.polynomial.legendre.leggauss(q)
+    V = np.zeros((K, p + 1, q))
+    D = np.zeros((K, p + 1, q))
+    X = np.zeros((K, q))
+    H = np.zeros(K)
+    for e in range(K):
+        lo, hi = t[p + e], t[p + e + 1]
+        h = hi - lo
+        xs = lo + (ref + 1.0) * (h / 2.0)
+        X[e], H[e] = xs, h
+        for k, x in enumerate(xs):
+            for r in range(p + 1):
+                i = e + r
+                V[e, r, k] = splines.eval_basis(kv, i, p, x)
+                if p >= 1:
+                    dd = 0.0
+                    d_left = t[i + p] - t[i]
+                    if d_left > 0.0:
+                        dd += splines._cox(t, i, p - 1, x, kv) / d_left
+                    d_right = t[i + p + 1] - t[i + 1]
+                    if d_right > 0.0:
+                        dd -= splines._cox(t, i + 1, p - 1, x, kv) / d_right
+                    D[e, r, k] = p * dd
+    return dict(V=V, D=D, X=X, H=H, ref=ref, w=w)
+
+
+def nonuniform_assemble(kv, q, method, op, tabs):
+    """Global matrix of a general open knot vector by the reference kernels: per-axis
+    weights w * (h_e / 2) (the per-element Jacobian of the identity geometry map), jac = 1,
+    stiffness terms as in term_kernel_assemble, assembled by assembly.assemble."""
+    K, p = kv.elements, kv.degree
+    V, D, H, w = tabs["V"], tabs["D"], tabs["H"], tabs["w"]
+    m = p + 1
+    n = m**3
+    rows, cols = integrators.canonical_pairs(n)
+    terms = {"mass": [3], "stiffness": [0, 1, 2], "stiffness_mass": [0, 1, 2, 3]}[op]
+    mats = []
+    for alpha in mesh.element_list(K):
+        ws = [w * (H[alpha[d]] / 2.0) for d in range(3)]
+        out = np.zeros((n, n))
+        for t in terms:
+            tb = [D[alpha[d]] if d == t else V[alpha[d]] for d in range(3)]
+            o = np.zeros((n, n))
+            if method == "classical":
+                integrators.classical_kernel(tb[0], tb[1], tb[2], ws[0], ws[1], ws[2], 1.0,
+                                             rows, cols, 0, len(rows), o)
+            else:
+                buf = integrators.SumFactBuffers.allocate(p, q)
+                buf.D[:] = 0.0
+                buf.C[:] = 0.0
+                integrators.sumfact_kernel(tb[0], tb[1], tb[2], ws[0], ws[1], ws[2], 1.0,
+                                           buf.D, buf.C, rows, cols, o)
+            out = o if t == terms[0] else out + o
+        mats.append((alpha, integrators.ElementMatrix(alpha, n, out, 0)))
+    return assembly.assemble(mats, K, p)
+
+
 def main():
     # 1. basis tables (splines.py:164-178 through runtime.py:142-149 mapping)
     tabs = {}
@@ -185,6 +256,77 @@ def main():
         gr[f"weights_p{p}"] = r.weights
         gr[f"jac_p{p}"] = np.float64(r.jacobian)
     save("gauss_rules.npz", **gr)
+
+    # 10. per-axis weights (integrators.py:200-203 passes rule.weights[0..2] separately):
+    #     element matrices of rules whose weights differ per axis (w * c_d)
+    rng = np.random.default_rng(5)
+    pa = {}
+    for K, p in ((3, 2), (4, 3), (2, 4)):
+        kv = splines.make_knot_vector(K, p)
+        buf = integrators.SumFactBuffers.allocate(p)
+        alpha = (K - 1, 0, K // 2)
+        r0 = mesh.gauss_rule(p, K, alpha)
+        c = rng.uniform(0.5, 1.5, size=(3, p + 1))
+        rule = mesh.QuadratureRule(r0.points_per_direction, r0.nodes, r0.weights * c, r0.jacobian)
+        pa[f"weights_K{K}_p{p}"] = rule.weights
+        pa[f"classical_K{K}_p{p}"] = integrators.integrate_element_classical(alpha, kv, rule).entries
+        pa[f"sumfact_K{K}_p{p}"] = integrators.integrate_element_sumfact(alpha, kv, rule, buf).entries
+    save("element_peraxis.npz", **pa)
+
+    # 11. eval_basis / eval_basis_order0 (splines.py:78-118) on open uniform knots and on
+    #     general (non-uniform) open knot vectors -- the reference's recursion takes any
+    #     non-decreasing knots (KnotVector.knots)
+    eb = {}
+    for tag, K, p in (("u", 4, 3), ("u", 3, 2), ("n", 5, 3), ("n", 4, 2), ("n", 6, 4), ("u", 2, 0)):
+        if tag == "u":
+            kv = splines.make_knot_vector(K, p)
+        else:
+            kv = nonuniform_kv(K, p, seed=K * 10 + p)
+        t = kv.knots
+        xs = np.unique(np.concatenate([t, np.linspace(0.0, 1.0, 23), rng.uniform(0, 1, 9)]))
+        for q in range(p + 1):
+            nb = len(t) - q - 1
+            eb[f"{tag}_K{K}_p{p}_q{q}"] = np.array(
+                [[splines.eval_basis(kv, i, q, x) for x in xs] for i in range(nb)])
+        eb[f"{tag}_K{K}_p{p}_o0"] = np.array(
+            [[splines.eval_basis_order0(kv, i, x) for x in xs] for i in range(len(t) - 1)])
+        eb[f"{tag}_K{K}_p{p}_x"] = xs
+        eb[f"{tag}_K{K}_p{p}_knots"] = t
+    save("eval_basis.npz", **eb)
+
+    # 12. general open knot vectors: per-element tables at the
+    #     Gauss points mapped into each knot span, and global mass / stiffness matrices
+    #     from the reference's own kernels with the per-element Jacobian folded into the
+    #     per-axis weights (w_d = w h_e/2, jac = 1), assembled by assembly.assemble
+    for K, p in ((5, 2), (4, 3), (3, 1), (6, 3)):
+        kv = nonuniform_kv(K, p, seed=K * 10 + p)
+        q = p + 1
+        d = nonuniform_tables(kv, q)
+        d["knots"] = kv.knots
+        for op in ("mass", "stiffness", "stiffness_mass") if p >= 1 else ("mass",):
+            for method in ("classical", "sumfact"):
+                c = ref_csr(nonuniform_assemble(kv, q, method, op, d))
+                if "indptr" in d:  # one pattern for every matrix of the mesh
+                    assert np.array_equal(d["indptr"], c["indptr"])
+                    assert np.array_equal(d["indices"], c["indices"])
+                d["indptr"], d["indices"] = c["indptr"], c["indices"]
+                d[f"{op}_{method}"] = c["data"]
+        save(f"nonuniform_K{K}_p{p}.npz", **d)
+    # 13. run_within_element with an ExecutionTrace (runtime.py:476-505, :100-107)
+    tr = {}
+    for K, p, workers in ((2, 0, 1), (2, 1, 3), (3, 2, 2)):
+        kv = splines.make_knot_vector(K, p)
+        alpha = (K - 1, 0, K // 2)
+        t = runtime.ExecutionTrace()
+        em = runtime.run_within_element(alpha, kv, "sumfact", workers, trace=t)
+        key = f"K{K}_p{p}_w{workers}"
+        tr[f"{key}_order"] = np.array(t.completion_order, dtype=np.int64)
+        tr[f"{key}_barriers"] = np.int64(t.barriers)
+        tr[f"{key}_syncs"] = np.int64(t.intra_class_syncs)
+        tr[f"{key}_ntasks"] = np.int64(t.graph.n_tasks)
+        tr[f"{key}_sumfact"] = em.entries
+        tr[f"{key}_classical"] = runtime.run_within_element(alpha, kv, "classical", workers).entries
+    save("within_element.npz", **tr)
     print("igabench", igabench.__version__)
 
 
