@@ -54,10 +54,34 @@ class GlobalGram:
     Fields match the reference dataclass (assembly.py:28-38): K, p, n_dofs, matrix.
     """
 
-    def __init__(self, K: int, p: int, n_dofs: int, values=None, dim: int = 3, matrix=None):
+    def __init__(self, K: int, p: int, n_dofs: int, values=None, dim: int = 3, matrix=None,
+                 shards=None):
         self.K, self.p, self.n_dofs, self.dim = K, p, n_dofs, dim
-        self.values = values  # torch fp64 on the device, CSR order
+        self._values = values  # torch fp64 on the device, CSR order
+        # multi-device result: the owned CSR value ranges of consecutive row slabs, one
+        # tensor per device (concatenated in row order they are the whole CSR)
+        self.shards = shards
         self._matrix = matrix
+
+    @property
+    def values(self):
+        """Device CSR values; for a multi-device result the shards are gathered onto the
+        first shard's device on first access."""
+        if self._values is None and self.shards is not None:
+            import torch
+
+            dev = self.shards[0].device
+            self._values = torch.cat([s.to(dev) for s in self.shards])
+        return self._values
+
+    @values.setter
+    def values(self, v):
+        self._values = v
+
+    def host_values(self) -> np.ndarray:
+        if self._values is None and self.shards is not None:
+            return np.concatenate([s.cpu().numpy() for s in self.shards])
+        return self.values.cpu().numpy()
 
     @property
     def matrix(self):
@@ -65,7 +89,7 @@ class GlobalGram:
             import scipy.sparse
 
             indptr, indices = host_pattern(self.dim, self.K, self.p)
-            data = self.values.cpu().numpy()
+            data = self.host_values()
             self._matrix = scipy.sparse.csr_matrix((data, indices, indptr),
                                                    shape=(self.n_dofs, self.n_dofs))
             self._matrix.has_sorted_indices = True

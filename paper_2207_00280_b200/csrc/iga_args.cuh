@@ -31,6 +31,12 @@ struct ScatterArgs {
   const double* V;  // [K][m][Q]
   const double* D;  // [K][m][Q] or null (mass)
   double* values;
+  // element colour of this launch: the elements e with e_d = c_d (mod p+1) -- a colour's
+  // elements share no dof, so each value receives at most one contribution per launch and
+  // the colours, launched in a fixed order, fix the summation order (no atomics)
+  int first0;                     // smallest e0 in [el_begin, el_end) of the colour
+  int c1, c2;                     // colour along axes 1, 2 (2D: c1 only)
+  int n0, n1, n2;                 // colour elements per axis (2D: n2 = 1)
 };
 
 struct GsfArgs {

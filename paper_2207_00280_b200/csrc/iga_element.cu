@@ -8,10 +8,10 @@
 //    order (oracle/iga_oracle.c orc_element defines the same order).
 //  * k_classical_scatter -- Algorithm 1 mesh-wide: grid over elements, warps
 //    over canonical pairs, lanes over quadrature points, warp-shuffle
-//    reduction, fused atomic scatter into the structured CSR.
+//    reduction, fused scatter into the structured CSR (by element colour).
 //  * k_sumfact_scatter -- Algorithm 2 element-local, stages in shared memory
 //    (Foata classes p+1..p+6 of taskgraph.py:204-223 -> barrier phases),
-//    fused atomic scatter.
+//    fused scatter (by element colour).
 #include "iga_args.cuh"
 #include "iga_dispatch.cuh"
 

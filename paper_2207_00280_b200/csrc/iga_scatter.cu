@@ -1,4 +1,9 @@
-// Element-local mesh-wide kernels with fused atomic scatter (see iga_element.cu header).
+// Element-local mesh-wide kernels with a fused, deterministic scatter (see iga_element.cu
+// header).  The elements are launched by colour (e_d mod (p+1), (p+1)^dim launches in a fixed
+// order): elements of one colour share no dof, so every CSR value receives at most one
+// contribution per launch, added with a plain read-modify-write -- the summation order is
+// the colour order whatever the schedule, and two runs give the same bits (the reference
+// promises bitwise-identical matrices for every schedule, runtime.py:16-20).
 //
 //  * k_element_strict  -- per-element matrices with the reference's exact
 //    operation order (strict IEEE via __dmul_rn/__dadd_rn): classical =
@@ -8,10 +13,10 @@
 //    order (oracle/iga_oracle.c orc_element defines the same order).
 //  * k_classical_scatter -- Algorithm 1 mesh-wide: grid over elements, warps
 //    over canonical pairs, lanes over quadrature points, warp-shuffle
-//    reduction, fused atomic scatter into the structured CSR.
+//    reduction, fused scatter into the structured CSR (by element colour).
 //  * k_sumfact_scatter -- Algorithm 2 element-local, stages in shared memory
 //    (Foata classes p+1..p+6 of taskgraph.py:204-223 -> barrier phases),
-//    fused atomic scatter.
+//    fused scatter (by element colour).
 #include <cstdlib>
 
 #include "iga_args.cuh"
@@ -20,6 +25,23 @@
 namespace iga {
 
 // --------------------------------------------------------- fused scatter
+// Element `el` of the launch's colour (elements lexicographic within the colour).
+__device__ __forceinline__ void colour_element(const ScatterArgs& a, int64_t el, int m, int dim,
+                                               int* alpha) {
+  if (dim == 3) {
+    const int i2 = (int)(el % a.n2), i1 = (int)((el / a.n2) % a.n1);
+    const int i0 = (int)(el / ((int64_t)a.n1 * a.n2));
+    alpha[0] = a.first0 + m * i0;
+    alpha[1] = a.c1 + m * i1;
+    alpha[2] = a.c2 + m * i2;
+  } else {
+    const int i1 = (int)(el % a.n1), i0 = (int)(el / a.n1);
+    alpha[0] = a.first0 + m * i0;
+    alpha[1] = a.c1 + m * i1;
+    alpha[2] = 0;
+  }
+}
+
 __device__ __forceinline__ void scatter_add(const ScatterArgs& a, int P, int64_t N,
                                             const int64_t* I, const int64_t* J, double v) {
   int64_t row;
@@ -33,7 +55,7 @@ __device__ __forceinline__ void scatter_add(const ScatterArgs& a, int P, int64_t
     off = rowptr2(I[0], I[1], P, N) + (J[0] - band_lo(I[0], P)) * band_cnt(I[1], P, N) +
           (J[1] - band_lo(I[1], P));
   }
-  atomicAdd(a.values + (off - a.base), v);
+  a.values[off - a.base] += v;  // one contribution per value per colour launch
 }
 
 // Algorithm 1 over the mesh.  One CTA per element (grid-stride), 8 warps over
@@ -48,22 +70,13 @@ __global__ void __launch_bounds__(256) k_classical_scatter(ScatterArgs a) {
   constexpr int npairs = n * (n + 1) / 2;
   __shared__ double sV[3][m][Q], sD[3][m][Q], sW[nq];
   const int64_t N = (int64_t)a.K + P;
-  const int Kb = DIM == 3 ? a.K : 1;
-  const int64_t n_el = (int64_t)(a.el_end - a.el_begin) * a.K * Kb;
+  const int64_t n_el = (int64_t)a.n0 * a.n1 * a.n2;
   const bool stiff = a.op != IGA_OP_MASS;
   const bool with_mass = a.op != IGA_OP_STIFFNESS;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int64_t el = blockIdx.x; el < n_el; el += gridDim.x) {
     int alpha[3];
-    if (DIM == 3) {
-      alpha[2] = (int)(el % a.K);
-      alpha[1] = (int)((el / a.K) % a.K);
-      alpha[0] = a.el_begin + (int)(el / ((int64_t)a.K * a.K));
-    } else {
-      alpha[2] = 0;
-      alpha[1] = (int)(el % a.K);
-      alpha[0] = a.el_begin + (int)(el / a.K);
-    }
+    colour_element(a, el, m, DIM, alpha);
     __syncthreads();
     for (int t = threadIdx.x; t < DIM * m * Q; t += blockDim.x) {
       const int d = t / (m * Q), rk = t % (m * Q);
@@ -142,7 +155,7 @@ __global__ void __launch_bounds__(256) k_classical_scatter(ScatterArgs a) {
 // lower triangle, so each element matrix is exactly symmetric like the
 // reference's (integrators.py:5 fills the mirror of each canonical pair, and
 // assembly.py:71-79 adds all n^2 entries of the symmetric element matrix); the
-// atomic inter-element order makes the assembled matrix symmetric to rounding.
+// inter-element (colour) order makes the assembled matrix symmetric to rounding.
 // Column slots come from per-element tables (row offset into the CSR window,
 // per-axis band shifts and counts) instead of per-entry int64 index math.
 __device__ __forceinline__ void dmma_acc(double& d0, double& d1, double a, double b) {
@@ -167,16 +180,14 @@ __global__ void __launch_bounds__(256) k_classical_mma(ScatterArgs a) {
   __shared__ int64_t s_rowoff[n];  // CSR offset of local row i (relative to a.base), -1: not owned
   __shared__ int s_shift[3][m], s_cnt[3][m];
   const int64_t N = (int64_t)a.K + P;
-  const int64_t n_el = (int64_t)(a.el_end - a.el_begin) * a.K * a.K;
+  const int64_t n_el = (int64_t)a.n0 * a.n1 * a.n2;
   const bool stiff = a.op != IGA_OP_MASS;
   const bool with_mass = a.op != IGA_OP_STIFFNESS;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, tq = lane & 3;
   for (int64_t el = blockIdx.x; el < n_el; el += gridDim.x) {
     int alpha[3];
-    alpha[2] = (int)(el % a.K);
-    alpha[1] = (int)((el / a.K) % a.K);
-    alpha[0] = a.el_begin + (int)(el / ((int64_t)a.K * a.K));
+    colour_element(a, el, m, 3, alpha);
     __syncthreads();
     for (int t = threadIdx.x; t < 3 * m * Q; t += blockDim.x) {
       const int d = t / (m * Q), rk = t % (m * Q);
@@ -278,13 +289,13 @@ __global__ void __launch_bounds__(256) k_classical_mma(ScatterArgs a) {
             if (off_i >= 0) {
               const int slot = ((j0 + s_shift[0][i0]) * s_cnt[1][i1] + j1 + s_shift[1][i1]) * s_cnt[2][i2] +
                                j2 + s_shift[2][i2];
-              atomicAdd(a.values + off_i + slot, v);
+              a.values[off_i + slot] += v;
             }
             const int64_t off_j = s_rowoff[j];
             if (j != i && off_j >= 0) {
               const int slot = ((i0 + s_shift[0][j0]) * s_cnt[1][j1] + i1 + s_shift[1][j1]) * s_cnt[2][j2] +
                                i2 + s_shift[2][j2];
-              atomicAdd(a.values + off_j + slot, v);
+              a.values[off_j + slot] += v;
             }
           }
         }
@@ -293,7 +304,7 @@ __global__ void __launch_bounds__(256) k_classical_mma(ScatterArgs a) {
   }
 }
 
-// Algorithm 2 element-local, merged stiffness form, fused atomic scatter.
+// Algorithm 2 element-local, merged stiffness form, fused scatter (by element colour).
 //   X_T[i1][j1][k2][k3] = sum_k1 T_i1 T_j1 W             (T in {V, D})
 //   Y_A[i2 i1 j2 j1][k3] = sum_k2 X_D VV + X_V DD,  Y_B = sum_k2 X_V VV
 //   S[pair] = sum_k3 Y_A VV3 + Y_B Z3  (Z3 = DD3, + VV3 for stiffness+mass)
@@ -313,13 +324,11 @@ __global__ void __launch_bounds__(256) k_sumfact_scatter(ScatterArgs a) {
   double* YA = XD + nX;
   double* YB = YA + nY;
   const int64_t N = (int64_t)a.K + P;
-  const int64_t n_el = (int64_t)(a.el_end - a.el_begin) * a.K * a.K;
+  const int64_t n_el = (int64_t)a.n0 * a.n1 * a.n2;
   const int op = a.op;
   for (int64_t el = blockIdx.x; el < n_el; el += gridDim.x) {
     int alpha[3];
-    alpha[2] = (int)(el % a.K);
-    alpha[1] = (int)((el / a.K) % a.K);
-    alpha[0] = a.el_begin + (int)(el / ((int64_t)a.K * a.K));
+    colour_element(a, el, m, 3, alpha);
     __syncthreads();
     for (int t = threadIdx.x; t < 3 * m * Q; t += blockDim.x) {
       const int d = t / (m * Q), rk = t % (m * Q);
@@ -401,15 +410,14 @@ __global__ void __launch_bounds__(256) k_sumfact_scatter(ScatterArgs a) {
 
 template <int P, int Q>
 struct ScatterLaunch {
-  static int run(const ScatterArgs& a, int method, cudaStream_t s) {
-    const int64_t Kb = a.dim == 3 ? a.K : 1;
-    const int64_t n_el = (int64_t)(a.el_end - a.el_begin) * a.K * Kb;
+  static int launch_colour(const ScatterArgs& a, int method, size_t shm, cudaStream_t s) {
+    const int64_t n_el = (int64_t)a.n0 * a.n1 * a.n2;
     if (n_el <= 0) return IGA_OK;
-    int64_t grid = n_el < 148 * 64 ? n_el : 148 * 64;
+    const int64_t grid = n_el < 148 * 64 ? n_el : 148 * 64;
     if (method == IGA_METHOD_CLASSICAL) {
       static const bool scalar = [] {
         const char* e = getenv("IGA_CLASSICAL_SCALAR");
-        return e && e[0] == '1';
+        return e && e[0] == '1' && e[1] == 0;
       }();
       if (a.dim == 3 && !scalar)
         k_classical_mma<P, Q><<<(unsigned)grid, 256, 0, s>>>(a);
@@ -418,17 +426,41 @@ struct ScatterLaunch {
       else
         k_classical_scatter<2, P, Q><<<(unsigned)grid, 256, 0, s>>>(a);
     } else {
-      if (a.dim != 3) return fail_einval("element-local sum factorization scatter is 3D only");
-      constexpr int m = P + 1;
-      const size_t shm = sizeof(double) * (6 * m * Q + Q * Q * Q + 2 * m * m * Q * Q +
-                                           2 * m * m * m * m * Q);
+      k_sumfact_scatter<P, Q><<<(unsigned)grid, 256, shm, s>>>(a);
+    }
+    return check_cuda(cudaGetLastError(), "scatter launch");
+  }
+
+  static int run(const ScatterArgs& a0, int method, cudaStream_t s) {
+    constexpr int m = P + 1;
+    if (a0.el_end <= a0.el_begin) return IGA_OK;
+    size_t shm = 0;
+    if (method != IGA_METHOD_CLASSICAL) {
+      if (a0.dim != 3) return fail_einval("element-local sum factorization scatter is 3D only");
+      shm = sizeof(double) * (6 * m * Q + Q * Q * Q + 2 * m * m * Q * Q + 2 * m * m * m * m * Q);
       if (shm > 48 * 1024) {
         cudaError_t e = smem_attr_once(reinterpret_cast<const void*>(k_sumfact_scatter<P, Q>), shm);
         if (e != cudaSuccess) return check_cuda(e, "sumfact smem attr");
       }
-      k_sumfact_scatter<P, Q><<<(unsigned)grid, 256, shm, s>>>(a);
     }
-    return check_cuda(cudaGetLastError(), "scatter launch");
+    auto count = [](int lo, int hi, int c) {  // e in [lo, hi) with e = c (mod m)
+      const int first = lo + ((c - lo % m) % m + m) % m;
+      return first >= hi ? 0 : (hi - 1 - first) / m + 1;
+    };
+    const int colours = a0.dim == 3 ? m * m * m : m * m;
+    for (int col = 0; col < colours; ++col) {  // fixed colour order = fixed summation order
+      ScatterArgs a = a0;
+      const int c0 = a0.dim == 3 ? col / (m * m) : col / m;
+      a.c1 = a0.dim == 3 ? (col / m) % m : col % m;
+      a.c2 = a0.dim == 3 ? col % m : 0;
+      a.first0 = a0.el_begin + ((c0 - a0.el_begin % m) % m + m) % m;
+      a.n0 = count(a0.el_begin, a0.el_end, c0);
+      a.n1 = count(0, a0.K, a.c1);
+      a.n2 = a0.dim == 3 ? count(0, a0.K, a.c2) : 1;
+      const int rc = launch_colour(a, method, shm, s);
+      if (rc) return rc;
+    }
+    return IGA_OK;
   }
 };
 

@@ -22,7 +22,6 @@ selects it for scalar coefficients and the assembled DMMA sum factorization
 from __future__ import annotations
 
 import threading
-import warnings
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -296,13 +295,11 @@ class IntegrationRuntime:
     """Owns the device buffers for one configuration; ``run`` is not reentrant
     (runtime.py:155-185)."""
 
-    def __init__(self, cfg: RunConfig):
+    def __init__(self, cfg: RunConfig, device_ids=None, exchange: str = "auto"):
         self.cfg = cfg
+        self.device_ids = device_ids  # devices > 1: GPU of each slab (default 0..devices-1)
+        self.exchange = exchange
         self._active = threading.Lock()
-        if cfg.devices > 1:
-            warnings.warn("devices > 1 in one process: use paper_2207_00280_b200.distributed "
-                          "(one process per GPU); running on the current device",
-                          RuntimeWarning, stacklevel=2)
 
     def run(self) -> RunResult:
         if not self._active.acquire(blocking=False):
@@ -312,9 +309,41 @@ class IntegrationRuntime:
         finally:
             self._active.release()
 
+    def _run_multi(self) -> RunResult:
+        """devices > 1: element slabs on G devices driven from this process with the NCCL
+        interface exchange (distributed.MultiDeviceRuntime)."""
+        torch = _lib.require_cuda()
+        from .distributed import MultiDeviceRuntime
+
+        cfg = self.cfg
+        if cfg.dim != 3:
+            raise ValueError("devices > 1 is implemented for dim=3")
+        rt = MultiDeviceRuntime(cfg, self.device_ids, exchange=self.exchange)
+        try:
+            times = []
+            for _ in range(cfg.repetitions):
+                ev = []
+                for s in rt.sessions:
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record(s.stream)
+                    ev.append((a, b))
+                shards = rt.step()
+                for (a, b), s in zip(ev, rt.sessions):
+                    b.record(s.stream)
+                rt.synchronize()
+                times.append(max(a.elapsed_time(b) for a, b in ev) / 1e3)
+        finally:
+            rt.close()
+        prob = rt.sessions[0].prob
+        gram = GlobalGram(K=cfg.mesh, p=cfg.degree, n_dofs=prob.n_dofs, dim=3, shards=shards)
+        per_el = flop_count(cfg.method, cfg.degree, cfg.points)
+        return RunResult(config=cfg, gram=gram, times=times, flops=per_el * prob.n_elements)
+
     def _run_locked(self) -> RunResult:
         torch = _lib.require_cuda()
         cfg = self.cfg
+        if cfg.devices > 1:
+            return self._run_multi()
         sess = DeviceSession(cfg)
         prob, stream = sess.prob, sess.stream
         times = []
@@ -332,6 +361,9 @@ class IntegrationRuntime:
         return RunResult(config=cfg, gram=gram, times=times, flops=per_el * prob.n_elements)
 
 
-def run_integration(cfg: RunConfig) -> RunResult:
-    """Integrate + assemble the mesh under cfg on the device (runtime.py:287-295)."""
-    return IntegrationRuntime(cfg).run()
+def run_integration(cfg: RunConfig, device_ids=None, exchange: str = "auto") -> RunResult:
+    """Integrate + assemble the mesh under cfg on the device (runtime.py:287-295).
+    ``cfg.devices = G > 1`` splits the elements into G slabs along the slowest axis on
+    ``device_ids`` (default 0..G-1) with the interface rows exchanged over NCCL
+    (``exchange="copy"``: device copies, e.g. when the slabs share one GPU)."""
+    return IntegrationRuntime(cfg, device_ids, exchange).run()

@@ -223,10 +223,19 @@ def test_reference_strategies_accepted(pkg):
         assert pkg.grams_bitwise_equal(grams[0], g2)
 
 
-@pytest.mark.parametrize("assembly", ["owner", "separable"])
-def test_assembled_sumfact_deterministic(pkg, assembly):
-    cfg = pkg.RunConfig("sumfact", "device", 12, 3, operator="stiffness", repetitions=2,
-                        assembly=assembly)
+@pytest.mark.parametrize("method,assembly,K,coef", [
+    ("sumfact", "owner", 12, False), ("sumfact", "separable", 12, False),
+    ("classical", "auto", 12, False), ("sumfact", "scatter", 12, False),
+    ("classical", "auto", 20, True), ("sumfact", "scatter", 20, True)])
+def test_every_path_bitwise_reproducible(pkg, method, assembly, K, coef):
+    """The reference promises bitwise-identical matrices for every schedule
+    (runtime.py:16-20, assembly.py:1-6): two runs of every device path give the same bits,
+    including the element-local classical and sum-factorization paths (colour-ordered
+    scatter, no atomics)."""
+    p = 3
+    c = (np.random.default_rng(1).uniform(0.5, 1.5, size=(K**3, (p + 1) ** 3)) if coef else None)
+    cfg = pkg.RunConfig(method, "device", K, p, operator="stiffness", repetitions=2,
+                        assembly=assembly, coefficient=c)
     a = pkg.run_integration(cfg).gram
     b = pkg.run_integration(cfg).gram
     assert pkg.grams_bitwise_equal(a, b)
