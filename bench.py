@@ -41,6 +41,10 @@ WORKLOADS = {
                     "assembled sum factorization"),
     "c5": dict(dim=3, K=256, p=3, op="stiffness", coef=None, method="sumfact",
                desc="C5: 3D Laplace stiffness 256^3 p=3 q=4 c=1, z-slabs + NCCL interface rows"),
+    "p9": dict(dim=3, K=30, p=9, op="mass", coef=None, method="sumfact",
+               desc="paper: 3D Gram (mass) 30^3 p=9 q=10 c=1 (PAPER.md:1095-1104; the paper's "
+                    "only timed configuration: sum factorization 403.6 s single core, 118.3 s on "
+                    "4 cores, classical 9931.8 s / 951 s on 12 cores)"),
 }
 
 
@@ -392,7 +396,8 @@ def main():
     # headline: the general sum-factorization kernel (per-quadrature-point coefficient
     # capable); the separable shortcut for a scalar coefficient is
     # reported beside it under "separable"
-    assembly = args.assembly or ("owner" if method == "sumfact" and wl["dim"] == 3 else "auto")
+    assembly = args.assembly or ("owner" if method == "sumfact" and wl["dim"] == 3 and p <= 5
+                                 else "auto")
     cfg = P.RunConfig(method, "device", K, p, operator=wl["op"], coefficient=coef,
                       dim=wl["dim"], devices=world, assembly=assembly)
     stream = torch.cuda.current_stream()
@@ -509,7 +514,8 @@ def main():
     # separable Kronecker shortcut, declared as such with its HBM roofline)
     other = None
     if world == 1 and wl["dim"] == 3 and coef is None and not args.no_alt and method == "sumfact":
-        other = alt_leg(cfg, "owner" if sess.code == 3 else "separable", args, flush, stream, wl,
+        other = alt_leg(cfg, ("owner" if p <= 5 else "scatter") if sess.code == 3 else "separable",
+                        args, flush, stream, wl,
                         total_el, peaks)
 
     cpu = None

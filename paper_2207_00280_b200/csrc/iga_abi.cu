@@ -251,7 +251,7 @@ int32_t iga_mesh_tables(int32_t K, int32_t p, int32_t q, const double* ref_nodes
   if (p < 0) return fail_einval("degree must be >= 0, got %d", p);
   if (q < 1 || q > kMaxQ) return fail_einval("quadrature points q=%d outside 1..%d", q, kMaxQ);
   if (!ref_nodes || !vals) return fail_einval("null pointer");
-  return dispatch_p<MeshTablesLaunch>(p, K, q, ref_nodes, vals, ders, as_stream(stream));
+  return dispatch_p_all<MeshTablesLaunch>(p, K, q, ref_nodes, vals, ders, as_stream(stream));
 }
 
 int32_t iga_basis_eval(int32_t K, int32_t p, int64_t n, const int32_t* elem, const double* x,
@@ -260,7 +260,7 @@ int32_t iga_basis_eval(int32_t K, int32_t p, int64_t n, const int32_t* elem, con
   if (p < 0) return fail_einval("degree must be >= 0, got %d", p);
   if (n < 0) return fail_einval("negative point count");
   if (n > 0 && (!elem || !x || !vals)) return fail_einval("null pointer");
-  return dispatch_p<BasisEvalLaunch>(p, K, n, elem, x, vals, ders, as_stream(stream));
+  return dispatch_p_all<BasisEvalLaunch>(p, K, n, elem, x, vals, ders, as_stream(stream));
 }
 
 int64_t iga_csr_nnz(int32_t dim, int32_t K, int32_t p, int64_t row_begin, int64_t row_end) {

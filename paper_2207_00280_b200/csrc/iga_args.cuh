@@ -18,6 +18,8 @@ struct ElemArgs {
   const double* elem_coef;     // [count][q^dim] per-element coefficients, or null (coef / scalar)
   int64_t count;
   double* out;
+  double* scratch;             // per-CTA sum-factorization stage buffers in global memory
+                               // (high degrees), or null (shared memory)
 };
 
 struct ScatterArgs {
@@ -37,6 +39,9 @@ struct ScatterArgs {
   int first0;                     // smallest e0 in [el_begin, el_end) of the colour
   int c1, c2;                     // colour along axes 1, 2 (2D: c1 only)
   int n0, n1, n2;                 // colour elements per axis (2D: n2 = 1)
+  int split;                      // CTAs per element (classical DMMA kernel: tile ranges)
+  double* scratch;                // element-local sum factorization, high degrees: per-CTA
+                                  // stage buffers in global memory (else shared memory)
 };
 
 struct GsfArgs {

@@ -14,8 +14,9 @@
 
 namespace iga {
 
-constexpr int kMaxP = 5;   // highest degree with device kernels
-constexpr int kMaxQ = 8;   // highest quadrature-point count per axis
+constexpr int kMaxP = 9;    // highest degree with device kernels (iga_dispatch.cuh: p <= 5 on
+                            // every path, 6..9 on the paths that opt in)
+constexpr int kMaxQ = 10;   // highest quadrature-point count per axis
 constexpr int kMaxKnots = 1 << 16;
 
 // ------------------------------------------------------------ error state
@@ -167,7 +168,3 @@ __host__ __device__ __forceinline__ int64_t col_slot3(const int64_t* I, const in
 
 }  // namespace iga
 
-// Dispatch helper: instantiate F<P,Q> for the supported (p, q) grid
-// (0 <= p <= 5, 1 <= q <= p+3, q <= 8).
-#define IGA_PQ_CASE(P, Q, ...) \
-  if (p == P && q == Q) { __VA_ARGS__(P, Q); }

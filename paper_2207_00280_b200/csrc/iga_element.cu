@@ -29,7 +29,10 @@ __global__ void __launch_bounds__(256) k_element_strict(ElemArgs a) {
   extern __shared__ double smem[];
   double* tabs = smem;                       // DIM*2*m*Q
   double* w = tabs + DIM * 2 * m * Q;        // DIM*Q
-  double* Dbuf = w + DIM * Q;                // m*m*Q*Q (3D) or m*m*Q (2D)
+  // sum-factorization stage buffers: shared memory, or (high degrees: m^4 Q doubles do not
+  // fit) this CTA's slice of the global scratch
+  double* Dbuf = a.scratch ? a.scratch + (int64_t)blockIdx.x * (m * m * Q * Q + m * m * m * m * Q)
+                           : w + DIM * Q;    // m*m*Q*Q (3D) or m*m*Q (2D)
   double* Cbuf = Dbuf + m * m * Q * Q;       // m^4*Q (3D)
   const int64_t el = blockIdx.x;
   if (el >= a.count) return;
@@ -200,28 +203,59 @@ __global__ void __launch_bounds__(256) k_element_strict(ElemArgs a) {
 
 template <int P, int Q>
 struct ElementStrictLaunch {
-  static int run(const ElemArgs& a, cudaStream_t s) {
+  static int run(const ElemArgs& a0, cudaStream_t s) {
     constexpr int m = P + 1;
-    if (a.count == 0) return IGA_OK;
-    if (a.count > 0x7fffffff) return fail_einval("too many elements");
-    size_t shm;
-    if (a.dim == 3) {
-      shm = sizeof(double) * (3 * 2 * m * Q + 3 * Q + m * m * Q * Q + m * m * m * m * Q);
+    if (a0.count == 0) return IGA_OK;
+    if (a0.count > 0x7fffffff) return fail_einval("too many elements");
+    if (a0.dim == 2) {
+      const size_t shm = sizeof(double) * (2 * 2 * m * Q + 2 * Q + m * m * Q * Q);
       if (shm > 48 * 1024) {
-        cudaError_t e = smem_attr_once(reinterpret_cast<const void*>(k_element_strict<3, P, Q>), shm);
+        cudaError_t e = smem_attr_once(reinterpret_cast<const void*>(k_element_strict<2, P, Q>), shm);
         if (e != cudaSuccess) return check_cuda(e, "element smem attr");
       }
-      k_element_strict<3, P, Q><<<(unsigned)a.count, 256, shm, s>>>(a);
-    } else {
-      shm = sizeof(double) * (2 * 2 * m * Q + 2 * Q + m * m * Q * Q);
-      k_element_strict<2, P, Q><<<(unsigned)a.count, 256, shm, s>>>(a);
+      k_element_strict<2, P, Q><<<(unsigned)a0.count, 256, shm, s>>>(a0);
+      return check_cuda(cudaGetLastError(), "iga_element_matrices launch");
     }
-    return check_cuda(cudaGetLastError(), "iga_element_matrices launch");
+    constexpr size_t stage = (size_t)m * m * Q * Q + (size_t)m * m * m * m * Q;  // D + C doubles
+    constexpr size_t base = 3 * 2 * m * Q + 3 * Q;
+    const bool global = a0.method == IGA_METHOD_SUMFACT && sizeof(double) * (base + stage) > 200 * 1024;
+    const size_t shm = sizeof(double) * (global || a0.method != IGA_METHOD_SUMFACT ? base : base + stage);
+    if (shm > 48 * 1024) {
+      cudaError_t e = smem_attr_once(reinterpret_cast<const void*>(k_element_strict<3, P, Q>), shm);
+      if (e != cudaSuccess) return check_cuda(e, "element smem attr");
+    }
+    if (!global) {
+      k_element_strict<3, P, Q><<<(unsigned)a0.count, 256, shm, s>>>(a0);
+      return check_cuda(cudaGetLastError(), "iga_element_matrices launch");
+    }
+    // high degrees: the m^4 Q stage buffer of every CTA in stream-ordered global scratch
+    // (cudaMallocAsync: graph-capturable, freed in stream order), chunks of <= 256 elements
+    constexpr int64_t kChunk = 256;
+    const int64_t chunk = a0.count < kChunk ? a0.count : kChunk;
+    double* scratch = nullptr;
+    int rc = check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&scratch),
+                                        sizeof(double) * stage * chunk, s), "element scratch");
+    if (rc) return rc;
+    constexpr int n = m * m * m, nq = Q * Q * Q;
+    for (int64_t off = 0; off < a0.count && !rc; off += chunk) {
+      ElemArgs a = a0;
+      a.count = a0.count - off < chunk ? a0.count - off : chunk;
+      a.elem_ids = a0.elem_ids + off * 3;
+      if (a0.elem_nodes) a.elem_nodes = a0.elem_nodes + off * 3 * Q;
+      if (a0.elem_weights) a.elem_weights = a0.elem_weights + off * 3 * Q;
+      if (a0.elem_coef) a.elem_coef = a0.elem_coef + off * nq;
+      a.out = a0.out + off * (int64_t)n * n;
+      a.scratch = scratch;
+      k_element_strict<3, P, Q><<<(unsigned)a.count, 256, shm, s>>>(a);
+      rc = check_cuda(cudaGetLastError(), "iga_element_matrices launch");
+    }
+    const int rf = check_cuda(cudaFreeAsync(scratch, s), "element scratch free");
+    return rc ? rc : rf;
   }
 };
 
 int launch_element_strict(const ElemArgs& a, int p, int q, cudaStream_t s) {
-  return dispatch_pq<ElementStrictLaunch>(p, q, a, s);
+  return dispatch_pq_all<ElementStrictLaunch>(p, q, a, s);
 }
 
 }  // namespace iga
@@ -248,6 +282,6 @@ extern "C" int32_t iga_element_matrices(const iga_problem* prob, int32_t method,
   a.jac = prob->jac; a.coef_scalar = prob->coef_scalar; a.coef = prob->coef;
   a.weights = prob->weights; a.ref_nodes = ref_nodes; a.elem_ids = elem_ids;
   a.elem_nodes = elem_nodes; a.elem_weights = elem_weights; a.elem_coef = elem_coef;
-  a.count = count; a.out = out;
+  a.count = count; a.out = out; a.scratch = nullptr;
   return launch_element_strict(a, prob->p, prob->q, as_stream(stream));
 }

@@ -55,9 +55,15 @@ constexpr int NT = 512;                  // threads: 16 warps
 constexpr int MT_A = NCOL / 8;           // 14 m-tiles of (g1,k2) columns
 constexpr int MT_B = NA0 * Q / 8;        // 7 m-tiles of (a0,k2) rows
 constexpr int MT_S = NCOMBO / 8;         // 49 m-tiles of combos
-constexpr int NWA = 4, NWB = 5, NWS = 7; // warps per role (NWA even: fixed type per A warp)
+#ifndef P3_NWB
+#define P3_NWB 5
+#endif
+#ifndef P3_NWS
+#define P3_NWS 7
+#endif
+constexpr int NWA = 4, NWB = P3_NWB, NWS = P3_NWS;  // warps per role (NWA even: fixed type per A warp)
+static_assert(NWA + NWB + NWS == 16, "16 warps");
 constexpr int MT_S_PER_WARP = (MT_S + NWS - 1) / NWS;  // 7
-static_assert(MT_S == MT_S_PER_WARP * NWS, "stage S m-tiles split evenly");
 constexpr int NHB = 2 * MT_B;            // stage-B half units (m-tile, ib pair)
 constexpr int NPEN = TA * TB;            // row pencils (I0, I1) of the tile
 
@@ -131,10 +137,23 @@ struct Lane {
 // hi = sum_{k < 4-t} y[k] (band offset 3+t), lo = sum of the rest (offset t-1)
 // Lane masks m_k = [k < 4-t] as exact 0/1 doubles: fma(m, y, acc) adds y or nothing
 // exactly, so the group sums need no data-dependent selects.
+#ifndef P3_SPLIT
+#define P3_SPLIT 0
+#endif
+__device__ __forceinline__ double sel(bool c, double a, double b) { return c ? a : b; }
 __device__ __forceinline__ void split_groups(const double* y, int t, double& hi, double& lo) {
+#if P3_SPLIT == 1
+  // three DADDs per lane and integer selects: A = y0 + y1, B = y2 + y3, and one lane-chosen
+  // sum C (t=0: A + B, t=1: A + y2, t=3: y1 + B)
+  const double A = y[0] + y[1], B = y[2] + y[3];
+  const double C = sel(t == 3, y[1], A) + sel(t == 1, y[2], B);
+  hi = sel(t <= 1, C, sel(t == 2, A, y[0]));
+  lo = sel(t == 1, y[3], sel(t == 2, B, C));
+#else
   const double m1 = t <= 2 ? 1.0 : 0.0, m2 = t <= 1 ? 1.0 : 0.0, m3 = t == 0 ? 1.0 : 0.0;
   hi = fma(m3, y[3], fma(m2, y[2], fma(m1, y[1], y[0])));
   lo = fma(1.0 - m3, y[3], fma(1.0 - m2, y[2], (1.0 - m1) * y[1]));
+#endif
 }
 
 // ---------------------------------------------------------------- stage A
@@ -311,6 +330,11 @@ __device__ __forceinline__ void stage_s_batch(const Lane& L, int ws, const doubl
   const int g = L.g, t = L.t;
   double a0[NM], a1[NM], cc[NM][2][2], lo[NM];
   int p[NM][2][2];
+  if (MT_S % NWS != 0 && ws + (I0 + NM - 1) * NWS >= MT_S) {
+    // uneven split: the last m-tile of this batch does not exist for this warp
+    if constexpr (NM > 1) stage_s_batch<PHI, I0, NM - 1>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd);
+    return;
+  }
 #pragma unroll
   for (int i = 0; i < NM; ++i) {
     const int mt = ws + (I0 + i) * NWS;
@@ -342,7 +366,11 @@ __device__ __forceinline__ void stage_s_batch(const Lane& L, int ws, const doubl
   for (int i = 0; i < NM; ++i) {
 #pragma unroll
     for (int k = 1; k < 4; ++k) Rs[p[i][k >> 1][k & 1]] = cc[i][k >> 1][k & 1];
+#ifndef P3_ABL_NOSTORE
     store_pair(a, meta[I0 + i], pb, pc, rd, cc[i][0][0], lo[i]);
+#else
+    if (cc[i][0][0] == 1.2345e-300) store_pair(a, meta[I0 + i], pb, pc, rd, cc[i][0][0], lo[i]);
+#endif
   }
 }
 
@@ -373,8 +401,15 @@ __device__ __forceinline__ void stage_s(const Lane& L, int ws, const double* Y, 
                                         const double (&b0)[2], const double (&b1)[2]) {
   const int t = L.t;
   const RowDst rd = row_dst(t, e2, N);
-  stage_s_batch<PHI, 0, 4>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd);
-  stage_s_batch<PHI, 4, 3>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd);
+  // batches of at most 4 m-tiles (loads of a batch issued before its DMMAs)
+  constexpr int B0 = MT_S_PER_WARP <= 4 ? MT_S_PER_WARP : (MT_S_PER_WARP <= 8 ? (MT_S_PER_WARP + 1) / 2 : 4);
+  constexpr int R1 = MT_S_PER_WARP - B0;
+  constexpr int B1 = R1 <= 4 ? R1 : (R1 + 1) / 2;
+  constexpr int B2 = R1 - B1;
+  static_assert(B2 <= 4, "stage S batches");
+  stage_s_batch<PHI, 0, B0>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd);
+  if constexpr (B1 > 0) stage_s_batch<PHI, B0, B1>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd);
+  if constexpr (B2 > 0) stage_s_batch<PHI, B0 + B1, B2>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd);
 }
 
 // Rows K .. K+P-1 (no element e2 = I2): both groups are complete in their slots.
@@ -505,10 +540,13 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
       }
       const int b = it & 1;
       if (it >= 2) mbar_wait(xempty + b, ((it >> 1) - 1) & 1);
+      PT(1);
       double* X = sm + OFF_X + b * SZ_X;
       int mt = mt0;
+#ifndef P3_ABL_NOA
       for (; mt + mstep < MT_A; mt += 2 * mstep) stage_a_units<2>(L, W, ba, X, mt, mstep, ty);
       if (mt < MT_A) stage_a_units<1>(L, W, ba, X, mt, mstep, ty);
+#endif
       mbar_arrive(xfull + b);
       PT(0);
     }
@@ -528,9 +566,12 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
       const int b = e2 & 1, n = e2 >> 1;
       mbar_wait(xfull + b, n & 1);
       if (n >= 1) mbar_wait(yempty + b, (n - 1) & 1);
+      PT(1);
       const double* X = sm + OFF_X + b * SZ_X;
       double* Y = sm + OFF_Y + b * SZ_Y;
+#ifndef P3_ABL_NOB
       for (int u = wb; u < NHB; u += NWB) stage_b_half(L, X, bv, bd, Y, u >> 1, u & 1);
+#endif
       mbar_arrive(xempty + b);
       mbar_arrive(yfull + b);
       PT(0);
@@ -568,7 +609,11 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
       PT(2);
       const int b = e2 & 1;
       mbar_wait(yfull + b, (e2 >> 1) & 1);
+      PT(1);
       const double* Y = sm + OFF_Y + b * SZ_Y;
+#ifdef P3_ABL_NOS
+      if (e2 < 0)
+#endif
       switch (e2 & 3) {
         case 0: stage_s<0>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1); break;
         case 1: stage_s<1>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1); break;
@@ -578,7 +623,6 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
       if (e2 + 1 < K) s_fragments(L, a, e2 + 1, sb0, sb1);
       mbar_arrive(yempty + b);
       PT(0);
-      PT(1);
     }
     // rows K .. K+P-1 received their last contribution from element K-1
     for (int I2 = K; I2 < N; ++I2) flush_tail(L, ws, Rs, I2, meta, pb, pc, a, N);

@@ -211,7 +211,9 @@ struct Spmv3Launch {
     // (an A/B knob read per call so a test can compare both kernels in one process; only
     // the value "1" enables it)
     const char* force_l1 = getenv("IGA_SPMV_L1");
-    if (N >= 160 && !(force_l1 != nullptr && force_l1[0] == '1' && force_l1[1] == 0)) {
+    constexpr size_t staged_sm = sizeof(double) * (2 * P + 1) * (kSpmvSB1 + 2 * P) * (kSpmvSeg + 2 * P);
+    if (staged_sm <= 200 * 1024 && N >= 160 &&
+        !(force_l1 != nullptr && force_l1[0] == '1' && force_l1[1] == 0)) {
       const int64_t nb1 = (N + kSpmvSB1 - 1) / kSpmvSB1, nsg = (N + kSpmvSeg - 1) / kSpmvSeg;
       const size_t sm = sizeof(double) * (2 * P + 1) * (kSpmvSB1 + 2 * P) * (kSpmvSeg + 2 * P);
       const void* fn = reinterpret_cast<const void*>(k_spmv3s<P>);
@@ -372,7 +374,7 @@ int32_t iga_spmv(int32_t dim, int32_t K, int32_t p, const double* values, const 
   if (K < 1 || p < 0) return fail_einval("mesh must be >= 1 and degree >= 0");
   if (!values || !x || !y) return fail_einval("null pointer");
   const int64_t N = (int64_t)K + p;
-  if (dim == 3) return dispatch_p<Spmv3Launch>(p, K, values, x, y, as_stream(stream));
+  if (dim == 3) return dispatch_p_all<Spmv3Launch>(p, K, values, x, y, as_stream(stream));
   const int64_t nrows = N * N;
   const int64_t threads = nrows * 32;
   k_spmv<<<(unsigned)((threads + 255) / 256), 256, 0, as_stream(stream)>>>(dim, K, p, values, x,

@@ -46,7 +46,8 @@ __host__ __device__ constexpr int kron_minb(int P) {
 #define KRON_GS 16
 #endif
 __host__ __device__ constexpr int kron_rows(int P, bool small_mesh) {
-  return P <= 2 ? 16 : (P == 3 ? (small_mesh ? KRON_GS : 8) : 4);
+  // high degrees: one row (NB^3 = 2197..6859 values) per staged chunk
+  return P <= 2 ? 16 : (P == 3 ? (small_mesh ? KRON_GS : 8) : (P <= 5 ? 4 : 1));
 }
 #ifndef KRON_NBUF
 #define KRON_NBUF 2
@@ -255,12 +256,14 @@ __global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) 
 // integrals, and the sums per band entry in build_band_tables' order -- so k_kron3
 // produces the same bits either way, and the launch is a few latency rounds on several
 // SMs instead of the quadrature prologue of every k_kron3 CTA.
-constexpr int kBandRows = 8;
+// band rows per CTA (8; 2 for the high degrees, whose element tables fill static smem)
+__host__ __device__ constexpr int band_rows(int P) { return P <= 5 ? 8 : 2; }
 template <int P, int Q>
 __global__ void __launch_bounds__(128) k_mesh_band(int K, const double* __restrict__ ref,
                                                    const double* __restrict__ weights, int stiff,
                                                    double* __restrict__ V, double* __restrict__ D,
                                                    double2* __restrict__ band) {
+  constexpr int kBandRows = band_rows(P);
   constexpr int M = P + 1, NB = 2 * P + 1, NEL = kBandRows + P;
   __shared__ double Vs[NEL * M * Q], Ds[NEL * M * Q];
   __shared__ double2 em[NEL * M * M];
@@ -319,7 +322,7 @@ struct BandLaunch {
   static int run(int K, const double* ref, const double* weights, int stiff, double* V, double* D,
                  double2* band, cudaStream_t s) {
     const int N = K + P;
-    k_mesh_band<P, Q><<<(N + kBandRows - 1) / kBandRows, 128, 0, s>>>(
+    k_mesh_band<P, Q><<<(N + band_rows(P) - 1) / band_rows(P), 128, 0, s>>>(
         K, ref, weights, stiff, V, D, band);
     return check_cuda(cudaGetLastError(), "band launch");
   }
@@ -327,7 +330,7 @@ struct BandLaunch {
 
 int launch_band_tables(int K, int p, int q, const double* ref, const double* weights, int stiff,
                        double* V, double* D, double* band, cudaStream_t s) {
-  return dispatch_pq<BandLaunch>(p, q, K, ref, weights, stiff, V, D,
+  return dispatch_pq_all<BandLaunch>(p, q, K, ref, weights, stiff, V, D,
                                  reinterpret_cast<double2*>(band), s);
 }
 
@@ -362,7 +365,7 @@ struct KronLaunch {
 };
 
 int launch_kron(const KronArgs& a, int p, int q, cudaStream_t s) {
-  return dispatch_pq<KronLaunch>(p, q, a, s);
+  return dispatch_pq_all<KronLaunch>(p, q, a, s);
 }
 
 }  // namespace iga

@@ -185,7 +185,13 @@ __global__ void __launch_bounds__(256) k_classical_mma(ScatterArgs a) {
   const bool with_mass = a.op != IGA_OP_STIFFNESS;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, tq = lane & 3;
-  for (int64_t el = blockIdx.x; el < n_el; el += gridDim.x) {
+  // high degrees: `split` CTAs share an element, each taking a contiguous part of its
+  // tile list (the parts write disjoint values, so the scatter stays one contribution per
+  // value and element)
+  const int split = a.split > 1 ? a.split : 1;
+  for (int64_t item = blockIdx.x; item < n_el * split; item += gridDim.x) {
+    const int64_t el = item / split;
+    const int part = (int)(item % split);
     int alpha[3];
     colour_element(a, el, m, 3, alpha);
     __syncthreads();
@@ -216,8 +222,9 @@ __global__ void __launch_bounds__(256) k_classical_mma(ScatterArgs a) {
     // contiguous, balanced ranges of the row-major upper-tile list per warp, cut into
     // segments of <= CH tiles sharing the row tile mt
     const int nwarps = blockDim.x >> 5;
-    const int t_hi = (warp + 1) * NTILES / nwarps;
-    for (int t = warp * NTILES / nwarps; t < t_hi;) {
+    const int p_lo = (int)((int64_t)part * NTILES / split), p_n = (int)((int64_t)(part + 1) * NTILES / split) - p_lo;
+    const int t_hi = p_lo + (warp + 1) * p_n / nwarps;
+    for (int t = p_lo + warp * p_n / nwarps; t < t_hi;) {
       int mt = 0, nt0 = t;
       while (nt0 >= MT - mt) nt0 -= MT - mt++;
       nt0 += mt;
@@ -319,7 +326,8 @@ __global__ void __launch_bounds__(256) k_sumfact_scatter(ScatterArgs a) {
   double* sV = smem;                 // [3][m][Q]
   double* sD = sV + 3 * m * Q;       // [3][m][Q]
   double* sW = sD + 3 * m * Q;       // [Q^3]
-  double* XV = sW + Q * Q * Q;
+  // stage buffers: shared memory, or (high degrees) this CTA's slice of the global scratch
+  double* XV = a.scratch ? a.scratch + (int64_t)blockIdx.x * (2 * nX + 2 * nY) : sW + Q * Q * Q;
   double* XD = XV + nX;
   double* YA = XD + nX;
   double* YB = YA + nY;
@@ -410,37 +418,67 @@ __global__ void __launch_bounds__(256) k_sumfact_scatter(ScatterArgs a) {
 
 template <int P, int Q>
 struct ScatterLaunch {
-  static int launch_colour(const ScatterArgs& a, int method, size_t shm, cudaStream_t s) {
+  static constexpr int m = P + 1;
+  static constexpr size_t kStage = 2 * (size_t)m * m * Q * Q + 2 * (size_t)m * m * m * m * Q;
+  static constexpr size_t kBase = 6 * m * Q + Q * Q * Q;
+  static constexpr bool kGlobalStage = sizeof(double) * (kBase + kStage) > 200 * 1024;
+
+  static int launch_colour(const ScatterArgs& a, int method, size_t shm, int64_t slots,
+                           cudaStream_t s) {
     const int64_t n_el = (int64_t)a.n0 * a.n1 * a.n2;
     if (n_el <= 0) return IGA_OK;
-    const int64_t grid = n_el < 148 * 64 ? n_el : 148 * 64;
+    int64_t grid = n_el < 148 * 64 ? n_el : 148 * 64;
     if (method == IGA_METHOD_CLASSICAL) {
       static const bool scalar = [] {
         const char* e = getenv("IGA_CLASSICAL_SCALAR");
         return e && e[0] == '1' && e[1] == 0;
       }();
-      if (a.dim == 3 && !scalar)
-        k_classical_mma<P, Q><<<(unsigned)grid, 256, 0, s>>>(a);
-      else if (a.dim == 3)
+      if (a.dim == 3 && !scalar) {
+        ScatterArgs b = a;
+        // few, large elements per colour (high degrees): several CTAs per element
+        constexpr int NT = ClassicalMma<P, Q>::NTILES;
+        b.split = 1;
+        if (P > kMaxPLow && n_el < 2 * 148) {
+          const int64_t want = (2 * 148 + n_el - 1) / n_el;
+          b.split = (int)(want < NT / 64 ? want : (NT / 64 > 1 ? NT / 64 : 1));
+        }
+        const int64_t items = n_el * b.split;
+        grid = items < 148 * 64 ? items : 148 * 64;
+        k_classical_mma<P, Q><<<(unsigned)grid, 256, 0, s>>>(b);
+      } else if (a.dim == 3) {
         k_classical_scatter<3, P, Q><<<(unsigned)grid, 256, 0, s>>>(a);
-      else
+      } else {
         k_classical_scatter<2, P, Q><<<(unsigned)grid, 256, 0, s>>>(a);
+      }
     } else {
+      if (slots > 0 && grid > slots) grid = slots;  // one scratch slice per CTA
       k_sumfact_scatter<P, Q><<<(unsigned)grid, 256, shm, s>>>(a);
     }
     return check_cuda(cudaGetLastError(), "scatter launch");
   }
 
   static int run(const ScatterArgs& a0, int method, cudaStream_t s) {
-    constexpr int m = P + 1;
     if (a0.el_end <= a0.el_begin) return IGA_OK;
     size_t shm = 0;
+    int64_t slots = 0;
+    double* scratch = nullptr;
     if (method != IGA_METHOD_CLASSICAL) {
       if (a0.dim != 3) return fail_einval("element-local sum factorization scatter is 3D only");
-      shm = sizeof(double) * (6 * m * Q + Q * Q * Q + 2 * m * m * Q * Q + 2 * m * m * m * m * Q);
+      shm = sizeof(double) * (kGlobalStage ? kBase : kBase + kStage);
       if (shm > 48 * 1024) {
         cudaError_t e = smem_attr_once(reinterpret_cast<const void*>(k_sumfact_scatter<P, Q>), shm);
         if (e != cudaSuccess) return check_cuda(e, "sumfact smem attr");
+      }
+      if (kGlobalStage) {
+        // high degrees: the stage buffers (m^4 Q doubles each) of one resident wave of CTAs
+        // in stream-ordered global scratch (cudaMallocAsync; graph-capturable), freed after
+        // the last colour
+        slots = (int64_t)sm_count() *
+                blocks_per_sm_once(reinterpret_cast<const void*>(k_sumfact_scatter<P, Q>), 256, shm);
+        const int rc = check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&scratch),
+                                                  sizeof(double) * kStage * slots, s),
+                                  "sumfact scratch");
+        if (rc) return rc;
       }
     }
     auto count = [](int lo, int hi, int c) {  // e in [lo, hi) with e = c (mod m)
@@ -448,7 +486,8 @@ struct ScatterLaunch {
       return first >= hi ? 0 : (hi - 1 - first) / m + 1;
     };
     const int colours = a0.dim == 3 ? m * m * m : m * m;
-    for (int col = 0; col < colours; ++col) {  // fixed colour order = fixed summation order
+    int rc = IGA_OK;
+    for (int col = 0; col < colours && !rc; ++col) {  // fixed colour order = fixed summation order
       ScatterArgs a = a0;
       const int c0 = a0.dim == 3 ? col / (m * m) : col / m;
       a.c1 = a0.dim == 3 ? (col / m) % m : col % m;
@@ -457,15 +496,20 @@ struct ScatterLaunch {
       a.n0 = count(a0.el_begin, a0.el_end, c0);
       a.n1 = count(0, a0.K, a.c1);
       a.n2 = a0.dim == 3 ? count(0, a0.K, a.c2) : 1;
-      const int rc = launch_colour(a, method, shm, s);
-      if (rc) return rc;
+      a.split = 1;
+      a.scratch = scratch;
+      rc = launch_colour(a, method, shm, slots, s);
     }
-    return IGA_OK;
+    if (scratch) {
+      const int rf = check_cuda(cudaFreeAsync(scratch, s), "sumfact scratch free");
+      if (!rc) rc = rf;
+    }
+    return rc;
   }
 };
 
 int launch_scatter(const ScatterArgs& a, int method, int p, int q, cudaStream_t s) {
-  return dispatch_pq<ScatterLaunch>(p, q, a, method, s);
+  return dispatch_pq_all<ScatterLaunch>(p, q, a, method, s);
 }
 
 }  // namespace iga

@@ -172,11 +172,15 @@ def grams_bitwise_equal(a: GlobalGram, b: GlobalGram) -> bool:
             and ma.data.tobytes() == mb.data.tobytes())
 
 
+MAX_P_ASSEMBLED = 5  # the assembled (row-owner) sum factorization kernels: p <= 5
+MAX_P = 9            # every other path (csrc/iga_dispatch.cuh)
+
+
 def separable_fits(K: int, p: int) -> bool:
     """Shared-memory budget of k_kron3 (csrc/iga_kron.cu: 1D band tables + two
     staging chunks)."""
     nb = 2 * p + 1
-    rows = 16 if p <= 2 else ((16 if K <= 96 else 8) if p == 3 else 4)
+    rows = 16 if p <= 2 else ((16 if K <= 96 else 8) if p == 3 else (4 if p <= 5 else 1))
     return 2 * 16 * (K + p) * nb + 16 * (rows * nb**3 + 2) <= 220 * 1024
 
 
@@ -207,6 +211,12 @@ def method_code(cfg: RunConfig) -> int:
     if (cfg.assembly == "auto" and (c is None or np.ndim(c) == 0)
             and separable_fits(cfg.mesh, cfg.degree)):
         return _lib.METHOD_SEPARABLE
+    if cfg.degree > MAX_P_ASSEMBLED:
+        if cfg.assembly == "owner":
+            raise ValueError(f"assembly='owner' runs p <= {MAX_P_ASSEMBLED}; p={cfg.degree} "
+                             "takes 'auto' (separable or element-local sum factorization)")
+        # high degrees: element-local sum factorization (stage buffers in global scratch)
+        return _lib.METHOD_SUMFACT
     return _lib.METHOD_SUMFACT_ASSEMBLED
 
 

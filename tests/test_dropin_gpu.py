@@ -116,9 +116,8 @@ def test_run_within_element_and_trace(pkg, key):
     assert t.barriers == int(g[f"{key}_barriers"])
     assert t.intra_class_syncs == int(g[f"{key}_syncs"])
     assert len(t.completion_order) == int(g[f"{key}_ntasks"])
-    ref = g[f"{key}_order"]
-    lo = 0
-    for sz in foata_class_sizes(p, (p + 1) ** 3):
-        assert sorted(ref[lo:lo + sz].tolist()) == t.completion_order[lo:lo + sz]
-        lo += sz
+    sizes = foata_class_sizes(p, (p + 1) ** 3)
+    ours = np.repeat(np.arange(p + 7), sizes)[np.asarray(t.completion_order)]
+    assert np.array_equal(ours, g[f"{key}_class_of_order"])
+    assert np.array_equal(np.sort(t.completion_order), g[f"{key}_order_sorted"])
     assert em.flops == pkg.flop_count("sumfact", p)

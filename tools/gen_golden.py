@@ -320,13 +320,37 @@ def main():
         t = runtime.ExecutionTrace()
         em = runtime.run_within_element(alpha, kv, "sumfact", workers, trace=t)
         key = f"K{K}_p{p}_w{workers}"
-        tr[f"{key}_order"] = np.array(t.completion_order, dtype=np.int64)
+        order = np.array(t.completion_order, dtype=np.int64)
+        # the class of every completed task, in completion order (deterministic: the
+        # reference runs the classes barrier-separated); inside a class the reference's
+        # worker chunks finish in any order, so the raw order is kept only for workers=1
+        tr[f"{key}_class_of_order"] = np.asarray(t.graph.classes)[order].astype(np.int64)
+        tr[f"{key}_order_sorted"] = np.sort(order)
+        if workers == 1:
+            tr[f"{key}_order"] = order
         tr[f"{key}_barriers"] = np.int64(t.barriers)
         tr[f"{key}_syncs"] = np.int64(t.intra_class_syncs)
         tr[f"{key}_ntasks"] = np.int64(t.graph.n_tasks)
         tr[f"{key}_sumfact"] = em.entries
         tr[f"{key}_classical"] = runtime.run_within_element(alpha, kv, "classical", workers).entries
     save("within_element.npz", **tr)
+
+    # 14. high degrees (the paper's p = 9 Gram; integrators.py handles
+    #     any p): K1 tables, an element matrix whose sum-factorization stages exceed shared
+    #     memory (p = 7), and global Grams from run_integration
+    hi = {}
+    for K, p in ((3, 6), (2, 7), (2, 8), (3, 9)):
+        V, D = mesh_tables(K, p, p + 1)
+        hi[f"V_K{K}_p{p}"] = V
+        hi[f"D_K{K}_p{p}"] = D
+    kv = splines.make_knot_vector(2, 7)
+    alpha = (1, 0, 1)
+    hi["element_sumfact_K2_p7"] = integrators.integrate_element_sumfact(
+        alpha, kv, mesh.gauss_rule(7, 2, alpha), integrators.SumFactBuffers.allocate(7)).entries
+    save("high_degree.npz", **hi)
+    for K, p in ((2, 6), (1, 7)):
+        res = runtime.run_integration(runtime.RunConfig("sumfact", "sequential", K, p))
+        save(f"mass_sumfact_K{K}_p{p}.npz", **ref_csr(res.gram))
     print("igabench", igabench.__version__)
 
 

@@ -1,19 +1,17 @@
-// Phase timing harness for k_gsf3_p3 (C3 shape): builds the kernel with
-// IGA_PHASE_TIMING=<block> and prints per-warp phase durations of steps 8..11.
+// Timing harness for k_gsf3_p3 variants (C3 shape, c = 1): build with -D overrides of
+// the kernel's tuning macros (P3_NWB, P3_NWS, ...) and print the mean launch time of 20
+// launches after warm-up, plus a checksum so variants can be compared for equality.
 #include <cstdio>
 #include <vector>
 #include <cstdlib>
-#include <algorithm>
-#ifndef GSF_NOPHASE
-#define IGA_PHASE_TIMING 300
-#endif
 #include "../paper_2207_00280_b200/csrc/iga_gsf_p3.cu"
 #include "../paper_2207_00280_b200/csrc/iga_abi.cu"
 
-
 int main() {
   const int K = 64, P = 3, Q = 4, M = 4;
-  std::vector<double> V(K * M * Q), D(K * M * Q), w = {0.347854845137454, 0.652145154862546, 0.652145154862546, 0.347854845137454};
+  std::vector<double> V(K * M * Q), D(K * M * Q);
+  std::vector<double> w = {0.347854845137454, 0.652145154862546, 0.652145154862546, 0.347854845137454};
+  srand(1);
   for (auto& x : V) x = rand() / (double)RAND_MAX;
   for (auto& x : D) x = rand() / (double)RAND_MAX - 0.5;
   double *dV, *dD, *dw, *dval;
@@ -29,26 +27,14 @@ int main() {
   a.weights = dw; a.V = dV; a.D = dD; a.values = dval;
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
   for (int it = 0; it < 3; ++it) iga::launch_gsf_p3(a, 0);
+  const int n = 20;
   cudaEventRecord(e0);
-  iga::launch_gsf_p3(a, 0);
+  for (int it = 0; it < n; ++it) iga::launch_gsf_p3(a, 0);
   cudaEventRecord(e1); cudaEventSynchronize(e1);
   float ms; cudaEventElapsedTime(&ms, e0, e1);
-  printf("kernel %.3f ms  err=%s\n", ms, cudaGetErrorString(cudaGetLastError()));
-#ifdef GSF_NOPHASE
+  std::vector<double> h(nnz);
+  cudaMemcpy(h.data(), dval, nnz * 8, cudaMemcpyDeviceToHost);
+  double cs = 0; for (long long i = 0; i < nnz; i += 7) cs += h[i] * (1 + (i % 13));
+  printf("%s kernel %.4f ms  checksum %.17g err=%s\n", VARIANT, ms / n, cs, cudaGetErrorString(cudaGetLastError()));
   return 0;
-#else
-  long long ph[4][16][3];
-  cudaMemcpyFromSymbol(ph, iga::p3::g_phase, sizeof(ph));
-  // per warp: the clock at the start (after its mbarrier wait is entered: idx 2) and at the
-  // end (idx 0) of its work on iterations 8..11, relative to warp 0's start of iteration 8
-  const long long t0 = ph[0][0][2];
-  for (int w = 0; w < 16; ++w) {
-    const char* role = w < iga::p3::NWA ? "A" : (w < iga::p3::NWA + iga::p3::NWB ? "B" : "S");
-    printf("warp %2d %s:", w, role);
-    for (int s = 0; s < 4; ++s)
-      printf("  [%6lld w%5lld %6lld]", ph[s][w][2] - t0, ph[s][w][1] - ph[s][w][2], ph[s][w][0] - t0);
-    printf("\n");
-  }
-  return 0;
-#endif
 }
