@@ -66,6 +66,15 @@ typedef struct iga_problem {
                              with it the integration kernel reads the 1D integrals instead of
                              forming them in every CTA (a shorter prologue).  Read-only: the
                              same buffer may feed concurrent launches on several streams. */
+  /* General open knot vector, the same on every axis like the
+   * reference's single KnotVector: knots [K + 2p + 1] non-decreasing, p + 1 equal at each
+   * end, K non-empty spans (element e = [t_{p+e}, t_{p+e+1}]), or NULL for the open uniform
+   * vector of make_knot_vector (splines.py:59-75).  With knots, element e's Jacobian is
+   * folded into the per-axis weights elem_weights [K][q] = w_k h_e / 2 (h_e the span
+   * length; iga_mesh_tables_general writes them) and jac must be 1.0; the CSR pattern is
+   * unchanged. */
+  const double* knots;
+  const double* elem_weights;
 } iga_problem;
 
 const char* iga_last_error(void);
@@ -78,11 +87,20 @@ int32_t iga_abi_version(void);
 int32_t iga_mesh_tables(int32_t K, int32_t p, int32_t q, const double* ref_nodes, double* vals,
                         double* ders, void* stream);
 
+/* K1 on a general open knot vector knots [K + 2p + 1]: tables at the Gauss points mapped
+ * into each span (x = lo + (ref + 1) h / 2, h = hi - lo) and the per-element weights
+ * elem_weights [K][q] = weights[k] * (h_e / 2) (either output may be NULL: not written). */
+int32_t iga_mesh_tables_general(int32_t K, int32_t p, int32_t q, const double* knots,
+                                const double* ref_nodes, const double* weights, double* vals,
+                                double* ders, double* elem_weights, void* stream);
+
 /* K1' -- nonzero basis values/derivatives at arbitrary points:
  * vals/ders [n][p+1] for point x[i] in element elem[i]
- * (splines.eval_nonzero_basis / eval_nonzero_basis_derivatives, splines.py:127-161). */
-int32_t iga_basis_eval(int32_t K, int32_t p, int64_t n, const int32_t* elem, const double* x,
-                       double* vals, double* ders, void* stream);
+ * (splines.eval_nonzero_basis / eval_nonzero_basis_derivatives, splines.py:127-161);
+ * knots: device general knot vector [K + 2p + 1], or NULL for the open uniform one. */
+int32_t iga_basis_eval(int32_t K, int32_t p, const double* knots, int64_t n,
+                       const int32_t* elem, const double* x, double* vals, double* ders,
+                       void* stream);
 
 /* eval_basis / eval_basis_order0 (splines.py:78-118) on any non-decreasing knot vector
  * knots[n_knots]: out[i] = B_{index[i], order}(x[i]) by the reference's two-term
@@ -98,9 +116,11 @@ int32_t iga_eval_basis(const double* knots, int32_t n_knots, int32_t order, int6
  *   m(I,J) = sum_e sum_k w_k V_e(I-e,k) V_e(J-e,k)   (k(I,J): the same with derivatives)
  * over all elements, elements ascending -- the 1D factors of the Kronecker form of the
  * reference's element quadrature summed by assemble (integrators.py:77-151,
- * assembly.py:80-82).  Uses prob->K, p, q, op, weights. */
+ * assembly.py:80-82).  Uses prob->K, p, q, op, weights and, for a general knot vector
+ * (prob->knots), writes the per-element weights into elem_weights [K][q] (the same values
+ * as iga_mesh_tables_general; NULL for the uniform mesh). */
 int32_t iga_band_tables(const iga_problem* prob, const double* ref_nodes, double* vals,
-                        double* ders, double* band, void* stream);
+                        double* ders, double* band, double* elem_weights, void* stream);
 
 /* Host arithmetic: number of CSR entries in global rows [row_begin, row_end). */
 int64_t iga_csr_nnz(int32_t dim, int32_t K, int32_t p, int64_t row_begin, int64_t row_end);

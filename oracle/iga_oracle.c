@@ -49,6 +49,33 @@ static void abs_inplace(double* a, size_t n) {
   for (size_t i = 0; i < n; ++i) a[i] = fabs(a[i]);
 }
 
+/* General open knot vector mode (off by default): the tables are
+ * evaluated from these knots at x = lo + (ref+1)*(h/2) in each span [t_{p+e}, t_{p+e+1}],
+ * and element e's Jacobian is folded into per-axis weights wt[e][k] = w_k * (h_e / 2)
+ * with jac = 1 -- the definition tools/gen_golden.py (section 12) feeds the reference's own
+ * kernels with. */
+static double* g_knots = NULL;
+static int g_nknots = 0;
+static double* g_wt = NULL;
+void orc_set_knots(const double* t, int nt, const double* wt, int K, int q) {
+  free(g_knots);
+  free(g_wt);
+  g_knots = NULL;
+  g_wt = NULL;
+  g_nknots = 0;
+  if (t == NULL) return;
+  g_knots = (double*)malloc(sizeof(double) * nt);
+  memcpy(g_knots, t, sizeof(double) * nt);
+  g_nknots = nt;
+  g_wt = (double*)malloc(sizeof(double) * K * q);
+  memcpy(g_wt, wt, sizeof(double) * K * q);
+}
+
+/* per-axis weights of element alpha[d] (general knots) or the reference weights */
+static inline const double* axis_w(const double* w, const int* alpha, int d, int q) {
+  return g_wt ? g_wt + (size_t)alpha[d] * q : w;
+}
+
 /* ---------------------------------------------------------------- splines */
 
 /* splines.py:59-75 make_knot_vector: p+1 zeros, arange(1,K)/K, p+1 ones. */
@@ -99,13 +126,20 @@ void orc_nonzero_basis(const double* t, int nt, int p, int e, double x, double* 
 void orc_tables(int K, int p, int q, const double* ref_nodes, double* V, double* D) {
   int nt = K + 2 * p + 1;
   double* t = (double*)malloc(sizeof(double) * nt);
-  orc_knots(K, p, t);
+  if (g_knots && g_nknots == nt)
+    memcpy(t, g_knots, sizeof(double) * nt);
+  else
+    orc_knots(K, p, t);
   int m = p + 1;
   double h = 1.0 / (double)K;
   double vals[32], ders[32];
   for (int e = 0; e < K; ++e) {
     for (int k = 0; k < q; ++k) {
       double x = (double)e * h + (ref_nodes[k] + 1.0) * (h / 2.0);
+      if (g_knots) {
+        double lo = t[p + e], he = t[p + e + 1] - t[p + e];
+        x = lo + (ref_nodes[k] + 1.0) * (he / 2.0);
+      }
       orc_nonzero_basis(t, nt, p, e, x, vals, D ? ders : NULL);
       for (int r = 0; r < m; ++r) {
         V[((size_t)e * m + r) * q + k] = vals[r];
@@ -128,8 +162,8 @@ static inline const double* pick(const double* V, const double* D, int axis, int
  * computed, mirrored).  tabs: per-axis value tables tv[d] and derivative
  * tables td[d] ([m][q] each); coef: q^dim factors (k1 slowest) or NULL. */
 static void classical_term(int dim, int m, int q, const double* b0, const double* b1,
-                           const double* b2, const double* w, double jac, const double* coef,
-                           double* out) {
+                           const double* b2, const double* w0, const double* w1,
+                           const double* w2, double jac, const double* coef, double* out) {
   int n = dim == 3 ? m * m * m : m * m;
   int m2 = m * m;
   for (int row = 0; row < n; ++row) {
@@ -142,7 +176,7 @@ static void classical_term(int dim, int m, int q, const double* b0, const double
           for (int k2 = 0; k2 < q; ++k2)
             for (int k3 = 0; k3 < q; ++k3) {
               double v = b0[i1 * q + k1] * b0[j1 * q + k1] * b1[i2 * q + k2] * b1[j2 * q + k2] *
-                         b2[i3 * q + k3] * b2[j3 * q + k3] * w[k1] * w[k2] * w[k3] * jac;
+                         b2[i3 * q + k3] * b2[j3 * q + k3] * w0[k1] * w1[k2] * w2[k3] * jac;
               if (coef) v = v * coef[(k1 * q + k2) * q + k3];
               acc += v;
             }
@@ -152,7 +186,7 @@ static void classical_term(int dim, int m, int q, const double* b0, const double
         for (int k1 = 0; k1 < q; ++k1)
           for (int k2 = 0; k2 < q; ++k2) {
             double v = b0[i1 * q + k1] * b0[j1 * q + k1] * b1[i2 * q + k2] * b1[j2 * q + k2] *
-                       w[k1] * w[k2] * jac;
+                       w0[k1] * w1[k2] * jac;
             if (coef) v = v * coef[k1 * q + k2];
             acc += v;
           }
@@ -166,8 +200,9 @@ static void classical_term(int dim, int m, int q, const double* b0, const double
 /* integrators.py:112-151 sumfact_kernel (3D) with the coefficient appended to
  * the stage-1 product; 2D = stage 1 then the last stage over axis 2. */
 static void sumfact_term(int dim, int m, int q, const double* b0, const double* b1,
-                         const double* b2, const double* w, double jac, const double* coef,
-                         double* Dbuf, double* Cbuf, double* out) {
+                         const double* b2, const double* w0, const double* w1, const double* w2,
+                         double jac, const double* coef, double* Dbuf, double* Cbuf,
+                         double* out) {
   int m2 = m * m;
   if (dim == 3) {
     int n = m2 * m;
@@ -178,7 +213,7 @@ static void sumfact_term(int dim, int m, int q, const double* b0, const double* 
         for (int k2 = 0; k2 < q; ++k2)
           for (int k3 = 0; k3 < q; ++k3)
             for (int k1 = 0; k1 < q; ++k1) {
-              double v = b0[i1 * q + k1] * b0[j1 * q + k1] * w[k1] * jac;
+              double v = b0[i1 * q + k1] * b0[j1 * q + k1] * w0[k1] * jac;
               if (coef) v = v * coef[(k1 * q + k2) * q + k3];
               Dbuf[((i1 * m + j1) * q + k2) * q + k3] += v;
             }
@@ -190,7 +225,7 @@ static void sumfact_term(int dim, int m, int q, const double* b0, const double* 
               for (int k2 = 0; k2 < q; ++k2)
                 Cbuf[(((i2 * m + i1) * m + j2) * m + j1) * q + k3] +=
                     b1[i2 * q + k2] * b1[j2 * q + k2] * Dbuf[((i1 * m + j1) * q + k2) * q + k3] *
-                    w[k2];
+                    w1[k2];
     for (int row = 0; row < n; ++row)
       for (int col = 0; col <= row; ++col) {
         int i1 = row / m2, i2 = (row / m) % m, i3 = row % m;
@@ -198,7 +233,7 @@ static void sumfact_term(int dim, int m, int q, const double* b0, const double* 
         double acc = 0.0;
         for (int k3 = 0; k3 < q; ++k3)
           acc += b2[i3 * q + k3] * b2[j3 * q + k3] *
-                 Cbuf[(((i2 * m + i1) * m + j2) * m + j1) * q + k3] * w[k3];
+                 Cbuf[(((i2 * m + i1) * m + j2) * m + j1) * q + k3] * w2[k3];
         out[row * n + col] = acc;
         out[col * n + row] = acc;
       }
@@ -209,7 +244,7 @@ static void sumfact_term(int dim, int m, int q, const double* b0, const double* 
       for (int j1 = 0; j1 < m; ++j1)
         for (int k2 = 0; k2 < q; ++k2)
           for (int k1 = 0; k1 < q; ++k1) {
-            double v = b0[i1 * q + k1] * b0[j1 * q + k1] * w[k1] * jac;
+            double v = b0[i1 * q + k1] * b0[j1 * q + k1] * w0[k1] * jac;
             if (coef) v = v * coef[k1 * q + k2];
             Dbuf[(i1 * m + j1) * q + k2] += v;
           }
@@ -218,7 +253,7 @@ static void sumfact_term(int dim, int m, int q, const double* b0, const double* 
         int i1 = row / m, i2 = row % m, j1 = col / m, j2 = col % m;
         double acc = 0.0;
         for (int k2 = 0; k2 < q; ++k2)
-          acc += b1[i2 * q + k2] * b1[j2 * q + k2] * Dbuf[(i1 * m + j1) * q + k2] * w[k2];
+          acc += b1[i2 * q + k2] * b1[j2 * q + k2] * Dbuf[(i1 * m + j1) * q + k2] * w1[k2];
         out[row * n + col] = acc;
         out[col * n + row] = acc;
       }
@@ -272,10 +307,14 @@ static void element_scratch(int dim, int p, int q, int op, int method, const dou
     const double* b1 = pick(tv[1], td[1], 1, term);
     const double* b2 = pick(tv[2], td[2], 2, term);
     double* dst = t == 0 ? out : tmp;
+    const double* w0 = axis_w(w, alpha, 0, q);
+    const double* w1 = axis_w(w, alpha, 1, q);
+    const double* w2 = axis_w(w, alpha, dim == 3 ? 2 : 1, q);
+    const double jj = g_wt ? 1.0 : jac;
     if (method == 0)
-      classical_term(dim, m, q, b0, b1, b2, w, jac, coef, dst);
+      classical_term(dim, m, q, b0, b1, b2, w0, w1, w2, jj, coef, dst);
     else
-      sumfact_term(dim, m, q, b0, b1, b2, w, jac, coef, Dbuf, Cbuf, dst);
+      sumfact_term(dim, m, q, b0, b1, b2, w0, w1, w2, jj, coef, Dbuf, Cbuf, dst);
     if (t > 0)
       for (int i = 0; i < n * n; ++i) out[i] = out[i] + tmp[i];
   }
@@ -304,6 +343,10 @@ static void classical_row(int dim, int p, int q, int op, const double* V, const 
     for (int d = 0; d < dim; ++d) terms[nterm++] = d;
     if (op == ORC_OP_STIFFNESS_MASS) terms[nterm++] = dim;
   }
+  const double* w0 = axis_w(w, alpha, 0, q);
+  const double* w1 = axis_w(w, alpha, 1, q);
+  const double* w2 = axis_w(w, alpha, dim == 3 ? 2 : 1, q);
+  if (g_wt) jac = 1.0;
   for (int j = 0; j < n; ++j) {
     int row = il > j ? il : j, col = il > j ? j : il;
     double total = 0.0;
@@ -319,7 +362,7 @@ static void classical_row(int dim, int p, int q, int op, const double* V, const 
           for (int k2 = 0; k2 < q; ++k2)
             for (int k3 = 0; k3 < q; ++k3) {
               double v = b0[i1 * q + k1] * b0[j1 * q + k1] * b1[i2 * q + k2] * b1[j2 * q + k2] *
-                         b2[i3 * q + k3] * b2[j3 * q + k3] * w[k1] * w[k2] * w[k3] * jac;
+                         b2[i3 * q + k3] * b2[j3 * q + k3] * w0[k1] * w1[k2] * w2[k3] * jac;
               if (coef) v = v * coef[(k1 * q + k2) * q + k3];
               acc += v;
             }
@@ -328,7 +371,7 @@ static void classical_row(int dim, int p, int q, int op, const double* V, const 
         for (int k1 = 0; k1 < q; ++k1)
           for (int k2 = 0; k2 < q; ++k2) {
             double v = b0[i1 * q + k1] * b0[j1 * q + k1] * b1[i2 * q + k2] * b1[j2 * q + k2] *
-                       w[k1] * w[k2] * jac;
+                       w0[k1] * w1[k2] * jac;
             if (coef) v = v * coef[k1 * q + k2];
             acc += v;
           }

@@ -30,7 +30,7 @@ from .integrators import (
     integrate_element_sumfact,
 )
 from .operator import MatrixFreeOperator, cg
-from .mesh import QuadratureRule, element_list, gauss_rule, local_index, support_set
+from .mesh import QuadratureRule, element_list, gauss_rule, knot_rule, local_index, support_set
 from .runtime import (
     ExecutionTrace,
     IntegrationRuntime,
@@ -50,7 +50,9 @@ from .splines import (
     eval_basis_order0,
     eval_nonzero_basis,
     eval_nonzero_basis_derivatives,
+    check_knots,
     find_element,
+    make_general_knot_vector,
     make_knot_vector,
 )
 
@@ -84,6 +86,9 @@ __all__ = [
     "find_element",
     "flop_count",
     "gauss_rule",
+    "knot_rule",
+    "make_general_knot_vector",
+    "check_knots",
     "grams_bitwise_equal",
     "integrate_element_classical",
     "integrate_element_sumfact",

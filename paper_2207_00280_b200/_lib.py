@@ -26,6 +26,7 @@ EXPORTS = (
     "iga_last_error",
     "iga_abi_version",
     "iga_mesh_tables",
+    "iga_mesh_tables_general",
     "iga_band_tables",
     "iga_basis_eval",
     "iga_eval_basis",
@@ -59,6 +60,8 @@ class IgaProblem(ctypes.Structure):
         ("tables_v", ctypes.c_void_p),
         ("tables_d", ctypes.c_void_p),
         ("band", ctypes.c_void_p),
+        ("knots", ctypes.c_void_p),
+        ("elem_weights", ctypes.c_void_p),
     ]
 
 
@@ -86,8 +89,9 @@ def load():
     L.iga_last_error.restype = ctypes.c_char_p
     L.iga_abi_version.restype = i32
     L.iga_mesh_tables.argtypes = [i32, i32, i32, vp, vp, vp, vp]
-    L.iga_band_tables.argtypes = [ctypes.POINTER(IgaProblem), vp, vp, vp, vp, vp]
-    L.iga_basis_eval.argtypes = [i32, i32, i64, vp, vp, vp, vp, vp]
+    L.iga_band_tables.argtypes = [ctypes.POINTER(IgaProblem), vp, vp, vp, vp, vp, vp]
+    L.iga_mesh_tables_general.argtypes = [i32, i32, i32, vp, vp, vp, vp, vp, vp, vp]
+    L.iga_basis_eval.argtypes = [i32, i32, vp, i64, vp, vp, vp, vp, vp]
     L.iga_eval_basis.argtypes = [vp, i32, i32, i64, vp, vp, vp, vp]
     L.iga_csr_nnz.argtypes = [i32, i32, i32, i64, i64]
     L.iga_csr_nnz.restype = i64
@@ -102,7 +106,7 @@ def load():
     L.iga_apply.argtypes = [ctypes.POINTER(IgaProblem), dp, dp, vp, vp, vp]
     L.iga_write_matrix_market.argtypes = [i32, i32, i32, vp, ctypes.c_char_p, i32, vp]
     L.iga_write_matrix_market_host.argtypes = [i32, i32, i32, vp, ctypes.c_char_p, i32]
-    for name in ("iga_mesh_tables", "iga_band_tables", "iga_basis_eval", "iga_eval_basis", "iga_csr_pattern", "iga_element_matrices",
+    for name in ("iga_mesh_tables", "iga_mesh_tables_general", "iga_band_tables", "iga_basis_eval", "iga_eval_basis", "iga_csr_pattern", "iga_element_matrices",
                  "iga_integrate_assemble", "iga_assemble_elements", "iga_axpy", "iga_spmv",
                  "iga_apply", "iga_write_matrix_market", "iga_write_matrix_market_host"):
         getattr(L, name).restype = i32

@@ -84,37 +84,43 @@ int blocks_per_sm_once(const void* fn, int threads, size_t smem) {
 // bottom-up Cox-de Boor triangle (bitwise equal to splines.py:108-161).
 template <int P>
 __global__ void k_mesh_tables(int K, int q, const double* __restrict__ ref, double* __restrict__ V,
-                              double* __restrict__ D) {
+                              double* __restrict__ D, const double* __restrict__ knots,
+                              const double* __restrict__ w, double* __restrict__ wt) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= K * q) return;
   const int e = t / q, k = t % q;
-  const double x = map_node(e, ref[k], K);
+  const double x = map_node(e, ref[k], K, P, knots);
   double vals[P + 1], ders[P + 1];
-  cox_de_boor<P>(e, x, K, vals, D ? ders : nullptr);
+  cox_de_boor<P>(e, x, K, vals, D ? ders : nullptr, knots);
 #pragma unroll
   for (int r = 0; r <= P; ++r) {
-    V[((size_t)e * (P + 1) + r) * q + k] = vals[r];
+    if (V) V[((size_t)e * (P + 1) + r) * q + k] = vals[r];
     if (D) D[((size_t)e * (P + 1) + r) * q + k] = ders[r];
+  }
+  if (wt) {  // w_k * (h_e / 2): the element's Jacobian folded into this axis' weights
+    const double h = sub(__ldg(knots + P + e + 1), __ldg(knots + P + e));
+    wt[e * q + k] = mul(w[k], dvd(h, 2.0));
   }
 }
 
 template <int P>
 struct MeshTablesLaunch {
-  static int run(int K, int q, const double* ref, double* V, double* D, cudaStream_t s) {
+  static int run(int K, int q, const double* ref, double* V, double* D, const double* knots,
+                 const double* w, double* wt, cudaStream_t s) {
     const int n = K * q;
-    k_mesh_tables<P><<<(n + 127) / 128, 128, 0, s>>>(K, q, ref, V, D);
+    k_mesh_tables<P><<<(n + 127) / 128, 128, 0, s>>>(K, q, ref, V, D, knots, w, wt);
     return check_cuda(cudaGetLastError(), "iga_mesh_tables launch");
   }
 };
 
 template <int P>
-__global__ void k_basis_eval(int K, int64_t n, const int32_t* __restrict__ elem,
-                             const double* __restrict__ x, double* __restrict__ V,
-                             double* __restrict__ D) {
+__global__ void k_basis_eval(int K, const double* __restrict__ knots, int64_t n,
+                             const int32_t* __restrict__ elem, const double* __restrict__ x,
+                             double* __restrict__ V, double* __restrict__ D) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
   double vals[P + 1], ders[P + 1];
-  cox_de_boor<P>(elem[t], x[t], K, vals, D ? ders : nullptr);
+  cox_de_boor<P>(elem[t], x[t], K, vals, D ? ders : nullptr, knots);
 #pragma unroll
   for (int r = 0; r <= P; ++r) {
     V[t * (P + 1) + r] = vals[r];
@@ -124,10 +130,10 @@ __global__ void k_basis_eval(int K, int64_t n, const int32_t* __restrict__ elem,
 
 template <int P>
 struct BasisEvalLaunch {
-  static int run(int K, int64_t n, const int32_t* elem, const double* x, double* V, double* D,
-                 cudaStream_t s) {
+  static int run(int K, const double* knots, int64_t n, const int32_t* elem, const double* x,
+                 double* V, double* D, cudaStream_t s) {
     if (n == 0) return IGA_OK;
-    k_basis_eval<P><<<(unsigned)((n + 127) / 128), 128, 0, s>>>(K, n, elem, x, V, D);
+    k_basis_eval<P><<<(unsigned)((n + 127) / 128), 128, 0, s>>>(K, knots, n, elem, x, V, D);
     return check_cuda(cudaGetLastError(), "iga_basis_eval launch");
   }
 };
@@ -251,16 +257,30 @@ int32_t iga_mesh_tables(int32_t K, int32_t p, int32_t q, const double* ref_nodes
   if (p < 0) return fail_einval("degree must be >= 0, got %d", p);
   if (q < 1 || q > kMaxQ) return fail_einval("quadrature points q=%d outside 1..%d", q, kMaxQ);
   if (!ref_nodes || !vals) return fail_einval("null pointer");
-  return dispatch_p_all<MeshTablesLaunch>(p, K, q, ref_nodes, vals, ders, as_stream(stream));
+  return dispatch_p_all<MeshTablesLaunch>(p, K, q, ref_nodes, vals, ders, nullptr, nullptr,
+                                          nullptr, as_stream(stream));
 }
 
-int32_t iga_basis_eval(int32_t K, int32_t p, int64_t n, const int32_t* elem, const double* x,
-                       double* vals, double* ders, void* stream) {
+int32_t iga_mesh_tables_general(int32_t K, int32_t p, int32_t q, const double* knots,
+                                const double* ref_nodes, const double* weights, double* vals,
+                                double* ders, double* elem_weights, void* stream) {
+  if (K < 1) return fail_einval("element count must be >= 1, got %d", K);
+  if (p < 0) return fail_einval("degree must be >= 0, got %d", p);
+  if (q < 1 || q > kMaxQ) return fail_einval("quadrature points q=%d outside 1..%d", q, kMaxQ);
+  if (!knots || !ref_nodes) return fail_einval("null pointer");
+  if (elem_weights && !weights) return fail_einval("elem_weights need the reference weights");
+  return dispatch_p_all<MeshTablesLaunch>(p, K, q, ref_nodes, vals, ders, knots, weights,
+                                          elem_weights, as_stream(stream));
+}
+
+int32_t iga_basis_eval(int32_t K, int32_t p, const double* knots, int64_t n,
+                       const int32_t* elem, const double* x, double* vals, double* ders,
+                       void* stream) {
   if (K < 1) return fail_einval("element count must be >= 1, got %d", K);
   if (p < 0) return fail_einval("degree must be >= 0, got %d", p);
   if (n < 0) return fail_einval("negative point count");
   if (n > 0 && (!elem || !x || !vals)) return fail_einval("null pointer");
-  return dispatch_p_all<BasisEvalLaunch>(p, K, n, elem, x, vals, ders, as_stream(stream));
+  return dispatch_p_all<BasisEvalLaunch>(p, K, knots, n, elem, x, vals, ders, as_stream(stream));
 }
 
 int64_t iga_csr_nnz(int32_t dim, int32_t K, int32_t p, int64_t row_begin, int64_t row_end) {

@@ -18,6 +18,7 @@ namespace iga {
 struct ApplyArgs {
   int K;
   double alpha, beta, jac, coef_scalar;
+  const double* wt;  // [K][Q] per-element weights (general knots), or null
   const double* coef;
   const double* weights;
   const double* V;
@@ -110,12 +111,12 @@ __global__ void __launch_bounds__(256, 4) k_apply3(ApplyArgs a) {
         g1 += u1[b][i0][k1][k2] * tv01[0][i0][k0];
         g2 += u2[b][i0][k1][k2] * tv01[0][i0][k0];
       }
-      double Wt = w[k0] * w[k1] * w[k2] * a.jac;
+      double Wt = 0.0;
       if (b < ne) {
+        Wt = axis_w(w, a.wt, e0, k0, Q) * axis_w(w, a.wt, e1, k1, Q) * axis_w(w, a.wt, eb + b, k2, Q) *
+             a.jac;
         const int64_t el = ((int64_t)e0 * K + e1) * K + eb + b;
         Wt *= a.coef ? a.coef[el * (Q * Q * Q) + k] : a.coef_scalar;
-      } else {
-        Wt = 0.0;
       }
       f[0][b][k0][k1][k2] = Wt * a.alpha * val;
       f[1][b][k0][k1][k2] = Wt * a.beta * g0;
@@ -219,7 +220,7 @@ __global__ void __launch_bounds__(256) k_apply_kron(ApplyArgs a) {
   double2* AB = reinterpret_cast<double2*>(X + W * W * ZH);  // [W][W][ZC]
   double2* CD = AB + W * W * ZC;                           // [W][T][ZC]
   build_band_tables<P, Q>(a.V, a.D, a.weights, K, stiff, 0, K, false, tb, work,
-                          apply_kron_work<P>(0), w_s, tid, nt);
+                          apply_kron_work<P>(0), w_s, tid, nt, a.wt);
   const double cj = a.jac * a.coef_scalar;
   const int nblk = (N + T - 1) / T;
   for (int blk = blockIdx.x; blk < nblk * nblk; blk += gridDim.x) {
@@ -316,7 +317,10 @@ extern "C" int32_t iga_apply(const iga_problem* prob, double alpha, double beta,
   const int64_t N = (int64_t)prob->K + prob->p;
   cudaStream_t s = as_stream(stream);
   ApplyArgs a;
+  if (prob->knots && !prob->elem_weights)
+    return fail_einval("a general knot vector needs elem_weights (iga_mesh_tables_general)");
   a.K = prob->K; a.alpha = alpha; a.beta = beta; a.jac = prob->jac;
+  a.wt = prob->knots ? prob->elem_weights : nullptr;
   a.coef_scalar = prob->coef_scalar; a.coef = prob->coef; a.weights = prob->weights;
   a.V = prob->tables_v; a.D = prob->tables_d; a.x = x; a.y = y;
   if (!prob->coef) {  // scalar coefficient: separable operator, y written once per dof

@@ -9,6 +9,8 @@ namespace iga {
 struct ElemArgs {
   int dim, K, q, op, method;
   double jac, coef_scalar;
+  const double* knots;         // general knot vector [K + 2p + 1], or null (open uniform)
+  const double* wt;            // [K][q] per-element weights of a general knot vector, or null
   const double* coef;
   const double* weights;
   const double* ref_nodes;
@@ -24,6 +26,7 @@ struct ElemArgs {
 
 struct ScatterArgs {
   int dim, K, op;
+  const double* wt;               // [K][Q] per-element weights (general knots), or null
   int el_begin, el_end;           // slab along the slowest axis
   int64_t row_first, row_last;    // global rows [row_first, row_last) written
   int64_t base;                   // rowptr(row_first)
@@ -46,6 +49,7 @@ struct ScatterArgs {
 
 struct GsfArgs {
   int K, op;
+  const double* wt;              // [K][Q] per-element weights (general knots), or null
   int el_begin, el_end;          // element slab along axis 0
   int plane_begin, plane_end;    // row planes I0 computed
   int segs;                      // segments of the element column e2 per tile (>= 1)
@@ -62,6 +66,7 @@ struct GsfArgs {
 
 struct KronArgs {
   int K, op;
+  const double* wt;              // [K][Q] per-element weights (general knots), or null
   int el_begin, el_end;          // element slab along axis 0
   int plane_begin, plane_end;    // row planes I0 written
   int64_t base;                  // rowptr of (plane_begin, 0, 0)

@@ -12,7 +12,8 @@ namespace iga {
 // derivative products, elements ascending, quadrature points ascending.
 template <int P, int Q>
 __device__ __forceinline__ double2 band1d(const double* V, const double* D, int K, const double* w,
-                                          int I, int d, int e_lo, int e_hi, bool stiff) {
+                                          int I, int d, int e_lo, int e_hi, bool stiff,
+                                          const double* wt = nullptr) {
   constexpr int M = P + 1;
   const int J = I + d - P;
   double m = 0.0, k = 0.0;
@@ -25,11 +26,11 @@ __device__ __forceinline__ double2 band1d(const double* V, const double* D, int 
       const double* Ve = V + e * M * Q;
       const int i = I - e, j = J - e;
 #pragma unroll
-      for (int q = 0; q < Q; ++q) m += (w[q] * Ve[i * Q + q]) * Ve[j * Q + q];
+      for (int q = 0; q < Q; ++q) m += (axis_w(w, wt, e, q, Q) * Ve[i * Q + q]) * Ve[j * Q + q];
       if (stiff) {
         const double* De = D + e * M * Q;
 #pragma unroll
-        for (int q = 0; q < Q; ++q) k += (w[q] * De[i * Q + q]) * De[j * Q + q];
+        for (int q = 0; q < Q; ++q) k += (axis_w(w, wt, e, q, Q) * De[i * Q + q]) * De[j * Q + q];
       }
     }
   }
@@ -41,7 +42,8 @@ __device__ __forceinline__ double2 band1d(const double* V, const double* D, int 
 // over its points first, then the elements ascending), so it reproduces those bits
 template <int P, int Q>
 __device__ __forceinline__ double2 band1d_el(const double* V, const double* D, int K, const double* w,
-                                             int I, int d, int e_lo, int e_hi, bool stiff) {
+                                             int I, int d, int e_lo, int e_hi, bool stiff,
+                                             const double* wt = nullptr) {
   constexpr int M = P + 1;
   const int J = I + d - P;
   double m = 0.0, k = 0.0;
@@ -51,11 +53,11 @@ __device__ __forceinline__ double2 band1d_el(const double* V, const double* D, i
     const int i = I - e, j = J - e;
     double me = 0.0, ke = 0.0;
 #pragma unroll
-    for (int q = 0; q < Q; ++q) me += (w[q] * Ve[i * Q + q]) * Ve[j * Q + q];
+    for (int q = 0; q < Q; ++q) me += (axis_w(w, wt, e, q, Q) * Ve[i * Q + q]) * Ve[j * Q + q];
     if (stiff) {
       const double* De = D + e * M * Q;
 #pragma unroll
-      for (int q = 0; q < Q; ++q) ke += (w[q] * De[i * Q + q]) * De[j * Q + q];
+      for (int q = 0; q < Q; ++q) ke += (axis_w(w, wt, e, q, Q) * De[i * Q + q]) * De[j * Q + q];
     }
     m += me;
     k += ke;
@@ -74,7 +76,7 @@ template <int P, int Q>
 __device__ void build_band_tables(const double* V, const double* D, const double* weights, int K,
                                   bool stiff, int slab_lo, int slab_hi, bool with_slab,
                                   double2* tb, double* scratch, int scratch_doubles, double* w_s,
-                                  int tid, int nt) {
+                                  int tid, int nt, const double* wt = nullptr) {
   constexpr int M = P + 1, NB = 2 * P + 1;
   const int N = K + P;
   const int nvd = K * M * Q, nem = K * M * M;
@@ -95,12 +97,12 @@ __device__ void build_band_tables(const double* V, const double* D, const double
       const double* vc = Vs + (e * M + c) * Q;
       double m = 0.0, k = 0.0;
 #pragma unroll
-      for (int q = 0; q < Q; ++q) m += (w_s[q] * vr[q]) * vc[q];
+      for (int q = 0; q < Q; ++q) m += (axis_w(w_s, wt, e, q, Q) * vr[q]) * vc[q];
       if (stiff) {
         const double* dr = Ds + (e * M + r) * Q;
         const double* dc = Ds + (e * M + c) * Q;
 #pragma unroll
-        for (int q = 0; q < Q; ++q) k += (w_s[q] * dr[q]) * dc[q];
+        for (int q = 0; q < Q; ++q) k += (axis_w(w_s, wt, e, q, Q) * dr[q]) * dc[q];
       }
       em[u] = make_double2(m, k);
     }
@@ -125,7 +127,7 @@ __device__ void build_band_tables(const double* V, const double* D, const double
       const int v = u < N * NB ? u : u - N * NB;
       const bool slab = u >= N * NB;
       tb[u] = band1d<P, Q>(V, D, K, w_s, v / NB, v % NB, slab ? slab_lo : 0, slab ? slab_hi : K,
-                           stiff);
+                           stiff, wt);
     }
   }
   __syncthreads();

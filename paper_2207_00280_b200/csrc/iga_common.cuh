@@ -42,8 +42,10 @@ __device__ __forceinline__ double dvd(double a, double b) { return __ddiv_rn(a, 
 
 // Knot t_i of the open uniform vector (splines.py:59-75): p+1 zeros,
 // i/K for the interior (np.arange(1,K)/K is a correctly rounded division),
-// p+1 ones.  Computed, never stored.
-__device__ __forceinline__ double knot(int i, int K, int p) {
+// p+1 ones.  Computed, never stored -- unless a general knot vector `t`
+// (K + 2p + 1 non-decreasing knots) is given.
+__device__ __forceinline__ double knot(int i, int K, int p, const double* t = nullptr) {
+  if (t != nullptr) return __ldg(t + i);
   if (i <= p) return 0.0;
   if (i >= K + p) return 1.0;
   return dvd((double)(i - p), (double)K);
@@ -56,18 +58,21 @@ __device__ __forceinline__ double knot(int i, int K, int p) {
 // Fills vals[r] = B_{e+r,p}(x), r = 0..p, and (if ders) the derivatives of
 // splines.py:139-161.
 template <int P>
-__device__ __forceinline__ void cox_de_boor(int e, double x, int K, double* vals, double* ders) {
+__device__ __forceinline__ void cox_de_boor(int e, double x, int K, double* vals, double* ders,
+                                            const double* t = nullptr) {
   // the 2P+2 knots t_e .. t_{e+2P+1} this point touches, each divided once
   double kn[2 * P + 2];
 #pragma unroll
-  for (int j = 0; j <= 2 * P + 1; ++j) kn[j] = knot(e + j, K, P);
+  for (int j = 0; j <= 2 * P + 1; ++j) kn[j] = knot(e + j, K, P, t);
   // level-0 indices e .. e+2P  (2P+1 values); level r needs e .. e+2P-r.
-  // order0 (splines.py:78-91) with the closed last span: the last knot is 1.0
+  // order0 (splines.py:78-91) with the closed last span: the last knot (1.0 for the
+  // uniform vector)
+  const double tl = t != nullptr ? __ldg(t + K + 2 * P) : 1.0;
   double N[2 * P + 1];
 #pragma unroll
   for (int j = 0; j <= 2 * P; ++j) {
     const double ti = kn[j], ti1 = kn[j + 1];
-    N[j] = (ti <= x && x < ti1) || (x == 1.0 && ti < ti1 && ti1 == 1.0) ? 1.0 : 0.0;
+    N[j] = (ti <= x && x < ti1) || (x == tl && ti < ti1 && ti1 == tl) ? 1.0 : 0.0;
   }
   double Nprev[2 * P + 1];  // level P-1 values, for derivatives
 #pragma unroll
@@ -119,14 +124,29 @@ __device__ __forceinline__ void cox_de_boor(int e, double x, int K, double* vals
 // Out-of-line copy (one per P per translation unit) for kernels templated on
 // more than P, to keep their code size and compile time bounded.
 template <int P>
-__device__ __noinline__ void cox_de_boor_ool(int e, double x, int K, double* vals, double* ders) {
-  cox_de_boor<P>(e, x, K, vals, ders);
+__device__ __noinline__ void cox_de_boor_ool(int e, double x, int K, double* vals, double* ders,
+                                             const double* t) {
+  cox_de_boor<P>(e, x, K, vals, ders, t);
 }
 
-// Node mapping of runtime.py:147 / mesh.py:88: e*h + (ref+1)*(h/2), h = 1/K.
-__device__ __forceinline__ double map_node(int e, double ref, int K) {
+// Node mapping of runtime.py:147 / mesh.py:88: e*h + (ref+1)*(h/2), h = 1/K.  For a
+// general knot vector t the element is the span [t_{p+e}, t_{p+e+1}]:
+// lo + (ref+1)*(h/2), h = hi - lo (tools/gen_golden.py nonuniform_tables).
+__device__ __forceinline__ double map_node(int e, double ref, int K, int p = 0,
+                                           const double* t = nullptr) {
+  if (t != nullptr) {
+    const double lo = __ldg(t + p + e), hi = __ldg(t + p + e + 1);
+    return add(lo, mul(add(ref, 1.0), dvd(sub(hi, lo), 2.0)));
+  }
   const double h = dvd(1.0, (double)K);
   return add(mul((double)e, h), mul(add(ref, 1.0), dvd(h, 2.0)));
+}
+
+// Weight of quadrature point k of element e along an axis: the reference weight (uniform
+// mesh: the Jacobian is the scalar jac) or, for a general knot vector, the per-element
+// table wt[e][k] = w_k h_e / 2 that K1 writes (the element's Jacobian folded per axis).
+__device__ __forceinline__ double axis_w(const double* w, const double* wt, int e, int k, int q) {
+  return wt != nullptr ? __ldg(wt + e * q + k) : w[k];
 }
 
 // ------------------------------------------------- structured CSR helpers

@@ -42,16 +42,17 @@ __global__ void __launch_bounds__(256) k_element_strict(ElemArgs a) {
   for (int t = threadIdx.x; t < DIM * Q; t += blockDim.x) {
     const int d = t / Q, k = t % Q;
     const double x = a.elem_nodes ? a.elem_nodes[(el * DIM + d) * Q + k]
-                                  : map_node(alpha[d], a.ref_nodes[k], a.K);
+                                  : map_node(alpha[d], a.ref_nodes[k], a.K, P, a.knots);
     double vals[m], ders[m];
-    cox_de_boor_ool<P>(alpha[d], x, a.K, vals, ders);
+    cox_de_boor_ool<P>(alpha[d], x, a.K, vals, ders, a.knots);
     for (int r = 0; r < m; ++r) {
       tabs[((d * 2 + 0) * m + r) * Q + k] = vals[r];
       tabs[((d * 2 + 1) * m + r) * Q + k] = ders[r];
     }
   }
   for (int u = threadIdx.x; u < DIM * Q; u += blockDim.x)
-    w[u] = a.elem_weights ? a.elem_weights[el * DIM * Q + u] : a.weights[u % Q];
+    w[u] = a.elem_weights ? a.elem_weights[el * DIM * Q + u]
+                          : axis_w(a.weights, a.wt, alpha[u / Q], u % Q, Q);
   __syncthreads();
   const double* w0 = w;
   const double* w1 = w + Q;
@@ -280,6 +281,9 @@ extern "C" int32_t iga_element_matrices(const iga_problem* prob, int32_t method,
   ElemArgs a;
   a.dim = prob->dim; a.K = prob->K; a.q = prob->q; a.op = prob->op; a.method = method;
   a.jac = prob->jac; a.coef_scalar = prob->coef_scalar; a.coef = prob->coef;
+  a.knots = prob->knots; a.wt = prob->knots ? prob->elem_weights : nullptr;
+  if (prob->knots && !elem_weights && !prob->elem_weights)
+    return fail_einval("a general knot vector needs elem_weights (iga_mesh_tables_general)");
   a.weights = prob->weights; a.ref_nodes = ref_nodes; a.elem_ids = elem_ids;
   a.elem_nodes = elem_nodes; a.elem_weights = elem_weights; a.elem_coef = elem_coef;
   a.count = count; a.out = out; a.scratch = nullptr;

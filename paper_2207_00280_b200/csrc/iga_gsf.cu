@@ -423,9 +423,10 @@ struct GsfLaunch {
       const char* env = getenv("IGA_GSF_GENERIC");
       if (!(env && env[0] == '1')) return launch_gsf_p3(a0, s);
     }
-    // DMMA GEMM formulation; IGA_GSF_SCALAR=1 selects this file's scalar kernel (A/B tests)
+    // DMMA GEMM formulation; IGA_GSF_SCALAR=1 selects this file's scalar kernel (A/B tests,
+    // uniform knots only)
     const char* sc = getenv("IGA_GSF_SCALAR");
-    if (!(sc && sc[0] == '1')) return launch_gsf_mma(a0, P, Q, s);
+    if (!(sc && sc[0] == '1') || a0.wt != nullptr) return launch_gsf_mma(a0, P, Q, s);
     if (a0.op == IGA_OP_MASS) return launch_gsf_generic<P, Q, false>(a0, s);
     if constexpr (P >= 1) return launch_gsf_generic<P, Q, true>(a0, s);
     set_error("derivatives require degree >= 1");

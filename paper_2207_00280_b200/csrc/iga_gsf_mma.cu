@@ -158,8 +158,18 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
   // coefficients of a unit are contiguous in memory); the thread's units are fixed, and
   // their coefficients for the next element column are prefetched into registers
   constexpr int NUW = KA * KB, UPT = cdiv(NUW, NT), Q3 = Q * Q * Q;
-  __shared__ double wqs[Q];
+  // per-axis weights of the tile's element windows (axis 0: la, axis 1: lb) and of the
+  // current column e2: the reference weights, or for a general knot vector the per-element
+  // tables w_k h_e / 2 (out-of-mesh window elements: 0, their pair tables are 0 as well)
+  __shared__ double wqs[Q], wa[KA], wb[KB];
   if (tid < Q) wqs[tid] = a.weights[tid];
+  for (int u = tid; u < KA + KB; u += NT) {
+    const bool ax0 = u < KA;
+    const int v = ax0 ? u : u - KA, l = v / Q, k = v % Q;
+    const int e = ax0 ? i00 - P + l : i10 - P + l;
+    const double w = a.wt == nullptr ? a.weights[k] : (e >= 0 && e < K ? __ldg(a.wt + e * Q + k) : 0.0);
+    if (ax0) wa[v] = w; else wb[v] = w;
+  }
   auto load_coef = [&](int e2, double (&cv)[UPT][Q]) {
 #pragma unroll
     for (int i = 0; i < UPT; ++i) {
@@ -282,10 +292,11 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
       const int u = tid + i * NT;
       if (u < NUW) {
         const int kk = u / KB, c1 = u - kk * KB;
-        const double w01 = wqs[kk % Q] * wqs[c1 % Q];
+        const double w01 = wa[kk] * wb[c1];
         double* dst = sW + kk * GCW + c1;  // column (k2, c1): k2 slowest
 #pragma unroll
-        for (int k2 = 0; k2 < Q; ++k2) dst[k2 * KB] = w01 * wqs[k2] * a.jac * cv[i][k2];
+        for (int k2 = 0; k2 < Q; ++k2)
+          dst[k2 * KB] = w01 * axis_w(wqs, a.wt, e2, k2, Q) * a.jac * cv[i][k2];
       }
     }
     load_coef(e2 + 1, cv);

@@ -440,7 +440,8 @@ __device__ __forceinline__ void form_w(double* W, const double* wq, const GsfArg
       const double cf = a.coef ? __ldg(a.coef + (((int64_t)e0 * K + e1) * K + e2) * (Q * Q * Q) +
                                        (k0 * Q + k1) * Q + k2)
                                : a.coef_scalar;
-      w = wq[k0] * wq[k1] * wq[k2] * a.jac * cf;
+      w = axis_w(wq, a.wt, e0, k0, Q) * axis_w(wq, a.wt, e1, k1, Q) * axis_w(wq, a.wt, e2, k2, Q) *
+          a.jac * cf;
     }
     W[row * WP + col] = w;
   }
@@ -516,7 +517,9 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
     pc[tid] = (I0 < N && I1 < N) ? (int)(band_cnt(I0, P, N) * band_cnt(I1, P, N)) : 0;
   }
   __syncthreads();
-  if (a.coef == nullptr) form_w(W, wq, a, 0, i00, i10, e0lo, e0hi, tid, NT);  // step-invariant
+  // step-invariant for a scalar coefficient on the uniform mesh
+  const bool w_per_step = a.coef != nullptr || a.wt != nullptr;
+  if (!w_per_step) form_w(W, wq, a, 0, i00, i10, e0lo, e0hi, tid, NT);
   __syncthreads();
 
   // pipeline: A on element column it, B on it-1, S on it-2, handed over by mbarriers
@@ -533,7 +536,7 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
     __syncthreads();  // every role holds its fragments before Y buffer 1 is written
     for (int it = 0; it < K; ++it) {
       PT(2);
-      if (a.coef != nullptr) {
+      if (w_per_step) {
         if (it > 0) asm volatile("bar.sync 1, %0;\n" ::"n"(NWA * 32));  // W of it-1 consumed
         form_w(W, wq, a, it, i00, i10, e0lo, e0hi, tid, NWA * 32);
         asm volatile("bar.sync 1, %0;\n" ::"n"(NWA * 32));

@@ -12,7 +12,8 @@ int launch_scatter(const ScatterArgs& a, int method, int p, int q, cudaStream_t 
 int launch_gsf(const GsfArgs& a, int p, int q, cudaStream_t s);
 int launch_kron(const KronArgs& a, int p, int q, cudaStream_t s);
 int launch_band_tables(int K, int p, int q, const double* ref, const double* weights, int stiff,
-                       double* V, double* D, double* band, cudaStream_t s);
+                       double* V, double* D, double* band, const double* knots, double* wt,
+                       cudaStream_t s);
 
 // assembly.assemble from element matrices: one warp per CSR row, lanes over
 // its columns; every value sums its element contributions in lexicographic
@@ -272,6 +273,8 @@ static int validate_problem(const iga_problem* prob) {
   if (!prob->weights || !prob->tables_v) return fail_einval("null weights/tables");
   if (prob->op != IGA_OP_MASS && !prob->tables_d) return fail_einval("stiffness needs tables_d");
   if (prob->reserved != 0) return fail_einval("reserved field must be 0");
+  if (prob->knots && !prob->elem_weights)
+    return fail_einval("a general knot vector needs elem_weights (iga_mesh_tables_general)");
   return IGA_OK;
 }
 
@@ -282,12 +285,17 @@ using namespace iga;
 extern "C" {
 
 int32_t iga_band_tables(const iga_problem* prob, const double* ref_nodes, double* vals,
-                        double* ders, double* band, void* stream) {
-  int rc = validate_problem(prob);
+                        double* ders, double* band, double* elem_weights, void* stream) {
+  if (!prob) return fail_einval("null problem");
+  if (prob->knots && !elem_weights) return fail_einval("a general knot vector needs elem_weights");
+  iga_problem pr = *prob;  // the weights are this call's output
+  if (pr.knots) pr.elem_weights = elem_weights;
+  int rc = validate_problem(&pr);
   if (rc) return rc;
   if (!ref_nodes || !band) return fail_einval("null ref_nodes/band");
   return launch_band_tables(prob->K, prob->p, prob->q, ref_nodes, prob->weights,
-                            prob->op != IGA_OP_MASS, vals, ders, band, as_stream(stream));
+                            prob->op != IGA_OP_MASS, vals, ders, band, prob->knots,
+                            prob->knots ? elem_weights : nullptr, as_stream(stream));
 }
 
 int32_t iga_integrate_assemble(const iga_problem* prob, int32_t method, int32_t el_begin,
@@ -317,6 +325,7 @@ int32_t iga_integrate_assemble(const iga_problem* prob, int32_t method, int32_t 
     if (prob->coef) return fail_einval("the separable method needs a scalar coefficient (coef == NULL)");
     KronArgs a;
     a.K = K; a.op = prob->op; a.el_begin = el_begin; a.el_end = el_end;
+    a.wt = prob->knots ? prob->elem_weights : nullptr;
     a.plane_begin = row_plane_begin; a.plane_end = row_plane_end; a.base = base;
     a.jc = prob->jac * prob->coef_scalar; a.weights = prob->weights;
     a.V = prob->tables_v; a.D = prob->tables_d; a.values = values;
@@ -330,6 +339,7 @@ int32_t iga_integrate_assemble(const iga_problem* prob, int32_t method, int32_t 
     }
     GsfArgs a;
     a.K = K; a.op = prob->op; a.el_begin = el_begin; a.el_end = el_end;
+    a.wt = prob->knots ? prob->elem_weights : nullptr;
     a.plane_begin = row_plane_begin; a.plane_end = row_plane_end; a.tiles1 = 0;
     a.segs = 1; a.seg_len = K;
     a.base = base; a.jac = prob->jac; a.coef_scalar = prob->coef_scalar; a.coef = prob->coef;
@@ -342,6 +352,7 @@ int32_t iga_integrate_assemble(const iga_problem* prob, int32_t method, int32_t 
   if (rc) return rc;
   ScatterArgs a;
   a.dim = dim; a.K = K; a.op = prob->op; a.el_begin = el_begin; a.el_end = el_end;
+  a.wt = prob->knots ? prob->elem_weights : nullptr;
   a.row_first = row_first; a.row_last = row_last; a.base = base; a.jac = prob->jac;
   a.coef_scalar = prob->coef_scalar; a.coef = prob->coef; a.weights = prob->weights;
   a.V = prob->tables_v; a.D = prob->tables_d; a.values = values;

@@ -54,7 +54,8 @@ __host__ __device__ constexpr int kron_rows(int P, bool small_mesh) {
 #endif
 // staging buffers per CTA (2: one bulk store in flight while the next chunk is produced;
 // 3 and 4 with proportionally fewer rows per chunk measured slower)
-constexpr int kron_nbuf() { return KRON_NBUF; }
+// high degrees stage one row per chunk: three buffers keep two bulk stores in flight
+__host__ __device__ constexpr int kron_nbuf(int P) { return P <= 5 ? KRON_NBUF : 3; }
 // doubles per staging buffer: a chunk of full rows plus 16-byte alignment padding
 __host__ __device__ constexpr int kron_stage(int P, int G) {
   return (G * (2 * P + 1) * (2 * P + 1) * (2 * P + 1) + 3) / 2 * 2;  // even: 16-byte aligned buffers
@@ -110,13 +111,14 @@ __global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) 
       const int i0hi = a.plane_begin + (int)((u_hi0 - 1) / nch / N);
       for (int u = tid; u < (i0hi - i0lo + 1) * NB; u += NT) {
         const int I0 = i0lo + u / NB, d = u % NB;
-        tb[N * NB + I0 * NB + d] = band1d_el<P, Q>(a.V, a.D, K, w, I0, d, a.el_begin, a.el_end, stiff);
+        tb[N * NB + I0 * NB + d] =
+            band1d_el<P, Q>(a.V, a.D, K, w, I0, d, a.el_begin, a.el_end, stiff, a.wt);
       }
     }
     __syncthreads();
   } else {
     build_band_tables<P, Q>(a.V, a.D, a.weights, K, stiff, a.el_begin, a.el_end, !full, tb, stage,
-                            kron_nbuf() * SG, w, tid, NT);
+                            kron_nbuf(P) * SG, w, tid, NT, a.wt);
   }
 
 #ifdef KRON_PROLOGUE_ONLY
@@ -193,11 +195,11 @@ __global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) 
       double* g = vals + off0;
       off0 += len;
       const int pad = (int)((reinterpret_cast<uintptr_t>(g) >> 3) & 1);
-      double* buf = stage + (chunk % kron_nbuf()) * SG;
+      double* buf = stage + (chunk % kron_nbuf(P)) * SG;
       // One CTA barrier per chunk: before it, the bulk store that last read this buffer
       // (chunk - NBUF, issued at the top of chunk - NBUF + 1) has finished reading it;
       // after it, the previous chunk is complete in shared memory and leaves.
-      if (tid == 0) asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(kron_nbuf() - 2) : "memory");
+      if (tid == 0) asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(kron_nbuf(P) - 2) : "memory");
       __syncthreads();
       if (tid == 0) issue();
       double* sb = buf + pad;
@@ -262,20 +264,30 @@ template <int P, int Q>
 __global__ void __launch_bounds__(128) k_mesh_band(int K, const double* __restrict__ ref,
                                                    const double* __restrict__ weights, int stiff,
                                                    double* __restrict__ V, double* __restrict__ D,
-                                                   double2* __restrict__ band) {
+                                                   double2* __restrict__ band,
+                                                   const double* __restrict__ knots,
+                                                   double* __restrict__ wt) {
   constexpr int kBandRows = band_rows(P);
   constexpr int M = P + 1, NB = 2 * P + 1, NEL = kBandRows + P;
   __shared__ double Vs[NEL * M * Q], Ds[NEL * M * Q];
   __shared__ double2 em[NEL * M * M];
-  __shared__ double w[Q];
+  __shared__ double w[Q], wes[NEL * Q];  // reference weights; per-element weights (knots)
   const int N = K + P, tid = threadIdx.x, nt = blockDim.x;
   const int i_lo = blockIdx.x * kBandRows, i_hi = min(N, i_lo + kBandRows);
   const int e0 = max(0, i_lo - P), e1 = min(K, i_hi), ne = e1 - e0;
   if (tid < Q) w[tid] = weights[tid];
+  if (knots) {  // w_k h_e / 2 of the CTA's elements (written once to wt by the CTA owning e)
+    for (int u = tid; u < ne * Q; u += nt) {
+      const int le = u / Q, k = u - le * Q, e = e0 + le;
+      const double h = sub(__ldg(knots + P + e + 1), __ldg(knots + P + e));
+      wes[u] = mul(weights[k], dvd(h, 2.0));
+      if (wt && e >= i_lo) wt[e * Q + k] = wes[u];
+    }
+  }
   for (int u = tid; u < ne * Q; u += nt) {
     const int le = u / Q, k = u - le * Q, e = e0 + le;
     double vals[M], ders[M];
-    cox_de_boor<P>(e, map_node(e, ref[k], K), K, vals, stiff ? ders : nullptr);
+    cox_de_boor<P>(e, map_node(e, ref[k], K, P, knots), K, vals, stiff ? ders : nullptr, knots);
 #pragma unroll
     for (int r = 0; r < M; ++r) {
       const int o = (le * M + r) * Q + k, og = (e * M + r) * Q + k;
@@ -293,13 +305,14 @@ __global__ void __launch_bounds__(128) k_mesh_band(int K, const double* __restri
     const double* vr = Vs + (le * M + r) * Q;
     const double* vc = Vs + (le * M + c) * Q;
     double m = 0.0, k = 0.0;
+    const double* we = knots ? wes + le * Q : w;
 #pragma unroll
-    for (int q = 0; q < Q; ++q) m += (w[q] * vr[q]) * vc[q];
+    for (int q = 0; q < Q; ++q) m += (we[q] * vr[q]) * vc[q];
     if (stiff) {
       const double* dr = Ds + (le * M + r) * Q;
       const double* dc = Ds + (le * M + c) * Q;
 #pragma unroll
-      for (int q = 0; q < Q; ++q) k += (w[q] * dr[q]) * dc[q];
+      for (int q = 0; q < Q; ++q) k += (we[q] * dr[q]) * dc[q];
     }
     em[u] = make_double2(m, k);
   }
@@ -320,25 +333,26 @@ __global__ void __launch_bounds__(128) k_mesh_band(int K, const double* __restri
 template <int P, int Q>
 struct BandLaunch {
   static int run(int K, const double* ref, const double* weights, int stiff, double* V, double* D,
-                 double2* band, cudaStream_t s) {
+                 double2* band, const double* knots, double* wt, cudaStream_t s) {
     const int N = K + P;
     k_mesh_band<P, Q><<<(N + band_rows(P) - 1) / band_rows(P), 128, 0, s>>>(
-        K, ref, weights, stiff, V, D, band);
+        K, ref, weights, stiff, V, D, band, knots, wt);
     return check_cuda(cudaGetLastError(), "band launch");
   }
 };
 
 int launch_band_tables(int K, int p, int q, const double* ref, const double* weights, int stiff,
-                       double* V, double* D, double* band, cudaStream_t s) {
+                       double* V, double* D, double* band, const double* knots, double* wt,
+                       cudaStream_t s) {
   return dispatch_pq_all<BandLaunch>(p, q, K, ref, weights, stiff, V, D,
-                                 reinterpret_cast<double2*>(band), s);
+                                     reinterpret_cast<double2*>(band), knots, wt, s);
 }
 
 template <int P, int Q, int G>
 static int launch_kron_g(const KronArgs& a, cudaStream_t s) {
   const int64_t N = (int64_t)a.K + P;
   constexpr int NT = kron_nt(P);
-  const size_t smem = 2 * sizeof(double2) * N * (2 * P + 1) + kron_nbuf() * sizeof(double) * kron_stage(P, G);
+  const size_t smem = 2 * sizeof(double2) * N * (2 * P + 1) + kron_nbuf(P) * sizeof(double) * kron_stage(P, G);
   if (smem > 220 * 1024) {
     set_error("separable path: 1D band tables of K=%d do not fit shared memory", a.K);
     return IGA_EUNSUPPORTED;

@@ -89,8 +89,9 @@ __global__ void __launch_bounds__(256) k_classical_scatter(ScatterArgs a) {
       const int k1 = DIM == 3 ? t / (Q * Q) : t / Q;
       const int k2 = DIM == 3 ? (t / Q) % Q : t % Q;
       const int k3 = DIM == 3 ? t % Q : 0;
-      double W = a.weights[k1] * a.weights[k2] * a.jac;
-      if (DIM == 3) W *= a.weights[k3];
+      double W = axis_w(a.weights, a.wt, alpha[0], k1, Q) * axis_w(a.weights, a.wt, alpha[1], k2, Q) *
+                 a.jac;
+      if (DIM == 3) W *= axis_w(a.weights, a.wt, alpha[2], k3, Q);
       W *= a.coef ? a.coef[eid * nq + t] : a.coef_scalar;
       sW[t] = W;
     }
@@ -203,7 +204,8 @@ __global__ void __launch_bounds__(256) k_classical_mma(ScatterArgs a) {
     const int64_t eid = ((int64_t)alpha[0] * a.K + alpha[1]) * a.K + alpha[2];
     for (int t = threadIdx.x; t < nq; t += blockDim.x) {
       const int k1 = t / (Q * Q), k2 = (t / Q) % Q, k3 = t % Q;
-      double W = a.weights[k1] * a.weights[k2] * a.jac * a.weights[k3];
+      double W = axis_w(a.weights, a.wt, alpha[0], k1, Q) * axis_w(a.weights, a.wt, alpha[1], k2, Q) *
+                 a.jac * axis_w(a.weights, a.wt, alpha[2], k3, Q);
       W *= a.coef ? a.coef[eid * nq + t] : a.coef_scalar;
       sW[t] = W;
     }
@@ -346,7 +348,8 @@ __global__ void __launch_bounds__(256) k_sumfact_scatter(ScatterArgs a) {
     const int64_t eid = ((int64_t)alpha[0] * a.K + alpha[1]) * a.K + alpha[2];
     for (int t = threadIdx.x; t < Q * Q * Q; t += blockDim.x) {
       const int k1 = t / (Q * Q), k2 = (t / Q) % Q, k3 = t % Q;
-      double W = a.weights[k1] * a.weights[k2] * a.weights[k3] * a.jac;
+      double W = axis_w(a.weights, a.wt, alpha[0], k1, Q) * axis_w(a.weights, a.wt, alpha[1], k2, Q) *
+                 axis_w(a.weights, a.wt, alpha[2], k3, Q) * a.jac;
       W *= a.coef ? a.coef[eid * Q * Q * Q + t] : a.coef_scalar;
       sW[t] = W;
     }

@@ -80,7 +80,7 @@ class MeshProblem:
     """Device state of one (dim, K, p, q, operator, coefficient) problem."""
 
     def __init__(self, dim: int, K: int, p: int, q: int | None = None, operator: str = "mass",
-                 coefficient=None, device=None, stream=None):
+                 coefficient=None, device=None, stream=None, knots=None):
         torch = _lib.require_cuda()
         if dim not in (2, 3):
             raise ValueError(f"dim must be 2 or 3, got {dim}")
@@ -101,7 +101,17 @@ class MeshProblem:
         self.weights_host = np.ascontiguousarray(w)
         self.ref_nodes = torch.from_numpy(self.ref_nodes_host).to(self.device)
         self.weights = torch.from_numpy(self.weights_host).to(self.device)
-        self.jac = jacobian(K, dim)
+        # general open knot vector: element Jacobians folded into
+        # per-element weights written by K1, jac = 1
+        self.knots_host = None
+        self.knots = self.elem_weights = None
+        if knots is not None:
+            from .splines import check_knots
+
+            self.knots_host = check_knots(knots, K, p)
+            self.knots = torch.from_numpy(self.knots_host).to(self.device)
+            self.elem_weights = torch.empty((K, q), dtype=torch.float64, device=self.device)
+        self.jac = jacobian(K, dim) if knots is None else 1.0
         m = p + 1
         self.tables_v = torch.empty((K, m, q), dtype=torch.float64, device=self.device)
         self.tables_d = torch.empty((K, m, q), dtype=torch.float64, device=self.device)
@@ -138,6 +148,12 @@ class MeshProblem:
     def build_tables(self, stream=None):
         """Basis values/derivatives per 1D element at the mapped nodes (K1)."""
         L = _lib.load()
+        if self.knots is not None:
+            _lib.check(L.iga_mesh_tables_general(
+                self.K, self.p, self.q, self.knots.data_ptr(), self.ref_nodes.data_ptr(),
+                self.weights.data_ptr(), self.tables_v.data_ptr(), self.tables_d.data_ptr(),
+                self.elem_weights.data_ptr(), _lib.stream_ptr(stream or self.stream)))
+            return
         _lib.check(L.iga_mesh_tables(self.K, self.p, self.q, self.ref_nodes.data_ptr(),
                                      self.tables_v.data_ptr(), self.tables_d.data_ptr(),
                                      _lib.stream_ptr(stream or self.stream)))
@@ -156,6 +172,8 @@ class MeshProblem:
         s.tables_v = self.tables_v.data_ptr()
         s.tables_d = self.tables_d.data_ptr() if self.operator != "mass" else None
         s.band = self.band.data_ptr() if band else None
+        s.knots = _lib.ptr(self.knots)
+        s.elem_weights = _lib.ptr(self.elem_weights)
         return s
 
     # -- K1 + 1D band matrices (separable method) ------------------------
@@ -170,7 +188,8 @@ class MeshProblem:
         s = self.problem_struct()
         rc = _lib.load().iga_band_tables(ctypes.byref(s), self.ref_nodes.data_ptr(),
                                          self.tables_v.data_ptr(), self.tables_d.data_ptr(),
-                                         self.band.data_ptr(), _lib.stream_ptr(stream or self.stream))
+                                         self.band.data_ptr(), _lib.ptr(self.elem_weights),
+                                         _lib.stream_ptr(stream or self.stream))
         if rc == _lib.IGA_EUNSUPPORTED:
             return False
         _lib.check(rc)
@@ -239,15 +258,21 @@ class MeshProblem:
         return out
 
 
-def basis_eval(K: int, p: int, elems, xs, derivatives: bool = True):
-    """K1' at arbitrary points: (values [n, p+1], derivatives [n, p+1]) on the device."""
+def basis_eval(K: int, p: int, elems, xs, derivatives: bool = True, knots=None):
+    """K1' at arbitrary points: (values [n, p+1], derivatives [n, p+1]) on the device, on
+    the open uniform knot vector or a general one (``knots``)."""
     torch = _lib.require_cuda()
     e = torch.as_tensor(np.ascontiguousarray(elems, dtype=np.int32)).cuda()
     x = torch.as_tensor(np.ascontiguousarray(xs, dtype=np.float64)).cuda()
+    t = None
+    if knots is not None:
+        from .splines import check_knots
+
+        t = torch.from_numpy(check_knots(knots, K, p)).cuda()
     n = e.numel()
     V = torch.empty((n, p + 1), dtype=torch.float64, device="cuda")
     D = torch.empty((n, p + 1), dtype=torch.float64, device="cuda") if derivatives else None
-    _lib.check(_lib.load().iga_basis_eval(K, p, n, e.data_ptr(), x.data_ptr(), V.data_ptr(),
-                                          None if D is None else D.data_ptr(),
+    _lib.check(_lib.load().iga_basis_eval(K, p, _lib.ptr(t), n, e.data_ptr(), x.data_ptr(),
+                                          V.data_ptr(), None if D is None else D.data_ptr(),
                                           _lib.stream_ptr()))
     return V, D

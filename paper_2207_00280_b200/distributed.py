@@ -186,7 +186,7 @@ class SlabSession:
         self.transport, self.group = transport, group
         self.code = method_code(cfg)
         self.prob = MeshProblem(3, cfg.mesh, cfg.degree, cfg.points, cfg.operator,
-                                cfg.coefficient, device=device)
+                                cfg.coefficient, device=device, knots=cfg.knots)
         self.n_own = plane_nnz(3, plan.K, plan.p, plan.own_lo, plan.own_hi)
         hi = plan.own_hi if halo == "recompute" else plan.comp_hi
         self.n_comp = plane_nnz(3, plan.K, plan.p, plan.own_lo, hi)

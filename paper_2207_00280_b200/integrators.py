@@ -86,13 +86,15 @@ def _check_inputs(alpha: ElementId, kv: KnotVector, rule: QuadratureRule) -> int
 
 
 @lru_cache(maxsize=32)
-def _element_problem(K: int, p: int, q: int, operator: str, device: int):
-    """Device problem reused by the per-element calls of one (K, p, q, operator): the
-    per-call inputs (nodes, per-axis weights, Jacobian, coefficient) travel with each call,
-    so a call uploads O(q) values (O(q^3) with a coefficient) -- never a mesh-wide array."""
+def _element_problem(K: int, p: int, q: int, operator: str, device: int, knots=None):
+    """Device problem reused by the per-element calls of one (K, p, q, operator, knots):
+    the per-call inputs (nodes, per-axis weights, Jacobian, coefficient) travel with each
+    call, so a call uploads O(q) values (O(q^3) with a coefficient) -- never a mesh-wide
+    array.  ``knots``: a general knot vector (tuple), whose tables the kernel evaluates."""
     from .device import MeshProblem
 
-    return MeshProblem(3, K, p, q, operator=operator)
+    return MeshProblem(3, K, p, q, operator=operator,
+                       knots=None if knots is None else np.asarray(knots))
 
 
 def _device_element(alpha, kv, rule, method_code, operator, coefficient):
@@ -110,7 +112,8 @@ def _device_element(alpha, kv, rule, method_code, operator, coefficient):
             if elem_coef.size != q**3:
                 raise ValueError(f"element coefficient needs {q**3} values, got {elem_coef.size}")
     torch = _lib.require_cuda()
-    prob = _element_problem(kv.elements, kv.degree, q, operator, torch.cuda.current_device())
+    prob = _element_problem(kv.elements, kv.degree, q, operator, torch.cuda.current_device(),
+                            None if kv.is_uniform else tuple(np.asarray(kv.knots).tolist()))
     nodes = np.ascontiguousarray(rule.nodes, dtype=np.float64).reshape(1, 3, q)
     weights = np.ascontiguousarray(rule.weights, dtype=np.float64).reshape(1, 3, q)
     out = prob.element_matrices([alpha], method_code, elem_nodes=nodes, elem_weights=weights,
@@ -150,7 +153,12 @@ def element_tables(kv: KnotVector, rule: QuadratureRule, alpha: ElementId):
 
 
 def default_rule(kv: KnotVector, alpha: ElementId, points: int | None = None) -> QuadratureRule:
-    """Gauss rule for alpha with an optional point override (integrators.py:233-251)."""
+    """Gauss rule for alpha with an optional point override (integrators.py:233-251); on a
+    general knot vector the rule of mesh.knot_rule."""
+    if not kv.is_uniform:
+        from .mesh import knot_rule
+
+        return knot_rule(kv, alpha, points)
     rule = gauss_rule(kv.degree, kv.elements, alpha)
     if points is None or points == kv.degree + 1:
         return rule

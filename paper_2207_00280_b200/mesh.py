@@ -63,3 +63,22 @@ def gauss_rule(p: int, K: int, alpha: ElementId) -> QuadratureRule:
     if p < 0:
         raise ValueError(f"degree must be >= 0, got {p}")
     return _rule(K, alpha, p + 1, (1.0 / (2.0 * K)) ** 3)
+
+
+def knot_rule(kv, alpha: ElementId, points: int | None = None) -> QuadratureRule:
+    """Gauss rule on element alpha of a general open knot vector:
+    nodes lo + (ref + 1) (h / 2) in each axis' span [lo, lo + h], per-axis weights
+    w * (h / 2) -- the element's Jacobian folded per axis -- and jacobian 1.0; the same
+    definition as the device's per-element weights (tools/gen_golden.py section 12)."""
+    q = kv.degree + 1 if points is None else points
+    if q < 1:
+        raise ValueError(f"quadrature points must be >= 1, got {q}")
+    ref, w = np.polynomial.legendre.leggauss(q)
+    nodes, weights = [], []
+    for d in range(3):
+        lo, hi = kv.element_bounds(alpha[d])
+        h = hi - lo
+        nodes.append(lo + (ref + 1.0) * (h / 2.0))
+        weights.append(w * (h / 2.0))
+    return QuadratureRule((q, q, q), np.stack(nodes), np.stack(weights), 1.0)
+

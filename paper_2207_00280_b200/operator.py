@@ -18,10 +18,11 @@ from .device import MeshProblem
 
 
 class MatrixFreeOperator:
-    def __init__(self, K: int, p: int, q: int | None = None, coefficient=None):
+    def __init__(self, K: int, p: int, q: int | None = None, coefficient=None, knots=None):
         if p < 1:
             raise ValueError("the gradient term requires degree >= 1")
-        self.prob = MeshProblem(3, K, p, q, operator="stiffness", coefficient=coefficient)
+        self.prob = MeshProblem(3, K, p, q, operator="stiffness", coefficient=coefficient,
+                                knots=knots)
         self.n_dofs = self.prob.n_dofs
 
     def apply(self, x, alpha: float = 1.0, beta: float = 0.0, out=None, stream=None):

@@ -53,6 +53,9 @@ class RunConfig:
     dim: int = 3
     devices: int = 1
     assembly: str = "auto"
+    # general open knot vector (K + 2p + 1 knots, the same on every axis like the reference's
+    # single KnotVector), or None for make_knot_vector's uniform mesh
+    knots: object = field(default=None, compare=False, repr=False)
 
     def __post_init__(self):
         if self.method not in METHODS:
@@ -79,6 +82,10 @@ class RunConfig:
             raise ValueError(f"assembly must be one of {ASSEMBLY}, got {self.assembly!r}")
         if self.quad_points is not None and self.quad_points < 1:
             raise ValueError("quad_points must be >= 1")
+        if self.knots is not None:
+            from .splines import check_knots
+
+            check_knots(self.knots, self.mesh, self.degree)
 
     @property
     def points(self) -> int:
@@ -181,7 +188,8 @@ def separable_fits(K: int, p: int) -> bool:
     staging chunks)."""
     nb = 2 * p + 1
     rows = 16 if p <= 2 else ((16 if K <= 96 else 8) if p == 3 else (4 if p <= 5 else 1))
-    return 2 * 16 * (K + p) * nb + 16 * (rows * nb**3 + 2) <= 220 * 1024
+    nbuf = 2 if p <= 5 else 3
+    return 2 * 16 * (K + p) * nb + 8 * nbuf * (rows * nb**3 + 2) <= 220 * 1024
 
 
 def method_code(cfg: RunConfig) -> int:
@@ -237,13 +245,15 @@ class DeviceSession:
         self._graph = None
         self.code = method_code(cfg)
         self.prob = MeshProblem(cfg.dim, cfg.mesh, cfg.degree, cfg.points, cfg.operator,
-                                cfg.coefficient)
+                                cfg.coefficient, knots=cfg.knots)
         self.stream = stream if stream is not None else torch.cuda.current_stream()
         # separable kernel: 1D band matrices precomputed by the K1 launch
         self.use_band = self.code == 3 and self.prob.build_band_tables(self.stream)
         self.values = torch.empty(self.prob.nnz(), dtype=torch.float64, device=self.prob.device)
         self._host_in = [torch.from_numpy(self.prob.ref_nodes_host).pin_memory(),
                          torch.from_numpy(self.prob.weights_host).pin_memory()]
+        if self.prob.knots is not None:
+            self._host_in.append(torch.from_numpy(self.prob.knots_host).pin_memory())
         self._host_coef = None
         if self.prob.coef is not None:
             self._host_coef = self.prob.coef.cpu().pin_memory()
@@ -294,6 +304,8 @@ class DeviceSession:
         with torch.cuda.stream(self.stream):
             self.prob.ref_nodes.copy_(self._host_in[0], non_blocking=True)
             self.prob.weights.copy_(self._host_in[1], non_blocking=True)
+            if self.prob.knots is not None:
+                self.prob.knots.copy_(self._host_in[2], non_blocking=True)
             if self._host_coef is not None:
                 self.prob.coef.copy_(self._host_coef, non_blocking=True)
             self.step()

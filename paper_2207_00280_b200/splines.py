@@ -25,10 +25,20 @@ class KnotVector:
     def n_basis(self) -> int:
         return self.elements + self.degree
 
+    @property
+    def is_uniform(self) -> bool:
+        """True for the open uniform vector of make_knot_vector (the reference's mesh)."""
+        return np.array_equal(self.knots, _uniform_knots(self.elements, self.degree))
+
     def element_bounds(self, e: int) -> tuple[float, float]:
+        """Span [t_{p+e}, t_{p+e+1}] of element e: (e/K, (e+1)/K) on the uniform vector
+        (the same floats as splines.py:38-42), the knot span on a general one."""
         if not 0 <= e < self.elements:
             raise IndexError(f"element index {e} out of range for K={self.elements}")
-        return e / self.elements, (e + 1) / self.elements
+        if self.is_uniform:
+            return e / self.elements, (e + 1) / self.elements
+        p = self.degree
+        return float(self.knots[p + e]), float(self.knots[p + e + 1])
 
 
 @dataclass(frozen=True)
@@ -39,17 +49,46 @@ class BasisValues:
     derivatives: np.ndarray | None = None
 
 
+def _uniform_knots(K: int, p: int) -> np.ndarray:
+    knots = np.empty(K + 2 * p + 1)
+    knots[: p + 1] = 0.0
+    knots[p + 1 : K + p] = np.arange(1, K) / K
+    knots[K + p :] = 1.0
+    return knots
+
+
 def make_knot_vector(K: int, p: int) -> KnotVector:
     """Clamped uniform knots on [0, 1] (same values as splines.py:59-75)."""
     if K < 1:
         raise ValueError(f"element count must be >= 1, got {K}")
     if p < 0:
         raise ValueError(f"degree must be >= 0, got {p}")
-    knots = np.empty(K + 2 * p + 1)
-    knots[: p + 1] = 0.0
-    knots[p + 1 : K + p] = np.arange(1, K) / K
-    knots[K + p :] = 1.0
-    return KnotVector(degree=p, elements=K, knots=knots)
+    return KnotVector(degree=p, elements=K, knots=_uniform_knots(K, p))
+
+
+def check_knots(knots, K: int, p: int) -> np.ndarray:
+    """Validate a general open knot vector for K elements of degree p (SURVEY.md 8(f) row
+    4): K + 2p + 1 finite values, p + 1 equal knots at each end, strictly increasing
+    interior breakpoints (K non-empty spans; the CSR pattern is then the uniform one)."""
+    t = np.ascontiguousarray(knots, dtype=np.float64).reshape(-1)
+    if t.size != K + 2 * p + 1:
+        raise ValueError(f"knot vector needs K + 2p + 1 = {K + 2 * p + 1} entries, got {t.size}")
+    if not np.all(np.isfinite(t)):
+        raise ValueError("knots must be finite")
+    if np.any(t[: p + 1] != t[0]) or np.any(t[K + p :] != t[-1]):
+        raise ValueError(f"an open knot vector repeats its end knots p + 1 = {p + 1} times")
+    if np.any(np.diff(t[p : K + p + 1]) <= 0.0):
+        raise ValueError("breakpoints must be strictly increasing (K non-empty spans)")
+    return t
+
+
+def make_general_knot_vector(knots, p: int) -> KnotVector:
+    """KnotVector over a general open knot vector (K = len(knots) - 2p - 1 spans)."""
+    t = np.ascontiguousarray(knots, dtype=np.float64).reshape(-1)
+    K = t.size - 2 * p - 1
+    if K < 1:
+        raise ValueError(f"{t.size} knots cannot carry degree {p}")
+    return KnotVector(degree=p, elements=K, knots=check_knots(t, K, p))
 
 
 def _eval_knots(kv: KnotVector, index, order: int, xs) -> np.ndarray:
@@ -104,7 +143,8 @@ def _check_point(kv: KnotVector, e: int, x: float) -> None:
 def _eval(kv: KnotVector, elems, xs, derivatives):
     from .device import basis_eval
 
-    V, D = basis_eval(kv.elements, kv.degree, elems, xs, derivatives)
+    V, D = basis_eval(kv.elements, kv.degree, elems, xs, derivatives,
+                      knots=None if kv.is_uniform else kv.knots)
     return V.cpu().numpy(), (None if D is None else D.cpu().numpy())
 
 
@@ -145,7 +185,15 @@ def basis_derivative_table(kv: KnotVector, e: int, points: np.ndarray) -> np.nda
 
 
 def find_element(kv: KnotVector, x: float) -> int:
-    """Element containing x; the last element is right-closed (splines.py:181-185)."""
-    if not 0.0 <= x <= 1.0:
-        raise ValueError(f"point {x} outside [0, 1]")
-    return min(int(x * kv.elements), kv.elements - 1)
+    """Element containing x; the last element is right-closed (splines.py:181-185); on a
+    general knot vector the span [t_{p+e}, t_{p+e+1}) holding x."""
+    if kv.is_uniform:
+        if not 0.0 <= x <= 1.0:
+            raise ValueError(f"point {x} outside [0, 1]")
+        return min(int(x * kv.elements), kv.elements - 1)
+    p, K = kv.degree, kv.elements
+    lo, hi = float(kv.knots[p]), float(kv.knots[p + K])
+    if not lo <= x <= hi:
+        raise ValueError(f"point {x} outside [{lo}, {hi}]")
+    e = int(np.searchsorted(kv.knots[p + 1:p + K], x, side="right"))
+    return min(e, K - 1)

@@ -785,7 +785,7 @@ def test_band_tables_read_only_and_in_bounds(pkg, K, p, op):
     s = mp.problem_struct()
     _lib.check(_lib.load().iga_band_tables(ctypes.byref(s), mp.ref_nodes.data_ptr(),
                                            mp.tables_v.data_ptr(), mp.tables_d.data_ptr(),
-                                           guard.data_ptr(), _lib.stream_ptr()))
+                                           guard.data_ptr(), None, _lib.stream_ptr()))
     torch.cuda.synchronize()
     assert (guard[nband:] == 777.0).all().item()
     snapshot = guard.clone()
