@@ -14,7 +14,8 @@ import os
 import subprocess
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libiga_b200.so")
+# IGA_LIB_PATH: load another build of the same ABI (tuning experiments: tools/gsf_variants.sh)
+LIB_PATH = os.environ.get("IGA_LIB_PATH") or os.path.join(_HERE, "lib", "libiga_b200.so")
 CSRC = os.path.join(_HERE, "csrc")
 
 IGA_OK, IGA_EINVAL, IGA_ECUDA, IGA_EUNSUPPORTED = 0, 1, 2, 3

@@ -18,6 +18,7 @@
 // accumulators leave as the C fragments (C[g][2t], C[g][2t+1]).  k_gsf3_p3 keeps
 // its hand-scheduled p = 3, q = 4 pipeline; this kernel serves the other degrees.
 #include <cstdlib>
+#include <type_traits>
 
 #include "iga_args.cuh"
 #include "iga_dispatch.cuh"
@@ -39,6 +40,93 @@ __host__ __device__ constexpr int pitch_mod(int n, int mod, int r) { return n + 
 __host__ __device__ constexpr int qw_dist(int s) { return s % 2 ? 4 : (s % 4 == 2 ? 2 : 1); }
 __device__ __forceinline__ int qw_row(int g, int d) {
   return d == 4 ? (g >> 1) + 4 * (g & 1) : (d == 2 ? (g & 4) + ((g >> 1) & 1) + 2 * (g & 1) : g);
+}
+
+// Structural zeros of the pair tables.  PA[a0][kk], a0 = (ia, d0), kk = (la, k0), is nonzero
+// only if the element la of the window supports both dofs: r = ia + P - la and s = ia + d0 - la
+// in [0, P] (PB the same with (ib, d1), (lb, k1)).  A DMMA k-step whose 8 x 4 fragment block is
+// zero on every tile is skipped; the nonzero k-steps of each 8-row tile form one contiguous
+// range [lo, hi) (C4, p = 4, TA = 1 / TB = 4: stage A 9 of 14 blocks, stage B 33 of 50).
+template <int P, int Q, int T>
+struct Band {
+  static constexpr int NB = 2 * P + 1, KK = (T + P) * Q, ROWS = T * NB;
+  static constexpr int MT = cdiv(ROWS, 8), KS = cdiv(KK, 4);
+  static constexpr bool nz(int mt, int ks) {
+    for (int a = mt * 8; a < mt * 8 + 8 && a < ROWS; ++a)
+      for (int kk = ks * 4; kk < ks * 4 + 4 && kk < KK; ++kk) {
+        const int i = a / NB, d = a % NB, l = kk / Q, r = i + P - l, s = i + d - l;
+        if (r >= 0 && r <= P && s >= 0 && s <= P) return true;
+      }
+    return false;
+  }
+  static constexpr int lo(int mt) {
+#ifdef GSF_NOSKIP
+    return 0;
+#endif
+    for (int ks = 0; ks < KS; ++ks)
+      if (nz(mt, ks)) return ks;
+    return KS;
+  }
+  static constexpr int hi(int mt) {
+#ifdef GSF_NOSKIP
+    return KS;
+#endif
+    for (int ks = KS; ks > 0; --ks)
+      if (nz(mt, ks - 1)) return ks;
+    return 0;
+  }
+};
+
+// Warps per tile of a stage: every warp keeps one tile's constant fragments and sweeps
+// `items` GEMM blocks of cost (hi - lo) k-steps; warps are added greedily to the tile with
+// the largest per-warp load (tiles with fewer nonzero k-steps get fewer warps).
+template <int MT>
+struct Split {
+  int cnt[MT];
+  int start[MT + 1];
+};
+template <int MT, class B>
+constexpr Split<MT> make_split(int nwarp, int items) {
+  Split<MT> s{};
+  for (int t = 0; t < MT; ++t) s.cnt[t] = 1;
+  for (int used = MT; used < nwarp; ++used) {
+    int best = -1, load = -1;
+    for (int t = 0; t < MT; ++t) {
+      const int l = cdiv(items, s.cnt[t]) * (B::hi(t) - B::lo(t));
+      if (l > load) { load = l; best = t; }
+    }
+    if (s.cnt[best] >= items) break;
+    ++s.cnt[best];
+  }
+  s.start[0] = 0;
+  for (int t = 0; t < MT; ++t) s.start[t + 1] = s.start[t] + s.cnt[t];
+  return s;
+}
+// this warp's tile, its index among the tile's warps, the tile's warp count and k-step range
+// (tile -1: idle in this stage)
+struct WarpTile {
+  int tile = -1, grp = 0, cnt = 1, lo = 0, hi = 0;
+};
+template <int MT, class B, int NW, int ITEMS>
+__device__ __forceinline__ WarpTile warp_tile(int warp) {
+  constexpr Split<MT> s = make_split<MT, B>(NW, ITEMS);
+  WarpTile w;
+#pragma unroll
+  for (int t = 0; t < MT; ++t)
+    if (warp >= s.start[t] && warp < s.start[t + 1]) {
+      w.tile = t; w.grp = warp - s.start[t]; w.cnt = s.cnt[t]; w.lo = B::lo(t); w.hi = B::hi(t);
+    }
+  return w;
+}
+
+// f(integral_constant<int, tile>) for the runtime tile index: the tile's k-step range is a
+// compile-time constant inside f, so its fragment loads are unrolled and hoisted
+template <int T, int MT, class F>
+__device__ __forceinline__ void tile_dispatch(int tile, F&& f) {
+  if constexpr (T < MT) {
+    if (tile == T) f(std::integral_constant<int, T>());
+    else tile_dispatch<T + 1, MT>(tile, f);
+  }
 }
 
 // ST: stiffness (two operand types, double2 elements) or mass (one type: double elements,
@@ -316,24 +404,28 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
     // ---- stage A: X_T[a0][col] = sum_kk PA_T[a0][kk] W[kk][col]; warp w keeps the PA
     // fragments of m-tile w % MT in registers and sweeps its n-tiles
     {
-      constexpr int MT = cdiv(NA0, 8), NTL = cdiv(GC, 8), KS = cdiv(KA, 4), GRP = NWARP / MT;
-      if (warp < MT * GRP) {
-        const int mt = warp % MT, grp = warp / MT, row = mt * 8 + g;
-        double2 pa[KS];
+      using BA = Band<P, Q, TA>;
+      constexpr int MT = cdiv(NA0, 8), NTL = cdiv(GC, 8), KS = cdiv(KA, 4);
+      static_assert(BA::MT == MT && BA::KS == KS, "stage-A band shape");
+      const WarpTile wt = warp_tile<MT, BA, NWARP, NTL>(warp);
+      tile_dispatch<0, MT>(wt.tile, [&](auto tc) {
+        constexpr int LO = BA::lo(decltype(tc)::value), HI = BA::hi(decltype(tc)::value);
+        const int row = decltype(tc)::value * 8 + g;
+        double2 pa[HI - LO];
 #pragma unroll
-        for (int ks = 0; ks < KS; ++ks) {
+        for (int ks = LO; ks < HI; ++ks) {
           const int kk = ks * 4 + t;
-          pa[ks] = (row < NA0 && kk < KA) ? as2(PA2[row * KAP + kk]) : make_double2(0.0, 0.0);
+          pa[ks - LO] = (row < NA0 && kk < KA) ? as2(PA2[row * KAP + kk]) : make_double2(0.0, 0.0);
         }
-        for (int ntl = grp; ntl < NTL; ntl += GRP) {
+        for (int ntl = wt.grp; ntl < NTL; ntl += wt.cnt) {
           const int col = ntl * 8 + g;
           double cv0 = 0.0, cv1 = 0.0, cd0 = 0.0, cd1 = 0.0;
 #pragma unroll
-          for (int ks = 0; ks < KS; ++ks) {
+          for (int ks = LO; ks < HI; ++ks) {  // structurally zero k-steps skipped
             const int kk = ks * 4 + t;
             const double w = (kk < KA && col < GC) ? sW[kk * GCW + col] : 0.0;
-            dmma(cv0, cv1, pa[ks].x, w);
-            if (STIFF) dmma(cd0, cd1, pa[ks].y, w);
+            dmma(cv0, cv1, pa[ks - LO].x, w);
+            if (STIFF) dmma(cd0, cd1, pa[ks - LO].y, w);
           }
           const int c0 = ntl * 8 + 2 * t;
           if (row < NA0) {
@@ -341,36 +433,40 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
             if (c0 + 1 < GC) X2[row * GC + c0 + 1] = Elem<STIFF>::mk(cv1, cd1);
           }
         }
-      }
+      });
     }
     __syncthreads();
 
     // ---- stage B: rows (a0, k2), columns b1; warp w keeps the PB fragments of n-tile
     // w % NTL in registers:  mass YA = XV VV;  stiffness YA = XV DD + XD VV, YB = XV VV
     {
-      constexpr int MT = cdiv(NR, 8), NTL = cdiv(NB1, 8), KS = cdiv(KB, 4), GRP = NWARP / NTL;
-      if (warp < NTL * GRP) {
-        const int ntl = warp % NTL, grp = warp / NTL, b1 = ntl * 8 + g;
+      using BB = Band<P, Q, TB>;
+      constexpr int MT = cdiv(NR, 8), NTL = cdiv(NB1, 8), KS = cdiv(KB, 4);
+      static_assert(BB::MT == NTL && BB::KS == KS, "stage-B band shape");
+      const WarpTile wt = warp_tile<NTL, BB, NWARP, MT>(warp);
+      tile_dispatch<0, NTL>(wt.tile, [&](auto tc) {
+        constexpr int LO = BB::lo(decltype(tc)::value), HI = BB::hi(decltype(tc)::value);
+        const int ntl = decltype(tc)::value, b1 = ntl * 8 + g;
         constexpr int DQ = qw_dist(KB);  // X rows (a0, k2) are KB double2 apart
-        double2 pb[KS];
+        double2 pb[HI - LO];
 #pragma unroll
-        for (int ks = 0; ks < KS; ++ks) {
+        for (int ks = LO; ks < HI; ++ks) {
           const int kk = ks * 4 + t;
-          pb[ks] = (b1 < NB1 && kk < KB) ? as2(PB2[b1 * KBP + kk]) : make_double2(0.0, 0.0);
+          pb[ks - LO] = (b1 < NB1 && kk < KB) ? as2(PB2[b1 * KBP + kk]) : make_double2(0.0, 0.0);
         }
-        for (int mt = grp; mt < MT; mt += GRP) {
+        for (int mt = wt.grp; mt < MT; mt += wt.cnt) {
           const int row = mt * 8 + qw_row(g, DQ), a0 = row / Q, k2 = row % Q;
           double ya0 = 0.0, ya1 = 0.0, yb0 = 0.0, yb1 = 0.0;
 #pragma unroll
-          for (int ks = 0; ks < KS; ++ks) {
+          for (int ks = LO; ks < HI; ++ks) {  // structurally zero k-steps skipped
             const int kk = ks * 4 + t;
             const double2 x = (row < NR && kk < KB) ? as2(X2[row * KB + kk]) : make_double2(0.0, 0.0);
             if (STIFF) {
-              dmma(ya0, ya1, x.x, pb[ks].y);
-              dmma(ya0, ya1, x.y, pb[ks].x);
-              dmma(yb0, yb1, x.x, pb[ks].x);
+              dmma(ya0, ya1, x.x, pb[ks - LO].y);
+              dmma(ya0, ya1, x.y, pb[ks - LO].x);
+              dmma(yb0, yb1, x.x, pb[ks - LO].x);
             } else {
-              dmma(ya0, ya1, x.x, pb[ks].x);
+              dmma(ya0, ya1, x.x, pb[ks - LO].x);
             }
           }
           const int c0 = ntl * 8 + 2 * t;
@@ -379,7 +475,7 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
             if (c0 + 1 < NB1) Y2[(a0 * NB1 + c0 + 1) * Q + k2] = Elem<STIFF>::mk(ya1, yb1);
           }
         }
-      }
+      });
     }
     __syncthreads();
 
@@ -387,8 +483,17 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
     // rows; warp w keeps the Z fragments of n-tile w % NTL and its lanes' two (r,s)
     // destinations, and sweeps the combo m-tiles
     {
-      constexpr int MM = m * m, MT = cdiv(NC, 8), NTL = cdiv(MM, 8), KS = cdiv(Q, 4);
+      // n-tiles of (r, s) pairs; one or two pairs left over past the last full n-tile
+      // (p = 2: 9 pairs, p = 4: 25) are summed with DFMAs below instead of a DMMA tile that
+      // is 1/8 or 2/8 useful
+      constexpr int MM = m * m, MT = cdiv(NC, 8), KS = cdiv(Q, 4);
+#ifndef GSF_NOLEFT
+      constexpr int NTL = (MM > 8 && MM % 8 != 0 && MM % 8 <= 2) ? MM / 8 : cdiv(MM, 8);
+#else
+      constexpr int NTL = cdiv(MM, 8);
+#endif
       constexpr int GRP = NWARP / NTL;
+      const int slot0 = e2 % m;
       if (warp < NTL * GRP) {
         const int ntl = warp % NTL, grp = warp / NTL, n = ntl * 8 + g;
         double2 z[KS];
@@ -398,7 +503,6 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
           z[ks] = (n < MM && k < Q) ? as2(Z2[k * MM + n]) : make_double2(0.0, 0.0);
         }
         int dst[2];  // offset of column (r, s) in a combo's R block, -1 if padding
-        const int slot0 = e2 % m;
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
           const int nn = ntl * 8 + 2 * t + j, r = nn / m, sc = nn % m;
@@ -421,6 +525,22 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
             if (dst[0] >= 0) Rc[dst[0]] += c0v;
             if (dst[1] >= 0) Rc[dst[1]] += c1v;
           }
+        }
+      }
+      if constexpr (NTL * 8 < MM) {
+        // leftover pairs: one (combo, pair) per thread, distinct R entries from the DMMA part
+        constexpr int NL = MM - NTL * 8;
+        for (int u = tid; u < NC * NL; u += NT) {
+          const int c = u / NL, nn = NTL * 8 + u % NL, r = nn / m, sc = nn % m;
+          double acc = 0.0;
+#pragma unroll
+          for (int k = 0; k < Q; ++k) {
+            const double2 y = as2(Y2[c * Q + k]), zz = as2(Z2[k * MM + nn]);
+            acc = fma(y.x, zz.x, acc);
+            if (STIFF) acc = fma(y.y, zz.y, acc);
+          }
+          const int slot = slot0 + r >= m ? slot0 + r - m : slot0 + r;
+          R[comboR[c] + slot * S::RP + sc - r + P] += acc;
         }
       }
     }

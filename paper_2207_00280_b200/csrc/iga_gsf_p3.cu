@@ -140,9 +140,16 @@ struct Lane {
 #ifndef P3_SPLIT
 #define P3_SPLIT 0
 #endif
+#ifndef P3_SORD
+#define P3_SORD 0
+#endif
 __device__ __forceinline__ double sel(bool c, double a, double b) { return c ? a : b; }
 __device__ __forceinline__ void split_groups(const double* y, int t, double& hi, double& lo) {
-#if P3_SPLIT == 1
+#if P3_SPLIT == 2
+  // ablation only (wrong values): two DADDs instead of the six FP64 ops
+  hi = y[0] + y[2];
+  lo = y[1] + y[3];
+#elif P3_SPLIT == 1
   // three DADDs per lane and integer selects: A = y0 + y1, B = y2 + y3, and one lane-chosen
   // sum C (t=0: A + B, t=1: A + y2, t=3: y1 + B)
   const double A = y[0] + y[1], B = y[2] + y[3];
@@ -350,6 +357,22 @@ __device__ __forceinline__ void stage_s_batch(const Lane& L, int ws, const doubl
       }
     lo[i] = Rs[rs_idx(mt, PHI, 1, L.lane)];
   }
+#if P3_SORD == 1
+  // consecutive DMMAs share their B fragment (a warp re-reading the same B issues
+  // DMMAs faster than one whose B changes every instruction)
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+    for (int i = 0; i < NM; ++i)
+      dmma(cc[i][nt][0], cc[i][nt][1], a0[i], b0[nt], cc[i][nt][0], cc[i][nt][1]);
+  if (L.stiff) {
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int i = 0; i < NM; ++i)
+        dmma(cc[i][nt][0], cc[i][nt][1], a1[i], b1[nt], cc[i][nt][0], cc[i][nt][1]);
+  }
+#else
 #pragma unroll
   for (int i = 0; i < NM; ++i)
 #pragma unroll
@@ -362,6 +385,7 @@ __device__ __forceinline__ void stage_s_batch(const Lane& L, int ws, const doubl
       for (int nt = 0; nt < 2; ++nt)
         dmma(cc[i][nt][0], cc[i][nt][1], a1[i], b1[nt], cc[i][nt][0], cc[i][nt][1]);
   }
+#endif
 #pragma unroll
   for (int i = 0; i < NM; ++i) {
 #pragma unroll
