@@ -17,6 +17,16 @@
 // rows/columns/k predicated to zero, nothing is padded in memory), and the
 // accumulators leave as the C fragments (C[g][2t], C[g][2t+1]).  k_gsf3_p3 keeps
 // its hand-scheduled p = 3, q = 4 pipeline; this kernel serves the other degrees.
+//
+// Work the tiles do not need is not issued (C4, 96^3 p = 4 stiffness+mass with a
+// coefficient field: 15.8 -> 11.8 ms; C2: 0.072 -> 0.059 ms):
+//  * k-steps whose PA / PB fragment block is structurally zero (Band: an element of the
+//    window supports both dofs of a row only in a band) are skipped, with compile-time
+//    k-step ranges per tile and warps split across tiles by their nonzero work;
+//  * stage S of the stiffness operators contracts [Y_A | Y_B] against [VV; DD] as one
+//    K = 2q product (q = 5: 3 k-steps instead of 2 x 2), the rolling-row values being the
+//    DMMA C operand, and the one or two (r, s) pairs past the last full n-tile (p = 2: 9
+//    pairs, p = 4: 25) are summed with DFMAs instead of an n-tile that is 1/8 useful.
 #include <cstdlib>
 #include <type_traits>
 
@@ -144,7 +154,11 @@ struct Shape {
   static constexpr int KAP = pitch_mod(KA, 8, 4), KBP = pitch_mod(KB, 8, 4);
   static constexpr int NA0 = TA * NB, NB1 = TB * NB, NC = NA0 * NB1, NR = NA0 * Q;
   static constexpr int rowVals = NB * NB * NB;
-  static constexpr int nW = KA * GCW, nY = EW * NC * Q;
+  // Y: mass [NC][Q] doubles; stiffness [NC][YPS] doubles, Y_A at k2 and Y_B at Q + k2, so
+  // stage S runs its two products as one K = 2Q contraction (C4: 3 k-steps instead of 2 x 2);
+  // YPS == 4 mod 8: the A fragments of a k-step (8 rows x 4 k) hit 16 distinct banks per phase
+  static constexpr int YPS = ST ? pitch_mod(2 * Q, 8, 4) : Q;
+  static constexpr int nW = KA * GCW, nY = NC * YPS;
   // Y aliases W (W is dead after stage A); even, so the double2 arrays after it are aligned
   static constexpr int nWY = ((nW > nY ? nW : nY) + 1) / 2 * 2;
   static constexpr int nX = EW * NA0 * GC;
@@ -190,7 +204,7 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
   constexpr int NA0 = S::NA0, NB1 = S::NB1, NC = S::NC, NR = S::NR;
   extern __shared__ double smem[];
   double* sW = smem;                                         // [KA][GCW]
-  E* Y2 = reinterpret_cast<E*>(smem);                        // [NC][Q] (aliases W)
+  double* Yd = smem;                                         // [NC][YPS] (aliases W)
   E* X2 = reinterpret_cast<E*>(smem + S::nWY);               // [NA0][Q][KB] (XV, XD)
   E* PA2 = X2 + NA0 * GC;                                    // [NA0][KAP] (VV, DD)
   E* PB2 = PA2 + NA0 * KAP;                                  // [NB1][KBP] (VV, DD)
@@ -258,21 +272,33 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
     const double w = a.wt == nullptr ? a.weights[k] : (e >= 0 && e < K ? __ldg(a.wt + e * Q + k) : 0.0);
     if (ax0) wa[v] = w; else wb[v] = w;
   }
+  // per unit: the coefficient offset without the e2 term (-1: out of the mesh) and the W row
+  // offset, computed once
+  int64_t cbase[UPT];
+  int wdst[UPT];
+#pragma unroll
+  for (int i = 0; i < UPT; ++i) {
+    const int u = tid + i * NT;
+    cbase[i] = -1;
+    wdst[i] = -1;
+    if (u < NUW) {
+      const int kk = u / KB, c1 = u - kk * KB, la = kk / Q, k0 = kk - la * Q;
+      const int lb = c1 / Q, k1 = c1 - lb * Q;
+      const int e0 = i00 - P + la, e1 = i10 - P + lb;
+      wdst[i] = kk * GCW + c1;
+      if (e0 >= 0 && e0 < K && e1 >= 0 && e1 < K)
+        cbase[i] = ((int64_t)e0 * K + e1) * K * Q3 + (k0 * Q + k1) * Q;
+    }
+  }
   auto load_coef = [&](int e2, double (&cv)[UPT][Q]) {
 #pragma unroll
     for (int i = 0; i < UPT; ++i) {
 #pragma unroll
       for (int k2 = 0; k2 < Q; ++k2) cv[i][k2] = a.coef_scalar;
-      const int u = tid + i * NT;
-      if (a.coef && u < NUW && e2 < K) {
-        const int kk = u / KB, c1 = u - kk * KB, la = kk / Q, k0 = kk - la * Q;
-        const int lb = c1 / Q, k1 = c1 - lb * Q;
-        const int e0 = i00 - P + la, e1 = i10 - P + lb;
-        if (e0 >= 0 && e0 < K && e1 >= 0 && e1 < K) {
-          const double* src = a.coef + (((int64_t)e0 * K + e1) * K + e2) * Q3 + (k0 * Q + k1) * Q;
+      if (a.coef && cbase[i] >= 0 && e2 < K) {
+        const double* src = a.coef + cbase[i] + (int64_t)e2 * Q3;
 #pragma unroll
-          for (int k2 = 0; k2 < Q; ++k2) cv[i][k2] = __ldg(src + k2);
-        }
+        for (int k2 = 0; k2 < Q; ++k2) cv[i][k2] = __ldg(src + k2);
       }
     }
   };
@@ -320,6 +346,13 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
   // (rc, v) loop below.  Both write the same values to the same addresses.
   constexpr int VT = cdiv(S::rowVals, 32) * 32, RCS = NT / VT;
   constexpr bool by_v = RCS >= 1 && RCS * VT == NT;
+  constexpr int VPT = cdiv(S::rowVals, NT);
+  int vd[VPT];  // (d0, d1, d2) of this thread's band positions, packed
+#pragma unroll
+  for (int j = 0; j < VPT; ++j) {
+    const int v = tid + j * NT;
+    vd[j] = (v / (NB * NB)) << 16 | ((v / NB) % NB) << 8 | (v % NB);
+  }
   auto flush_row = [&](int I2) {
     const int slot = I2 % m;
     const int lod2 = max(0, P - I2), c2 = (int)band_cnt(I2, P, N);
@@ -351,40 +384,53 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
       }
       return;
     }
-    for (int u = tid; u < TA * TB * S::rowVals; u += NT) {
-      const int rc = u / S::rowVals, v = u - rc * S::rowVals;
-      double* Rv = R + (rc * m + slot) * S::RP + v;
-      const int64_t off = rowoff[rc];
-      if (off >= 0) {
-        const int mt = rowmeta[rc];
-        if (mt == 0) {
-          a.values[off + v] = *Rv;  // full band: CSR order is the R order
-        } else {
-          const int lod0 = (mt >> 1) & 31, lod1 = (mt >> 6) & 31, c0 = (mt >> 11) & 31,
-                    c1 = (mt >> 16) & 31;
-          const int d2 = v % NB, d1 = (v / NB) % NB, d0 = v / (NB * NB);
-          if (d0 >= lod0 && d0 < lod0 + c0 && d1 >= lod1 && d1 < lod1 + c1 && d2 >= lod2 &&
-              d2 < lod2 + c2)
-            a.values[off + ((d0 - lod0) * c1 + (d1 - lod1)) * c2 + (d2 - lod2)] = *Rv;
+    // otherwise every thread keeps its band positions v = tid + j NT (decomposed once) and
+    // walks the pencils
+#pragma unroll
+    for (int j = 0; j < VPT; ++j) {
+      const int v = tid + j * NT;
+      if (v >= S::rowVals) break;
+      const int d2 = vd[j] & 255, d1 = (vd[j] >> 8) & 255, d0 = vd[j] >> 16;
+      const bool in2 = d2 >= lod2 && d2 < lod2 + c2;
+#pragma unroll
+      for (int rc = 0; rc < TA * TB; ++rc) {
+        double* Rv = R + (rc * m + slot) * S::RP + v;
+        const int64_t off = rowoff[rc];
+        if (off >= 0) {
+          const int mt = rowmeta[rc];
+          if (mt == 0) {
+            a.values[off + v] = *Rv;  // full band: CSR order is the R order
+          } else {
+            const int lod0 = (mt >> 1) & 31, lod1 = (mt >> 6) & 31, c0 = (mt >> 11) & 31,
+                      c1 = (mt >> 16) & 31;
+            if (in2 && d0 >= lod0 && d0 < lod0 + c0 && d1 >= lod1 && d1 < lod1 + c1)
+              a.values[off + ((d0 - lod0) * c1 + (d1 - lod1)) * c2 + (d2 - lod2)] = *Rv;
+          }
         }
+        *Rv = 0.0;
       }
-      *Rv = 0.0;
     }
   };
   int pending = -1;
   for (int e2 = e_first; e2 < s1; ++e2) {
     __syncthreads();  // previous column's stage S (reads Y, aliasing W) is done
     if (pending >= 0) set_rowoff(pending);
+#ifdef GSF_ABL_W
+    if (e2 < 0)
+#endif
+    {
+      double w2[Q];  // axis-2 weights of this column
 #pragma unroll
-    for (int i = 0; i < UPT; ++i) {  // W = ((w0 w1) w2) jac c, the reference's factor order
-      const int u = tid + i * NT;
-      if (u < NUW) {
-        const int kk = u / KB, c1 = u - kk * KB;
-        const double w01 = wa[kk] * wb[c1];
-        double* dst = sW + kk * GCW + c1;  // column (k2, c1): k2 slowest
+      for (int k2 = 0; k2 < Q; ++k2) w2[k2] = axis_w(wqs, a.wt, e2, k2, Q);
 #pragma unroll
-        for (int k2 = 0; k2 < Q; ++k2)
-          dst[k2 * KB] = w01 * axis_w(wqs, a.wt, e2, k2, Q) * a.jac * cv[i][k2];
+      for (int i = 0; i < UPT; ++i) {  // W = ((w0 w1) w2) jac c, the reference's factor order
+        if (wdst[i] >= 0) {
+          const int u = tid + i * NT, kk = u / KB, c1 = u - kk * KB;
+          const double w01 = wa[kk] * wb[c1];
+          double* dst = sW + wdst[i];  // column (k2, c1): k2 slowest
+#pragma unroll
+          for (int k2 = 0; k2 < Q; ++k2) dst[k2 * KB] = w01 * w2[k2] * a.jac * cv[i][k2];
+        }
       }
     }
     load_coef(e2 + 1, cv);
@@ -400,9 +446,14 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
     load_z(e2 + 1, zv);
     __syncthreads();
 
+#ifndef GSF_ABL_F  // ablation knob (tools/gsf_variants.sh): skip the row flush
     if (pending >= 0) flush_row(pending);
+#endif
     // ---- stage A: X_T[a0][col] = sum_kk PA_T[a0][kk] W[kk][col]; warp w keeps the PA
     // fragments of m-tile w % MT in registers and sweeps its n-tiles
+#ifdef GSF_ABL_A
+    if (e2 < 0)
+#endif
     {
       using BA = Band<P, Q, TA>;
       constexpr int MT = cdiv(NA0, 8), NTL = cdiv(GC, 8), KS = cdiv(KA, 4);
@@ -439,6 +490,9 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
 
     // ---- stage B: rows (a0, k2), columns b1; warp w keeps the PB fragments of n-tile
     // w % NTL in registers:  mass YA = XV VV;  stiffness YA = XV DD + XD VV, YB = XV VV
+#ifdef GSF_ABL_B
+    if (e2 < 0)
+#endif
     {
       using BB = Band<P, Q, TB>;
       constexpr int MT = cdiv(NR, 8), NTL = cdiv(NB1, 8), KS = cdiv(KB, 4);
@@ -471,8 +525,15 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
           }
           const int c0 = ntl * 8 + 2 * t;
           if (row < NR) {
-            if (c0 < NB1) Y2[(a0 * NB1 + c0) * Q + k2] = Elem<STIFF>::mk(ya0, yb0);
-            if (c0 + 1 < NB1) Y2[(a0 * NB1 + c0 + 1) * Q + k2] = Elem<STIFF>::mk(ya1, yb1);
+            constexpr int YPS = S::YPS;
+            if (c0 < NB1) {
+              Yd[(a0 * NB1 + c0) * YPS + k2] = ya0;
+              if (STIFF) Yd[(a0 * NB1 + c0) * YPS + Q + k2] = yb0;
+            }
+            if (c0 + 1 < NB1) {
+              Yd[(a0 * NB1 + c0 + 1) * YPS + k2] = ya1;
+              if (STIFF) Yd[(a0 * NB1 + c0 + 1) * YPS + Q + k2] = yb1;
+            }
           }
         }
       });
@@ -482,11 +543,15 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
     // ---- stage S: C[combo][(r,s)] = sum_k2 Y[combo][k2] Z[k2][(r,s)] into the rolling
     // rows; warp w keeps the Z fragments of n-tile w % NTL and its lanes' two (r,s)
     // destinations, and sweeps the combo m-tiles
+#ifdef GSF_ABL_S
+    if (e2 < 0)
+#endif
     {
       // n-tiles of (r, s) pairs; one or two pairs left over past the last full n-tile
       // (p = 2: 9 pairs, p = 4: 25) are summed with DFMAs below instead of a DMMA tile that
       // is 1/8 or 2/8 useful
-      constexpr int MM = m * m, MT = cdiv(NC, 8), KS = cdiv(Q, 4);
+      constexpr int MM = m * m, MT = cdiv(NC, 8), KQ = STIFF ? 2 * Q : Q, KS = cdiv(KQ, 4);
+      constexpr int YPS = S::YPS;
 #ifndef GSF_NOLEFT
       constexpr int NTL = (MM > 8 && MM % 8 != 0 && MM % 8 <= 2) ? MM / 8 : cdiv(MM, 8);
 #else
@@ -496,12 +561,24 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
       const int slot0 = e2 % m;
       if (warp < NTL * GRP) {
         const int ntl = warp % NTL, grp = warp / NTL, n = ntl * 8 + g;
-        double2 z[KS];
+        // B fragments: k < Q value products (VV), Q <= k < 2Q derivative products (DD (+VV))
+#ifndef GSF_NOSTACK
+        double z[KS];
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks) {
           const int k = ks * 4 + t;
-          z[ks] = (n < MM && k < Q) ? as2(Z2[k * MM + n]) : make_double2(0.0, 0.0);
+          const double2 zz = (n < MM && k < KQ) ? as2(Z2[(k < Q ? k : k - Q) * MM + n]) : make_double2(0.0, 0.0);
+          z[ks] = k < Q ? zz.x : zz.y;
         }
+#else
+        constexpr int KS1 = cdiv(Q, 4);
+        double2 z2[KS1];
+#pragma unroll
+        for (int ks = 0; ks < KS1; ++ks) {
+          const int k = ks * 4 + t;
+          z2[ks] = (n < MM && k < Q) ? as2(Z2[k * MM + n]) : make_double2(0.0, 0.0);
+        }
+#endif
         int dst[2];  // offset of column (r, s) in a combo's R block, -1 if padding
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
@@ -510,20 +587,34 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
           dst[j] = nn < MM ? slot * S::RP + sc - r + P : -1;
         }
         for (int mt = grp; mt < MT; mt += GRP) {
-          const int combo = mt * 8 + qw_row(g, qw_dist(Q));  // Y rows are Q double2 apart
-          double c0v = 0.0, c1v = 0.0;
+          const int combo = mt * 8 + g;
+          const int cc = combo;  // C row = A row of this lane
+          double* Rc = R + comboR[cc < NC ? cc : 0];
+          // the rolling-row values are the C operand: R += Y Z in the DMMA itself
+          double c0v = (cc < NC && dst[0] >= 0) ? Rc[dst[0]] : 0.0;
+          double c1v = (cc < NC && dst[1] >= 0) ? Rc[dst[1]] : 0.0;
+#ifndef GSF_NOSTACK
 #pragma unroll
           for (int ks = 0; ks < KS; ++ks) {
             const int k = ks * 4 + t;
-            const double2 y = (combo < NC && k < Q) ? as2(Y2[combo * Q + k]) : make_double2(0.0, 0.0);
-            dmma(c0v, c1v, y.x, z[ks].x);
-            if (STIFF) dmma(c0v, c1v, y.y, z[ks].y);
+            const double y = (combo < NC && k < KQ) ? Yd[combo * YPS + k] : 0.0;
+            dmma(c0v, c1v, y, z[ks]);
           }
-          const int cc = combo;  // C row = A row of this lane
+#else
+#pragma unroll
+          for (int ks = 0; ks < KS1; ++ks) {
+            const int k = ks * 4 + t;
+            const double ya = (combo < NC && k < Q) ? Yd[combo * YPS + k] : 0.0;
+            dmma(c0v, c1v, ya, z2[ks].x);
+            if (STIFF) {
+              const double yb = (combo < NC && k < Q) ? Yd[combo * YPS + Q + k] : 0.0;
+              dmma(c0v, c1v, yb, z2[ks].y);
+            }
+          }
+#endif
           if (cc < NC) {
-            double* Rc = R + comboR[cc];
-            if (dst[0] >= 0) Rc[dst[0]] += c0v;
-            if (dst[1] >= 0) Rc[dst[1]] += c1v;
+            if (dst[0] >= 0) Rc[dst[0]] = c0v;
+            if (dst[1] >= 0) Rc[dst[1]] = c1v;
           }
         }
       }
@@ -532,15 +623,15 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
         constexpr int NL = MM - NTL * 8;
         for (int u = tid; u < NC * NL; u += NT) {
           const int c = u / NL, nn = NTL * 8 + u % NL, r = nn / m, sc = nn % m;
-          double acc = 0.0;
-#pragma unroll
-          for (int k = 0; k < Q; ++k) {
-            const double2 y = as2(Y2[c * Q + k]), zz = as2(Z2[k * MM + nn]);
-            acc = fma(y.x, zz.x, acc);
-            if (STIFF) acc = fma(y.y, zz.y, acc);
-          }
           const int slot = slot0 + r >= m ? slot0 + r - m : slot0 + r;
-          R[comboR[c] + slot * S::RP + sc - r + P] += acc;
+          double* Rr = R + comboR[c] + slot * S::RP + sc - r + P;
+          double acc = *Rr;
+#pragma unroll
+          for (int k = 0; k < KQ; ++k) {
+            const double2 zz = as2(Z2[(k < Q ? k : k - Q) * MM + nn]);
+            acc = fma(Yd[c * YPS + k], k < Q ? zz.x : zz.y, acc);
+          }
+          *Rr = acc;
         }
       }
     }

@@ -51,7 +51,6 @@ constexpr int XP = NCOL + 4;             // X row pitch (== 4 mod 16: conflict-f
 constexpr int NA0 = TA * NB;             // (ia, d0) rows (14)
 constexpr int NCOMBO = NA0 * TB * NB;    // (ia, d0, ib, d1) combos (392)
 constexpr int YP = NCOMBO + 4;           // Y pitch (== 12 mod 16: conflict-free A loads)
-constexpr int NT = 512;                  // threads: 16 warps
 constexpr int MT_A = NCOL / 8;           // 14 m-tiles of (g1,k2) columns
 constexpr int MT_B = NA0 * Q / 8;        // 7 m-tiles of (a0,k2) rows
 constexpr int MT_S = NCOMBO / 8;         // 49 m-tiles of combos
@@ -61,8 +60,12 @@ constexpr int MT_S = NCOMBO / 8;         // 49 m-tiles of combos
 #ifndef P3_NWS
 #define P3_NWS 7
 #endif
-constexpr int NWA = 4, NWB = P3_NWB, NWS = P3_NWS;  // warps per role (NWA even: fixed type per A warp)
-static_assert(NWA + NWB + NWS == 16, "16 warps");
+#ifndef P3_NWA
+#define P3_NWA 4
+#endif
+constexpr int NWA = P3_NWA, NWB = P3_NWB, NWS = P3_NWS;  // warps per role (NWA even: fixed type per A warp)
+static_assert(NWA % 2 == 0, "stage-A warps come in (value, derivative) pairs");
+constexpr int NT = 32 * (NWA + NWB + NWS);  // threads (16 warps by default)
 constexpr int MT_S_PER_WARP = (MT_S + NWS - 1) / NWS;  // 7
 constexpr int NHB = 2 * MT_B;            // stage-B half units (m-tile, ib pair)
 constexpr int NPEN = TA * TB;            // row pencils (I0, I1) of the tile
@@ -107,12 +110,23 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* b, int parity) {
+#ifdef P3_MBHINT
+  // suspend-time hint (ns): a waiting warp sleeps until the phase completes instead of
+  // re-polling, leaving its issue slots to the warps that feed the tensor pipe
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "MBW%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      " @!p bra MBW%=;\n}\n" ::"r"(smem_u32(b)),
+      "r"(parity), "n"(P3_MBHINT)
+      : "memory");
+#else
   asm volatile(
       "{\n .reg .pred p;\n"
       "MBW%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
       " @!p bra MBW%=;\n}\n" ::"r"(smem_u32(b)),
       "r"(parity)
       : "memory");
+#endif
 }
 
 __host__ __device__ constexpr int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
@@ -142,6 +156,9 @@ struct Lane {
 #endif
 #ifndef P3_SORD
 #define P3_SORD 0
+#endif
+#ifndef P3_ROWP
+#define P3_ROWP 0
 #endif
 __device__ __forceinline__ double sel(bool c, double a, double b) { return c ? a : b; }
 __device__ __forceinline__ void split_groups(const double* y, int t, double& hi, double& lo) {
@@ -329,17 +346,49 @@ __device__ __forceinline__ void store_pair(const GsfArgs& a, int m, const int64_
   }
 }
 
+// this lane's CSR destinations of row e2 for each of its stage-S m-tiles (nullptr: the combo
+// is not written here) and the two band offsets; independent of Y, so the S warps form
+// them while they wait for stage B
+struct SDst {
+  double* rowp[MT_S_PER_WARP];
+  int dh, dl;
+};
+__device__ __forceinline__ void s_dst(SDst& d, int t, int I2, int64_t N, const GsfArgs& a,
+                                      const int (&meta)[MT_S_PER_WARP], const int64_t* pb,
+                                      const int* pc) {
+  const RowDst rd = row_dst(t, I2, N);
+  d.dh = rd.dh;
+  d.dl = rd.dl;
+#pragma unroll
+  for (int i = 0; i < MT_S_PER_WARP; ++i) {
+    const int m = meta[i];
+    d.rowp[i] = nullptr;
+    if (m >= 0) {
+      const int rc = m >> 16, b01 = m & 0xffff;
+      d.rowp[i] = a.values + pb[rc] + (int64_t)pc[rc] * rd.pre2 + b01 * rd.c2;
+    }
+  }
+}
+__device__ __forceinline__ void store_dst(const SDst& d, int i, double hi, double lo) {
+  double* row = d.rowp[i];
+  if (row != nullptr) {
+    if (d.dh >= 0) row[d.dh] = hi;
+    if (d.dl >= 0) row[d.dl] = lo;
+  }
+}
+
 template <int PHI, int I0, int NM>
 __device__ __forceinline__ void stage_s_batch(const Lane& L, int ws, const double* Y, double* Rs,
                                               const double (&b0)[2], const double (&b1)[2],
                                               const int (&meta)[MT_S_PER_WARP], const int64_t* pb,
-                                              const int* pc, const GsfArgs& a, const RowDst& rd) {
+                                              const int* pc, const GsfArgs& a, const RowDst& rd,
+                                              const SDst& sd) {
   const int g = L.g, t = L.t;
   double a0[NM], a1[NM], cc[NM][2][2], lo[NM];
   int p[NM][2][2];
   if (MT_S % NWS != 0 && ws + (I0 + NM - 1) * NWS >= MT_S) {
     // uneven split: the last m-tile of this batch does not exist for this warp
-    if constexpr (NM > 1) stage_s_batch<PHI, I0, NM - 1>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd);
+    if constexpr (NM > 1) stage_s_batch<PHI, I0, NM - 1>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd, sd);
     return;
   }
 #pragma unroll
@@ -391,7 +440,11 @@ __device__ __forceinline__ void stage_s_batch(const Lane& L, int ws, const doubl
 #pragma unroll
     for (int k = 1; k < 4; ++k) Rs[p[i][k >> 1][k & 1]] = cc[i][k >> 1][k & 1];
 #ifndef P3_ABL_NOSTORE
+#if P3_ROWP
+    store_dst(sd, I0 + i, cc[i][0][0], lo[i]);
+#else
     store_pair(a, meta[I0 + i], pb, pc, rd, cc[i][0][0], lo[i]);
+#endif
 #else
     if (cc[i][0][0] == 1.2345e-300) store_pair(a, meta[I0 + i], pb, pc, rd, cc[i][0][0], lo[i]);
 #endif
@@ -422,18 +475,22 @@ template <int PHI>
 __device__ __forceinline__ void stage_s(const Lane& L, int ws, const double* Y, double* Rs,
                                         const GsfArgs& a, int e2, const int (&meta)[MT_S_PER_WARP],
                                         const int64_t* pb, const int* pc, int64_t N,
-                                        const double (&b0)[2], const double (&b1)[2]) {
+                                        const double (&b0)[2], const double (&b1)[2], const SDst& sd) {
   const int t = L.t;
+#if P3_ROWP
+  const RowDst rd{};
+#else
   const RowDst rd = row_dst(t, e2, N);
+#endif
   // batches of at most 4 m-tiles (loads of a batch issued before its DMMAs)
   constexpr int B0 = MT_S_PER_WARP <= 4 ? MT_S_PER_WARP : (MT_S_PER_WARP <= 8 ? (MT_S_PER_WARP + 1) / 2 : 4);
   constexpr int R1 = MT_S_PER_WARP - B0;
   constexpr int B1 = R1 <= 4 ? R1 : (R1 + 1) / 2;
   constexpr int B2 = R1 - B1;
   static_assert(B2 <= 4, "stage S batches");
-  stage_s_batch<PHI, 0, B0>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd);
-  if constexpr (B1 > 0) stage_s_batch<PHI, B0, B1>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd);
-  if constexpr (B2 > 0) stage_s_batch<PHI, B0 + B1, B2>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd);
+  stage_s_batch<PHI, 0, B0>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd, sd);
+  if constexpr (B1 > 0) stage_s_batch<PHI, B0, B1>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd, sd);
+  if constexpr (B2 > 0) stage_s_batch<PHI, B0 + B1, B2>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd, sd);
 }
 
 // Rows K .. K+P-1 (no element e2 = I2): both groups are complete in their slots.
@@ -635,6 +692,10 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
       const int it = e2 + 2;
       PT(2);
       const int b = e2 & 1;
+      SDst sd;
+#if P3_ROWP
+      s_dst(sd, L.t, e2, N, a, meta, pb, pc);
+#endif
       mbar_wait(yfull + b, (e2 >> 1) & 1);
       PT(1);
       const double* Y = sm + OFF_Y + b * SZ_Y;
@@ -642,10 +703,10 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
       if (e2 < 0)
 #endif
       switch (e2 & 3) {
-        case 0: stage_s<0>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1); break;
-        case 1: stage_s<1>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1); break;
-        case 2: stage_s<2>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1); break;
-        default: stage_s<3>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1); break;
+        case 0: stage_s<0>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1, sd); break;
+        case 1: stage_s<1>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1, sd); break;
+        case 2: stage_s<2>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1, sd); break;
+        default: stage_s<3>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1, sd); break;
       }
       if (e2 + 1 < K) s_fragments(L, a, e2 + 1, sb0, sb1);
       mbar_arrive(yempty + b);

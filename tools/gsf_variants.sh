@@ -12,3 +12,4 @@ for v in "$@"; do
     $NV -shared -o tune/$name/libiga_b200.so tune/$name/iga_gsf_mma.o $OBJS -lcudart ) &
 done
 wait
+for v in "$@"; do name=${v%%:*}; test -f tune/$name/libiga_b200.so || { echo "variant $name failed:"; grep -m5 error tune/$name/ptxas.log; exit 1; }; done
