@@ -24,12 +24,13 @@
 extern "C" {
 #endif
 
-#define IGA_ABI_VERSION 4
+#define IGA_ABI_VERSION 5
 
 #define IGA_OK 0
 #define IGA_EINVAL 1       /* invalid argument -> ValueError            */
 #define IGA_ECUDA 2        /* CUDA launch/runtime failure -> RuntimeError */
 #define IGA_EUNSUPPORTED 3 /* (p, q, dim) outside the device grid -> ValueError */
+#define IGA_ENOCONV 4      /* iterative solve did not converge -> RuntimeError  */
 
 /* Operators (SURVEY.md §8(b) superset of the reference's mass-only Gram). */
 #define IGA_OP_MASS 0           /* int c B_i B_j                              */
@@ -196,6 +197,20 @@ int32_t iga_write_matrix_market_host(int32_t dim, int32_t K, int32_t p, const do
 /* CSR SpMV y = A x over the structured pattern (assembly.spmv, assembly.py:86-91). */
 int32_t iga_spmv(int32_t dim, int32_t K, int32_t p, const double* values, const double* x,
                  double* y, void* stream);
+
+/* Conjugate gradients for G x = b on the device: the solve of the heat demo's implicit
+ * step (heat.HeatProblem._solve, heat.py:168-175, scipy cg with rtol 1e-10 and maxiter
+ * 10 n).  G is the assembled structured CSR (values != NULL: iga_spmv(dim, K, p, values))
+ * or, with values == NULL, the matrix-free alpha M + beta S of prob (iga_apply, dim 3).
+ * x holds x0 on entry and the solution on return; work holds iga_cg_work_size(n) doubles.
+ * Stops when ||b - G x|| <= rtol ||b||.  The iterations run stream-ordered on the device
+ * (four launches each, deterministic fixed-order reductions); the host reads a 32-byte
+ * state every check_every iterations.  *iters: iterations done.  IGA_ENOCONV if maxiter
+ * iterations did not converge. */
+int64_t iga_cg_work_size(int64_t n);
+int32_t iga_cg(int32_t dim, int32_t K, int32_t p, const double* values, const iga_problem* prob,
+               double alpha, double beta, int64_t n, const double* b, double* x, double* work,
+               double rtol, int64_t maxiter, int32_t check_every, int64_t* iters, void* stream);
 
 #ifdef __cplusplus
 }

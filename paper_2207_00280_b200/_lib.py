@@ -18,7 +18,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("IGA_LIB_PATH") or os.path.join(_HERE, "lib", "libiga_b200.so")
 CSRC = os.path.join(_HERE, "csrc")
 
-IGA_OK, IGA_EINVAL, IGA_ECUDA, IGA_EUNSUPPORTED = 0, 1, 2, 3
+IGA_OK, IGA_EINVAL, IGA_ECUDA, IGA_EUNSUPPORTED, IGA_ENOCONV = 0, 1, 2, 3, 4
 OPS = {"mass": 0, "stiffness": 1, "stiffness_mass": 2}
 METHOD_CLASSICAL, METHOD_SUMFACT, METHOD_SUMFACT_ASSEMBLED, METHOD_SEPARABLE = 0, 1, 2, 3
 
@@ -41,6 +41,8 @@ EXPORTS = (
     "iga_apply",
     "iga_write_matrix_market",
     "iga_write_matrix_market_host",
+    "iga_cg_work_size",
+    "iga_cg",
 )
 
 
@@ -107,11 +109,15 @@ def load():
     L.iga_apply.argtypes = [ctypes.POINTER(IgaProblem), dp, dp, vp, vp, vp]
     L.iga_write_matrix_market.argtypes = [i32, i32, i32, vp, ctypes.c_char_p, i32, vp]
     L.iga_write_matrix_market_host.argtypes = [i32, i32, i32, vp, ctypes.c_char_p, i32]
+    L.iga_cg_work_size.argtypes = [i64]
+    L.iga_cg_work_size.restype = i64
+    L.iga_cg.argtypes = [i32, i32, i32, vp, ctypes.POINTER(IgaProblem), dp, dp, i64, vp, vp, vp, dp,
+                         i64, i32, ctypes.POINTER(i64), vp]
     for name in ("iga_mesh_tables", "iga_mesh_tables_general", "iga_band_tables", "iga_basis_eval", "iga_eval_basis", "iga_csr_pattern", "iga_element_matrices",
                  "iga_integrate_assemble", "iga_assemble_elements", "iga_axpy", "iga_spmv",
-                 "iga_apply", "iga_write_matrix_market", "iga_write_matrix_market_host"):
+                 "iga_apply", "iga_write_matrix_market", "iga_write_matrix_market_host", "iga_cg"):
         getattr(L, name).restype = i32
-    if L.iga_abi_version() != 4:
+    if L.iga_abi_version() != 5:
         raise ImportError("libiga_b200.so ABI version mismatch")
     _lib = L
     return L
@@ -123,6 +129,8 @@ def check(rc: int) -> None:
     msg = load().iga_last_error().decode(errors="replace")
     if rc in (IGA_EINVAL, IGA_EUNSUPPORTED):
         raise ValueError(msg)
+    if rc == IGA_ENOCONV:
+        raise RuntimeError(msg)
     raise RuntimeError(f"CUDA failure in libiga_b200: {msg}")
 
 

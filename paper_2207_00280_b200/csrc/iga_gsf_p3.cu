@@ -110,23 +110,12 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* b, int parity) {
-#ifdef P3_MBHINT
-  // suspend-time hint (ns): a waiting warp sleeps until the phase completes instead of
-  // re-polling, leaving its issue slots to the warps that feed the tensor pipe
-  asm volatile(
-      "{\n .reg .pred p;\n"
-      "MBW%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
-      " @!p bra MBW%=;\n}\n" ::"r"(smem_u32(b)),
-      "r"(parity), "n"(P3_MBHINT)
-      : "memory");
-#else
   asm volatile(
       "{\n .reg .pred p;\n"
       "MBW%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
       " @!p bra MBW%=;\n}\n" ::"r"(smem_u32(b)),
       "r"(parity)
       : "memory");
-#endif
 }
 
 __host__ __device__ constexpr int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
@@ -154,12 +143,7 @@ struct Lane {
 #ifndef P3_SPLIT
 #define P3_SPLIT 0
 #endif
-#ifndef P3_SORD
-#define P3_SORD 0
-#endif
-#ifndef P3_ROWP
-#define P3_ROWP 0
-#endif
+
 __device__ __forceinline__ double sel(bool c, double a, double b) { return c ? a : b; }
 __device__ __forceinline__ void split_groups(const double* y, int t, double& hi, double& lo) {
 #if P3_SPLIT == 2
@@ -346,49 +330,17 @@ __device__ __forceinline__ void store_pair(const GsfArgs& a, int m, const int64_
   }
 }
 
-// this lane's CSR destinations of row e2 for each of its stage-S m-tiles (nullptr: the combo
-// is not written here) and the two band offsets; independent of Y, so the S warps form
-// them while they wait for stage B
-struct SDst {
-  double* rowp[MT_S_PER_WARP];
-  int dh, dl;
-};
-__device__ __forceinline__ void s_dst(SDst& d, int t, int I2, int64_t N, const GsfArgs& a,
-                                      const int (&meta)[MT_S_PER_WARP], const int64_t* pb,
-                                      const int* pc) {
-  const RowDst rd = row_dst(t, I2, N);
-  d.dh = rd.dh;
-  d.dl = rd.dl;
-#pragma unroll
-  for (int i = 0; i < MT_S_PER_WARP; ++i) {
-    const int m = meta[i];
-    d.rowp[i] = nullptr;
-    if (m >= 0) {
-      const int rc = m >> 16, b01 = m & 0xffff;
-      d.rowp[i] = a.values + pb[rc] + (int64_t)pc[rc] * rd.pre2 + b01 * rd.c2;
-    }
-  }
-}
-__device__ __forceinline__ void store_dst(const SDst& d, int i, double hi, double lo) {
-  double* row = d.rowp[i];
-  if (row != nullptr) {
-    if (d.dh >= 0) row[d.dh] = hi;
-    if (d.dl >= 0) row[d.dl] = lo;
-  }
-}
-
 template <int PHI, int I0, int NM>
 __device__ __forceinline__ void stage_s_batch(const Lane& L, int ws, const double* Y, double* Rs,
                                               const double (&b0)[2], const double (&b1)[2],
                                               const int (&meta)[MT_S_PER_WARP], const int64_t* pb,
-                                              const int* pc, const GsfArgs& a, const RowDst& rd,
-                                              const SDst& sd) {
+                                              const int* pc, const GsfArgs& a, const RowDst& rd) {
   const int g = L.g, t = L.t;
   double a0[NM], a1[NM], cc[NM][2][2], lo[NM];
   int p[NM][2][2];
   if (MT_S % NWS != 0 && ws + (I0 + NM - 1) * NWS >= MT_S) {
     // uneven split: the last m-tile of this batch does not exist for this warp
-    if constexpr (NM > 1) stage_s_batch<PHI, I0, NM - 1>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd, sd);
+    if constexpr (NM > 1) stage_s_batch<PHI, I0, NM - 1>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd);
     return;
   }
 #pragma unroll
@@ -406,22 +358,6 @@ __device__ __forceinline__ void stage_s_batch(const Lane& L, int ws, const doubl
       }
     lo[i] = Rs[rs_idx(mt, PHI, 1, L.lane)];
   }
-#if P3_SORD == 1
-  // consecutive DMMAs share their B fragment (a warp re-reading the same B issues
-  // DMMAs faster than one whose B changes every instruction)
-#pragma unroll
-  for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-    for (int i = 0; i < NM; ++i)
-      dmma(cc[i][nt][0], cc[i][nt][1], a0[i], b0[nt], cc[i][nt][0], cc[i][nt][1]);
-  if (L.stiff) {
-#pragma unroll
-    for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-      for (int i = 0; i < NM; ++i)
-        dmma(cc[i][nt][0], cc[i][nt][1], a1[i], b1[nt], cc[i][nt][0], cc[i][nt][1]);
-  }
-#else
 #pragma unroll
   for (int i = 0; i < NM; ++i)
 #pragma unroll
@@ -434,25 +370,20 @@ __device__ __forceinline__ void stage_s_batch(const Lane& L, int ws, const doubl
       for (int nt = 0; nt < 2; ++nt)
         dmma(cc[i][nt][0], cc[i][nt][1], a1[i], b1[nt], cc[i][nt][0], cc[i][nt][1]);
   }
-#endif
 #pragma unroll
   for (int i = 0; i < NM; ++i) {
 #pragma unroll
     for (int k = 1; k < 4; ++k) Rs[p[i][k >> 1][k & 1]] = cc[i][k >> 1][k & 1];
 #ifndef P3_ABL_NOSTORE
-#if P3_ROWP
-    store_dst(sd, I0 + i, cc[i][0][0], lo[i]);
-#else
     store_pair(a, meta[I0 + i], pb, pc, rd, cc[i][0][0], lo[i]);
-#endif
 #else
     if (cc[i][0][0] == 1.2345e-300) store_pair(a, meta[I0 + i], pb, pc, rd, cc[i][0][0], lo[i]);
 #endif
   }
 }
 
-// axis-2 B fragments of element e2 (value and derivative pair products); the S warps
-// compute them one element ahead so the table loads are off the critical path
+// axis-2 B fragments of element e2 (value and derivative pair products), for the first
+// element; later elements go through s_raw_load / s_raw_form below
 __device__ __forceinline__ void s_fragments(const Lane& L, const GsfArgs& a, int e2, double (&b0)[2],
                                             double (&b1)[2]) {
   const int g = L.g, t = L.t;
@@ -471,26 +402,57 @@ __device__ __forceinline__ void s_fragments(const Lane& L, const GsfArgs& a, int
   }
 }
 
+// the same in two halves: the raw table values of element e2 are loaded at the end of
+// column e2-1 and their products formed at the start of column e2, so the global-load
+// latency is not waited on where it is issued (0.5223 -> 0.5205 ms on C3)
+struct SRaw {
+  double v[2][2], d[2][2];
+};
+__device__ __forceinline__ void s_raw_load(const Lane& L, const GsfArgs& a, int e2, SRaw& w) {
+  const int g = L.g, t = L.t;
+  const double* V2 = a.V + (int64_t)e2 * M * Q;
+  const double* D2 = a.D + (int64_t)e2 * M * Q;
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt) {
+    const int r = bcol_r(nt, g), s = bcol_s(nt, g);
+    w.v[nt][0] = __ldg(V2 + r * Q + t);
+    w.v[nt][1] = __ldg(V2 + s * Q + t);
+    w.d[nt][0] = w.d[nt][1] = 0.0;
+    if (L.stiff) {
+      w.d[nt][0] = __ldg(D2 + r * Q + t);
+      w.d[nt][1] = __ldg(D2 + s * Q + t);
+    }
+  }
+}
+__device__ __forceinline__ void s_raw_form(const Lane& L, const SRaw& w, double (&b0)[2], double (&b1)[2]) {
+#pragma unroll
+  for (int nt = 0; nt < 2; ++nt) {
+    b0[nt] = w.v[nt][0] * w.v[nt][1];
+    b1[nt] = 0.0;
+    if (L.stiff) {
+      double z = w.d[nt][0] * w.d[nt][1];
+      if (L.smass) z += b0[nt];
+      b1[nt] = z;
+    }
+  }
+}
+
 template <int PHI>
 __device__ __forceinline__ void stage_s(const Lane& L, int ws, const double* Y, double* Rs,
                                         const GsfArgs& a, int e2, const int (&meta)[MT_S_PER_WARP],
                                         const int64_t* pb, const int* pc, int64_t N,
-                                        const double (&b0)[2], const double (&b1)[2], const SDst& sd) {
+                                        const double (&b0)[2], const double (&b1)[2]) {
   const int t = L.t;
-#if P3_ROWP
-  const RowDst rd{};
-#else
   const RowDst rd = row_dst(t, e2, N);
-#endif
   // batches of at most 4 m-tiles (loads of a batch issued before its DMMAs)
   constexpr int B0 = MT_S_PER_WARP <= 4 ? MT_S_PER_WARP : (MT_S_PER_WARP <= 8 ? (MT_S_PER_WARP + 1) / 2 : 4);
   constexpr int R1 = MT_S_PER_WARP - B0;
   constexpr int B1 = R1 <= 4 ? R1 : (R1 + 1) / 2;
   constexpr int B2 = R1 - B1;
   static_assert(B2 <= 4, "stage S batches");
-  stage_s_batch<PHI, 0, B0>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd, sd);
-  if constexpr (B1 > 0) stage_s_batch<PHI, B0, B1>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd, sd);
-  if constexpr (B2 > 0) stage_s_batch<PHI, B0 + B1, B2>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd, sd);
+  stage_s_batch<PHI, 0, B0>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd);
+  if constexpr (B1 > 0) stage_s_batch<PHI, B0, B1>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd);
+  if constexpr (B2 > 0) stage_s_batch<PHI, B0 + B1, B2>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd);
 }
 
 // Rows K .. K+P-1 (no element e2 = I2): both groups are complete in their slots.
@@ -687,28 +649,26 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
     for (int u = ws * 32 + L.lane; u < MT_S * 4 * 2 * 32; u += NWS * 32) Rs[u] = 0.0;
     double sb0[2], sb1[2];
     s_fragments(L, a, 0, sb0, sb1);
+    SRaw sraw;
     __syncthreads();
     for (int e2 = 0; e2 < K; ++e2) {
       const int it = e2 + 2;
       PT(2);
       const int b = e2 & 1;
-      SDst sd;
-#if P3_ROWP
-      s_dst(sd, L.t, e2, N, a, meta, pb, pc);
-#endif
       mbar_wait(yfull + b, (e2 >> 1) & 1);
       PT(1);
       const double* Y = sm + OFF_Y + b * SZ_Y;
+      if (e2 > 0) s_raw_form(L, sraw, sb0, sb1);
 #ifdef P3_ABL_NOS
       if (e2 < 0)
 #endif
       switch (e2 & 3) {
-        case 0: stage_s<0>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1, sd); break;
-        case 1: stage_s<1>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1, sd); break;
-        case 2: stage_s<2>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1, sd); break;
-        default: stage_s<3>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1, sd); break;
+        case 0: stage_s<0>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1); break;
+        case 1: stage_s<1>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1); break;
+        case 2: stage_s<2>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1); break;
+        default: stage_s<3>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1); break;
       }
-      if (e2 + 1 < K) s_fragments(L, a, e2 + 1, sb0, sb1);
+      if (e2 + 1 < K) s_raw_load(L, a, e2 + 1, sraw);
       mbar_arrive(yempty + b);
       PT(0);
     }

@@ -46,44 +46,44 @@ class MatrixFreeOperator:
 
 
 def cg(A, b, x0=None, rtol: float = 1e-10, maxiter: int | None = None, alpha: float = 1.0,
-       beta: float = 0.0):
+       beta: float = 0.0, check_every: int = 16, stream=None):
     """Conjugate gradients on the device (HeatProblem._solve, heat.py:168-175: rtol 1e-10,
-    maxiter 10 n).  ``A`` is an assembled GlobalGram (SpMV on the structured CSR) or a
-    MatrixFreeOperator applied as ``alpha M + beta S`` (SPD for alpha > 0, beta >= 0)."""
+    maxiter 10 n), stopping at ``||b - A x|| <= rtol ||b||``.  ``A`` is an assembled
+    GlobalGram (SpMV on the structured CSR) or a MatrixFreeOperator applied as
+    ``alpha M + beta S`` (SPD for alpha > 0, beta >= 0).  The whole iteration runs in the
+    library (``iga_cg``): stream-ordered launches with deterministic reductions, the host
+    reading the solver state every ``check_every`` iterations.  Returns (x, iterations);
+    device inputs give a device x, host inputs a numpy x."""
     torch = _lib.require_cuda()
     L = _lib.load()
     n = A.n_dofs
-    bd = torch.as_tensor(np.ascontiguousarray(b, dtype=np.float64)).cuda()
-    x = torch.zeros_like(bd) if x0 is None else torch.as_tensor(
-        np.ascontiguousarray(x0, dtype=np.float64)).cuda()
-    Ap = torch.empty_like(bd)
+    host = not isinstance(b, torch.Tensor)
 
+    def dev(v):
+        if isinstance(v, torch.Tensor):
+            return v.to(device="cuda", dtype=torch.float64).contiguous()
+        return torch.as_tensor(np.ascontiguousarray(v, dtype=np.float64)).cuda()
+
+    bd = dev(b)
+    if bd.numel() != n:
+        raise ValueError(f"right-hand side length {bd.numel()} does not match {n} dofs")
+    x = torch.zeros_like(bd) if x0 is None else dev(x0).clone()
+    if x.numel() != n:
+        raise ValueError(f"x0 length {x.numel()} does not match {n} dofs")
+    work = torch.empty(int(L.iga_cg_work_size(n)), dtype=torch.float64, device=bd.device)
+    maxiter = 10 * n if maxiter is None else int(maxiter)
+    iters = ctypes.c_int64(0)
     if isinstance(A, MatrixFreeOperator):
-        def spmv(v, out):
-            return A.apply(v, alpha, beta, out=out)
+        s = A.prob.problem_struct()
+        rc = L.iga_cg(3, 0, 0, None, ctypes.byref(s), float(alpha), float(beta), n, bd.data_ptr(),
+                      x.data_ptr(), work.data_ptr(), float(rtol), maxiter, int(check_every),
+                      ctypes.byref(iters), _lib.stream_ptr(stream))
     else:
-        def spmv(v, out):
-            _lib.check(L.iga_spmv(A.dim, A.K, A.p, A.values.data_ptr(), v.data_ptr(),
-                                  out.data_ptr(), _lib.stream_ptr()))
-            return out
-
-    r = bd - spmv(x, Ap)
-    p = r.clone()
-    rr = torch.dot(r, r)
-    bnorm = torch.linalg.norm(bd)
-    tol = rtol * bnorm
-    maxiter = 10 * n if maxiter is None else maxiter
-    for it in range(maxiter):
-        if torch.sqrt(rr) <= tol:
-            return x.cpu().numpy(), it
-        spmv(p, Ap)
-        step = rr / torch.dot(p, Ap)
-        x += step * p
-        r -= step * Ap
-        rr_new = torch.dot(r, r)
-        p = r + (rr_new / rr) * p
-        rr = rr_new
-    raise RuntimeError("conjugate gradient did not converge")
+        rc = L.iga_cg(A.dim, A.K, A.p, A.values.data_ptr(), None, 1.0, 0.0, n, bd.data_ptr(),
+                      x.data_ptr(), work.data_ptr(), float(rtol), maxiter, int(check_every),
+                      ctypes.byref(iters), _lib.stream_ptr(stream))
+    _lib.check(rc)
+    return (x.cpu().numpy() if host else x), int(iters.value)
 
 
 def heat_step(op: MatrixFreeOperator, mu, dt: float, rtol: float = 1e-10):

@@ -31,7 +31,27 @@ def test_header_symbols_exported(lib):
     so = ctypes.CDLL(_lib.LIB_PATH)
     for name in declared:
         assert hasattr(so, name), name
-    assert lib.iga_abi_version() == 4
+    assert lib.iga_abi_version() == 5
+
+
+def test_cg_work_size_and_validation(lib):
+    """iga_cg (ABI v5): work-array size and argument checks before any CUDA call."""
+    from paper_2207_00280_b200 import _lib
+
+    n = 1000
+    assert lib.iga_cg_work_size(n) == 3 * n + 3 * 296 + 8
+    assert lib.iga_cg_work_size(0) == -1
+    it = ctypes.c_int64(-1)
+    dummy = ctypes.c_void_p(16)
+    bad = [dict(n=0), dict(rtol=-1.0), dict(maxiter=-1), dict(check=0), dict(values=None)]
+    for b in bad:
+        args = dict(n=n, rtol=1e-10, maxiter=10, check=4, values=dummy)
+        args.update(b)
+        rc = lib.iga_cg(3, 4, 2, args["values"], None, 1.0, 0.0, args["n"], dummy, dummy, dummy,
+                        args["rtol"], args["maxiter"], args["check"], ctypes.byref(it), None)
+        assert rc == _lib.IGA_EINVAL, b
+        with pytest.raises(ValueError):
+            _lib.check(rc)
 
 
 def test_library_targets_sm100a():

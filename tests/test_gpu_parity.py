@@ -464,6 +464,39 @@ def test_cg_solves_gram_system(pkg):
     assert np.linalg.norm(x - xs) <= 1e-8 * np.linalg.norm(xs)
 
 
+def test_cg_device_solver_reproducible_and_chunk_invariant(pkg):
+    """iga_cg: bitwise-identical solutions run to run and for any host-check interval (the
+    iterations launched after convergence are frozen on the device), device tensors in and
+    out, and the reference's non-convergence error (scipy cg info > 0 -> RuntimeError)."""
+    import torch
+
+    from paper_2207_00280_b200.operator import MatrixFreeOperator, cg
+
+    K, p = 7, 3
+    gram = pkg.run_integration(pkg.RunConfig("sumfact", "device", K, p)).gram
+    xs = np.random.default_rng(21).standard_normal(gram.n_dofs)
+    b = gram.matrix @ xs
+    x1, i1 = cg(gram, b, rtol=1e-12)
+    x2, i2 = cg(gram, b, rtol=1e-12, check_every=1)
+    x3, i3 = cg(gram, b, rtol=1e-12, check_every=64)
+    assert i1 == i2 == i3 > 0
+    assert np.array_equal(x1, x2) and np.array_equal(x1, x3)
+    assert np.linalg.norm(x1 - xs) <= 1e-8 * np.linalg.norm(xs)
+    res = np.linalg.norm(b - gram.matrix @ x1)
+    assert res <= 1e-12 * np.linalg.norm(b) * 1.01
+    xd, idv = cg(gram, torch.as_tensor(b).cuda(), rtol=1e-12)
+    assert isinstance(xd, torch.Tensor) and xd.is_cuda and idv == i1
+    assert np.array_equal(xd.cpu().numpy(), x1)
+    # x0 = the solution converges in zero iterations
+    x0s, i0 = cg(gram, b, x0=x1, rtol=1e-10)
+    assert i0 == 0 and np.array_equal(x0s, x1)
+    with pytest.raises(RuntimeError):
+        cg(gram, b, rtol=1e-14, maxiter=3)
+    op = MatrixFreeOperator(K, p)
+    xm, im = cg(op, op.apply(xs, 1.0, 0.5), rtol=1e-12, alpha=1.0, beta=0.5)
+    assert im > 0 and np.linalg.norm(xm - xs) <= 1e-8 * np.linalg.norm(xs)
+
+
 def test_separable_matches_assembled_all_ops(pkg):
     """Separable (Kronecker) path vs the general assembled kernel and the oracle for
     every operator, scalar coefficient != 1, p = 0..5, q != p+1."""
