@@ -1,5 +1,7 @@
 """Matrix-free operator application (iga_apply) vs SpMV on the assembled matrix
-(iga_spmv) for the C3 mesh: device time per application (CUDA events, L2 flushed)."""
+(iga_spmv) for the C3 mesh: device time per application (CUDA events, L2 flushed);
+then the heat step's CG solve (iga_cg, the loop inside the library) against the same
+iteration written as eager torch with a host sync per iteration (round 1's operator.cg)."""
 import json
 import os
 import sys
@@ -54,8 +56,61 @@ def main():
         _lib.check(L.iga_spmv(3, K, p, _lib.ptr(vals), _lib.ptr(x), _lib.ptr(y), st))
 
     t_spmv = timeit(spmv)
-    print(json.dumps({"K": K, "p": p, "n_dofs": n, "apply_ms": t_apply, "spmv_ms": t_spmv,
-                      "spmv_GBps": (vals.numel() * 8 + 2 * n * 8) / (t_spmv / 1e3) / 1e9}))
+    out = {"K": K, "p": p, "n_dofs": n, "apply_ms": t_apply, "spmv_ms": t_spmv,
+           "spmv_GBps": (vals.numel() * 8 + 2 * n * 8) / (t_spmv / 1e3) / 1e9}
+
+    # CG: (M + dt S) u = b matrix-free, and G u = b on the assembled mass matrix
+    from paper_2207_00280_b200.operator import cg
+
+    gram_m = P.run_integration(P.RunConfig("sumfact", "device", K, p)).gram
+    b = torch.randn(n, dtype=torch.float64, device="cuda")
+
+    def eager(apply_fn, rtol=1e-10):
+        xk = torch.zeros_like(b)
+        r = b.clone()
+        pk = r.clone()
+        Ap = torch.empty_like(b)
+        rr = torch.dot(r, r)
+        tol = rtol * torch.linalg.norm(b)
+        for it in range(10 * n):
+            if torch.sqrt(rr) <= tol:  # host sync every iteration
+                return it
+            apply_fn(pk, Ap)
+            a = rr / torch.dot(pk, Ap)
+            xk += a * pk
+            r -= a * Ap
+            rr2 = torch.dot(r, r)
+            pk = r + (rr2 / rr) * pk
+            rr = rr2
+        return -1
+
+    def mf_apply(v, o):
+        _lib.check(L.iga_apply(ctypes.byref(s), 1.0, 0.01, _lib.ptr(v), _lib.ptr(o), st))
+
+    def mass_spmv(v, o):
+        _lib.check(L.iga_spmv(3, K, p, _lib.ptr(gram_m.values), _lib.ptr(v), _lib.ptr(o), st))
+
+    for name, A, kw, fn in (("cg_matrix_free", op, dict(alpha=1.0, beta=0.01), mf_apply),
+                            ("cg_assembled_mass", gram_m, {}, mass_spmv)):
+        res = {}
+        for _ in range(2):
+            torch.cuda.synchronize()
+            a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            _, its = cg(A, b, rtol=1e-10, **kw)
+            e.record()
+            torch.cuda.synchronize()
+            res = {"iters": its, "ms": a.elapsed_time(e)}
+        a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        its_e = eager(fn)
+        e.record()
+        torch.cuda.synchronize()
+        res.update(ms_per_iter=res["ms"] / max(1, res["iters"]), eager_iters=its_e,
+                   eager_ms=a.elapsed_time(e))
+        res["eager_ms_per_iter"] = res["eager_ms"] / max(1, its_e)
+        out[name] = res
+    print(json.dumps(out))
 
 
 if __name__ == "__main__":
