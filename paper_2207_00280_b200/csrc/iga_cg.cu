@@ -154,6 +154,15 @@ int32_t iga_cg(int32_t dim, int32_t K, int32_t p, const double* values, const ig
   if (rtol < 0.0) return fail_einval("rtol must be >= 0");
   if (maxiter < 0) return fail_einval("maxiter must be >= 0");
   if (check_every < 1) return fail_einval("check_every must be >= 1");
+  {
+    const int d = values ? dim : 3;
+    const int64_t N = values ? (int64_t)K + p : (int64_t)prob->K + prob->p;
+    int64_t want = 1;
+    for (int i = 0; i < d; ++i) want *= N;
+    if ((d != 2 && d != 3) || N < 1 || n != want)
+      return fail_einval("system size %lld does not match the operator's %lld dofs", (long long)n,
+                         (long long)want);
+  }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   double* r = work;
   double* pv = r + n;

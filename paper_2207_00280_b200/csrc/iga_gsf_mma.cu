@@ -119,7 +119,9 @@ struct WarpTile {
 };
 template <int MT, class B, int NW, int ITEMS>
 __device__ __forceinline__ WarpTile warp_tile(int warp) {
+  static_assert(MT <= NW, "every tile needs at least one warp");
   constexpr Split<MT> s = make_split<MT, B>(NW, ITEMS);
+  static_assert(s.start[MT] <= NW, "warp split exceeds the CTA");
   WarpTile w;
 #pragma unroll
   for (int t = 0; t < MT; ++t)

@@ -43,7 +43,9 @@ def test_cg_work_size_and_validation(lib):
     assert lib.iga_cg_work_size(0) == -1
     it = ctypes.c_int64(-1)
     dummy = ctypes.c_void_p(16)
-    bad = [dict(n=0), dict(rtol=-1.0), dict(maxiter=-1), dict(check=0), dict(values=None)]
+    n = (4 + 2) ** 3  # K = 4, p = 2
+    bad = [dict(n=0), dict(n=n + 1), dict(rtol=-1.0), dict(maxiter=-1), dict(check=0),
+           dict(values=None)]
     for b in bad:
         args = dict(n=n, rtol=1e-10, maxiter=10, check=4, values=dummy)
         args.update(b)
