@@ -376,6 +376,8 @@ struct GsfTile {
 
 int launch_gsf_p3(const GsfArgs& a, cudaStream_t s);  // iga_gsf_p3.cu (DMMA, p=3 q=4)
 int launch_gsf_mma(const GsfArgs& a, int p, int q, cudaStream_t s);  // iga_gsf_mma.cu (DMMA)
+int launch_gsf_tile(const GsfArgs& a, int p, int q, cudaStream_t s);  // iga_tile.cu (p <= 2)
+bool tile_wins(int p, int op);                                         // iga_tile.cu
 
 template <int P, int Q, bool ST>
 static int launch_gsf_generic(const GsfArgs& a0, cudaStream_t s) {
@@ -422,6 +424,18 @@ struct GsfLaunch {
       // tensor-core specialisation; IGA_GSF_GENERIC=1 selects the generic kernel (A/B tests)
       const char* env = getenv("IGA_GSF_GENERIC");
       if (!(env && env[0] == '1')) return launch_gsf_p3(a0, s);
+    }
+    if constexpr (P >= 1 && P <= 2) {
+      // non-streaming tile kernel where it is the faster one; IGA_GSF_TILE=0 / 1 forces the
+      // streaming / tile kernels (A/B tests)
+      static const int tile_env = [] {
+        const char* e = getenv("IGA_GSF_TILE");
+        return e == nullptr || e[0] == 0 || e[1] != 0 ? -1 : (e[0] == '0' ? 0 : (e[0] == '1' ? 1 : -1));
+      }();
+      if (tile_env == 1 || (tile_env == -1 && tile_wins(P, a0.op))) {
+        const int rc = launch_gsf_tile(a0, P, Q, s);
+        if (rc != IGA_EUNSUPPORTED) return rc;  // else: tile does not fit shared memory
+      }
     }
     // DMMA GEMM formulation; IGA_GSF_SCALAR=1 selects this file's scalar kernel (A/B tests,
     // uniform knots only)
