@@ -375,6 +375,12 @@ struct GsfTile {
 };
 
 int launch_gsf_p3(const GsfArgs& a, cudaStream_t s);  // iga_gsf_p3.cu (DMMA, p=3 q=4)
+
+// A/B knobs: on only for the exact value "1", read once per process
+static bool env_is_one(const char* name) {
+  const char* e = getenv(name);
+  return e != nullptr && e[0] == '1' && e[1] == 0;
+}
 int launch_gsf_mma(const GsfArgs& a, int p, int q, cudaStream_t s);  // iga_gsf_mma.cu (DMMA)
 int launch_gsf_tile(const GsfArgs& a, int p, int q, cudaStream_t s);  // iga_tile.cu (p <= 2)
 bool tile_wins(int p, int op);                                         // iga_tile.cu
@@ -422,8 +428,8 @@ struct GsfLaunch {
   static int run(const GsfArgs& a0, cudaStream_t s) {
     if constexpr (P == 3 && Q == 4) {
       // tensor-core specialisation; IGA_GSF_GENERIC=1 selects the generic kernel (A/B tests)
-      const char* env = getenv("IGA_GSF_GENERIC");
-      if (!(env && env[0] == '1')) return launch_gsf_p3(a0, s);
+      static const bool generic = env_is_one("IGA_GSF_GENERIC");
+      if (!generic) return launch_gsf_p3(a0, s);
     }
     if constexpr (P >= 1 && P <= 2) {
       // non-streaming tile kernel where it is the faster one; IGA_GSF_TILE=0 / 1 forces the
@@ -439,8 +445,8 @@ struct GsfLaunch {
     }
     // DMMA GEMM formulation; IGA_GSF_SCALAR=1 selects this file's scalar kernel (A/B tests,
     // uniform knots only)
-    const char* sc = getenv("IGA_GSF_SCALAR");
-    if (!(sc && sc[0] == '1') || a0.wt != nullptr) return launch_gsf_mma(a0, P, Q, s);
+    static const bool scalar = env_is_one("IGA_GSF_SCALAR");
+    if (!scalar || a0.wt != nullptr) return launch_gsf_mma(a0, P, Q, s);
     if (a0.op == IGA_OP_MASS) return launch_gsf_generic<P, Q, false>(a0, s);
     if constexpr (P >= 1) return launch_gsf_generic<P, Q, true>(a0, s);
     set_error("derivatives require degree >= 1");

@@ -693,9 +693,12 @@ static int launch_t(const GsfArgs& a0, cudaStream_t s) {
     const int64_t slots = (int64_t)sm_count() * blocks_per_sm_once(fn, NT, Sh::bytes);
     int best = 1;
     double best_cost = 1e300;
-    const char* es = getenv("IGA_GSF_SEGS");  // tuning knob: force the segment count
+    static const int force_segs = [] {  // tuning knob: force the segment count (read once)
+      const char* es = getenv("IGA_GSF_SEGS");
+      return es && *es ? atoi(es) : 0;
+    }();
     for (int sg = 1; sg <= a.K; ++sg) {
-      if (es && *es && sg != atoi(es)) continue;
+      if (force_segs > 0 && sg != force_segs) continue;
       const int L = (a.K + sg - 1) / sg;
       if (L < P && sg > 1) break;
       const double waves = (double)((tiles * sg + slots - 1) / slots);
