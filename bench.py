@@ -258,7 +258,13 @@ def kernel_roofline(code, wl, K, p, q, k_el, by, kern_ms, peaks):
     name = KERNEL_NAMES[code]
     if code == 0 and wl["dim"] == 2:
         name = f"k_classical_scatter<2,{p},{q}> (Algorithm 1, scalar FP64 + fused CSR scatter)"
-    if code == 2 and not (p == 3 and q == 4):
+    tile_env = os.environ.get("IGA_GSF_TILE")
+    tile = wl["dim"] == 3 and (tile_env == "1" or (tile_env != "0" and (p == 1 or (p == 2 and wl["op"] == "mass"))))
+    if code == 2 and p in (1, 2) and tile:
+        # the dispatch of csrc/iga_gsf.cu (tile_wins): non-streaming tile kernel
+        name = (f"k_tile3<{p},{q}> (assembled sum factorization per 3D row tile: TMA coefficient "
+                f"window, register band rows, scalar FP64 + CSR write)")
+    elif code == 2 and not (p == 3 and q == 4):
         name = (f"k_gsf3<{p},{q}> (assembled sum factorization, scalar FP64 + CSR write)"
                 if os.environ.get("IGA_GSF_SCALAR") == "1" else
                 f"k_gsf3_mma<{p},{q}> (assembled sum factorization, DMMA GEMMs + CSR write)")

@@ -2,7 +2,7 @@
 # reference arm, C4, C2, p9), ncu launch lists and full captures of the kernels they
 # time, GPU suite and smoke.  Run under gpurun (one GPU); summarise with
 # tools/profile_summary.py into profiles/.
-TAG=${TAG:-r02m}
+TAG=${TAG:-r02q}
 O=gpurun_out
 set -x
 python bench.py > $O/${TAG}_bench.json 2> $O/${TAG}_bench.err
@@ -20,7 +20,7 @@ $NCUF -k regex:k_kron3 -o $O/${TAG}_kron $B --assembly separable --no-alt > $O/$
 $NCUL --log-file $O/${TAG}_launches_c4.csv $B --workload c4 --no-alt > $O/${TAG}_ncu_l4.log 2>&1
 $NCUF -k regex:k_gsf3_mma -o $O/${TAG}_c4 $B --workload c4 --no-alt > $O/${TAG}_ncu_c4.log 2>&1
 $NCUL --log-file $O/${TAG}_launches_c2.csv $B --workload c2 --no-alt > $O/${TAG}_ncu_l2.log 2>&1
-$NCUF -k regex:k_gsf3_mma -o $O/${TAG}_c2 $B --workload c2 --no-alt > $O/${TAG}_ncu_c2.log 2>&1
+$NCUF -k regex:"k_tile3|k_gsf3_mma" -o $O/${TAG}_c2 $B --workload c2 --no-alt > $O/${TAG}_ncu_c2.log 2>&1
 export IGA_PARITY_LOG=$O/${TAG}_parity.jsonl
 rm -f $IGA_PARITY_LOG
 python -m pytest tests -m gpu -q > $O/${TAG}_pytest.log 2>&1; tail -2 $O/${TAG}_pytest.log
