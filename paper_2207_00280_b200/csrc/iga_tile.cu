@@ -400,49 +400,54 @@ __global__ void __launch_bounds__(NT, 2)
         });
   __syncthreads();
 
-  // ---- stage S: vectors = the ((ia,d0), (ib,d1)) rows of Y (d1 fastest: consecutive lanes
-  // write consecutive (d0, d1) blocks of a CSR row); the outputs go straight to the CSR.
-  // (Assembling a pencil's rows in shared memory first and writing contiguous runs measured
-  // 25% slower on C2: the extra barrier and copy loop cost more than the strided stores.)
+  // ---- stage S: vectors = the ((ia,d0), (ib,d1)) rows of Y; the outputs go straight to the
+  // CSR.  Each thread keeps one (I0, I1) pencil of its row ic = i (TPP threads per pencil,
+  // taking its (d0, d1) blocks TPP apart), so the pencil's row base and band bounds are read
+  // once per stage instead of per vector.  (Assembling a pencil's rows in shared memory and
+  // writing contiguous runs measured 25% slower on C2: the extra barrier and copy loop cost
+  // more than the 2p+1-value block stores.)
   {
-    int64_t gbase = 0;     // CSR offset of the current vector's (d0, d1) block in row ic = i
+    constexpr int TPI = NT / TC, NPEN = TA * TB, TPP = TPI / NPEN, NBLK = NB * NB;
+    static_assert(TPI % NPEN == 0 && TPP >= 1, "threads split evenly over the pencils");
+    constexpr int KV = (NBLK + TPP - 1) / TPP;  // blocks per thread (the last may be partial)
+    const int ic = tid / TPI, sub = tid - ic * TPI, pen = sub / TPP, bsub = sub - pen * TPP;
+    const int ia = pen / TB, ib = pen - ia * TB;
+    const int lod0 = bnd01[4 * pen], c0 = bnd01[4 * pen + 1], lod1 = bnd01[4 * pen + 2],
+              c1 = bnd01[4 * pen + 3];
+    const int lod2 = bnd2[2 * ic], c2 = bnd2[2 * ic + 1];
+    const int64_t rb = rowb[pen * TC + ic];
+    int64_t gbase = 0;     // CSR offset of the current block in row ic, minus lod2
     int slo = 0, shi = 0;  // its valid d2 range [slo, shi) (empty: outside the band / mesh)
-    auto sctx = [&](int u, int i) {
-      const int ia = u / (TB * NB * NB), r1 = u - ia * (TB * NB * NB);
-      const int ib = r1 / (NB * NB), r2 = r1 - ib * (NB * NB);
-      const int d0 = r2 / NB, d1 = r2 - d0 * NB;
-      const int* bb = bnd01 + 4 * (ia * TB + ib);
-      const int lod0 = bb[0], c0 = bb[1], lod1 = bb[2], c1 = bb[3];
-      const int lod2 = bnd2[2 * i], c2 = bnd2[2 * i + 1];
-      const int64_t rb = rowb[(ia * TB + ib) * TC + i];
+    int yrow = 0;          // its Y row (ia, d0) x (ib, d1)
+    // vector j of stage_band = the thread's (j / TPI)-th block
+    auto sctx = [&](int j) {
+      const int blk = bsub + (j / TPI) * TPP;
+      const int d0 = blk / NB, d1 = blk - d0 * NB;
       slo = shi = 0;
-      if (rb >= 0 && d0 >= lod0 && d0 < lod0 + c0 && d1 >= lod1 && d1 < lod1 + c1) {
+      yrow = blk < NBLK ? (ia * NB + d0) * RB + ib * NB + d1 : 0;
+      if (blk < NBLK && rb >= 0 && d0 >= lod0 && d0 < lod0 + c0 && d1 >= lod1 && d1 < lod1 + c1) {
         gbase = rb + (int64_t)((d0 - lod0) * c1 + (d1 - lod1)) * c2 - lod2;
         slo = lod2;
         shi = lod2 + c2;
       }
-      return (ia * NB + d0) * RB + ib * NB + d1;  // Y row
     };
     for (int ch = 0; ch < NSPL; ++ch)
       stage_band<P, Q, TC, NSPL, ST>(
-          tid, ch, TA * TB * NB * NB, PC, S::GCP, ST ? PC + S::RC * S::GCP : nullptr, S::GCP,
-          [&](int u, int i, double (&v)[(P + 1) * Q]) {
-            const int yr = sctx(u, i);
-            const double* yc = Y + ((ST ? RA * RB : 0) + yr) * GCY + i * Q;  // Y_B (stiffness) / Y
+          tid, ch, TPI * KV, PC, S::GCP, ST ? PC + S::RC * S::GCP : nullptr, S::GCP,
+          [&](int j, int i, double (&v)[(P + 1) * Q]) {
+            sctx(j);
+            const double* yc = Y + ((ST ? RA * RB : 0) + yrow) * GCY + i * Q;  // Y_B (stiffness) / Y
 #pragma unroll
-            for (int j = 0; j < (P + 1) * Q; ++j) v[j] = yc[j];
+            for (int k = 0; k < (P + 1) * Q; ++k) v[k] = yc[k];
           },
           [&](int, int row, double x, double) {
             const int d2 = row % NB;
             if (d2 >= slo && d2 < shi) a.values[gbase + d2] = x;
           },
-          [&](int u, int i, double (&v)[(P + 1) * Q]) {  // second operand type (Y_A)
-            const int ia = u / (TB * NB * NB), r1 = u - ia * (TB * NB * NB);
-            const int ib = r1 / (NB * NB), r2 = r1 - ib * (NB * NB);
-            const int d0 = r2 / NB, d1 = r2 - d0 * NB;
-            const double* yc = Y + ((ia * NB + d0) * RB + ib * NB + d1) * GCY + i * Q;
+          [&](int, int i, double (&v)[(P + 1) * Q]) {  // second operand type (Y_A), same block
+            const double* yc = Y + yrow * GCY + i * Q;
 #pragma unroll
-            for (int j = 0; j < (P + 1) * Q; ++j) v[j] = yc[j];
+            for (int k = 0; k < (P + 1) * Q; ++k) v[k] = yc[k];
           });
   }
   }  // tiles
