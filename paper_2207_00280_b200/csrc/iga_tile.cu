@@ -11,19 +11,21 @@
 // offset d (column J = I - p + d).  P?[(i,d)][(l,k)] = T(I - e, k) T(J - e, k) w_k is
 // nonzero only where the element e = base + l supports both dofs, a compile-time band
 // l in [i + max(0, d - p), i + min(p, d)]: every contraction is a fully unrolled DFMA
-// sequence over exactly its nonzero terms.  The quadrature weights (and the Jacobian) are
-// folded into the P tables, so W is the coefficient field itself, copied into shared
-// memory with cp.async (zero outside the mesh or the element slab).
+// sequence over exactly its nonzero terms, and a thread keeps the band rows of its tile
+// index in registers (stage_band).  The quadrature weights (and the Jacobian) are folded
+// into the P tables, so W is the coefficient field itself, copied into shared memory by
+// one 3D TMA box (zero outside the mesh or the element slab; cp.async where TMA cannot
+// describe the window).  CTAs are persistent, each over a contiguous range of tiles.
 //
 // Why a second kernel for p <= 2: the streaming kernels (k_gsf3_mma, iga_gsf_mma.cu) pay
 // per element column four CTA barriers, a row flush, the pair-table setup of a short
 // segment and DMMA tiles that are mostly padding at these sizes; on C2 (32^3, p = 2 mass
 // with a coefficient field) that was ~680 warp instructions per row, instruction-issue
-// bound at 9% of the HBM roofline.  Here a CTA issues ~4 barriers in total, each thread
-// works on whole columns of one stage with operands in registers, and two CTAs per SM
-// overlap one tile's coefficient copy with the other's arithmetic.  The window
-// recomputation ((T + p) / T per axis) costs flops, which these degrees have to spare.
-// Summation order is fixed (bitwise reproducible).
+// bound at 9% of the HBM roofline.  Here a tile costs ~4 barriers, each thread works on
+// whole vectors of one stage with operands in registers, and two CTAs per SM overlap one
+// tile's coefficient copy with the other's arithmetic.  The window recomputation
+// ((T + p) / T per axis) costs flops, which these degrees have to spare.  Dispatch:
+// tile_wins() below.  Summation order is fixed (bitwise reproducible).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -48,7 +50,7 @@ struct Shape {
   static constexpr int GA = LA * Q, GB = LB * Q, GC = LC * Q;
   static constexpr int RA = TA * NB, RB = TB * NB, RC = TC * NB;
   static constexpr int GCY = GC | 1;  // Y row pitch: odd, stage-S row loads conflict-free
-  // pair-table rows padded to an even length (double2 loads; the pad is 0)
+  // pair-table rows padded to an even length (16-byte aligned rows; the pad is 0)
   static constexpr int GAP = (GA + 1) / 2 * 2, GBP = (GB + 1) / 2 * 2, GCP = (GC + 1) / 2 * 2;
   static constexpr int nW = GA * GB * GC;
   static constexpr int nX = (E * RA * GB * GC + 1) / 2 * 2;
@@ -124,24 +126,6 @@ __device__ __forceinline__ void pair_table(double* Pt, const double* Er, int i0,
       }
     }
     Pt[u] = v;
-  }
-}
-
-// acc[k] += sum_{g in [lo, hi)} p[g] v[k][g] over NK tasks, p read as double2 pairs from an
-// even g (the table is 0 outside the band and in its pad, so the pair's extra term adds an
-// exact 0): one 16-byte broadcast load feeds 2 NK FMAs
-template <int NK, int GP>
-__device__ __forceinline__ void band_dot(const double* p, const double (&v)[NK][GP], double (&acc)[NK], int lo,
-                                         int hi) {
-#pragma unroll
-  for (int g = 0; g < GP; g += 2) {
-    if (g + 1 < lo || g >= hi) continue;  // lo, hi are constants once the caller's loops unroll
-    const double2 pp = *reinterpret_cast<const double2*>(p + g);
-#pragma unroll
-    for (int k = 0; k < NK; ++k) {
-      acc[k] = fma(pp.x, v[k][g], acc[k]);
-      acc[k] = fma(pp.y, v[k][g + 1], acc[k]);
-    }
   }
 }
 
