@@ -80,7 +80,6 @@ __global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) 
   constexpr int SG = kron_stage(P, G);
   extern __shared__ __align__(16) double2 tb[];  // [2][N][NB] (m, k): all elements, slab
   __shared__ double w[Q];
-  __shared__ double2 Fbuf[2][NB * NB];  // pair factors of the current pencil (by pencil parity)
   const int K = a.K, tid = threadIdx.x;
   const int64_t N = (int64_t)K + P;
   const bool stiff = a.op != IGA_OP_MASS;
@@ -125,7 +124,6 @@ __global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) 
   if (a.K > 0) return;
 #endif
   int chunk = 0;  // chunks issued by this CTA (selects the staging buffer)
-  int npen = 0;   // pencil set-ups of this CTA (selects the pair-factor buffer)
   const int64_t T = band_prefix(N, P, N);  // values of a full-length band row set
   // the chunk produced last, stored after the next barrier (thread 0)
   double* pg = nullptr;
@@ -167,21 +165,14 @@ __global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) 
     };
     const int ncnt = c01 * NB;  // values of an interior row
     double fa[NE], fb[NE];
-    int d2[NE];
+    int d2[NE], bp[NE];  // the thread's (pair b, band offset d2) per slot j of an interior row
 #pragma unroll
     for (int j = 0; j < NE; ++j) {
       const int e = tid + j * NT;
       fa[j] = fb[j] = 0.0;
       d2[j] = e % NB;
-      if (e < ncnt) factors(e / NB, fa[j], fb[j]);
-    }
-    // the pencil's pair factors for the truncated rows (visible after the chunk barrier;
-    // double-buffered: a thread may start this pencil while others finish the last)
-    double2* F = Fbuf[npen++ & 1];
-    for (int b = tid; b < c01; b += NT) {
-      double f0, f1;
-      factors(b, f0, f1);
-      F[b] = make_double2(f0, f1);
+      bp[j] = e / NB;
+      if (e < ncnt) factors(bp[j], fa[j], fb[j]);
     }
     const int64_t pc0 = u_lo - pen * nch, pc1 = u_hi - pen * nch;
     const int ch0 = pc0 > 0 ? (int)pc0 : 0, ch1 = pc1 < nch ? (int)pc1 : nch;
@@ -203,16 +194,20 @@ __global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) 
       __syncthreads();
       if (tid == 0) issue();
       double* sb = buf + pad;
-      // truncated-band rows (I2 < P or I2 >= K): b = e / c2 by a reciprocal (exact for
-      // e < 2^20 / NB), factors from the pencil table F
+      // truncated-band rows (I2 < P or I2 >= K): a row holds the same (pair b, offset d2)
+      // values as an interior row for d2 in [lod2, lod2 + c2), at b c2 + d2 - lod2, so every
+      // thread reuses its interior slots' factors (one multiply-add per value; the per-value
+      // division and pair-factor table of round 1 made these rows ~2.5x dearer per value)
       auto boundary_row = [&](int I2, int loc) {
         const double2* t2 = tb + I2 * NB;
         const int c2 = (int)band_cnt(I2, P, N), lod2 = max(0, P - I2);
-        const unsigned inv = (1u << 20) / (unsigned)c2 + 1u;
-        for (int e = tid; e < c01 * c2; e += NT) {
-          const int b = (int)(((unsigned)e * inv) >> 20);
-          const double2 f = F[b], x2 = t2[lod2 + e - b * c2];
-          sb[loc + e] = f.x * x2.x + f.y * x2.y;
+#pragma unroll
+        for (int j = 0; j < NE; ++j) {
+          const int e = tid + j * NT;
+          if (e < ncnt && d2[j] >= lod2 && d2[j] < lod2 + c2) {
+            const double2 x2 = t2[d2[j]];
+            sb[loc + bp[j] * c2 + d2[j] - lod2] = fa[j] * x2.x + fb[j] * x2.y;
+          }
         }
         return loc + c01 * c2;
       };
