@@ -182,7 +182,9 @@ __global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) 
     for (int R0 = ch0 * G; R0 < ch1 * G; R0 += G, ++chunk) {
       const int R1 = min((int)N, R0 + G);
       const bool fast = R0 >= P && R0 + G <= K;
-      const int len = fast ? G * ncnt : c01 * (int)(band_prefix(R1, P, N) - band_prefix(R0, P, N));
+      const int len = fast ? G * ncnt
+                           : (G == 1 ? c01 * (int)band_cnt(R0, P, N)
+                                     : c01 * (int)(band_prefix(R1, P, N) - band_prefix(R0, P, N)));
       double* g = vals + off0;
       off0 += len;
       const int pad = (int)((reinterpret_cast<uintptr_t>(g) >> 3) & 1);
