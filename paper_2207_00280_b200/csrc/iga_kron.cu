@@ -29,15 +29,24 @@ namespace iga {
 #define KRON_MINB 2
 #endif
 
-// threads per CTA: one per value of an interior row (NB^3, rounded to warps, <= 1024)
+// high degrees (p >= 6): every row is split into KRON_HS halves by pair range, each half
+// its own chunk, so a chunk is ~27 KB and two 512-thread CTAs fit one SM (one CTA's per-row
+// barrier overlaps the other's work)
+#ifndef KRON_HS
+#define KRON_HS 2
+#endif
+__host__ __device__ constexpr int kron_split(int P) { return P >= 6 ? KRON_HS : 1; }
+// threads per CTA: one per value of an interior row (NB^3, rounded to warps, <= 1024); 512
+// for the split rows of the high degrees
 __host__ __device__ constexpr int kron_nt(int P) {
-  return ((2 * P + 1) * (2 * P + 1) * (2 * P + 1) + 31) / 32 * 32 > 1024
+  return kron_split(P) > 1 ? 512
+         : ((2 * P + 1) * (2 * P + 1) * (2 * P + 1) + 31) / 32 * 32 > 1024
              ? 1024
              : ((2 * P + 1) * (2 * P + 1) * (2 * P + 1) + 31) / 32 * 32;
 }
 // resident CTAs per SM asked of the register allocator
 __host__ __device__ constexpr int kron_minb(int P) {
-  return P > 3 || kron_nt(P) * KRON_MINB > 1536 ? 1 : KRON_MINB;
+  return kron_split(P) > 1 ? 2 : (P > 3 || kron_nt(P) * KRON_MINB > 1536 ? 1 : KRON_MINB);
 }
 // rows per staged chunk (one TMA bulk store each)
 // (measured on B200: 16 rows with 2 CTAs/SM for the small meshes, where the chunk
@@ -58,7 +67,8 @@ __host__ __device__ constexpr int kron_rows(int P, bool small_mesh) {
 __host__ __device__ constexpr int kron_nbuf(int P) { return P <= 5 ? KRON_NBUF : 3; }
 // doubles per staging buffer: a chunk of full rows plus 16-byte alignment padding
 __host__ __device__ constexpr int kron_stage(int P, int G) {
-  return (G * (2 * P + 1) * (2 * P + 1) * (2 * P + 1) + 3) / 2 * 2;  // even: 16-byte aligned buffers
+  // (a split row: the values of its larger half)
+  return (G * (((2 * P + 1) * (2 * P + 1) + kron_split(P) - 1) / kron_split(P)) * (2 * P + 1) + 3) / 2 * 2;
 }
 
 __device__ __forceinline__ void bulk_store(double* g, const double* sm, int bytes) {
@@ -76,7 +86,10 @@ template <int P, int Q, int G>
 __global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) {
   constexpr int NB = 2 * P + 1;
   constexpr int NT = kron_nt(P);
-  constexpr int NE = (NB * NB * NB + NT - 1) / NT;  // interior values per thread and row
+  constexpr int HS = kron_split(P);
+  static_assert(HS == 1 || G == 1, "split rows are one-row chunks");
+  constexpr int HP0 = (NB * NB + HS - 1) / HS;        // pairs of a full half
+  constexpr int NE = (HP0 * NB + NT - 1) / NT;        // interior values per thread and (half) row
   constexpr int SG = kron_stage(P, G);
   extern __shared__ __align__(16) double2 tb[];  // [2][N][NB] (m, k): all elements, slab
   __shared__ double w[Q];
@@ -96,7 +109,8 @@ __global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) 
   // Work: chunks of G rows of a pencil, in CSR order; CTA b takes the contiguous
   // range [b U / grid, (b+1) U / grid) of the U chunks (balanced to a chunk)
   const int nch = (int)((N + G - 1) / G);
-  const int64_t nunit = (int64_t)(a.plane_end - a.plane_begin) * N * nch;
+  // units: (pencil, half, chunk), in that order
+  const int64_t nunit = (int64_t)(a.plane_end - a.plane_begin) * N * HS * nch;
   const int64_t u_lo0 = nunit * blockIdx.x / gridDim.x, u_hi0 = nunit * (blockIdx.x + 1) / gridDim.x;
   if (a.band) {
     // 1D band matrices precomputed once per step (iga_band_tables): a short copy instead
@@ -106,8 +120,8 @@ __global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) 
     if (!full) {
       if (tid < Q) w[tid] = a.weights[tid];
       __syncthreads();
-      const int i0lo = a.plane_begin + (int)(u_lo0 / nch / N);
-      const int i0hi = a.plane_begin + (int)((u_hi0 - 1) / nch / N);
+      const int i0lo = a.plane_begin + (int)(u_lo0 / nch / HS / N);
+      const int i0hi = a.plane_begin + (int)((u_hi0 - 1) / nch / HS / N);
       for (int u = tid; u < (i0hi - i0lo + 1) * NB; u += NT) {
         const int I0 = i0lo + u / NB, d = u % NB;
         tb[N * NB + I0 * NB + d] =
@@ -141,7 +155,9 @@ __global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) 
   };
   const int64_t u_lo = u_lo0, u_hi = u_hi0;
   double* vals = nullptr;  // first value of the current pencil
-  for (int64_t pen = u_lo / nch; pen * nch < u_hi; ++pen) {
+  for (int64_t ph = u_lo / nch; ph * nch < u_hi; ++ph) {
+    const int64_t pen = ph / HS;
+    const int half = (int)(ph - pen * HS);
     const int I0 = a.plane_begin + (int)(pen / N), I1 = (int)(pen % N);
     // consecutive pencils are contiguous in the CSR: one 64-bit rowptr per CTA
     if (vals == nullptr) vals = a.values + (rowptr3(I0, I1, 0, P, N) - a.base);
@@ -149,6 +165,8 @@ __global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) 
     const int lod0 = max(0, P - I0), lod1 = max(0, P - I1);
     const int c0 = (int)band_cnt(I0, P, N), c1 = (int)band_cnt(I1, P, N), c01 = c0 * c1;
     const double2* r1 = tb + I1 * NB;
+    // this half's pairs [b0, b0 + nb) (the whole row when HS = 1)
+    const int hp = (c01 + HS - 1) / HS, b0 = half * hp, nb = min(c01, b0 + hp) - b0;
     // per-pair factors: value = fa * m2 + fb * k2
     const unsigned inv1 = (1u << 20) / (unsigned)c1 + 1u;  // b / c1 for b < 2^20 / NB
     auto factors = [&](int b, double& fa, double& fb) {
@@ -163,18 +181,19 @@ __global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) 
         fa = s; fb = mm;
       }
     };
-    const int ncnt = c01 * NB;  // values of an interior row
+    const int ncnt = c01 * NB;   // values of an interior row
+    const int hcnt = nb * NB;    // values of this half of an interior row
     double fa[NE], fb[NE];
-    int d2[NE], bp[NE];  // the thread's (pair b, band offset d2) per slot j of an interior row
+    int d2[NE], bp[NE];  // the thread's (pair b - b0, band offset d2) per slot j of the half row
 #pragma unroll
     for (int j = 0; j < NE; ++j) {
-      const int e = tid + j * NT;
+      const int e = tid + j * NT;  // value index inside the half row
       fa[j] = fb[j] = 0.0;
       d2[j] = e % NB;
       bp[j] = e / NB;
-      if (e < ncnt) factors(bp[j], fa[j], fb[j]);
+      if (e < hcnt) factors(b0 + bp[j], fa[j], fb[j]);
     }
-    const int64_t pc0 = u_lo - pen * nch, pc1 = u_hi - pen * nch;
+    const int64_t pc0 = u_lo - ph * nch, pc1 = u_hi - ph * nch;
     const int ch0 = pc0 > 0 ? (int)pc0 : 0, ch1 = pc1 < nch ? (int)pc1 : nch;
     // value offset of row R0 inside the pencil (int: a pencil holds < 2^31 values);
     // full-band chunks advance it without the band_prefix arithmetic
@@ -182,11 +201,13 @@ __global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) 
     for (int R0 = ch0 * G; R0 < ch1 * G; R0 += G, ++chunk) {
       const int R1 = min((int)N, R0 + G);
       const bool fast = R0 >= P && R0 + G <= K;
-      const int len = fast ? G * ncnt
-                           : (G == 1 ? c01 * (int)band_cnt(R0, P, N)
-                                     : c01 * (int)(band_prefix(R1, P, N) - band_prefix(R0, P, N)));
-      double* g = vals + off0;
-      off0 += len;
+      // rows of the chunk: their band counts sum (one row: band_cnt, no band_prefix pair)
+      const int rows_c2 = fast ? G * NB
+                               : (G == 1 ? (int)band_cnt(R0, P, N)
+                                         : (int)(band_prefix(R1, P, N) - band_prefix(R0, P, N)));
+      const int len = nb * rows_c2;                       // values of this chunk
+      double* g = vals + off0 + (HS > 1 ? b0 * rows_c2 : 0);  // (HS > 1: one row)
+      off0 += c01 * rows_c2;
       const int pad = (int)((reinterpret_cast<uintptr_t>(g) >> 3) & 1);
       double* buf = stage + (chunk % kron_nbuf(P)) * SG;
       // One CTA barrier per chunk: before it, the bulk store that last read this buffer
@@ -206,16 +227,16 @@ __global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) 
 #pragma unroll
         for (int j = 0; j < NE; ++j) {
           const int e = tid + j * NT;
-          if (e < ncnt && d2[j] >= lod2 && d2[j] < lod2 + c2) {
+          if (e < hcnt && d2[j] >= lod2 && d2[j] < lod2 + c2) {
             const double2 x2 = t2[d2[j]];
             sb[loc + bp[j] * c2 + d2[j] - lod2] = fa[j] * x2.x + fb[j] * x2.y;
           }
         }
-        return loc + c01 * c2;
+        return loc + nb * c2;
       };
       int loc = 0;  // value offset of the next row inside the chunk
       for (int I2 = R0; I2 < min(R1, P); ++I2) loc = boundary_row(I2, loc);
-      // full-band rows [max(R0,P), min(R1,K)): a fixed (pair, d2) per thread, rows ncnt apart
+      // full-band rows [max(R0,P), min(R1,K)): a fixed (pair, d2) per thread, rows hcnt apart
       const int ib = max(R0, P), nr = min(R1, K) - ib;
       if (nr > 0) {
         const double2* t2 = tb + ib * NB;
@@ -226,13 +247,13 @@ __global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) 
 #pragma unroll
             for (int j = 0; j < NE; ++j) {
               const int e = tid + j * NT;
-              if (e < ncnt) {
+              if (e < hcnt) {
                 const double2 x2 = t2[r * NB + d2[j]];
-                sbi[r * ncnt + e] = fa[j] * x2.x + fb[j] * x2.y;
+                sbi[r * hcnt + e] = fa[j] * x2.x + fb[j] * x2.y;
               }
             }
           }
-        loc += nr * ncnt;
+        loc += nr * hcnt;
       }
       for (int I2 = max(R0, max(K, P)); I2 < R1; ++I2) loc = boundary_row(I2, loc);
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -240,7 +261,8 @@ __global__ void __launch_bounds__(kron_nt(P), kron_minb(P)) k_kron3(KronArgs a) 
         pg = g; psb = sb; plen = len; ppad = pad;
       }
     }
-    vals += (int64_t)c01 * T;
+    (void)ncnt;
+    if (half == HS - 1) vals += (int64_t)c01 * T;
   }
   __syncthreads();
   if (tid == 0) {
@@ -358,7 +380,7 @@ static int launch_kron_g(const KronArgs& a, cudaStream_t s) {
   cudaError_t e = smem_attr_once(fn, smem, true);
   if (e != cudaSuccess) return check_cuda(e, "kron smem attr");
   const int per_sm = blocks_per_sm_once(fn, NT, smem), sms = sm_count();
-  const int64_t nunit = (int64_t)(a.plane_end - a.plane_begin) * N * ((N + G - 1) / G);
+  const int64_t nunit = (int64_t)(a.plane_end - a.plane_begin) * N * kron_split(P) * ((N + G - 1) / G);
   int64_t grid = (int64_t)sms * per_sm;
   if (grid > nunit) grid = nunit;
   if (grid <= 0) return IGA_OK;
