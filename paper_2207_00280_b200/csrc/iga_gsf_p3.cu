@@ -57,6 +57,9 @@ constexpr int MT_S = NCOMBO / 8;         // 49 m-tiles of combos
 #ifndef P3_NWB
 #define P3_NWB 5
 #endif
+#ifndef P3_BT
+#define P3_BT 1
+#endif
 #ifndef P3_NWS
 #define P3_NWS 7
 #endif
@@ -85,9 +88,11 @@ constexpr int OFF_WQ = OFF_Y + 2 * SZ_Y;          // weights [Q]
 constexpr int OFF_PB = OFF_WQ + Q;                // pencil row-pointer bases (int64) [NPEN]
 constexpr int OFF_PC = OFF_PB + NPEN;             // pencil c0*c1 (int in double slots) [NPEN]
 constexpr int OFF_R = OFF_PC + NPEN;              // rolling rows [MT_S][4 slots][2 groups][32]
-constexpr int OFF_MB = OFF_R + MT_S * 4 * 2 * 32;  // mbarriers [xfull 2][xempty 2][yfull 2][yempty 2]
+// axis-2 band table {band_prefix(I2), band_cnt(I2)} for meshes with N <= NBT rows (else computed)
+constexpr int NBT = 1024;
+constexpr int OFF_BT = OFF_R + MT_S * 4 * 2 * 32;  // int2 [NBT]
+constexpr int OFF_MB = OFF_BT + (P3_BT ? NBT : 0);  // mbarriers [xfull 2][xempty 2][yfull 2][yempty 2]
 constexpr int SMEM_DOUBLES = OFF_MB + 8;
-static_assert(SMEM_DOUBLES * 8 <= 227 * 1024, "shared memory budget");
 static_assert(SMEM_DOUBLES * 8 <= 227 * 1024, "shared memory budget");
 constexpr size_t SMEM_BYTES = SMEM_DOUBLES * sizeof(double);
 
@@ -308,11 +313,18 @@ struct RowDst {
   int c2, dh, dl;
 };
 
-__device__ __forceinline__ RowDst row_dst(int t, int I2, int64_t N) {
+// {band_prefix(I2), band_cnt(I2)}: from the shared table when it holds the mesh's rows
+__device__ __forceinline__ int2 band_of(const double* sm, int I2, int64_t N) {
+  if (P3_BT && N <= NBT) return reinterpret_cast<const int2*>(sm + OFF_BT)[I2];
+  return make_int2((int)band_prefix(I2, P, N), (int)band_cnt(I2, P, N));
+}
+
+__device__ __forceinline__ RowDst row_dst(int t, int I2, int64_t N, const double* sm) {
   RowDst r;
   const int lod2 = max(0, P - I2);
-  r.c2 = (int)band_cnt(I2, P, N);
-  r.pre2 = band_prefix(I2, P, N);
+  const int2 b = band_of(sm, I2, N);
+  r.c2 = b.y;
+  r.pre2 = b.x;
   r.dh = P + t - lod2;
   r.dl = t - 1 - lod2;
   if (r.dh >= r.c2) r.dh = -1;
@@ -443,7 +455,7 @@ __device__ __forceinline__ void stage_s(const Lane& L, int ws, const double* Y, 
                                         const int64_t* pb, const int* pc, int64_t N,
                                         const double (&b0)[2], const double (&b1)[2]) {
   const int t = L.t;
-  const RowDst rd = row_dst(t, e2, N);
+  const RowDst rd = row_dst(t, e2, N, Rs - OFF_R);  // Rs = sm + OFF_R
   // batches of at most 4 m-tiles (loads of a batch issued before its DMMAs)
   constexpr int B0 = MT_S_PER_WARP <= 4 ? MT_S_PER_WARP : (MT_S_PER_WARP <= 8 ? (MT_S_PER_WARP + 1) / 2 : 4);
   constexpr int R1 = MT_S_PER_WARP - B0;
@@ -459,7 +471,7 @@ __device__ __forceinline__ void stage_s(const Lane& L, int ws, const double* Y, 
 __device__ __forceinline__ void flush_tail(const Lane& L, int ws, const double* Rs, int I2,
                                            const int (&meta)[MT_S_PER_WARP], const int64_t* pb,
                                            const int* pc, const GsfArgs& a, int64_t N) {
-  const RowDst rd = row_dst(L.t, I2, N);
+  const RowDst rd = row_dst(L.t, I2, N, Rs - OFF_R);
   const int sl = I2 & 3;
 #pragma unroll
   for (int i = 0; i < MT_S_PER_WARP; ++i) {
@@ -554,6 +566,10 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (tid < Q) wq[tid] = a.weights[tid];
+  if (P3_BT && N <= NBT) {
+    int2* bt = reinterpret_cast<int2*>(sm + OFF_BT);
+    for (int I = tid; I < N; I += NT) bt[I] = make_int2((int)band_prefix(I, P, N), (int)band_cnt(I, P, N));
+  }
   if (tid < NPEN) {
     const int64_t I0 = i00 + tid / TB, I1 = i10 + tid % TB;
     pb[tid] = (I0 < N && I1 < N) ? rowptr3(I0, I1, 0, P, N) - a.base : 0;
