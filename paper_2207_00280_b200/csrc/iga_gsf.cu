@@ -374,7 +374,8 @@ struct GsfTile {
                             : GsfShape<P, Q, 2, 2, ST>::bytes <= cap ? 2 : 1;
 };
 
-int launch_gsf_p3(const GsfArgs& a, cudaStream_t s);  // iga_gsf_p3.cu (DMMA, p=3 q=4)
+int launch_gsf_p3(const GsfArgs& a, cudaStream_t s);   // iga_gsf_p3.cu (DMMA, p=3 q=4)
+int launch_gsf_p3s(const GsfArgs& a, cudaStream_t s);  // iga_gsf_p3s.cu (symmetric, whole mesh)
 
 // A/B knobs: on only for the exact value "1", read once per process
 static bool env_is_one(const char* name) {
@@ -429,6 +430,15 @@ struct GsfLaunch {
     if constexpr (P == 3 && Q == 4) {
       // tensor-core specialisation; IGA_GSF_GENERIC=1 selects the generic kernel (A/B tests)
       static const bool generic = env_is_one("IGA_GSF_GENERIC");
+      // the symmetric variant computes J0 >= I0 and mirrors the rest, so it needs every row
+      // of the mesh (a whole-mesh run); IGA_GSF_SYM=0 selects k_gsf3_p3 (A/B tests)
+      static const bool no_sym = [] {
+        const char* e = getenv("IGA_GSF_SYM");
+        return e != nullptr && e[0] == '0' && e[1] == 0;
+      }();
+      const bool whole = a0.plane_begin == 0 && a0.plane_end == a0.K + P && a0.el_begin <= 0 &&
+                         a0.el_end >= a0.K && a0.base == 0;
+      if (!generic && whole && !no_sym) return launch_gsf_p3s(a0, s);
       if (!generic) return launch_gsf_p3(a0, s);
     }
     if constexpr (P >= 1 && P <= 2) {

@@ -1,5 +1,4 @@
-// EXPERIMENT, not part of the library (timed with tools/p3s_time.cu):
-// symmetric variant of k_gsf3_p3 (iga_gsf_p3.cu): the same warp-specialised DMMA pipeline
+// Symmetric variant of k_gsf3_p3 (iga_gsf_p3.cu): the same warp-specialised DMMA pipeline
 // for p = 3, q = 4, computing only the values S[I, J] with J0 >= I0 and writing each value
 // with J0 > I0 twice, at (I, J) and mirrored at (J, I) -- the matrix is symmetric
 // (assembly.py:77-79 stores both triangles; SURVEY.md 9.6 allows computing one and
@@ -9,17 +8,21 @@
 // the hi group is exactly J0 >= I0, so stage A keeps only its hi sums and X has TA (p+1)
 // instead of TA (2p+1) rows: stage B then runs 4 of 7 m-tiles and stage S 28 of 49 (DMMAs
 // per element column 546 -> 372), and the band-group DFMAs of stage A halve.  The mirrored
-// stores are scattered (another pencil's row per lane): measured on C3 the kernel takes
-// 0.391 ms without them and 0.571 ms with them (k_gsf3_p3: 0.520) -- 32 partial-sector L2
-// writes per warp store instruction.  Only valid for whole-mesh runs (every mirror target
-// row in range).
+// values land in another pencil's row per lane: written directly they cost 32 partial-sector
+// L2 writes per warp store instruction (C3: 0.571 ms, against 0.391 without them).  Instead
+// each S warp keeps per-combo rings of its mirrored values by target row (ring_put) and
+// writes every target row's values of a combo as one contiguous run once its last source row
+// is done (emit_runs: hi runs d2' = 0..3 when source row J2 completes, lo runs d2' = 4..6
+// three columns later): C3 0.458 ms against 0.509 for k_gsf3_p3.  Whole-mesh runs only
+// (every mirror target row in range); element slabs and row-plane ranges (multi-GPU) take
+// k_gsf3_p3.
 //
 // Everything else -- tiling, the roles, the mbarrier hand-off, the rolling rows of stage S,
 // the summation order of each computed value -- is k_gsf3_p3's; see its header.
 #include <type_traits>
 
-#include "../../paper_2207_00280_b200/csrc/iga_args.cuh"
-#include "../../paper_2207_00280_b200/csrc/iga_dispatch.cuh"
+#include "iga_args.cuh"
+#include "iga_dispatch.cuh"
 
 namespace iga {
 namespace p3s {
@@ -38,13 +41,16 @@ constexpr int MT_A = NCOL / 8;           // 14 m-tiles of (g1,k2) columns
 constexpr int MT_B = NA0 * Q / 8;        // 7 m-tiles of (a0,k2) rows
 constexpr int MT_S = NCOMBO / 8;         // 49 m-tiles of combos
 #ifndef P3S_NWB
-#define P3S_NWB 4
+#define P3S_NWB 5
 #endif
 #ifndef P3S_NWS
-#define P3S_NWS 6
+#define P3S_NWS 7
 #endif
 #ifndef P3S_NWA
-#define P3S_NWA 6
+#define P3S_NWA 4
+#endif
+#ifndef P3S_RING
+#define P3S_RING 1
 #endif
 constexpr int NWA = P3S_NWA, NWB = P3S_NWB, NWS = P3S_NWS;  // warps per role (NWA even: fixed type per A warp)
 static_assert(NWA % 2 == 0, "stage-A warps come in (value, derivative) pairs");
@@ -74,7 +80,11 @@ constexpr int OFF_MM = OFF_R + MT_S * 4 * 2 * 32;  // [NWS][MT_S_PER_WARP][2][32
 // axis-2 band table {band_prefix(I2), band_cnt(I2)} for meshes with N <= NBT rows (else computed)
 constexpr int NBT = 1024;
 constexpr int OFF_BT = OFF_MM + NWS * MT_S_PER_WARP * 2 * 32;  // int2 [NBT]
-constexpr int OFF_MB = OFF_BT + NBT;  // mbarriers [xfull 2][xempty 2][yfull 2][yempty 2]
+// per S warp, per (m-tile, combo): rings of the mirrored values by target row -- hi runs
+// [4 rows][d2' 0..3], lo runs [4 rows][d2' 4..6] -- so they leave as contiguous runs
+constexpr int RING = 28;
+constexpr int OFF_RING = OFF_BT + NBT;                 // [NWS][MT_S_PER_WARP][8][RING]
+constexpr int OFF_MB = OFF_RING + (P3S_RING ? NWS * MT_S_PER_WARP * 8 * RING : 0);  // mbarriers
 constexpr int SMEM_DOUBLES = OFF_MB + 8;
 static_assert(SMEM_DOUBLES * 8 <= 227 * 1024, "shared memory budget");
 constexpr size_t SMEM_BYTES = SMEM_DOUBLES * sizeof(double);
@@ -354,18 +364,50 @@ __device__ __forceinline__ void store_mirror(const GsfArgs& a, const double* mm,
   }
 }
 
+// Row I2's mirrored values into this lane group's rings: hi -> target J2 = I2 + t at d2' = 3 - t,
+// lo -> J2 = I2 + t - 4 at d2' = 7 - t (ring entry d2' - 4); slot = J2 mod 4
+__device__ __forceinline__ void ring_put(double* rg, int i, int g, int t, int I2, double hi, double lo) {
+  double* r = rg + (i * 8 + g) * RING;
+  const int slot = (I2 + t) & 3;
+  r[slot * 4 + (3 - t)] = hi;
+  if (t > 0) r[16 + slot * 3 + (3 - t)] = lo;
+}
+
+// Target row J2's complete runs of this warp's m-tiles: hi (d2' = t) or lo (d2' = 4 + t, t < 3),
+// one contiguous run per combo (the 4 lanes of its group write consecutive values)
+__device__ __forceinline__ void emit_runs(const GsfArgs& a, const double* rg, const double* mm, int ws, const Lane& L,
+                                          int J2, bool hi, const int2* bt, int64_t N) {
+  const int t = L.t, g = L.g;
+  if (!hi && t == 3) return;
+  const int2 b = band_of(bt, J2, N);
+  const int off = (hi ? t : 4 + t) - max(0, P - J2);
+  if (off < 0 || off >= b.y) return;
+  const int slot = J2 & 3;
+#pragma unroll
+  for (int i = 0; i < MT_S_PER_WARP; ++i) {
+    const int mt = ws + i * NWS;
+    if (mt >= MT_S) break;
+    const int2 cb = *reinterpret_cast<const int2*>(mm + i * 64 + 32);
+    if (cb.y < 0) continue;
+    const int64_t base = *reinterpret_cast<const int64_t*>(mm + i * 64);
+    const double* r = rg + (i * 8 + g) * RING;
+    const double v = hi ? r[slot * 4 + t] : r[16 + slot * 3 + t];
+    a.values[base + (int64_t)cb.x * b.x + cb.y * b.y + off] = v;
+  }
+}
+
 template <int PHI, int I0, int NM>
 __device__ __forceinline__ void stage_s_batch(const Lane& L, int ws, const double* Y, double* Rs,
                                               const double (&b0)[2], const double (&b1)[2],
                                               const int (&meta)[MT_S_PER_WARP], const int64_t* pb,
                                               const int* pc, const GsfArgs& a, const RowDst& rd,
-                                              const double* mm, const MirDst& md) {
+                                              const double* mm, const MirDst& md, double* rg, int e2) {
   const int g = L.g, t = L.t;
   double a0[NM], a1[NM], cc[NM][2][2], lo[NM];
   int p[NM][2][2];
   if (MT_S % NWS != 0 && ws + (I0 + NM - 1) * NWS >= MT_S) {
     // uneven split: the last m-tile of this batch does not exist for this warp
-    if constexpr (NM > 1) stage_s_batch<PHI, I0, NM - 1>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd, mm, md);
+    if constexpr (NM > 1) stage_s_batch<PHI, I0, NM - 1>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd, mm, md, rg, e2);
     return;
   }
 #pragma unroll
@@ -400,7 +442,11 @@ __device__ __forceinline__ void stage_s_batch(const Lane& L, int ws, const doubl
 #pragma unroll
     for (int k = 1; k < 4; ++k) Rs[p[i][k >> 1][k & 1]] = cc[i][k >> 1][k & 1];
     store_pair(a, meta[I0 + i], pb, pc, rd, cc[i][0][0], lo[i]);
+#if P3S_RING
+    ring_put(rg, I0 + i, g, t, e2, cc[i][0][0], lo[i]);
+#else
     store_mirror(a, mm + (I0 + i) * 64, md, cc[i][0][0], lo[i]);
+#endif
   }
 }
 
@@ -463,7 +509,8 @@ template <int PHI>
 __device__ __forceinline__ void stage_s(const Lane& L, int ws, const double* Y, double* Rs,
                                         const GsfArgs& a, int e2, const int (&meta)[MT_S_PER_WARP],
                                         const int64_t* pb, const int* pc, int64_t N,
-                                        const double (&b0)[2], const double (&b1)[2], const double* mm) {
+                                        const double (&b0)[2], const double (&b1)[2], const double* mm,
+                                        double* rg) {
   const int t = L.t;
   const int2* bt = reinterpret_cast<const int2*>(Rs - OFF_R + OFF_BT);  // Rs = sm + OFF_R
   const RowDst rd = row_dst(t, e2, N, bt);
@@ -474,15 +521,22 @@ __device__ __forceinline__ void stage_s(const Lane& L, int ws, const double* Y, 
   constexpr int B1 = R1 <= 4 ? R1 : (R1 + 1) / 2;
   constexpr int B2 = R1 - B1;
   static_assert(B2 <= 4, "stage S batches");
-  stage_s_batch<PHI, 0, B0>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd, mm, md);
-  if constexpr (B1 > 0) stage_s_batch<PHI, B0, B1>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd, mm, md);
-  if constexpr (B2 > 0) stage_s_batch<PHI, B0 + B1, B2>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd, mm, md);
+  stage_s_batch<PHI, 0, B0>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd, mm, md, rg, e2);
+  if constexpr (B1 > 0) stage_s_batch<PHI, B0, B1>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd, mm, md, rg, e2);
+  if constexpr (B2 > 0) stage_s_batch<PHI, B0 + B1, B2>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd, mm, md, rg, e2);
+#if P3S_RING
+  __syncwarp();
+  emit_runs(a, rg, mm, ws, L, e2, true, bt, N);
+  if (e2 >= 3) emit_runs(a, rg, mm, ws, L, e2 - 3, false, bt, N);
+  __syncwarp();
+#endif
 }
 
 // Rows K .. K+P-1 (no element e2 = I2): both groups are complete in their slots.
 __device__ __forceinline__ void flush_tail(const Lane& L, int ws, const double* Rs, int I2,
                                            const int (&meta)[MT_S_PER_WARP], const int64_t* pb,
-                                           const int* pc, const GsfArgs& a, int64_t N, const double* mm) {
+                                           const int* pc, const GsfArgs& a, int64_t N, const double* mm,
+                                           double* rg) {
   const int2* bt = reinterpret_cast<const int2*>(Rs - OFF_R + OFF_BT);  // Rs = sm + OFF_R
   const RowDst rd = row_dst(L.t, I2, N, bt);
   const MirDst md = mir_dst(L.t, I2, N, rd, bt);
@@ -493,9 +547,19 @@ __device__ __forceinline__ void flush_tail(const Lane& L, int ws, const double* 
     if (mt < MT_S) {
       const double hi = Rs[rs_idx(mt, sl, 0, L.lane)], lo = Rs[rs_idx(mt, sl, 1, L.lane)];
       store_pair(a, meta[i], pb, pc, rd, hi, lo);
+#if P3S_RING
+      ring_put(rg, i, L.g, L.t, I2, hi, lo);
+#else
       store_mirror(a, mm + i * 64, md, hi, lo);
+#endif
     }
   }
+#if P3S_RING
+  __syncwarp();
+  emit_runs(a, rg, mm, ws, L, I2, true, bt, N);
+  if (I2 >= 3) emit_runs(a, rg, mm, ws, L, I2 - 3, false, bt, N);
+  __syncwarp();
+#endif
 }
 
 // W[(la,k0)][(g1,k2)] = c w0 w1 w2 jac on the CTA's quadrature slab of column e2
@@ -642,6 +706,7 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3s(GsfArgs a) {
     // b01 = (d0-lo0)*c1 + (d1-lo1) in the CSR row; -1 if the combo is outside
     int meta[MT_S_PER_WARP];
     double* mmw = sm + OFF_MM + ws * MT_S_PER_WARP * 64 + L.lane;  // this lane's mirror metadata
+    double* rgw = sm + OFF_RING + ws * MT_S_PER_WARP * 8 * RING;       // this warp's rings
 #pragma unroll
     for (int i = 0; i < MT_S_PER_WARP; ++i) {
       const int mt = ws + i * NWS;
@@ -687,16 +752,23 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3s(GsfArgs a) {
       const double* Y = sm + OFF_Y + b * SZ_Y;
       if (e2 > 0) s_raw_form(L, sraw, sb0, sb1);
       switch (e2 & 3) {
-        case 0: stage_s<0>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1, mmw); break;
-        case 1: stage_s<1>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1, mmw); break;
-        case 2: stage_s<2>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1, mmw); break;
-        default: stage_s<3>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1, mmw); break;
+        case 0: stage_s<0>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1, mmw, rgw); break;
+        case 1: stage_s<1>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1, mmw, rgw); break;
+        case 2: stage_s<2>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1, mmw, rgw); break;
+        default: stage_s<3>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1, mmw, rgw); break;
       }
       if (e2 + 1 < K) s_raw_load(L, a, e2 + 1, sraw);
       mbar_arrive(yempty + b);
     }
     // rows K .. K+P-1 received their last contribution from element K-1
-    for (int I2 = K; I2 < N; ++I2) flush_tail(L, ws, Rs, I2, meta, pb, pc, a, N, mmw);
+    for (int I2 = K; I2 < N; ++I2) flush_tail(L, ws, Rs, I2, meta, pb, pc, a, N, mmw, rgw);
+#if P3S_RING
+    {
+      // lo runs of the last three target rows (their later sources do not exist)
+      const int2* bt = reinterpret_cast<const int2*>(sm + OFF_BT);
+      for (int J2 = max(0, (int)N - 3); J2 < N; ++J2) emit_runs(a, rgw, mmw, ws, L, J2, false, bt, N);
+    }
+#endif
   }
 }
 

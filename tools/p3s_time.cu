@@ -4,7 +4,7 @@
 #include <cstdio>
 #include <vector>
 #include <cstdlib>
-#include "experiments/iga_gsf_p3s.cu"
+#include "../paper_2207_00280_b200/csrc/iga_gsf_p3s.cu"
 #include "../paper_2207_00280_b200/csrc/iga_abi.cu"
 
 int main() {
