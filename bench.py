@@ -232,6 +232,9 @@ def kernel_roofline(code, wl, K, p, q, k_el, by, kern_ms, peaks):
     from paper_2207_00280_b200 import perfmodel
 
     own = None
+    # the dispatch of csrc/iga_gsf.cu: whole-mesh p = 3, q = 4 runs take the symmetric kernel
+    sym = (code == 2 and wl["dim"] == 3 and p == 3 and q == 4 and k_el == K**wl["dim"]
+           and os.environ.get("IGA_GSF_SYM") != "0" and os.environ.get("IGA_GSF_GENERIC") != "1")
     if code == 3:
         fl = perfmodel.separable_flops(wl["op"], K, p, q) * k_el / K**3
     elif code in (1, 2) and wl["dim"] == 3:
@@ -241,6 +244,9 @@ def kernel_roofline(code, wl, K, p, q, k_el, by, kern_ms, peaks):
         fl = perfmodel.element_sumfact_flops(wl["op"], p, q) * k_el
         if code == 2:
             own = perfmodel.assembled_flops(wl["op"], K, p, q) * k_el / K**3
+            if sym:
+                own_full = own
+                own = perfmodel.symmetric_assembled_flops(wl["op"], K, p, q)
     elif code == 0:
         fl = perfmodel.classical_flops(wl["op"], p, q, wl["dim"]) * k_el
     else:
@@ -268,6 +274,10 @@ def kernel_roofline(code, wl, K, p, q, k_el, by, kern_ms, peaks):
         name = (f"k_gsf3<{p},{q}> (assembled sum factorization, scalar FP64 + CSR write)"
                 if os.environ.get("IGA_GSF_SCALAR") == "1" else
                 f"k_gsf3_mma<{p},{q}> (assembled sum factorization, DMMA GEMMs + CSR write)")
+    elif code == 2 and sym:
+        name = ("k_gsf3_p3s (symmetric assembled sum factorization on DMMA: J0 >= I0 computed, "
+                "the rest mirrored through per-warp rings; general per-quadrature-point "
+                "coefficient path)")
     elif code == 2:
         name = name.replace("k_gsf3", "k_gsf3_p3")
     roof.update({
@@ -287,10 +297,14 @@ def kernel_roofline(code, wl, K, p, q, k_el, by, kern_ms, peaks):
     if own is not None:
         a_own = own / (kern_ms / 1e3) / 1e12
         roof["own_algorithm"] = {
-            "what": "assembled sum factorization (contractions shared by overlapping elements, "
-                    "perfmodel.assembled_flops)",
+            "what": ("symmetric assembled sum factorization (J0 >= I0 half; "
+                     "perfmodel.symmetric_assembled_flops)" if sym else
+                     "assembled sum factorization (contractions shared by overlapping elements, "
+                     "perfmodel.assembled_flops)"),
             "flops": own, "flops_per_element": own / k_el, "achieved": a_own,
             "unit": "TFLOP/s", "frac": a_own / peaks["fp64_tflops"]}
+        if sym:
+            roof["own_algorithm"]["full_assembled_flops"] = own_full
     return roof
 
 

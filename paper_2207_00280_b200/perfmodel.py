@@ -12,6 +12,9 @@ with nnz1 = (K+p)(2p+1) - p(p+1) the 1D band pairs.  Each 1D band pair
 (I, J) overlaps sum_e = K (p+1)^2 element-local pairs in total, which is
 where the K (p+1)^2 factors come from.
 
+The symmetric p = 3 kernel (iga_gsf_p3s.cu, whole-mesh runs) needs only the J0 >= I0 half:
+symmetric_assembled_macs.
+
 Separable path (iga_kron.cu, scalar coefficient): the 1D element integrals
 (types x K (p+1)^2 q MACs per axis, computed once) and per CSR value one
 multiply and one FMA (stiffness; mass: one multiply) -- a few flops per 8-byte
@@ -43,6 +46,30 @@ def assembled_macs(op: str, K: int, p: int, q: int) -> int:
 
 def assembled_flops(op: str, K: int, p: int, q: int) -> int:
     return 2 * assembled_macs(op, K, p, q)
+
+
+def nnz1_half(K: int, p: int) -> int:
+    """1D band pairs with J >= I (one triangle and the diagonal)."""
+    N = K + p
+    return (p + 1) * N - p * (p + 1) // 2
+
+
+def symmetric_assembled_macs(op: str, K: int, p: int, q: int) -> int:
+    """The symmetric kernel (csrc/iga_gsf_p3s.cu) computes only the values with J0 >= I0:
+    stage A the element-local pairs with s >= r ((p+1)(p+2)/2 of (p+1)^2), stages B and S the
+    X / Y rows of the nnz1_half axis-0 band pairs; the other values are mirrored copies (no
+    arithmetic)."""
+    m2 = (p + 1) ** 2
+    t, th = nnz1(K, p), nnz1_half(K, p)
+    types, pb, ps = (1, 1, 1) if op == "mass" else (2, 3, 2)
+    a = types * K**3 * ((p + 1) * (p + 2) // 2) * q**3
+    b = pb * th * K**2 * m2 * q**2
+    s = ps * th * t * K * m2 * q
+    return a + b + s
+
+
+def symmetric_assembled_flops(op: str, K: int, p: int, q: int) -> int:
+    return 2 * symmetric_assembled_macs(op, K, p, q)
 
 
 def separable_flops(op: str, K: int, p: int, q: int) -> int:
