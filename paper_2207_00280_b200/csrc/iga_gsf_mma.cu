@@ -57,14 +57,15 @@ __device__ __forceinline__ int qw_row(int g, int d) {
 // in [0, P] (PB the same with (ib, d1), (lb, k1)).  A DMMA k-step whose 8 x 4 fragment block is
 // zero on every tile is skipped; the nonzero k-steps of each 8-row tile form one contiguous
 // range [lo, hi) (C4, p = 4, TA = 1 / TB = 4: stage A 9 of 14 blocks, stage B 33 of 50).
-template <int P, int Q, int T>
+// (NBX, D0X: the symmetric kernel keeps only the rows d = D0X .. D0X + NBX - 1 of each i)
+template <int P, int Q, int T, int NBX = 2 * P + 1, int D0X = 0>
 struct Band {
-  static constexpr int NB = 2 * P + 1, KK = (T + P) * Q, ROWS = T * NB;
+  static constexpr int NB = 2 * P + 1, KK = (T + P) * Q, ROWS = T * NBX;
   static constexpr int MT = cdiv(ROWS, 8), KS = cdiv(KK, 4);
   static constexpr bool nz(int mt, int ks) {
     for (int a = mt * 8; a < mt * 8 + 8 && a < ROWS; ++a)
       for (int kk = ks * 4; kk < ks * 4 + 4 && kk < KK; ++kk) {
-        const int i = a / NB, d = a % NB, l = kk / Q, r = i + P - l, s = i + d - l;
+        const int i = a / NBX, d = D0X + a % NBX, l = kk / Q, r = i + P - l, s = i + d - l;
         if (r >= 0 && r <= P && s >= 0 && s <= P) return true;
       }
     return false;
@@ -143,10 +144,12 @@ __device__ __forceinline__ void tile_dispatch(int tile, F&& f) {
 
 // ST: stiffness (two operand types, double2 elements) or mass (one type: double elements,
 // half the footprint of X, Y, PA, PB and Z, so p = 2 mass runs four CTAs per SM)
-template <int P, int Q, int TA, int TB, bool ST = true>
+template <int P, int Q, int TA, int TB, bool ST = true, bool SYM = false>
 struct Shape {
   static constexpr int EW = ST ? 2 : 1;
   static constexpr int m = P + 1, NB = 2 * P + 1;
+  // axis-0 band offsets kept: all 2p+1, or (symmetric half) d0 = p .. 2p (J0 >= I0)
+  static constexpr int NBX = SYM ? P + 1 : NB, D0X = SYM ? P : 0;
   static constexpr int LA = TA + P, LB = TB + P;
   static constexpr int KA = LA * Q, KB = LB * Q;  // contraction lengths of stages A, B
   static constexpr int GC = KB * Q;               // stage-A columns (k2, lb, k1), k2 slowest
@@ -154,8 +157,8 @@ struct Shape {
   // doubles; PA / PB rows (16-byte A / B fragments, 8-lane phases) == 4 mod 8 double2
   static constexpr int GCW = pitch_mod(GC, 16, 4);
   static constexpr int KAP = pitch_mod(KA, 8, 4), KBP = pitch_mod(KB, 8, 4);
-  static constexpr int NA0 = TA * NB, NB1 = TB * NB, NC = NA0 * NB1, NR = NA0 * Q;
-  static constexpr int rowVals = NB * NB * NB;
+  static constexpr int NA0 = TA * NBX, NB1 = TB * NB, NC = NA0 * NB1, NR = NA0 * Q;
+  static constexpr int rowVals = NBX * NB * NB;  // values of a rolling row (the kept d0 blocks)
   // Y: mass [NC][Q] doubles; stiffness [NC][YPS] doubles, Y_A at k2 and Y_B at Q + k2, so
   // stage S runs its two products as one K = 2Q contraction (C4: 3 k-steps instead of 2 x 2);
   // YPS == 4 mod 8: the A fragments of a k-step (8 rows x 4 k) hit 16 distinct banks per phase
@@ -169,11 +172,18 @@ struct Shape {
   // rolling-row slot pitch: rowVals + a pad that spreads the stage-S read-modify-writes
   // over the shared-memory banks (picked by simulating the access pattern of the two
   // coefficient-field configs: 37% fewer wavefronts at p = 4, q = 5; 20% at p = 2, q = 3)
-  static constexpr int RP = rowVals + (P == 4 && Q == 5 && TA * TB == 4          ? 1
+  static constexpr int RP = rowVals + (SYM                                      ? 0
+                                       : P == 4 && Q == 5 && TA * TB == 4          ? 1
                                        : P == 2 && Q == 3 && TA == 3 && TB == 3 ? 7
                                                                                 : 0);
   static constexpr int nR = TA * TB * m * RP;
-  static constexpr size_t bytes = sizeof(double) * ((size_t)nWY + nX + nPA + nPB + nZ + nR);
+  // symmetric half: the mirrored combos (d0 > p), per combo a ring of hi runs [m rows][m]
+  // and lo runs [m rows][p] by target row; their mirror metadata; an axis-2 band table
+  static constexpr int NRC = SYM ? TA * P * NB1 : 0, RING = m * NB;
+  static constexpr int NBT = 1024;
+  static constexpr int nRing = NRC * RING, nMM = 2 * NRC, nBT = SYM ? NBT : 0;
+  static constexpr size_t bytes =
+      sizeof(double) * ((size_t)nWY + nX + nPA + nPB + nZ + nR + nRing + nMM + nBT);
 };
 
 // shared-memory element of the operand tables: (V, D) pairs for stiffness, V only for mass
@@ -196,10 +206,11 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
       : "d"(a), "d"(b));
 }
 
-template <int P, int Q, int TA, int TB, bool STIFF>
+template <int P, int Q, int TA, int TB, bool STIFF, bool SYM>
 __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs a) {
   constexpr int NT = nt_of<P>();
-  using S = Shape<P, Q, TA, TB, STIFF>;
+  using S = Shape<P, Q, TA, TB, STIFF, SYM>;
+  constexpr int NBX = S::NBX, D0X = S::D0X;
   using E = typename Elem<STIFF>::T;
   constexpr int m = S::m, NB = S::NB, KA = S::KA, KB = S::KB, GC = S::GC;
   constexpr int GCW = S::GCW, KAP = S::KAP, KBP = S::KBP;
@@ -212,6 +223,9 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
   E* PB2 = PA2 + NA0 * KAP;                                  // [NB1][KBP] (VV, DD)
   E* Z2 = PB2 + NB1 * KBP;                                   // [Q][m*m] (VV, DD(+VV))
   double* R = reinterpret_cast<double*>(Z2 + m * m * Q);     // [TA*TB][m][RP]
+  double* RG = R + S::nR;                                    // [NRC][RING] mirror rings
+  double* MM = RG + S::nRing;                                // [NRC] {int64 base, int2 {c01, b01}}
+  int2* BT = reinterpret_cast<int2*>(MM + S::nMM);           // [NBT] {band_prefix, band_cnt}
   __shared__ int64_t rowoff[TA * TB];
   __shared__ int comboR[NC];  // R offset of combo (a0, b1): pencil block + (d0, d1) row
 
@@ -231,7 +245,7 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
   // ---- constant pair tables (axis 0 slab-restricted, axis 1)
   for (int u = tid; u < NA0 * KA; u += NT) {
     const int a0 = u / KA, kk = u % KA, la = kk / Q, k0 = kk % Q;
-    const int I0 = i00 + a0 / NB, J0 = I0 - P + a0 % NB, e0 = i00 - P + la;
+    const int I0 = i00 + a0 / NBX, J0 = I0 - P + D0X + a0 % NBX, e0 = i00 - P + la;
     const int r = I0 - e0, sc = J0 - e0;
     double2 v = make_double2(0.0, 0.0);
     if (e0 >= e0lo && e0 < e0hi && r >= 0 && r <= P && sc >= 0 && sc <= P && J0 >= 0 && J0 < N) {
@@ -254,8 +268,29 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
   for (int u = tid; u < S::nR; u += NT) R[u] = 0.0;
   for (int c = tid; c < NC; c += NT) {
     const int a0 = c / NB1, b1 = c % NB1;
-    const int ia = a0 / NB, d0 = a0 % NB, ib = b1 / NB, d1 = b1 % NB;
-    comboR[c] = (ia * TB + ib) * m * S::RP + (d0 * NB + d1) * NB;
+    const int ia = a0 / NBX, dx = a0 % NBX, ib = b1 / NB, d1 = b1 % NB;
+    comboR[c] = (ia * TB + ib) * m * S::RP + (dx * NB + d1) * NB;
+  }
+  if constexpr (SYM) {
+    // mirror metadata of combo c = ((ia p + dx - 1) TB + ib) NB + d1 (d0 = p + dx > p): the
+    // value at (I, J) also belongs at (J, I), J = (I0 + dx, I1 + d1 - p, .), whose row holds
+    // it at block (p - dx, 2p - d1); b01 -1: no mirror
+    for (int c = tid; c < S::NRC; c += NT) {
+      const int d1 = c % NB, ib = (c / NB) % TB, dx = 1 + (c / (NB * TB)) % P, ia = c / (NB * TB * P);
+      const int I0 = i00 + ia, I1 = i10 + ib, J0 = I0 + dx, J1 = I1 - P + d1;
+      int64_t base = 0;
+      int c01 = 0, b01 = -1;
+      if (I0 < a.plane_end && I1 < N && J0 < N && J1 >= 0 && J1 < N) {
+        const int jc1 = (int)band_cnt(J1, P, N);
+        base = rowptr3(J0, J1, 0, P, N) - a.base;
+        c01 = (int)band_cnt(J0, P, N) * jc1;
+        b01 = (P - dx - max(0, P - J0)) * jc1 + (2 * P - d1 - max(0, P - J1));
+      }
+      *reinterpret_cast<int64_t*>(MM + 2 * c) = base;
+      *reinterpret_cast<int2*>(MM + 2 * c + 1) = make_int2(c01, b01);
+    }
+    if (N <= S::NBT)
+      for (int I = tid; I < N; I += NT) BT[I] = make_int2((int)band_prefix(I, P, N), (int)band_cnt(I, P, N));
   }
 
   // W units: one (kk, (lb, k1)) row segment of Q contiguous k2 columns per unit (the Q
@@ -347,9 +382,9 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
   // v and its (d0, d1, d2) for the whole flush and walks the pencils; otherwise the flat
   // (rc, v) loop below.  Both write the same values to the same addresses.
   constexpr int VT = cdiv(S::rowVals, 32) * 32, RCS = NT / VT;
-  constexpr bool by_v = RCS >= 1 && RCS * VT == NT;
+  constexpr bool by_v = !SYM && RCS >= 1 && RCS * VT == NT;
   constexpr int VPT = cdiv(S::rowVals, NT);
-  int vd[VPT];  // (d0, d1, d2) of this thread's band positions, packed
+  int vd[VPT];  // (d0 - D0X, d1, d2) of this thread's band positions, packed
 #pragma unroll
   for (int j = 0; j < VPT; ++j) {
     const int v = tid + j * NT;
@@ -392,24 +427,57 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
     for (int j = 0; j < VPT; ++j) {
       const int v = tid + j * NT;
       if (v >= S::rowVals) break;
-      const int d2 = vd[j] & 255, d1 = (vd[j] >> 8) & 255, d0 = vd[j] >> 16;
+      const int d2 = vd[j] & 255, d1 = (vd[j] >> 8) & 255, dx = vd[j] >> 16, d0 = D0X + dx;
       const bool in2 = d2 >= lod2 && d2 < lod2 + c2;
+      // symmetric half: target row J2 of this value's mirror and its ring entry
+      const int J2 = I2 + d2 - P, d2p = 2 * P - d2;
+      const int rg_off = J2 % m * (d2p <= P ? m : P) + (d2p <= P ? d2p : m * m + d2p - m);
 #pragma unroll
       for (int rc = 0; rc < TA * TB; ++rc) {
         double* Rv = R + (rc * m + slot) * S::RP + v;
+        const double val = *Rv;
         const int64_t off = rowoff[rc];
         if (off >= 0) {
           const int mt = rowmeta[rc];
           if (mt == 0) {
-            a.values[off + v] = *Rv;  // full band: CSR order is the R order
+            a.values[off + D0X * NB * NB + v] = val;  // full band: CSR order is the R order
           } else {
             const int lod0 = (mt >> 1) & 31, lod1 = (mt >> 6) & 31, c0 = (mt >> 11) & 31,
                       c1 = (mt >> 16) & 31;
             if (in2 && d0 >= lod0 && d0 < lod0 + c0 && d1 >= lod1 && d1 < lod1 + c1)
-              a.values[off + ((d0 - lod0) * c1 + (d1 - lod1)) * c2 + (d2 - lod2)] = *Rv;
+              a.values[off + ((d0 - lod0) * c1 + (d1 - lod1)) * c2 + (d2 - lod2)] = val;
+          }
+        }
+        if constexpr (SYM) {
+          if (dx > 0 && J2 >= 0 && J2 < N) {
+            const int c = (((rc / TB) * P + dx - 1) * TB + rc % TB) * NB + d1;
+            RG[c * S::RING + rg_off] = val;
           }
         }
         *Rv = 0.0;
+      }
+    }
+  };
+  // Symmetric half: target row J2's complete mirror runs, hi (d2' = 0..p, complete once its
+  // source row J2 is flushed) or lo (d2' = p+1..2p, once J2 + p is), one thread per (combo,
+  // entry): consecutive threads write consecutive values of a run.  Only entries whose source
+  // row this CTA writes (its segment) leave here.
+  auto emit = [&](int J2, bool hi) {
+    if constexpr (SYM) {
+      if (J2 < 0 || J2 >= N) return;
+      const int2 bq = N <= S::NBT ? BT[J2] : make_int2((int)band_prefix(J2, P, N), (int)band_cnt(J2, P, N));
+      const int lod2 = max(0, P - J2), slot = J2 % m, ne = hi ? m : P;
+      const int s1w = s1 == K ? (int)N : s1;
+      for (int u = tid; u < S::NRC * ne; u += NT) {
+        const int c = u / ne, e = u - c * ne, d2p = hi ? e : m + e;
+        const int I2s = J2 - P + d2p;  // source row of the entry
+        const int off = d2p - lod2;
+        if (I2s < s0 || I2s >= s1w || off < 0 || off >= bq.y) continue;
+        const int2 cb = *reinterpret_cast<const int2*>(MM + 2 * c + 1);
+        if (cb.y < 0) continue;
+        const int64_t base = *reinterpret_cast<const int64_t*>(MM + 2 * c);
+        a.values[base + (int64_t)cb.x * bq.x + (int64_t)cb.y * bq.y + off] =
+            RG[c * S::RING + (hi ? slot * m + e : m * m + slot * P + e)];
       }
     }
   };
@@ -457,7 +525,7 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
     if (e2 < 0)
 #endif
     {
-      using BA = Band<P, Q, TA>;
+      using BA = Band<P, Q, TA, NBX, D0X>;
       constexpr int MT = cdiv(NA0, 8), NTL = cdiv(GC, 8), KS = cdiv(KA, 4);
       static_assert(BA::MT == MT && BA::KS == KS, "stage-A band shape");
       const WarpTile wt = warp_tile<MT, BA, NWARP, NTL>(warp);
@@ -490,6 +558,12 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
     }
     __syncthreads();
 
+    if constexpr (SYM) {
+      if (pending >= 0) {  // the row flushed in this column's stage-A phase
+        emit(pending, true);
+        emit(pending - P, false);
+      }
+    }
     // ---- stage B: rows (a0, k2), columns b1; warp w keeps the PB fragments of n-tile
     // w % NTL in registers:  mass YA = XV VV;  stiffness YA = XV DD + XD VV, YB = XV VV
 #ifdef GSF_ABL_B
@@ -648,6 +722,18 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
       set_rowoff(I2);
       __syncthreads();
       flush_row(I2);
+      if constexpr (SYM) {
+        __syncthreads();
+        emit(I2, true);
+        emit(I2 - P, false);
+      }
+    }
+    if constexpr (SYM) {
+      // runs this CTA's last rows feed but never completed here: the lo runs of the last p
+      // target rows and, before the next segment, the hi runs of the p rows after it (the
+      // entries of other segments' source rows are theirs)
+      for (int J2 = last + 1 - P; J2 <= last; ++J2) emit(J2, false);
+      for (int J2 = last + 1; J2 <= last + P; ++J2) emit(J2, true);
     }
   }
 }
@@ -672,10 +758,12 @@ struct Tile {
                             : Shape<P, Q, 2, 2, ST>::bytes <= cap ? 2 : 1;
 };
 
-template <int P, int Q, bool ST, int TA = Tile<P, Q, ST>::TA, int TB = Tile<P, Q, ST>::TB>
+template <int P, int Q, bool ST, bool SYM = false, int TA = Tile<P, Q, ST>::TA, int TB = Tile<P, Q, ST>::TB>
 static int launch_t(const GsfArgs& a0, cudaStream_t s) {
-  using Sh = Shape<P, Q, TA, TB, ST>;
-  if constexpr (Sh::bytes > 227 * 1024) {
+  using Sh = Shape<P, Q, TA, TB, ST, SYM>;
+  if constexpr (SYM && Sh::bytes > 227 * 1024) {
+    return launch_t<P, Q, ST, false>(a0, s);  // the symmetric half's rings do not fit
+  } else if constexpr (Sh::bytes > 227 * 1024) {
     set_error("assembled sum factorization: p=%d q=%d needs %zu B shared memory", P, Q, Sh::bytes);
     return IGA_EUNSUPPORTED;
   } else {
@@ -686,7 +774,7 @@ static int launch_t(const GsfArgs& a0, cudaStream_t s) {
     const int tiles0 = (planes + TA - 1) / TA;
     a.tiles1 = (int)((N + TB - 1) / TB);
     const int64_t tiles = (int64_t)tiles0 * a.tiles1;
-    const void* fn = reinterpret_cast<const void*>(k_gsf3_mma<P, Q, TA, TB, ST>);
+    const void* fn = reinterpret_cast<const void*>(k_gsf3_mma<P, Q, TA, TB, ST, SYM>);
     cudaError_t e = smem_attr_once(fn, Sh::bytes, true);
     if (e != cudaSuccess) return check_cuda(e, "gsf mma smem attr");
     constexpr int NT = nt_of<P>();
@@ -707,16 +795,25 @@ static int launch_t(const GsfArgs& a0, cudaStream_t s) {
     }
     a.segs = best;
     a.seg_len = (a.K + best - 1) / best;
-    k_gsf3_mma<P, Q, TA, TB, ST><<<(unsigned)(tiles * best), NT, Sh::bytes, s>>>(a);
+    k_gsf3_mma<P, Q, TA, TB, ST, SYM><<<(unsigned)(tiles * best), NT, Sh::bytes, s>>>(a);
     return check_cuda(cudaGetLastError(), "gsf mma launch");
   }
 }
 
+// Symmetric half (SYM): only the J0 >= I0 values are computed and the rest mirrored, so the
+// launch must cover every row of the mesh; IGA_GSF_SYM=0 selects the full computation (A/B).
 template <int P, int Q>
 struct Launch {
   static int run(const GsfArgs& a, cudaStream_t s) {
-    if (a.op == IGA_OP_MASS) return launch_t<P, Q, false>(a, s);
-    if constexpr (P >= 1) return launch_t<P, Q, true>(a, s);
+    static const bool no_sym = [] {
+      const char* e = getenv("IGA_GSF_SYM");
+      return e != nullptr && e[0] == '0' && e[1] == 0;
+    }();
+    const bool whole = a.plane_begin == 0 && a.plane_end == a.K + P && a.el_begin <= 0 && a.el_end >= a.K &&
+                       a.base == 0 && a.K + P <= Shape<P, Q, 1, 1, true, true>::NBT;
+    const bool sym = whole && !no_sym && P >= 1;
+    if (a.op == IGA_OP_MASS) return sym ? launch_t<P, Q, false, true>(a, s) : launch_t<P, Q, false>(a, s);
+    if constexpr (P >= 1) return sym ? launch_t<P, Q, true, true>(a, s) : launch_t<P, Q, true>(a, s);
     set_error("derivatives require degree >= 1");
     return IGA_EINVAL;
   }

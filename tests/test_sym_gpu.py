@@ -1,8 +1,11 @@
-"""GPU parity of the symmetric p = 3 kernel (csrc/iga_gsf_p3s.cu: computes S[I, J] for
-J0 >= I0 and mirrors the rest through per-warp rings) against the oracle's classical
-integration (reference integrators.py:77-109 + assembly.py:80-82), forced on and off
-(IGA_GSF_SYM=0 selects k_gsf3_p3; the variable is read once per process, hence the
-subprocess), on meshes small enough to exercise the rings' first and last target rows."""
+"""GPU parity of the symmetric-half kernels -- k_gsf3_p3s (csrc/iga_gsf_p3s.cu, p = 3, q = 4)
+and the SYM mode of the generic DMMA kernel (csrc/iga_gsf_mma.cu, other degrees): both
+compute S[I, J] for J0 >= I0 and mirror the rest through rings -- against the oracle's
+classical integration (reference integrators.py:77-109 + assembly.py:80-82), forced on and
+off (IGA_GSF_SYM=0; read once per process, hence the subprocesses), on meshes small enough to
+exercise the rings' first and last target rows, and with the generic kernel's element
+columns forced into 3 segments (IGA_GSF_SEGS=3: every segment emits the runs its rows feed
+across its boundaries)."""
 import json
 import os
 import subprocess
@@ -18,16 +21,20 @@ if ROOT not in sys.path:
 from oracle import oracle as O  # noqa: E402
 from tests.parity import compare  # noqa: E402
 
-# (K, operator, coefficient kind)
-CASES = [(1, "stiffness", "scalar"), (2, "mass", "field"), (3, "stiffness_mass", "field"),
-         (4, "stiffness", "field"), (5, "mass", "scalar"), (6, "stiffness", "scalar"),
-         (7, "stiffness_mass", "scalar"), (9, "stiffness", "field")]
+# (K, p, q, operator, coefficient kind): p = 3 q = 4 -> k_gsf3_p3s, the rest the generic kernel
+# (p = 2 stiffness: the tile kernel serves p = 2 mass and p = 1)
+CASES = [(1, 3, 4, "stiffness", "scalar"), (2, 3, 4, "mass", "field"), (3, 3, 4, "stiffness_mass", "field"),
+         (4, 3, 4, "stiffness", "field"), (5, 3, 4, "mass", "scalar"), (6, 3, 4, "stiffness", "scalar"),
+         (7, 3, 4, "stiffness_mass", "scalar"), (9, 3, 4, "stiffness", "field"),
+         (5, 2, 3, "stiffness", "field"), (8, 2, 3, "stiffness_mass", "scalar"), (7, 2, 4, "stiffness", "scalar"),
+         (3, 4, 5, "stiffness_mass", "field"), (7, 4, 5, "stiffness", "scalar"), (6, 5, 6, "mass", "field"),
+         (4, 3, 5, "stiffness", "field")]
 
 
-def _coef(K, kind, seed):
+def _coef(K, q, kind, seed):
     if kind == "scalar":
         return None
-    return np.random.default_rng(seed).uniform(0.5, 1.5, size=(K**3, 64))
+    return np.random.default_rng(seed).uniform(0.5, 1.5, size=(K**3, q**3))
 
 
 def _run_cases():
@@ -36,27 +43,29 @@ def _run_cases():
     ones: exactly 0 when the mirror lands where it should)."""
     import paper_2207_00280_b200 as pkg
 
-    for i, (K, op, kind) in enumerate(CASES):
-        coef = _coef(K, kind, 200 + i)
-        ip, ix, ref = O.integrate_assemble(3, K, 3, op, "classical", q=4, coef=coef)
-        _, _, A = O.integrate_assemble(3, K, 3, op, "classical", q=4, coef=coef, absolute=True)
-        res = pkg.run_integration(pkg.RunConfig("sumfact", "device", K, 3, operator=op, coefficient=coef,
-                                                assembly="owner"))
+    for i, (K, p, q, op, kind) in enumerate(CASES):
+        coef = _coef(K, q, kind, 200 + i)
+        ip, ix, ref = O.integrate_assemble(3, K, p, op, "classical", q=q, coef=coef)
+        _, _, A = O.integrate_assemble(3, K, p, op, "classical", q=q, coef=coef, absolute=True)
+        res = pkg.run_integration(pkg.RunConfig("sumfact", "device", K, p, quad_points=q, operator=op,
+                                                coefficient=coef, assembly="owner"))
         v = res.gram.values.cpu().numpy()
         st = compare(v, ref, ip, absref=A)
         import scipy.sparse as sp
 
-        N = K + 3
+        N = K + p
         M = sp.csr_matrix((v, ix, ip), shape=(len(ip) - 1, len(ip) - 1))
         D = (M - M.T).tocoo()
         i0, j0 = D.row // (N * N), D.col // (N * N)
         asym = float(np.max(np.abs(D.data[i0 != j0]), initial=0.0))
-        print(json.dumps({"case": [K, op, kind], "ok": bool(st["ok"]), "max_rel": float(st["max_rel"]),
+        print(json.dumps({"case": [K, p, q, op, kind], "ok": bool(st["ok"]), "max_rel": float(st["max_rel"]),
                           "asym_mirrored": asym}), flush=True)
 
 
-def _child(sym):
+def _child(sym, segs=None):
     env = dict(os.environ, IGA_GSF_SYM=sym)
+    if segs is not None:
+        env["IGA_GSF_SEGS"] = str(segs)
     out = subprocess.run([sys.executable, os.path.abspath(__file__), "--case"], env=env, cwd=ROOT,
                          capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
@@ -64,8 +73,9 @@ def _child(sym):
 
 
 @pytest.mark.gpu
-def test_symmetric_kernel_vs_oracle_and_exact_mirror():
-    rows = _child("1")
+@pytest.mark.parametrize("segs", [None, 3])
+def test_symmetric_kernel_vs_oracle_and_exact_mirror(segs):
+    rows = _child("1", segs)
     assert len(rows) == len(CASES)
     bad = [r for r in rows if not r["ok"]]
     assert not bad, bad
