@@ -233,8 +233,12 @@ def kernel_roofline(code, wl, K, p, q, k_el, by, kern_ms, peaks):
 
     own = None
     # the dispatch of csrc/iga_gsf.cu: whole-mesh p = 3, q = 4 runs take the symmetric kernel
-    sym = (code == 2 and wl["dim"] == 3 and p == 3 and q == 4 and k_el == K**wl["dim"]
-           and os.environ.get("IGA_GSF_SYM") != "0" and os.environ.get("IGA_GSF_GENERIC") != "1")
+    # (symmetric half: k_gsf3_p3s for p = 3, q = 4, the generic kernel's SYM mode otherwise;
+    # the low-degree tile kernel computes everything)
+    tile_env = os.environ.get("IGA_GSF_TILE")
+    tile = wl["dim"] == 3 and (tile_env == "1" or (tile_env != "0" and (p == 1 or (p == 2 and wl["op"] == "mass"))))
+    sym = (code == 2 and wl["dim"] == 3 and k_el == K**wl["dim"] and not tile and p >= 1
+           and os.environ.get("IGA_GSF_SYM") != "0")
     if code == 3:
         fl = perfmodel.separable_flops(wl["op"], K, p, q) * k_el / K**3
     elif code in (1, 2) and wl["dim"] == 3:
@@ -264,8 +268,6 @@ def kernel_roofline(code, wl, K, p, q, k_el, by, kern_ms, peaks):
     name = KERNEL_NAMES[code]
     if code == 0 and wl["dim"] == 2:
         name = f"k_classical_scatter<2,{p},{q}> (Algorithm 1, scalar FP64 + fused CSR scatter)"
-    tile_env = os.environ.get("IGA_GSF_TILE")
-    tile = wl["dim"] == 3 and (tile_env == "1" or (tile_env != "0" and (p == 1 or (p == 2 and wl["op"] == "mass"))))
     if code == 2 and p in (1, 2) and tile:
         # the dispatch of csrc/iga_gsf.cu (tile_wins): non-streaming tile kernel
         name = (f"k_tile3<{p},{q}> (assembled sum factorization per 3D row tile: TMA coefficient "
@@ -273,7 +275,8 @@ def kernel_roofline(code, wl, K, p, q, k_el, by, kern_ms, peaks):
     elif code == 2 and not (p == 3 and q == 4):
         name = (f"k_gsf3<{p},{q}> (assembled sum factorization, scalar FP64 + CSR write)"
                 if os.environ.get("IGA_GSF_SCALAR") == "1" else
-                f"k_gsf3_mma<{p},{q}> (assembled sum factorization, DMMA GEMMs + CSR write)")
+                f"k_gsf3_mma<{p},{q}>{' symmetric half' if sym else ''} (assembled sum factorization, "
+                f"DMMA GEMMs + CSR write{'; J0 >= I0 computed, the rest mirrored through rings' if sym else ''})")
     elif code == 2 and sym:
         name = ("k_gsf3_p3s (symmetric assembled sum factorization on DMMA: J0 >= I0 computed, "
                 "the rest mirrored through per-warp rings; general per-quadrature-point "
