@@ -237,7 +237,7 @@ def kernel_roofline(code, wl, K, p, q, k_el, by, kern_ms, peaks):
     # the low-degree tile kernel computes everything)
     tile_env = os.environ.get("IGA_GSF_TILE")
     tile = wl["dim"] == 3 and (tile_env == "1" or (tile_env != "0" and (p == 1 or (p == 2 and wl["op"] == "mass"))))
-    sym = (code == 2 and wl["dim"] == 3 and k_el == K**wl["dim"] and not tile and p >= 1
+    sym = (code == 2 and wl["dim"] == 3 and k_el == K**wl["dim"] and not tile and p >= 3
            and os.environ.get("IGA_GSF_SYM") != "0")
     if code == 3:
         fl = perfmodel.separable_flops(wl["op"], K, p, q) * k_el / K**3

@@ -800,8 +800,8 @@ static int launch_t(const GsfArgs& a0, cudaStream_t s) {
   }
 }
 
-// Symmetric half (SYM): only the J0 >= I0 values are computed and the rest mirrored, so the
-// launch must cover every row of the mesh; IGA_GSF_SYM=0 selects the full computation (A/B).
+// Symmetric half (SYM, p >= 3): only the J0 >= I0 values are computed and the rest mirrored, so
+// the launch must cover every row of the mesh; IGA_GSF_SYM=0 selects the full computation (A/B).
 template <int P, int Q>
 struct Launch {
   static int run(const GsfArgs& a, cudaStream_t s) {
@@ -811,7 +811,10 @@ struct Launch {
     }();
     const bool whole = a.plane_begin == 0 && a.plane_end == a.K + P && a.el_begin <= 0 && a.el_end >= a.K &&
                        a.base == 0 && a.K + P <= Shape<P, Q, 1, 1, true, true>::NBT;
-    const bool sym = whole && !no_sym && P >= 1;
+    // p <= 2: the ring and run-emission work outweighs the halved stages B and S
+    // (tools/tile_shapes.py, IGA_GSF_TILE=0: 64^3 p = 2 stiffness 0.430 vs 0.422 ms, p = 1 mass
+    // 0.197 vs 0.123); C4 (p = 4): 10.19 vs 11.71 ms
+    const bool sym = whole && !no_sym && P >= 3;
     if (a.op == IGA_OP_MASS) return sym ? launch_t<P, Q, false, true>(a, s) : launch_t<P, Q, false>(a, s);
     if constexpr (P >= 1) return sym ? launch_t<P, Q, true, true>(a, s) : launch_t<P, Q, true>(a, s);
     set_error("derivatives require degree >= 1");

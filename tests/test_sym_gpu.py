@@ -21,8 +21,8 @@ if ROOT not in sys.path:
 from oracle import oracle as O  # noqa: E402
 from tests.parity import compare  # noqa: E402
 
-# (K, p, q, operator, coefficient kind): p = 3 q = 4 -> k_gsf3_p3s, the rest the generic kernel
-# (p = 2 stiffness: the tile kernel serves p = 2 mass and p = 1)
+# (K, p, q, operator, coefficient kind): p = 3 q = 4 -> k_gsf3_p3s, p >= 3 otherwise the generic
+# kernel's symmetric mode; p = 2 stiffness runs the generic kernel in full (also checked)
 CASES = [(1, 3, 4, "stiffness", "scalar"), (2, 3, 4, "mass", "field"), (3, 3, 4, "stiffness_mass", "field"),
          (4, 3, 4, "stiffness", "field"), (5, 3, 4, "mass", "scalar"), (6, 3, 4, "stiffness", "scalar"),
          (7, 3, 4, "stiffness_mass", "scalar"), (9, 3, 4, "stiffness", "field"),
