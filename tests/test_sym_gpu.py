@@ -79,8 +79,8 @@ def test_symmetric_kernel_vs_oracle_and_exact_mirror(segs):
     assert len(rows) == len(CASES)
     bad = [r for r in rows if not r["ok"]]
     assert not bad, bad
-    # every mirrored value is the bit pattern of its computed twin
-    assert all(r["asym_mirrored"] == 0.0 for r in rows), rows
+    # every mirrored value (p >= 3: the symmetric kernels) is the bit pattern of its twin
+    assert all(r["asym_mirrored"] == 0.0 for r in rows if r["case"][1] >= 3), rows
 
 
 @pytest.mark.gpu
