@@ -2,7 +2,7 @@
 # reference arm, C4, C2, p9), ncu launch lists and full captures of the kernels they
 # time, GPU suite and smoke.  Run under gpurun (one GPU); summarise with
 # tools/profile_summary.py into profiles/.
-TAG=${TAG:-r02r}
+TAG=${TAG:-r02s}
 O=gpurun_out
 set -x
 python bench.py > $O/${TAG}_bench.json 2> $O/${TAG}_bench.err
@@ -10,6 +10,7 @@ python bench.py --impl reference --steps 3 --warmup 3 > $O/${TAG}_ref.json 2> $O
 python bench.py --workload c4 --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > $O/${TAG}_bench_c4.json 2>&1
 python bench.py --workload c2 --steps 20 --warmup 3 --no-cpu-baseline --no-e2e > $O/${TAG}_bench_c2.json 2>&1
 python bench.py --workload p9 --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > $O/${TAG}_bench_p9.json 2>&1
+python bench.py --workload c5 --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > $O/${TAG}_bench_c5.json 2>&1
 NCUL="ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv"
 NCUF="ncu --set full --clock-control none --import-source on --launch-skip 3 -c 1 -f"
 B="python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e"
