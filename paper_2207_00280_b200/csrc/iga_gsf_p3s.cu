@@ -49,9 +49,6 @@ constexpr int MT_S = NCOMBO / 8;         // 49 m-tiles of combos
 #ifndef P3S_NWA
 #define P3S_NWA 4
 #endif
-#ifndef P3S_RING
-#define P3S_RING 1
-#endif
 constexpr int NWA = P3S_NWA, NWB = P3S_NWB, NWS = P3S_NWS;  // warps per role (NWA even: fixed type per A warp)
 static_assert(NWA % 2 == 0, "stage-A warps come in (value, derivative) pairs");
 constexpr int NT = 32 * (NWA + NWB + NWS);  // threads (16 warps by default)
@@ -84,7 +81,7 @@ constexpr int OFF_BT = OFF_MM + NWS * MT_S_PER_WARP * 2 * 32;  // int2 [NBT]
 // [4 rows][d2' 0..3], lo runs [4 rows][d2' 4..6] -- so they leave as contiguous runs
 constexpr int RING = 28;
 constexpr int OFF_RING = OFF_BT + NBT;                 // [NWS][MT_S_PER_WARP][8][RING]
-constexpr int OFF_MB = OFF_RING + (P3S_RING ? NWS * MT_S_PER_WARP * 8 * RING : 0);  // mbarriers
+constexpr int OFF_MB = OFF_RING + NWS * MT_S_PER_WARP * 8 * RING;  // mbarriers
 constexpr int SMEM_DOUBLES = OFF_MB + 8;
 static_assert(SMEM_DOUBLES * 8 <= 227 * 1024, "shared memory budget");
 constexpr size_t SMEM_BYTES = SMEM_DOUBLES * sizeof(double);
@@ -318,52 +315,6 @@ __device__ __forceinline__ void store_pair(const GsfArgs& a, int m, const int64_
   }
 }
 
-// Mirror targets of row I2's values for this lane: the hi value (J2 = I2 + t) goes to row
-// J2 of the target pencil at axis-2 offset 3 - t, the lo value (J2 = I2 + t - 4) at 7 - t
-// (offsets relative to the target row's band start; -1: the value does not exist)
-struct MirDst {
-  int64_t preh, prel;
-  int c2h, c2l, oh, ol;
-};
-
-__device__ __forceinline__ MirDst mir_dst(int t, int I2, int64_t N, const RowDst& rd, const int2* bt) {
-  MirDst m;
-  m.preh = m.prel = 0;
-  m.c2h = m.c2l = 0;
-  m.oh = m.ol = -1;
-  if (rd.dh >= 0) {
-    const int J2 = I2 + t;
-    const int2 b = band_of(bt, J2, N);
-    m.preh = b.x;
-    m.c2h = b.y;
-    m.oh = (P - t) - max(0, P - J2);
-  }
-  if (rd.dl >= 0) {
-    const int J2 = I2 + t - 4;
-    const int2 b = band_of(bt, J2, N);
-    m.prel = b.x;
-    m.c2l = b.y;
-    m.ol = (P + 4 - t) - max(0, P - J2);
-  }
-  return m;
-}
-
-// mm: this lane's mirror metadata of one m-tile (smem: int64 pencil base, then {c0 c1,
-// (d0, d1) block offset of the target row} as an int pair in the next 32-lane slot)
-__device__ __forceinline__ void store_mirror(const GsfArgs& a, const double* mm, const MirDst& md, double hi,
-                                             double lo) {
-  const int2 cb = *reinterpret_cast<const int2*>(mm + 32);
-#ifdef P3S_ABL_NOMIRROR  // timing ablation only (wrong values)
-  if (cb.y >= 0 && hi == 1.2345e-300) {
-#else
-  if (cb.y >= 0) {
-#endif
-    const int64_t base = *reinterpret_cast<const int64_t*>(mm);
-    if (md.oh >= 0) a.values[base + (int64_t)cb.x * md.preh + cb.y * md.c2h + md.oh] = hi;
-    if (md.ol >= 0) a.values[base + (int64_t)cb.x * md.prel + cb.y * md.c2l + md.ol] = lo;
-  }
-}
-
 // Row I2's mirrored values into this lane group's rings: hi -> target J2 = I2 + t at d2' = 3 - t,
 // lo -> J2 = I2 + t - 4 at d2' = 7 - t (ring entry d2' - 4); slot = J2 mod 4
 __device__ __forceinline__ void ring_put(double* rg, int i, int g, int t, int I2, double hi, double lo) {
@@ -401,13 +352,13 @@ __device__ __forceinline__ void stage_s_batch(const Lane& L, int ws, const doubl
                                               const double (&b0)[2], const double (&b1)[2],
                                               const int (&meta)[MT_S_PER_WARP], const int64_t* pb,
                                               const int* pc, const GsfArgs& a, const RowDst& rd,
-                                              const double* mm, const MirDst& md, double* rg, int e2) {
+                                              double* rg, int e2) {
   const int g = L.g, t = L.t;
   double a0[NM], a1[NM], cc[NM][2][2], lo[NM];
   int p[NM][2][2];
   if (MT_S % NWS != 0 && ws + (I0 + NM - 1) * NWS >= MT_S) {
     // uneven split: the last m-tile of this batch does not exist for this warp
-    if constexpr (NM > 1) stage_s_batch<PHI, I0, NM - 1>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd, mm, md, rg, e2);
+    if constexpr (NM > 1) stage_s_batch<PHI, I0, NM - 1>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd, rg, e2);
     return;
   }
 #pragma unroll
@@ -442,11 +393,7 @@ __device__ __forceinline__ void stage_s_batch(const Lane& L, int ws, const doubl
 #pragma unroll
     for (int k = 1; k < 4; ++k) Rs[p[i][k >> 1][k & 1]] = cc[i][k >> 1][k & 1];
     store_pair(a, meta[I0 + i], pb, pc, rd, cc[i][0][0], lo[i]);
-#if P3S_RING
     ring_put(rg, I0 + i, g, t, e2, cc[i][0][0], lo[i]);
-#else
-    store_mirror(a, mm + (I0 + i) * 64, md, cc[i][0][0], lo[i]);
-#endif
   }
 }
 
@@ -514,22 +461,19 @@ __device__ __forceinline__ void stage_s(const Lane& L, int ws, const double* Y, 
   const int t = L.t;
   const int2* bt = reinterpret_cast<const int2*>(Rs - OFF_R + OFF_BT);  // Rs = sm + OFF_R
   const RowDst rd = row_dst(t, e2, N, bt);
-  const MirDst md = mir_dst(t, e2, N, rd, bt);
   // batches of at most 4 m-tiles (loads of a batch issued before its DMMAs)
   constexpr int B0 = MT_S_PER_WARP <= 4 ? MT_S_PER_WARP : (MT_S_PER_WARP <= 8 ? (MT_S_PER_WARP + 1) / 2 : 4);
   constexpr int R1 = MT_S_PER_WARP - B0;
   constexpr int B1 = R1 <= 4 ? R1 : (R1 + 1) / 2;
   constexpr int B2 = R1 - B1;
   static_assert(B2 <= 4, "stage S batches");
-  stage_s_batch<PHI, 0, B0>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd, mm, md, rg, e2);
-  if constexpr (B1 > 0) stage_s_batch<PHI, B0, B1>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd, mm, md, rg, e2);
-  if constexpr (B2 > 0) stage_s_batch<PHI, B0 + B1, B2>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd, mm, md, rg, e2);
-#if P3S_RING
+  stage_s_batch<PHI, 0, B0>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd, rg, e2);
+  if constexpr (B1 > 0) stage_s_batch<PHI, B0, B1>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd, rg, e2);
+  if constexpr (B2 > 0) stage_s_batch<PHI, B0 + B1, B2>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd, rg, e2);
   __syncwarp();
   emit_runs(a, rg, mm, ws, L, e2, true, bt, N);
   if (e2 >= 3) emit_runs(a, rg, mm, ws, L, e2 - 3, false, bt, N);
   __syncwarp();
-#endif
 }
 
 // Rows K .. K+P-1 (no element e2 = I2): both groups are complete in their slots.
@@ -539,7 +483,6 @@ __device__ __forceinline__ void flush_tail(const Lane& L, int ws, const double* 
                                            double* rg) {
   const int2* bt = reinterpret_cast<const int2*>(Rs - OFF_R + OFF_BT);  // Rs = sm + OFF_R
   const RowDst rd = row_dst(L.t, I2, N, bt);
-  const MirDst md = mir_dst(L.t, I2, N, rd, bt);
   const int sl = I2 & 3;
 #pragma unroll
   for (int i = 0; i < MT_S_PER_WARP; ++i) {
@@ -547,19 +490,13 @@ __device__ __forceinline__ void flush_tail(const Lane& L, int ws, const double* 
     if (mt < MT_S) {
       const double hi = Rs[rs_idx(mt, sl, 0, L.lane)], lo = Rs[rs_idx(mt, sl, 1, L.lane)];
       store_pair(a, meta[i], pb, pc, rd, hi, lo);
-#if P3S_RING
       ring_put(rg, i, L.g, L.t, I2, hi, lo);
-#else
-      store_mirror(a, mm + i * 64, md, hi, lo);
-#endif
     }
   }
-#if P3S_RING
   __syncwarp();
   emit_runs(a, rg, mm, ws, L, I2, true, bt, N);
   if (I2 >= 3) emit_runs(a, rg, mm, ws, L, I2 - 3, false, bt, N);
   __syncwarp();
-#endif
 }
 
 // W[(la,k0)][(g1,k2)] = c w0 w1 w2 jac on the CTA's quadrature slab of column e2
@@ -762,13 +699,11 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3s(GsfArgs a) {
     }
     // rows K .. K+P-1 received their last contribution from element K-1
     for (int I2 = K; I2 < N; ++I2) flush_tail(L, ws, Rs, I2, meta, pb, pc, a, N, mmw, rgw);
-#if P3S_RING
     {
       // lo runs of the last three target rows (their later sources do not exist)
       const int2* bt = reinterpret_cast<const int2*>(sm + OFF_BT);
       for (int J2 = max(0, (int)N - 3); J2 < N; ++J2) emit_runs(a, rgw, mmw, ws, L, J2, false, bt, N);
     }
-#endif
   }
 }
 
