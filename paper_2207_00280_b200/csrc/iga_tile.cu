@@ -61,8 +61,15 @@ struct Shape {
   static constexpr int nE = ((LA + LB + LC) * (2 * m + 1) * Q + 1) / 2 * 2;  // element records
   // doubles; the int64 row bases and int band info follow
   static constexpr int nD = nR1 + nX + nPA + nPB + nPC + nE;
-  static constexpr size_t bytes = sizeof(double) * nD + sizeof(int64_t) * nRows +
+  static constexpr int ER = (2 * m + 1) * Q;  // doubles of an element record (V, D, w)
+  static constexpr size_t bytes = sizeof(double) * nD + sizeof(int64_t) * (nRows + TA * TB) +
                                   sizeof(int) * (4 * TA * TB + 2 * TC);
+  // the mesh's element records cached once per CTA after that, for K <= kall(): within the
+  // shared memory of the kernel's two CTAs per SM (or one, for the shapes that need more)
+  // (228 KB per SM hold two CTAs of <= 111 KB dynamic + the static and reserved 1 KB each)
+  static constexpr size_t lim = bytes <= 111 * 1024 ? 111 * 1024 : 225 * 1024;
+  static constexpr size_t eall_off = (bytes + 15) / 16 * 16;
+  static constexpr int kall() { return lim > eall_off ? (int)((lim - eall_off) / (ER * sizeof(double))) : 0; }
 };
 
 // first / one-past-last window element of band row (i, d) (element l supports tile row i
@@ -99,12 +106,13 @@ __device__ __forceinline__ void stage_elements(double* Er, int first, int elo, i
   }
 }
 
-// Pair table of one axis: Pt[t][(i,d)][(l,k)] for the tile rows I = i0 + i and the window
-// records Er (element e = i0 - P + l), with the axis weight (and `scale`) folded in; type 1 =
-// derivative products, plus the value products if `addv` (stiffness + mass, axis 2).
+// Pair table of one axis: Pt[t][(i,d)][(l,k)] for the tile rows I = i0 + i, element e = i0 - P + l
+// read from the records Er[e - ebase] where e is in [elo, ehi) (else 0), with the axis weight (and
+// `scale`) folded in; type 1 = derivative products, plus the value products if `addv`
+// (stiffness + mass, axis 2).
 template <int P, int Q, int T, int E>
-__device__ __forceinline__ void pair_table(double* Pt, const double* Er, int i0, int N, double scale, bool addv,
-                                           int tid) {
+__device__ __forceinline__ void pair_table(double* Pt, const double* Er, int ebase, int elo, int ehi, int i0, int N,
+                                           double scale, bool addv, int tid) {
   constexpr int NB = 2 * P + 1, m = P + 1, G = (T + P) * Q, GP = (G + 1) / 2 * 2, R = T * NB;
   constexpr int ER = erec<P, Q>();
   for (int u = tid; u < E * R * GP; u += NT) {
@@ -113,8 +121,9 @@ __device__ __forceinline__ void pair_table(double* Pt, const double* Er, int i0,
     const int J = i0 + i - P + d;
     const int r = P + i - l, s = i + d - l;  // I - e, J - e
     double v = 0.0;
-    if (g < G && r >= 0 && r <= P && s >= 0 && s <= P && J >= 0 && J < N) {
-      const double* rec = Er + l * ER;
+    const int e = i0 - P + l;
+    if (g < G && r >= 0 && r <= P && s >= 0 && s <= P && J >= 0 && J < N && e >= elo && e < ehi) {
+      const double* rec = Er + (e - ebase) * ER;
       const double w = rec[2 * m * Q + k] * scale;  // 0 outside the mesh / slab
       const double vv = rec[r * Q + k] * rec[s * Q + k];
       if (ty == 0) {
@@ -203,7 +212,7 @@ __device__ __forceinline__ void stage_band(int tid, int ch, int NV, const double
 
 template <int P, int Q, int TA, int TB, int TC, bool ST>
 __global__ void __launch_bounds__(NT, 2)
-    k_tile3(GsfArgs a, const __grid_constant__ CUtensorMap tm, int use_tma, int ntiles) {
+    k_tile3(GsfArgs a, const __grid_constant__ CUtensorMap tm, int use_tma, int ntiles, int eall) {
   using S = Shape<P, Q, TA, TB, TC, ST>;
   constexpr int NB = S::NB, LA = S::LA, LB = S::LB, LC = S::LC;
   constexpr int GB = S::GB, GC = S::GC, GCY = S::GCY;
@@ -219,8 +228,10 @@ __global__ void __launch_bounds__(NT, 2)
   double* EB = EA + LA * ER;
   double* EC = EB + LB * ER;
   int64_t* rowb = reinterpret_cast<int64_t*>(EA + S::nE);  // [TA][TB][TC]
-  int* bnd01 = reinterpret_cast<int*>(rowb + S::nRows);     // [TA*TB][lod0, c0, lod1, c1]
+  int64_t* base01 = rowb + S::nRows;                         // [TA*TB] CSR offset of row (I0, I1, 0)
+  int* bnd01 = reinterpret_cast<int*>(base01 + TA * TB);    // [TA*TB][lod0, c0, lod1, c1]
   int* bnd2 = bnd01 + 4 * TA * TB;                            // [TC][lod2, c2]
+  double* EALL = reinterpret_cast<double*>(reinterpret_cast<char*>(sm) + S::eall_off);  // [K][ER] if eall
   __shared__ uint64_t wbar;
 
   const int K = a.K, N = K + P, tid = threadIdx.x;
@@ -230,6 +241,20 @@ __global__ void __launch_bounds__(NT, 2)
   if (use_tma && tid == 0) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(wbar_s) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+
+  if (eall) {
+    // every element record of the mesh, once (the windows below then read shared memory)
+    for (int u = tid; u < K * ER; u += NT) {
+      const int e = u / ER, j = u - e * ER;
+      constexpr int m = P + 1;
+      double val;
+      if (j < m * Q) val = __ldg(a.V + (int64_t)e * m * Q + j);
+      else if (j < 2 * m * Q) val = a.D != nullptr ? __ldg(a.D + (int64_t)e * m * Q + j - m * Q) : 0.0;
+      else val = axis_w(a.weights, a.wt, e, j - 2 * m * Q, Q);
+      EALL[u] = val;
+    }
+    __syncthreads();
   }
 
   // Persistent CTAs (one wave), each taking a contiguous range of tiles (t2 fastest): a pair
@@ -296,19 +321,34 @@ __global__ void __launch_bounds__(NT, 2)
     }
 
     // ---- pair tables of the changed axes (weights folded; the Jacobian on axis 2)
-    if (n0) stage_elements<P, Q, LA>(EA, i0 - P, e0lo, e0hi, a, tid);
-    if (n1) stage_elements<P, Q, LB>(EB, i1 - P, 0, K, a, tid);
-    if (n2) stage_elements<P, Q, LC>(EC, i2 - P, 0, K, a, tid);
-    __syncthreads();
-    if (n0) pair_table<P, Q, TA, S::E>(PA, EA, i0, N, 1.0, false, tid);
-    if (n1) pair_table<P, Q, TB, S::E>(PB, EB, i1, N, 1.0, false, tid);
-    if (n2) pair_table<P, Q, TC, S::E>(PC, EC, i2, N, a.jac, a.op == IGA_OP_STIFFNESS_MASS, tid);
-    // ---- the tile's CSR rows
+    constexpr int BIG = 0x7fffffff;
+    if (eall) {
+      if (n0) pair_table<P, Q, TA, S::E>(PA, EALL, 0, e0lo, e0hi, i0, N, 1.0, false, tid);
+      if (n1) pair_table<P, Q, TB, S::E>(PB, EALL, 0, 0, K, i1, N, 1.0, false, tid);
+      if (n2) pair_table<P, Q, TC, S::E>(PC, EALL, 0, 0, K, i2, N, a.jac, a.op == IGA_OP_STIFFNESS_MASS, tid);
+    } else {
+      if (n0) stage_elements<P, Q, LA>(EA, i0 - P, e0lo, e0hi, a, tid);
+      if (n1) stage_elements<P, Q, LB>(EB, i1 - P, 0, K, a, tid);
+      if (n2) stage_elements<P, Q, LC>(EC, i2 - P, 0, K, a, tid);
+      __syncthreads();
+      if (n0) pair_table<P, Q, TA, S::E>(PA, EA, i0 - P, -BIG, BIG, i0, N, 1.0, false, tid);
+      if (n1) pair_table<P, Q, TB, S::E>(PB, EB, i1 - P, -BIG, BIG, i1, N, 1.0, false, tid);
+      if (n2)
+        pair_table<P, Q, TC, S::E>(PC, EC, i2 - P, -BIG, BIG, i2, N, a.jac, a.op == IGA_OP_STIFFNESS_MASS, tid);
+    }
+    // ---- the tile's CSR rows: row (I0, I1, I2) = row (I0, I1, 0) + c0 c1 band_prefix(I2)
+    if (n0 || n1) {
+      for (int u = tid; u < TA * TB; u += NT) {
+        const int I0 = i0 + u / TB, I1 = i1 + u % TB;
+        base01[u] = I0 < a.plane_end && I0 < N && I1 < N ? rowptr3(I0, I1, 0, P, N) - a.base : -1;
+      }
+      __syncthreads();
+    }
     for (int u = tid; u < S::nRows; u += NT) {
-      const int ia = u / (TB * TC), ib = (u / TC) % TB, ic = u % TC;
-      const int I0 = i0 + ia, I1 = i1 + ib, I2 = i2 + ic;
-      const bool ok = I0 < a.plane_end && I0 < N && I1 < N && I2 < N;
-      rowb[u] = ok ? rowptr3(I0, I1, I2, P, N) - a.base : -1;
+      const int pc = u / TC, ic = u - pc * TC;
+      const int I0 = i0 + pc / TB, I1 = i1 + pc % TB, I2 = i2 + ic;
+      const int64_t b = base01[pc];
+      rowb[u] = b >= 0 && I2 < N ? b + band_cnt(I0, P, N) * band_cnt(I1, P, N) * band_prefix(I2, P, N) : -1;
     }
     if (n0 || n1) {
       for (int u = tid; u < TA * TB; u += NT) {
@@ -493,13 +533,15 @@ static int launch_t(const GsfArgs& a0, cudaStream_t s) {
       return IGA_EUNSUPPORTED;
     }
     const void* fn = reinterpret_cast<const void*>(k_tile3<P, Q, TA, TB, TC, ST>);
-    cudaError_t e = smem_attr_once(fn, Sh::bytes, true);
+    cudaError_t e = smem_attr_once(fn, Sh::lim, true);
     if (e != cudaSuccess) return check_cuda(e, "tile smem attr");
     CUtensorMap tm{};
     const int use_tma = a.coef != nullptr && coef_tensor_map(tm, a, Q * Q * Q, Sh::LA, Sh::LB, Sh::LC);
     const int64_t slots = (int64_t)sm_count() * blocks_per_sm_once(fn, NT, Sh::bytes);
     const int64_t ctas = grid < slots ? grid : slots;
-    k_tile3<P, Q, TA, TB, TC, ST><<<(unsigned)ctas, NT, Sh::bytes, s>>>(a, tm, use_tma, (int)grid);
+    const int eall = a.K <= Sh::kall();
+    const size_t smem = eall ? Sh::eall_off + (size_t)a.K * Sh::ER * sizeof(double) : Sh::bytes;
+    k_tile3<P, Q, TA, TB, TC, ST><<<(unsigned)ctas, NT, smem, s>>>(a, tm, use_tma, (int)grid, eall);
     return check_cuda(cudaGetLastError(), "tile launch");
   }
 }
