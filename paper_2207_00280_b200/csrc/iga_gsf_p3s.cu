@@ -38,8 +38,8 @@ constexpr int NA0 = TA * NBH;            // (ia, dh) rows, d0 = P + dh >= P (8)
 constexpr int NCOMBO = NA0 * TB * NB;    // (ia, dh, ib, d1) combos (224)
 constexpr int YP = NCOMBO + 4;           // Y pitch (== 12 mod 16: conflict-free A loads)
 constexpr int MT_A = NCOL / 8;           // 14 m-tiles of (g1,k2) columns
-constexpr int MT_B = NA0 * Q / 8;        // 7 m-tiles of (a0,k2) rows
-constexpr int MT_S = NCOMBO / 8;         // 49 m-tiles of combos
+constexpr int MT_B = NA0 * Q / 8;        // 4 m-tiles of (a0,k2) rows
+constexpr int MT_S = NCOMBO / 8;         // 28 m-tiles of combos
 #ifndef P3S_NWB
 #define P3S_NWB 5
 #endif
@@ -51,8 +51,8 @@ constexpr int MT_S = NCOMBO / 8;         // 49 m-tiles of combos
 #endif
 constexpr int NWA = P3S_NWA, NWB = P3S_NWB, NWS = P3S_NWS;  // warps per role (NWA even: fixed type per A warp)
 static_assert(NWA % 2 == 0, "stage-A warps come in (value, derivative) pairs");
-constexpr int NT = 32 * (NWA + NWB + NWS);  // threads (16 warps by default)
-constexpr int MT_S_PER_WARP = (MT_S + NWS - 1) / NWS;  // 5
+constexpr int NT = 32 * (NWA + NWB + NWS);  // threads (16 warps by default: 4 A, 5 B, 7 S)
+constexpr int MT_S_PER_WARP = (MT_S + NWS - 1) / NWS;  // 4
 constexpr int NHB = 2 * MT_B;            // stage-B half units (m-tile, ib pair)
 constexpr int NPEN = TA * TB;            // row pencils (I0, I1) of the tile
 
