@@ -377,6 +377,27 @@ struct GsfTile {
 int launch_gsf_p3(const GsfArgs& a, cudaStream_t s);   // iga_gsf_p3.cu (DMMA, p=3 q=4)
 int launch_gsf_p3s(const GsfArgs& a, cudaStream_t s);  // iga_gsf_p3s.cu (symmetric, whole mesh)
 
+// The symmetric-half kernels write S[I, J] and its mirror S[J, I] from one computation, valid
+// when the call writes every row its element range touches: rows [el_begin, el_end + p) of
+// the mesh (a whole mesh; a multi-GPU slab with its interface planes)
+bool sym_covers(const GsfArgs& a, int p) {
+  const int e0 = a.el_begin > 0 ? a.el_begin : 0, e1 = a.el_end < a.K ? a.el_end : a.K;
+  const int last = e1 + p < a.K + p ? e1 + p : a.K + p;
+  return e1 > e0 && a.plane_begin <= e0 && a.plane_end >= last;
+}
+
+// Before a symmetric launch on a slab (plane_begin > 0): the first p planes' rows hold values
+// with J0 < plane_begin, which no element of the slab supports (they are 0) and which the
+// symmetric kernels would only write as mirrors of rows outside the slab -- zero those rows
+int sym_prezero(const GsfArgs& a, int p, cudaStream_t s) {
+  if (a.plane_begin <= 0) return IGA_OK;
+  const int64_t N = (int64_t)a.K + p;
+  const int64_t hi = a.plane_begin + p < a.plane_end ? a.plane_begin + p : a.plane_end;
+  const int64_t n = rowptr3(hi, 0, 0, p, N) - rowptr3(a.plane_begin, 0, 0, p, N);
+  if (n > 0) return check_cuda(cudaMemsetAsync(a.values, 0, (size_t)n * sizeof(double), s), "slab prezero");
+  return IGA_OK;
+}
+
 // A/B knobs: on only for the exact value "1", read once per process
 static bool env_is_one(const char* name) {
   const char* e = getenv(name);
@@ -430,15 +451,17 @@ struct GsfLaunch {
     if constexpr (P == 3 && Q == 4) {
       // tensor-core specialisation; IGA_GSF_GENERIC=1 selects the generic kernel (A/B tests)
       static const bool generic = env_is_one("IGA_GSF_GENERIC");
-      // the symmetric variant computes J0 >= I0 and mirrors the rest, so it needs every row
-      // of the mesh (a whole-mesh run); IGA_GSF_SYM=0 selects k_gsf3_p3 (A/B tests)
+      // the symmetric variant computes J0 >= I0 and mirrors the rest, so the call must write
+      // every row its elements touch (a whole mesh, or an element slab with its interface
+      // planes); IGA_GSF_SYM=0 selects k_gsf3_p3 (A/B tests)
       static const bool no_sym = [] {
         const char* e = getenv("IGA_GSF_SYM");
         return e != nullptr && e[0] == '0' && e[1] == 0;
       }();
-      const bool whole = a0.plane_begin == 0 && a0.plane_end == a0.K + P && a0.el_begin <= 0 &&
-                         a0.el_end >= a0.K && a0.base == 0;
-      if (!generic && whole && !no_sym) return launch_gsf_p3s(a0, s);
+      if (!generic && sym_covers(a0, P) && !no_sym) {
+        const int rc = sym_prezero(a0, P, s);
+        return rc != IGA_OK ? rc : launch_gsf_p3s(a0, s);
+      }
       if (!generic) return launch_gsf_p3(a0, s);
     }
     if constexpr (P >= 1 && P <= 2) {

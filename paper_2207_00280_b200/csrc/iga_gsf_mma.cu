@@ -34,6 +34,8 @@
 #include "iga_dispatch.cuh"
 
 namespace iga {
+bool sym_covers(const GsfArgs& a, int p);                // iga_gsf.cu
+int sym_prezero(const GsfArgs& a, int p, cudaStream_t s);  // iga_gsf.cu
 namespace mma {
 
 // threads per CTA: 512 (one CTA per SM, shared-memory bound) for p >= 3; 256 for p <= 2, whose
@@ -280,7 +282,8 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
       const int I0 = i00 + ia, I1 = i10 + ib, J0 = I0 + dx, J1 = I1 - P + d1;
       int64_t base = 0;
       int c01 = 0, b01 = -1;
-      if (I0 < a.plane_end && I1 < N && J0 < N && J1 >= 0 && J1 < N) {
+      // (a slab's J0 past its planes: the value is 0 there, no element of the slab supports both rows)
+      if (I0 < a.plane_end && I1 < N && J0 < a.plane_end && J0 < N && J1 >= 0 && J1 < N) {
         const int jc1 = (int)band_cnt(J1, P, N);
         base = rowptr3(J0, J1, 0, P, N) - a.base;
         c01 = (int)band_cnt(J0, P, N) * jc1;
@@ -801,7 +804,8 @@ static int launch_t(const GsfArgs& a0, cudaStream_t s) {
 }
 
 // Symmetric half (SYM, p >= 3): only the J0 >= I0 values are computed and the rest mirrored, so
-// the launch must cover every row of the mesh; IGA_GSF_SYM=0 selects the full computation (A/B).
+// the launch must write every row its elements touch (sym_covers); IGA_GSF_SYM=0 selects the
+// full computation (A/B).
 template <int P, int Q>
 struct Launch {
   static int run(const GsfArgs& a, cudaStream_t s) {
@@ -809,12 +813,14 @@ struct Launch {
       const char* e = getenv("IGA_GSF_SYM");
       return e != nullptr && e[0] == '0' && e[1] == 0;
     }();
-    const bool whole = a.plane_begin == 0 && a.plane_end == a.K + P && a.el_begin <= 0 && a.el_end >= a.K &&
-                       a.base == 0 && a.K + P <= Shape<P, Q, 1, 1, true, true>::NBT;
     // p <= 2: the ring and run-emission work outweighs the halved stages B and S
     // (tools/tile_shapes.py, IGA_GSF_TILE=0: 64^3 p = 2 stiffness 0.430 vs 0.422 ms, p = 1 mass
     // 0.197 vs 0.123); C4 (p = 4): 10.19 vs 11.71 ms
-    const bool sym = whole && !no_sym && P >= 3;
+    const bool sym = sym_covers(a, P) && !no_sym && P >= 3;
+    if (sym) {
+      const int rc = sym_prezero(a, P, s);
+      if (rc != IGA_OK) return rc;
+    }
     if (a.op == IGA_OP_MASS) return sym ? launch_t<P, Q, false, true>(a, s) : launch_t<P, Q, false>(a, s);
     if constexpr (P >= 1) return sym ? launch_t<P, Q, true, true>(a, s) : launch_t<P, Q, true>(a, s);
     set_error("derivatives require degree >= 1");

@@ -13,9 +13,9 @@
 // each S warp keeps per-combo rings of its mirrored values by target row (ring_put) and
 // writes every target row's values of a combo as one contiguous run once its last source row
 // is done (emit_runs: hi runs d2' = 0..3 when source row J2 completes, lo runs d2' = 4..6
-// three columns later): C3 0.458 ms against 0.509 for k_gsf3_p3.  Whole-mesh runs only
-// (every mirror target row in range); element slabs and row-plane ranges (multi-GPU) take
-// k_gsf3_p3.
+// three columns later): C3 0.458 ms against 0.509 for k_gsf3_p3.  Valid when the call writes
+// every row its elements touch (sym_covers: a whole mesh, or a multi-GPU element slab with
+// its interface planes); other plane ranges take k_gsf3_p3.
 //
 // Everything else -- tiling, the roles, the mbarrier hand-off, the rolling rows of stage S,
 // the summation order of each computed value -- is k_gsf3_p3's; see its header.
@@ -660,8 +660,10 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3s(GsfArgs a) {
           const int c0 = (int)band_cnt(I0, P, N), c1 = (int)band_cnt(I1, P, N);
           if (d0 >= lod0 && d0 < lod0 + c0 && d1 >= lod1 && d1 < lod1 + c1) {
             meta[i] = ((ia * TB + ib) << 16) | ((d0 - lod0) * c1 + (d1 - lod1));
-            if (dh > 0) {
+            if (dh > 0 && I0 + dh < a.plane_end) {
               // mirror: row J = (I0 + dh, I1 + d1 - P, .) holds this value at (P - dh, 2P - d1, .)
+              // (a slab's J0 past its planes: the value is 0 there, no element of the slab
+              // supports both rows)
               const int J0 = I0 + dh, J1 = I1 + d1 - P;
               const int jl0 = max(0, P - J0), jl1 = max(0, P - J1);
               const int jc1 = (int)band_cnt(J1, P, N);

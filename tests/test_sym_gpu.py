@@ -93,3 +93,41 @@ def test_nonsymmetric_kernel_vs_oracle():
 
 if __name__ == "__main__" and "--case" in sys.argv:
     _run_cases()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("K,p,op", [(10, 3, "stiffness"), (9, 4, "stiffness_mass"), (8, 3, "mass")])
+def test_symmetric_slabs_sum_to_full(K, p, op):
+    """Element slabs with their interface planes (the multi-GPU decomposition) run
+    the symmetric kernels too: a slab's contribution is symmetric and lives in the rows it
+    writes.  The outputs start as NaN, so a value the kernels fail to write (the slab's first p
+    planes hold zeros for columns below it) shows up; the partial planes add up to the
+    whole-mesh matrix."""
+    import torch
+
+    from paper_2207_00280_b200 import _lib
+    from paper_2207_00280_b200.device import MeshProblem
+
+    q = p + 1
+    N = K + p
+    coef = torch.from_numpy(_coef(K, q, "field", 11)).cuda()
+    mp = MeshProblem(3, K, p, operator=op, coefficient=coef)
+    full = torch.full((mp.nnz(),), float("nan"), dtype=torch.float64, device="cuda")
+    mp.integrate_assemble(full, _lib.METHOD_SUMFACT_ASSEMBLED)
+    acc = torch.zeros_like(full)
+    bounds = [0, 3, 6, K]
+    for g in range(3):
+        lo, hi = bounds[g], bounds[g + 1]
+        phi = min(hi + p, N)
+        part = torch.full((mp.nnz(lo, phi),), float("nan"), dtype=torch.float64, device="cuda")
+        mp.integrate_assemble(part, _lib.METHOD_SUMFACT_ASSEMBLED, el_range=(lo, hi), plane_range=(lo, phi))
+        assert not torch.isnan(part).any(), f"slab {g}: unwritten values"
+        off = mp.nnz(0, lo)
+        acc[off:off + part.numel()] += part
+    c = coef.cpu().numpy()
+    ip, _, ref = O.integrate_assemble(3, K, p, op, "classical", q=q, coef=c)
+    _, _, A = O.integrate_assemble(3, K, p, op, "classical", q=q, coef=c, absolute=True)
+    from tests.parity import assert_parity
+
+    assert_parity(full.cpu().numpy(), ref, ip, what=f"sym full {op} K={K} p={p}", absref=A)
+    assert_parity(acc.cpu().numpy(), ref, ip, what=f"sym slabs {op} K={K} p={p}", absref=A)
