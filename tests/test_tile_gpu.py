@@ -120,3 +120,39 @@ def test_tile_bitwise_reproducible():
 
 if __name__ == "__main__" and "--case" in sys.argv:
     _run_cases()
+
+
+def _sampled_values(K, p, op, idx_seed, n_samples, out_path):
+    """Child: one owner run, the values at seeded sample indices saved to out_path."""
+    import paper_2207_00280_b200 as pkg
+
+    q = p + 1
+    coef = np.random.default_rng(5).uniform(0.5, 1.5, size=(K**3, q**3))
+    res = pkg.run_integration(pkg.RunConfig("sumfact", "device", K, p, quad_points=q, operator=op, coefficient=coef,
+                                            assembly="owner"))
+    v = res.gram.values
+    idx = np.random.default_rng(idx_seed).integers(0, v.numel(), size=n_samples)
+    import torch
+
+    np.save(out_path, v[torch.from_numpy(idx).to(v.device)].cpu().numpy())
+
+
+@pytest.mark.gpu
+def test_tile_kernel_uncached_records_match_streaming(tmp_path):
+    """p = 2 stiffness at K = 88: the mesh's element records exceed the tile kernel's shared
+    cache (K <= 81 for this shape), so its per-tile staging path runs; forced on, its values
+    match the streaming kernel's at 200,000 sampled entries (both are oracle-checked on small
+    meshes above)."""
+    K, p, op = 88, 2, "stiffness"
+    outs = {}
+    for forced in ("1", "0"):
+        path = str(tmp_path / f"v{forced}.npy")
+        code = (f"import sys; sys.path.insert(0, {ROOT!r}); from tests.test_tile_gpu import _sampled_values; "
+                f"_sampled_values({K}, {p}, {op!r}, 9, 200000, {path!r})")
+        out = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, IGA_GSF_TILE=forced), cwd=ROOT,
+                             capture_output=True, text=True, timeout=900)
+        assert out.returncode == 0, out.stderr[-2000:]
+        outs[forced] = np.load(path)
+    a, b = outs["1"], outs["0"]
+    scale = np.abs(b).max()
+    assert np.all(np.abs(a - b) <= 1e-12 * np.abs(b) + 1e-13 * scale), np.max(np.abs(a - b))
