@@ -470,10 +470,6 @@ __device__ __forceinline__ void stage_s(const Lane& L, int ws, const double* Y, 
   stage_s_batch<PHI, 0, B0>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd, rg, e2);
   if constexpr (B1 > 0) stage_s_batch<PHI, B0, B1>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd, rg, e2);
   if constexpr (B2 > 0) stage_s_batch<PHI, B0 + B1, B2>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd, rg, e2);
-  __syncwarp();
-  emit_runs(a, rg, mm, ws, L, e2, true, bt, N);
-  if (e2 >= 3) emit_runs(a, rg, mm, ws, L, e2 - 3, false, bt, N);
-  __syncwarp();
 }
 
 // Rows K .. K+P-1 (no element e2 = I2): both groups are complete in their slots.
@@ -698,6 +694,12 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3s(GsfArgs a) {
       }
       if (e2 + 1 < K) s_raw_load(L, a, e2 + 1, sraw);
       mbar_arrive(yempty + b);
+      // the mirrored runs leave after the Y buffer is released: stage B refills it meanwhile
+      // (C3 0.458 -> 0.437 ms; releasing Y before the rolling-row and CSR stores too: 0.446)
+      __syncwarp();
+      emit_runs(a, rgw, mmw, ws, L, e2, true, reinterpret_cast<const int2*>(sm + OFF_BT), N);
+      if (e2 >= 3) emit_runs(a, rgw, mmw, ws, L, e2 - 3, false, reinterpret_cast<const int2*>(sm + OFF_BT), N);
+      __syncwarp();
     }
     // rows K .. K+P-1 received their last contribution from element K-1
     for (int I2 = K; I2 < N; ++I2) flush_tail(L, ws, Rs, I2, meta, pb, pc, a, N, mmw, rgw);
