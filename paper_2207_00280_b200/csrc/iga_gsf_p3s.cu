@@ -10,12 +10,16 @@
 // per element column 546 -> 372), and the band-group DFMAs of stage A halve.  The mirrored
 // values land in another pencil's row per lane: written directly they cost 32 partial-sector
 // L2 writes per warp store instruction (C3: 0.571 ms, against 0.391 without them).  Instead
-// each S warp keeps per-combo rings of its mirrored values by target row (ring_put) and
-// writes every target row's values of a combo as one contiguous run once its last source row
-// is done (emit_runs: hi runs d2' = 0..3 when source row J2 completes, lo runs d2' = 4..6
-// three columns later): C3 0.458 ms against 0.509 for k_gsf3_p3.  Valid when the call writes
-// every row its elements touch (sym_covers: a whole mesh, or a multi-GPU element slab with
-// its interface planes); other plane ranges take k_gsf3_p3.
+// each S warp keeps per-combo rings of its mirrored values by target row (ring_put), and a
+// fourth role, the emitter warps (role E, emit_all), writes every target row's values of a
+// combo as one contiguous run once its last source row is done (hi runs d2' = 0..3 when
+// source row J2 completes, lo runs d2' = 4..6 three columns later).  The S warps hand a row
+// to the emitters through mbarriers (rfull / rfree) and may run two rows ahead of them.  With
+// the S warps emitting their own runs they were the slowest role (stage B waited on their Y
+// buffers: 10% of the stall samples); 20 warps cost 96 registers per thread, which the roles
+// fit.  C3: 0.419 ms against 0.437 with S-warp emission and 0.509 for k_gsf3_p3.  Valid when
+// the call writes every row its elements touch (sym_covers: a whole mesh, or a multi-GPU
+// element slab with its interface planes); other plane ranges take k_gsf3_p3.
 //
 // Everything else -- tiling, the roles, the mbarrier hand-off, the rolling rows of stage S,
 // the summation order of each computed value -- is k_gsf3_p3's; see its header.
@@ -49,9 +53,16 @@ constexpr int MT_S = NCOMBO / 8;         // 28 m-tiles of combos
 #ifndef P3S_NWA
 #define P3S_NWA 4
 #endif
-constexpr int NWA = P3S_NWA, NWB = P3S_NWB, NWS = P3S_NWS;  // warps per role (NWA even: fixed type per A warp)
+#ifndef P3S_NWE
+#define P3S_NWE 4
+#endif
+// warps per role (NWA even: fixed type per A warp); the NWE emitter warps write the mirrored
+// runs out of the S warps' rings.  17..20 warps cost the same 96 registers per thread (5 warps
+// per SM sub-partition), so the emitters come in fours.
+constexpr int NWA = P3S_NWA, NWB = P3S_NWB, NWS = P3S_NWS, NWE = P3S_NWE;
 static_assert(NWA % 2 == 0, "stage-A warps come in (value, derivative) pairs");
-constexpr int NT = 32 * (NWA + NWB + NWS);  // threads (16 warps by default: 4 A, 5 B, 7 S)
+static_assert(NWE >= 1, "role E writes the mirrored runs");
+constexpr int NT = 32 * (NWA + NWB + NWS + NWE);  // threads (20 warps by default: 4 A, 5 B, 7 S, 4 E)
 constexpr int MT_S_PER_WARP = (MT_S + NWS - 1) / NWS;  // 4
 constexpr int NHB = 2 * MT_B;            // stage-B half units (m-tile, ib pair)
 constexpr int NPEN = TA * TB;            // row pencils (I0, I1) of the tile
@@ -71,18 +82,21 @@ constexpr int OFF_WQ = OFF_Y + 2 * SZ_Y;          // weights [Q]
 constexpr int OFF_PB = OFF_WQ + Q;                // pencil row-pointer bases (int64) [NPEN]
 constexpr int OFF_PC = OFF_PB + NPEN;             // pencil c0*c1 (int in double slots) [NPEN]
 constexpr int OFF_R = OFF_PC + NPEN;              // rolling rows [MT_S][4 slots][2 groups][32]
-// mirror metadata of the S warps' m-tiles, per lane: CSR base of the target pencil (int64)
-// and (c0 c1, (d0, d1) block offset) of the target row (int pair); block -1: no mirror
-constexpr int OFF_MM = OFF_R + MT_S * 4 * 2 * 32;  // [NWS][MT_S_PER_WARP][2][32]
+// mirror metadata per ring combo c = ((ws, i), g), written by the S warps and read once by
+// the emitters: CSR base of the target pencil (int64) and (c0 c1, (d0, d1) block offset) of
+// the target row (int pair); block -1: no mirror
+constexpr int NRC = NWS * MT_S_PER_WARP * 8;       // ring combos (224)
+constexpr int OFF_MM = OFF_R + MT_S * 4 * 2 * 32;  // [NRC][2]
 // axis-2 band table {band_prefix(I2), band_cnt(I2)} for meshes with N <= NBT rows (else computed)
-constexpr int NBT = 1024;
-constexpr int OFF_BT = OFF_MM + NWS * MT_S_PER_WARP * 2 * 32;  // int2 [NBT]
-// per S warp, per (m-tile, combo): rings of the mirrored values by target row -- hi runs
-// [4 rows][d2' 0..3], lo runs [4 rows][d2' 4..6] -- so they leave as contiguous runs
-constexpr int RING = 28;
-constexpr int OFF_RING = OFF_BT + NBT;                 // [NWS][MT_S_PER_WARP][8][RING]
-constexpr int OFF_MB = OFF_RING + NWS * MT_S_PER_WARP * 8 * RING;  // mbarriers
-constexpr int SMEM_DOUBLES = OFF_MB + 8;
+constexpr int NBT = 512;
+constexpr int OFF_BT = OFF_MM + NRC * 2;  // int2 [NBT]
+// per ring combo: the mirrored values by target row J2 -- hi runs [J2 mod 8][d2' 0..3], lo runs
+// [J2 mod 4][d2' 4..6] -- so they leave as contiguous runs.  The slot counts let the S warps
+// run a whole element column ahead of the emitters (ring_put / role E below).
+constexpr int RING_LO = 32, RING = RING_LO + 12;
+constexpr int OFF_RING = OFF_BT + NBT;     // [NRC][RING]
+constexpr int OFF_MB = OFF_RING + NRC * RING;  // mbarriers
+constexpr int SMEM_DOUBLES = OFF_MB + 12;
 static_assert(SMEM_DOUBLES * 8 <= 227 * 1024, "shared memory budget");
 constexpr size_t SMEM_BYTES = SMEM_DOUBLES * sizeof(double);
 
@@ -315,36 +329,44 @@ __device__ __forceinline__ void store_pair(const GsfArgs& a, int m, const int64_
   }
 }
 
-// Row I2's mirrored values into this lane group's rings: hi -> target J2 = I2 + t at d2' = 3 - t,
-// lo -> J2 = I2 + t - 4 at d2' = 7 - t (ring entry d2' - 4); slot = J2 mod 4
+// Row I2's mirrored values into this lane group's rings: hi -> target J2 = I2 + t at d2' = 3 - t
+// (slot J2 mod 8), lo -> J2 = I2 + t - 4 at d2' = 7 - t (ring entry d2' - 4, slot J2 mod 4).
+// The hi slot was last read for target J2 - 8, emitted with row J2 - 8 <= I2 - 5; the lo slot
+// for target J2 - 4, emitted with row J2 - 1 <= I2 - 2: row I2's values may be put once the
+// emitters are done with row I2 - 2.
 __device__ __forceinline__ void ring_put(double* rg, int i, int g, int t, int I2, double hi, double lo) {
   double* r = rg + (i * 8 + g) * RING;
-  const int slot = (I2 + t) & 3;
-  r[slot * 4 + (3 - t)] = hi;
-  if (t > 0) r[16 + slot * 3 + (3 - t)] = lo;
+  r[((I2 + t) & 7) * 4 + (3 - t)] = hi;
+  if (t > 0) r[RING_LO + ((I2 + t) & 3) * 3 + (3 - t)] = lo;
 }
 
-// Target row J2's complete runs of this warp's m-tiles: hi (d2' = t) or lo (d2' = 4 + t, t < 3),
-// one contiguous run per combo (the 4 lanes of its group write consecutive values)
-__device__ __forceinline__ void emit_runs(const GsfArgs& a, const double* rg, const double* mm, int ws, const Lane& L,
-                                          int J2, bool hi, const int2* bt, int64_t N) {
-  const int t = L.t, g = L.g;
-  if (!hi && t == 3) return;
-  const int2 b = band_of(bt, J2, N);
-  const int off = (hi ? t : 4 + t) - max(0, P - J2);
-  if (off < 0 || off >= b.y) return;
-  const int slot = J2 & 3;
+// Target row J2's complete runs, written by the emitter warps (role E): hi (d2' = t) or lo
+// (d2' = 4 + t, t < 3), one contiguous run per combo (the 4 lanes of a group write consecutive
+// values).  The ring combos, in ring order, are dealt to the NWE * 8 lane groups; a lane keeps
+// t and the CSR metadata of its ENJ combos in registers, so a row's emission is ENJ
+// independent {ring load, address, store} sequences.
+constexpr int ENG = NWE * 8;                   // lane groups
+constexpr int ENJ = (NRC + ENG - 1) / ENG;     // combos per lane (7)
+struct EMeta {
+  double* row[ENJ];  // values + CSR base of the target pencil
+  int cx[ENJ], cy[ENJ];
+};
+template <bool HI>
+__device__ __forceinline__ void emit_all(const GsfArgs& a, const double* sm, const EMeta& em, int et, int J2,
+                                         int64_t N) {
+  const int2 b = band_of(reinterpret_cast<const int2*>(sm + OFF_BT), J2, N);
+  const int t = et & 3;
+  const int off = (HI ? t : 4 + t) - max(0, P - J2);
+  const bool ok = (HI || t < 3) && off >= 0 && off < b.y;
+  const double* r = sm + OFF_RING + (et >> 2) * RING +
+                    (HI ? (J2 & 7) * 4 + t : RING_LO + (J2 & 3) * 3 + (t < 3 ? t : 0));
+  double v[ENJ];
 #pragma unroll
-  for (int i = 0; i < MT_S_PER_WARP; ++i) {
-    const int mt = ws + i * NWS;
-    if (mt >= MT_S) break;
-    const int2 cb = *reinterpret_cast<const int2*>(mm + i * 64 + 32);
-    if (cb.y < 0) continue;
-    const int64_t base = *reinterpret_cast<const int64_t*>(mm + i * 64);
-    const double* r = rg + (i * 8 + g) * RING;
-    const double v = hi ? r[slot * 4 + t] : r[16 + slot * 3 + t];
-    a.values[base + (int64_t)cb.x * b.x + cb.y * b.y + off] = v;
-  }
+  for (int j = 0; j < ENJ; ++j) v[j] = em.cy[j] >= 0 ? r[j * ENG * RING] : 0.0;
+  // offsets within a pencil fit 32 bits: c0 c1 band_prefix(J2) + (block) band_cnt(J2) + off < 343 N
+#pragma unroll
+  for (int j = 0; j < ENJ; ++j)
+    if (ok && em.cy[j] >= 0) em.row[j][em.cx[j] * b.x + em.cy[j] * b.y + off] = v[j];
 }
 
 template <int PHI, int I0, int NM>
@@ -388,6 +410,9 @@ __device__ __forceinline__ void stage_s_batch(const Lane& L, int ws, const doubl
       for (int nt = 0; nt < 2; ++nt)
         dmma(cc[i][nt][0], cc[i][nt][1], a1[i], b1[nt], cc[i][nt][0], cc[i][nt][1]);
   }
+  // the emitters are done with row e2 - 2 (ring_put): its slots are reused from here on
+  if (I0 == 0 && e2 >= 2)
+    mbar_wait(reinterpret_cast<uint64_t*>(Rs - OFF_R + OFF_MB) + 10 + (e2 & 1), ((e2 >> 1) - 1) & 1);
 #pragma unroll
   for (int i = 0; i < NM; ++i) {
 #pragma unroll
@@ -456,8 +481,7 @@ template <int PHI>
 __device__ __forceinline__ void stage_s(const Lane& L, int ws, const double* Y, double* Rs,
                                         const GsfArgs& a, int e2, const int (&meta)[MT_S_PER_WARP],
                                         const int64_t* pb, const int* pc, int64_t N,
-                                        const double (&b0)[2], const double (&b1)[2], const double* mm,
-                                        double* rg) {
+                                        const double (&b0)[2], const double (&b1)[2], double* rg) {
   const int t = L.t;
   const int2* bt = reinterpret_cast<const int2*>(Rs - OFF_R + OFF_BT);  // Rs = sm + OFF_R
   const RowDst rd = row_dst(t, e2, N, bt);
@@ -475,8 +499,7 @@ __device__ __forceinline__ void stage_s(const Lane& L, int ws, const double* Y, 
 // Rows K .. K+P-1 (no element e2 = I2): both groups are complete in their slots.
 __device__ __forceinline__ void flush_tail(const Lane& L, int ws, const double* Rs, int I2,
                                            const int (&meta)[MT_S_PER_WARP], const int64_t* pb,
-                                           const int* pc, const GsfArgs& a, int64_t N, const double* mm,
-                                           double* rg) {
+                                           const int* pc, const GsfArgs& a, int64_t N, double* rg) {
   const int2* bt = reinterpret_cast<const int2*>(Rs - OFF_R + OFF_BT);  // Rs = sm + OFF_R
   const RowDst rd = row_dst(L.t, I2, N, bt);
   const int sl = I2 & 3;
@@ -489,10 +512,6 @@ __device__ __forceinline__ void flush_tail(const Lane& L, int ws, const double* 
       ring_put(rg, i, L.g, L.t, I2, hi, lo);
     }
   }
-  __syncwarp();
-  emit_runs(a, rg, mm, ws, L, I2, true, bt, N);
-  if (I2 >= 3) emit_runs(a, rg, mm, ws, L, I2 - 3, false, bt, N);
-  __syncwarp();
 }
 
 // W[(la,k0)][(g1,k2)] = c w0 w1 w2 jac on the CTA's quadrature slab of column e2
@@ -561,7 +580,14 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3s(GsfArgs a) {
   }
   uint64_t* mb = reinterpret_cast<uint64_t*>(sm + OFF_MB);
   uint64_t *xfull = mb, *xempty = mb + 2, *yfull = mb + 4, *yempty = mb + 6;
+  // S -> E: row e2's ring values are in place (rfull[e2 & 1]); E -> S: its runs are written
+  // (rfree[e2 & 1]).  Two barriers each: the S warps may be two rows ahead of the emitters.
+  uint64_t *rfull = mb + 8, *rfree = mb + 10;
   if (tid == 0) {
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(rfull + b, NWS * 32);
+      mbar_init(rfree + b, NWE * 32);
+    }
     for (int b = 0; b < 2; ++b) {
       mbar_init(xfull + b, NWA * 32);
       mbar_init(xempty + b, NWB * 32);
@@ -632,14 +658,39 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3s(GsfArgs a) {
       mbar_arrive(xempty + b);
       mbar_arrive(yfull + b);
     }
+  } else if (warp >= NWA + NWB + NWS) {
+    // ------------------------------------------------------------ role E
+    // the mirrored runs of target rows e2 (hi) and e2 - 3 (lo) leave once the S warps have put
+    // row e2's values into their rings
+    const int et = tid - (NWA + NWB + NWS) * 32;
+    __syncthreads();  // the S warps have written their mirror metadata
+    EMeta em;
+#pragma unroll
+    for (int j = 0; j < ENJ; ++j) {
+      const int c = (et >> 2) + j * ENG;
+      em.row[j] = a.values; em.cx[j] = 0; em.cy[j] = -1;
+      if (c < NRC) {
+        const int2 cb = *reinterpret_cast<const int2*>(sm + OFF_MM + 2 * c + 1);
+        em.row[j] = a.values + *reinterpret_cast<const int64_t*>(sm + OFF_MM + 2 * c);
+        em.cx[j] = cb.x; em.cy[j] = cb.y;
+      }
+    }
+    for (int e2 = 0; e2 < N; ++e2) {
+      mbar_wait(rfull + (e2 & 1), (e2 >> 1) & 1);
+      emit_all<true>(a, sm, em, et, e2, N);
+      if (e2 >= 3) emit_all<false>(a, sm, em, et, e2 - 3, N);
+      mbar_arrive(rfree + (e2 & 1));
+    }
+    // lo runs of the last three target rows (their later sources do not exist)
+    for (int J2 = max(0, (int)N - 3); J2 < N; ++J2) emit_all<false>(a, sm, em, et, J2, N);
   } else {
     // ------------------------------------------------------------ role S
     const int ws = warp - NWA - NWB;
     // per-lane store metadata of its m-tiles: pencil rc and the (d0,d1) block offset
     // b01 = (d0-lo0)*c1 + (d1-lo1) in the CSR row; -1 if the combo is outside
     int meta[MT_S_PER_WARP];
-    double* mmw = sm + OFF_MM + ws * MT_S_PER_WARP * 64 + L.lane;  // this lane's mirror metadata
-    double* rgw = sm + OFF_RING + ws * MT_S_PER_WARP * 8 * RING;       // this warp's rings
+    double* mmw = sm + OFF_MM + 2 * (ws * MT_S_PER_WARP * 8 + L.g);  // its lane groups' mirror metadata
+    double* rgw = sm + OFF_RING + ws * MT_S_PER_WARP * 8 * RING;     // this warp's rings
 #pragma unroll
     for (int i = 0; i < MT_S_PER_WARP; ++i) {
       const int mt = ws + i * NWS;
@@ -669,10 +720,12 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3s(GsfArgs a) {
             }
           }
         }
-        *reinterpret_cast<int64_t*>(mmw + i * 64) = mbase;
-        *reinterpret_cast<int2*>(mmw + i * 64 + 32) = make_int2(mc01, mb01);
-      } else {
-        *reinterpret_cast<int2*>(mmw + i * 64 + 32) = make_int2(0, -1);
+        if (L.t == 0) {
+          *reinterpret_cast<int64_t*>(mmw + i * 16) = mbase;
+          *reinterpret_cast<int2*>(mmw + i * 16 + 1) = make_int2(mc01, mb01);
+        }
+      } else if (L.t == 0) {
+        *reinterpret_cast<int2*>(mmw + i * 16 + 1) = make_int2(0, -1);
       }
     }
     double* Rs = sm + OFF_R;
@@ -687,26 +740,20 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3s(GsfArgs a) {
       const double* Y = sm + OFF_Y + b * SZ_Y;
       if (e2 > 0) s_raw_form(L, sraw, sb0, sb1);
       switch (e2 & 3) {
-        case 0: stage_s<0>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1, mmw, rgw); break;
-        case 1: stage_s<1>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1, mmw, rgw); break;
-        case 2: stage_s<2>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1, mmw, rgw); break;
-        default: stage_s<3>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1, mmw, rgw); break;
+        case 0: stage_s<0>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1, rgw); break;
+        case 1: stage_s<1>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1, rgw); break;
+        case 2: stage_s<2>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1, rgw); break;
+        default: stage_s<3>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1, rgw); break;
       }
       if (e2 + 1 < K) s_raw_load(L, a, e2 + 1, sraw);
       mbar_arrive(yempty + b);
-      // the mirrored runs leave after the Y buffer is released: stage B refills it meanwhile
-      // (C3 0.458 -> 0.437 ms; releasing Y before the rolling-row and CSR stores too: 0.446)
-      __syncwarp();
-      emit_runs(a, rgw, mmw, ws, L, e2, true, reinterpret_cast<const int2*>(sm + OFF_BT), N);
-      if (e2 >= 3) emit_runs(a, rgw, mmw, ws, L, e2 - 3, false, reinterpret_cast<const int2*>(sm + OFF_BT), N);
-      __syncwarp();
+      mbar_arrive(rfull + b);  // role E writes the mirrored runs this row completes
     }
     // rows K .. K+P-1 received their last contribution from element K-1
-    for (int I2 = K; I2 < N; ++I2) flush_tail(L, ws, Rs, I2, meta, pb, pc, a, N, mmw, rgw);
-    {
-      // lo runs of the last three target rows (their later sources do not exist)
-      const int2* bt = reinterpret_cast<const int2*>(sm + OFF_BT);
-      for (int J2 = max(0, (int)N - 3); J2 < N; ++J2) emit_runs(a, rgw, mmw, ws, L, J2, false, bt, N);
+    for (int I2 = K; I2 < N; ++I2) {
+      if (I2 >= 2) mbar_wait(rfree + (I2 & 1), ((I2 >> 1) - 1) & 1);
+      flush_tail(L, ws, Rs, I2, meta, pb, pc, a, N, rgw);
+      mbar_arrive(rfull + (I2 & 1));
     }
   }
 }

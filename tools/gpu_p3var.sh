@@ -1,2 +1,2 @@
 # time built p3 variants (build/p3 is gpurun-ignored, so variants are copied to tune/p3)
-for v in "$@"; do ./tune/p3/$v; done
+for v in "$@"; do timeout 30 ./tune/p3/$v; done
