@@ -386,11 +386,23 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
   // (rc, v) loop below.  Both write the same values to the same addresses.
   constexpr int VT = cdiv(S::rowVals, 32) * 32, RCS = NT / VT;
   constexpr bool by_v = !SYM && RCS >= 1 && RCS * VT == NT;
-  constexpr int VPT = cdiv(S::rowVals, NT);
+  // The flat flush shares its barrier phase with stage A.  Where stage A is one m-tile whose
+  // n-tiles give the first NHV warps two and the others one (symmetric p = 4: 25 n-tiles, 16
+  // warps), the other warps flush (GSF_REV & 4); else the band positions are dealt from the
+  // last warp down (GSF_REV & 1), so the warps left without flush work are the first ones.
+#ifndef GSF_REV
+#define GSF_REV 7
+#endif
+  constexpr int NTL_A = cdiv(GC, 8), NWARP_ = NT / 32;
+  constexpr bool split_flush = (GSF_REV & 4) && SYM && cdiv(NA0, 8) == 1 && NTL_A > NWARP_ && NTL_A < 2 * NWARP_;
+  constexpr int NHV = split_flush ? NTL_A - NWARP_ : 0;  // warps with two stage-A n-tiles
+  constexpr int NFT = NT - 32 * NHV;                      // flushing threads
+  constexpr int VPT = cdiv(S::rowVals, NFT);
+  const int FT = split_flush ? (tid >= 32 * NHV ? tid - 32 * NHV : S::rowVals) : (GSF_REV & 1) ? NT - 1 - tid : tid;
   int vd[VPT];  // (d0 - D0X, d1, d2) of this thread's band positions, packed
 #pragma unroll
   for (int j = 0; j < VPT; ++j) {
-    const int v = tid + j * NT;
+    const int v = FT + j * NFT;
     vd[j] = (v / (NB * NB)) << 16 | ((v / NB) % NB) << 8 | (v % NB);
   }
   auto flush_row = [&](int I2) {
@@ -428,7 +440,7 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
     // walks the pencils
 #pragma unroll
     for (int j = 0; j < VPT; ++j) {
-      const int v = tid + j * NT;
+      const int v = FT + j * NFT;
       if (v >= S::rowVals) break;
       const int d2 = vd[j] & 255, d1 = (vd[j] >> 8) & 255, dx = vd[j] >> 16, d0 = D0X + dx;
       const bool in2 = d2 >= lod2 && d2 < lod2 + c2;
@@ -700,7 +712,9 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
       if constexpr (NTL * 8 < MM) {
         // leftover pairs: one (combo, pair) per thread, distinct R entries from the DMMA part
         constexpr int NL = MM - NTL * 8;
-        for (int u = tid; u < NC * NL; u += NT) {
+        // (dealt from the last warp down, GSF_REV & 2: the warps past NTL * GRP and those of
+        // the last groups have the fewest m-tiles)
+        for (int u = (GSF_REV & 2) ? NT - 1 - tid : tid; u < NC * NL; u += NT) {
           const int c = u / NL, nn = NTL * 8 + u % NL, r = nn / m, sc = nn % m;
           const int slot = slot0 + r >= m ? slot0 + r - m : slot0 + r;
           double* Rr = R + comboR[c] + slot * S::RP + sc - r + P;
