@@ -131,3 +131,32 @@ def test_symmetric_slabs_sum_to_full(K, p, op):
 
     assert_parity(full.cpu().numpy(), ref, ip, what=f"sym full {op} K={K} p={p}", absref=A)
     assert_parity(acc.cpu().numpy(), ref, ip, what=f"sym slabs {op} K={K} p={p}", absref=A)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("K,p,op,kind", [(40, 3, "stiffness", "scalar"), (23, 3, "stiffness_mass", "field"),
+                                        (12, 4, "stiffness_mass", "field")])
+def test_symmetric_kernels_repeat_bitwise(K, p, op, kind):
+    """The symmetric kernels hand rows between warp roles through mbarriers (k_gsf3_p3s: stages
+    A / B / S and the emitter warps) or CTA barriers (generic kernel): a missing wait would
+    show as run-to-run differences or as values left unwritten.  20 runs into a NaN-prefilled
+    target are bitwise equal to the first (the reference's reproducibility promise,
+    runtime.py:16-20)."""
+    import torch
+
+    import paper_2207_00280_b200 as pkg
+    from paper_2207_00280_b200.runtime import DeviceSession
+
+    q = p + 1
+    coef = None if kind == "scalar" else np.random.default_rng(7).uniform(0.5, 1.5, size=(K,) * 3 + (q,) * 3)
+    cfg = pkg.RunConfig("sumfact", "device", K, p, operator=op, coefficient=coef, dim=3, assembly="owner")
+    sess = DeviceSession(cfg, use_graph=False)
+    sess.step()
+    torch.cuda.synchronize()
+    first = sess.values.clone()
+    assert not torch.isnan(first).any()
+    for _ in range(20):
+        sess.values.fill_(float("nan"))
+        sess.step()
+        torch.cuda.synchronize()
+        assert torch.equal(sess.values.view(torch.int64), first.view(torch.int64))
