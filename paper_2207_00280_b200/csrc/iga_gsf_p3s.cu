@@ -424,20 +424,24 @@ __device__ __forceinline__ void stage_s_batch(const Lane& L, int ws, const doubl
 
 // axis-2 B fragments of element e2 (value and derivative pair products), for the first
 // element; later elements go through s_raw_load / s_raw_form below
-__device__ __forceinline__ void s_fragments(const Lane& L, const GsfArgs& a, int e2, double (&b0)[2],
+// (ws: the axis-2 weight w_k2 h_e2 / 2 times the Jacobian when the weights are folded into the
+// fragments, else 1 -- see `folded` in the kernel)
+template <bool FOLD>
+__device__ __forceinline__ void s_fragments(const Lane& L, const GsfArgs& a, int e2, double ws, double (&b0)[2],
                                             double (&b1)[2]) {
   const int g = L.g, t = L.t;
   const double* V2 = a.V + (int64_t)e2 * M * Q;
 #pragma unroll
   for (int nt = 0; nt < 2; ++nt) {
     const int r = bcol_r(nt, g), s = bcol_s(nt, g);
-    b0[nt] = __ldg(V2 + r * Q + t) * __ldg(V2 + s * Q + t);
+    const double vv = __ldg(V2 + r * Q + t) * __ldg(V2 + s * Q + t);
+    b0[nt] = FOLD ? vv * ws : vv;
     b1[nt] = 0.0;
     if (L.stiff) {
       const double* D2 = a.D + (int64_t)e2 * M * Q;
       double z = __ldg(D2 + r * Q + t) * __ldg(D2 + s * Q + t);
-      if (L.smass) z += b0[nt];
-      b1[nt] = z;
+      if (L.smass) z += vv;
+      b1[nt] = FOLD ? z * ws : z;
     }
   }
 }
@@ -446,9 +450,10 @@ __device__ __forceinline__ void s_fragments(const Lane& L, const GsfArgs& a, int
 // column e2-1 and their products formed at the start of column e2, so the global-load
 // latency is not waited on where it is issued (0.5223 -> 0.5205 ms on C3)
 struct SRaw {
-  double v[2][2], d[2][2];
+  double v[2][2], d[2][2], ws;
 };
-__device__ __forceinline__ void s_raw_load(const Lane& L, const GsfArgs& a, int e2, SRaw& w) {
+template <bool FOLD>
+__device__ __forceinline__ void s_raw_load(const Lane& L, const GsfArgs& a, int e2, double ws, SRaw& w) {
   const int g = L.g, t = L.t;
   const double* V2 = a.V + (int64_t)e2 * M * Q;
   const double* D2 = a.D + (int64_t)e2 * M * Q;
@@ -463,18 +468,53 @@ __device__ __forceinline__ void s_raw_load(const Lane& L, const GsfArgs& a, int 
       w.d[nt][1] = __ldg(D2 + s * Q + t);
     }
   }
+  if (FOLD) w.ws = ws;
 }
+template <bool FOLD>
 __device__ __forceinline__ void s_raw_form(const Lane& L, const SRaw& w, double (&b0)[2], double (&b1)[2]) {
 #pragma unroll
   for (int nt = 0; nt < 2; ++nt) {
-    b0[nt] = w.v[nt][0] * w.v[nt][1];
+    const double vv = w.v[nt][0] * w.v[nt][1];
+    b0[nt] = FOLD ? vv * w.ws : vv;
     b1[nt] = 0.0;
     if (L.stiff) {
       double z = w.d[nt][0] * w.d[nt][1];
-      if (L.smass) z += b0[nt];
-      b1[nt] = z;
+      if (L.smass) z += vv;
+      b1[nt] = FOLD ? z * w.ws : z;
     }
   }
+}
+
+// The coefficient field of element column e2 over the tile's window, copied asynchronously into
+// W (folded mode: W is the raw coefficient).  For fixed (la, k0, lb) the 16 values (k1, k2) are
+// contiguous in memory (128 aligned bytes) and in the W row; out-of-mesh / out-of-slab
+// elements are zero-filled (source size 0).
+__device__ __forceinline__ void copy_coef_column(double* W, const GsfArgs& a, int e2, int i00, int i10, int e0lo,
+                                                 int e0hi, int tid, int nt) {
+  const int K = a.K;
+  if (reinterpret_cast<uintptr_t>(a.coef) & 15) {  // a caller's 8-byte aligned field: word copies
+    for (int u = tid; u < LA * Q * LB * 16; u += nt) {
+      const int part = u & 15, seg = u >> 4, row = seg / LB, lb = seg - row * LB;
+      const int la = row >> 2, k0 = row & 3;
+      const int e0 = i00 - P + la, e1 = i10 - P + lb;
+      const bool ok = e0 >= e0lo && e0 < e0hi && e1 >= 0 && e1 < K;
+      const double* src = ok ? a.coef + (((int64_t)e0 * K + e1) * K + e2) * (Q * Q * Q) + k0 * (Q * Q) + part : a.coef;
+      const unsigned dst = smem_u32(W + row * WP + lb * (Q * Q) + part);
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(ok ? 8 : 0) : "memory");
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    return;
+  }
+  for (int u = tid; u < LA * Q * LB * 8; u += nt) {
+    const int part = u & 7, seg = u >> 3, row = seg / LB, lb = seg - row * LB;
+    const int la = row >> 2, k0 = row & 3;
+    const int e0 = i00 - P + la, e1 = i10 - P + lb;
+    const bool ok = e0 >= e0lo && e0 < e0hi && e1 >= 0 && e1 < K;
+    const double* src = ok ? a.coef + (((int64_t)e0 * K + e1) * K + e2) * (Q * Q * Q) + k0 * (Q * Q) + part * 2 : a.coef;
+    const unsigned dst = smem_u32(W + row * WP + lb * (Q * Q) + part * 2);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(ok ? 16 : 0) : "memory");
+  }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
 }
 
 template <int PHI>
@@ -516,7 +556,7 @@ __device__ __forceinline__ void flush_tail(const Lane& L, int ws, const double* 
 
 // W[(la,k0)][(g1,k2)] = c w0 w1 w2 jac on the CTA's quadrature slab of column e2
 __device__ __forceinline__ void form_w(double* W, const double* wq, const GsfArgs& a, int e2,
-                                       int i00, int i10, int e0lo, int e0hi, int tid, int nt) {
+                                       int i00, int i10, int e0lo, int e0hi, int tid, int nt, bool raw = false) {
   const int K = a.K;
   for (int u = tid; u < LA * Q * NCOL; u += nt) {
     const int row = u / NCOL, col = u - row * NCOL;
@@ -528,14 +568,18 @@ __device__ __forceinline__ void form_w(double* W, const double* wq, const GsfArg
       const double cf = a.coef ? __ldg(a.coef + (((int64_t)e0 * K + e1) * K + e2) * (Q * Q * Q) +
                                        (k0 * Q + k1) * Q + k2)
                                : a.coef_scalar;
-      w = axis_w(wq, a.wt, e0, k0, Q) * axis_w(wq, a.wt, e1, k1, Q) * axis_w(wq, a.wt, e2, k2, Q) *
-          a.jac * cf;
+      w = raw ? cf
+              : axis_w(wq, a.wt, e0, k0, Q) * axis_w(wq, a.wt, e1, k1, Q) * axis_w(wq, a.wt, e2, k2, Q) *
+                    a.jac * cf;
     }
     W[row * WP + col] = w;
   }
 }
 
 
+// FOLD: the axis weights live in the fragments and W is the raw coefficient (see `folded`
+// below); the launcher picks it for a coefficient field or a general knot vector
+template <bool FOLD>
 __global__ void __launch_bounds__(NT, 1) k_gsf3_p3s(GsfArgs a) {
   extern __shared__ double sm[];
   const int tid = threadIdx.x, warp = tid >> 5;
@@ -564,6 +608,7 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3s(GsfArgs a) {
     if (e0 >= 0 && e0 < K && (type == 0 || L.stiff)) {
       const double* T = (type == 0 ? a.V : a.D) + (int64_t)e0 * M * Q;
       v = T[r * Q + tt] * T[sc * Q + tt];
+      if (FOLD) v *= axis_w(a.weights, a.wt, e0, tt, Q);
     }
     BA[u] = v;
   }
@@ -575,6 +620,7 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3s(GsfArgs a) {
     if (e1 >= 0 && e1 < K && (prod == 0 || L.stiff)) {
       const double* T = (prod == 0 ? a.V : a.D) + (int64_t)e1 * M * Q;
       v = T[r * Q + tt] * T[sc * Q + tt];
+      if (FOLD) v *= axis_w(a.weights, a.wt, e1, tt, Q);
     }
     BB[u] = v;
   }
@@ -607,9 +653,16 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3s(GsfArgs a) {
     pc[tid] = (I0 < N && I1 < N) ? (int)(band_cnt(I0, P, N) * band_cnt(I1, P, N)) : 0;
   }
   __syncthreads();
-  // step-invariant for a scalar coefficient on the uniform mesh
-  const bool w_per_step = a.coef != nullptr || a.wt != nullptr;
-  if (!w_per_step) form_w(W, wq, a, 0, i00, i10, e0lo, e0hi, tid, NT);
+  // Scalar coefficient on the uniform mesh: W = c w0 w1 w2 jac (the reference's factor order)
+  // is the same for every element column and formed once.  Otherwise (`folded`: a coefficient
+  // field, or per-element weights of a general knot vector) the axis weights go into the
+  // constant fragments -- w0 into stage A's, w1 into stage B's, w2 jac into stage S's per
+  // column -- and W is the raw coefficient: a constant for a scalar, else copied a column
+  // ahead by the A warps with cp.async (no per-column weight pass on their critical path:
+  // a coefficient field used to run the C3 shape in 2.24 ms against 0.43 for a scalar).
+  constexpr bool folded = FOLD;
+  const bool w_per_step = FOLD && a.coef != nullptr;
+  if (!w_per_step) form_w(W, wq, a, 0, i00, i10, e0lo, e0hi, tid, NT, folded);
   __syncthreads();
 
   // pipeline: A on element column it, B on it-1, S on it-2, handed over by mbarriers
@@ -624,19 +677,23 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3s(GsfArgs a) {
     for (int i = 0; i < NPA; ++i) ba[i] = BA[(ty * LA + pa_la(i)) * 32 + L.lane];
     const int mt0 = L.stiff ? (wa >> 1) : wa, mstep = L.stiff ? NWA / 2 : NWA;
     __syncthreads();  // every role holds its fragments before Y buffer 1 is written
+    if (w_per_step) copy_coef_column(W, a, 0, i00, i10, e0lo, e0hi, tid, NWA * 32);
     for (int it = 0; it < K; ++it) {
-      if (w_per_step) {
-        if (it > 0) asm volatile("bar.sync 1, %0;\n" ::"n"(NWA * 32));  // W of it-1 consumed
-        form_w(W, wq, a, it, i00, i10, e0lo, e0hi, tid, NWA * 32);
-        asm volatile("bar.sync 1, %0;\n" ::"n"(NWA * 32));
-      }
       const int b = it & 1;
       if (it >= 2) mbar_wait(xempty + b, ((it >> 1) - 1) & 1);
+      if (w_per_step) {  // this column's coefficients have landed, for every A warp
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
+        asm volatile("bar.sync 1, %0;\n" ::"n"(NWA * 32));
+      }
       double* X = sm + OFF_X + b * SZ_X;
       int mt = mt0;
       for (; mt + mstep < MT_A; mt += 2 * mstep) stage_a_units<2>(L, W, ba, X, mt, mstep, ty);
       if (mt < MT_A) stage_a_units<1>(L, W, ba, X, mt, mstep, ty);
       mbar_arrive(xfull + b);
+      if (w_per_step && it + 1 < K) {  // W consumed by every A warp: the next column's copy starts
+        asm volatile("bar.sync 1, %0;\n" ::"n"(NWA * 32));
+        copy_coef_column(W, a, it + 1, i00, i10, e0lo, e0hi, tid, NWA * 32);
+      }
     }
   } else if (warp < NWA + NWB) {
     // ------------------------------------------------------------ role B
@@ -731,21 +788,21 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3s(GsfArgs a) {
     double* Rs = sm + OFF_R;
     for (int u = ws * 32 + L.lane; u < MT_S * 4 * 2 * 32; u += NWS * 32) Rs[u] = 0.0;
     double sb0[2], sb1[2];
-    s_fragments(L, a, 0, sb0, sb1);
+    s_fragments<FOLD>(L, a, 0, FOLD ? axis_w(wq, a.wt, 0, L.t, Q) * a.jac : 1.0, sb0, sb1);
     SRaw sraw;
     __syncthreads();
     for (int e2 = 0; e2 < K; ++e2) {
       const int b = e2 & 1;
       mbar_wait(yfull + b, (e2 >> 1) & 1);
       const double* Y = sm + OFF_Y + b * SZ_Y;
-      if (e2 > 0) s_raw_form(L, sraw, sb0, sb1);
+      if (e2 > 0) s_raw_form<FOLD>(L, sraw, sb0, sb1);
       switch (e2 & 3) {
         case 0: stage_s<0>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1, rgw); break;
         case 1: stage_s<1>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1, rgw); break;
         case 2: stage_s<2>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1, rgw); break;
         default: stage_s<3>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1, rgw); break;
       }
-      if (e2 + 1 < K) s_raw_load(L, a, e2 + 1, sraw);
+      if (e2 + 1 < K) s_raw_load<FOLD>(L, a, e2 + 1, FOLD ? axis_w(wq, a.wt, e2 + 1, L.t, Q) * a.jac : 1.0, sraw);
       mbar_arrive(yempty + b);
       mbar_arrive(rfull + b);  // role E writes the mirrored runs this row completes
     }
@@ -768,9 +825,12 @@ int launch_gsf_p3s(const GsfArgs& a0, cudaStream_t s) {
   const int tiles0 = (planes + p3s::TA - 1) / p3s::TA;
   a.tiles1 = (int)((N + p3s::TB - 1) / p3s::TB);
   const int64_t grid = (int64_t)tiles0 * a.tiles1;
-  cudaError_t e = smem_attr_once(reinterpret_cast<const void*>(p3s::k_gsf3_p3s), p3s::SMEM_BYTES);
+  const bool fold = a.coef != nullptr || a.wt != nullptr;
+  cudaError_t e = smem_attr_once(reinterpret_cast<const void*>(fold ? p3s::k_gsf3_p3s<true> : p3s::k_gsf3_p3s<false>),
+                                 p3s::SMEM_BYTES);
   if (e != cudaSuccess) return check_cuda(e, "gsf_p3 smem attr");
-  p3s::k_gsf3_p3s<<<(unsigned)grid, p3s::NT, p3s::SMEM_BYTES, s>>>(a);
+  if (fold) p3s::k_gsf3_p3s<true><<<(unsigned)grid, p3s::NT, p3s::SMEM_BYTES, s>>>(a);
+  else p3s::k_gsf3_p3s<false><<<(unsigned)grid, p3s::NT, p3s::SMEM_BYTES, s>>>(a);
   return check_cuda(cudaGetLastError(), "gsf_p3 launch");
 }
 
