@@ -36,6 +36,10 @@ WORKLOADS = {
     "c3": dict(dim=3, K=64, p=3, op="stiffness", coef=None, method="sumfact",
                desc="C3: 3D Laplace stiffness 64^3 p=3 q=4 c=1, sum factorization fused with "
                     "CSR assembly"),
+    "c3f": dict(dim=3, K=64, p=3, op="stiffness", coef="uniform", method="sumfact",
+                desc="C3 mesh with a per-quadrature-point coefficient: 3D stiffness 64^3 p=3 q=4, "
+                     "coefficient U[0.5,1.5] seed 42 (the general path of the headline kernel with "
+                     "an actual field), sum factorization fused with CSR assembly"),
     "c4": dict(dim=3, K=96, p=4, op="stiffness_mass", coef="sines", method="sumfact",
                desc="C4: 3D stiffness+mass 96^3 p=4 q=5, smooth 8-mode sine coefficient, "
                     "assembled sum factorization"),
@@ -281,6 +285,9 @@ def kernel_roofline(code, wl, K, p, q, k_el, by, kern_ms, peaks):
         name = ("k_gsf3_p3s (symmetric assembled sum factorization on DMMA: J0 >= I0 computed, "
                 "the rest mirrored through per-warp rings; general per-quadrature-point "
                 "coefficient path)")
+        if wl.get("coef") is not None:
+            name = name.replace("k_gsf3_p3s (", "k_gsf3_p3s<FOLD> (coefficient field copied per element "
+                                "column with cp.async, weights folded into the fragments; ")
     elif code == 2:
         name = name.replace("k_gsf3", "k_gsf3_p3")
     roof.update({

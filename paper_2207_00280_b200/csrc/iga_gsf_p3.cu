@@ -396,20 +396,25 @@ __device__ __forceinline__ void stage_s_batch(const Lane& L, int ws, const doubl
 
 // axis-2 B fragments of element e2 (value and derivative pair products), for the first
 // element; later elements go through s_raw_load / s_raw_form below
-__device__ __forceinline__ void s_fragments(const Lane& L, const GsfArgs& a, int e2, double (&b0)[2],
+// (FOLD: the axis weights live in the fragments -- ws = w_k2 h_e2 / 2 times the Jacobian
+// here -- and W is the raw coefficient; the same arithmetic as k_gsf3_p3s<FOLD>, so slab rows
+// stay bitwise equal to the whole-mesh rows)
+template <bool FOLD>
+__device__ __forceinline__ void s_fragments(const Lane& L, const GsfArgs& a, int e2, double ws, double (&b0)[2],
                                             double (&b1)[2]) {
   const int g = L.g, t = L.t;
   const double* V2 = a.V + (int64_t)e2 * M * Q;
 #pragma unroll
   for (int nt = 0; nt < 2; ++nt) {
     const int r = bcol_r(nt, g), s = bcol_s(nt, g);
-    b0[nt] = __ldg(V2 + r * Q + t) * __ldg(V2 + s * Q + t);
+    const double vv = __ldg(V2 + r * Q + t) * __ldg(V2 + s * Q + t);
+    b0[nt] = FOLD ? vv * ws : vv;
     b1[nt] = 0.0;
     if (L.stiff) {
       const double* D2 = a.D + (int64_t)e2 * M * Q;
       double z = __ldg(D2 + r * Q + t) * __ldg(D2 + s * Q + t);
-      if (L.smass) z += b0[nt];
-      b1[nt] = z;
+      if (L.smass) z += vv;
+      b1[nt] = FOLD ? z * ws : z;
     }
   }
 }
@@ -418,9 +423,10 @@ __device__ __forceinline__ void s_fragments(const Lane& L, const GsfArgs& a, int
 // column e2-1 and their products formed at the start of column e2, so the global-load
 // latency is not waited on where it is issued (0.5223 -> 0.5205 ms on C3)
 struct SRaw {
-  double v[2][2], d[2][2];
+  double v[2][2], d[2][2], ws;
 };
-__device__ __forceinline__ void s_raw_load(const Lane& L, const GsfArgs& a, int e2, SRaw& w) {
+template <bool FOLD>
+__device__ __forceinline__ void s_raw_load(const Lane& L, const GsfArgs& a, int e2, double ws, SRaw& w) {
   const int g = L.g, t = L.t;
   const double* V2 = a.V + (int64_t)e2 * M * Q;
   const double* D2 = a.D + (int64_t)e2 * M * Q;
@@ -435,16 +441,19 @@ __device__ __forceinline__ void s_raw_load(const Lane& L, const GsfArgs& a, int 
       w.d[nt][1] = __ldg(D2 + s * Q + t);
     }
   }
+  if (FOLD) w.ws = ws;
 }
+template <bool FOLD>
 __device__ __forceinline__ void s_raw_form(const Lane& L, const SRaw& w, double (&b0)[2], double (&b1)[2]) {
 #pragma unroll
   for (int nt = 0; nt < 2; ++nt) {
-    b0[nt] = w.v[nt][0] * w.v[nt][1];
+    const double vv = w.v[nt][0] * w.v[nt][1];
+    b0[nt] = FOLD ? vv * w.ws : vv;
     b1[nt] = 0.0;
     if (L.stiff) {
       double z = w.d[nt][0] * w.d[nt][1];
-      if (L.smass) z += b0[nt];
-      b1[nt] = z;
+      if (L.smass) z += vv;
+      b1[nt] = FOLD ? z * w.ws : z;
     }
   }
 }
@@ -483,7 +492,7 @@ __device__ __forceinline__ void flush_tail(const Lane& L, int ws, const double* 
 
 // W[(la,k0)][(g1,k2)] = c w0 w1 w2 jac on the CTA's quadrature slab of column e2
 __device__ __forceinline__ void form_w(double* W, const double* wq, const GsfArgs& a, int e2,
-                                       int i00, int i10, int e0lo, int e0hi, int tid, int nt) {
+                                       int i00, int i10, int e0lo, int e0hi, int tid, int nt, bool raw = false) {
   const int K = a.K;
   for (int u = tid; u < LA * Q * NCOL; u += nt) {
     const int row = u / NCOL, col = u - row * NCOL;
@@ -495,11 +504,35 @@ __device__ __forceinline__ void form_w(double* W, const double* wq, const GsfArg
       const double cf = a.coef ? __ldg(a.coef + (((int64_t)e0 * K + e1) * K + e2) * (Q * Q * Q) +
                                        (k0 * Q + k1) * Q + k2)
                                : a.coef_scalar;
-      w = axis_w(wq, a.wt, e0, k0, Q) * axis_w(wq, a.wt, e1, k1, Q) * axis_w(wq, a.wt, e2, k2, Q) *
-          a.jac * cf;
+      w = raw ? cf
+              : axis_w(wq, a.wt, e0, k0, Q) * axis_w(wq, a.wt, e1, k1, Q) * axis_w(wq, a.wt, e2, k2, Q) *
+                    a.jac * cf;
     }
     W[row * WP + col] = w;
   }
+}
+
+// The coefficient field of element column e2 over the tile's window, copied asynchronously into
+// W (FOLD: W is the raw coefficient).  For fixed (la, k0, lb) the 16 values (k1, k2) are
+// contiguous in memory and in the W row; out-of-mesh / out-of-slab elements are zero-filled.
+__device__ __forceinline__ void copy_coef_column(double* W, const GsfArgs& a, int e2, int i00, int i10, int e0lo,
+                                                 int e0hi, int tid, int nt) {
+  const int K = a.K;
+  const bool al16 = (reinterpret_cast<uintptr_t>(a.coef) & 15) == 0;  // else 8-byte word copies
+  const int np = al16 ? 8 : 16, wd = al16 ? 2 : 1;
+  for (int u = tid; u < LA * Q * LB * np; u += nt) {
+    const int part = u % np, seg = u / np, row = seg / LB, lb = seg - row * LB;
+    const int la = row >> 2, k0 = row & 3;
+    const int e0 = i00 - P + la, e1 = i10 - P + lb;
+    const bool ok = e0 >= e0lo && e0 < e0hi && e1 >= 0 && e1 < K;
+    const double* src = ok ? a.coef + (((int64_t)e0 * K + e1) * K + e2) * (Q * Q * Q) + k0 * (Q * Q) + part * wd : a.coef;
+    const unsigned dst = (unsigned)__cvta_generic_to_shared(W + row * WP + lb * (Q * Q) + part * wd);
+    if (al16)
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(ok ? 16 : 0) : "memory");
+    else
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(ok ? 8 : 0) : "memory");
+  }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
 }
 
 #ifdef IGA_PHASE_TIMING
@@ -512,6 +545,7 @@ __device__ long long g_phase[4][NT / 32][3];
 #define PT(idx)
 #endif
 
+template <bool FOLD>
 __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
   extern __shared__ double sm[];
   const int tid = threadIdx.x, warp = tid >> 5;
@@ -540,6 +574,7 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
     if (e0 >= 0 && e0 < K && (type == 0 || L.stiff)) {
       const double* T = (type == 0 ? a.V : a.D) + (int64_t)e0 * M * Q;
       v = T[r * Q + tt] * T[sc * Q + tt];
+      if (FOLD) v *= axis_w(a.weights, a.wt, e0, tt, Q);
     }
     BA[u] = v;
   }
@@ -551,6 +586,7 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
     if (e1 >= 0 && e1 < K && (prod == 0 || L.stiff)) {
       const double* T = (prod == 0 ? a.V : a.D) + (int64_t)e1 * M * Q;
       v = T[r * Q + tt] * T[sc * Q + tt];
+      if (FOLD) v *= axis_w(a.weights, a.wt, e1, tt, Q);
     }
     BB[u] = v;
   }
@@ -576,9 +612,13 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
     pc[tid] = (I0 < N && I1 < N) ? (int)(band_cnt(I0, P, N) * band_cnt(I1, P, N)) : 0;
   }
   __syncthreads();
-  // step-invariant for a scalar coefficient on the uniform mesh
-  const bool w_per_step = a.coef != nullptr || a.wt != nullptr;
-  if (!w_per_step) form_w(W, wq, a, 0, i00, i10, e0lo, e0hi, tid, NT);
+  // Scalar coefficient on the uniform mesh: W = c w0 w1 w2 jac, formed once.  FOLD (a
+  // coefficient field or a general knot vector): the weights are in the fragments and W is
+  // the raw coefficient -- a constant for a scalar, else copied per element column with
+  // cp.async after the A warps are done with the previous one (iga_gsf_p3s.cu has the
+  // double-buffered version).
+  const bool w_per_step = FOLD && a.coef != nullptr;
+  if (!w_per_step) form_w(W, wq, a, 0, i00, i10, e0lo, e0hi, tid, NT, FOLD);
   __syncthreads();
 
   // pipeline: A on element column it, B on it-1, S on it-2, handed over by mbarriers
@@ -593,11 +633,15 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
     for (int i = 0; i < NPA; ++i) ba[i] = BA[(ty * LA + pa_la(i)) * 32 + L.lane];
     const int mt0 = L.stiff ? (wa >> 1) : wa, mstep = L.stiff ? NWA / 2 : NWA;
     __syncthreads();  // every role holds its fragments before Y buffer 1 is written
+    if (w_per_step) copy_coef_column(W, a, 0, i00, i10, e0lo, e0hi, tid, NWA * 32);
     for (int it = 0; it < K; ++it) {
       PT(2);
       if (w_per_step) {
-        if (it > 0) asm volatile("bar.sync 1, %0;\n" ::"n"(NWA * 32));  // W of it-1 consumed
-        form_w(W, wq, a, it, i00, i10, e0lo, e0hi, tid, NWA * 32);
+        if (it > 0) {  // W of it-1 consumed by every A warp: this column's copy starts
+          asm volatile("bar.sync 1, %0;\n" ::"n"(NWA * 32));
+          copy_coef_column(W, a, it, i00, i10, e0lo, e0hi, tid, NWA * 32);
+        }
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
         asm volatile("bar.sync 1, %0;\n" ::"n"(NWA * 32));
       }
       const int b = it & 1;
@@ -664,7 +708,7 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
     double* Rs = sm + OFF_R;
     for (int u = ws * 32 + L.lane; u < MT_S * 4 * 2 * 32; u += NWS * 32) Rs[u] = 0.0;
     double sb0[2], sb1[2];
-    s_fragments(L, a, 0, sb0, sb1);
+    s_fragments<FOLD>(L, a, 0, FOLD ? axis_w(wq, a.wt, 0, L.t, Q) * a.jac : 1.0, sb0, sb1);
     SRaw sraw;
     __syncthreads();
     for (int e2 = 0; e2 < K; ++e2) {
@@ -674,7 +718,7 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
       mbar_wait(yfull + b, (e2 >> 1) & 1);
       PT(1);
       const double* Y = sm + OFF_Y + b * SZ_Y;
-      if (e2 > 0) s_raw_form(L, sraw, sb0, sb1);
+      if (e2 > 0) s_raw_form<FOLD>(L, sraw, sb0, sb1);
 #ifdef P3_ABL_NOS
       if (e2 < 0)
 #endif
@@ -684,7 +728,7 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
         case 2: stage_s<2>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1); break;
         default: stage_s<3>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1); break;
       }
-      if (e2 + 1 < K) s_raw_load(L, a, e2 + 1, sraw);
+      if (e2 + 1 < K) s_raw_load<FOLD>(L, a, e2 + 1, FOLD ? axis_w(wq, a.wt, e2 + 1, L.t, Q) * a.jac : 1.0, sraw);
       mbar_arrive(yempty + b);
       PT(0);
     }
@@ -703,9 +747,12 @@ int launch_gsf_p3(const GsfArgs& a0, cudaStream_t s) {
   const int tiles0 = (planes + p3::TA - 1) / p3::TA;
   a.tiles1 = (int)((N + p3::TB - 1) / p3::TB);
   const int64_t grid = (int64_t)tiles0 * a.tiles1;
-  cudaError_t e = smem_attr_once(reinterpret_cast<const void*>(p3::k_gsf3_p3), p3::SMEM_BYTES);
+  const bool fold = a.coef != nullptr || a.wt != nullptr;
+  cudaError_t e = smem_attr_once(reinterpret_cast<const void*>(fold ? p3::k_gsf3_p3<true> : p3::k_gsf3_p3<false>),
+                                 p3::SMEM_BYTES);
   if (e != cudaSuccess) return check_cuda(e, "gsf_p3 smem attr");
-  p3::k_gsf3_p3<<<(unsigned)grid, p3::NT, p3::SMEM_BYTES, s>>>(a);
+  if (fold) p3::k_gsf3_p3<true><<<(unsigned)grid, p3::NT, p3::SMEM_BYTES, s>>>(a);
+  else p3::k_gsf3_p3<false><<<(unsigned)grid, p3::NT, p3::SMEM_BYTES, s>>>(a);
   return check_cuda(cudaGetLastError(), "gsf_p3 launch");
 }
 

@@ -90,15 +90,23 @@ constexpr int OFF_MM = OFF_R + MT_S * 4 * 2 * 32;  // [NRC][2]
 // axis-2 band table {band_prefix(I2), band_cnt(I2)} for meshes with N <= NBT rows (else computed)
 constexpr int NBT = 512;
 constexpr int OFF_BT = OFF_MM + NRC * 2;  // int2 [NBT]
-// per ring combo: the mirrored values by target row J2 -- hi runs [J2 mod 8][d2' 0..3], lo runs
-// [J2 mod 4][d2' 4..6] -- so they leave as contiguous runs.  The slot counts let the S warps
-// run a whole element column ahead of the emitters (ring_put / role E below).
-constexpr int RING_LO = 32, RING = RING_LO + 12;
-constexpr int OFF_RING = OFF_BT + NBT;     // [NRC][RING]
-constexpr int OFF_MB = OFF_RING + NRC * RING;  // mbarriers
-constexpr int SMEM_DOUBLES = OFF_MB + 12;
-static_assert(SMEM_DOUBLES * 8 <= 227 * 1024, "shared memory budget");
-constexpr size_t SMEM_BYTES = SMEM_DOUBLES * sizeof(double);
+constexpr int OFF_MB = OFF_BT + NBT;       // mbarriers
+constexpr int OFF_RING = OFF_MB + 12;      // [NRC][RING]
+// per ring combo: the mirrored values by target row J2 -- hi runs [J2 mod HS][d2' 0..3], lo runs
+// [J2 mod 4][d2' 4..6] -- so they leave as contiguous runs.  HS = 8 hi slots let the S warps
+// run two rows ahead of the emitters (LAG; ring_put / role E below).  The folded kernel
+// (FOLD, coefficient fields) keeps 4 and one row, and spends the shared memory on a second
+// W buffer, so the next element column's coefficients are copied while this one is used.
+template <bool FOLD>
+struct Rg {
+  static constexpr int HS = FOLD ? 4 : 8, LAG = FOLD ? 1 : 2;
+  static constexpr int LO = HS * 4, RING = LO + 12;
+  static constexpr int OFF_W2 = OFF_RING + NRC * RING;  // second W buffer (FOLD)
+  static constexpr int SMEM_DOUBLES = FOLD ? OFF_W2 + LA * Q * WP : OFF_W2;
+  static_assert(SMEM_DOUBLES * 8 <= 227 * 1024, "shared memory budget");
+  static_assert(OFF_W2 % 2 == 0, "16-byte aligned cp.async destinations");
+  static constexpr size_t SMEM_BYTES = SMEM_DOUBLES * sizeof(double);
+};
 
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b, double c0,
                                      double c1) {
@@ -334,10 +342,12 @@ __device__ __forceinline__ void store_pair(const GsfArgs& a, int m, const int64_
 // The hi slot was last read for target J2 - 8, emitted with row J2 - 8 <= I2 - 5; the lo slot
 // for target J2 - 4, emitted with row J2 - 1 <= I2 - 2: row I2's values may be put once the
 // emitters are done with row I2 - 2.
+template <bool FOLD>
 __device__ __forceinline__ void ring_put(double* rg, int i, int g, int t, int I2, double hi, double lo) {
-  double* r = rg + (i * 8 + g) * RING;
-  r[((I2 + t) & 7) * 4 + (3 - t)] = hi;
-  if (t > 0) r[RING_LO + ((I2 + t) & 3) * 3 + (3 - t)] = lo;
+  using G = Rg<FOLD>;
+  double* r = rg + (i * 8 + g) * G::RING;
+  r[((I2 + t) & (G::HS - 1)) * 4 + (3 - t)] = hi;
+  if (t > 0) r[G::LO + ((I2 + t) & 3) * 3 + (3 - t)] = lo;
 }
 
 // Target row J2's complete runs, written by the emitter warps (role E): hi (d2' = t) or lo
@@ -351,25 +361,26 @@ struct EMeta {
   double* row[ENJ];  // values + CSR base of the target pencil
   int cx[ENJ], cy[ENJ];
 };
-template <bool HI>
+template <bool HI, bool FOLD>
 __device__ __forceinline__ void emit_all(const GsfArgs& a, const double* sm, const EMeta& em, int et, int J2,
                                          int64_t N) {
   const int2 b = band_of(reinterpret_cast<const int2*>(sm + OFF_BT), J2, N);
   const int t = et & 3;
   const int off = (HI ? t : 4 + t) - max(0, P - J2);
   const bool ok = (HI || t < 3) && off >= 0 && off < b.y;
-  const double* r = sm + OFF_RING + (et >> 2) * RING +
-                    (HI ? (J2 & 7) * 4 + t : RING_LO + (J2 & 3) * 3 + (t < 3 ? t : 0));
+  using G = Rg<FOLD>;
+  const double* r = sm + OFF_RING + (et >> 2) * G::RING +
+                    (HI ? (J2 & (G::HS - 1)) * 4 + t : G::LO + (J2 & 3) * 3 + (t < 3 ? t : 0));
   double v[ENJ];
 #pragma unroll
-  for (int j = 0; j < ENJ; ++j) v[j] = em.cy[j] >= 0 ? r[j * ENG * RING] : 0.0;
+  for (int j = 0; j < ENJ; ++j) v[j] = em.cy[j] >= 0 ? r[j * ENG * G::RING] : 0.0;
   // offsets within a pencil fit 32 bits: c0 c1 band_prefix(J2) + (block) band_cnt(J2) + off < 343 N
 #pragma unroll
   for (int j = 0; j < ENJ; ++j)
     if (ok && em.cy[j] >= 0) em.row[j][em.cx[j] * b.x + em.cy[j] * b.y + off] = v[j];
 }
 
-template <int PHI, int I0, int NM>
+template <int PHI, int I0, int NM, bool FOLD>
 __device__ __forceinline__ void stage_s_batch(const Lane& L, int ws, const double* Y, double* Rs,
                                               const double (&b0)[2], const double (&b1)[2],
                                               const int (&meta)[MT_S_PER_WARP], const int64_t* pb,
@@ -380,7 +391,7 @@ __device__ __forceinline__ void stage_s_batch(const Lane& L, int ws, const doubl
   int p[NM][2][2];
   if (MT_S % NWS != 0 && ws + (I0 + NM - 1) * NWS >= MT_S) {
     // uneven split: the last m-tile of this batch does not exist for this warp
-    if constexpr (NM > 1) stage_s_batch<PHI, I0, NM - 1>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd, rg, e2);
+    if constexpr (NM > 1) stage_s_batch<PHI, I0, NM - 1, FOLD>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd, rg, e2);
     return;
   }
 #pragma unroll
@@ -410,15 +421,16 @@ __device__ __forceinline__ void stage_s_batch(const Lane& L, int ws, const doubl
       for (int nt = 0; nt < 2; ++nt)
         dmma(cc[i][nt][0], cc[i][nt][1], a1[i], b1[nt], cc[i][nt][0], cc[i][nt][1]);
   }
-  // the emitters are done with row e2 - 2 (ring_put): its slots are reused from here on
-  if (I0 == 0 && e2 >= 2)
-    mbar_wait(reinterpret_cast<uint64_t*>(Rs - OFF_R + OFF_MB) + 10 + (e2 & 1), ((e2 >> 1) - 1) & 1);
+  // the emitters are done with row e2 - LAG (ring_put): its slots are reused from here on
+  constexpr int LAG = Rg<FOLD>::LAG;
+  if (I0 == 0 && e2 >= LAG)
+    mbar_wait(reinterpret_cast<uint64_t*>(Rs - OFF_R + OFF_MB) + 10 + ((e2 - LAG) & 1), ((e2 - LAG) >> 1) & 1);
 #pragma unroll
   for (int i = 0; i < NM; ++i) {
 #pragma unroll
     for (int k = 1; k < 4; ++k) Rs[p[i][k >> 1][k & 1]] = cc[i][k >> 1][k & 1];
     store_pair(a, meta[I0 + i], pb, pc, rd, cc[i][0][0], lo[i]);
-    ring_put(rg, I0 + i, g, t, e2, cc[i][0][0], lo[i]);
+    ring_put<FOLD>(rg, I0 + i, g, t, e2, cc[i][0][0], lo[i]);
   }
 }
 
@@ -517,7 +529,7 @@ __device__ __forceinline__ void copy_coef_column(double* W, const GsfArgs& a, in
   asm volatile("cp.async.commit_group;\n" ::: "memory");
 }
 
-template <int PHI>
+template <int PHI, bool FOLD>
 __device__ __forceinline__ void stage_s(const Lane& L, int ws, const double* Y, double* Rs,
                                         const GsfArgs& a, int e2, const int (&meta)[MT_S_PER_WARP],
                                         const int64_t* pb, const int* pc, int64_t N,
@@ -531,12 +543,13 @@ __device__ __forceinline__ void stage_s(const Lane& L, int ws, const double* Y, 
   constexpr int B1 = R1 <= 4 ? R1 : (R1 + 1) / 2;
   constexpr int B2 = R1 - B1;
   static_assert(B2 <= 4, "stage S batches");
-  stage_s_batch<PHI, 0, B0>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd, rg, e2);
-  if constexpr (B1 > 0) stage_s_batch<PHI, B0, B1>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd, rg, e2);
-  if constexpr (B2 > 0) stage_s_batch<PHI, B0 + B1, B2>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd, rg, e2);
+  stage_s_batch<PHI, 0, B0, FOLD>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd, rg, e2);
+  if constexpr (B1 > 0) stage_s_batch<PHI, B0, B1, FOLD>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd, rg, e2);
+  if constexpr (B2 > 0) stage_s_batch<PHI, B0 + B1, B2, FOLD>(L, ws, Y, Rs, b0, b1, meta, pb, pc, a, rd, rg, e2);
 }
 
 // Rows K .. K+P-1 (no element e2 = I2): both groups are complete in their slots.
+template <bool FOLD>
 __device__ __forceinline__ void flush_tail(const Lane& L, int ws, const double* Rs, int I2,
                                            const int (&meta)[MT_S_PER_WARP], const int64_t* pb,
                                            const int* pc, const GsfArgs& a, int64_t N, double* rg) {
@@ -549,7 +562,7 @@ __device__ __forceinline__ void flush_tail(const Lane& L, int ws, const double* 
     if (mt < MT_S) {
       const double hi = Rs[rs_idx(mt, sl, 0, L.lane)], lo = Rs[rs_idx(mt, sl, 1, L.lane)];
       store_pair(a, meta[i], pb, pc, rd, hi, lo);
-      ring_put(rg, i, L.g, L.t, I2, hi, lo);
+      ring_put<FOLD>(rg, i, L.g, L.t, I2, hi, lo);
     }
   }
 }
@@ -677,23 +690,25 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3s(GsfArgs a) {
     for (int i = 0; i < NPA; ++i) ba[i] = BA[(ty * LA + pa_la(i)) * 32 + L.lane];
     const int mt0 = L.stiff ? (wa >> 1) : wa, mstep = L.stiff ? NWA / 2 : NWA;
     __syncthreads();  // every role holds its fragments before Y buffer 1 is written
+    // coefficient field: W is double-buffered, column it + 1 is copied while it is used
+    double* W2 = sm + Rg<FOLD>::OFF_W2;
     if (w_per_step) copy_coef_column(W, a, 0, i00, i10, e0lo, e0hi, tid, NWA * 32);
     for (int it = 0; it < K; ++it) {
       const int b = it & 1;
-      if (it >= 2) mbar_wait(xempty + b, ((it >> 1) - 1) & 1);
-      if (w_per_step) {  // this column's coefficients have landed, for every A warp
+      if (w_per_step) {
+        // this column's coefficients have landed, for every A warp, and every A warp is done
+        // with the other buffer (column it - 1): the next column's copy starts
         asm volatile("cp.async.wait_all;\n" ::: "memory");
         asm volatile("bar.sync 1, %0;\n" ::"n"(NWA * 32));
+        if (it + 1 < K) copy_coef_column(b ? W : W2, a, it + 1, i00, i10, e0lo, e0hi, tid, NWA * 32);
       }
+      const double* Wc = (w_per_step && b) ? W2 : W;
+      if (it >= 2) mbar_wait(xempty + b, ((it >> 1) - 1) & 1);
       double* X = sm + OFF_X + b * SZ_X;
       int mt = mt0;
-      for (; mt + mstep < MT_A; mt += 2 * mstep) stage_a_units<2>(L, W, ba, X, mt, mstep, ty);
-      if (mt < MT_A) stage_a_units<1>(L, W, ba, X, mt, mstep, ty);
+      for (; mt + mstep < MT_A; mt += 2 * mstep) stage_a_units<2>(L, Wc, ba, X, mt, mstep, ty);
+      if (mt < MT_A) stage_a_units<1>(L, Wc, ba, X, mt, mstep, ty);
       mbar_arrive(xfull + b);
-      if (w_per_step && it + 1 < K) {  // W consumed by every A warp: the next column's copy starts
-        asm volatile("bar.sync 1, %0;\n" ::"n"(NWA * 32));
-        copy_coef_column(W, a, it + 1, i00, i10, e0lo, e0hi, tid, NWA * 32);
-      }
     }
   } else if (warp < NWA + NWB) {
     // ------------------------------------------------------------ role B
@@ -734,12 +749,12 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3s(GsfArgs a) {
     }
     for (int e2 = 0; e2 < N; ++e2) {
       mbar_wait(rfull + (e2 & 1), (e2 >> 1) & 1);
-      emit_all<true>(a, sm, em, et, e2, N);
-      if (e2 >= 3) emit_all<false>(a, sm, em, et, e2 - 3, N);
+      emit_all<true, FOLD>(a, sm, em, et, e2, N);
+      if (e2 >= 3) emit_all<false, FOLD>(a, sm, em, et, e2 - 3, N);
       mbar_arrive(rfree + (e2 & 1));
     }
     // lo runs of the last three target rows (their later sources do not exist)
-    for (int J2 = max(0, (int)N - 3); J2 < N; ++J2) emit_all<false>(a, sm, em, et, J2, N);
+    for (int J2 = max(0, (int)N - 3); J2 < N; ++J2) emit_all<false, FOLD>(a, sm, em, et, J2, N);
   } else {
     // ------------------------------------------------------------ role S
     const int ws = warp - NWA - NWB;
@@ -747,7 +762,7 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3s(GsfArgs a) {
     // b01 = (d0-lo0)*c1 + (d1-lo1) in the CSR row; -1 if the combo is outside
     int meta[MT_S_PER_WARP];
     double* mmw = sm + OFF_MM + 2 * (ws * MT_S_PER_WARP * 8 + L.g);  // its lane groups' mirror metadata
-    double* rgw = sm + OFF_RING + ws * MT_S_PER_WARP * 8 * RING;     // this warp's rings
+    double* rgw = sm + OFF_RING + ws * MT_S_PER_WARP * 8 * Rg<FOLD>::RING;  // this warp's rings
 #pragma unroll
     for (int i = 0; i < MT_S_PER_WARP; ++i) {
       const int mt = ws + i * NWS;
@@ -797,10 +812,10 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3s(GsfArgs a) {
       const double* Y = sm + OFF_Y + b * SZ_Y;
       if (e2 > 0) s_raw_form<FOLD>(L, sraw, sb0, sb1);
       switch (e2 & 3) {
-        case 0: stage_s<0>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1, rgw); break;
-        case 1: stage_s<1>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1, rgw); break;
-        case 2: stage_s<2>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1, rgw); break;
-        default: stage_s<3>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1, rgw); break;
+        case 0: stage_s<0, FOLD>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1, rgw); break;
+        case 1: stage_s<1, FOLD>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1, rgw); break;
+        case 2: stage_s<2, FOLD>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1, rgw); break;
+        default: stage_s<3, FOLD>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1, rgw); break;
       }
       if (e2 + 1 < K) s_raw_load<FOLD>(L, a, e2 + 1, FOLD ? axis_w(wq, a.wt, e2 + 1, L.t, Q) * a.jac : 1.0, sraw);
       mbar_arrive(yempty + b);
@@ -808,8 +823,9 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3s(GsfArgs a) {
     }
     // rows K .. K+P-1 received their last contribution from element K-1
     for (int I2 = K; I2 < N; ++I2) {
-      if (I2 >= 2) mbar_wait(rfree + (I2 & 1), ((I2 >> 1) - 1) & 1);
-      flush_tail(L, ws, Rs, I2, meta, pb, pc, a, N, rgw);
+      constexpr int LAG = Rg<FOLD>::LAG;
+      if (I2 >= LAG) mbar_wait(rfree + ((I2 - LAG) & 1), ((I2 - LAG) >> 1) & 1);
+      flush_tail<FOLD>(L, ws, Rs, I2, meta, pb, pc, a, N, rgw);
       mbar_arrive(rfull + (I2 & 1));
     }
   }
@@ -826,11 +842,11 @@ int launch_gsf_p3s(const GsfArgs& a0, cudaStream_t s) {
   a.tiles1 = (int)((N + p3s::TB - 1) / p3s::TB);
   const int64_t grid = (int64_t)tiles0 * a.tiles1;
   const bool fold = a.coef != nullptr || a.wt != nullptr;
-  cudaError_t e = smem_attr_once(reinterpret_cast<const void*>(fold ? p3s::k_gsf3_p3s<true> : p3s::k_gsf3_p3s<false>),
-                                 p3s::SMEM_BYTES);
+  const size_t smem = fold ? p3s::Rg<true>::SMEM_BYTES : p3s::Rg<false>::SMEM_BYTES;
+  cudaError_t e = smem_attr_once(reinterpret_cast<const void*>(fold ? p3s::k_gsf3_p3s<true> : p3s::k_gsf3_p3s<false>), smem);
   if (e != cudaSuccess) return check_cuda(e, "gsf_p3 smem attr");
-  if (fold) p3s::k_gsf3_p3s<true><<<(unsigned)grid, p3s::NT, p3s::SMEM_BYTES, s>>>(a);
-  else p3s::k_gsf3_p3s<false><<<(unsigned)grid, p3s::NT, p3s::SMEM_BYTES, s>>>(a);
+  if (fold) p3s::k_gsf3_p3s<true><<<(unsigned)grid, p3s::NT, smem, s>>>(a);
+  else p3s::k_gsf3_p3s<false><<<(unsigned)grid, p3s::NT, smem, s>>>(a);
   return check_cuda(cudaGetLastError(), "gsf_p3 launch");
 }
 
