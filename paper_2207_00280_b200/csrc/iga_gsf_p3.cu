@@ -407,14 +407,23 @@ __device__ __forceinline__ void s_fragments(const Lane& L, const GsfArgs& a, int
 #pragma unroll
   for (int nt = 0; nt < 2; ++nt) {
     const int r = bcol_r(nt, g), s = bcol_s(nt, g);
-    const double vv = __ldg(V2 + r * Q + t) * __ldg(V2 + s * Q + t);
-    b0[nt] = FOLD ? vv * ws : vv;
+    // (FOLD: explicit roundings, so k_gsf3_p3 and k_gsf3_p3s form bitwise equal fragments
+    // whatever the compiler contracts)
+    const double vv = FOLD ? __dmul_rn(__ldg(V2 + r * Q + t), __ldg(V2 + s * Q + t))
+                           : __ldg(V2 + r * Q + t) * __ldg(V2 + s * Q + t);
+    b0[nt] = FOLD ? __dmul_rn(vv, ws) : vv;
     b1[nt] = 0.0;
     if (L.stiff) {
       const double* D2 = a.D + (int64_t)e2 * M * Q;
-      double z = __ldg(D2 + r * Q + t) * __ldg(D2 + s * Q + t);
-      if (L.smass) z += vv;
-      b1[nt] = FOLD ? z * ws : z;
+      if (FOLD) {
+        double z = __dmul_rn(__ldg(D2 + r * Q + t), __ldg(D2 + s * Q + t));
+        if (L.smass) z = __dadd_rn(z, vv);
+        b1[nt] = __dmul_rn(z, ws);
+      } else {
+        double z = __ldg(D2 + r * Q + t) * __ldg(D2 + s * Q + t);
+        if (L.smass) z += vv;
+        b1[nt] = z;
+      }
     }
   }
 }
@@ -447,13 +456,19 @@ template <bool FOLD>
 __device__ __forceinline__ void s_raw_form(const Lane& L, const SRaw& w, double (&b0)[2], double (&b1)[2]) {
 #pragma unroll
   for (int nt = 0; nt < 2; ++nt) {
-    const double vv = w.v[nt][0] * w.v[nt][1];
-    b0[nt] = FOLD ? vv * w.ws : vv;
+    const double vv = FOLD ? __dmul_rn(w.v[nt][0], w.v[nt][1]) : w.v[nt][0] * w.v[nt][1];
+    b0[nt] = FOLD ? __dmul_rn(vv, w.ws) : vv;
     b1[nt] = 0.0;
     if (L.stiff) {
-      double z = w.d[nt][0] * w.d[nt][1];
-      if (L.smass) z += vv;
-      b1[nt] = FOLD ? z * w.ws : z;
+      if (FOLD) {
+        double z = __dmul_rn(w.d[nt][0], w.d[nt][1]);
+        if (L.smass) z = __dadd_rn(z, vv);
+        b1[nt] = __dmul_rn(z, w.ws);
+      } else {
+        double z = w.d[nt][0] * w.d[nt][1];
+        if (L.smass) z += vv;
+        b1[nt] = z;
+      }
     }
   }
 }
@@ -574,7 +589,7 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
     if (e0 >= 0 && e0 < K && (type == 0 || L.stiff)) {
       const double* T = (type == 0 ? a.V : a.D) + (int64_t)e0 * M * Q;
       v = T[r * Q + tt] * T[sc * Q + tt];
-      if (FOLD) v *= axis_w(a.weights, a.wt, e0, tt, Q);
+      if (FOLD) v = __dmul_rn(v, axis_w(a.weights, a.wt, e0, tt, Q));
     }
     BA[u] = v;
   }
@@ -586,7 +601,7 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
     if (e1 >= 0 && e1 < K && (prod == 0 || L.stiff)) {
       const double* T = (prod == 0 ? a.V : a.D) + (int64_t)e1 * M * Q;
       v = T[r * Q + tt] * T[sc * Q + tt];
-      if (FOLD) v *= axis_w(a.weights, a.wt, e1, tt, Q);
+      if (FOLD) v = __dmul_rn(v, axis_w(a.weights, a.wt, e1, tt, Q));
     }
     BB[u] = v;
   }
@@ -708,7 +723,7 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
     double* Rs = sm + OFF_R;
     for (int u = ws * 32 + L.lane; u < MT_S * 4 * 2 * 32; u += NWS * 32) Rs[u] = 0.0;
     double sb0[2], sb1[2];
-    s_fragments<FOLD>(L, a, 0, FOLD ? axis_w(wq, a.wt, 0, L.t, Q) * a.jac : 1.0, sb0, sb1);
+    s_fragments<FOLD>(L, a, 0, FOLD ? __dmul_rn(axis_w(wq, a.wt, 0, L.t, Q), a.jac) : 1.0, sb0, sb1);
     SRaw sraw;
     __syncthreads();
     for (int e2 = 0; e2 < K; ++e2) {
@@ -728,7 +743,7 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
         case 2: stage_s<2>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1); break;
         default: stage_s<3>(L, ws, Y, Rs, a, e2, meta, pb, pc, N, sb0, sb1); break;
       }
-      if (e2 + 1 < K) s_raw_load<FOLD>(L, a, e2 + 1, FOLD ? axis_w(wq, a.wt, e2 + 1, L.t, Q) * a.jac : 1.0, sraw);
+      if (e2 + 1 < K) s_raw_load<FOLD>(L, a, e2 + 1, FOLD ? __dmul_rn(axis_w(wq, a.wt, e2 + 1, L.t, Q), a.jac) : 1.0, sraw);
       mbar_arrive(yempty + b);
       PT(0);
     }

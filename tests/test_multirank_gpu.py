@@ -81,6 +81,7 @@ def _worker(rank, world, port, K, p, op, assembly, coef_seed):
 @pytest.mark.parametrize("G,K,p,op,assembly,coef", [
     (2, 12, 3, "stiffness", "owner", None), (3, 12, 3, "stiffness", "owner", None),
     (4, 16, 3, "stiffness", "owner", None), (2, 9, 2, "mass", "owner", 4),
+    (2, 12, 3, "stiffness_mass", "owner", 7),
     (3, 12, 4, "stiffness_mass", "owner", 5)])
 def test_ranks_exchange_over_gloo_with_device_kernels(G, K, p, op, assembly, coef):
     import torch.multiprocessing as mp
