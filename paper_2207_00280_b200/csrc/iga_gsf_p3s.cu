@@ -90,8 +90,7 @@ constexpr int OFF_MM = OFF_R + MT_S * 4 * 2 * 32;  // [NRC][2]
 // axis-2 band table {band_prefix(I2), band_cnt(I2)} for meshes with N <= NBT rows (else computed)
 constexpr int NBT = 512;
 constexpr int OFF_BT = OFF_MM + NRC * 2;  // int2 [NBT]
-constexpr int OFF_MB = OFF_BT + NBT;       // mbarriers
-constexpr int OFF_RING = OFF_MB + 12;      // [NRC][RING]
+constexpr int OFF_RING = OFF_BT + NBT;     // [NRC][RING]
 // per ring combo: the mirrored values by target row J2 -- hi runs [J2 mod HS][d2' 0..3], lo runs
 // [J2 mod 4][d2' 4..6] -- so they leave as contiguous runs.  HS = 8 hi slots let the S warps
 // run two rows ahead of the emitters (LAG; ring_put / role E below).  The folded kernel
@@ -102,7 +101,8 @@ struct Rg {
   static constexpr int HS = FOLD ? 4 : 8, LAG = FOLD ? 1 : 2;
   static constexpr int LO = HS * 4, RING = LO + 12;
   static constexpr int OFF_W2 = OFF_RING + NRC * RING;  // second W buffer (FOLD)
-  static constexpr int SMEM_DOUBLES = FOLD ? OFF_W2 + LA * Q * WP : OFF_W2;
+  static constexpr int OFF_MB = FOLD ? OFF_W2 + LA * Q * WP : OFF_W2;  // mbarriers
+  static constexpr int SMEM_DOUBLES = OFF_MB + 12;
   static_assert(SMEM_DOUBLES * 8 <= 227 * 1024, "shared memory budget");
   static_assert(OFF_W2 % 2 == 0, "16-byte aligned cp.async destinations");
   static constexpr size_t SMEM_BYTES = SMEM_DOUBLES * sizeof(double);
@@ -424,7 +424,8 @@ __device__ __forceinline__ void stage_s_batch(const Lane& L, int ws, const doubl
   // the emitters are done with row e2 - LAG (ring_put): its slots are reused from here on
   constexpr int LAG = Rg<FOLD>::LAG;
   if (I0 == 0 && e2 >= LAG)
-    mbar_wait(reinterpret_cast<uint64_t*>(Rs - OFF_R + OFF_MB) + 10 + ((e2 - LAG) & 1), ((e2 - LAG) >> 1) & 1);
+    mbar_wait(reinterpret_cast<uint64_t*>(Rs - OFF_R + Rg<FOLD>::OFF_MB) + 10 + ((e2 - LAG) & 1),
+              ((e2 - LAG) >> 1) & 1);
 #pragma unroll
   for (int i = 0; i < NM; ++i) {
 #pragma unroll
@@ -652,7 +653,7 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3s(GsfArgs a) {
     }
     BB[u] = v;
   }
-  uint64_t* mb = reinterpret_cast<uint64_t*>(sm + OFF_MB);
+  uint64_t* mb = reinterpret_cast<uint64_t*>(sm + Rg<FOLD>::OFF_MB);
   uint64_t *xfull = mb, *xempty = mb + 2, *yfull = mb + 4, *yempty = mb + 6;
   // S -> E: row e2's ring values are in place (rfull[e2 & 1]); E -> S: its runs are written
   // (rfree[e2 & 1]).  Two barriers each: the S warps may be two rows ahead of the emitters.
@@ -688,9 +689,10 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3s(GsfArgs a) {
   // column -- and W is the raw coefficient: a constant for a scalar, else copied a column
   // ahead by the A warps with cp.async (no per-column weight pass on their critical path:
   // a coefficient field used to run the C3 shape in 2.24 ms against 0.43 for a scalar).
-  constexpr bool folded = FOLD;
-  const bool w_per_step = FOLD && a.coef != nullptr;
-  if (!w_per_step) form_w(W, wq, a, 0, i00, i10, e0lo, e0hi, tid, NT, folded);
+  // (FOLD is the launcher's choice for a coefficient field; a general knot vector with a scalar
+  // coefficient keeps the unfolded kernel and forms W per column, as before)
+  const bool w_per_step = FOLD || a.wt != nullptr;
+  if (!w_per_step) form_w(W, wq, a, 0, i00, i10, e0lo, e0hi, tid, NT);
   __syncthreads();
 
   // pipeline: A on element column it, B on it-1, S on it-2, handed over by mbarriers
@@ -707,17 +709,22 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3s(GsfArgs a) {
     __syncthreads();  // every role holds its fragments before Y buffer 1 is written
     // coefficient field: W is double-buffered, column it + 1 is copied while it is used
     double* W2 = sm + Rg<FOLD>::OFF_W2;
-    if (w_per_step) copy_coef_column(W, a, 0, i00, i10, e0lo, e0hi, tid, NWA * 32);
+    if (FOLD) copy_coef_column(W, a, 0, i00, i10, e0lo, e0hi, tid, NWA * 32);
     for (int it = 0; it < K; ++it) {
       const int b = it & 1;
-      if (w_per_step) {
+      if (!FOLD && w_per_step) {
+        if (it > 0) asm volatile("bar.sync 1, %0;\n" ::"n"(NWA * 32));  // W of it-1 consumed
+        form_w(W, wq, a, it, i00, i10, e0lo, e0hi, tid, NWA * 32);
+        asm volatile("bar.sync 1, %0;\n" ::"n"(NWA * 32));
+      }
+      if (FOLD) {
         // this column's coefficients have landed, for every A warp, and every A warp is done
         // with the other buffer (column it - 1): the next column's copy starts
         asm volatile("cp.async.wait_all;\n" ::: "memory");
         asm volatile("bar.sync 1, %0;\n" ::"n"(NWA * 32));
         if (it + 1 < K) copy_coef_column(b ? W : W2, a, it + 1, i00, i10, e0lo, e0hi, tid, NWA * 32);
       }
-      const double* Wc = (w_per_step && b) ? W2 : W;
+      const double* Wc = (FOLD && b) ? W2 : W;
       if (it >= 2) mbar_wait(xempty + b, ((it >> 1) - 1) & 1);
       double* X = sm + OFF_X + b * SZ_X;
       int mt = mt0;
@@ -856,7 +863,7 @@ int launch_gsf_p3s(const GsfArgs& a0, cudaStream_t s) {
   const int tiles0 = (planes + p3s::TA - 1) / p3s::TA;
   a.tiles1 = (int)((N + p3s::TB - 1) / p3s::TB);
   const int64_t grid = (int64_t)tiles0 * a.tiles1;
-  const bool fold = a.coef != nullptr || a.wt != nullptr;
+  const bool fold = a.coef != nullptr;
   const size_t smem = fold ? p3s::Rg<true>::SMEM_BYTES : p3s::Rg<false>::SMEM_BYTES;
   cudaError_t e = smem_attr_once(reinterpret_cast<const void*>(fold ? p3s::k_gsf3_p3s<true> : p3s::k_gsf3_p3s<false>), smem);
   if (e != cudaSuccess) return check_cuda(e, "gsf_p3 smem attr");

@@ -2,7 +2,7 @@
 # reference arm, C4, C2, p9), ncu launch lists and full captures of the kernels they
 # time, GPU suite and smoke.  Run under gpurun (one GPU); summarise with
 # tools/profile_summary.py into profiles/.
-TAG=${TAG:-r02w}
+TAG=${TAG:-r02x}
 O=gpurun_out
 set -x
 python bench.py > $O/${TAG}_bench.json 2> $O/${TAG}_bench.err
