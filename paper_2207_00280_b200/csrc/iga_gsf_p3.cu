@@ -628,12 +628,13 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
   }
   __syncthreads();
   // Scalar coefficient on the uniform mesh: W = c w0 w1 w2 jac, formed once.  FOLD (a
-  // coefficient field or a general knot vector): the weights are in the fragments and W is
-  // the raw coefficient -- a constant for a scalar, else copied per element column with
-  // cp.async after the A warps are done with the previous one (iga_gsf_p3s.cu has the
-  // double-buffered version).
-  const bool w_per_step = FOLD && a.coef != nullptr;
-  if (!w_per_step) form_w(W, wq, a, 0, i00, i10, e0lo, e0hi, tid, NT, FOLD);
+  // coefficient field): the weights are in the fragments and W is the raw coefficient,
+  // copied per element column with cp.async after the A warps are done with the previous
+  // one (iga_gsf_p3s.cu has the double-buffered version).
+  // (FOLD is the launcher's choice for a coefficient field; a general knot vector with a scalar
+  // coefficient keeps the unfolded kernel and forms W per column)
+  const bool w_per_step = FOLD || a.wt != nullptr;
+  if (!w_per_step) form_w(W, wq, a, 0, i00, i10, e0lo, e0hi, tid, NT);
   __syncthreads();
 
   // pipeline: A on element column it, B on it-1, S on it-2, handed over by mbarriers
@@ -648,10 +649,15 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3(GsfArgs a) {
     for (int i = 0; i < NPA; ++i) ba[i] = BA[(ty * LA + pa_la(i)) * 32 + L.lane];
     const int mt0 = L.stiff ? (wa >> 1) : wa, mstep = L.stiff ? NWA / 2 : NWA;
     __syncthreads();  // every role holds its fragments before Y buffer 1 is written
-    if (w_per_step) copy_coef_column(W, a, 0, i00, i10, e0lo, e0hi, tid, NWA * 32);
+    if (FOLD) copy_coef_column(W, a, 0, i00, i10, e0lo, e0hi, tid, NWA * 32);
     for (int it = 0; it < K; ++it) {
       PT(2);
-      if (w_per_step) {
+      if (!FOLD && w_per_step) {
+        if (it > 0) asm volatile("bar.sync 1, %0;\n" ::"n"(NWA * 32));  // W of it-1 consumed
+        form_w(W, wq, a, it, i00, i10, e0lo, e0hi, tid, NWA * 32);
+        asm volatile("bar.sync 1, %0;\n" ::"n"(NWA * 32));
+      }
+      if (FOLD) {
         if (it > 0) {  // W of it-1 consumed by every A warp: this column's copy starts
           asm volatile("bar.sync 1, %0;\n" ::"n"(NWA * 32));
           copy_coef_column(W, a, it, i00, i10, e0lo, e0hi, tid, NWA * 32);
@@ -762,7 +768,7 @@ int launch_gsf_p3(const GsfArgs& a0, cudaStream_t s) {
   const int tiles0 = (planes + p3::TA - 1) / p3::TA;
   a.tiles1 = (int)((N + p3::TB - 1) / p3::TB);
   const int64_t grid = (int64_t)tiles0 * a.tiles1;
-  const bool fold = a.coef != nullptr || a.wt != nullptr;
+  const bool fold = a.coef != nullptr;
   cudaError_t e = smem_attr_once(reinterpret_cast<const void*>(fold ? p3::k_gsf3_p3<true> : p3::k_gsf3_p3<false>),
                                  p3::SMEM_BYTES);
   if (e != cudaSuccess) return check_cuda(e, "gsf_p3 smem attr");

@@ -683,14 +683,12 @@ __global__ void __launch_bounds__(NT, 1) k_gsf3_p3s(GsfArgs a) {
   }
   __syncthreads();
   // Scalar coefficient on the uniform mesh: W = c w0 w1 w2 jac (the reference's factor order)
-  // is the same for every element column and formed once.  Otherwise (`folded`: a coefficient
-  // field, or per-element weights of a general knot vector) the axis weights go into the
-  // constant fragments -- w0 into stage A's, w1 into stage B's, w2 jac into stage S's per
-  // column -- and W is the raw coefficient: a constant for a scalar, else copied a column
-  // ahead by the A warps with cp.async (no per-column weight pass on their critical path:
-  // a coefficient field used to run the C3 shape in 2.24 ms against 0.43 for a scalar).
-  // (FOLD is the launcher's choice for a coefficient field; a general knot vector with a scalar
-  // coefficient keeps the unfolded kernel and forms W per column, as before)
+  // is the same for every element column and formed once; with a general knot vector it is
+  // formed per column by the A warps.  FOLD (the launcher's choice for a coefficient field):
+  // the axis weights go into the constant fragments -- w0 into stage A's, w1 into stage B's,
+  // w2 jac into stage S's per column -- and W is the raw coefficient, copied a column ahead
+  // by the A warps with cp.async (no per-column weight pass on their critical path: a
+  // coefficient field used to run the C3 shape in 2.24 ms against 0.43 for a scalar).
   const bool w_per_step = FOLD || a.wt != nullptr;
   if (!w_per_step) form_w(W, wq, a, 0, i00, i10, e0lo, e0hi, tid, NT);
   __syncthreads();
