@@ -160,3 +160,37 @@ def test_symmetric_kernels_repeat_bitwise(K, p, op, kind):
         sess.step()
         torch.cuda.synchronize()
         assert torch.equal(sess.values.view(torch.int64), first.view(torch.int64))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("sym", ["1", "0"])
+def test_p3_field_unaligned_coefficient_pointer(sym):
+    """The folded p = 3 kernels copy the coefficient field with 16-byte cp.async when the
+    caller's pointer allows it and with 8-byte copies otherwise (a C-ABI caller may pass any
+    8-byte aligned device pointer): a field stored one double into an allocation gives the
+    same bits as the aligned one (IGA_GSF_SYM is read once per process, hence the child)."""
+    code = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, %r)
+from paper_2207_00280_b200.device import MeshProblem
+K, p = 7, 3
+coef = np.random.default_rng(3).uniform(0.5, 1.5, size=(K**3, 64))
+prob = MeshProblem(3, K, p, operator="stiffness_mass", coefficient=coef)
+out = []
+for shift in (0, 1):
+    buf = torch.empty(coef.size + 2, dtype=torch.float64, device="cuda")
+    view = buf[shift:shift + coef.size].view(K**3, 64)
+    view.copy_(torch.from_numpy(coef))
+    assert view.data_ptr() %% 16 == 8 * shift
+    prob.coef = view
+    vals = torch.full((prob.nnz(),), float("nan"), dtype=torch.float64, device="cuda")
+    prob.integrate_assemble(vals, 2)
+    torch.cuda.synchronize()
+    out.append(vals.cpu().numpy())
+assert not np.isnan(out[0]).any()
+assert out[0].tobytes() == out[1].tobytes()
+print("ok")
+""" % ROOT
+    env = dict(os.environ, IGA_GSF_SYM=sym)
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
