@@ -253,6 +253,12 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
     if (e0 >= e0lo && e0 < e0hi && r >= 0 && r <= P && sc >= 0 && sc <= P && J0 >= 0 && J0 < N) {
       v.x = V[((int64_t)e0 * m + r) * Q + k0] * V[((int64_t)e0 * m + sc) * Q + k0];
       if (STIFF) v.y = D[((int64_t)e0 * m + r) * Q + k0] * D[((int64_t)e0 * m + sc) * Q + k0];
+#ifndef GSF_NOFOLD
+      // the axis-0 weight lives in the pair table (W is the raw coefficient, below)
+      const double w0 = axis_w(a.weights, a.wt, e0, k0, Q);
+      v.x = __dmul_rn(v.x, w0);
+      v.y = __dmul_rn(v.y, w0);
+#endif
     }
     PA2[a0 * KAP + kk] = Elem<STIFF>::mk(v.x, v.y);
   }
@@ -264,6 +270,11 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
     if (e1 >= 0 && e1 < K && r >= 0 && r <= P && sc >= 0 && sc <= P && J1 >= 0 && J1 < N) {
       v.x = V[((int64_t)e1 * m + r) * Q + k1] * V[((int64_t)e1 * m + sc) * Q + k1];
       if (STIFF) v.y = D[((int64_t)e1 * m + r) * Q + k1] * D[((int64_t)e1 * m + sc) * Q + k1];
+#ifndef GSF_NOFOLD
+      const double w1 = axis_w(a.weights, a.wt, e1, k1, Q);
+      v.x = __dmul_rn(v.x, w1);
+      v.y = __dmul_rn(v.y, w1);
+#endif
     }
     PB2[b1 * KBP + kk] = Elem<STIFF>::mk(v.x, v.y);
   }
@@ -504,6 +515,20 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
     if (e2 < 0)
 #endif
     {
+#ifndef GSF_NOFOLD
+      // W is the raw coefficient: the axis weights live in the pair tables (w0 in PA, w1 in
+      // PB) and in this column's Z (w2 jac), so the weight pass is a copy of the prefetched
+      // coefficients (it was 22% of the C4 kernel with three multiplies and three weight
+      // lookups per value)
+#pragma unroll
+      for (int i = 0; i < UPT; ++i) {
+        if (wdst[i] >= 0) {
+          double* dst = sW + wdst[i];  // column (k2, c1): k2 slowest
+#pragma unroll
+          for (int k2 = 0; k2 < Q; ++k2) dst[k2 * KB] = cv[i][k2];
+        }
+      }
+#else
       double w2[Q];  // axis-2 weights of this column
 #pragma unroll
       for (int k2 = 0; k2 < Q; ++k2) w2[k2] = axis_w(wqs, a.wt, e2, k2, Q);
@@ -517,9 +542,20 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
           for (int k2 = 0; k2 < Q; ++k2) dst[k2 * KB] = w01 * w2[k2] * a.jac * cv[i][k2];
         }
       }
+#endif
     }
     load_coef(e2 + 1, cv);
     if (tid < m * m * Q) {  // Z[k2][(r,s)]
+#ifndef GSF_NOFOLD
+      const double ws = __dmul_rn(axis_w(wqs, a.wt, e2, tid / (m * m), Q), a.jac);
+      const double vv = __dmul_rn(zv[0], zv[1]);
+      double dd = 0.0;
+      if (STIFF) {
+        dd = __dmul_rn(zv[2], zv[3]);
+        if (a.op == IGA_OP_STIFFNESS_MASS) dd = __dadd_rn(dd, vv);
+      }
+      Z2[tid] = Elem<STIFF>::mk(__dmul_rn(vv, ws), __dmul_rn(dd, ws));
+#else
       const double vv = zv[0] * zv[1];
       double dd = 0.0;
       if (STIFF) {
@@ -527,6 +563,7 @@ __global__ void __launch_bounds__(nt_of<P>(), P <= 2 ? 4 : 1) k_gsf3_mma(GsfArgs
         if (a.op == IGA_OP_STIFFNESS_MASS) dd += vv;
       }
       Z2[tid] = Elem<STIFF>::mk(vv, dd);
+#endif
     }
     load_z(e2 + 1, zv);
     __syncthreads();
