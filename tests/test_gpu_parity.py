@@ -327,6 +327,7 @@ def _sample_rows(K, p, n_rand, seed=0):
     dict(K=32, p=2, op="mass", coef="uniform", name="C2", assembly="scatter"),
     dict(K=48, p=3, op="stiffness", coef="uniform", name="C3-48 coef field", method="classical"),
     dict(K=48, p=3, op="stiffness", coef="uniform", name="C3-48 coef field", assembly="owner"),
+    dict(K=64, p=3, op="stiffness", coef="uniform", name="C3 coef field (bench c3f)", assembly="owner"),
 ])
 def test_full_size_sampled_rows(pkg, cfg):
     """BASELINE configs at full size: sampled rows (corner/edge/interior) vs the
